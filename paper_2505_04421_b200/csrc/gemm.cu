@@ -1,0 +1,185 @@
+// gemm.cu — generic tcgen05 GEMM with fused epilogues. See gemm.cuh for the contract.
+#include "gemm.cuh"
+#include "sm100.cuh"
+#include "tma.cuh"
+
+#include <algorithm>
+
+namespace longer {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int STAGES = 4;
+constexpr int kThreads = 192;  // w0 TMA, w1 MMA + TMEM owner, w2..w5 epilogue
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+  const float c = 0.7978845608028654f, a = 0.044715f;
+  float u = c * (x + a * x * x * x);
+  return 0.5f * x * (1.0f + tanhf(u));
+}
+
+template <int BN>
+struct Smem {
+  static constexpr int A_BYTES = BM * BK * 2;        // 16 KB
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TOTAL = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+            GemmArgs g, int kb_per_split) {
+  using S = Smem<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x / 32;
+  const int n0 = blockIdx.x * BN;
+  const int m0 = blockIdx.y * BM;
+  const int nkb_total = (g.K + BK - 1) / BK;
+  const int kb_begin = blockIdx.z * kb_per_split;
+  const int kb_end = min(nkb_total, kb_begin + kb_per_split);
+  const int nkb = kb_end - kb_begin;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], 1); }
+    sm100::mbar_init(tmem_full, 1);
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) sm100::tmem_alloc<(BN < 32 ? 32 : BN)>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (sm100::elect_one()) {
+      sm100::tma_prefetch(&tmA);
+      sm100::tma_prefetch(&tmB);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % STAGES, round = i / STAGES;
+        if (i >= STAGES) sm100::mbar_wait(&empty[s], (round - 1) & 1);
+        uint8_t* sa = smem + s * S::STAGE_BYTES;
+        uint8_t* sb = sa + S::A_BYTES;
+        sm100::mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
+        const int k0 = (kb_begin + i) * BK;
+        if (!g.a_mn_major) {
+          sm100::tma_load_2d(sa, &tmA, &full[s], k0, m0);
+        } else {
+          sm100::tma_load_2d(sa, &tmA, &full[s], m0, k0);
+          sm100::tma_load_2d(sa + 8192, &tmA, &full[s], m0 + 64, k0);
+        }
+        if (!g.b_mn_major) {
+          sm100::tma_load_2d(sb, &tmB, &full[s], k0, n0);
+        } else {
+#pragma unroll
+          for (int j = 0; j < BN / 64; ++j) sm100::tma_load_2d(sb + j * 8192, &tmB, &full[s], n0 + 64 * j, k0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (sm100::elect_one()) {
+      const uint32_t idesc = sm100::make_idesc_bf16(BM, BN, g.a_mn_major, g.b_mn_major);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % STAGES, round = i / STAGES;
+        sm100::mbar_wait(&full[s], round & 1);
+        sm100::tc_fence_after();
+        const uint32_t sa = sm100::smem_u32(smem + s * S::STAGE_BYTES);
+        const uint32_t sb = sa + S::A_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk) {
+          uint64_t ad = g.a_mn_major ? sm100::make_sdesc(sa + kk * 2048, 8192, 1024, sm100::LAYOUT_SW128)
+                                     : sm100::make_sdesc(sa + kk * 32, 16, 1024, sm100::LAYOUT_SW128);
+          uint64_t bd = g.b_mn_major ? sm100::make_sdesc(sb + kk * 2048, 8192, 1024, sm100::LAYOUT_SW128)
+                                     : sm100::make_sdesc(sb + kk * 32, 16, 1024, sm100::LAYOUT_SW128);
+          sm100::mma_bf16(tmem, ad, bd, idesc, (i | kk) != 0);
+        }
+        sm100::mma_commit(&empty[s]);
+      }
+      sm100::mma_commit(tmem_full);
+    }
+  } else {
+    // epilogue warps 2..5 → TMEM lane quarter (warp % 4)
+    const int q = warp & 3;
+    const int row = m0 + q * 32 + (threadIdx.x & 31);
+    sm100::mbar_wait(tmem_full, 0);
+    sm100::tc_fence_after();
+    const uint32_t flags = g.flags;
+    const bool row_ok = row < g.M;
+    float rmask = 1.0f;
+    if ((flags & EPI_ROWMASK) && row_ok) rmask = g.rowmask[row];
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      sm100::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + c, r);
+      sm100::tmem_ld_wait();
+      if (!row_ok || n0 + c >= g.N) continue;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int n = n0 + c + j;
+        if (n >= g.N) break;
+        float v = __uint_as_float(r[j]);
+        if (flags & EPI_BIAS) v += g.bias[n];
+        if (flags & EPI_SAVE_PRE)
+          reinterpret_cast<__nv_bfloat16*>(g.pre_bf16)[(size_t)row * g.ldc_bf + n] = __float2bfloat16(v);
+        if (flags & EPI_GELU) v = gelu_tanh(v);
+        if (flags & EPI_RESID) v += g.resid[(size_t)row * g.ldr + n];
+        if (flags & EPI_ROWMASK) v *= rmask;
+        if (flags & EPI_OUT_F32) {
+          float* dst = g.C + (size_t)row * g.ldc + n;
+          if (flags & EPI_ATOMIC) atomicAdd(dst, v); else *dst = v;
+        }
+        if (flags & EPI_OUT_BF16)
+          reinterpret_cast<__nv_bfloat16*>(g.C_bf16)[(size_t)row * g.ldc_bf + n] = __float2bfloat16(v);
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) sm100::tmem_dealloc<(BN < 32 ? 32 : BN)>(tmem);
+}
+
+template <int BN>
+int launch_bn(const GemmArgs& g, cudaStream_t st) {
+  CUtensorMap tA, tB;
+  int rc;
+  // A
+  if (!g.a_mn_major) rc = tma::encode_2d_bf16(&tA, g.A, g.K, g.M, g.lda, BK, BM);
+  else rc = tma::encode_2d_bf16(&tA, g.A, g.M, g.K, g.lda, 64, BK);
+  if (rc) return rc;
+  if (!g.b_mn_major) rc = tma::encode_2d_bf16(&tB, g.B, g.K, g.N, g.ldb, BK, BN);
+  else rc = tma::encode_2d_bf16(&tB, g.B, g.N, g.K, g.ldb, 64, BK);
+  if (rc) return rc;
+  const int nkb = (g.K + BK - 1) / BK;
+  int split = std::max(1, std::min(g.split_k, nkb));
+  int kb_per = (nkb + split - 1) / split;
+  split = (nkb + kb_per - 1) / kb_per;
+  dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, split);
+  const int smem = Smem<BN>::TOTAL;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr_set = true;
+  }
+  gemm_kernel<BN><<<grid, kThreads, smem, st>>>(tA, tB, g, kb_per);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+int gemm_launch(const GemmArgs& g, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0 || g.K <= 0) return 0;
+  if (g.split_k > 1 && !(g.flags & EPI_ATOMIC)) return (int)cudaErrorInvalidValue;
+  if (g.N <= 64) return launch_bn<64>(g, st);
+  if (g.N <= 128) return launch_bn<128>(g, st);
+  return launch_bn<256>(g, st);
+}
+
+}  // namespace longer
