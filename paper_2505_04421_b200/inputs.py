@@ -1,0 +1,208 @@
+"""Sample records and their tensorisation into the device batch layout.
+
+``Event``/``UserFeatures``/``Candidate``/``Sample`` mirror the reference records
+(``pkg/src/longrec/inputs.py:35-99``) so reference datasets drop in unchanged.
+
+``Batch`` is the layout the C-ABI consumes (``include/longer.h`` ``LongerBatch``): token
+arrays ``[B, L]`` right-aligned exactly like ``encode_events`` (``inputs.py:457-482``: keep the
+last L events, left-pad), plus per-sample scalars.  Time deltas are ``candidate_ts - event_ts``
+in seconds; the device computes the log2 bucket (``inputs.py:307-315``).  Because buckets clamp
+at ``n_time_buckets - 1 <= 31``, clamping deltas to int32 max is exact.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+from .config import ModelConfig
+from .errors import ConfigError, EmbeddingLookupError
+
+INT32_MAX = 2 ** 31 - 1
+
+
+@dataclass(frozen=True)
+class Event:
+    item_id: int
+    action_type: int
+    timestamp: int
+
+
+@dataclass(frozen=True)
+class UserFeatures:
+    uid: int
+    profile_bucket: int
+
+
+@dataclass(frozen=True)
+class Candidate:
+    item_id: int
+    timestamp: int
+
+
+@dataclass(frozen=True)
+class Sample:
+    events: tuple
+    user_features: UserFeatures
+    candidate: Candidate
+    label: int
+
+
+@dataclass
+class Batch:
+    """Host (numpy) or device (torch) arrays in the C-ABI batch layout."""
+
+    items: object       # int32 [B, L]
+    actions: object     # int32 [B, L]
+    dt: object          # int32 [B, L]   candidate_ts - event_ts, clamped to int32
+    n_events: object    # int32 [B]      real events (<= L), right-aligned
+    uid: object         # int32 [B]
+    profile: object     # int32 [B]
+    cand_item: object   # int32 [B]
+    label: object       # float32 [B]
+
+    FIELDS = ("items", "actions", "dt", "n_events", "uid", "profile", "cand_item", "label")
+
+    @property
+    def size(self) -> int:
+        return int(self.n_events.shape[0])
+
+    def as_dict(self) -> dict:
+        return {f: getattr(self, f) for f in self.FIELDS}
+
+    def to(self, device, non_blocking: bool = True) -> "Batch":
+        import torch
+        out = {}
+        for f in self.FIELDS:
+            v = getattr(self, f)
+            if isinstance(v, np.ndarray):
+                v = torch.from_numpy(np.ascontiguousarray(v))
+            out[f] = v.to(device, non_blocking=non_blocking)
+        return Batch(**out)
+
+    def pin(self) -> "Batch":
+        import torch
+        out = {}
+        for f in self.FIELDS:
+            v = getattr(self, f)
+            if isinstance(v, np.ndarray):
+                v = torch.from_numpy(np.ascontiguousarray(v))
+            out[f] = v.pin_memory()
+        return Batch(**out)
+
+    def nbytes(self) -> int:
+        return int(sum(getattr(self, f).nbytes for f in self.FIELDS))
+
+
+def _check_ids(name: str, arr: np.ndarray, rows: int) -> None:
+    """``_checked_ids`` (pkg/src/longrec/inputs.py:406-411): never clamp."""
+    if arr.size and (arr.min() < 0 or arr.max() >= rows):
+        raise EmbeddingLookupError(f"{name} id out of range [0, {rows}): {arr.min()}..{arr.max()}")
+
+
+def tensorize(samples: Sequence[Sample], cfg: ModelConfig, check: bool = True) -> Batch:
+    """Samples → ``Batch`` (host numpy).  Raises the reference's errors for bad input."""
+    B, L = len(samples), cfg.L
+    items = np.zeros((B, L), np.int32)
+    actions = np.zeros((B, L), np.int32)
+    dt = np.zeros((B, L), np.int32)
+    n_events = np.zeros(B, np.int32)
+    uid = np.zeros(B, np.int32)
+    profile = np.zeros(B, np.int32)
+    cand = np.zeros(B, np.int32)
+    label = np.zeros(B, np.float32)
+    for b, s in enumerate(samples):
+        ev = tuple(s.events)[-L:]
+        n = len(ev)
+        n_events[b] = n
+        if n:
+            it = np.fromiter((e.item_id for e in ev), np.int64, n)
+            ac = np.fromiter((e.action_type for e in ev), np.int64, n)
+            ts = np.fromiter((e.timestamp for e in ev), np.int64, n)
+            delta = int(s.candidate.timestamp) - ts
+            if check:
+                _check_ids("item", it, cfg.vocab)
+                _check_ids("action", ac, cfg.n_actions)
+                if (delta < 0).any():
+                    raise ConfigError("future event: negative time delta")
+            items[b, L - n:] = it
+            actions[b, L - n:] = ac
+            dt[b, L - n:] = np.minimum(delta, INT32_MAX)
+        uid[b] = s.user_features.uid
+        profile[b] = s.user_features.profile_bucket
+        cand[b] = s.candidate.item_id
+        label[b] = s.label
+    if check:
+        _check_ids("uid", uid, cfg.n_users)
+        _check_ids("profile", profile, cfg.n_profiles)
+        _check_ids("item", cand, cfg.vocab)
+    return Batch(items, actions, dt, n_events, uid, profile, cand, label)
+
+
+def check_batch(batch: Batch, cfg: ModelConfig) -> None:
+    """Range checks on an already-tensorised host batch (real tokens only)."""
+    items = np.asarray(batch.items)
+    L = cfg.L
+    n = np.asarray(batch.n_events)
+    if items.shape[1] != L:
+        raise ConfigError(f"batch has L={items.shape[1]}, config L={L}")
+    if (n < 0).any() or (n > L).any():
+        raise ConfigError("n_events must lie in [0, L]")
+    real = np.arange(L)[None, :] >= (L - n)[:, None]
+    _check_ids("item", np.asarray(batch.items)[real], cfg.vocab)
+    _check_ids("action", np.asarray(batch.actions)[real], cfg.n_actions)
+    if (np.asarray(batch.dt)[real] < 0).any():
+        raise ConfigError("future event: negative time delta")
+    _check_ids("uid", np.asarray(batch.uid), cfg.n_users)
+    _check_ids("profile", np.asarray(batch.profile), cfg.n_profiles)
+    _check_ids("item", np.asarray(batch.cand_item), cfg.vocab)
+
+
+def synthetic_samples(cfg: ModelConfig, n: int, seed: int = 1, n_events: Optional[int] = None,
+                      base_time: int = 1_700_000_000, gap=(30, 900)) -> list:
+    """Synthetic behaviour samples drawn exactly as BASELINE.md §3.1 prescribes (one
+    ``default_rng(seed)`` consumed sample after sample: L × (gap, item, action), uid, profile,
+    candidate item, label).  Gaps default to ``GeneratorConfig.gap_min/gap_max``."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        t = base_time
+        ne = cfg.L if n_events is None else n_events
+        events = []
+        for _ in range(ne):
+            t += int(rng.integers(gap[0], gap[1]))
+            item = int(rng.integers(cfg.vocab))
+            act = int(rng.integers(cfg.n_actions))
+            events.append(Event(item, act, t))
+        uid = int(rng.integers(cfg.n_users))
+        prof = int(rng.integers(cfg.n_profiles))
+        cand = int(rng.integers(cfg.vocab))
+        label = int(rng.integers(2))
+        out.append(Sample(tuple(events), UserFeatures(uid, prof), Candidate(cand, t + 60), label))
+    return out
+
+
+def synthetic_batch(cfg: ModelConfig, B: int, seed: int = 1, min_events: Optional[int] = None) -> Batch:
+    """Vectorised synthetic batch (same distributions as :func:`synthetic_samples`, not the
+    same stream): full-length sequences unless ``min_events`` is given."""
+    rng = np.random.default_rng(seed)
+    L = cfg.L
+    gaps = rng.integers(30, 900, size=(B, L)).astype(np.int64)
+    # dt of event j = sum of gaps after it + 60 s (candidate = last event + 60)
+    dt = np.cumsum(gaps[:, ::-1], axis=1)[:, ::-1] - gaps + 60
+    items = rng.integers(0, cfg.vocab, size=(B, L)).astype(np.int32)
+    actions = rng.integers(0, cfg.n_actions, size=(B, L)).astype(np.int32)
+    if min_events is None:
+        n_ev = np.full(B, L, np.int32)
+    else:
+        n_ev = rng.integers(min_events, L + 1, size=B).astype(np.int32)
+    real = np.arange(L)[None, :] >= (L - n_ev)[:, None]
+    items = np.where(real, items, 0).astype(np.int32)
+    actions = np.where(real, actions, 0).astype(np.int32)
+    dt = np.where(real, np.minimum(dt, INT32_MAX), 0).astype(np.int32)
+    uid = rng.integers(0, cfg.n_users, size=B).astype(np.int32)
+    prof = rng.integers(0, cfg.n_profiles, size=B).astype(np.int32)
+    cand = rng.integers(0, cfg.vocab, size=B).astype(np.int32)
+    label = rng.integers(0, 2, size=B).astype(np.float32)
+    return Batch(items, actions, dt, n_ev, uid, prof, cand, label)
