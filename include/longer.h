@@ -1,0 +1,94 @@
+/* longer.h — C ABI of the B200 (sm_100a) LONGER encoder library `_longer_sm100.so`.
+ *
+ * The reference (`longrec`, pure Python/NumPy) has no FFI layer; its seam is the module API
+ * (SURVEY.md §8b).  These entry points replace, for a whole batch at once:
+ *
+ *   longer_forward           LongRecModel.forward_tensor over a batch + sigmoid
+ *                            (pkg/src/longrec/model.py:307-363, :365-377)
+ *   longer_forward_backward  the train-step body: zero_grads → per-sample T.bce(forward_tensor)
+ *                            → T.mean_scalars → loss.backward() (pkg/src/longrec/model.py:555-567;
+ *                            pkg/src/longrec/tensors.py:536-571, :141-175)
+ *   longer_adam_step         Adam.step (pkg/src/longrec/model.py:453-482)
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Every buffer is allocated by the caller (device memory,
+ *     stream-ordered); the library never allocates global memory.
+ *   - `params` / `grads` are ONE contiguous fp32 array each, holding every parameter in the
+ *     reference `LongRecModel.params()` order and shapes (row-major, weights [in, out]);
+ *     `longer_param_count` gives its length.
+ *   - `ws` is scratch of at least `longer_workspace_bytes` bytes (256-byte aligned).
+ *   - Return value: 0 on success, otherwise a LONGER_E* code; `longer_last_error()` gives text.
+ *     Codes map 1:1 onto the reference exception classes (pkg/src/longrec/errors.py:8-29).
+ *   - One thread drives one stream per device; calls are stream-ordered and graph-capturable
+ *     (no host synchronisation inside).
+ */
+#ifndef LONGER_H_
+#define LONGER_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LONGER_OK 0
+#define LONGER_ECONFIG 1      /* ConfigError */
+#define LONGER_EDIM 2         /* DimensionError */
+#define LONGER_ELOOKUP 3      /* EmbeddingLookupError */
+#define LONGER_ENUMERIC 4     /* NumericalError */
+#define LONGER_ESTALE 5       /* StaleCacheError */
+#define LONGER_ECUDA 6        /* CUDA runtime failure (RuntimeError) */
+
+/* ModelConfig fields (pkg/src/longrec/config.py:29-49) + batch size. */
+typedef struct LongerDims {
+  int32_t L, d, K, m, k, N, heads;
+  int32_t merge_inner;      /* 0 = "concat", 1 = "inner" */
+  int32_t inner_layers;
+  int32_t query_strategy;   /* 0 = "recent" (the only strategy on the device path) */
+  int32_t head_hidden, d_item, d_act, d_time, n_time_buckets;
+  int32_t vocab, n_actions, n_users, n_profiles;
+  int32_t batch;            /* samples in this call */
+} LongerDims;
+
+/* A batch in the right-aligned layout of encode_events (pkg/src/longrec/inputs.py:457-482):
+ * sample b's n_events[b] real events occupy token columns L-n .. L-1. Device pointers. */
+typedef struct LongerBatch {
+  const int32_t* items;     /* [B, L] */
+  const int32_t* actions;   /* [B, L] */
+  const int32_t* dt;        /* [B, L] candidate_ts - event_ts (>= 0, seconds) */
+  const int32_t* n_events;  /* [B] */
+  const int32_t* uid;       /* [B] */
+  const int32_t* profile;   /* [B] */
+  const int32_t* cand_item; /* [B] */
+  const float* label;       /* [B] 0/1 */
+} LongerBatch;
+
+int longer_param_count(const LongerDims* dims, int64_t* count);
+int longer_workspace_bytes(const LongerDims* dims, size_t* bytes);
+
+/* probs[B] = sigmoid(logit).  Inference: no activations are kept for backward. */
+int longer_forward(const LongerDims* dims, const float* params, const LongerBatch* batch,
+                   void* ws, size_t ws_bytes, float* probs, void* stream);
+
+/* Training step body: probs[B], loss[0] = batch-mean BCE, grads (overwritten) = dloss/dparams. */
+int longer_forward_backward(const LongerDims* dims, const float* params, const LongerBatch* batch,
+                            void* ws, size_t ws_bytes, float* probs, float* loss, float* grads,
+                            void* stream);
+
+/* In-place Adam on the flat buffers (beta1 .9, beta2 .999, eps 1e-8, bias-corrected, step t>=1).
+ * m, v: fp32 [count] moments (caller-zeroed before step 1). */
+int longer_adam_step(float* params, const float* grads, float* m, float* v, int64_t count, float lr,
+                     int32_t t, void* stream);
+
+/* Device-side input validation flags accumulated since the last call (and reset):
+ * bit0 = id out of range (EmbeddingLookupError), bit1 = negative time delta (ConfigError).
+ * Reads back through a synchronous copy on `stream`. */
+int longer_read_status(void* ws, int32_t* flags, void* stream);
+
+const char* longer_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LONGER_H_ */

@@ -1,0 +1,68 @@
+// common.cuh — shared device helpers: GELU, warp reductions, bf16 access, visibility rule.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace longer {
+
+typedef __nv_bfloat16 bf16;
+
+constexpr float kGeluC = 0.7978845608028654f;  // sqrt(2/pi)   (pkg/src/longrec/tensors.py:36)
+constexpr float kGeluA = 0.044715f;            //              (pkg/src/longrec/tensors.py:37)
+constexpr float kLnEps = 1e-12f;               //              (pkg/src/longrec/tensors.py:39)
+constexpr float kProbEps = 1e-12f;             //              (pkg/src/longrec/tensors.py:38)
+
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// tanh-GELU (pkg/src/longrec/tensors.py:292-304)
+__device__ __forceinline__ float gelu_f(float x) {
+  float t = tanh_fast(kGeluC * (x + kGeluA * x * x * x));
+  return 0.5f * x * (1.0f + t);
+}
+__device__ __forceinline__ float gelu_grad_f(float x) {
+  float t = tanh_fast(kGeluC * (x + kGeluA * x * x * x));
+  float du = kGeluC * (1.0f + 3.0f * kGeluA * x * x);
+  return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * du;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ float ldf(const float* p) { return *p; }
+__device__ __forceinline__ float ldf(const bf16* p) { return __bfloat162float(*p); }
+__device__ __forceinline__ void stf(float* p, float v) { *p = v; }
+__device__ __forceinline__ void stf(bf16* p, float v) { *p = __float2bfloat16(v); }
+
+// Visibility rule of the hybrid attention (pkg/src/longrec/attention.py:49-87 with the
+// metadata of pkg/src/longrec/model.py:275-293, "recent" query strategy):
+//   queries: i < k  → sequence query of merged group G-k+i;  i >= k → global of rank i-k
+//   keys:    j < ns → sequence key of merged group goff+j;    j >= ns → global of rank j-ns
+//   (cross layer: ns = G, goff = 0;   self layers: ns = k, goff = G-k)
+//   a group is pad iff group < npg (pad groups form a prefix of the left-padded grid).
+struct VisRule {
+  int k, G, ns, goff, npg;
+  __device__ __forceinline__ bool operator()(int i, int j) const {
+    if (i < k) {
+      const int gq = G - k + i;
+      if (gq < npg || j >= ns) return false;
+      const int gk = goff + j;
+      return gk >= npg && gk <= gq;
+    }
+    if (j < ns) return goff + j >= npg;
+    return (j - ns) <= (i - k);
+  }
+};
+
+}  // namespace longer

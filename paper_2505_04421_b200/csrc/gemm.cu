@@ -2,6 +2,7 @@
 #include "gemm.cuh"
 #include "sm100.cuh"
 #include "tma.cuh"
+#include "common.cuh"
 
 #include <algorithm>
 
@@ -14,11 +15,6 @@ constexpr int BK = 64;
 constexpr int STAGES = 4;
 constexpr int kThreads = 192;  // w0 TMA, w1 MMA + TMEM owner, w2..w5 epilogue
 
-__device__ __forceinline__ float gelu_tanh(float x) {
-  const float c = 0.7978845608028654f, a = 0.044715f;
-  float u = c * (x + a * x * x * x);
-  return 0.5f * x * (1.0f + tanhf(u));
-}
 
 template <int BN>
 struct Smem {
@@ -129,7 +125,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         if (flags & EPI_BIAS) v += g.bias[n];
         if (flags & EPI_SAVE_PRE)
           reinterpret_cast<__nv_bfloat16*>(g.pre_bf16)[(size_t)row * g.ldc_bf + n] = __float2bfloat16(v);
-        if (flags & EPI_GELU) v = gelu_tanh(v);
+        if (flags & EPI_GELU) v = gelu_f(v);
+        if (flags & EPI_GELU_BWD)
+          v *= gelu_grad_f(__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(g.pre_bf16)[(size_t)row * g.ldc_bf + n]));
         if (flags & EPI_RESID) v += g.resid[(size_t)row * g.ldr + n];
         if (flags & EPI_ROWMASK) v *= rmask;
         if (flags & EPI_OUT_F32) {
@@ -158,7 +156,10 @@ int launch_bn(const GemmArgs& g, cudaStream_t st) {
   else rc = tma::encode_2d_bf16(&tB, g.B, g.N, g.K, g.ldb, 64, BK);
   if (rc) return rc;
   const int nkb = (g.K + BK - 1) / BK;
-  int split = std::max(1, std::min(g.split_k, nkb));
+  const int tiles = ((g.N + BN - 1) / BN) * ((g.M + BM - 1) / BM);
+  int want = g.split_k;
+  if (want == 0) want = (g.flags & EPI_ATOMIC) ? std::max(1, std::min(296 / tiles, nkb / 4)) : 1;
+  int split = std::max(1, std::min(want, nkb));
   int kb_per = (nkb + split - 1) / split;
   split = (nkb + kb_per - 1) / kb_per;
   dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, split);
@@ -176,7 +177,7 @@ int launch_bn(const GemmArgs& g, cudaStream_t st) {
 
 int gemm_launch(const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0) return 0;
-  if (g.split_k > 1 && !(g.flags & EPI_ATOMIC)) return (int)cudaErrorInvalidValue;
+  if (g.split_k != 1 && !(g.flags & EPI_ATOMIC)) return (int)cudaErrorInvalidValue;
   if (g.N <= 64) return launch_bn<64>(g, st);
   if (g.N <= 128) return launch_bn<128>(g, st);
   return launch_bn<256>(g, st);

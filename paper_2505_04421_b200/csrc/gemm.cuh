@@ -23,13 +23,14 @@ enum EpiFlags : uint32_t {
   EPI_ATOMIC = 1u << 5,     // fp32 atomicAdd into C (split-K / gradient accumulation)
   EPI_SAVE_PRE = 1u << 6,   // store pre-activation (bf16, ld = ldc_bf) into pre_bf16
   EPI_ROWMASK = 1u << 7,    // multiply output rows by rowmask[m] (0/1 fp32)
+  EPI_GELU_BWD = 1u << 8,   // multiply by GELU'(pre[m, n]) (pre_bf16 is an INPUT, ld = ldc_bf)
 };
 
 struct GemmArgs {
   const void* A = nullptr; int lda = 0; int a_mn_major = 0;   // bf16
   const void* B = nullptr; int ldb = 0; int b_mn_major = 0;   // bf16
   int M = 0, N = 0, K = 0;
-  int split_k = 1;                  // >1 → K split across gridDim.z (requires EPI_ATOMIC)
+  int split_k = 1;                  // >1 → K split across gridDim.z (requires EPI_ATOMIC); 0 = auto
   uint32_t flags = EPI_OUT_F32;
   const float* bias = nullptr;
   const float* resid = nullptr; int ldr = 0;

@@ -1,0 +1,739 @@
+// longer.cu — C ABI (include/longer.h) and the native step orchestrator.
+//
+// One call runs a whole batch through the LONGER encoder on one stream:
+//   pack weights → featurise tokens → token MLP → [InnerTrans] → global tokens → cross block →
+//   N self blocks → head + BCE  (forward, pkg/src/longrec/model.py:307-363)
+// and, for training, the exact reverse sweep (pkg/src/longrec/tensors.py:141-175).
+// Dense contractions go through the tcgen05 GEMM (gemm.cu), everything else through ops.cu.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "gemm.cuh"
+#include "longer.h"
+#include "ops.cuh"
+
+namespace longer {
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* msg) {
+  g_err = msg;
+  return code;
+}
+
+// ------------------------------------------------------------------ parameter offsets
+constexpr int kMaxInner = 8;
+constexpr int kMaxSelf = 16;
+
+struct BlockOff {
+  long long w_q, b_q, w_k, b_k, w_v, b_v, w_o, b_o, w1, b1, w2, b2, ln1_g, ln1_b, ln2_g, ln2_b;
+};
+
+struct ParamOff {
+  long long item, act, time, uid, prof, pos, cls;
+  long long tok_w, tok_b, seq_w1, seq_b1, seq_w2, seq_b2, lift_w, lift_b, glob_w1, glob_b1, glob_w2, glob_b2;
+  BlockOff inner[kMaxInner], cross, self_[kMaxSelf];
+  long long head_w1, head_b1, head_w2, head_b2;
+  long long total;
+};
+
+// Same order and shapes as LongRecModel.params() (pkg/src/longrec/model.py:252-263).
+ParamOff param_offsets(const LongerDims& d) {
+  ParamOff o{};
+  long long off = 0;
+  auto take = [&](long long n) { long long r = off; off += n; return r; };
+  const long long D = (long long)d.K * d.d, F = d.d_item + d.d_act + d.d_time;
+  o.item = take((long long)d.vocab * d.d_item);
+  o.act = take((long long)d.n_actions * d.d_act);
+  o.time = take((long long)d.n_time_buckets * d.d_time);
+  o.uid = take((long long)d.n_users * d.d);
+  o.prof = take((long long)d.n_profiles * d.d);
+  o.pos = take((long long)d.L * d.d);
+  o.cls = take((long long)(d.m - 2) * D);
+  o.tok_w = take(F * d.d); o.tok_b = take(d.d);
+  o.seq_w1 = take(d.d * 2 * D); o.seq_b1 = take(2 * D);
+  o.seq_w2 = take(2 * D * d.d); o.seq_b2 = take(d.d);
+  o.lift_w = take(d.d * D); o.lift_b = take(D);
+  o.glob_w1 = take(D * 2 * D); o.glob_b1 = take(2 * D);
+  o.glob_w2 = take(2 * D * D); o.glob_b2 = take(D);
+  auto block = [&](long long w) {
+    BlockOff b;
+    b.w_q = take(w * w); b.b_q = take(w); b.w_k = take(w * w); b.b_k = take(w);
+    b.w_v = take(w * w); b.b_v = take(w); b.w_o = take(w * w); b.b_o = take(w);
+    b.w1 = take(w * 4 * w); b.b1 = take(4 * w); b.w2 = take(4 * w * w); b.b2 = take(w);
+    b.ln1_g = take(w); b.ln1_b = take(w); b.ln2_g = take(w); b.ln2_b = take(w);
+    return b;
+  };
+  if (d.merge_inner)
+    for (int i = 0; i < d.inner_layers; ++i) o.inner[i] = block(d.d);
+  o.cross = block(D);
+  for (int i = 0; i < d.N; ++i) o.self_[i] = block(D);
+  const long long hin = 4 * D + 2 * d.d;
+  o.head_w1 = take(hin * d.head_hidden); o.head_b1 = take(d.head_hidden);
+  o.head_w2 = take(d.head_hidden); o.head_b2 = take(1);
+  o.total = off;
+  return o;
+}
+
+int validate(const LongerDims& d) {
+  if (d.L < 1 || d.d < 1 || d.K < 1) return fail(LONGER_ECONFIG, "L, d, K must all be >= 1");
+  if (d.m < 3) return fail(LONGER_ECONFIG, "m must be >= 3 (UID, at least one CLS, target)");
+  if (d.N < 1 || d.k < 1) return fail(LONGER_ECONFIG, "N and k must be >= 1");
+  if (d.query_strategy != 0) return fail(LONGER_ECONFIG, "device path implements the 'recent' query strategy");
+  const int Lp = (d.L + d.K - 1) / d.K * d.K, G = Lp / d.K, D = d.K * d.d;
+  if (d.k > G) return fail(LONGER_ECONFIG, "k exceeds merged length");
+  if (d.heads < 1 || D % d.heads) return fail(LONGER_ECONFIG, "D not divisible by heads");
+  if (d.d % 8) return fail(LONGER_ECONFIG, "device path needs d % 8 == 0 (16-byte TMA rows)");
+  if (D / d.heads > 256) return fail(LONGER_ECONFIG, "head width D/heads must be <= 256");
+  if (d.d > 64 || d.d_item + d.d_act + d.d_time > 64) return fail(LONGER_ECONFIG, "d and feature width must be <= 64");
+  if (d.n_time_buckets < 1 || d.n_time_buckets > 32) return fail(LONGER_ECONFIG, "n_time_buckets must be in [1, 32]");
+  if (d.merge_inner && (d.inner_layers < 1 || d.inner_layers > kMaxInner)) return fail(LONGER_ECONFIG, "inner_layers out of range");
+  if (d.merge_inner && d.K > 16) return fail(LONGER_ECONFIG, "InnerTrans group size K must be <= 16");
+  if (d.N > kMaxSelf) return fail(LONGER_ECONFIG, "N too large");
+  if (d.k + d.m > 256) return fail(LONGER_ECONFIG, "k + m must be <= 256");
+  if (d.batch < 1) return fail(LONGER_EDIM, "batch must be >= 1");
+  return LONGER_OK;
+}
+
+// ------------------------------------------------------------------ workspace plan
+struct Bump {
+  char* base;
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t n) {
+    off = (off + 255) & ~size_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += n * sizeof(T);
+    return p;
+  }
+};
+
+struct BlockBufs {            // one attention block over the q query rows
+  bf16 *qn, *qkv, *ctx, *x1n, *f1, *gf;
+  float *m1, *r1, *lse, *x1, *m2, *r2, *out;
+};
+struct InnerBufs {            // one InnerTrans layer over T tokens
+  bf16 *xn, *ctx, *x1n, *f1, *gf;
+  float *m1, *r1, *qkv, *probs, *x1, *m2, *r2, *out;
+};
+struct Packed {               // bf16 / fp32 operand copies of the weights
+  bf16 *seq_w1, *seq_w2, *glob_w1, *glob_w2;
+  bf16 *in_wqkv[kMaxInner], *in_wo[kMaxInner], *in_w1[kMaxInner], *in_w2[kMaxInner];
+  float* in_bqkv[kMaxInner];
+  bf16 *c_wq, *c_wkv, *c_wo, *c_w1, *c_w2;
+  float* c_bkv;
+  bf16 *s_wqkv[kMaxSelf], *s_wo[kMaxSelf], *s_w1[kMaxSelf], *s_w2[kMaxSelf];
+  float* s_bqkv[kMaxSelf];
+};
+
+struct Plan {
+  LongerDims dims;
+  void* ws;
+  int B, L, Lp, d, K, G, D, m, k, q, v, N, heads, inner, IL, hh, F, FP, HIN;
+  long long T;
+  ParamOff po;
+  int* status;
+  int32_t* npg;
+  Packed pk;
+  // tokens
+  bf16 *feat, *x0, *a1, *g1;
+  float *real, *keep, *h;
+  InnerBufs in[kMaxInner];
+  float* merged;
+  // globals
+  float *raw, *td, *glob;
+  bf16 *raw_bf, *ga, *gg;
+  // cross
+  float *O, *mk, *rk;
+  bf16 *kn, *KV;
+  BlockBufs cb;
+  BlockBufs sb[kMaxSelf];
+  // head
+  float *hin, *z1, *loss_per, *dz, *dz1;
+  // backward scratch (query rows)
+  float *dx, *dx1n, *dx1, *dctx, *dqn, *dO;
+  bf16 *dx_bf, *df1, *dx1_bf, *dqkv;
+  float* dkn;
+  bf16* dKV;
+  float *dmerged, *dglob, *draw;
+  bf16 *dglob_bf, *dga;
+  // backward scratch (tokens)
+  float *t_dx, *t_dx1n, *t_dx1, *t_dctx, *t_dxn, *dx0;
+  bf16 *t_dx_bf, *t_df1, *t_dx1_bf, *t_dqkv, *dh_bf, *da1, *dx0_bf;
+  size_t bytes;
+};
+
+Plan make_plan(const LongerDims& d, void* ws) {
+  Plan p{};
+  p.dims = d;
+  p.ws = ws;
+  p.B = d.batch; p.L = d.L; p.K = d.K; p.d = d.d;
+  p.Lp = (d.L + d.K - 1) / d.K * d.K;
+  p.G = p.Lp / d.K; p.D = d.K * d.d; p.m = d.m; p.k = d.k; p.q = d.k + d.m; p.v = p.G + d.m;
+  p.N = d.N; p.heads = d.heads; p.inner = d.merge_inner; p.IL = d.merge_inner ? d.inner_layers : 0;
+  p.hh = d.head_hidden; p.F = d.d_item + d.d_act + d.d_time; p.FP = (p.F + 7) / 8 * 8;
+  p.HIN = 4 * p.D + 2 * d.d;
+  p.T = (long long)p.B * p.Lp;
+  p.po = param_offsets(d);
+  Bump a{reinterpret_cast<char*>(ws)};
+  const long long T = p.T;
+  const int B = p.B, D = p.D, q = p.q, v = p.v, m = p.m, dd = p.d;
+  const long long Q = (long long)B * q, V = (long long)B * v, M = (long long)B * m;
+  p.status = a.take<int>(64);
+  p.npg = a.take<int32_t>(B);
+  // packed weights
+  p.pk.seq_w1 = a.take<bf16>(dd * 2 * D); p.pk.seq_w2 = a.take<bf16>(2 * D * dd);
+  p.pk.glob_w1 = a.take<bf16>(D * 2 * D); p.pk.glob_w2 = a.take<bf16>(2 * D * D);
+  for (int i = 0; i < p.IL; ++i) {
+    p.pk.in_wqkv[i] = a.take<bf16>(dd * 3 * dd); p.pk.in_bqkv[i] = a.take<float>(3 * dd);
+    p.pk.in_wo[i] = a.take<bf16>(dd * dd); p.pk.in_w1[i] = a.take<bf16>(dd * 4 * dd); p.pk.in_w2[i] = a.take<bf16>(4 * dd * dd);
+  }
+  p.pk.c_wq = a.take<bf16>(D * D); p.pk.c_wkv = a.take<bf16>(D * 2 * D); p.pk.c_bkv = a.take<float>(2 * D);
+  p.pk.c_wo = a.take<bf16>(D * D); p.pk.c_w1 = a.take<bf16>(D * 4 * D); p.pk.c_w2 = a.take<bf16>(4 * D * D);
+  for (int i = 0; i < p.N; ++i) {
+    p.pk.s_wqkv[i] = a.take<bf16>(D * 3 * D); p.pk.s_bqkv[i] = a.take<float>(3 * D);
+    p.pk.s_wo[i] = a.take<bf16>(D * D); p.pk.s_w1[i] = a.take<bf16>(D * 4 * D); p.pk.s_w2[i] = a.take<bf16>(4 * D * D);
+  }
+  // tokens
+  p.feat = a.take<bf16>(T * p.FP); p.x0 = a.take<bf16>(T * dd);
+  p.real = a.take<float>(T); p.keep = a.take<float>(T);
+  p.a1 = a.take<bf16>(T * 2 * D); p.g1 = a.take<bf16>(T * 2 * D);
+  p.h = a.take<float>(T * dd);
+  for (int i = 0; i < p.IL; ++i) {
+    InnerBufs& b = p.in[i];
+    b.xn = a.take<bf16>(T * dd); b.m1 = a.take<float>(T); b.r1 = a.take<float>(T);
+    b.qkv = a.take<float>(T * 3 * dd); b.probs = a.take<float>(T * d.K); b.ctx = a.take<bf16>(T * dd);
+    b.x1 = a.take<float>(T * dd); b.x1n = a.take<bf16>(T * dd); b.m2 = a.take<float>(T); b.r2 = a.take<float>(T);
+    b.f1 = a.take<bf16>(T * 4 * dd); b.gf = a.take<bf16>(T * 4 * dd); b.out = a.take<float>(T * dd);
+  }
+  p.merged = p.IL ? p.in[p.IL - 1].out : p.h;
+  // globals
+  p.raw = a.take<float>(M * D); p.raw_bf = a.take<bf16>(M * D); p.td = a.take<float>((long long)B * dd);
+  p.ga = a.take<bf16>(M * 2 * D); p.gg = a.take<bf16>(M * 2 * D); p.glob = a.take<float>(M * D);
+  // cross
+  p.O = a.take<float>(Q * D);
+  p.kn = a.take<bf16>(V * D); p.mk = a.take<float>(V); p.rk = a.take<float>(V);
+  p.KV = a.take<bf16>(V * 2 * D);
+  auto block_bufs = [&](BlockBufs& b, int qkv_cols) {
+    b.qn = a.take<bf16>(Q * D); b.m1 = a.take<float>(Q); b.r1 = a.take<float>(Q);
+    b.qkv = a.take<bf16>(Q * qkv_cols); b.ctx = a.take<bf16>(Q * D); b.lse = a.take<float>(Q * p.heads);
+    b.x1 = a.take<float>(Q * D); b.x1n = a.take<bf16>(Q * D); b.m2 = a.take<float>(Q); b.r2 = a.take<float>(Q);
+    b.f1 = a.take<bf16>(Q * 4 * D); b.gf = a.take<bf16>(Q * 4 * D); b.out = a.take<float>(Q * D);
+  };
+  block_bufs(p.cb, D);
+  for (int i = 0; i < p.N; ++i) block_bufs(p.sb[i], 3 * D);
+  // head
+  p.hin = a.take<float>((long long)B * p.HIN); p.z1 = a.take<float>((long long)B * p.hh);
+  p.loss_per = a.take<float>(B); p.dz = a.take<float>(B); p.dz1 = a.take<float>((long long)B * p.hh);
+  // backward (query rows)
+  p.dx = a.take<float>(Q * D); p.dx1n = a.take<float>(Q * D); p.dx1 = a.take<float>(Q * D);
+  p.dctx = a.take<float>(Q * D); p.dqn = a.take<float>(Q * D); p.dO = a.take<float>(Q * D);
+  p.dx_bf = a.take<bf16>(Q * D); p.df1 = a.take<bf16>(Q * 4 * D); p.dx1_bf = a.take<bf16>(Q * D);
+  p.dqkv = a.take<bf16>(Q * 3 * D);
+  p.dkn = a.take<float>(V * D); p.dKV = a.take<bf16>(V * 2 * D);
+  p.dmerged = a.take<float>(T * dd); p.dglob = a.take<float>(M * D); p.draw = a.take<float>(M * D);
+  p.dglob_bf = a.take<bf16>(M * D); p.dga = a.take<bf16>(M * 2 * D);
+  // backward (tokens)
+  if (p.IL) {
+    p.t_dx = a.take<float>(T * dd); p.t_dx1n = a.take<float>(T * dd); p.t_dx1 = a.take<float>(T * dd);
+    p.t_dctx = a.take<float>(T * dd); p.t_dxn = a.take<float>(T * dd);
+    p.t_dx_bf = a.take<bf16>(T * dd); p.t_df1 = a.take<bf16>(T * 4 * dd); p.t_dx1_bf = a.take<bf16>(T * dd);
+    p.t_dqkv = a.take<bf16>(T * 3 * dd);
+  }
+  p.dh_bf = a.take<bf16>(T * dd); p.da1 = a.take<bf16>(T * 2 * D);
+  p.dx0 = a.take<float>(T * dd); p.dx0_bf = a.take<bf16>(T * dd);
+  p.bytes = a.off + 256;
+  return p;
+}
+
+// ------------------------------------------------------------------ helpers
+struct Ctx {
+  const Plan& p;
+  const float* P;       // fp32 params
+  float* G;             // fp32 grads
+  cudaStream_t st;
+  int rc = 0;
+  const float* w(long long off) const { return P + off; }
+  float* g(long long off) const { return G + off; }
+};
+
+#define TRY(expr)                                   \
+  do {                                              \
+    int _rc = (expr);                               \
+    if (_rc) return fail(LONGER_ECUDA, #expr);      \
+  } while (0)
+
+// C[M,N] (=|+=) epi(A[M,K]·B[K,N]); majors: a_mn / b_mn as in gemm.cuh
+GemmArgs G_(const void* A, int lda, int amn, const void* B, int ldb, int bmn, long long M, int N, long long K) {
+  GemmArgs g;
+  g.A = A; g.lda = lda; g.a_mn_major = amn; g.B = B; g.ldb = ldb; g.b_mn_major = bmn;
+  g.M = (int)M; g.N = N; g.K = (int)K; g.flags = 0;
+  return g;
+}
+
+// Y = X·W (+bias) variants
+int lin_fwd(cudaStream_t st, const bf16* X, int ldx, long long rows, const bf16* W, int in, int out, const float* bias,
+            uint32_t flags, float* C, bf16* Cbf, bf16* pre, const float* resid = nullptr, int ldr = 0,
+            const float* rowmask = nullptr) {
+  GemmArgs g = G_(X, ldx, 0, W, out, 1, rows, out, in);
+  g.flags = flags | (bias ? EPI_BIAS : 0u) | (C ? EPI_OUT_F32 : 0u) | (Cbf ? EPI_OUT_BF16 : 0u) |
+            (resid ? EPI_RESID : 0u) | (rowmask ? EPI_ROWMASK : 0u);
+  g.bias = bias; g.C = C; g.ldc = out; g.C_bf16 = Cbf; g.ldc_bf = out; g.pre_bf16 = pre;
+  g.resid = resid; g.ldr = ldr; g.rowmask = rowmask;
+  return gemm_launch(g, st);
+}
+
+// dX = dY·Wᵀ  (W stored [in, out] row-major = [N][K] K-major B), optional GELU' epilogue
+int lin_dx(cudaStream_t st, const bf16* dY, int lddy, long long rows, const bf16* W, int ldw, int in, int out,
+           float* C, int ldc, bf16* Cbf, int ldcbf, const bf16* gelu_pre = nullptr, const float* rowmask = nullptr) {
+  GemmArgs g = G_(dY, lddy, 0, W, ldw, 0, rows, in, out);
+  g.flags = (C ? EPI_OUT_F32 : 0u) | (Cbf ? EPI_OUT_BF16 : 0u) | (gelu_pre ? EPI_GELU_BWD : 0u) |
+            (rowmask ? EPI_ROWMASK : 0u);
+  g.C = C; g.ldc = ldc; g.C_bf16 = Cbf; g.ldc_bf = ldcbf; g.pre_bf16 = const_cast<bf16*>(gelu_pre);
+  g.rowmask = rowmask;
+  return gemm_launch(g, st);
+}
+
+// dW[in, out] += Xᵀ·dY over `rows` rows (both stored row-major → MN-major operands)
+int lin_dw(cudaStream_t st, const bf16* X, int ldx, int in, const bf16* dY, int lddy, int out, long long rows,
+           float* dW) {
+  GemmArgs g = G_(X, ldx, 1, dY, lddy, 1, in, out, rows);
+  g.flags = EPI_OUT_F32 | EPI_ATOMIC;
+  g.split_k = 0;
+  g.C = dW; g.ldc = out;
+  return gemm_launch(g, st);
+}
+
+RowMap rows_plain(const float* x, int ld, long long rows) {
+  RowMap r{};
+  r.A = x; r.lda = ld; r.a_rows = (int)rows; r.a_off = 0; r.na = (int)rows; r.Bsrc = nullptr; r.ldb = 0; r.nb = 0;
+  r.batch = 1;
+  return r;
+}
+RowMapW rows_plain_w(float* x, int ld, long long rows) {
+  RowMapW r{};
+  r.A = x; r.lda = ld; r.a_rows = (int)rows; r.a_off = 0; r.na = (int)rows; r.Bsrc = nullptr; r.ldb = 0; r.nb = 0;
+  r.batch = 1;
+  return r;
+}
+
+// ------------------------------------------------------------------ weight packing
+void add_spec(PackList& L, long long src, void* dst, void* base, int rows, int cols, int src_ld, int dst_ld,
+              int to_bf16, int dst_col = 0) {
+  CopySpec s;
+  const long long byte_off = reinterpret_cast<char*>(dst) - reinterpret_cast<char*>(base);
+  const int esz = to_bf16 ? 2 : 4;
+  s.src_off = (int)src;
+  s.dst_off = (int)(byte_off / esz) + dst_col;
+  s.rows = rows; s.cols = cols; s.src_ld = src_ld; s.dst_ld = dst_ld; s.to_bf16 = to_bf16;
+  L.s[L.n++] = s;
+}
+
+int pack_weights(const Plan& p, const float* params, void* ws, cudaStream_t st) {
+  PackList L;
+  L.n = 0;
+  const ParamOff& o = p.po;
+  const int d = p.d, D = p.D;
+  // bf16 destinations are addressed in bf16 elements from ws; fp32 in floats from ws (both 256-aligned)
+  add_spec(L, o.seq_w1, p.pk.seq_w1, ws, d, 2 * D, 2 * D, 2 * D, 1);
+  add_spec(L, o.seq_w2, p.pk.seq_w2, ws, 2 * D, d, d, d, 1);
+  add_spec(L, o.glob_w1, p.pk.glob_w1, ws, D, 2 * D, 2 * D, 2 * D, 1);
+  add_spec(L, o.glob_w2, p.pk.glob_w2, ws, 2 * D, D, D, D, 1);
+  for (int i = 0; i < p.IL; ++i) {
+    const BlockOff& b = o.inner[i];
+    add_spec(L, b.w_q, p.pk.in_wqkv[i], ws, d, d, d, 3 * d, 1, 0);
+    add_spec(L, b.w_k, p.pk.in_wqkv[i], ws, d, d, d, 3 * d, 1, d);
+    add_spec(L, b.w_v, p.pk.in_wqkv[i], ws, d, d, d, 3 * d, 1, 2 * d);
+    add_spec(L, b.b_q, p.pk.in_bqkv[i], ws, 1, d, d, d, 0, 0);
+    add_spec(L, b.b_k, p.pk.in_bqkv[i], ws, 1, d, d, d, 0, d);
+    add_spec(L, b.b_v, p.pk.in_bqkv[i], ws, 1, d, d, d, 0, 2 * d);
+    add_spec(L, b.w_o, p.pk.in_wo[i], ws, d, d, d, d, 1);
+    add_spec(L, b.w1, p.pk.in_w1[i], ws, d, 4 * d, 4 * d, 4 * d, 1);
+    add_spec(L, b.w2, p.pk.in_w2[i], ws, 4 * d, d, d, d, 1);
+  }
+  {
+    const BlockOff& b = o.cross;
+    add_spec(L, b.w_q, p.pk.c_wq, ws, D, D, D, D, 1);
+    add_spec(L, b.w_k, p.pk.c_wkv, ws, D, D, D, 2 * D, 1, 0);
+    add_spec(L, b.w_v, p.pk.c_wkv, ws, D, D, D, 2 * D, 1, D);
+    add_spec(L, b.b_k, p.pk.c_bkv, ws, 1, D, D, D, 0, 0);
+    add_spec(L, b.b_v, p.pk.c_bkv, ws, 1, D, D, D, 0, D);
+    add_spec(L, b.w_o, p.pk.c_wo, ws, D, D, D, D, 1);
+    add_spec(L, b.w1, p.pk.c_w1, ws, D, 4 * D, 4 * D, 4 * D, 1);
+    add_spec(L, b.w2, p.pk.c_w2, ws, 4 * D, D, D, D, 1);
+  }
+  for (int i = 0; i < p.N; ++i) {
+    const BlockOff& b = o.self_[i];
+    add_spec(L, b.w_q, p.pk.s_wqkv[i], ws, D, D, D, 3 * D, 1, 0);
+    add_spec(L, b.w_k, p.pk.s_wqkv[i], ws, D, D, D, 3 * D, 1, D);
+    add_spec(L, b.w_v, p.pk.s_wqkv[i], ws, D, D, D, 3 * D, 1, 2 * D);
+    add_spec(L, b.b_q, p.pk.s_bqkv[i], ws, 1, D, D, D, 0, 0);
+    add_spec(L, b.b_k, p.pk.s_bqkv[i], ws, 1, D, D, D, 0, D);
+    add_spec(L, b.b_v, p.pk.s_bqkv[i], ws, 1, D, D, D, 0, 2 * D);
+    add_spec(L, b.w_o, p.pk.s_wo[i], ws, D, D, D, D, 1);
+    add_spec(L, b.w1, p.pk.s_w1[i], ws, D, 4 * D, 4 * D, 4 * D, 1);
+    add_spec(L, b.w2, p.pk.s_w2[i], ws, 4 * D, D, D, D, 1);
+  }
+  pack_params(params, L, ws, st);
+  return (int)cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ forward
+// One pre-norm attention block over the q query rows (pkg/src/longrec/attention.py:172-212).
+int block_fwd(const Ctx& c, const BlockOff& bo, BlockBufs& b, const float* xq, bool cross, const bf16* Wqkv,
+              const float* bqkv, const bf16* Wo, const bf16* W1, const bf16* W2) {
+  const Plan& p = c.p;
+  cudaStream_t st = c.st;
+  const int D = p.D;
+  const long long Q = (long long)p.B * p.q;
+  layernorm_fwd(rows_plain(xq, D, Q), D, c.w(bo.ln1_g), c.w(bo.ln1_b), b.qn, b.m1, b.r1, st);
+  AttnArgs a{};
+  a.nq = p.q; a.D = D; a.heads = p.heads; a.k = p.k; a.G = p.G; a.npg = p.npg; a.B = p.B;
+  a.ctx = b.ctx; a.ldc = D; a.sc = (long long)p.q * D; a.lse = b.lse;
+  if (cross) {
+    // R = [merged; globals] → LN1 (same ln1 params) → [K | V] projection over all v rows
+    RowMap r{};
+    r.A = p.merged; r.lda = D; r.a_rows = p.G; r.a_off = 0; r.na = p.G; r.Bsrc = p.glob; r.ldb = D; r.nb = p.m;
+    r.batch = p.B;
+    layernorm_fwd(r, D, c.w(bo.ln1_g), c.w(bo.ln1_b), p.kn, p.mk, p.rk, st);
+    TRY(lin_fwd(st, b.qn, D, Q, Wqkv, D, D, c.w(bo.b_q), 0, nullptr, b.qkv, nullptr));
+    TRY(lin_fwd(st, p.kn, D, (long long)p.B * p.v, p.pk.c_wkv, D, 2 * D, p.pk.c_bkv, 0, nullptr, p.KV, nullptr));
+    a.Q = b.qkv; a.ldq = D; a.sq = (long long)p.q * D;
+    a.Kp = p.KV; a.ldk = 2 * D; a.sk = (long long)p.v * 2 * D;
+    a.V = p.KV + D; a.ldv = 2 * D; a.sv = (long long)p.v * 2 * D;
+    a.nk = p.v; a.ns = p.G; a.goff = 0;
+  } else {
+    TRY(lin_fwd(st, b.qn, D, Q, Wqkv, D, 3 * D, bqkv, 0, nullptr, b.qkv, nullptr));
+    a.Q = b.qkv; a.ldq = 3 * D; a.sq = (long long)p.q * 3 * D;
+    a.Kp = b.qkv + D; a.ldk = 3 * D; a.sk = a.sq;
+    a.V = b.qkv + 2 * D; a.ldv = 3 * D; a.sv = a.sq;
+    a.nk = p.q; a.ns = p.k; a.goff = p.G - p.k;
+  }
+  attn_fwd(a, st);
+  TRY(lin_fwd(st, b.ctx, D, Q, Wo, D, D, c.w(bo.b_o), 0, b.x1, nullptr, nullptr, xq, D));
+  layernorm_fwd(rows_plain(b.x1, D, Q), D, c.w(bo.ln2_g), c.w(bo.ln2_b), b.x1n, b.m2, b.r2, st);
+  TRY(lin_fwd(st, b.x1n, D, Q, W1, D, 4 * D, c.w(bo.b1), EPI_GELU | EPI_SAVE_PRE, nullptr, b.gf, b.f1));
+  TRY(lin_fwd(st, b.gf, 4 * D, Q, W2, 4 * D, D, c.w(bo.b2), 0, b.out, nullptr, nullptr, b.x1, D));
+  return 0;
+}
+
+int forward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs, float* loss, int with_loss) {
+  cudaStream_t st = c.st;
+  const ParamOff& o = p.po;
+  const LongerDims& dm = p.dims;
+  const int d = p.d, D = p.D;
+  const long long T = p.T, M = (long long)p.B * p.m;
+  TRY(pack_weights(p, c.P, p.ws, st));
+  // featurise + recency position (inputs.py:434-482)
+  EmbedArgs e{};
+  e.items = bt.items; e.actions = bt.actions; e.dt = bt.dt; e.n_events = bt.n_events;
+  e.B = p.B; e.L = p.L; e.Lp = p.Lp; e.d = d; e.d_item = dm.d_item; e.d_act = dm.d_act; e.d_time = dm.d_time;
+  e.FP = p.FP; e.nb = dm.n_time_buckets; e.vocab = dm.vocab; e.n_actions = dm.n_actions; e.K = p.K;
+  e.item_tab = c.w(o.item); e.act_tab = c.w(o.act); e.time_tab = c.w(o.time); e.pos_tab = c.w(o.pos);
+  e.tok_w = c.w(o.tok_w); e.tok_b = c.w(o.tok_b);
+  e.feat = p.feat; e.x0 = p.x0; e.real = p.real; e.keep = p.keep; e.status = p.status; e.npg = p.npg;
+  embed_fwd(e, st);
+  // per-token input MLP (inputs.py:447-449); pad rows zeroed (inputs.py:478-481)
+  TRY(lin_fwd(st, p.x0, d, T, p.pk.seq_w1, d, 2 * D, c.w(o.seq_b1), EPI_GELU | EPI_SAVE_PRE, nullptr, p.g1, p.a1));
+  TRY(lin_fwd(st, p.g1, 2 * D, T, p.pk.seq_w2, 2 * D, d, c.w(o.seq_b2), 0, p.h, nullptr, nullptr, nullptr, 0, p.real));
+  // InnerTrans merge (merge.py:83-112)
+  const float* x = p.h;
+  for (int i = 0; i < p.IL; ++i) {
+    const InnerBufs& b = p.in[i];
+    const BlockOff& bo = o.inner[i];
+    layernorm_fwd(rows_plain(x, d, T), d, c.w(bo.ln1_g), c.w(bo.ln1_b), b.xn, b.m1, b.r1, st);
+    TRY(lin_fwd(st, b.xn, d, T, p.pk.in_wqkv[i], d, 3 * d, p.pk.in_bqkv[i], 0, b.qkv, nullptr, nullptr));
+    group_attn_fwd(b.qkv, (int)T, p.K, d, b.ctx, b.probs, st);
+    TRY(lin_fwd(st, b.ctx, d, T, p.pk.in_wo[i], d, d, c.w(bo.b_o), 0, b.x1, nullptr, nullptr, x, d));
+    layernorm_fwd(rows_plain(b.x1, d, T), d, c.w(bo.ln2_g), c.w(bo.ln2_b), b.x1n, b.m2, b.r2, st);
+    TRY(lin_fwd(st, b.x1n, d, T, p.pk.in_w1[i], d, 4 * d, c.w(bo.b1), EPI_GELU | EPI_SAVE_PRE, nullptr, b.gf, b.f1));
+    TRY(lin_fwd(st, b.gf, 4 * d, T, p.pk.in_w2[i], 4 * d, d, c.w(bo.b2), 0, b.out, nullptr, nullptr, b.x1, d,
+                i == p.IL - 1 ? p.keep : nullptr));
+    x = b.out;
+  }
+  // global tokens (inputs.py:500-537)
+  GlobalsArgs ga{};
+  ga.uid = bt.uid; ga.cand_item = bt.cand_item; ga.B = p.B; ga.m = p.m; ga.d = d; ga.D = D;
+  ga.d_item = dm.d_item; ga.d_act = dm.d_act; ga.d_time = dm.d_time;
+  ga.uid_tab = c.w(o.uid); ga.item_tab = c.w(o.item); ga.time_tab = c.w(o.time); ga.cls = c.w(o.cls);
+  ga.tok_w = c.w(o.tok_w); ga.tok_b = c.w(o.tok_b); ga.lift_w = c.w(o.lift_w); ga.lift_b = c.w(o.lift_b);
+  ga.raw = p.raw; ga.raw_bf = p.raw_bf; ga.td = p.td;
+  globals_raw_fwd(ga, st);
+  TRY(lin_fwd(st, p.raw_bf, D, M, p.pk.glob_w1, D, 2 * D, c.w(o.glob_b1), EPI_GELU | EPI_SAVE_PRE, nullptr, p.gg, p.ga));
+  TRY(lin_fwd(st, p.gg, 2 * D, M, p.pk.glob_w2, 2 * D, D, c.w(o.glob_b2), 0, p.glob, nullptr, nullptr));
+  // composite queries O = [merged[G-k:]; globals] (model.py:317-319)
+  gather_rows_f32(p.merged, p.B, p.G, p.G - p.k, p.k, p.O, p.q, 0, D, st);
+  gather_rows_f32(p.glob, p.B, p.m, 0, p.m, p.O, p.q, p.k, D, st);
+  Plan& pm = const_cast<Plan&>(p);
+  TRY(block_fwd(c, o.cross, pm.cb, p.O, true, p.pk.c_wq, nullptr, p.pk.c_wo, p.pk.c_w1, p.pk.c_w2));
+  const float* xl = p.cb.out;
+  for (int i = 0; i < p.N; ++i) {
+    TRY(block_fwd(c, o.self_[i], pm.sb[i], xl, false, p.pk.s_wqkv[i], p.pk.s_bqkv[i], p.pk.s_wo[i], p.pk.s_w1[i],
+                  p.pk.s_w2[i]));
+    xl = p.sb[i].out;
+  }
+  HeadArgs h{};
+  h.x = xl; h.B = p.B; h.q = p.q; h.k = p.k; h.m = p.m; h.D = D; h.d = d; h.hh = p.hh;
+  h.uid = bt.uid; h.profile = bt.profile; h.label = bt.label;
+  h.uid_tab = c.w(o.uid); h.prof_tab = c.w(o.prof);
+  h.w1 = c.w(o.head_w1); h.b1 = c.w(o.head_b1); h.w2 = c.w(o.head_w2); h.b2 = c.w(o.head_b2);
+  h.hin = p.hin; h.z1 = p.z1; h.probs = probs;
+  h.loss_per = with_loss ? p.loss_per : nullptr; h.dz = p.dz; h.loss = loss;
+  head_fwd(h, with_loss, st);
+  TRY((int)cudaGetLastError());
+  return 0;
+}
+
+// Backward of one attention block; dout in p.dx, d(x_q) written back to p.dx (self) or into
+// dmerged / dglob (cross).  (pkg/src/longrec/attention.py:172-212 + tensors.py backward closures)
+int block_bwd(const Ctx& c, const BlockOff& bo, const BlockBufs& b, const float* xq, bool cross, const bf16* Wqkv,
+              const bf16* Wo, const bf16* W1, const bf16* W2) {
+  const Plan& p = c.p;
+  cudaStream_t st = c.st;
+  const int D = p.D;
+  const long long Q = (long long)p.B * p.q, V = (long long)p.B * p.v;
+  cast_rows_bf16(p.dx, (int)Q, D, D, p.dx_bf, D, nullptr, st);
+  // FFN + residual
+  TRY(lin_dx(st, p.dx_bf, D, Q, W2, D, 4 * D, D, nullptr, 0, p.df1, 4 * D, b.f1));
+  TRY(lin_dw(st, b.gf, 4 * D, 4 * D, p.dx_bf, D, D, Q, c.g(bo.w2)));
+  colsum_f32(p.dx, (int)Q, D, D, c.g(bo.b2), st);
+  TRY(lin_dx(st, p.df1, 4 * D, Q, W1, 4 * D, D, 4 * D, p.dx1n, D, nullptr, 0));
+  TRY(lin_dw(st, b.x1n, D, D, p.df1, 4 * D, 4 * D, Q, c.g(bo.w1)));
+  colsum_bf16(p.df1, (int)Q, 4 * D, 4 * D, c.g(bo.b1), st);
+  TRY((int)cudaMemcpyAsync(p.dx1, p.dx, Q * D * 4, cudaMemcpyDeviceToDevice, st));
+  layernorm_bwd(rows_plain(b.x1, D, Q), D, c.w(bo.ln2_g), b.m2, b.r2, p.dx1n, D, rows_plain_w(p.dx1, D, Q), 1,
+                nullptr, c.g(bo.ln2_g), c.g(bo.ln2_b), st);
+  cast_rows_bf16(p.dx1, (int)Q, D, D, p.dx1_bf, D, nullptr, st);
+  // output projection + residual
+  TRY(lin_dx(st, p.dx1_bf, D, Q, Wo, D, D, D, p.dctx, D, nullptr, 0));
+  TRY(lin_dw(st, b.ctx, D, D, p.dx1_bf, D, D, Q, c.g(bo.w_o)));
+  colsum_f32(p.dx1, (int)Q, D, D, c.g(bo.b_o), st);
+  // attention
+  AttnArgs a{};
+  a.nq = p.q; a.D = D; a.heads = p.heads; a.k = p.k; a.G = p.G; a.npg = p.npg; a.B = p.B;
+  a.ctx = b.ctx; a.ldc = D; a.sc = (long long)p.q * D; a.lse = b.lse;
+  a.dctx = p.dctx; a.lddc = D; a.sdc = (long long)p.q * D; a.ctx_in = b.ctx;
+  if (cross) {
+    a.Q = b.qkv; a.ldq = D; a.sq = (long long)p.q * D;
+    a.Kp = p.KV; a.ldk = 2 * D; a.sk = (long long)p.v * 2 * D;
+    a.V = p.KV + D; a.ldv = 2 * D; a.sv = a.sk;
+    a.nk = p.v; a.ns = p.G; a.goff = 0;
+    a.dQ = p.dqkv; a.lddq = D; a.sdq = (long long)p.q * D;
+    a.dK = p.dKV; a.lddk = 2 * D; a.sdk = (long long)p.v * 2 * D;
+    a.dV = p.dKV + D; a.lddv = 2 * D; a.sdv = a.sdk;
+  } else {
+    a.Q = b.qkv; a.ldq = 3 * D; a.sq = (long long)p.q * 3 * D;
+    a.Kp = b.qkv + D; a.ldk = 3 * D; a.sk = a.sq;
+    a.V = b.qkv + 2 * D; a.ldv = 3 * D; a.sv = a.sq;
+    a.nk = p.q; a.ns = p.k; a.goff = p.G - p.k;
+    a.dQ = p.dqkv; a.lddq = 3 * D; a.sdq = (long long)p.q * 3 * D;
+    a.dK = p.dqkv + D; a.lddk = 3 * D; a.sdk = a.sdq;
+    a.dV = p.dqkv + 2 * D; a.lddv = 3 * D; a.sdv = a.sdq;
+  }
+  attn_bwd(a, st);
+  if (cross) {
+    TRY(lin_dx(st, p.dqkv, D, Q, Wqkv, D, D, D, p.dqn, D, nullptr, 0));
+    TRY(lin_dw(st, b.qn, D, D, p.dqkv, D, D, Q, c.g(bo.w_q)));
+    colsum_bf16(p.dqkv, (int)Q, D, D, c.g(bo.b_q), st);
+    TRY(lin_dx(st, p.dKV, 2 * D, V, p.pk.c_wkv, 2 * D, D, 2 * D, p.dkn, D, nullptr, 0));
+    TRY(lin_dw(st, p.kn, D, D, p.dKV, 2 * D, D, V, c.g(bo.w_k)));
+    TRY(lin_dw(st, p.kn, D, D, p.dKV + D, 2 * D, D, V, c.g(bo.w_v)));
+    colsum_bf16(p.dKV, (int)V, D, 2 * D, c.g(bo.b_k), st);
+    colsum_bf16(p.dKV + D, (int)V, D, 2 * D, c.g(bo.b_v), st);
+    RowMap r{};
+    r.A = p.merged; r.lda = D; r.a_rows = p.G; r.a_off = 0; r.na = p.G; r.Bsrc = p.glob; r.ldb = D; r.nb = p.m;
+    r.batch = p.B;
+    RowMapW rw{};
+    rw.A = p.dmerged; rw.lda = D; rw.a_rows = p.G; rw.a_off = 0; rw.na = p.G; rw.Bsrc = p.dglob; rw.ldb = D;
+    rw.nb = p.m; rw.batch = p.B;
+    layernorm_bwd(r, D, c.w(bo.ln1_g), p.mk, p.rk, p.dkn, D, rw, 0, nullptr, c.g(bo.ln1_g), c.g(bo.ln1_b), st);
+    TRY((int)cudaMemcpyAsync(p.dO, p.dx1, Q * D * 4, cudaMemcpyDeviceToDevice, st));
+    layernorm_bwd(rows_plain(xq, D, Q), D, c.w(bo.ln1_g), b.m1, b.r1, p.dqn, D, rows_plain_w(p.dO, D, Q), 1,
+                  nullptr, c.g(bo.ln1_g), c.g(bo.ln1_b), st);
+    add_rows_f32(p.dO, p.B, p.q, 0, p.k, p.dmerged, p.G, p.G - p.k, D, st);
+    add_rows_f32(p.dO, p.B, p.q, p.k, p.m, p.dglob, p.m, 0, D, st);
+  } else {
+    TRY(lin_dx(st, p.dqkv, 3 * D, Q, Wqkv, 3 * D, D, 3 * D, p.dqn, D, nullptr, 0));
+    for (int j = 0; j < 3; ++j) {
+      const long long wo = j == 0 ? bo.w_q : (j == 1 ? bo.w_k : bo.w_v);
+      const long long bb = j == 0 ? bo.b_q : (j == 1 ? bo.b_k : bo.b_v);
+      TRY(lin_dw(st, b.qn, D, D, p.dqkv + j * D, 3 * D, D, Q, c.g(wo)));
+      colsum_bf16(p.dqkv + j * D, (int)Q, D, 3 * D, c.g(bb), st);
+    }
+    TRY((int)cudaMemcpyAsync(p.dx, p.dx1, Q * D * 4, cudaMemcpyDeviceToDevice, st));
+    layernorm_bwd(rows_plain(xq, D, Q), D, c.w(bo.ln1_g), b.m1, b.r1, p.dqn, D, rows_plain_w(p.dx, D, Q), 1,
+                  nullptr, c.g(bo.ln1_g), c.g(bo.ln1_b), st);
+  }
+  return 0;
+}
+
+int backward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs) {
+  cudaStream_t st = c.st;
+  const ParamOff& o = p.po;
+  const LongerDims& dm = p.dims;
+  const int d = p.d, D = p.D;
+  const long long T = p.T, M = (long long)p.B * p.m, Q = (long long)p.B * p.q;
+  TRY((int)cudaMemsetAsync(c.G, 0, o.total * 4, st));
+  TRY((int)cudaMemsetAsync(p.dx, 0, Q * D * 4, st));
+  // head (model.py:346-362) → dx rows k+m-1 (target) and k+1 (CLS)
+  HeadArgs h{};
+  h.x = p.N ? p.sb[p.N - 1].out : p.cb.out;
+  h.B = p.B; h.q = p.q; h.k = p.k; h.m = p.m; h.D = D; h.d = d; h.hh = p.hh;
+  h.uid = bt.uid; h.profile = bt.profile; h.label = bt.label;
+  h.uid_tab = c.w(o.uid); h.prof_tab = c.w(o.prof);
+  h.w1 = c.w(o.head_w1); h.b1 = c.w(o.head_b1); h.w2 = c.w(o.head_w2); h.b2 = c.w(o.head_b2);
+  h.hin = p.hin; h.z1 = p.z1; h.probs = probs; h.dz = p.dz; h.dz1 = p.dz1; h.dx = p.dx;
+  h.g_w1 = c.g(o.head_w1); h.g_b1 = c.g(o.head_b1); h.g_w2 = c.g(o.head_w2); h.g_b2 = c.g(o.head_b2);
+  h.g_uid = c.g(o.uid); h.g_prof = c.g(o.prof);
+  head_bwd(h, st);
+  for (int i = p.N - 1; i >= 0; --i) {
+    const float* xin = i == 0 ? p.cb.out : p.sb[i - 1].out;
+    TRY(block_bwd(c, o.self_[i], p.sb[i], xin, false, p.pk.s_wqkv[i], p.pk.s_wo[i], p.pk.s_w1[i], p.pk.s_w2[i]));
+  }
+  TRY(block_bwd(c, o.cross, p.cb, p.O, true, p.pk.c_wq, p.pk.c_wo, p.pk.c_w1, p.pk.c_w2));
+  // global-token MLP and raw rows
+  cast_rows_bf16(p.dglob, (int)M, D, D, p.dglob_bf, D, nullptr, st);
+  TRY(lin_dx(st, p.dglob_bf, D, M, p.pk.glob_w2, D, 2 * D, D, nullptr, 0, p.dga, 2 * D, p.ga));
+  TRY(lin_dw(st, p.gg, 2 * D, 2 * D, p.dglob_bf, D, D, M, c.g(o.glob_w2)));
+  colsum_f32(p.dglob, (int)M, D, D, c.g(o.glob_b2), st);
+  TRY(lin_dx(st, p.dga, 2 * D, M, p.pk.glob_w1, 2 * D, D, 2 * D, p.draw, D, nullptr, 0));
+  TRY(lin_dw(st, p.raw_bf, D, D, p.dga, 2 * D, 2 * D, M, c.g(o.glob_w1)));
+  colsum_bf16(p.dga, (int)M, 2 * D, 2 * D, c.g(o.glob_b1), st);
+  GlobalsArgs ga{};
+  ga.uid = bt.uid; ga.cand_item = bt.cand_item; ga.B = p.B; ga.m = p.m; ga.d = d; ga.D = D;
+  ga.d_item = dm.d_item; ga.d_act = dm.d_act; ga.d_time = dm.d_time;
+  ga.uid_tab = c.w(o.uid); ga.item_tab = c.w(o.item); ga.time_tab = c.w(o.time); ga.cls = c.w(o.cls);
+  ga.tok_w = c.w(o.tok_w); ga.tok_b = c.w(o.tok_b); ga.lift_w = c.w(o.lift_w); ga.lift_b = c.w(o.lift_b);
+  ga.td = p.td; ga.draw = p.draw;
+  ga.g_uid = c.g(o.uid); ga.g_item = c.g(o.item); ga.g_time = c.g(o.time); ga.g_cls = c.g(o.cls);
+  ga.g_tok_w = c.g(o.tok_w); ga.g_tok_b = c.g(o.tok_b); ga.g_lift_w = c.g(o.lift_w); ga.g_lift_b = c.g(o.lift_b);
+  globals_raw_bwd(ga, st);
+  // InnerTrans backward (all-pad groups were zeroed after the last layer)
+  float* dxt = p.dmerged;
+  if (p.IL) mul_rows_inplace(dxt, (int)T, d, p.keep, st);
+  for (int i = p.IL - 1; i >= 0; --i) {
+    const InnerBufs& b = p.in[i];
+    const BlockOff& bo = o.inner[i];
+    const float* xin = i == 0 ? p.h : p.in[i - 1].out;
+    cast_rows_bf16(dxt, (int)T, d, d, p.t_dx_bf, d, nullptr, st);
+    TRY(lin_dx(st, p.t_dx_bf, d, T, p.pk.in_w2[i], d, 4 * d, d, nullptr, 0, p.t_df1, 4 * d, b.f1));
+    TRY(lin_dw(st, b.gf, 4 * d, 4 * d, p.t_dx_bf, d, d, T, c.g(bo.w2)));
+    colsum_f32(dxt, (int)T, d, d, c.g(bo.b2), st);
+    TRY(lin_dx(st, p.t_df1, 4 * d, T, p.pk.in_w1[i], 4 * d, d, 4 * d, p.t_dx1n, d, nullptr, 0));
+    TRY(lin_dw(st, b.x1n, d, d, p.t_df1, 4 * d, 4 * d, T, c.g(bo.w1)));
+    colsum_bf16(p.t_df1, (int)T, 4 * d, 4 * d, c.g(bo.b1), st);
+    TRY((int)cudaMemcpyAsync(p.t_dx1, dxt, T * d * 4, cudaMemcpyDeviceToDevice, st));
+    layernorm_bwd(rows_plain(b.x1, d, T), d, c.w(bo.ln2_g), b.m2, b.r2, p.t_dx1n, d, rows_plain_w(p.t_dx1, d, T), 1,
+                  nullptr, c.g(bo.ln2_g), c.g(bo.ln2_b), st);
+    cast_rows_bf16(p.t_dx1, (int)T, d, d, p.t_dx1_bf, d, nullptr, st);
+    TRY(lin_dx(st, p.t_dx1_bf, d, T, p.pk.in_wo[i], d, d, d, p.t_dctx, d, nullptr, 0));
+    TRY(lin_dw(st, b.ctx, d, d, p.t_dx1_bf, d, d, T, c.g(bo.w_o)));
+    colsum_f32(p.t_dx1, (int)T, d, d, c.g(bo.b_o), st);
+    group_attn_bwd(b.qkv, b.probs, p.t_dctx, (int)T, p.K, d, p.t_dqkv, st);
+    TRY(lin_dx(st, p.t_dqkv, 3 * d, T, p.pk.in_wqkv[i], 3 * d, d, 3 * d, p.t_dxn, d, nullptr, 0));
+    for (int j = 0; j < 3; ++j) {
+      const long long wo = j == 0 ? bo.w_q : (j == 1 ? bo.w_k : bo.w_v);
+      const long long bb = j == 0 ? bo.b_q : (j == 1 ? bo.b_k : bo.b_v);
+      TRY(lin_dw(st, b.xn, d, d, p.t_dqkv + j * d, 3 * d, d, T, c.g(wo)));
+      colsum_bf16(p.t_dqkv + j * d, (int)T, d, 3 * d, c.g(bb), st);
+    }
+    TRY((int)cudaMemcpyAsync(p.t_dx, p.t_dx1, T * d * 4, cudaMemcpyDeviceToDevice, st));
+    layernorm_bwd(rows_plain(xin, d, T), d, c.w(bo.ln1_g), b.m1, b.r1, p.t_dxn, d, rows_plain_w(p.t_dx, d, T), 1,
+                  nullptr, c.g(bo.ln1_g), c.g(bo.ln1_b), st);
+    dxt = p.t_dx;
+  }
+  // token MLP + featuriser (inputs.py:434-482); only real tokens carry gradient
+  cast_rows_bf16(dxt, (int)T, d, d, p.dh_bf, d, p.real, st);
+  TRY(lin_dx(st, p.dh_bf, d, T, p.pk.seq_w2, d, 2 * D, d, nullptr, 0, p.da1, 2 * D, p.a1));
+  TRY(lin_dw(st, p.g1, 2 * D, 2 * D, p.dh_bf, d, d, T, c.g(o.seq_w2)));
+  colsum_bf16(p.dh_bf, (int)T, d, d, c.g(o.seq_b2), st);
+  TRY(lin_dx(st, p.da1, 2 * D, T, p.pk.seq_w1, 2 * D, d, 2 * D, p.dx0, d, p.dx0_bf, d, nullptr, p.real));
+  TRY(lin_dw(st, p.x0, d, d, p.da1, 2 * D, 2 * D, T, c.g(o.seq_w1)));
+  colsum_bf16(p.da1, (int)T, 2 * D, 2 * D, c.g(o.seq_b1), st);
+  TRY(lin_dw(st, p.feat, p.FP, p.F, p.dx0_bf, d, d, T, c.g(o.tok_w)));
+  colsum_f32(p.dx0, (int)T, d, d, c.g(o.tok_b), st);
+  EmbedBwdArgs eb{};
+  eb.items = bt.items; eb.actions = bt.actions; eb.dt = bt.dt; eb.n_events = bt.n_events;
+  eb.B = p.B; eb.L = p.L; eb.Lp = p.Lp; eb.d = d; eb.d_item = dm.d_item; eb.d_act = dm.d_act; eb.d_time = dm.d_time;
+  eb.nb = dm.n_time_buckets; eb.vocab = dm.vocab; eb.n_actions = dm.n_actions;
+  eb.tok_w = c.w(o.tok_w); eb.dx0 = p.dx0;
+  eb.g_item = c.g(o.item); eb.g_act = c.g(o.act); eb.g_time = c.g(o.time); eb.g_pos = c.g(o.pos);
+  embed_bwd(eb, st);
+  TRY((int)cudaGetLastError());
+  return 0;
+}
+
+int check_call(const LongerDims* dims, size_t ws_bytes, Plan* out, void* ws) {
+  if (!dims) return fail(LONGER_EDIM, "null dims");
+  int rc = validate(*dims);
+  if (rc) return rc;
+  *out = make_plan(*dims, ws);
+  if (ws_bytes < out->bytes) return fail(LONGER_EDIM, "workspace too small");
+  if (reinterpret_cast<uintptr_t>(ws) & 255) return fail(LONGER_EDIM, "workspace must be 256-byte aligned");
+  return 0;
+}
+
+}  // namespace
+}  // namespace longer
+
+using namespace longer;
+
+extern "C" int longer_param_count(const LongerDims* dims, int64_t* count) {
+  if (!dims || !count) return fail(LONGER_EDIM, "null argument");
+  int rc = validate(*dims);
+  if (rc) return rc;
+  *count = param_offsets(*dims).total;
+  return 0;
+}
+
+extern "C" int longer_workspace_bytes(const LongerDims* dims, size_t* bytes) {
+  if (!dims || !bytes) return fail(LONGER_EDIM, "null argument");
+  int rc = validate(*dims);
+  if (rc) return rc;
+  *bytes = make_plan(*dims, nullptr).bytes;
+  return 0;
+}
+
+extern "C" int longer_forward(const LongerDims* dims, const float* params, const LongerBatch* batch, void* ws,
+                              size_t ws_bytes, float* probs, void* stream) {
+  static Plan p;   // large struct; one driving thread per device (see longer.h)
+  int rc = check_call(dims, ws_bytes, &p, ws);
+  if (rc) return rc;
+  Ctx c{p, params, nullptr, (cudaStream_t)stream};
+  return forward(c, p, *batch, probs, nullptr, 0);
+}
+
+extern "C" int longer_forward_backward(const LongerDims* dims, const float* params, const LongerBatch* batch,
+                                       void* ws, size_t ws_bytes, float* probs, float* loss, float* grads,
+                                       void* stream) {
+  static Plan p;
+  int rc = check_call(dims, ws_bytes, &p, ws);
+  if (rc) return rc;
+  Ctx c{p, params, grads, (cudaStream_t)stream};
+  rc = forward(c, p, *batch, probs, loss, 1);
+  if (rc) return rc;
+  return backward(c, p, *batch, probs);
+}
+
+extern "C" int longer_adam_step(float* params, const float* grads, float* m, float* v, int64_t count, float lr,
+                                int32_t t, void* stream) {
+  if (t < 1) return fail(LONGER_ECONFIG, "Adam step counter must be >= 1");
+  adam_step(params, grads, m, v, count, lr, t, (cudaStream_t)stream);
+  int e = (int)cudaGetLastError();
+  return e ? fail(LONGER_ECUDA, cudaGetErrorString((cudaError_t)e)) : 0;
+}
+
+extern "C" int longer_read_status(void* ws, int32_t* flags, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  int e = (int)cudaMemcpyAsync(flags, ws, 4, cudaMemcpyDeviceToHost, st);
+  if (!e) e = (int)cudaStreamSynchronize(st);
+  if (!e) e = (int)cudaMemsetAsync(ws, 0, 4, st);
+  return e ? fail(LONGER_ECUDA, cudaGetErrorString((cudaError_t)e)) : 0;
+}
+
+extern "C" const char* longer_last_error(void) { return g_err.c_str(); }

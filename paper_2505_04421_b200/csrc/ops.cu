@@ -1,0 +1,907 @@
+// ops.cu — SIMT kernels of the LONGER step that are not dense GEMMs: token featurisation,
+// layer norms, bias/column reductions, grouped + hybrid attention, global tokens, head + BCE,
+// parameter packing and Adam.  Each kernel cites the reference function it restates.
+#include "ops.cuh"
+
+#include <math.h>
+#include <algorithm>
+
+namespace longer {
+
+namespace {
+inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+}
+
+// ============================================================== front-end: featurisation
+// _event_features + abs-pos add (pkg/src/longrec/inputs.py:434-444, :474-476) and the pad
+// bookkeeping of encode_events / merge (inputs.py:457-482, merge.py:45-62). One thread/token.
+__global__ void embed_fwd_kernel(EmbedArgs a) {
+  extern __shared__ float sw[];                    // tok_w [F*d] + tok_b [d]
+  const int F = a.d_item + a.d_act + a.d_time;
+  for (int i = threadIdx.x; i < F * a.d + a.d; i += blockDim.x)
+    sw[i] = i < F * a.d ? a.tok_w[i] : a.tok_b[i - F * a.d];
+  __syncthreads();
+  const long long T = (long long)a.B * a.Lp;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const int b = (int)(t / a.Lp), j = (int)(t % a.Lp);
+  const int n = min(max(a.n_events[b], 0), a.L);
+  const bool real = j >= a.Lp - n;
+  const int npg = (a.Lp - n) / a.K;
+  a.real[t] = real ? 1.f : 0.f;
+  a.keep[t] = (j / a.K) >= npg ? 1.f : 0.f;
+  if (j == 0) a.npg[b] = npg;
+  bf16* fo = a.feat + t * a.FP;
+  bf16* xo = a.x0 + t * a.d;
+  if (!real) {
+    for (int f = 0; f < a.FP; ++f) fo[f] = __float2bfloat16(0.f);
+    for (int c = 0; c < a.d; ++c) xo[c] = __float2bfloat16(0.f);
+    return;
+  }
+  const long long src = (long long)b * a.L + (j - (a.Lp - a.L));
+  int item = a.items[src], act = a.actions[src], dt = a.dt[src];
+  int bad = 0;
+  if (item < 0 || item >= a.vocab) { bad |= 1; item = 0; }
+  if (act < 0 || act >= a.n_actions) { bad |= 1; act = 0; }
+  if (dt < 0) { bad |= 2; dt = 0; }
+  if (bad) atomicOr(a.status, bad);
+  const int bucket = min(32 - __clz(dt), a.nb - 1);          // time_bucket (inputs.py:307-315)
+  const int rec = a.Lp - 1 - j;                              // recency, 0 = most recent
+  float feat[64];
+  int f = 0;
+  for (int c = 0; c < a.d_item; ++c) feat[f++] = a.item_tab[item * a.d_item + c];
+  for (int c = 0; c < a.d_act; ++c) feat[f++] = a.act_tab[act * a.d_act + c];
+  for (int c = 0; c < a.d_time; ++c) feat[f++] = a.time_tab[bucket * a.d_time + c];
+  for (int c = 0; c < a.FP; ++c) fo[c] = __float2bfloat16(c < F ? feat[c] : 0.f);
+  const float* pos = a.pos_tab + (long long)rec * a.d;
+  for (int c = 0; c < a.d; ++c) {
+    float acc = sw[F * a.d + c] + pos[c];
+    for (int i = 0; i < F; ++i) acc = fmaf(feat[i], sw[i * a.d + c], acc);
+    xo[c] = __float2bfloat16(acc);
+  }
+}
+
+void embed_fwd(const EmbedArgs& a, cudaStream_t st) {
+  const long long T = (long long)a.B * a.Lp;
+  const int F = a.d_item + a.d_act + a.d_time;
+  const int smem = (F * a.d + a.d) * 4;
+  embed_fwd_kernel<<<cdiv(T, 256), 256, smem, st>>>(a);
+}
+
+// Backward of the featuriser: dfeat = dx0·W_tpᵀ scattered into the item/action/time tables with
+// shared-memory privatised accumulators (gather_rows bw = np.add.at, tensors.py:505-510).
+__global__ void embed_bwd_kernel(EmbedBwdArgs a, int tokens_per_block, int item_in_smem) {
+  extern __shared__ float sm[];
+  const int F = a.d_item + a.d_act + a.d_time;
+  float* s_w = sm;                                   // F*d
+  float* s_time = s_w + F * a.d;                     // nb*d_time
+  float* s_act = s_time + a.nb * a.d_time;           // n_actions*d_act
+  float* s_item = s_act + a.n_actions * a.d_act;     // vocab*d_item (optional)
+  const int n_item = item_in_smem ? a.vocab * a.d_item : 0;
+  const int tot = F * a.d + a.nb * a.d_time + a.n_actions * a.d_act + n_item;
+  for (int i = threadIdx.x; i < tot; i += blockDim.x) sm[i] = i < F * a.d ? a.tok_w[i] : 0.f;
+  __syncthreads();
+  const long long T = (long long)a.B * a.Lp;
+  const long long t0 = (long long)blockIdx.x * tokens_per_block;
+  for (long long t = t0 + threadIdx.x; t < min(T, t0 + tokens_per_block); t += blockDim.x) {
+    const int b = (int)(t / a.Lp), j = (int)(t % a.Lp);
+    const int n = min(max(a.n_events[b], 0), a.L);
+    if (j < a.Lp - n) continue;
+    const long long src = (long long)b * a.L + (j - (a.Lp - a.L));
+    int item = a.items[src], act = a.actions[src], dt = a.dt[src];
+    if (item < 0 || item >= a.vocab) item = 0;
+    if (act < 0 || act >= a.n_actions) act = 0;
+    if (dt < 0) dt = 0;
+    const int bucket = min(32 - __clz(dt), a.nb - 1);
+    float dx[64];
+    for (int c = 0; c < a.d; ++c) dx[c] = a.dx0[t * a.d + c];
+    for (int fi = 0; fi < F; ++fi) {
+      float g = 0.f;
+      for (int c = 0; c < a.d; ++c) g = fmaf(dx[c], s_w[fi * a.d + c], g);
+      if (fi < a.d_item) {
+        if (item_in_smem) atomicAdd(&s_item[item * a.d_item + fi], g);
+        else atomicAdd(&a.g_item[item * a.d_item + fi], g);
+      } else if (fi < a.d_item + a.d_act) {
+        atomicAdd(&s_act[act * a.d_act + fi - a.d_item], g);
+      } else {
+        atomicAdd(&s_time[bucket * a.d_time + fi - a.d_item - a.d_act], g);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < a.nb * a.d_time; i += blockDim.x)
+    if (s_time[i] != 0.f) atomicAdd(&a.g_time[i], s_time[i]);
+  for (int i = threadIdx.x; i < a.n_actions * a.d_act; i += blockDim.x)
+    if (s_act[i] != 0.f) atomicAdd(&a.g_act[i], s_act[i]);
+  for (int i = threadIdx.x; i < n_item; i += blockDim.x)
+    if (s_item[i] != 0.f) atomicAdd(&a.g_item[i], s_item[i]);
+}
+
+// abs_pos_table gradient: row r collects dx0 of the token with recency r of every sample —
+// a deterministic strided column reduction instead of scatter atomics.
+__global__ void pos_grad_kernel(EmbedBwdArgs a) {
+  const int r = blockIdx.x;                     // recency row
+  for (int c = threadIdx.x; c < a.d; c += blockDim.x) {
+    float acc = 0.f;
+    for (int b = 0; b < a.B; ++b) {
+      const int n = min(max(a.n_events[b], 0), a.L);
+      if (r < n) acc += a.dx0[((long long)b * a.Lp + (a.Lp - 1 - r)) * a.d + c];
+    }
+    a.g_pos[(long long)r * a.d + c] += acc;
+  }
+}
+
+void embed_bwd(const EmbedBwdArgs& a, cudaStream_t st) {
+  const long long T = (long long)a.B * a.Lp;
+  const int F = a.d_item + a.d_act + a.d_time;
+  int item_in_smem = (a.vocab * a.d_item <= 12288) ? 1 : 0;
+  const int smem = 4 * (F * a.d + a.nb * a.d_time + a.n_actions * a.d_act + (item_in_smem ? a.vocab * a.d_item : 0));
+  const int tpb = 4096;
+  static int attr_done = 0;
+  if (!attr_done) { cudaFuncSetAttribute(embed_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024); attr_done = 1; }
+  embed_bwd_kernel<<<cdiv(T, tpb), 256, smem, st>>>(a, tpb, item_in_smem);
+  pos_grad_kernel<<<a.L, 32 * cdiv(a.d, 32), 0, st>>>(a);
+}
+
+// ============================================================== layer norm
+template <int VPT>
+__global__ void ln_fwd_kernel(RowMap x, int W, const float* __restrict__ g, const float* __restrict__ bta,
+                              bf16* y, float* mean, float* rstd) {
+  const int warps = blockDim.x / 32;
+  const int row = blockIdx.x * warps + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= x.rows()) return;
+  const int per = x.na + x.nb;
+  const int b = row / per, j = row % per;
+  const float* src = j < x.na ? x.A + (long long)(b * x.a_rows + x.a_off + j) * x.lda
+                              : x.Bsrc + (long long)(b * x.nb + j - x.na) * x.ldb;
+  float v[VPT];
+  float s = 0.f;
+#pragma unroll
+  for (int u = 0; u < VPT; ++u) {
+    const int c = lane + 32 * u;
+    v[u] = c < W ? src[c] : 0.f;
+    s += v[u];
+  }
+  const float mu = warp_sum(s) / W;
+  float q = 0.f;
+#pragma unroll
+  for (int u = 0; u < VPT; ++u) {
+    const int c = lane + 32 * u;
+    const float dv = c < W ? v[u] - mu : 0.f;
+    q += dv * dv;
+  }
+  const float var = warp_sum(q) / W;
+  const float inv = rsqrtf(var + kLnEps);
+#pragma unroll
+  for (int u = 0; u < VPT; ++u) {
+    const int c = lane + 32 * u;
+    if (c < W) y[(long long)row * W + c] = __float2bfloat16((v[u] - mu) * inv * g[c] + bta[c]);
+  }
+  if (lane == 0) { mean[row] = mu; rstd[row] = inv; }
+}
+
+void layernorm_fwd(const RowMap& x, int W, const float* g, const float* b, bf16* y, float* mean, float* rstd,
+                   cudaStream_t st) {
+  const int rows = x.rows();
+  const int grid = cdiv(rows, 8);
+  if (W <= 32) ln_fwd_kernel<1><<<grid, 256, 0, st>>>(x, W, g, b, y, mean, rstd);
+  else if (W <= 64) ln_fwd_kernel<2><<<grid, 256, 0, st>>>(x, W, g, b, y, mean, rstd);
+  else if (W <= 128) ln_fwd_kernel<4><<<grid, 256, 0, st>>>(x, W, g, b, y, mean, rstd);
+  else ln_fwd_kernel<8><<<grid, 256, 0, st>>>(x, W, g, b, y, mean, rstd);
+}
+
+// LN backward (pkg/src/longrec/tensors.py:368-378): dx = (ĝ − mean ĝ − x̂·mean(ĝx̂))·σ⁻¹, ĝ = dy·g
+template <int VPT>
+__global__ void ln_bwd_kernel(RowMap x, int W, const float* __restrict__ g, const float* __restrict__ mean,
+                              const float* __restrict__ rstd, const float* __restrict__ dy, int ldy, RowMapW out,
+                              int accumulate, const float* rowmask, float* dgain, float* dbias) {
+  __shared__ float sg[8][VPT * 32], sb[8][VPT * 32];
+  const int warps = blockDim.x / 32;
+  const int wid = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int rows = x.rows();
+  const int per = x.na + x.nb;
+  float pg[VPT], pb[VPT];
+#pragma unroll
+  for (int u = 0; u < VPT; ++u) { pg[u] = 0.f; pb[u] = 0.f; }
+  for (int row = blockIdx.x * warps + wid; row < rows; row += gridDim.x * warps) {
+    const int b = row / per, j = row % per;
+    const float* src = j < x.na ? x.A + (long long)(b * x.a_rows + x.a_off + j) * x.lda
+                                : x.Bsrc + (long long)(b * x.nb + j - x.na) * x.ldb;
+    float* dst = j < out.na ? out.A + (long long)(b * out.a_rows + out.a_off + j) * out.lda
+                            : out.Bsrc + (long long)(b * out.nb + j - out.na) * out.ldb;
+    const float mu = mean[row], inv = rstd[row];
+    float xh[VPT], gh[VPT];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) {
+      const int c = lane + 32 * u;
+      if (c < W) {
+        const float dyv = dy[(long long)row * ldy + c];
+        xh[u] = (src[c] - mu) * inv;
+        gh[u] = dyv * g[c];
+        pg[u] += dyv * xh[u];
+        pb[u] += dyv;
+      } else {
+        xh[u] = 0.f; gh[u] = 0.f;
+      }
+      s1 += gh[u];
+      s2 += gh[u] * xh[u];
+    }
+    const float m1 = warp_sum(s1) / W, m2 = warp_sum(s2) / W;
+    const float rm = rowmask ? rowmask[row] : 1.f;
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) {
+      const int c = lane + 32 * u;
+      if (c < W) {
+        float v = (gh[u] - m1 - xh[u] * m2) * inv;
+        if (accumulate) v += dst[c];
+        dst[c] = v * rm;
+      }
+    }
+  }
+  if (dgain) {
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) { sg[wid][lane + 32 * u] = pg[u]; sb[wid][lane + 32 * u] = pb[u]; }
+    __syncthreads();
+    for (int c = threadIdx.x; c < W; c += blockDim.x) {
+      float a = 0.f, bb = 0.f;
+      for (int w = 0; w < warps; ++w) { a += sg[w][c]; bb += sb[w][c]; }
+      atomicAdd(&dgain[c], a);
+      atomicAdd(&dbias[c], bb);
+    }
+  }
+}
+
+void layernorm_bwd(const RowMap& x, int W, const float* g, const float* mean, const float* rstd, const float* dy,
+                   int ldy, const RowMapW& out, int accumulate, const float* rowmask, float* dgain, float* dbias,
+                   cudaStream_t st) {
+  const int rows = x.rows();
+  const int grid = std::min(cdiv(rows, 8), 148 * 8);
+  if (W <= 32) ln_bwd_kernel<1><<<grid, 256, 0, st>>>(x, W, g, mean, rstd, dy, ldy, out, accumulate, rowmask, dgain, dbias);
+  else if (W <= 64) ln_bwd_kernel<2><<<grid, 256, 0, st>>>(x, W, g, mean, rstd, dy, ldy, out, accumulate, rowmask, dgain, dbias);
+  else if (W <= 128) ln_bwd_kernel<4><<<grid, 256, 0, st>>>(x, W, g, mean, rstd, dy, ldy, out, accumulate, rowmask, dgain, dbias);
+  else ln_bwd_kernel<8><<<grid, 256, 0, st>>>(x, W, g, mean, rstd, dy, ldy, out, accumulate, rowmask, dgain, dbias);
+}
+
+// ============================================================== reductions / copies
+template <typename T>
+__global__ void colsum_kernel(const T* __restrict__ x, int rows, int W, int ld, int rows_per_block, float* out) {
+  __shared__ float red[256];
+  const int cpp = W < 256 ? W : 256;
+  const int rpp = 256 / cpp;
+  const int tid = threadIdx.x;
+  const int r0 = blockIdx.x * rows_per_block;
+  const int r1 = min(rows, r0 + rows_per_block);
+  for (int c0 = 0; c0 < W; c0 += cpp) {
+    float acc = 0.f;
+    const int c = c0 + tid % cpp;
+    if (tid < cpp * rpp && c < W)
+      for (int r = r0 + tid / cpp; r < r1; r += rpp) acc += ldf(x + (long long)r * ld + c);
+    red[tid] = acc;
+    __syncthreads();
+    if (tid < cpp && c0 + tid < W) {
+      float s = 0.f;
+      for (int q = 0; q < rpp; ++q) s += red[q * cpp + tid];
+      atomicAdd(&out[c0 + tid], s);
+    }
+    __syncthreads();
+  }
+}
+
+void colsum_f32(const float* x, int rows, int W, int ld, float* out, cudaStream_t st) {
+  const int rpb = std::max(64, cdiv(rows, 148 * 4));
+  colsum_kernel<float><<<cdiv(rows, rpb), 256, 0, st>>>(x, rows, W, ld, rpb, out);
+}
+void colsum_bf16(const bf16* x, int rows, int W, int ld, float* out, cudaStream_t st) {
+  const int rpb = std::max(64, cdiv(rows, 148 * 4));
+  colsum_kernel<bf16><<<cdiv(rows, rpb), 256, 0, st>>>(x, rows, W, ld, rpb, out);
+}
+
+__global__ void cast_rows_kernel(const float* x, int rows, int W, int ldx, bf16* y, int ldy, const float* rowmask) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)rows * W) return;
+  const int r = (int)(i / W), c = (int)(i % W);
+  float v = x[(long long)r * ldx + c];
+  if (rowmask) v *= rowmask[r];
+  y[(long long)r * ldy + c] = __float2bfloat16(v);
+}
+void cast_rows_bf16(const float* x, int rows, int W, int ldx, bf16* y, int ldy, const float* rowmask, cudaStream_t st) {
+  const long long n = (long long)rows * W;
+  if (n) cast_rows_kernel<<<cdiv(n, 256), 256, 0, st>>>(x, rows, W, ldx, y, ldy, rowmask);
+}
+
+__global__ void mul_rows_kernel(float* x, int rows, int W, const float* rowmask) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)rows * W) return;
+  x[i] *= rowmask[i / W];
+}
+void mul_rows_inplace(float* x, int rows, int W, const float* rowmask, cudaStream_t st) {
+  const long long n = (long long)rows * W;
+  if (n) mul_rows_kernel<<<cdiv(n, 256), 256, 0, st>>>(x, rows, W, rowmask);
+}
+
+template <int ADD>
+__global__ void move_rows_kernel(const float* src, int batch, int src_rows, int src_off, int n, float* dst,
+                                 int dst_rows, int dst_off, int W) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)batch * n * W) return;
+  const int c = (int)(i % W);
+  const long long r = i / W;
+  const int b = (int)(r / n), j = (int)(r % n);
+  const float v = src[((long long)b * src_rows + src_off + j) * W + c];
+  float* d = dst + ((long long)b * dst_rows + dst_off + j) * W + c;
+  if (ADD) *d += v; else *d = v;
+}
+void gather_rows_f32(const float* src, int batch, int src_rows, int src_off, int n, float* dst, int dst_rows,
+                     int dst_off, int W, cudaStream_t st) {
+  const long long tot = (long long)batch * n * W;
+  if (tot) move_rows_kernel<0><<<cdiv(tot, 256), 256, 0, st>>>(src, batch, src_rows, src_off, n, dst, dst_rows, dst_off, W);
+}
+void add_rows_f32(const float* src, int batch, int src_rows, int src_off, int n, float* dst, int dst_rows,
+                  int dst_off, int W, cudaStream_t st) {
+  const long long tot = (long long)batch * n * W;
+  if (tot) move_rows_kernel<1><<<cdiv(tot, 256), 256, 0, st>>>(src, batch, src_rows, src_off, n, dst, dst_rows, dst_off, W);
+}
+
+// ============================================================== grouped attention (InnerTrans)
+// grouped_attention (pkg/src/longrec/tensors.py:406-444): softmax(q kᵀ/√w) v inside each group of
+// K consecutive rows.  One thread per row; qkv = [q | k | v] fp32 [T, 3w].
+__global__ void group_attn_fwd_kernel(const float* __restrict__ qkv, int T, int K, int w, bf16* ctx, float* probs) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const long long g0 = t - t % K;
+  const float scale = rsqrtf((float)w);
+  const float* q = qkv + t * 3 * w;
+  float s[16];
+  float mx = -INFINITY;
+  for (int j = 0; j < K; ++j) {
+    const float* kr = qkv + (g0 + j) * 3 * w + w;
+    float acc = 0.f;
+    for (int c = 0; c < w; ++c) acc = fmaf(q[c], kr[c], acc);
+    s[j] = acc * scale;
+    mx = fmaxf(mx, s[j]);
+  }
+  float tot = 0.f;
+  for (int j = 0; j < K; ++j) { s[j] = __expf(s[j] - mx); tot += s[j]; }
+  const float inv = 1.f / tot;
+  for (int j = 0; j < K; ++j) { s[j] *= inv; probs[t * K + j] = s[j]; }
+  for (int c = 0; c < w; ++c) {
+    float acc = 0.f;
+    for (int j = 0; j < K; ++j) acc = fmaf(s[j], qkv[(g0 + j) * 3 * w + 2 * w + c], acc);
+    ctx[t * w + c] = __float2bfloat16(acc);
+  }
+}
+
+__global__ void group_attn_bwd_kernel(const float* __restrict__ qkv, const float* __restrict__ probs,
+                                      const float* __restrict__ dctx, int T, int K, int w, bf16* dqkv) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const long long g0 = t - t % K;
+  const int me = (int)(t - g0);
+  const float scale = rsqrtf((float)w);
+  // dP[i][j] = dctx[i]·v[j];  dS = P ∘ (dP − rowsum(dP∘P)) · scale
+  float dS[16][16];
+  for (int i = 0; i < K; ++i) {
+    float dp[16];
+    float dot = 0.f;
+    for (int j = 0; j < K; ++j) {
+      float acc = 0.f;
+      const float* dr = dctx + (g0 + i) * w;
+      const float* vr = qkv + (g0 + j) * 3 * w + 2 * w;
+      for (int c = 0; c < w; ++c) acc = fmaf(dr[c], vr[c], acc);
+      dp[j] = acc;
+      dot += acc * probs[(g0 + i) * K + j];
+    }
+    for (int j = 0; j < K; ++j) dS[i][j] = probs[(g0 + i) * K + j] * (dp[j] - dot) * scale;
+  }
+  for (int c = 0; c < w; ++c) {
+    float dq = 0.f, dk = 0.f, dv = 0.f;
+    for (int j = 0; j < K; ++j) dq = fmaf(dS[me][j], qkv[(g0 + j) * 3 * w + w + c], dq);
+    for (int i = 0; i < K; ++i) {
+      dk = fmaf(dS[i][me], qkv[(g0 + i) * 3 * w + c], dk);
+      dv = fmaf(probs[(g0 + i) * K + me], dctx[(g0 + i) * w + c], dv);
+    }
+    dqkv[t * 3 * w + c] = __float2bfloat16(dq);
+    dqkv[t * 3 * w + w + c] = __float2bfloat16(dk);
+    dqkv[t * 3 * w + 2 * w + c] = __float2bfloat16(dv);
+  }
+}
+
+void group_attn_fwd(const float* qkv, int T, int K, int w, bf16* ctx, float* probs, cudaStream_t st) {
+  group_attn_fwd_kernel<<<cdiv(T, 128), 128, 0, st>>>(qkv, T, K, w, ctx, probs);
+}
+void group_attn_bwd(const float* qkv, const float* probs, const float* dctx, int T, int K, int w, bf16* dqkv,
+                    cudaStream_t st) {
+  group_attn_bwd_kernel<<<cdiv(T, 128), 128, 0, st>>>(qkv, probs, dctx, T, K, w, dqkv);
+}
+
+// ============================================================== hybrid attention
+// _multi_head_attention + masked_softmax (pkg/src/longrec/attention.py:153-169,
+// tensors.py:323-351) for one (sample, head) per CTA: Q staged in smem, K/V streamed in chunks,
+// one warp per query row with an fp32 online softmax.  Fully-masked rows give ctx = 0.
+constexpr int kAttnChunk = 64;
+
+__global__ void attn_fwd_kernel(AttnArgs a) {
+  extern __shared__ float sm[];
+  const int b = blockIdx.x / a.heads, h = blockIdx.x % a.heads;
+  const int dh = a.D / a.heads;
+  const int ldp = dh + 1;                                  // padded rows: conflict-free
+  float* sQ = sm;                                          // nq * ldp
+  float* sK = sQ + a.nq * ldp;                             // chunk * ldp
+  float* sV = sK + kAttnChunk * ldp;
+  const int wid = threadIdx.x / 32, lane = threadIdx.x & 31, nw = blockDim.x / 32;
+  const float scale = rsqrtf((float)dh);
+  const VisRule vis{a.k, a.G, a.ns, a.goff, a.npg[b]};
+  const bf16* Q = a.Q + b * a.sq + h * dh;
+  const bf16* Kg = a.Kp + b * a.sk + h * dh;
+  const bf16* Vg = a.V + b * a.sv + h * dh;
+  for (int i = threadIdx.x; i < a.nq * dh; i += blockDim.x)
+    sQ[(i / dh) * ldp + i % dh] = __bfloat162float(Q[(long long)(i / dh) * a.ldq + i % dh]) * scale;
+  constexpr int MAXD = 8;                                  // dh <= 256
+  const int nd = (dh + 31) / 32;
+  const int myq = (a.nq + nw - 1) / nw;                    // queries per warp (<= 8)
+  float m_[8], l_[8], acc[8][MAXD];
+  for (int r = 0; r < 8; ++r) {
+    m_[r] = -INFINITY; l_[r] = 0.f;
+    for (int u = 0; u < MAXD; ++u) acc[r][u] = 0.f;
+  }
+  for (int c0 = 0; c0 < a.nk; c0 += kAttnChunk) {
+    const int cn = min(kAttnChunk, a.nk - c0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < cn * dh; i += blockDim.x) {
+      const int r = i / dh, c = i % dh;
+      sK[r * ldp + c] = __bfloat162float(Kg[(long long)(c0 + r) * a.ldk + c]);
+      sV[r * ldp + c] = __bfloat162float(Vg[(long long)(c0 + r) * a.ldv + c]);
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int r = 0; r < myq && r < 8; ++r) {
+      const int i = wid + r * nw;
+      if (i >= a.nq) break;
+      float s[2];
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int j = lane + 32 * hh;
+        float v = -INFINITY;
+        if (j < cn && vis(i, c0 + j)) {
+          float dot = 0.f;
+          for (int c = 0; c < dh; ++c) dot = fmaf(sQ[i * ldp + c], sK[j * ldp + c], dot);
+          v = dot;
+        }
+        s[hh] = v;
+      }
+      const float cmax = warp_max(fmaxf(s[0], s[1]));
+      if (cmax == -INFINITY) continue;                      // nothing visible in this chunk
+      const float mnew = fmaxf(m_[r], cmax);
+      const float corr = __expf(m_[r] - mnew);
+      const float p0 = __expf(s[0] - mnew), p1 = __expf(s[1] - mnew);
+      l_[r] = l_[r] * corr + warp_sum(p0 + p1);
+      m_[r] = mnew;
+      for (int u = 0; u < nd; ++u) acc[r][u] *= corr;
+      for (int j = 0; j < cn; ++j) {
+        const float pj = __shfl_sync(0xffffffffu, j < 32 ? p0 : p1, j & 31);
+        if (pj == 0.f) continue;
+        for (int u = 0; u < nd; ++u) {
+          const int c = lane + 32 * u;
+          if (c < dh) acc[r][u] = fmaf(pj, sV[j * ldp + c], acc[r][u]);
+        }
+      }
+    }
+  }
+  for (int r = 0; r < myq && r < 8; ++r) {
+    const int i = wid + r * nw;
+    if (i >= a.nq) break;
+    const float inv = l_[r] > 0.f ? 1.f / l_[r] : 0.f;
+    bf16* o = a.ctx + b * a.sc + (long long)i * a.ldc + h * dh;
+    for (int u = 0; u < nd; ++u) {
+      const int c = lane + 32 * u;
+      if (c < dh) o[c] = __float2bfloat16(acc[r][u] * inv);
+    }
+    if (lane == 0) a.lse[((long long)b * a.heads + h) * a.nq + i] = l_[r] > 0.f ? m_[r] + __logf(l_[r]) : -INFINITY;
+  }
+}
+
+void attn_fwd(const AttnArgs& a, cudaStream_t st) {
+  const int dh = a.D / a.heads;
+  const int smem = 4 * (a.nq + 2 * kAttnChunk) * (dh + 1);
+  static int done = 0;
+  if (!done) { cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); done = 1; }
+  const int threads = std::min(1024, 32 * std::max(4, (a.nq + 7) / 8));
+  attn_fwd_kernel<<<a.B * a.heads, threads, smem, st>>>(a);
+}
+
+// Backward (masked_softmax bw p⊙(g−Σg⊙p), tensors.py:346-349; matmul bws, tensors.py:219-244).
+// P is recomputed from the saved log-sum-exp; dQ accumulates in smem across key chunks.
+__global__ void attn_bwd_kernel(AttnArgs a) {
+  extern __shared__ float sm[];
+  const int b = blockIdx.x / a.heads, h = blockIdx.x % a.heads;
+  const int dh = a.D / a.heads;
+  const int ldp = dh + 1;
+  const int nq = a.nq;
+  float* sQ = sm;                          // nq*ldp (pre-scaled)
+  float* sdO = sQ + nq * ldp;              // nq*ldp
+  float* sdQ = sdO + nq * ldp;             // nq*ldp
+  float* sK = sdQ + nq * ldp;              // C*ldp
+  float* sV = sK + kAttnChunk * ldp;       // C*ldp
+  float* sP = sV + kAttnChunk * ldp;       // nq*C
+  float* sdS = sP + nq * kAttnChunk;       // nq*C
+  float* sDi = sdS + nq * kAttnChunk;      // nq
+  float* sL = sDi + nq;                    // nq
+  const float scale = rsqrtf((float)dh);
+  const VisRule vis{a.k, a.G, a.ns, a.goff, a.npg[b]};
+  const bf16* Q = a.Q + b * a.sq + h * dh;
+  const bf16* Kg = a.Kp + b * a.sk + h * dh;
+  const bf16* Vg = a.V + b * a.sv + h * dh;
+  const float* dO = a.dctx + b * a.sdc + h * dh;
+  const bf16* O = a.ctx_in + b * a.sc + h * dh;
+  for (int i = threadIdx.x; i < nq * dh; i += blockDim.x) {
+    const int r = i / dh, c = i % dh;
+    sQ[r * ldp + c] = __bfloat162float(Q[(long long)r * a.ldq + c]) * scale;
+    sdO[r * ldp + c] = dO[(long long)r * a.lddc + c];
+    sdQ[r * ldp + c] = 0.f;
+  }
+  __syncthreads();
+  const int wid = threadIdx.x / 32, lane = threadIdx.x & 31, nw = blockDim.x / 32;
+  for (int i = wid; i < nq; i += nw) {                      // D_i = rowsum(dO ∘ O)
+    float s = 0.f;
+    for (int c = lane; c < dh; c += 32) s += sdO[i * ldp + c] * __bfloat162float(O[(long long)i * a.ldc + c]);
+    s = warp_sum(s);
+    if (lane == 0) { sDi[i] = s; sL[i] = a.lse[((long long)b * a.heads + h) * nq + i]; }
+  }
+  for (int c0 = 0; c0 < a.nk; c0 += kAttnChunk) {
+    const int cn = min(kAttnChunk, a.nk - c0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < cn * dh; i += blockDim.x) {
+      const int r = i / dh, c = i % dh;
+      sK[r * ldp + c] = __bfloat162float(Kg[(long long)(c0 + r) * a.ldk + c]);
+      sV[r * ldp + c] = __bfloat162float(Vg[(long long)(c0 + r) * a.ldv + c]);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nq * kAttnChunk; e += blockDim.x) {
+      const int i = e / kAttnChunk, j = e % kAttnChunk;
+      float p = 0.f, ds = 0.f;
+      if (j < cn && sL[i] != -INFINITY && vis(i, c0 + j)) {
+        float s = 0.f, dp = 0.f;
+        for (int c = 0; c < dh; ++c) {
+          s = fmaf(sQ[i * ldp + c], sK[j * ldp + c], s);
+          dp = fmaf(sdO[i * ldp + c], sV[j * ldp + c], dp);
+        }
+        p = __expf(s - sL[i]);
+        ds = p * (dp - sDi[i]);
+      }
+      sP[i * kAttnChunk + j] = p;
+      sdS[i * kAttnChunk + j] = ds;
+    }
+    __syncthreads();
+    // dV[j] = Σ_i P[i,j] dO[i];  dK[j] = scale Σ_i dS[i,j] Q̃[i]/scale... (sQ is pre-scaled: Q̃ = scale·Q)
+    for (int e = threadIdx.x; e < cn * dh; e += blockDim.x) {
+      const int j = e / dh, c = e % dh;
+      float dv = 0.f, dk = 0.f;
+      for (int i = 0; i < nq; ++i) {
+        dv = fmaf(sP[i * kAttnChunk + j], sdO[i * ldp + c], dv);
+        dk = fmaf(sdS[i * kAttnChunk + j], sQ[i * ldp + c], dk);
+      }
+      a.dV[b * a.sdv + (long long)(c0 + j) * a.lddv + h * dh + c] = __float2bfloat16(dv);
+      a.dK[b * a.sdk + (long long)(c0 + j) * a.lddk + h * dh + c] = __float2bfloat16(dk);
+    }
+    for (int e = threadIdx.x; e < nq * dh; e += blockDim.x) {
+      const int i = e / dh, c = e % dh;
+      float dq = 0.f;
+      for (int j = 0; j < cn; ++j) dq = fmaf(sdS[i * kAttnChunk + j], sK[j * ldp + c], dq);
+      sdQ[i * ldp + c] += dq * scale;
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nq * dh; e += blockDim.x) {
+    const int i = e / dh, c = e % dh;
+    a.dQ[b * a.sdq + (long long)i * a.lddq + h * dh + c] = __float2bfloat16(sdQ[i * ldp + c]);
+  }
+}
+
+void attn_bwd(const AttnArgs& a, cudaStream_t st) {
+  const int dh = a.D / a.heads;
+  const int ldp = dh + 1;
+  const int smem = 4 * (3 * a.nq * ldp + 2 * kAttnChunk * ldp + 2 * a.nq * kAttnChunk + 2 * a.nq);
+  static int done = 0;
+  if (!done) { cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); done = 1; }
+  attn_bwd_kernel<<<a.B * a.heads, 256, smem, st>>>(a);
+}
+
+// ============================================================== global tokens
+// nontarget_global_tokens / target_global_token raw rows (pkg/src/longrec/inputs.py:500-537),
+// before the shared global MLP (which runs as tcgen05 GEMMs).  One CTA per sample.
+__global__ void globals_raw_fwd_kernel(GlobalsArgs a) {
+  __shared__ float s_u[64], s_tf[64], s_td[64];
+  const int b = blockIdx.x;
+  const int F = a.d_item + a.d_act + a.d_time;
+  int uid = a.uid[b], cand = a.cand_item[b];
+  for (int i = threadIdx.x; i < a.d; i += blockDim.x) s_u[i] = a.uid_tab[(long long)uid * a.d + i];
+  for (int f = threadIdx.x; f < F; f += blockDim.x) {
+    float v = 0.f;
+    if (f < a.d_item) v = a.item_tab[(long long)cand * a.d_item + f];
+    else if (f >= a.d_item + a.d_act) v = a.time_tab[f - a.d_item - a.d_act];   // time bucket 0
+    s_tf[f] = v;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < a.d; c += blockDim.x) {
+    float acc = a.tok_b[c];
+    for (int f = 0; f < F; ++f) acc = fmaf(s_tf[f], a.tok_w[f * a.d + c], acc);
+    s_td[c] = acc;
+    a.td[(long long)b * a.d + c] = acc;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < a.D; c += blockDim.x) {
+    float u = a.lift_b[c], t = a.lift_b[c];
+    for (int i = 0; i < a.d; ++i) {
+      u = fmaf(s_u[i], a.lift_w[i * a.D + c], u);
+      t = fmaf(s_td[i], a.lift_w[i * a.D + c], t);
+    }
+    const long long r0 = (long long)b * a.m;
+    a.raw[(r0) * a.D + c] = u;
+    a.raw[(r0 + a.m - 1) * a.D + c] = t;
+    a.raw_bf[(r0) * a.D + c] = __float2bfloat16(u);
+    a.raw_bf[(r0 + a.m - 1) * a.D + c] = __float2bfloat16(t);
+    for (int r = 1; r < a.m - 1; ++r) {
+      const float v = a.cls[(r - 1) * a.D + c];
+      a.raw[(r0 + r) * a.D + c] = v;
+      a.raw_bf[(r0 + r) * a.D + c] = __float2bfloat16(v);
+    }
+  }
+}
+
+void globals_raw_fwd(const GlobalsArgs& a, cudaStream_t st) {
+  globals_raw_fwd_kernel<<<a.B, 128, 0, st>>>(a);
+}
+
+// Backward of the raw global rows: lift / token-projection / cls / table gradients, accumulated
+// per CTA in shared memory over a slice of samples, then flushed with one atomic per entry.
+__global__ void globals_raw_bwd_kernel(GlobalsArgs a, int per_block) {
+  extern __shared__ float sm[];
+  const int F = a.d_item + a.d_act + a.d_time;
+  float* s_lw = sm;                       // d*D
+  float* s_lb = s_lw + a.d * a.D;         // D
+  float* s_cls = s_lb + a.D;              // (m-2)*D
+  float* s_tw = s_cls + (a.m - 2) * a.D;  // F*d
+  float* s_tb = s_tw + F * a.d;           // d
+  float* s_vec = s_tb + a.d;              // scratch: u[d], td[d], dtd[d], tf[F]
+  const int tot = a.d * a.D + a.D + (a.m - 2) * a.D + F * a.d + a.d;
+  for (int i = threadIdx.x; i < tot; i += blockDim.x) sm[i] = 0.f;
+  float* s_u = s_vec;
+  float* s_td = s_u + 64;
+  float* s_dtd = s_td + 64;
+  float* s_tf = s_dtd + 64;
+  __syncthreads();
+  const int b0 = blockIdx.x * per_block;
+  for (int b = b0; b < min(a.B, b0 + per_block); ++b) {
+    const int uid = a.uid[b], cand = a.cand_item[b];
+    const float* d0 = a.draw + (long long)b * a.m * a.D;
+    const float* dl = d0 + (long long)(a.m - 1) * a.D;
+    for (int i = threadIdx.x; i < a.d; i += blockDim.x) {
+      s_u[i] = a.uid_tab[(long long)uid * a.d + i];
+      s_td[i] = a.td[(long long)b * a.d + i];
+    }
+    for (int f = threadIdx.x; f < F; f += blockDim.x) {
+      float v = 0.f;
+      if (f < a.d_item) v = a.item_tab[(long long)cand * a.d_item + f];
+      else if (f >= a.d_item + a.d_act) v = a.time_tab[f - a.d_item - a.d_act];
+      s_tf[f] = v;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < a.d * a.D; e += blockDim.x) {
+      const int i = e / a.D, c = e % a.D;
+      s_lw[e] += s_u[i] * d0[c] + s_td[i] * dl[c];
+    }
+    for (int c = threadIdx.x; c < a.D; c += blockDim.x) {
+      s_lb[c] += d0[c] + dl[c];
+      for (int r = 1; r < a.m - 1; ++r) s_cls[(r - 1) * a.D + c] += d0[(long long)r * a.D + c];
+    }
+    // d uid_emb and d td (both through lift_w)
+    for (int i = threadIdx.x; i < 2 * a.d; i += blockDim.x) {
+      const int ii = i % a.d;
+      const float* src = i < a.d ? d0 : dl;
+      float acc = 0.f;
+      for (int c = 0; c < a.D; ++c) acc = fmaf(src[c], a.lift_w[ii * a.D + c], acc);
+      if (i < a.d) atomicAdd(&a.g_uid[(long long)uid * a.d + ii], acc);
+      else s_dtd[ii] = acc;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < F * a.d; e += blockDim.x) {
+      const int f = e / a.d, i = e % a.d;
+      s_tw[e] += s_tf[f] * s_dtd[i];
+    }
+    for (int i = threadIdx.x; i < a.d; i += blockDim.x) s_tb[i] += s_dtd[i];
+    for (int f = threadIdx.x; f < F; f += blockDim.x) {
+      if (f >= a.d_item && f < a.d_item + a.d_act) continue;     // zero action slot is a constant
+      float acc = 0.f;
+      for (int i = 0; i < a.d; ++i) acc = fmaf(s_dtd[i], a.tok_w[f * a.d + i], acc);
+      if (f < a.d_item) atomicAdd(&a.g_item[(long long)cand * a.d_item + f], acc);
+      else atomicAdd(&a.g_time[f - a.d_item - a.d_act], acc);
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < a.d * a.D; e += blockDim.x) atomicAdd(&a.g_lift_w[e], s_lw[e]);
+  for (int c = threadIdx.x; c < a.D; c += blockDim.x) atomicAdd(&a.g_lift_b[c], s_lb[c]);
+  for (int e = threadIdx.x; e < (a.m - 2) * a.D; e += blockDim.x) atomicAdd(&a.g_cls[e], s_cls[e]);
+  for (int e = threadIdx.x; e < F * a.d; e += blockDim.x) atomicAdd(&a.g_tok_w[e], s_tw[e]);
+  for (int i = threadIdx.x; i < a.d; i += blockDim.x) atomicAdd(&a.g_tok_b[i], s_tb[i]);
+}
+
+void globals_raw_bwd(const GlobalsArgs& a, cudaStream_t st) {
+  const int F = a.d_item + a.d_act + a.d_time;
+  const int smem = 4 * (a.d * a.D + a.D + (a.m - 2) * a.D + F * a.d + a.d + 3 * 64 + 64);
+  static int done = 0;
+  if (!done) { cudaFuncSetAttribute(globals_raw_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); done = 1; }
+  const int per = std::max(1, cdiv(a.B, 64));
+  globals_raw_bwd_kernel<<<cdiv(a.B, per), 256, smem, st>>>(a, per);
+}
+
+// ============================================================== head + BCE
+// Head of forward_tensor (pkg/src/longrec/model.py:346-362): [t, c, t⊙c, t⊙t, u_d] → GELU MLP →
+// sigmoid; BCE with the 1e-12 clamp (tensors.py:551-571).  One CTA per sample.
+__global__ void head_fwd_kernel(HeadArgs a) {
+  extern __shared__ float s_in[];                  // HIN + hh
+  const int b = blockIdx.x;
+  const int D = a.D, HIN = 4 * D + 2 * a.d;
+  const float* t = a.x + ((long long)b * a.q + a.k + a.m - 1) * D;
+  const float* c = a.x + ((long long)b * a.q + a.k + 1) * D;
+  const int uid = a.uid[b], prof = a.profile[b];
+  for (int i = threadIdx.x; i < D; i += blockDim.x) {
+    const float tv = t[i], cv = c[i];
+    s_in[i] = tv; s_in[D + i] = cv; s_in[2 * D + i] = tv * cv; s_in[3 * D + i] = tv * tv;
+  }
+  for (int i = threadIdx.x; i < a.d; i += blockDim.x) {
+    s_in[4 * D + i] = a.uid_tab[(long long)uid * a.d + i];
+    s_in[4 * D + a.d + i] = a.prof_tab[(long long)prof * a.d + i];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < HIN; i += blockDim.x) a.hin[(long long)b * HIN + i] = s_in[i];
+  float* s_h = s_in + HIN;
+  for (int j = threadIdx.x; j < a.hh; j += blockDim.x) {
+    float acc = a.b1[j];
+    for (int i = 0; i < HIN; ++i) acc = fmaf(s_in[i], a.w1[i * a.hh + j], acc);
+    a.z1[(long long)b * a.hh + j] = acc;
+    s_h[j] = gelu_f(acc);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float acc = 0.f;
+    for (int j = threadIdx.x; j < a.hh; j += 32) acc = fmaf(s_h[j], a.w2[j], acc);
+    acc = warp_sum(acc);
+    if (threadIdx.x == 0) {
+      const float z = acc + a.b2[0];
+      const float e = __expf(-fabsf(z));
+      const float p = z >= 0.f ? 1.f / (1.f + e) : e / (1.f + e);
+      a.probs[b] = p;
+      if (a.loss_per) {
+        const float y = a.label[b];
+        const float pc = fminf(fmaxf(p, kProbEps), 1.f - kProbEps);
+        a.loss_per[b] = -(y * __logf(pc) + (1.f - y) * __logf(1.f - pc));
+        const bool inr = p > kProbEps && p < 1.f - kProbEps;
+        a.dz[b] = inr ? (p - y) / (float)a.B : 0.f;
+      }
+    }
+  }
+}
+
+__global__ void loss_mean_kernel(const float* loss_per, int B, float* loss) {
+  __shared__ float red[256];
+  float s = 0.f;
+  for (int i = threadIdx.x; i < B; i += blockDim.x) s += loss_per[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) loss[0] = red[0] / (float)B;
+}
+
+void head_fwd(const HeadArgs& a, int with_loss, cudaStream_t st) {
+  const int smem = 4 * (4 * a.D + 2 * a.d + a.hh);
+  head_fwd_kernel<<<a.B, 128, smem, st>>>(a);
+  if (with_loss) loss_mean_kernel<<<1, 256, 0, st>>>(a.loss_per, a.B, a.loss);
+}
+
+__global__ void head_bwd_kernel(HeadArgs a) {
+  extern __shared__ float s[];
+  const int b = blockIdx.x;
+  const int D = a.D, HIN = 4 * D + 2 * a.d;
+  float* s_dz1 = s;              // hh
+  float* s_dhin = s + a.hh;      // HIN
+  const float dz = a.dz[b];
+  for (int j = threadIdx.x; j < a.hh; j += blockDim.x) {
+    const float v = dz * a.w2[j] * gelu_grad_f(a.z1[(long long)b * a.hh + j]);
+    s_dz1[j] = v;
+    a.dz1[(long long)b * a.hh + j] = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < HIN; i += blockDim.x) {
+    float acc = 0.f;
+    for (int j = 0; j < a.hh; ++j) acc = fmaf(s_dz1[j], a.w1[i * a.hh + j], acc);
+    s_dhin[i] = acc;
+  }
+  __syncthreads();
+  const float* hin = a.hin + (long long)b * HIN;
+  float* dt = a.dx + ((long long)b * a.q + a.k + a.m - 1) * D;
+  float* dc = a.dx + ((long long)b * a.q + a.k + 1) * D;
+  for (int i = threadIdx.x; i < D; i += blockDim.x) {
+    const float t = hin[i], c = hin[D + i];
+    dt[i] = s_dhin[i] + s_dhin[2 * D + i] * c + 2.f * s_dhin[3 * D + i] * t;
+    dc[i] = s_dhin[D + i] + s_dhin[2 * D + i] * t;
+  }
+  const int uid = a.uid[b], prof = a.profile[b];
+  for (int i = threadIdx.x; i < a.d; i += blockDim.x) {
+    atomicAdd(&a.g_uid[(long long)uid * a.d + i], s_dhin[4 * D + i]);
+    atomicAdd(&a.g_prof[(long long)prof * a.d + i], s_dhin[4 * D + a.d + i]);
+  }
+}
+
+// head weight gradients: deterministic reductions over the batch (one thread per weight)
+__global__ void head_wgrad_kernel(HeadArgs a) {
+  const int HIN = 4 * a.D + 2 * a.d;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n_w1 = HIN * a.hh;
+  if (e < n_w1) {
+    const int i = e / a.hh, j = e % a.hh;
+    float acc = 0.f;
+    for (int b = 0; b < a.B; ++b) acc = fmaf(a.hin[(long long)b * HIN + i], a.dz1[(long long)b * a.hh + j], acc);
+    a.g_w1[e] += acc;
+  } else if (e < n_w1 + a.hh) {
+    const int j = e - n_w1;
+    float acc = 0.f, acc2 = 0.f;
+    for (int b = 0; b < a.B; ++b) {
+      acc += a.dz1[(long long)b * a.hh + j];
+      acc2 = fmaf(gelu_f(a.z1[(long long)b * a.hh + j]), a.dz[b], acc2);
+    }
+    a.g_b1[j] += acc;
+    a.g_w2[j] += acc2;
+  } else if (e == n_w1 + a.hh) {
+    float acc = 0.f;
+    for (int b = 0; b < a.B; ++b) acc += a.dz[b];
+    a.g_b2[0] += acc;
+  }
+}
+
+void head_bwd(const HeadArgs& a, cudaStream_t st) {
+  const int HIN = 4 * a.D + 2 * a.d;
+  head_bwd_kernel<<<a.B, 128, 4 * (a.hh + HIN), st>>>(a);
+  const int n = HIN * a.hh + a.hh + 1;
+  head_wgrad_kernel<<<cdiv(n, 128), 128, 0, st>>>(a);
+}
+
+// ============================================================== parameters
+__global__ void pack_kernel(const float* __restrict__ params, const PackList specs, void* dst) {
+  const CopySpec s = specs.s[blockIdx.y];
+  const long long n = (long long)s.rows * s.cols;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e / s.cols), c = (int)(e % s.cols);
+    const float v = params[s.src_off + (long long)r * s.src_ld + c];
+    const long long o = s.dst_off + (long long)r * s.dst_ld + c;
+    if (s.to_bf16) reinterpret_cast<bf16*>(dst)[o] = __float2bfloat16(v);
+    else reinterpret_cast<float*>(dst)[o] = v;
+  }
+}
+
+void pack_params(const float* params, const PackList& specs, void* dst_base, cudaStream_t st) {
+  if (specs.n) pack_kernel<<<dim3(64, specs.n), 256, 0, st>>>(params, specs, dst_base);
+}
+
+// Adam (pkg/src/longrec/model.py:467-482)
+__global__ void adam_kernel(float* p, const float* g, float* m, float* v, long long n, float lr, float c1, float c2) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    const float mi = 0.9f * m[i] + 0.1f * gi;
+    const float vi = 0.999f * v[i] + 0.001f * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    p[i] -= lr * (mi / c1) / (sqrtf(vi / c2) + 1e-8f);
+  }
+}
+
+void adam_step(float* p, const float* g, float* m, float* v, long long n, float lr, int t, cudaStream_t st) {
+  const float c1 = (float)(1.0 - pow(0.9, t)), c2 = (float)(1.0 - pow(0.999, t));
+  adam_kernel<<<148 * 8, 256, 0, st>>>(p, g, m, v, n, lr, c1, c2);
+}
+
+}  // namespace longer

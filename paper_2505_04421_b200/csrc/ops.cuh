@@ -1,0 +1,149 @@
+// ops.cuh — launchers of the non-GEMM kernels (embedding, norms, attention, head, globals).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace longer {
+
+// ---------------------------------------------------------------- front-end (tokens)
+struct EmbedArgs {
+  const int32_t *items, *actions, *dt, *n_events;
+  int B, L, Lp, d, d_item, d_act, d_time, FP, nb, vocab, n_actions;
+  const float *item_tab, *act_tab, *time_tab, *pos_tab, *tok_w, *tok_b;   // fp32 master
+  bf16* feat;        // [T, FP]  concat(item, act, time) embedding, zero-padded to FP
+  bf16* x0;          // [T, d]   feat·W_tp + b_tp + abs_pos[recency]   (0 for pad tokens)
+  float* real;       // [T]      1 real / 0 pad
+  float* keep;       // [T]      1 unless the token's merged group is all padding
+  int K;
+  int* status;       // bit0 id out of range, bit1 negative delta
+  int32_t* npg;      // [B] all-pad merged groups per sample ((Lp - n) // K)
+};
+void embed_fwd(const EmbedArgs& a, cudaStream_t st);
+
+struct EmbedBwdArgs {
+  const int32_t *items, *actions, *dt, *n_events;
+  int B, L, Lp, d, d_item, d_act, d_time, nb, vocab, n_actions;
+  const float* tok_w;        // [F, d]
+  const float* dx0;          // [T, d] fp32 (already masked to real tokens)
+  float *g_item, *g_act, *g_time, *g_pos;
+};
+void embed_bwd(const EmbedBwdArgs& a, cudaStream_t st);
+
+// ---------------------------------------------------------------- row layer norm
+// Rows are addressed through a two-source remap so LN can read R = [merged; globals] or
+// O = [merged[G-k:]; globals] without materialising them:
+//   for batch b, output row j (< na + nb):  j < na → A[(b*a_rows + a_off + j) * lda]
+//                                            else  → Bsrc[(b*nb + j - na) * ldb]
+struct RowMap {
+  const float* A; int lda; int a_rows; int a_off; int na;
+  const float* Bsrc; int ldb; int nb;
+  int batch;
+  __host__ __device__ int rows() const { return batch * (na + nb); }
+};
+// y = LN(x)·g + b  → bf16 [rows, W]; mean/rstd saved
+void layernorm_fwd(const RowMap& x, int W, const float* g, const float* b, bf16* y, float* mean, float* rstd,
+                   cudaStream_t st);
+// out(remap-writable) (+)= LN_bw(dy); dgain/dbias accumulated (atomic) into grads.
+struct RowMapW {
+  float* A; int lda; int a_rows; int a_off; int na;
+  float* Bsrc; int ldb; int nb;
+  int batch;
+};
+void layernorm_bwd(const RowMap& x, int W, const float* g, const float* mean, const float* rstd,
+                   const float* dy, int ldy, const RowMapW& out, int accumulate, const float* rowmask,
+                   float* dgain, float* dbias, cudaStream_t st);
+
+// column sums of a [rows, W] matrix (fp32 or bf16), atomically added to out[W]
+void colsum_f32(const float* x, int rows, int W, int ld, float* out, cudaStream_t st);
+void colsum_bf16(const bf16* x, int rows, int W, int ld, float* out, cudaStream_t st);
+
+// elementwise helpers
+void cast_rows_bf16(const float* x, int rows, int W, int ldx, bf16* y, int ldy, const float* rowmask,
+                    cudaStream_t st);
+void mul_rows_inplace(float* x, int rows, int W, const float* rowmask, cudaStream_t st);
+void gather_rows_f32(const float* src, int batch, int src_rows, int src_off, int n, float* dst_base,
+                     int dst_rows, int dst_off, int W, cudaStream_t st);
+void add_rows_f32(const float* src, int batch, int src_rows, int src_off, int n, float* dst_base,
+                  int dst_rows, int dst_off, int W, cudaStream_t st);
+
+// ---------------------------------------------------------------- attention
+// grouped (InnerTrans) attention: groups of K consecutive rows, no mask, scale 1/sqrt(w)
+void group_attn_fwd(const float* qkv, int T, int K, int w, bf16* ctx, float* probs, cudaStream_t st);
+void group_attn_bwd(const float* qkv, const float* probs, const float* dctx, int T, int K, int w, bf16* dqkv,
+                    cudaStream_t st);
+
+// hybrid (cross/self) attention per sample with the VisRule mask.
+struct AttnArgs {
+  const bf16* Q; int ldq; long long sq;     // per-sample stride (elements)
+  const bf16* Kp; int ldk; long long sk;
+  const bf16* V; int ldv; long long sv;
+  int nq, nk, D, heads;
+  int k, G, ns, goff;                        // VisRule parameters
+  const int32_t* npg;                        // [B] pad groups
+  int B;
+  bf16* ctx; int ldc; long long sc;          // fwd out
+  float* lse;                                // [B, heads, nq] (−inf for fully masked rows)
+  // backward
+  const float* dctx; int lddc; long long sdc;
+  const bf16* ctx_in;                        // forward context (for D_i)
+  bf16* dQ; int lddq; long long sdq;
+  bf16* dK; int lddk; long long sdk;
+  bf16* dV; int lddv; long long sdv;
+};
+void attn_fwd(const AttnArgs& a, cudaStream_t st);
+void attn_bwd(const AttnArgs& a, cudaStream_t st);
+
+// ---------------------------------------------------------------- globals + head
+struct GlobalsArgs {
+  const int32_t *uid, *cand_item;
+  int B, m, d, D, d_item, d_act, d_time;
+  const float *uid_tab, *item_tab, *time_tab, *cls, *tok_w, *tok_b, *lift_w, *lift_b;
+  float* raw;      // [B*m, D] fp32
+  bf16* raw_bf;    // [B*m, D]
+  float* td;       // [B, d]   target featurizer output (pre-lift)
+  // backward
+  const float* draw;   // [B*m, D]
+  float *g_uid, *g_item, *g_time, *g_cls, *g_tok_w, *g_tok_b, *g_lift_w, *g_lift_b;
+};
+void globals_raw_fwd(const GlobalsArgs& a, cudaStream_t st);
+void globals_raw_bwd(const GlobalsArgs& a, cudaStream_t st);
+
+struct HeadArgs {
+  const float* x;      // [B*q, D] final layer output
+  int B, q, k, m, D, d, hh;
+  const int32_t *uid, *profile;
+  const float *label, *uid_tab, *prof_tab, *w1, *b1, *w2, *b2;
+  float* hin;          // [B, 4D+2d]
+  float* z1;           // [B, hh]
+  float* probs;        // [B]
+  float* loss_per;     // [B]
+  float* dz;           // [B]
+  float* loss;         // [1] batch mean
+  // backward
+  float* dx;           // [B*q, D]  (zeroed by caller) ← head grads into rows k+m-1 and k+1
+  float *g_w1, *g_b1, *g_w2, *g_b2, *g_uid, *g_prof;
+  float* dz1;          // [B, hh] scratch
+};
+void head_fwd(const HeadArgs& a, int with_loss, cudaStream_t st);
+void head_bwd(const HeadArgs& a, cudaStream_t st);
+
+// ---------------------------------------------------------------- weights
+// Packs fp32 master parameters into the bf16 / fp32 operand layouts the kernels use.
+struct CopySpec {
+  int src_off;    // element offset into params
+  int dst_off;    // element offset into the destination buffer
+  int rows, cols, src_ld, dst_ld;
+  int to_bf16;    // 1: bf16 destination, 0: fp32
+};
+constexpr int kMaxPackSpecs = 256;
+struct PackList {
+  int n;
+  CopySpec s[kMaxPackSpecs];
+};
+void pack_params(const float* params, const PackList& specs, void* dst_base, cudaStream_t st);
+
+void adam_step(float* p, const float* g, float* m, float* v, long long n, float lr, int t, cudaStream_t st);
+
+}  // namespace longer

@@ -1,0 +1,248 @@
+"""``LongerModel`` — the drop-in for ``longrec.LongRecModel`` on the B200 path.
+
+Same constructor (``LongerModel(cfg, seed)``), same ``params()`` names/shapes/order and the
+same initial weights (``params.init_params`` replays the reference RNG stream), same
+``forward``/``score`` semantics and the same checkpoint format (``LRCKPT01``,
+``pkg/src/longrec/model.py:381-427``).  The difference: a call takes a whole batch and runs it
+through the sm_100a library (``include/longer.h``) in one stream-ordered call; there is no CPU
+fallback.
+
+Master parameters are one fp32 device buffer in ``params()`` order (views per name); gradients
+live in a second buffer of the same layout.
+"""
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import json
+import math
+import struct
+from typing import Optional, Sequence, Union
+
+import numpy as np
+
+from . import _lib
+from .config import ModelConfig
+from .errors import ConfigError, EmbeddingLookupError, NumericalError
+from .inputs import Batch, Sample, check_batch, tensorize
+from .params import init_params, param_shapes
+
+CHECKPOINT_MAGIC = b"LRCKPT01"
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class LongerModel:
+    """Long-sequence recommender transformer (LONGER) on B200.
+
+    ``forward(batch)`` → probabilities ``[B]`` (device tensor);
+    ``loss_backward(batch)`` → batch-mean BCE (float) and fills ``grad_flat`` / ``grads()``.
+    ``batch`` may be a list of ``Sample``, a host ``Batch`` (numpy) or a device ``Batch``.
+    """
+
+    def __init__(self, cfg: ModelConfig, seed: int = 0, device: str = "cuda") -> None:
+        torch = _torch()
+        cfg.validate()
+        if cfg.query_strategy != "recent":
+            raise ConfigError("the B200 path implements the 'recent' query strategy")
+        if cfg.d % 8:
+            raise ConfigError("the B200 path needs d % 8 == 0 (16-byte rows for TMA)")
+        self.cfg = cfg
+        self.device = torch.device(device)
+        if self.device.type != "cuda":
+            raise RuntimeError("LongerModel runs on a CUDA (sm_100a) device only")
+        self._lib = _lib.load()
+        self.shapes = param_shapes(cfg)
+        init = init_params(cfg, seed)
+        flat = np.concatenate([a.ravel() for a in init.values()]).astype(np.float32)
+        n = ctypes.c_int64()
+        _lib.check(self._lib.longer_param_count(ctypes.byref(_lib.dims_of(cfg, 1)), ctypes.byref(n)))
+        if n.value != flat.size:
+            raise RuntimeError(f"parameter layout mismatch: library {n.value}, host {flat.size}")
+        self.flat = torch.from_numpy(flat).to(self.device)
+        self.grad_flat = torch.zeros_like(self.flat)
+        self._views = self._make_views(self.flat)
+        self._gviews = self._make_views(self.grad_flat)
+        self.param_version = 0
+        self._ws = {}
+        self._probs = {}
+        self._loss = torch.zeros(1, dtype=torch.float32, device=self.device)
+
+    # ------------------------------------------------------------------ parameters
+    def _make_views(self, buf):
+        out, off = {}, 0
+        for name, shape in self.shapes.items():
+            size = int(np.prod(shape))
+            out[name] = buf[off:off + size].view(*shape)
+            off += size
+        return out
+
+    def params(self):
+        """[(name, fp32 device tensor)] in reference order (pkg/src/longrec/model.py:252-263)."""
+        return list(self._views.items())
+
+    def grads(self):
+        return list(self._gviews.items())
+
+    def param_count(self) -> int:
+        return int(self.flat.numel())
+
+    def load_params(self, named) -> None:
+        """Copy weights by name (e.g. from a reference ``LongRecModel.params()``)."""
+        torch = _torch()
+        for name, value in (named.items() if isinstance(named, dict) else named):
+            data = getattr(value, "data", value)
+            arr = np.asarray(data, dtype=np.float32)
+            if name not in self._views:
+                raise ConfigError(f"unknown parameter {name!r}")
+            if tuple(arr.shape) != tuple(self._views[name].shape):
+                raise ConfigError(f"parameter {name!r} shape {arr.shape} != {tuple(self._views[name].shape)}")
+            self._views[name].copy_(torch.from_numpy(arr))
+        self.param_version += 1
+
+    def fingerprint(self) -> str:
+        """sha256(config, param_version) (pkg/src/longrec/model.py:268-271)."""
+        payload = json.dumps(self.cfg.to_dict(), sort_keys=True)
+        return hashlib.sha256(f"{payload}|v{self.param_version}".encode()).hexdigest()[:16]
+
+    # ------------------------------------------------------------------ batches
+    def to_device_batch(self, batch: Union[Batch, Sequence[Sample]]) -> Batch:
+        torch = _torch()
+        if not isinstance(batch, Batch):
+            batch = tensorize(list(batch), self.cfg)
+        elif isinstance(batch.items, np.ndarray):
+            check_batch(batch, self.cfg)
+        if isinstance(batch.items, np.ndarray) or batch.items.device != self.device:
+            batch = batch.to(self.device)
+        return batch
+
+    def _struct(self, b: Batch) -> _lib.LongerBatch:
+        return _lib.LongerBatch(*[int(getattr(b, f).data_ptr()) for f in Batch.FIELDS])
+
+    def _workspace(self, B: int):
+        torch = _torch()
+        if B not in self._ws:
+            nbytes = ctypes.c_size_t()
+            _lib.check(self._lib.longer_workspace_bytes(ctypes.byref(_lib.dims_of(self.cfg, B)), ctypes.byref(nbytes)))
+            self._ws[B] = torch.zeros(nbytes.value + 256, dtype=torch.uint8, device=self.device)
+            self._probs[B] = torch.zeros(B, dtype=torch.float32, device=self.device)
+        ws = self._ws[B]
+        base = (ws.data_ptr() + 255) & ~255
+        return base, ws.numel() - (base - ws.data_ptr())
+
+    def _stream(self):
+        return ctypes.c_void_p(_torch().cuda.current_stream(self.device).cuda_stream)
+
+    def read_status(self, B: int) -> None:
+        """Raise the reference error for device-detected bad inputs (ids / time deltas)."""
+        base, _ = self._workspace(B)
+        flags = ctypes.c_int32()
+        _lib.check(self._lib.longer_read_status(ctypes.c_void_p(base), ctypes.byref(flags), self._stream()))
+        if flags.value & 1:
+            raise EmbeddingLookupError("an id fell outside its embedding table")
+        if flags.value & 2:
+            raise ConfigError("future event: negative time delta")
+
+    # ------------------------------------------------------------------ compute
+    def forward(self, batch, sync_check: bool = False):
+        """Probabilities [B] for a batch (``forward_tensor`` + sigmoid, model.py:307-377)."""
+        b = self.to_device_batch(batch)
+        B = b.size
+        base, nbytes = self._workspace(B)
+        probs = self._probs[B]
+        rc = self._lib.longer_forward(ctypes.byref(_lib.dims_of(self.cfg, B)), ctypes.c_void_p(self.flat.data_ptr()),
+                                      ctypes.byref(self._struct(b)), ctypes.c_void_p(base), nbytes,
+                                      ctypes.c_void_p(probs.data_ptr()), self._stream())
+        _lib.check(rc)
+        if sync_check:
+            self.read_status(B)
+        return probs
+
+    def score(self, sample: Sample) -> float:
+        return float(self.forward([sample], sync_check=True)[0].item())
+
+    def loss_backward(self, batch, check: bool = True):
+        """Train-step body (model.py:555-567): grads ← d(mean BCE)/dparams; returns the loss.
+
+        With ``check`` the loss is read back (one D2H sync) and a non-finite value raises
+        ``NumericalError`` exactly like ``train`` (model.py:563-566)."""
+        b = self.to_device_batch(batch)
+        B = b.size
+        base, nbytes = self._workspace(B)
+        probs = self._probs[B]
+        rc = self._lib.longer_forward_backward(
+            ctypes.byref(_lib.dims_of(self.cfg, B)), ctypes.c_void_p(self.flat.data_ptr()),
+            ctypes.byref(self._struct(b)), ctypes.c_void_p(base), nbytes, ctypes.c_void_p(probs.data_ptr()),
+            ctypes.c_void_p(self._loss.data_ptr()), ctypes.c_void_p(self.grad_flat.data_ptr()), self._stream())
+        _lib.check(rc)
+        if not check:
+            return self._loss
+        self.read_status(B)
+        value = float(self._loss.item())
+        if not math.isfinite(value):
+            raise NumericalError("non-finite loss")
+        return value
+
+    # ------------------------------------------------------------------ checkpoints
+    def save(self, path: str) -> None:
+        """``LRCKPT01`` (model.py:381-406): magic, <Q header length, JSON header, float64 LE arrays."""
+        named = [(n, v.detach().double().cpu().numpy()) for n, v in self.params()]
+        header = {"format_version": 1, "config": self.cfg.to_dict(), "param_version": self.param_version,
+                  "arrays": [{"name": n, "shape": list(a.shape)} for n, a in named]}
+        blob = json.dumps(header, sort_keys=True).encode("utf-8")
+        with open(path, "wb") as fh:
+            fh.write(CHECKPOINT_MAGIC)
+            fh.write(struct.pack("<Q", len(blob)))
+            fh.write(blob)
+            for _, a in named:
+                fh.write(a.astype("<f8").tobytes())
+
+    @classmethod
+    def load(cls, path: str, device: str = "cuda") -> "LongerModel":
+        with open(path, "rb") as fh:
+            magic = fh.read(8)
+            if magic != CHECKPOINT_MAGIC:
+                raise ConfigError(f"not a checkpoint file: bad magic {magic!r}")
+            (hlen,) = struct.unpack("<Q", fh.read(8))
+            header = json.loads(fh.read(hlen).decode("utf-8"))
+            if header.get("format_version") != 1:
+                raise ConfigError("unsupported checkpoint format version")
+            cfg = ModelConfig.from_dict(header["config"])
+            model = cls(cfg, seed=0, device=device)
+            named = {}
+            for entry in header["arrays"]:
+                name, shape = entry["name"], tuple(entry["shape"])
+                if name not in model._views:
+                    raise ConfigError(f"checkpoint array {name!r} not in model")
+                if tuple(model._views[name].shape) != shape:
+                    raise ConfigError(f"checkpoint array {name!r} shape mismatch")
+                count = int(np.prod(shape)) if shape else 1
+                named[name] = np.frombuffer(fh.read(count * 8), dtype="<f8").reshape(shape)
+            model.load_params(named)
+            model.param_version = int(header["param_version"])
+        return model
+
+
+class Adam:
+    """Adam with the reference's fixed hyper-parameters (model.py:453-482) on the flat buffers,
+    one fused sm_100a kernel per step."""
+
+    def __init__(self, model: LongerModel, lr: float) -> None:
+        torch = _torch()
+        self.model = model
+        self.lr = float(lr)
+        self.t = 0
+        self.m = torch.zeros_like(model.flat)
+        self.v = torch.zeros_like(model.flat)
+
+    def step(self) -> None:
+        self.t += 1
+        mdl = self.model
+        _lib.check(mdl._lib.longer_adam_step(
+            ctypes.c_void_p(mdl.flat.data_ptr()), ctypes.c_void_p(mdl.grad_flat.data_ptr()),
+            ctypes.c_void_p(self.m.data_ptr()), ctypes.c_void_p(self.v.data_ptr()), mdl.flat.numel(),
+            self.lr, self.t, mdl._stream()))
+        mdl.param_version += 1

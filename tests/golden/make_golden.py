@@ -45,6 +45,10 @@ CASES = {
     "tiny_oddL": (dict(TINY, L=7, merge_mode="inner"), [7, 4, 1, 9], 8),
     "small_c1": (dict(L=64, d=16, K=4, k=16, N=1, m=3, n_users=64), [64, 64, 40, 10, 64], 9),
     "small_c2_inner": (dict(L=64, d=32, K=4, k=8, N=2, m=3, merge_mode="inner", n_users=64), [64, 50, 64, 3], 10),
+    # device-eligible (d % 8 == 0) edge cases: odd L, heads=2, m=4, two inner layers, pad queries
+    "gpu_d8_h2": (dict(L=30, d=8, K=4, m=4, k=5, N=2, heads=2, merge_mode="inner", inner_layers=2,
+                       head_hidden=16, n_users=50, vocab=60), [30, 17, 5, 0, 40, 12], 11),
+    "gpu_concat_d8": (dict(L=48, d=8, K=2, k=6, N=3, n_users=40), [48, 20, 3, 48], 12),
 }
 
 
