@@ -1,0 +1,310 @@
+#!/usr/bin/env python
+"""LONGER encoder training-step throughput on B200 (BASELINE.json metric).
+
+metric: samples/sec of fwd+bwd at L=2000 (config 2: B=256/GPU, d=32, K=4 → D=128, k=32
+recent queries + m=3 globals, 1 cross + N=2 self layers, InnerTrans merge), whole job.
+
+A step = forward + backward (+ NCCL gradient allreduce when N>1) + Adam, through the C ABI
+(`longer_forward_backward`, `longer_adam_step`), captured in one CUDA graph.  `value` times the
+device step with CUDA events (inputs resident in HBM, L2 flushed between steps); `e2e` times the
+same step with the batch copied from pinned host memory and the loss read back every step.
+
+`--impl reference` times the CPU reference algorithm (the float64 oracle port of longrec in
+oracle/, all host threads) on a bounded sample of the same workload.
+
+Launch: python bench.py [--gpus N --steps K --warmup W]; N>1 under torch.distributed.run.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c2_inner": dict(L=2000, d=32, K=4, k=32, N=2, m=3, merge_mode="inner"),
+    "c2_concat": dict(L=2000, d=32, K=4, k=32, N=2, m=3, merge_mode="concat"),
+    "c1": dict(L=256, d=16, K=4, k=16, N=1, m=3),
+    "c5_inner": dict(L=10000, d=32, K=8, k=32, N=4, m=3, merge_mode="inner"),
+}
+
+
+def flops_per_sample(cfg) -> int:
+    """6 × the reference's exact forward MAC count (pkg/src/longrec/analysis.py:152-171):
+    2 FLOP/MAC × (forward + 2 × backward)."""
+    d, D, F = cfg.d, cfg.D, cfg.feat_width
+    q, v = cfg.k + cfg.m, cfg.merged_len + cfg.m
+    n_events = cfg.L
+    total = n_events * (F * d + 4 * d * D)
+    total += F * d + 2 * d * D + cfg.m * 4 * D * D
+    if cfg.merge_mode == "inner":
+        Lp = cfg.L_padded
+        total += cfg.inner_layers * (12 * Lp * d * d + 2 * Lp * cfg.K * d)
+    total += 10 * q * D * D + 2 * v * D * D + 2 * q * v * D
+    total += cfg.N * (12 * q * D * D + 2 * q * q * D)
+    total += (4 * D + 2 * d) * cfg.head_hidden + cfg.head_hidden
+    return 6 * total
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return p["bf16_tflops"], p.get("bf16_tflops_sustained"), p["hbm_gbs"], "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def start(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 7:
+                for i, n in enumerate(names):
+                    if r[3 + i].lower() == "active":
+                        reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def cpu_reference_rate(cfg, n_samples: int, seed: int = 1):
+    """Float64 oracle port of the reference algorithm, one batch of n_samples (all BLAS threads)."""
+    import numpy as np
+    from oracle import longer_oracle as O
+    from paper_2505_04421_b200 import init_params, synthetic_batch
+    P = init_params(cfg, 0)
+    batch = synthetic_batch(cfg, n_samples, seed=seed).as_dict()
+    O.forward_backward(P, cfg, {k: v[:1] for k, v in batch.items()})   # warm-up
+    t0 = time.perf_counter()
+    O.forward_backward(P, cfg, batch)
+    dt = time.perf_counter() - t0
+    return n_samples / dt, dt
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np  # noqa: F401
+    sample = args.cpu_samples
+    rates, total = [], 0.0
+    for i in range(args.warmup + args.steps):
+        r, dt = cpu_reference_rate(cfg, sample, seed=1 + i)
+        if i >= args.warmup:
+            rates.append(r)
+            total += dt
+    value = sample * len(rates) / total
+    line = {
+        "impl": "reference", "metric": "samples/sec fwd+bwd at L=2000", "value": value, "unit": "samples/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(rates), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, **CONFIGS[args.config], "samples_per_step": sample},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": os.cpu_count(), "kind": "port",
+                         "sample": f"{sample} samples/step, float64 NumPy oracle port of longrec fwd+bwd"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2_inner", choices=sorted(CONFIGS))
+    ap.add_argument("--batch", type=int, default=256, help="samples per GPU per step")
+    ap.add_argument("--cpu-samples", type=int, default=8)
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    from paper_2505_04421_b200 import ModelConfig
+    cfg = ModelConfig(**CONFIGS[args.config]).validate()
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2505_04421_b200 import synthetic_batch
+    from paper_2505_04421_b200.model import Adam, LongerModel
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    B = args.batch
+    model = LongerModel(cfg, seed=0, device=str(dev))
+    opt = Adam(model, cfg.lr)
+    # a few distinct synthetic batches, resident in HBM; host pinned copies for e2e
+    n_batches = 4
+    host = [synthetic_batch(cfg, B, seed=100 + rank * 17 + i).pin() for i in range(n_batches)]
+    dev_batches = [h.to(dev) for h in host]
+    static = synthetic_batch(cfg, B, seed=1).to(dev)          # graph input slot
+
+    def load(b):
+        for f in type(b).FIELDS:
+            getattr(static, f).copy_(getattr(b, f), non_blocking=True)
+
+    def step_body():
+        model.loss_backward(static, check=False)
+        if world > 1:
+            dist.all_reduce(model.grad_flat)
+            model.grad_flat.mul_(1.0 / world)
+        opt.step()
+
+    stream = torch.cuda.current_stream(dev)
+    # warm-up (eager) — also sets kernel attributes before capture
+    for i in range(2):
+        load(dev_batches[i % n_batches])
+        step_body()
+    torch.cuda.synchronize()
+    graph = None
+    if not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(dev)
+        s.wait_stream(stream)
+        with torch.cuda.stream(s):
+            step_body()
+        stream.wait_stream(s)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph):
+            step_body()
+        torch.cuda.synchronize()
+
+    def run_step():
+        if graph is not None:
+            graph.replay()
+        else:
+            step_body()
+
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    for i in range(args.warmup):
+        load(dev_batches[i % n_batches])
+        run_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    # ---------------- timed region: device step, inputs resident, L2 flushed between steps
+    clocks = ClockSampler(local)
+    clocks.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    for i in range(args.steps):
+        load(dev_batches[i % n_batches])
+        flush.fill_(i & 0xFF)
+        ev[i][0].record(stream)
+        run_step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+
+    # ---------------- e2e: pinned host batch → H2D, step, loss D2H, every step
+    loss_host = torch.zeros(1, dtype=torch.float32).pin_memory()
+    e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    h2d_bytes = host[0].nbytes()
+    for i in range(args.steps):
+        e2e_ev[i][0].record(stream)
+        load(host[i % n_batches])
+        run_step()
+        loss_host.copy_(model._loss, non_blocking=True)
+        e2e_ev[i][1].record(stream)
+        e2e_ev[i][1].synchronize()
+    e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev)
+
+    t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, e2e_ms = float(t[0]), float(t[1])
+    samples = world * B * args.steps
+    value = samples / (ms / 1e3)
+    e2e_value = samples / (e2e_ms / 1e3)
+    ms_step = ms / args.steps
+
+    if rank == 0:
+        burst, sustained, hbm, src = peaks()
+        fps = flops_per_sample(cfg)
+        achieved = value / world * fps / 1e12
+        line = {
+            "metric": "samples/sec fwd+bwd at L=2000", "value": value, "unit": "samples/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
+            "config": {"workload": args.config, **CONFIGS[args.config], "global_batch": world * B,
+                       "per_gpu_batch": B, "parallelism": f"dp{world}", "l2": "flushed between steps",
+                       "step": "fwd+bwd+allreduce+adam" if world > 1 else "fwd+bwd+adam",
+                       "cuda_graph": graph is not None},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": burst, "unit": "TFLOP/s",
+                         "frac": achieved / burst, "traffic": None, "peak_source": src,
+                         "scope": "whole step (algorithmic FLOPs = 6 x analysis.muladds_full_forward per sample)",
+                         "frac_of_sustained": achieved / sustained if sustained else None},
+            "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d_bytes,
+                    "d2h_bytes_per_step": 4},
+            "clocks": clk,
+        }
+        if not args.no_cpu_baseline:
+            try:
+                r, dt = cpu_reference_rate(cfg, args.cpu_samples)
+                line["cpu_baseline"] = {"value": r, "unit": "samples/s", "cores": os.cpu_count(), "kind": "port",
+                                        "sample": f"{args.cpu_samples} samples, one fwd+bwd of the float64 oracle "
+                                                  f"port ({dt:.1f} s)"}
+            except Exception as exc:  # pragma: no cover
+                line["cpu_baseline"] = {"value": None, "error": str(exc)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
