@@ -1,4 +1,8 @@
 // gemm.cu — generic tcgen05 GEMM with fused epilogues. See gemm.cuh for the contract.
+//
+// CTA = 1 TMA warp + 1 MMA warp (also owns TMEM) + 8 epilogue warps.  The smem ring depth is a
+// template parameter chosen from the K extent (1, 2 or 4 stages) so that the short-K GEMMs of the
+// token pipeline keep 2-3 CTAs per SM and overlap one CTA's epilogue with another's MMA.
 #include "gemm.cuh"
 #include "sm100.cuh"
 #include "tma.cuh"
@@ -12,29 +16,29 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int STAGES = 4;
-constexpr int kThreads = 192;  // w0 TMA, w1 MMA + TMEM owner, w2..w5 epilogue
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 
-
-template <int BN>
+template <int BN, int STAGES>
 struct Smem {
   static constexpr int A_BYTES = BM * BK * 2;        // 16 KB
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int TOTAL = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int TOTAL = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + kEpiWarps * 32 * 33 * 4;
 };
 
-template <int BN>
+template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
             GemmArgs g, int kb_per_split) {
-  using S = Smem<BN>;
+  using S = Smem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tmem_full = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  float* stage_base = reinterpret_cast<float*>(smem + STAGES * S::STAGE_BYTES + 256);
 
   const int warp = threadIdx.x / 32;
   const int n0 = blockIdx.x * BN;
@@ -102,41 +106,62 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       sm100::mma_commit(tmem_full);
     }
   } else {
-    // epilogue warps 2..5 → TMEM lane quarter (warp % 4)
+    // Epilogue warps e = 0..7: TMEM lane quarter q = warp % 4, column chunks c ≡ e/4 (mod 2).
+    // Each 32x32 accumulator block is transposed through a padded per-warp smem tile so every
+    // global load/store is row-contiguous across the warp; loads for 8 rows are issued before use.
+    const int e = warp - 2;
     const int q = warp & 3;
-    const int row = m0 + q * 32 + (threadIdx.x & 31);
+    const int lane = threadIdx.x & 31;
+    float* stg = stage_base + e * 32 * 33;
     sm100::mbar_wait(tmem_full, 0);
     sm100::tc_fence_after();
     const uint32_t flags = g.flags;
-    const bool row_ok = row < g.M;
-    float rmask = 1.0f;
-    if ((flags & EPI_ROWMASK) && row_ok) rmask = g.rowmask[row];
+    const int row0 = m0 + q * 32;
+    const __nv_bfloat16* pre_in = reinterpret_cast<const __nv_bfloat16*>(g.pre_bf16);
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
+    for (int c = (e >> 2) * 32; c < BN; c += 64) {
       uint32_t r[32];
       sm100::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + c, r);
       sm100::tmem_ld_wait();
-      if (!row_ok || n0 + c >= g.N) continue;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int n = n0 + c + j;
-        if (n >= g.N) break;
-        float v = __uint_as_float(r[j]);
-        if (flags & EPI_BIAS) v += g.bias[n];
-        if (flags & EPI_SAVE_PRE)
-          reinterpret_cast<__nv_bfloat16*>(g.pre_bf16)[(size_t)row * g.ldc_bf + n] = __float2bfloat16(v);
-        if (flags & EPI_GELU) v = gelu_f(v);
-        if (flags & EPI_GELU_BWD)
-          v *= gelu_grad_f(__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(g.pre_bf16)[(size_t)row * g.ldc_bf + n]));
-        if (flags & EPI_RESID) v += g.resid[(size_t)row * g.ldr + n];
-        if (flags & EPI_ROWMASK) v *= rmask;
-        if (flags & EPI_OUT_F32) {
-          float* dst = g.C + (size_t)row * g.ldc + n;
-          if (flags & EPI_ATOMIC) atomicAdd(dst, v); else *dst = v;
+      for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = __uint_as_float(r[j]);
+      __syncwarp();
+      const int n = n0 + c + lane;
+      if (n0 + c < g.N && row0 < g.M) {
+        const bool col_ok = n < g.N;
+        const float bias_n = ((flags & EPI_BIAS) && col_ok) ? g.bias[n] : 0.f;
+#pragma unroll 1
+        for (int r0 = 0; r0 < 32; r0 += 8) {
+          float pv[8], rv[8], mv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int row = row0 + r0 + u;
+            const bool ok = col_ok && row < g.M;
+            pv[u] = ((flags & EPI_GELU_BWD) && ok) ? __bfloat162float(pre_in[(size_t)row * g.ldc_bf + n]) : 0.f;
+            rv[u] = ((flags & EPI_RESID) && ok) ? g.resid[(size_t)row * g.ldr + n] : 0.f;
+            mv[u] = ((flags & EPI_ROWMASK) && row < g.M) ? g.rowmask[row] : 1.f;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int row = row0 + r0 + u;
+            if (!col_ok || row >= g.M) continue;
+            float v = stg[(r0 + u) * 33 + lane] + bias_n;
+            if (flags & EPI_SAVE_PRE)
+              reinterpret_cast<__nv_bfloat16*>(g.pre_bf16)[(size_t)row * g.ldc_bf + n] = __float2bfloat16(v);
+            if (flags & EPI_GELU) v = gelu_f(v);
+            if (flags & EPI_GELU_BWD) v *= gelu_grad_f(pv[u]);
+            v += rv[u];
+            v *= mv[u];
+            if (flags & EPI_OUT_F32) {
+              float* dst = g.C + (size_t)row * g.ldc + n;
+              if (flags & EPI_ATOMIC) atomicAdd(dst, v); else *dst = v;
+            }
+            if (flags & EPI_OUT_BF16)
+              reinterpret_cast<__nv_bfloat16*>(g.C_bf16)[(size_t)row * g.ldc_bf + n] = __float2bfloat16(v);
+          }
         }
-        if (flags & EPI_OUT_BF16)
-          reinterpret_cast<__nv_bfloat16*>(g.C_bf16)[(size_t)row * g.ldc_bf + n] = __float2bfloat16(v);
       }
+      __syncwarp();
     }
   }
   sm100::tc_fence_before();
@@ -144,11 +169,23 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   if (warp == 1) sm100::tmem_dealloc<(BN < 32 ? 32 : BN)>(tmem);
 }
 
+template <int BN, int STAGES>
+int launch_cfg(const GemmArgs& g, const CUtensorMap& tA, const CUtensorMap& tB, dim3 grid, int kb_per,
+               cudaStream_t st) {
+  const int smem = Smem<BN, STAGES>::TOTAL;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gemm_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr_set = true;
+  }
+  gemm_kernel<BN, STAGES><<<grid, kThreads, smem, st>>>(tA, tB, g, kb_per);
+  return (int)cudaGetLastError();
+}
+
 template <int BN>
 int launch_bn(const GemmArgs& g, cudaStream_t st) {
   CUtensorMap tA, tB;
   int rc;
-  // A
   if (!g.a_mn_major) rc = tma::encode_2d_bf16(&tA, g.A, g.K, g.M, g.lda, BK, BM);
   else rc = tma::encode_2d_bf16(&tA, g.A, g.M, g.K, g.lda, 64, BK);
   if (rc) return rc;
@@ -163,14 +200,9 @@ int launch_bn(const GemmArgs& g, cudaStream_t st) {
   int kb_per = (nkb + split - 1) / split;
   split = (nkb + kb_per - 1) / kb_per;
   dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, split);
-  const int smem = Smem<BN>::TOTAL;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr_set = true;
-  }
-  gemm_kernel<BN><<<grid, kThreads, smem, st>>>(tA, tB, g, kb_per);
-  return (int)cudaGetLastError();
+  if (kb_per <= 1) return launch_cfg<BN, 1>(g, tA, tB, grid, kb_per, st);
+  if (kb_per <= 2) return launch_cfg<BN, 2>(g, tA, tB, grid, kb_per, st);
+  return launch_cfg<BN, 4>(g, tA, tB, grid, kb_per, st);
 }
 
 }  // namespace

@@ -346,74 +346,149 @@ void add_rows_f32(const float* src, int batch, int src_rows, int src_off, int n,
 
 // ============================================================== grouped attention (InnerTrans)
 // grouped_attention (pkg/src/longrec/tensors.py:406-444): softmax(q kᵀ/√w) v inside each group of
-// K consecutive rows.  One thread per row; qkv = [q | k | v] fp32 [T, 3w].
-__global__ void group_attn_fwd_kernel(const float* __restrict__ qkv, int T, int K, int w, bf16* ctx, float* probs) {
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= T) return;
-  const long long g0 = t - t % K;
-  const float scale = rsqrtf((float)w);
-  const float* q = qkv + t * 3 * w;
-  float s[16];
-  float mx = -INFINITY;
-  for (int j = 0; j < K; ++j) {
-    const float* kr = qkv + (g0 + j) * 3 * w + w;
-    float acc = 0.f;
-    for (int c = 0; c < w; ++c) acc = fmaf(q[c], kr[c], acc);
-    s[j] = acc * scale;
-    mx = fmaxf(mx, s[j]);
+// K consecutive rows.  A CTA stages a tile of whole groups (qkv = [q | k | v] fp32 [T, 3w]) in
+// shared memory with coalesced loads, one thread computes one row, and results leave through
+// shared memory with coalesced stores.
+template <int KT>
+__global__ void group_attn_fwd_kernel(const float* __restrict__ qkv, int T, int Kr, int w, bf16* ctx, float* probs) {
+  extern __shared__ float sm[];
+  const int K = KT > 0 ? KT : Kr;
+  const int TT = (blockDim.x / K) * K;                   // tokens per tile (whole groups)
+  const int ld = 3 * w + 1;
+  float* s_in = sm;                                      // TT * ld
+  float* s_out = sm + TT * ld;                           // TT * (w+1)
+  const long long t0 = (long long)blockIdx.x * TT;
+  const int nt = (int)min((long long)TT, T - t0);
+  for (int e = threadIdx.x; e < nt * 3 * w; e += blockDim.x)
+    s_in[(e / (3 * w)) * ld + e % (3 * w)] = qkv[t0 * 3 * w + e];
+  __syncthreads();
+  const int i = threadIdx.x;
+  if (i < nt) {
+    const int g0 = i - i % K;
+    const float scale = rsqrtf((float)w);
+    constexpr int KM = KT > 0 ? KT : 16;
+    float s[KM];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < KM; ++j) {
+      if (j >= K) break;
+      float acc = 0.f;
+      for (int c = 0; c < w; ++c) acc = fmaf(s_in[i * ld + c], s_in[(g0 + j) * ld + w + c], acc);
+      s[j] = acc * scale;
+      mx = fmaxf(mx, s[j]);
+    }
+    float tot = 0.f;
+#pragma unroll
+    for (int j = 0; j < KM; ++j) { if (j >= K) break; s[j] = __expf(s[j] - mx); tot += s[j]; }
+    const float inv = 1.f / tot;
+#pragma unroll
+    for (int j = 0; j < KM; ++j) { if (j >= K) break; s[j] *= inv; probs[(t0 + i) * K + j] = s[j]; }
+    for (int c = 0; c < w; ++c) {
+      float acc = 0.f;
+#pragma unroll
+      for (int j = 0; j < KM; ++j) { if (j >= K) break; acc = fmaf(s[j], s_in[(g0 + j) * ld + 2 * w + c], acc); }
+      s_out[i * (w + 1) + c] = acc;
+    }
   }
-  float tot = 0.f;
-  for (int j = 0; j < K; ++j) { s[j] = __expf(s[j] - mx); tot += s[j]; }
-  const float inv = 1.f / tot;
-  for (int j = 0; j < K; ++j) { s[j] *= inv; probs[t * K + j] = s[j]; }
-  for (int c = 0; c < w; ++c) {
-    float acc = 0.f;
-    for (int j = 0; j < K; ++j) acc = fmaf(s[j], qkv[(g0 + j) * 3 * w + 2 * w + c], acc);
-    ctx[t * w + c] = __float2bfloat16(acc);
-  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nt * w; e += blockDim.x)
+    ctx[t0 * w + e] = __float2bfloat16(s_out[(e / w) * (w + 1) + e % w]);
 }
 
+template <int KT>
 __global__ void group_attn_bwd_kernel(const float* __restrict__ qkv, const float* __restrict__ probs,
-                                      const float* __restrict__ dctx, int T, int K, int w, bf16* dqkv) {
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= T) return;
-  const long long g0 = t - t % K;
-  const int me = (int)(t - g0);
-  const float scale = rsqrtf((float)w);
-  // dP[i][j] = dctx[i]·v[j];  dS = P ∘ (dP − rowsum(dP∘P)) · scale
-  float dS[16][16];
-  for (int i = 0; i < K; ++i) {
-    float dp[16];
-    float dot = 0.f;
-    for (int j = 0; j < K; ++j) {
-      float acc = 0.f;
-      const float* dr = dctx + (g0 + i) * w;
-      const float* vr = qkv + (g0 + j) * 3 * w + 2 * w;
-      for (int c = 0; c < w; ++c) acc = fmaf(dr[c], vr[c], acc);
-      dp[j] = acc;
-      dot += acc * probs[(g0 + i) * K + j];
+                                      const float* __restrict__ dctx, int T, int Kr, int w, bf16* dqkv) {
+  extern __shared__ float sm[];
+  const int K = KT > 0 ? KT : Kr;
+  const int TT = (blockDim.x / K) * K;
+  const int ld = 3 * w + 1;
+  float* s_in = sm;                          // TT * ld   (q|k|v)
+  float* s_do = s_in + TT * ld;              // TT * (w+1)
+  float* s_out = s_do + TT * (w + 1);        // TT * ld   (dq|dk|dv)
+  const long long t0 = (long long)blockIdx.x * TT;
+  const int nt = (int)min((long long)TT, T - t0);
+  for (int e = threadIdx.x; e < nt * 3 * w; e += blockDim.x)
+    s_in[(e / (3 * w)) * ld + e % (3 * w)] = qkv[t0 * 3 * w + e];
+  for (int e = threadIdx.x; e < nt * w; e += blockDim.x) s_do[(e / w) * (w + 1) + e % w] = dctx[t0 * w + e];
+  __syncthreads();
+  const int me_t = threadIdx.x;
+  if (me_t < nt) {
+    const int g0 = me_t - me_t % K;
+    const int me = me_t - g0;
+    const float scale = rsqrtf((float)w);
+    constexpr int KM = KT > 0 ? KT : 16;
+    // dP[i][j] = dctx[i]·v[j];  dS = P ∘ (dP − rowsum(dP∘P)) · scale
+    float dS[KM][KM], P[KM][KM];
+#pragma unroll
+    for (int i = 0; i < KM; ++i) {
+      if (i >= K) break;
+      float dp[KM];
+      float dot = 0.f;
+#pragma unroll
+      for (int j = 0; j < KM; ++j) {
+        if (j >= K) break;
+        float acc = 0.f;
+        for (int c = 0; c < w; ++c) acc = fmaf(s_do[(g0 + i) * (w + 1) + c], s_in[(g0 + j) * ld + 2 * w + c], acc);
+        dp[j] = acc;
+        P[i][j] = probs[(t0 + g0 + i) * K + j];
+        dot += acc * P[i][j];
+      }
+#pragma unroll
+      for (int j = 0; j < KM; ++j) { if (j >= K) break; dS[i][j] = P[i][j] * (dp[j] - dot) * scale; }
     }
-    for (int j = 0; j < K; ++j) dS[i][j] = probs[(g0 + i) * K + j] * (dp[j] - dot) * scale;
-  }
-  for (int c = 0; c < w; ++c) {
-    float dq = 0.f, dk = 0.f, dv = 0.f;
-    for (int j = 0; j < K; ++j) dq = fmaf(dS[me][j], qkv[(g0 + j) * 3 * w + w + c], dq);
-    for (int i = 0; i < K; ++i) {
-      dk = fmaf(dS[i][me], qkv[(g0 + i) * 3 * w + c], dk);
-      dv = fmaf(probs[(g0 + i) * K + me], dctx[(g0 + i) * w + c], dv);
+    for (int c = 0; c < w; ++c) {
+      float dq = 0.f, dk = 0.f, dv = 0.f;
+#pragma unroll
+      for (int j = 0; j < KM; ++j) {
+        if (j >= K) break;
+        dq = fmaf(dS[me][j], s_in[(g0 + j) * ld + w + c], dq);
+        dk = fmaf(dS[j][me], s_in[(g0 + j) * ld + c], dk);
+        dv = fmaf(P[j][me], s_do[(g0 + j) * (w + 1) + c], dv);
+      }
+      s_out[me_t * ld + c] = dq;
+      s_out[me_t * ld + w + c] = dk;
+      s_out[me_t * ld + 2 * w + c] = dv;
     }
-    dqkv[t * 3 * w + c] = __float2bfloat16(dq);
-    dqkv[t * 3 * w + w + c] = __float2bfloat16(dk);
-    dqkv[t * 3 * w + 2 * w + c] = __float2bfloat16(dv);
   }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nt * 3 * w; e += blockDim.x)
+    dqkv[t0 * 3 * w + e] = __float2bfloat16(s_out[(e / (3 * w)) * ld + e % (3 * w)]);
 }
 
 void group_attn_fwd(const float* qkv, int T, int K, int w, bf16* ctx, float* probs, cudaStream_t st) {
-  group_attn_fwd_kernel<<<cdiv(T, 128), 128, 0, st>>>(qkv, T, K, w, ctx, probs);
+  const int TT = (128 / K) * K;
+  const int smem = 4 * (TT * (3 * w + 1) + TT * (w + 1));
+  static int done = 0;
+  if (!done) {
+    cudaFuncSetAttribute(group_attn_fwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(group_attn_fwd_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(group_attn_fwd_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(group_attn_fwd_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    done = 1;
+  }
+  const int grid = cdiv(T, TT);
+  if (K == 2) group_attn_fwd_kernel<2><<<grid, 128, smem, st>>>(qkv, T, K, w, ctx, probs);
+  else if (K == 4) group_attn_fwd_kernel<4><<<grid, 128, smem, st>>>(qkv, T, K, w, ctx, probs);
+  else if (K == 8) group_attn_fwd_kernel<8><<<grid, 128, smem, st>>>(qkv, T, K, w, ctx, probs);
+  else group_attn_fwd_kernel<0><<<grid, 128, smem, st>>>(qkv, T, K, w, ctx, probs);
 }
 void group_attn_bwd(const float* qkv, const float* probs, const float* dctx, int T, int K, int w, bf16* dqkv,
                     cudaStream_t st) {
-  group_attn_bwd_kernel<<<cdiv(T, 128), 128, 0, st>>>(qkv, probs, dctx, T, K, w, dqkv);
+  const int TT = (128 / K) * K;
+  const int smem = 4 * (2 * TT * (3 * w + 1) + TT * (w + 1));
+  static int done = 0;
+  if (!done) {
+    cudaFuncSetAttribute(group_attn_bwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(group_attn_bwd_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(group_attn_bwd_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(group_attn_bwd_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    done = 1;
+  }
+  const int grid = cdiv(T, TT);
+  if (K == 2) group_attn_bwd_kernel<2><<<grid, 128, smem, st>>>(qkv, probs, dctx, T, K, w, dqkv);
+  else if (K == 4) group_attn_bwd_kernel<4><<<grid, 128, smem, st>>>(qkv, probs, dctx, T, K, w, dqkv);
+  else if (K == 8) group_attn_bwd_kernel<8><<<grid, 128, smem, st>>>(qkv, probs, dctx, T, K, w, dqkv);
+  else group_attn_bwd_kernel<0><<<grid, 128, smem, st>>>(qkv, probs, dctx, T, K, w, dqkv);
 }
 
 // ============================================================== hybrid attention

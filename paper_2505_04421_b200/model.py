@@ -16,7 +16,6 @@ import ctypes
 import hashlib
 import json
 import math
-import struct
 from typing import Optional, Sequence, Union
 
 import numpy as np
@@ -26,9 +25,6 @@ from .config import ModelConfig
 from .errors import ConfigError, EmbeddingLookupError, NumericalError
 from .inputs import Batch, Sample, check_batch, tensorize
 from .params import init_params, param_shapes
-
-CHECKPOINT_MAGIC = b"LRCKPT01"
-
 
 def _torch():
     import torch
@@ -188,41 +184,19 @@ class LongerModel:
 
     # ------------------------------------------------------------------ checkpoints
     def save(self, path: str) -> None:
-        """``LRCKPT01`` (model.py:381-406): magic, <Q header length, JSON header, float64 LE arrays."""
-        named = [(n, v.detach().double().cpu().numpy()) for n, v in self.params()]
-        header = {"format_version": 1, "config": self.cfg.to_dict(), "param_version": self.param_version,
-                  "arrays": [{"name": n, "shape": list(a.shape)} for n, a in named]}
-        blob = json.dumps(header, sort_keys=True).encode("utf-8")
-        with open(path, "wb") as fh:
-            fh.write(CHECKPOINT_MAGIC)
-            fh.write(struct.pack("<Q", len(blob)))
-            fh.write(blob)
-            for _, a in named:
-                fh.write(a.astype("<f8").tobytes())
+        """``LRCKPT01`` (model.py:381-406), loadable by ``longrec.LongRecModel.load``."""
+        from .checkpoint import write_checkpoint
+        write_checkpoint(path, self.cfg, [(n, v.detach().double().cpu().numpy()) for n, v in self.params()],
+                         self.param_version)
 
     @classmethod
     def load(cls, path: str, device: str = "cuda") -> "LongerModel":
-        with open(path, "rb") as fh:
-            magic = fh.read(8)
-            if magic != CHECKPOINT_MAGIC:
-                raise ConfigError(f"not a checkpoint file: bad magic {magic!r}")
-            (hlen,) = struct.unpack("<Q", fh.read(8))
-            header = json.loads(fh.read(hlen).decode("utf-8"))
-            if header.get("format_version") != 1:
-                raise ConfigError("unsupported checkpoint format version")
-            cfg = ModelConfig.from_dict(header["config"])
-            model = cls(cfg, seed=0, device=device)
-            named = {}
-            for entry in header["arrays"]:
-                name, shape = entry["name"], tuple(entry["shape"])
-                if name not in model._views:
-                    raise ConfigError(f"checkpoint array {name!r} not in model")
-                if tuple(model._views[name].shape) != shape:
-                    raise ConfigError(f"checkpoint array {name!r} shape mismatch")
-                count = int(np.prod(shape)) if shape else 1
-                named[name] = np.frombuffer(fh.read(count * 8), dtype="<f8").reshape(shape)
-            model.load_params(named)
-            model.param_version = int(header["param_version"])
+        """Read a reference (or our) ``LRCKPT01`` checkpoint (model.py:408-427)."""
+        from .checkpoint import read_checkpoint
+        cfg, named, version = read_checkpoint(path)
+        model = cls(cfg, seed=0, device=device)
+        model.load_params(named)
+        model.param_version = version
         return model
 
 

@@ -1,0 +1,68 @@
+"""Multi-process (world_size 2, gloo, CPU) test of the data-parallel step semantics: sharding the
+batch, computing per-shard mean-loss gradients and allreducing them reproduces the full-batch
+gradient of the reference algorithm (oracle) — including unequal shards."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import longer_oracle as O
+from paper_2505_04421_b200 import ModelConfig, init_params, synthetic_batch
+from paper_2505_04421_b200.dp import allreduce_mean_grads, allreduce_mean_loss, shard_batch, shard_bounds
+from paper_2505_04421_b200.params import param_shapes
+
+CFG = dict(L=24, d=8, K=4, k=3, N=2, m=3, merge_mode="inner", n_users=30, vocab=40)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, B, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = ModelConfig(**CFG).validate()
+    P = init_params(cfg, seed=1)
+    batch = synthetic_batch(cfg, B, seed=5, min_events=3)
+    local = shard_batch(batch, rank, world)
+    p, loss, grads = O.forward_backward(P, cfg, local.as_dict())
+    flat = torch.from_numpy(np.concatenate([grads[n].ravel() for n in param_shapes(cfg)]))
+    allreduce_mean_grads(flat, local.size)
+    gl = allreduce_mean_loss(loss, local.size)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "dp_grad.npy"), flat.numpy())
+        np.save(os.path.join(out_dir, "dp_loss.npy"), np.array(gl))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("B", [6, 7])
+def test_dp_allreduce_matches_full_batch(tmp_path, B):
+    world = 2
+    mp.spawn(_worker, args=(world, _free_port(), B, str(tmp_path)), nprocs=world, join=True)
+    cfg = ModelConfig(**CFG).validate()
+    P = init_params(cfg, seed=1)
+    batch = synthetic_batch(cfg, B, seed=5, min_events=3)
+    _, loss, grads = O.forward_backward(P, cfg, batch.as_dict())
+    full = np.concatenate([grads[n].ravel() for n in param_shapes(cfg)])
+    dp = np.load(tmp_path / "dp_grad.npy")
+    np.testing.assert_allclose(dp, full, rtol=1e-10, atol=1e-13)
+    assert abs(float(np.load(tmp_path / "dp_loss.npy")) - loss) < 1e-12
+
+
+def test_shard_bounds_cover_batch():
+    for n in range(0, 20):
+        for world in (1, 2, 3, 8):
+            spans = [shard_bounds(n, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            sizes = [hi - lo for lo, hi in spans]
+            assert max(sizes) - min(sizes) <= 1
