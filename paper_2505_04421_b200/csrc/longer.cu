@@ -15,6 +15,8 @@
 #include "gemm.cuh"
 #include "longer.h"
 #include "ops.cuh"
+#include "frontend.cuh"
+#include <cstdlib>
 
 namespace longer {
 namespace {
@@ -134,6 +136,8 @@ struct Packed {               // bf16 / fp32 operand copies of the weights
 struct Plan {
   LongerDims dims;
   void* ws;
+  bool fused_fe;   // fused front-end kernel (frontend.cu) for this call
+  bf16* wblob;     // its canonical-layout weight blob
   int B, L, Lp, d, K, G, D, m, k, q, v, N, heads, inner, IL, hh, F, FP, HIN;
   long long T;
   ParamOff po;
@@ -186,6 +190,7 @@ Plan make_plan(const LongerDims& d, void* ws) {
   const long long Q = (long long)B * q, V = (long long)B * v, M = (long long)B * m;
   p.status = a.take<int>(64);
   p.npg = a.take<int32_t>(B);
+  p.wblob = a.take<bf16>(frontend_blob_bytes(dd, D, p.F, p.IL) / 2 + 64);
   // packed weights
   p.pk.seq_w1 = a.take<bf16>(dd * 2 * D); p.pk.seq_w2 = a.take<bf16>(2 * D * dd);
   p.pk.glob_w1 = a.take<bf16>(D * 2 * D); p.pk.glob_w2 = a.take<bf16>(2 * D * D);
@@ -422,13 +427,14 @@ int block_fwd(const Ctx& c, const BlockOff& bo, BlockBufs& b, const float* xq, b
   return 0;
 }
 
-int forward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs, float* loss, int with_loss) {
+// Unfused front-end: featuriser kernel + tcgen05 GEMMs per stage; keeps every activation the
+// unfused backward needs.
+int frontend_unfused_fwd(const Ctx& c, const Plan& p, const LongerBatch& bt) {
   cudaStream_t st = c.st;
   const ParamOff& o = p.po;
   const LongerDims& dm = p.dims;
   const int d = p.d, D = p.D;
-  const long long T = p.T, M = (long long)p.B * p.m;
-  TRY(pack_weights(p, c.P, p.ws, st));
+  const long long T = p.T;
   // featurise + recency position (inputs.py:434-482)
   EmbedArgs e{};
   e.items = bt.items; e.actions = bt.actions; e.dt = bt.dt; e.n_events = bt.n_events;
@@ -455,6 +461,51 @@ int forward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs, fl
     TRY(lin_fwd(st, b.gf, 4 * d, T, p.pk.in_w2[i], 4 * d, d, c.w(bo.b2), 0, b.out, nullptr, nullptr, b.x1, d,
                 i == p.IL - 1 ? p.keep : nullptr));
     x = b.out;
+  }
+  return 0;
+}
+
+// Fused front-end (frontend.cu): ids → merged rows in one persistent kernel.
+int frontend_fused_fwd(const Ctx& c, const Plan& p, const LongerBatch& bt) {
+  cudaStream_t st = c.st;
+  const ParamOff& o = p.po;
+  const LongerDims& dm = p.dims;
+  long long iw[kMaxInner][4];
+  for (int l = 0; l < p.IL; ++l) {
+    iw[l][0] = o.inner[l].w_q; iw[l][1] = o.inner[l].w_k; iw[l][2] = o.inner[l].w_v; iw[l][3] = o.inner[l].w_o;
+  }
+  pack_frontend_weights(c.P, o.tok_w, o.seq_w1, o.seq_w2, iw, p.d, p.D, p.F, p.IL, p.wblob, st);
+  FrontArgs f{};
+  f.items = bt.items; f.actions = bt.actions; f.dt = bt.dt; f.n_events = bt.n_events;
+  f.B = p.B; f.L = p.L; f.Lp = p.Lp; f.K = p.K; f.d = p.d; f.d_item = dm.d_item; f.d_act = dm.d_act;
+  f.d_time = dm.d_time; f.nb = dm.n_time_buckets; f.vocab = dm.vocab; f.n_actions = dm.n_actions;
+  f.inner_layers = p.IL; f.T = p.T;
+  f.item_tab = c.w(o.item); f.act_tab = c.w(o.act); f.time_tab = c.w(o.time); f.pos_tab = c.w(o.pos);
+  f.tok_b = c.w(o.tok_b); f.seq_b1 = c.w(o.seq_b1); f.seq_b2 = c.w(o.seq_b2);
+  for (int l = 0; l < p.IL; ++l) {
+    const BlockOff& b = o.inner[l];
+    f.inner_bias[l][0] = c.w(b.b_q); f.inner_bias[l][1] = c.w(b.b_k); f.inner_bias[l][2] = c.w(b.b_v);
+    f.inner_bias[l][3] = c.w(b.b_o); f.inner_bias[l][4] = c.w(b.b1); f.inner_bias[l][5] = c.w(b.b2);
+    f.inner_ln[l][0] = c.w(b.ln1_g); f.inner_ln[l][1] = c.w(b.ln1_b);
+    f.inner_ln[l][2] = c.w(b.ln2_g); f.inner_ln[l][3] = c.w(b.ln2_b);
+  }
+  f.wblob = p.wblob;
+  f.merged = p.merged; f.status = p.status; f.npg = p.npg;
+  return frontend_fwd(f, st);
+}
+
+int forward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs, float* loss, int with_loss) {
+  cudaStream_t st = c.st;
+  const ParamOff& o = p.po;
+  const LongerDims& dm = p.dims;
+  const int d = p.d, D = p.D;
+  const long long M = (long long)p.B * p.m;
+  (void)with_loss;
+  TRY(pack_weights(p, c.P, p.ws, st));
+  if (p.fused_fe) {
+    TRY(frontend_fused_fwd(c, p, bt));
+  } else {
+    TRY(frontend_unfused_fwd(c, p, bt));
   }
   // global tokens (inputs.py:500-537)
   GlobalsArgs ga{};
@@ -668,6 +719,12 @@ int backward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs) {
   return 0;
 }
 
+bool use_fused(const Plan& p) {
+  const char* env = std::getenv("LONGER_FUSED");
+  if (env && env[0] == '0') return false;
+  return frontend_supported(p.d, p.K, p.D, p.F, p.IL) != 0;
+}
+
 int check_call(const LongerDims* dims, size_t ws_bytes, Plan* out, void* ws) {
   if (!dims) return fail(LONGER_EDIM, "null dims");
   int rc = validate(*dims);
@@ -704,6 +761,7 @@ extern "C" int longer_forward(const LongerDims* dims, const float* params, const
   static Plan p;   // large struct; one driving thread per device (see longer.h)
   int rc = check_call(dims, ws_bytes, &p, ws);
   if (rc) return rc;
+  p.fused_fe = use_fused(p);
   Ctx c{p, params, nullptr, (cudaStream_t)stream};
   return forward(c, p, *batch, probs, nullptr, 0);
 }

@@ -86,7 +86,7 @@ def test_forward_backward_matches_reference_golden(path):
     assert_grads_close(grads, G, os.path.basename(path))
     # inference entry point agrees with the training forward
     p2 = model.forward(batch).cpu().numpy()
-    np.testing.assert_allclose(p2, p, rtol=0, atol=1e-6)
+    np.testing.assert_allclose(p2, p, rtol=0, atol=2e-3)   # fused vs unfused front-end
 
 
 C2 = dict(L=2000, d=32, K=4, k=32, N=2, m=3, merge_mode="inner")
@@ -112,3 +112,6 @@ def test_matches_oracle_on_synthetic(kw, B, min_events):
     assert np.max(np.abs(p - p_ref)) <= 5e-3
     assert abs(loss - loss_ref) <= loss_tol(p_ref, batch.label)
     assert_grads_close(grads, G, str(kw))
+    # inference entry point (fused front-end when the shape allows it)
+    pf = model.forward(batch).cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(pf - p_ref)) <= 5e-3, np.abs(pf - p_ref)
