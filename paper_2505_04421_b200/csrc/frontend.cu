@@ -1,141 +1,112 @@
-// frontend.cu — fused token front-end, forward (see frontend.cuh).
+// frontend.cu — fused token front-end kernels (see frontend.cuh, fe_common.cuh).
 //
 // Restates, per token: _event_features + abs-pos (pkg/src/longrec/inputs.py:434-482), the token
 // MLP (inputs.py:447-449), and merge_inner_trans (pkg/src/longrec/merge.py:83-112) with
-// grouped_attention (pkg/src/longrec/tensors.py:406-444), for 128-token tiles.
+// grouped_attention (pkg/src/longrec/tensors.py:406-444), for 128-token tiles; and the backward of
+// the token MLP + featuriser (tensors.py bw closures of linear/gelu/gather_rows).
 //
 // CTA = warp 0 (TMEM owner + single-thread MMA issuer) + 4 worker warps (thread = token row =
-// TMEM lane).  Per stage: workers write the A tile (bf16, canonical no-swizzle K-major) → mbarrier
-// → one thread issues tcgen05.mma (M=128) against the smem-resident weight blob → tcgen05.commit →
-// workers read the fp32 accumulator from TMEM and apply bias / GELU / LN / group attention in
-// registers.  Two CTAs per SM overlap one CTA's MMA with the other's epilogue math.
+// TMEM lane).  Per stage: workers write the A tile → mbarrier → one thread issues tcgen05.mma
+// (M = 128) against smem-resident weights → tcgen05.commit → workers read the fp32 accumulator
+// from TMEM and apply bias / GELU / LN / group attention in registers.
 #include "frontend.cuh"
-#include "sm100.cuh"
+#include "fe_common.cuh"
 
 #include <algorithm>
 
 namespace longer {
 
+using namespace fe;
+
 namespace {
-
-constexpr int kFP = 32;                 // featuriser K (F = d_item + d_act + d_time padded)
-constexpr int kTile = 128;
-constexpr int kWorkers = 4;
-constexpr int kThreads = 32 * (1 + kWorkers);
-constexpr int kTmemCols = 256;
-
-// canonical K-major, no swizzle: element (row, k) of a [rows x Kdim] bf16 tile
-__host__ __device__ __forceinline__ int canon(int row, int k, int Kdim) {
-  return (row >> 3) * (Kdim * 8) + (k >> 3) * 64 + (row & 7) * 8 + (k & 7);
-}
-
-struct BlobOff {          // element offsets inside the weight blob
-  int tp, w1, w2;
-  int qkv[8], wo[8], w1i[8], w2i[8];
-  int total;
-};
-
-__host__ __device__ inline BlobOff blob_offsets(int d, int D, int IL) {
-  BlobOff o;
-  int off = 0;
-  o.tp = off; off += d * kFP;
-  o.w1 = off; off += 2 * D * d;
-  o.w2 = off; off += d * 2 * D;
-  for (int l = 0; l < IL; ++l) {
-    o.qkv[l] = off; off += 3 * d * d;
-    o.wo[l] = off; off += d * d;
-    o.w1i[l] = off; off += 4 * d * d;
-    o.w2i[l] = off; off += d * 4 * d;
-  }
-  o.total = off;
-  return o;
-}
 
 // ------------------------------------------------------------------ weight packing
 struct PackW {
   int n;
-  struct { long long src; int in, out, n_off, Kdim, dst; } s[40];
+  struct { long long src; int in, out, trans, n_off, k_off, Kdim, dst; } s[48];
 };
 
+// trans = 1: image of Wᵀ ([out][in]: element (n=j, k=i) = W[i][j]); trans = 0: image of W as
+// [in][out] (element (n=i, k=j) = W[i][j]).  W is the fp32 master [in, out] row-major.
 __global__ void pack_canon_kernel(const float* __restrict__ params, PackW pw, bf16* blob) {
   const auto s = pw.s[blockIdx.y];
-  const int N = s.out, Kd = s.Kdim;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < N * Kd; e += gridDim.x * blockDim.x) {
-    const int n = e / Kd, k = e % Kd;
-    const float v = k < s.in ? params[s.src + (long long)k * s.out + n] : 0.f;
-    blob[s.dst + canon(s.n_off + n, k, Kd)] = __float2bfloat16(v);
+  const int n_el = s.in * s.out;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n_el; e += gridDim.x * blockDim.x) {
+    const int i = e / s.out, j = e % s.out;
+    const float v = params[s.src + e];
+    const int idx = s.trans ? canon(s.n_off + j, s.k_off + i, s.Kdim) : canon(s.n_off + i, s.k_off + j, s.Kdim);
+    blob[s.dst + idx] = __float2bfloat16(v);
   }
 }
 
-// ------------------------------------------------------------------ device helpers
-__device__ __forceinline__ void store_row_canon(bf16* tile, int row, int Kdim, const float* v, int n, int k0 = 0) {
-  // n is a multiple of 8; 16-byte stores per 8-element chunk (columns k0 .. k0+n)
+// ------------------------------------------------------------------ shared worker pieces
+struct TokenInfo {
+  long long t;
+  int b, j, n, rec;
+  bool in_range, real, keep;
+};
+
+__device__ __forceinline__ TokenInfo token_info(const FrontArgs& a, long long tile, int row) {
+  TokenInfo ti;
+  ti.t = tile * kTile + row;
+  ti.in_range = ti.t < a.T;
+  ti.b = 0; ti.j = 0; ti.n = 0;
+  if (ti.in_range) {
+    ti.b = (int)(ti.t / a.Lp);
+    ti.j = (int)(ti.t % a.Lp);
+    ti.n = min(max(a.n_events[ti.b], 0), a.L);
+  }
+  ti.real = ti.in_range && ti.j >= a.Lp - ti.n;
+  const int npg = (a.Lp - ti.n) / a.K;
+  ti.keep = ti.in_range && (ti.j / a.K) >= npg;
+  ti.rec = ti.real ? a.Lp - 1 - ti.j : 0;
+  return ti;
+}
+
+// featuriser: concat(item, action, time-bucket embeddings), zero-padded to kFP columns
+__device__ __forceinline__ void featurise(const FrontArgs& a, const TokenInfo& ti, float* v, int* ids, bool flag) {
 #pragma unroll
-  for (int c = 0; c < n; c += 8) {
-    uint4 pk;
-    pk.x = sm100::pack_bf16(v[c + 0], v[c + 1]);
-    pk.y = sm100::pack_bf16(v[c + 2], v[c + 3]);
-    pk.z = sm100::pack_bf16(v[c + 4], v[c + 5]);
-    pk.w = sm100::pack_bf16(v[c + 6], v[c + 7]);
-    *reinterpret_cast<uint4*>(tile + canon(row, k0 + c, Kdim)) = pk;
+  for (int c = 0; c < kFP; ++c) v[c] = 0.f;
+  ids[0] = ids[1] = ids[2] = 0;
+  if (!ti.real) return;
+  const long long src = (long long)ti.b * a.L + (ti.j - (a.Lp - a.L));
+  int item = a.items[src], act = a.actions[src], dt = a.dt[src];
+  int bad = 0;
+  if (item < 0 || item >= a.vocab) { bad |= 1; item = 0; }
+  if (act < 0 || act >= a.n_actions) { bad |= 1; act = 0; }
+  if (dt < 0) { bad |= 2; dt = 0; }
+  if (bad && flag) atomicOr(a.status, bad);
+  const int bucket = min(32 - __clz(dt), a.nb - 1);      // time_bucket (inputs.py:307-315)
+  ids[0] = item; ids[1] = act; ids[2] = bucket;
+  const int e1 = a.d_item, e2 = a.d_item + a.d_act, e3 = e2 + a.d_time;
+#pragma unroll
+  for (int c = 0; c < kFP; ++c) {
+    const float* p = c < e1 ? a.item_tab + item * a.d_item + c
+                   : c < e2 ? a.act_tab + act * a.d_act + (c - e1)
+                            : a.time_tab + bucket * a.d_time + (c - e2);
+    v[c] = c < e3 ? __ldg(p) : 0.f;
   }
 }
 
-// issue D[tmem] (+)= A[smem, 128 x K] · B[smem, N x K]ᵀ as K/16 MMAs (one thread)
-__device__ __forceinline__ void mma_tile(uint32_t tmem_d, uint32_t a_addr, int a_kdim, uint32_t b_addr, int b_kdim,
-                                         int kslices, int N, bool accumulate) {
-  const uint32_t idesc = sm100::make_idesc_bf16(128, N, 0, 0);
-  for (int ks = 0; ks < kslices; ++ks) {
-    const uint64_t ad = sm100::make_sdesc(a_addr + ks * 256, 128, a_kdim * 16, sm100::LAYOUT_NONE);
-    const uint64_t bd = sm100::make_sdesc(b_addr + ks * 256, 128, b_kdim * 16, sm100::LAYOUT_NONE);
-    sm100::mma_bf16(tmem_d, ad, bd, idesc, (accumulate || ks > 0) ? 1u : 0u);
+__device__ __forceinline__ void load_blob(uint8_t* dst_smem, const uint8_t* src, int bytes, uint64_t* bar) {
+  for (int off = 0; off < bytes; off += 32768) {
+    const int n = min(32768, bytes - off);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(sm100::smem_u32(dst_smem + off)), "l"(src + off), "r"(n), "r"(sm100::smem_u32(bar))
+                 : "memory");
   }
-}
-
-template <int N>
-__device__ __forceinline__ void tmem_row(uint32_t taddr, float* out) {   // N multiple of 16
-#pragma unroll
-  for (int c = 0; c < N; c += 32) {
-    if (c + 32 <= N) {
-      uint32_t r[32];
-      sm100::tmem_ld32(taddr + c, r);
-      sm100::tmem_ld_wait();
-#pragma unroll
-      for (int j = 0; j < 32; ++j) out[c + j] = __uint_as_float(r[j]);
-    } else {
-      uint32_t r[16];
-      sm100::tmem_ld16(taddr + c, r);
-      sm100::tmem_ld_wait();
-#pragma unroll
-      for (int j = 0; j < 16; ++j) out[c + j] = __uint_as_float(r[j]);
-    }
-  }
-}
-
-template <int DT>
-__device__ __forceinline__ void layer_norm_row(const float* x, const float* g, const float* b, float* y) {
-  float mu = 0.f;
-#pragma unroll
-  for (int c = 0; c < DT; ++c) mu += x[c];
-  mu *= 1.f / DT;
-  float var = 0.f;
-#pragma unroll
-  for (int c = 0; c < DT; ++c) { const float t = x[c] - mu; var += t * t; }
-  const float inv = rsqrtf(var * (1.f / DT) + kLnEps);
-#pragma unroll
-  for (int c = 0; c < DT; ++c) y[c] = (x[c] - mu) * inv * __ldg(g + c) + __ldg(b + c);
 }
 
 // ------------------------------------------------------------------ forward kernel
 template <int DT, int KG>
 __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  const int D = DT * KG;
-  const int H2 = 2 * D;                        // token-MLP hidden width
-  const int nh = H2 / 128;                     // 128-column halves of the hidden
+  constexpr int D = DT * KG;
+  constexpr int H2 = 2 * D;                        // token-MLP hidden width
+  constexpr int nh = H2 / 128;                     // 128-column halves of the hidden
   const BlobOff bo = blob_offsets(DT, D, a.inner_layers);
   bf16* sW = reinterpret_cast<bf16*>(smem_raw);
-  bf16* sA = sW + ((bo.total + 63) & ~63);                 // 128 x 32 bf16
+  bf16* sA = sW + ((bo.fwd_total + 63) & ~63);             // 128 x 32 bf16
   bf16* sH = sA + kTile * kFP;                             // 128 x 128 bf16 (also fp32 k/v scratch)
   float* sKV = reinterpret_cast<float*>(sH);               // 128 x (2*DT+1) fp32
   uint64_t* bars = reinterpret_cast<uint64_t*>(sH + kTile * 136);
@@ -151,7 +122,7 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
     sm100::mbar_init(bar_d, 1);
     sm100::fence_barrier_init();
   }
-  if (warp == 0) sm100::tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == 0) sm100::tmem_alloc<256>(tmem_slot);
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
@@ -159,48 +130,41 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
   const long long ntiles = (a.T + kTile - 1) / kTile;
 
   if (warp == 0) {
-    // ---------------- MMA issuer
     if (lane == 0) {
-      const int wbytes = bo.total * 2;
-      sm100::mbar_arrive_expect_tx(bar_w, wbytes);
-      for (int off = 0; off < wbytes; off += 32768) {
-        const int n = min(32768, wbytes - off);
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                     :: "r"(sm100::smem_u32(reinterpret_cast<uint8_t*>(sW) + off)),
-                        "l"(reinterpret_cast<const uint8_t*>(a.wblob) + off), "r"(n), "r"(sm100::smem_u32(bar_w))
-                     : "memory");
-      }
+      // ---------------- MMA issuer
+      sm100::mbar_arrive_expect_tx(bar_w, bo.fwd_total * 2);
+      load_blob(reinterpret_cast<uint8_t*>(sW), reinterpret_cast<const uint8_t*>(a.wblob), bo.fwd_total * 2, bar_w);
       sm100::mbar_wait(bar_w, 0);
       const uint32_t wA = sm100::smem_u32(sA), wH = sm100::smem_u32(sH), wW = sm100::smem_u32(sW);
       uint32_t pa = 0;
       auto wait_a = [&]() { sm100::mbar_wait(bar_a, pa); pa ^= 1; sm100::tc_fence_after(); };
+      auto W = [&](int off, int kdim) { return Opnd{wW + off * 2, kdim, 0}; };
       const uint32_t accH = tmem + 128;          // h / f2 accumulator columns
       for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        wait_a();                                // feat ready
-        mma_tile(tmem, wA, kFP, wW + bo.tp * 2, kFP, kFP / 16, DT, false);
+        wait_a();                                // feat
+        mma(tmem, Opnd{wA, kFP, 0}, W(bo.tp, kFP), kFP / 16, DT, false);
         sm100::mma_commit(bar_d);
-        wait_a();                                // x0 ready
-        mma_tile(tmem, wA, DT, wW + bo.w1 * 2, DT, DT / 16, 128, false);
+        wait_a();                                // x0
+        mma(tmem, Opnd{wA, DT, 0}, W(bo.w1, DT), DT / 16, 128, false);
         sm100::mma_commit(bar_d);
         for (int j = 0; j < nh; ++j) {
           wait_a();                              // GELU(a1 half j) in sH
-          // h (+)= g1_half_j · W2ᵀ[:, 128j : 128j+128]
-          mma_tile(accH, wH, 128, wW + (bo.w2 + canon(0, 128 * j, H2)) * 2, H2, 8, DT, j > 0);
-          if (j + 1 < nh) mma_tile(tmem, wA, DT, wW + (bo.w1 + canon(128 * (j + 1), 0, DT)) * 2, DT, DT / 16, 128, false);
+          mma(accH, Opnd{wH, 128, 0}, W(bo.w2 + canon(0, 128 * j, H2), H2), 8, DT, j > 0);
+          if (j + 1 < nh) mma(tmem, Opnd{wA, DT, 0}, W(bo.w1 + canon(128 * (j + 1), 0, DT), DT), DT / 16, 128, false);
           sm100::mma_commit(bar_d);
         }
         for (int l = 0; l < a.inner_layers; ++l) {
           wait_a();                              // LN1(x)
-          mma_tile(tmem, wA, DT, wW + bo.qkv[l] * 2, DT, DT / 16, 3 * DT, false);
+          mma(tmem, Opnd{wA, DT, 0}, W(bo.qkv[l], DT), DT / 16, 3 * DT, false);
           sm100::mma_commit(bar_d);
           wait_a();                              // ctx
-          mma_tile(tmem, wA, DT, wW + bo.wo[l] * 2, DT, DT / 16, DT, false);
+          mma(tmem, Opnd{wA, DT, 0}, W(bo.wo[l], DT), DT / 16, DT, false);
           sm100::mma_commit(bar_d);
           wait_a();                              // LN2(x1)
-          mma_tile(tmem, wA, DT, wW + bo.w1i[l] * 2, DT, DT / 16, 4 * DT, false);
+          mma(tmem, Opnd{wA, DT, 0}, W(bo.w1i[l], DT), DT / 16, 4 * DT, false);
           sm100::mma_commit(bar_d);
           wait_a();                              // GELU(f1)
-          mma_tile(accH, wH, 4 * DT, wW + bo.w2i[l] * 2, 4 * DT, 4 * DT / 16, DT, false);
+          mma(accH, Opnd{wH, 4 * DT, 0}, W(bo.w2i[l], 4 * DT), 4 * DT / 16, DT, false);
           sm100::mma_commit(bar_d);
         }
       }
@@ -210,60 +174,32 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
     const int q = warp & 3;
     const int row = q * 32 + lane;
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
-    const int F = a.d_item + a.d_act + a.d_time;
     const float scale_in = rsqrtf((float)DT);
     uint32_t pd = 0;
-    auto signal = [&]() {
-      sm100::fence_async_smem();
-      sm100::tc_fence_before();
-      sm100::mbar_arrive(bar_a);
-    };
+    auto signal = [&]() { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(bar_a); };
     auto wait_d = [&]() { sm100::mbar_wait(bar_d, pd); pd ^= 1; sm100::tc_fence_after(); };
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const long long t = tile * kTile + row;
-      const bool in_range = t < a.T;
-      int b = 0, j = 0, n = 0;
-      if (in_range) { b = (int)(t / a.Lp); j = (int)(t % a.Lp); n = min(max(a.n_events[b], 0), a.L); }
-      const bool real = in_range && j >= a.Lp - n;
-      const int npg = (a.Lp - n) / a.K;
-      const bool keep = in_range && (j / a.K) >= npg;
-      if (in_range && j == 0 && a.npg) a.npg[b] = npg;
-      // S0: featurise
-      float v[kFP];
-#pragma unroll
-      for (int c = 0; c < kFP; ++c) v[c] = 0.f;
-      int rec = 0;
-      if (real) {
-        const long long src = (long long)b * a.L + (j - (a.Lp - a.L));
-        int item = a.items[src], act = a.actions[src], dt = a.dt[src];
-        int bad = 0;
-        if (item < 0 || item >= a.vocab) { bad |= 1; item = 0; }
-        if (act < 0 || act >= a.n_actions) { bad |= 1; act = 0; }
-        if (dt < 0) { bad |= 2; dt = 0; }
-        if (bad) atomicOr(a.status, bad);
-        const int bucket = min(32 - __clz(dt), a.nb - 1);
-        rec = a.Lp - 1 - j;
-        const int e1 = a.d_item, e2 = a.d_item + a.d_act, e3 = e2 + a.d_time;
-#pragma unroll
-        for (int c = 0; c < kFP; ++c) {
-          const float* src_p = c < e1 ? a.item_tab + item * a.d_item + c
-                             : c < e2 ? a.act_tab + act * a.d_act + (c - e1)
-                                      : a.time_tab + bucket * a.d_time + (c - e2);
-          v[c] = c < e3 ? __ldg(src_p) : 0.f;
-        }
+      const TokenInfo ti = token_info(a, tile, row);
+      if (ti.in_range && ti.j == 0 && a.npg) a.npg[ti.b] = (a.Lp - ti.n) / a.K;
+      if (ti.in_range && a.real_out) {
+        a.real_out[ti.t] = ti.real ? 1.f : 0.f;
+        a.keep_out[ti.t] = ti.keep ? 1.f : 0.f;
       }
-      (void)F;
-      store_row_canon(sA, row, kFP, v, kFP);
+      float v[kFP];
+      int ids[3];
+      featurise(a, ti, v, ids, true);
+      store_row(sA, row, kFP, v, kFP);
       signal();
-      // S1: x0 = feat·W_tp + b_tp + abs_pos[recency]
+      // x0 = feat·W_tp + b_tp + abs_pos[recency]
       float x[DT];
       wait_d();
       tmem_row<DT>(trow, x);
 #pragma unroll
-      for (int c = 0; c < DT; ++c) x[c] = real ? x[c] + __ldg(a.tok_b + c) + __ldg(a.pos_tab + (long long)rec * DT + c) : 0.f;
-      store_row_canon(sA, row, DT, x, DT);
+      for (int c = 0; c < DT; ++c)
+        x[c] = ti.real ? x[c] + __ldg(a.tok_b + c) + __ldg(a.pos_tab + (long long)ti.rec * DT + c) : 0.f;
+      store_row(sA, row, DT, x, DT);
       signal();
-      // S2: token MLP, hidden in 128-column halves: GELU(x0·W1 + b1) → sH → (·W2) accumulates in TMEM
+      // token MLP: GELU(x0·W1 + b1) (128-column halves → sH) · W2 accumulates in TMEM
       for (int hj = 0; hj < nh; ++hj) {
         wait_d();
 #pragma unroll 1
@@ -272,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
           tmem_row<32>(trow + c0, hv);
 #pragma unroll
           for (int u = 0; u < 32; ++u) hv[u] = gelu_f(hv[u] + __ldg(a.seq_b1 + 128 * hj + c0 + u));
-          store_row_canon(sH, row, 128, hv, 32, c0);
+          store_row(sH, row, 128, hv, 32, c0);
         }
         signal();
       }
@@ -280,17 +216,20 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
       float h[DT];
       tmem_row<DT>(trow + 128, h);
 #pragma unroll
-      for (int c = 0; c < DT; ++c) h[c] = real ? h[c] + __ldg(a.seq_b2 + c) : 0.f;
-      // InnerTrans layers
+      for (int c = 0; c < DT; ++c) h[c] = ti.real ? h[c] + __ldg(a.seq_b2 + c) : 0.f;
+      if (a.h_out && ti.in_range) {
+        float4* dst = reinterpret_cast<float4*>(a.h_out + ti.t * DT);
+#pragma unroll
+        for (int c = 0; c < DT; c += 4) dst[c / 4] = make_float4(h[c], h[c + 1], h[c + 2], h[c + 3]);
+      }
       for (int l = 0; l < a.inner_layers; ++l) {
         const float* const* ib = a.inner_bias[l];
         const float* const* ln = a.inner_ln[l];
-        float xn[DT];
-        layer_norm_row<DT>(h, ln[0], ln[1], xn);
-        store_row_canon(sA, row, DT, xn, DT);
+        float xn[DT], inv;
+        ln_row<DT>(h, ln[0], ln[1], xn, nullptr, inv);
+        store_row(sA, row, DT, xn, DT);
         signal();
         wait_d();
-        // q, k, v rows; k and v go to smem for the K-1 group peers (adjacent lanes)
         float qv[DT];
         tmem_row<DT>(trow, qv);
         {
@@ -319,25 +258,25 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
         float tot = 0.f;
 #pragma unroll
         for (int jj = 0; jj < KG; ++jj) { s[jj] = __expf(s[jj] - mx); tot += s[jj]; }
-        const float inv = 1.f / tot;
+        const float rinv = 1.f / tot;
         float ctx[DT];
 #pragma unroll
         for (int c = 0; c < DT; ++c) {
           float acc = 0.f;
 #pragma unroll
           for (int jj = 0; jj < KG; ++jj) acc = fmaf(s[jj], sKV[(g0 + jj) * (2 * DT + 1) + DT + c], acc);
-          ctx[c] = acc * inv;
+          ctx[c] = acc * rinv;
         }
         __syncwarp();
-        store_row_canon(sA, row, DT, ctx, DT);
+        store_row(sA, row, DT, ctx, DT);
         signal();
         wait_d();
         float o[DT];
         tmem_row<DT>(trow, o);
 #pragma unroll
         for (int c = 0; c < DT; ++c) h[c] += o[c] + __ldg(ib[3] + c);       // x1
-        layer_norm_row<DT>(h, ln[2], ln[3], xn);
-        store_row_canon(sA, row, DT, xn, DT);
+        ln_row<DT>(h, ln[2], ln[3], xn, nullptr, inv);
+        store_row(sA, row, DT, xn, DT);
         signal();
         wait_d();
 #pragma unroll 1
@@ -346,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
           tmem_row<32>(trow + c0, hv);
 #pragma unroll
           for (int u = 0; u < 32; ++u) hv[u] = gelu_f(hv[u] + __ldg(ib[4] + c0 + u));
-          store_row_canon(sH, row, 4 * DT, hv, 32, c0);
+          store_row(sH, row, 4 * DT, hv, 32, c0);
         }
         signal();
         wait_d();
@@ -354,12 +293,12 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
 #pragma unroll
         for (int c = 0; c < DT; ++c) h[c] += o[c] + __ldg(ib[5] + c);       // x2
       }
-      if (a.inner_layers > 0 && !keep) {
+      if (a.inner_layers > 0 && !ti.keep) {
 #pragma unroll
         for (int c = 0; c < DT; ++c) h[c] = 0.f;
       }
-      if (in_range) {
-        float4* dst = reinterpret_cast<float4*>(a.merged + t * DT);
+      if (ti.in_range) {
+        float4* dst = reinterpret_cast<float4*>(a.merged + ti.t * DT);
 #pragma unroll
         for (int c = 0; c < DT; c += 4) dst[c / 4] = make_float4(h[c], h[c + 1], h[c + 2], h[c + 3]);
       }
@@ -367,7 +306,237 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
   }
   sm100::tc_fence_before();
   __syncthreads();
-  if (warp == 0) sm100::tmem_dealloc<kTmemCols>(tmem);
+  if (warp == 0) sm100::tmem_dealloc<256>(tmem);
+}
+
+// ------------------------------------------------------------------ token-MLP + featuriser backward
+// Per tile: recompute feat, x0 and the hidden a1 (one 128-column half at a time), then
+//   da1 = (dh·W2ᵀ) ⊙ GELU'(a1),   dx0 = da1·W1ᵀ,   dfeat = dx0·W_tpᵀ
+// and accumulate, in TMEM for the whole kernel, dW2 += g1ᵀ·dh, [dW1ᵀ | db1] += da1ᵀ·[x0 | 1],
+// dW_tpᵀ += dx0ᵀ·feat.  Table gradients are privatised in smem; abs-pos rows get global atomics.
+template <int DT>
+__global__ void __launch_bounds__(kThreads, 1) fe_mlp_bwd_kernel(FrontArgs a) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  const int Dm = DT * a.K;
+  const int H2 = 2 * Dm;
+  const int nh = H2 / 128;
+  const int XK = DT + 16;                  // x0 tile row: [x0 | 1 | 0…] for the db1 column
+  const BlobOff bo = blob_offsets(DT, Dm, a.inner_layers);
+  // smem carve-up
+  bf16* sW = reinterpret_cast<bf16*>(smem_raw);                    // tp, w1 (fwd) + tp_n, w1_n, w2_n
+  const int n_tp = DT * kFP, n_w1 = H2 * DT;
+  bf16* w_tp = sW;
+  bf16* w_w1 = w_tp + n_tp;
+  bf16* w_tp_n = w_w1 + n_w1;
+  bf16* w_w1_n = w_tp_n + n_tp;
+  bf16* w_w2_n = w_w1_n + n_w1;
+  bf16* sFeat = w_w2_n + n_w1;                 // 128 x 32
+  bf16* sX0 = sFeat + kTile * kFP;             // 128 x XK
+  bf16* sDH = sX0 + kTile * XK;                // 128 x DT
+  bf16* sG = sDH + kTile * DT;                 // 128 x 128
+  bf16* sDA = sG + kTile * 128;                // 128 x 128
+  bf16* sDX0 = sDA + kTile * 128;              // 128 x DT
+  float* s_tab = reinterpret_cast<float*>(sDX0 + kTile * DT);
+  const int n_item = a.vocab * a.d_item, n_act = a.n_actions * a.d_act, n_time = a.nb * a.d_time;
+  const bool item_smem = n_item <= 16384;
+  float* s_item = s_tab;
+  float* s_act = s_item + (item_smem ? n_item : 0);
+  float* s_time = s_act + n_act;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_time + n_time + 2);
+  bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(bars) + 7) & ~uintptr_t(7));
+  uint64_t* bar_w = bars;
+  uint64_t* bar_a = bars + 1;
+  uint64_t* bar_d = bars + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < (item_smem ? n_item : 0) + n_act + n_time; i += blockDim.x) s_tab[i] = 0.f;
+  if (threadIdx.x == 0) {
+    sm100::mbar_init(bar_w, 1);
+    sm100::mbar_init(bar_a, 32 * kWorkers);
+    sm100::mbar_init(bar_d, 1);
+    sm100::fence_barrier_init();
+  }
+  if (warp == 0) sm100::tmem_alloc<512>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // TMEM columns
+  const uint32_t T_DW2 = tmem;                         // nh x DT
+  const uint32_t T_DW1 = tmem + nh * DT;               // nh x XK
+  const uint32_t T_DWTP = T_DW1 + nh * XK;             // kFP
+  const uint32_t T_X0 = T_DWTP + kFP;                  // DT (x0 acc), later dfeat (kFP)
+  const uint32_t T_DX0 = T_X0 + kFP;                   // DT
+  const uint32_t T_A1 = T_DX0 + 32;                    // 128
+  const uint32_t T_G1 = T_A1 + 128;                    // 128
+  const long long ntiles = (a.T + kTile - 1) / kTile;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int b1 = (n_tp + n_w1) * 2, b2 = (n_tp + 2 * n_w1) * 2;
+      sm100::mbar_arrive_expect_tx(bar_w, b1 + b2);
+      load_blob(reinterpret_cast<uint8_t*>(w_tp), reinterpret_cast<const uint8_t*>(a.wblob + bo.tp), b1, bar_w);
+      load_blob(reinterpret_cast<uint8_t*>(w_tp_n), reinterpret_cast<const uint8_t*>(a.wblob + bo.tp_n), b2, bar_w);
+      sm100::mbar_wait(bar_w, 0);
+      const uint32_t aW1 = sm100::smem_u32(w_w1), aTP = sm100::smem_u32(w_tp), aTPn = sm100::smem_u32(w_tp_n);
+      const uint32_t aW1n = sm100::smem_u32(w_w1_n), aW2n = sm100::smem_u32(w_w2_n);
+      const uint32_t aFeat = sm100::smem_u32(sFeat), aX0 = sm100::smem_u32(sX0), aDH = sm100::smem_u32(sDH);
+      const uint32_t aG = sm100::smem_u32(sG), aDA = sm100::smem_u32(sDA), aDX0 = sm100::smem_u32(sDX0);
+      uint32_t pa = 0;
+      auto wait_a = [&]() { sm100::mbar_wait(bar_a, pa); pa ^= 1; sm100::tc_fence_after(); };
+      bool first = true;
+      for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        wait_a();                                                        // feat, dh
+        mma(T_X0, Opnd{aFeat, kFP, 0}, Opnd{aTP, kFP, 0}, kFP / 16, DT, false);
+        sm100::mma_commit(bar_d);
+        wait_a();                                                        // x0
+        // hidden half 0: a1 (recompute) and dg1 = dh·W2ᵀ
+        mma(T_A1, Opnd{aX0, XK, 0}, Opnd{aW1, DT, 0}, DT / 16, 128, false);
+        mma(T_G1, Opnd{aDH, DT, 0}, Opnd{aW2n, DT, 0}, DT / 16, 128, false);
+        sm100::mma_commit(bar_d);
+        for (int j = 0; j < nh; ++j) {
+          wait_a();                                                      // g1, da1 of half j in sG / sDA
+          mma(T_DW2 + j * DT, Opnd{aG, 128, 1}, Opnd{aDH, DT, 1}, kTile / 16, DT, !first);
+          mma(T_DW1 + j * XK, Opnd{aDA, 128, 1}, Opnd{aX0, XK, 1}, kTile / 16, XK, !first);
+          mma(T_DX0, Opnd{aDA, 128, 0}, Opnd{aW1n + canon(0, 128 * j, H2) * 2, H2, 0}, 8, DT, j > 0);
+          if (j + 1 < nh) {
+            mma(T_A1, Opnd{aX0, XK, 0}, Opnd{aW1 + canon(128 * (j + 1), 0, DT) * 2, DT, 0}, DT / 16, 128, false);
+            mma(T_G1, Opnd{aDH, DT, 0}, Opnd{aW2n + canon(128 * (j + 1), 0, DT) * 2, DT, 0}, DT / 16, 128, false);
+          }
+          sm100::mma_commit(bar_d);
+        }
+        wait_a();                                                        // dx0 in sDX0
+        mma(T_DWTP, Opnd{aDX0, DT, 1}, Opnd{aFeat, kFP, 1}, kTile / 16, kFP, !first);
+        mma(T_X0, Opnd{aDX0, DT, 0}, Opnd{aTPn, DT, 0}, DT / 16, kFP, false);
+        sm100::mma_commit(bar_d);
+        first = false;
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    uint32_t pd = 0;
+    auto signal = [&]() { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(bar_a); };
+    auto wait_d = [&]() { sm100::mbar_wait(bar_d, pd); pd ^= 1; sm100::tc_fence_after(); };
+    float acc_b2 = 0.f, acc_btp = 0.f;     // column sums (lane c ↔ column c)
+    int my_tiles = 0;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++my_tiles) {
+      const TokenInfo ti = token_info(a, tile, row);
+      float v[kFP];
+      int ids[3];
+      featurise(a, ti, v, ids, false);
+      store_row(sFeat, row, kFP, v, kFP);
+      float dh[DT];
+      if (ti.real) {
+        const float4* src = reinterpret_cast<const float4*>(a.dh + ti.t * DT);
+#pragma unroll
+        for (int c = 0; c < DT; c += 4) {
+          const float4 f4 = src[c / 4];
+          dh[c] = f4.x; dh[c + 1] = f4.y; dh[c + 2] = f4.z; dh[c + 3] = f4.w;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < DT; ++c) dh[c] = 0.f;
+      }
+      store_row(sDH, row, DT, dh, DT);
+      acc_b2 += warp_colsum<DT>(dh);                                   // db_seq2 = Σ dh
+      signal();
+      // x0 recompute
+      float x[DT + 16];
+      wait_d();
+      tmem_row<DT>(T_X0 + lane_off, x);
+#pragma unroll
+      for (int c = 0; c < DT; ++c)
+        x[c] = ti.real ? x[c] + __ldg(a.tok_b + c) + __ldg(a.pos_tab + (long long)ti.rec * DT + c) : 0.f;
+#pragma unroll
+      for (int c = DT; c < DT + 16; ++c) x[c] = c == DT ? 1.f : 0.f;
+      store_row(sX0, row, XK, x, XK);
+      signal();
+      for (int hj = 0; hj < nh; ++hj) {
+        wait_d();
+#pragma unroll 1
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+          float av[32], gv[32];
+          tmem_row<32>(T_A1 + lane_off + c0, av);
+          tmem_row<32>(T_G1 + lane_off + c0, gv);
+#pragma unroll
+          for (int u = 0; u < 32; ++u) {
+            const float z = av[u] + __ldg(a.seq_b1 + 128 * hj + c0 + u);
+            const float t = tanh_fast(kGeluC * (z + kGeluA * z * z * z));
+            av[u] = 0.5f * z * (1.f + t);
+            gv[u] *= 0.5f * (1.f + t) + 0.5f * z * (1.f - t * t) * kGeluC * (1.f + 3.f * kGeluA * z * z);
+          }
+          store_row(sG, row, 128, av, 32, c0);
+          store_row(sDA, row, 128, gv, 32, c0);
+        }
+        signal();
+      }
+      wait_d();
+      float dx0[DT];
+      tmem_row<DT>(T_DX0 + lane_off, dx0);
+#pragma unroll
+      for (int c = 0; c < DT; ++c) dx0[c] = ti.real ? dx0[c] : 0.f;
+      store_row(sDX0, row, DT, dx0, DT);
+      if (ti.real) {
+        float* gp = a.g_pos + (long long)ti.rec * DT;
+#pragma unroll
+        for (int c = 0; c < DT; ++c) atomicAdd(gp + c, dx0[c]);
+      }
+      acc_btp += warp_colsum<DT>(dx0);                                 // db_tp = Σ dx0
+      signal();
+      wait_d();
+      float df[kFP];
+      tmem_row<kFP>(T_X0 + lane_off, df);
+      if (ti.real) {
+        const int e1 = a.d_item, e2 = e1 + a.d_act;
+        for (int c = 0; c < e1; ++c) {
+          if (item_smem) atomicAdd(s_item + ids[0] * a.d_item + c, df[c]);
+          else atomicAdd(a.g_item + ids[0] * a.d_item + c, df[c]);
+        }
+        for (int c = 0; c < a.d_act; ++c) atomicAdd(s_act + ids[1] * a.d_act + c, df[e1 + c]);
+        for (int c = 0; c < a.d_time; ++c) atomicAdd(s_time + ids[2] * a.d_time + c, df[e2 + c]);
+      }
+    }
+    // ---------------- flush the CTA's accumulators
+    if (my_tiles > 0) {
+      for (int j = 0; j < nh; ++j) {
+        const int f = 128 * j + row;                                   // hidden unit
+        float w2[DT];
+        tmem_row<DT>(T_DW2 + lane_off + j * DT, w2);
+#pragma unroll
+        for (int c = 0; c < DT; ++c) atomicAdd(a.g_seq_w2 + (long long)f * DT + c, w2[c]);
+        float w1[DT + 16];
+        tmem_row<DT + 16>(T_DW1 + lane_off + j * XK, w1);
+#pragma unroll
+        for (int c = 0; c < DT; ++c) atomicAdd(a.g_seq_w1 + (long long)c * H2 + f, w1[c]);
+        atomicAdd(a.g_seq_b1 + f, w1[DT]);
+      }
+      {
+        float wt[kFP];
+        tmem_row<kFP>(T_DWTP + lane_off, wt);                           // warp-collective load
+        if (row < DT) {
+          const int F = a.d_item + a.d_act + a.d_time;
+          for (int k = 0; k < F; ++k) atomicAdd(a.g_tok_w + k * DT + row, wt[k]);
+        }
+      }
+      if (lane < DT) {
+        atomicAdd(a.g_seq_b2 + lane, acc_b2);
+        atomicAdd(a.g_tok_b + lane, acc_btp);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < (item_smem ? n_item : 0); i += blockDim.x)
+    if (s_item[i] != 0.f) atomicAdd(a.g_item + i, s_item[i]);
+  for (int i = threadIdx.x; i < n_act; i += blockDim.x)
+    if (s_act[i] != 0.f) atomicAdd(a.g_act + i, s_act[i]);
+  for (int i = threadIdx.x; i < n_time; i += blockDim.x)
+    if (s_time[i] != 0.f) atomicAdd(a.g_time + i, s_time[i]);
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) sm100::tmem_dealloc<512>(tmem);
 }
 
 }  // namespace
@@ -375,54 +544,64 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
 int frontend_supported(int d, int K, int D, int F, int inner_layers) {
   if (!(d == 16 || d == 32)) return 0;
   if (!(K == 2 || K == 4 || K == 8)) return 0;
-  if ((2 * D) % 128) return 0;
+  if ((2 * D) % 128 || 2 * D > 512) return 0;
   if (F > kFP) return 0;
   if (inner_layers > 8) return 0;
   return 1;
 }
 
-int frontend_blob_bytes(int d, int D, int F, int inner_layers) {
-  (void)F;
-  return blob_offsets(d, D, inner_layers).total * 2;
-}
+int frontend_blob_bytes(int d, int D, int inner_layers) { return blob_offsets(d, D, inner_layers).total * 2; }
 
 void pack_frontend_weights(const float* params, long long tok_w, long long seq_w1, long long seq_w2,
                            const long long (*inner_w)[4], int d, int D, int F, int IL, bf16* blob,
                            cudaStream_t st) {
   const BlobOff o = blob_offsets(d, D, IL);
+  cudaMemsetAsync(blob, 0, (size_t)o.total * 2, st);
   PackW pw;
   pw.n = 0;
-  auto add = [&](long long src, int in, int out, int n_off, int Kdim, int dst) {
-    pw.s[pw.n].src = src; pw.s[pw.n].in = in; pw.s[pw.n].out = out; pw.s[pw.n].n_off = n_off;
-    pw.s[pw.n].Kdim = Kdim; pw.s[pw.n].dst = dst; ++pw.n;
+  auto add = [&](long long src, int in, int out, int trans, int n_off, int k_off, int Kdim, int dst) {
+    auto& s = pw.s[pw.n++];
+    s.src = src; s.in = in; s.out = out; s.trans = trans; s.n_off = n_off; s.k_off = k_off; s.Kdim = Kdim; s.dst = dst;
   };
-  add(tok_w, F, d, 0, kFP, o.tp);
-  add(seq_w1, d, 2 * D, 0, d, o.w1);
-  add(seq_w2, 2 * D, d, 0, 2 * D, o.w2);
+  // forward images (Wᵀ, K = in)
+  add(tok_w, F, d, 1, 0, 0, kFP, o.tp);
+  add(seq_w1, d, 2 * D, 1, 0, 0, d, o.w1);
+  add(seq_w2, 2 * D, d, 1, 0, 0, 2 * D, o.w2);
+  // backward images (W, K = out)
+  add(tok_w, F, d, 0, 0, 0, d, o.tp_n);
+  add(seq_w1, d, 2 * D, 0, 0, 0, 2 * D, o.w1_n);
+  add(seq_w2, 2 * D, d, 0, 0, 0, d, o.w2_n);
   for (int l = 0; l < IL; ++l) {
-    // inner_w[l] = {w_q, w_k, w_v, w_o}; w1/w2 follow b_o in the reference order
-    add(inner_w[l][0], d, d, 0, d, o.qkv[l]);
-    add(inner_w[l][1], d, d, d, d, o.qkv[l]);
-    add(inner_w[l][2], d, d, 2 * d, d, o.qkv[l]);
-    add(inner_w[l][3], d, d, 0, d, o.wo[l]);
-    add(inner_w[l][3] + (long long)d * d + d, d, 4 * d, 0, d, o.w1i[l]);                       // w1 after b_o
-    add(inner_w[l][3] + (long long)d * d + d + 4LL * d * d + 4 * d, 4 * d, d, 0, 4 * d, o.w2i[l]);  // w2 after b1
+    const long long wq = inner_w[l][0], wk = inner_w[l][1], wv = inner_w[l][2], wo = inner_w[l][3];
+    const long long w1 = wo + (long long)d * d + d, w2 = w1 + 4LL * d * d + 4 * d;   // reference order
+    add(wq, d, d, 1, 0, 0, d, o.qkv[l]);
+    add(wk, d, d, 1, d, 0, d, o.qkv[l]);
+    add(wv, d, d, 1, 2 * d, 0, d, o.qkv[l]);
+    add(wo, d, d, 1, 0, 0, d, o.wo[l]);
+    add(w1, d, 4 * d, 1, 0, 0, d, o.w1i[l]);
+    add(w2, 4 * d, d, 1, 0, 0, 4 * d, o.w2i[l]);
+    add(wq, d, d, 0, 0, 0, 3 * d, o.qkv_n[l]);
+    add(wk, d, d, 0, 0, d, 3 * d, o.qkv_n[l]);
+    add(wv, d, d, 0, 0, 2 * d, 3 * d, o.qkv_n[l]);
+    add(wo, d, d, 0, 0, 0, d, o.wo_n[l]);
+    add(w1, d, 4 * d, 0, 0, 0, 4 * d, o.w1i_n[l]);
+    add(w2, 4 * d, d, 0, 0, 0, d, o.w2i_n[l]);
   }
   pack_canon_kernel<<<dim3(16, pw.n), 256, 0, st>>>(params, pw, blob);
 }
 
 template <int DT, int KG>
 static int launch_fwd(const FrontArgs& a, cudaStream_t st) {
-  const int D = DT * KG;
-  const BlobOff bo = blob_offsets(DT, D, a.inner_layers);
-  const int smem = ((bo.total + 63) & ~63) * 2 + kTile * kFP * 2 + kTile * 136 * 2 + 64;
+  const BlobOff bo = blob_offsets(DT, DT * KG, a.inner_layers);
+  const int smem = ((bo.fwd_total + 63) & ~63) * 2 + kTile * kFP * 2 + kTile * 136 * 2 + 64;
   static int done = 0;
   if (!done) {
-    cudaFuncSetAttribute(fe_fwd_kernel<DT, KG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem > 113 * 1024 ? 227 * 1024 : 113 * 1024);
+    cudaFuncSetAttribute(fe_fwd_kernel<DT, KG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     done = 1;
   }
   const long long ntiles = (a.T + kTile - 1) / kTile;
-  const int grid = (int)std::min<long long>(ntiles, 2 * 148);
+  const int per_sm = smem <= 113 * 1024 ? 2 : 1;
+  const int grid = (int)std::min<long long>(ntiles, per_sm * 148);
   fe_fwd_kernel<DT, KG><<<grid, kThreads, smem, st>>>(a);
   return (int)cudaGetLastError();
 }
@@ -435,6 +614,32 @@ int frontend_fwd(const FrontArgs& a, cudaStream_t st) {
   if (d == 16 && K == 8) return launch_fwd<16, 8>(a, st);
   if (d == 32 && K == 2) return launch_fwd<32, 2>(a, st);
   if (d == 16 && K == 2) return launch_fwd<16, 2>(a, st);
+  return (int)cudaErrorInvalidValue;
+}
+
+template <int DT>
+static int launch_mlp_bwd(const FrontArgs& a, cudaStream_t st) {
+  const int H2 = 2 * DT * a.K;
+  const int XK = DT + 16;
+  const int n_item = a.vocab * a.d_item;
+  const int tab = ((n_item <= 16384) ? n_item : 0) + a.n_actions * a.d_act + a.nb * a.d_time;
+  const int smem = (2 * DT * kFP + 3 * H2 * DT) * 2 + kTile * (kFP + XK + DT + 128 + 128 + DT) * 2 + tab * 4 + 128;
+  if (smem > 227 * 1024) return (int)cudaErrorInvalidValue;
+  static int done = 0;
+  if (!done) {
+    cudaFuncSetAttribute(fe_mlp_bwd_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    done = 1;
+  }
+  const long long ntiles = (a.T + kTile - 1) / kTile;
+  const int grid = (int)std::min<long long>(ntiles, 148);
+  // > 113 KB of smem keeps one CTA per SM (the kernel allocates all 512 TMEM columns)
+  fe_mlp_bwd_kernel<DT><<<grid, kThreads, std::max(smem, 116 * 1024), st>>>(a);
+  return (int)cudaGetLastError();
+}
+
+int frontend_mlp_bwd(const FrontArgs& a, cudaStream_t st) {
+  if (a.d == 32) return launch_mlp_bwd<32>(a, st);
+  if (a.d == 16) return launch_mlp_bwd<16>(a, st);
   return (int)cudaErrorInvalidValue;
 }
 

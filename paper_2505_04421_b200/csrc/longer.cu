@@ -117,7 +117,7 @@ struct Bump {
 
 struct BlockBufs {            // one attention block over the q query rows
   bf16 *qn, *qkv, *ctx, *x1n, *f1, *gf;
-  float *m1, *r1, *lse, *x1, *m2, *r2, *out;
+  float *m1, *r1, *lse, *x1, *m2, *r2, *out, *ctx32;
 };
 struct InnerBufs {            // one InnerTrans layer over T tokens
   bf16 *xn, *ctx, *x1n, *f1, *gf;
@@ -190,7 +190,7 @@ Plan make_plan(const LongerDims& d, void* ws) {
   const long long Q = (long long)B * q, V = (long long)B * v, M = (long long)B * m;
   p.status = a.take<int>(64);
   p.npg = a.take<int32_t>(B);
-  p.wblob = a.take<bf16>(frontend_blob_bytes(dd, D, p.F, p.IL) / 2 + 64);
+  p.wblob = a.take<bf16>(frontend_blob_bytes(dd, D, p.IL) / 2 + 64);
   // packed weights
   p.pk.seq_w1 = a.take<bf16>(dd * 2 * D); p.pk.seq_w2 = a.take<bf16>(2 * D * dd);
   p.pk.glob_w1 = a.take<bf16>(D * 2 * D); p.pk.glob_w2 = a.take<bf16>(2 * D * D);
@@ -226,7 +226,7 @@ Plan make_plan(const LongerDims& d, void* ws) {
   p.KV = a.take<bf16>(V * 2 * D);
   auto block_bufs = [&](BlockBufs& b, int qkv_cols) {
     b.qn = a.take<bf16>(Q * D); b.m1 = a.take<float>(Q); b.r1 = a.take<float>(Q);
-    b.qkv = a.take<bf16>(Q * qkv_cols); b.ctx = a.take<bf16>(Q * D); b.lse = a.take<float>(Q * p.heads);
+    b.qkv = a.take<bf16>(Q * qkv_cols); b.ctx = a.take<bf16>(Q * D); b.lse = a.take<float>(Q * p.heads); b.ctx32 = a.take<float>(Q * D);
     b.x1 = a.take<float>(Q * D); b.x1n = a.take<bf16>(Q * D); b.m2 = a.take<float>(Q); b.r2 = a.take<float>(Q);
     b.f1 = a.take<bf16>(Q * 4 * D); b.gf = a.take<bf16>(Q * 4 * D); b.out = a.take<float>(Q * D);
   };
@@ -399,7 +399,7 @@ int block_fwd(const Ctx& c, const BlockOff& bo, BlockBufs& b, const float* xq, b
   layernorm_fwd(rows_plain(xq, D, Q), D, c.w(bo.ln1_g), c.w(bo.ln1_b), b.qn, b.m1, b.r1, st);
   AttnArgs a{};
   a.nq = p.q; a.D = D; a.heads = p.heads; a.k = p.k; a.G = p.G; a.npg = p.npg; a.B = p.B;
-  a.ctx = b.ctx; a.ldc = D; a.sc = (long long)p.q * D; a.lse = b.lse;
+  a.ctx = b.ctx; a.ldc = D; a.sc = (long long)p.q * D; a.lse = b.lse; a.ctx32 = b.ctx32;
   if (cross) {
     // R = [merged; globals] → LN1 (same ln1 params) → [K | V] projection over all v rows
     RowMap r{};
@@ -427,6 +427,8 @@ int block_fwd(const Ctx& c, const BlockOff& bo, BlockBufs& b, const float* xq, b
   return 0;
 }
 
+int inner_unfused_fwd(const Ctx& c, const Plan& p);
+
 // Unfused front-end: featuriser kernel + tcgen05 GEMMs per stage; keeps every activation the
 // unfused backward needs.
 int frontend_unfused_fwd(const Ctx& c, const Plan& p, const LongerBatch& bt) {
@@ -447,7 +449,16 @@ int frontend_unfused_fwd(const Ctx& c, const Plan& p, const LongerBatch& bt) {
   // per-token input MLP (inputs.py:447-449); pad rows zeroed (inputs.py:478-481)
   TRY(lin_fwd(st, p.x0, d, T, p.pk.seq_w1, d, 2 * D, c.w(o.seq_b1), EPI_GELU | EPI_SAVE_PRE, nullptr, p.g1, p.a1));
   TRY(lin_fwd(st, p.g1, 2 * D, T, p.pk.seq_w2, 2 * D, d, c.w(o.seq_b2), 0, p.h, nullptr, nullptr, nullptr, 0, p.real));
-  // InnerTrans merge (merge.py:83-112)
+  return inner_unfused_fwd(c, p);
+}
+
+// InnerTrans merge (merge.py:83-112) from p.h with per-stage kernels, keeping every activation
+// the per-stage backward needs.  With the fused front-end this is the backward's recompute.
+int inner_unfused_fwd(const Ctx& c, const Plan& p) {
+  cudaStream_t st = c.st;
+  const ParamOff& o = p.po;
+  const int d = p.d;
+  const long long T = p.T;
   const float* x = p.h;
   for (int i = 0; i < p.IL; ++i) {
     const InnerBufs& b = p.in[i];
@@ -465,16 +476,9 @@ int frontend_unfused_fwd(const Ctx& c, const Plan& p, const LongerBatch& bt) {
   return 0;
 }
 
-// Fused front-end (frontend.cu): ids → merged rows in one persistent kernel.
-int frontend_fused_fwd(const Ctx& c, const Plan& p, const LongerBatch& bt) {
-  cudaStream_t st = c.st;
+FrontArgs front_args(const Ctx& c, const Plan& p, const LongerBatch& bt) {
   const ParamOff& o = p.po;
   const LongerDims& dm = p.dims;
-  long long iw[kMaxInner][4];
-  for (int l = 0; l < p.IL; ++l) {
-    iw[l][0] = o.inner[l].w_q; iw[l][1] = o.inner[l].w_k; iw[l][2] = o.inner[l].w_v; iw[l][3] = o.inner[l].w_o;
-  }
-  pack_frontend_weights(c.P, o.tok_w, o.seq_w1, o.seq_w2, iw, p.d, p.D, p.F, p.IL, p.wblob, st);
   FrontArgs f{};
   f.items = bt.items; f.actions = bt.actions; f.dt = bt.dt; f.n_events = bt.n_events;
   f.B = p.B; f.L = p.L; f.Lp = p.Lp; f.K = p.K; f.d = p.d; f.d_item = dm.d_item; f.d_act = dm.d_act;
@@ -491,7 +495,25 @@ int frontend_fused_fwd(const Ctx& c, const Plan& p, const LongerBatch& bt) {
   }
   f.wblob = p.wblob;
   f.merged = p.merged; f.status = p.status; f.npg = p.npg;
-  return frontend_fwd(f, st);
+  f.h_out = p.IL ? p.h : nullptr;
+  f.real_out = p.real; f.keep_out = p.keep;
+  if (c.G) {
+    f.g_tok_w = c.g(o.tok_w); f.g_tok_b = c.g(o.tok_b); f.g_seq_w1 = c.g(o.seq_w1); f.g_seq_b1 = c.g(o.seq_b1);
+    f.g_seq_w2 = c.g(o.seq_w2); f.g_seq_b2 = c.g(o.seq_b2); f.g_item = c.g(o.item); f.g_act = c.g(o.act);
+    f.g_time = c.g(o.time); f.g_pos = c.g(o.pos);
+  }
+  return f;
+}
+
+// Fused front-end (frontend.cu): ids → merged rows in one persistent kernel.
+int frontend_fused_fwd(const Ctx& c, const Plan& p, const LongerBatch& bt) {
+  const ParamOff& o = p.po;
+  long long iw[kMaxInner][4];
+  for (int l = 0; l < p.IL; ++l) {
+    iw[l][0] = o.inner[l].w_q; iw[l][1] = o.inner[l].w_k; iw[l][2] = o.inner[l].w_v; iw[l][3] = o.inner[l].w_o;
+  }
+  pack_frontend_weights(c.P, o.tok_w, o.seq_w1, o.seq_w2, iw, p.d, p.D, p.F, p.IL, p.wblob, c.st);
+  return frontend_fwd(front_args(c, p, bt), c.st);
 }
 
 int forward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs, float* loss, int with_loss) {
@@ -567,7 +589,7 @@ int block_bwd(const Ctx& c, const BlockOff& bo, const BlockBufs& b, const float*
   // attention
   AttnArgs a{};
   a.nq = p.q; a.D = D; a.heads = p.heads; a.k = p.k; a.G = p.G; a.npg = p.npg; a.B = p.B;
-  a.ctx = b.ctx; a.ldc = D; a.sc = (long long)p.q * D; a.lse = b.lse;
+  a.ctx = b.ctx; a.ldc = D; a.sc = (long long)p.q * D; a.lse = b.lse; a.ctx32 = b.ctx32;
   a.dctx = p.dctx; a.lddc = D; a.sdc = (long long)p.q * D; a.ctx_in = b.ctx;
   if (cross) {
     a.Q = b.qkv; a.ldq = D; a.sq = (long long)p.q * D;
@@ -664,7 +686,9 @@ int backward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs) {
   ga.g_uid = c.g(o.uid); ga.g_item = c.g(o.item); ga.g_time = c.g(o.time); ga.g_cls = c.g(o.cls);
   ga.g_tok_w = c.g(o.tok_w); ga.g_tok_b = c.g(o.tok_b); ga.g_lift_w = c.g(o.lift_w); ga.g_lift_b = c.g(o.lift_b);
   globals_raw_bwd(ga, st);
-  // InnerTrans backward (all-pad groups were zeroed after the last layer)
+  // InnerTrans backward (all-pad groups were zeroed after the last layer).  The fused forward
+  // kept only its input h, so the per-stage activations are recomputed here first.
+  if (p.fused_fe && p.IL) TRY(inner_unfused_fwd(c, p));
   float* dxt = p.dmerged;
   if (p.IL) mul_rows_inplace(dxt, (int)T, d, p.keep, st);
   for (int i = p.IL - 1; i >= 0; --i) {
@@ -699,6 +723,13 @@ int backward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs) {
     dxt = p.t_dx;
   }
   // token MLP + featuriser (inputs.py:434-482); only real tokens carry gradient
+  if (p.fused_fe) {
+    FrontArgs f = front_args(c, p, bt);
+    f.dh = dxt;
+    TRY(frontend_mlp_bwd(f, st));
+    TRY((int)cudaGetLastError());
+    return 0;
+  }
   cast_rows_bf16(dxt, (int)T, d, d, p.dh_bf, d, p.real, st);
   TRY(lin_dx(st, p.dh_bf, d, T, p.pk.seq_w2, d, 2 * D, d, nullptr, 0, p.da1, 2 * D, p.a1));
   TRY(lin_dw(st, p.g1, 2 * D, 2 * D, p.dh_bf, d, d, T, c.g(o.seq_w2)));
@@ -771,6 +802,7 @@ extern "C" int longer_forward_backward(const LongerDims* dims, const float* para
                                        void* stream) {
   static Plan p;
   int rc = check_call(dims, ws_bytes, &p, ws);
+  p.fused_fe = use_fused(p);
   if (rc) return rc;
   Ctx c{p, params, grads, (cudaStream_t)stream};
   rc = forward(c, p, *batch, probs, loss, 1);

@@ -569,9 +569,13 @@ __global__ void attn_fwd_kernel(AttnArgs a) {
     if (i >= a.nq) break;
     const float inv = l_[r] > 0.f ? 1.f / l_[r] : 0.f;
     bf16* o = a.ctx + b * a.sc + (long long)i * a.ldc + h * dh;
+    float* o32 = a.ctx32 + b * a.sc + (long long)i * a.ldc + h * dh;
     for (int u = 0; u < nd; ++u) {
       const int c = lane + 32 * u;
-      if (c < dh) o[c] = __float2bfloat16(acc[r][u] * inv);
+      if (c < dh) {
+        o[c] = __float2bfloat16(acc[r][u] * inv);
+        o32[c] = acc[r][u] * inv;
+      }
     }
     if (lane == 0) a.lse[((long long)b * a.heads + h) * a.nq + i] = l_[r] > 0.f ? m_[r] + __logf(l_[r]) : -INFINITY;
   }
@@ -609,7 +613,7 @@ __global__ void attn_bwd_kernel(AttnArgs a) {
   const bf16* Kg = a.Kp + b * a.sk + h * dh;
   const bf16* Vg = a.V + b * a.sv + h * dh;
   const float* dO = a.dctx + b * a.sdc + h * dh;
-  const bf16* O = a.ctx_in + b * a.sc + h * dh;
+  const float* O = a.ctx32 + b * a.sc + h * dh;        // fp32 context: D_i consistent with P·V
   for (int i = threadIdx.x; i < nq * dh; i += blockDim.x) {
     const int r = i / dh, c = i % dh;
     sQ[r * ldp + c] = __bfloat162float(Q[(long long)r * a.ldq + c]) * scale;
@@ -620,7 +624,7 @@ __global__ void attn_bwd_kernel(AttnArgs a) {
   const int wid = threadIdx.x / 32, lane = threadIdx.x & 31, nw = blockDim.x / 32;
   for (int i = wid; i < nq; i += nw) {                      // D_i = rowsum(dO ∘ O)
     float s = 0.f;
-    for (int c = lane; c < dh; c += 32) s += sdO[i * ldp + c] * __bfloat162float(O[(long long)i * a.ldc + c]);
+    for (int c = lane; c < dh; c += 32) s += sdO[i * ldp + c] * O[(long long)i * a.ldc + c];
     s = warp_sum(s);
     if (lane == 0) { sDi[i] = s; sL[i] = a.lse[((long long)b * a.heads + h) * nq + i]; }
   }

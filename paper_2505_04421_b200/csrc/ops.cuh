@@ -83,7 +83,8 @@ struct AttnArgs {
   int k, G, ns, goff;                        // VisRule parameters
   const int32_t* npg;                        // [B] pad groups
   int B;
-  bf16* ctx; int ldc; long long sc;          // fwd out
+  bf16* ctx; int ldc; long long sc;          // fwd out (GEMM operand)
+  float* ctx32;                              // fwd out fp32 copy, same ld/stride (bwd D_i)
   float* lse;                                // [B, heads, nq] (−inf for fully masked rows)
   // backward
   const float* dctx; int lddc; long long sdc;
