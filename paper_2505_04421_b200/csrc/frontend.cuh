@@ -34,6 +34,11 @@ struct FrontArgs {
   const float* dh;             // [T, d] gradient w.r.t. the token-MLP output (MLP backward input)
   float *g_tok_w, *g_tok_b, *g_seq_w1, *g_seq_b1, *g_seq_w2, *g_seq_b2;
   float *g_item, *g_act, *g_time, *g_pos;
+  // InnerTrans backward (layer 0): h saved by the forward, dmerged in, dh out
+  const float* h_in;           // [T, d]
+  const float* dmerged;        // [T, d]
+  float* dh_out;               // [T, d]
+  float* g_inner[16];          // grads of w_q,b_q,w_k,b_k,w_v,b_v,w_o,b_o,w1,b1,w2,b2,ln1_g,ln1_b,ln2_g,ln2_b
 };
 
 int frontend_blob_bytes(int d, int D, int inner_layers);
@@ -47,5 +52,7 @@ int frontend_supported(int d, int K, int D, int F, int inner_layers);
 int frontend_fwd(const FrontArgs& a, cudaStream_t st);
 // token-MLP + featuriser backward: dh → all front-end MLP/featuriser/table/pos gradients
 int frontend_mlp_bwd(const FrontArgs& a, cudaStream_t st);
+// InnerTrans (one layer) backward: recompute the layer from h, dmerged → dh + layer gradients
+int frontend_inner_bwd(const FrontArgs& a, cudaStream_t st);
 
 }  // namespace longer

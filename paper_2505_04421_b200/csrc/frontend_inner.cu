@@ -1,0 +1,418 @@
+// frontend_inner.cu — fused InnerTrans backward (one layer) for 128-token tiles.
+//
+// Backward of merge_inner_trans (pkg/src/longrec/merge.py:83-112): pre-LN block at width d with
+// full attention inside each K-group (grouped_attention, pkg/src/longrec/tensors.py:406-444),
+// layer_norm / linear / gelu backward closures (tensors.py:292-404).  The layer is recomputed from
+// its saved input h, every contraction is a tcgen05 MMA against smem-resident weights, the four
+// weight gradients accumulate in TMEM for the whole kernel (bias gradients ride along as a column
+// of ones appended to the contracted activation), and LN / bias column sums use warp transposes.
+#include "fe_common.cuh"
+#include "frontend.cuh"
+
+#include <algorithm>
+
+namespace longer {
+
+using namespace fe;
+
+namespace {
+
+template <int DT, int KG>
+__global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  constexpr int XK = DT + 16;                 // activation rows carrying a ones column
+  constexpr int F4 = 4 * DT;
+  constexpr int QS = 3 * DT + 2;              // bf16 q|k|v scratch row (padded)
+  const BlobOff bo = blob_offsets(DT, DT * KG, a.inner_layers);
+  // weights: forward images [qkv | wo | w1i] and backward images [qkv_n | wo_n | w1i_n | w2i_n]
+  bf16* sWf = reinterpret_cast<bf16*>(smem_raw);
+  const int nWf = 3 * DT * DT + DT * DT + 4 * DT * DT;
+  const int nWb = 3 * DT * DT + DT * DT + 4 * DT * DT + 4 * DT * DT;
+  bf16* sWb = sWf + nWf;
+  bf16* w_qkv = sWf;
+  bf16* w_wo = w_qkv + 3 * DT * DT;
+  bf16* w_w1i = w_wo + DT * DT;
+  bf16* w_qkv_n = sWb;
+  bf16* w_wo_n = w_qkv_n + 3 * DT * DT;
+  bf16* w_w1i_n = w_wo_n + DT * DT;
+  bf16* w_w2i_n = w_w1i_n + 4 * DT * DT;
+  bf16* sXN = sWb + nWb;                      // 128 x XK
+  bf16* sCTX = sXN + kTile * XK;              // 128 x XK
+  bf16* sX1N = sCTX + kTile * XK;             // 128 x XK
+  bf16* sDX2 = sX1N + kTile * XK;             // 128 x DT
+  bf16* sDX1 = sDX2 + kTile * DT;             // 128 x DT
+  bf16* sGF = sDX1 + kTile * DT;              // 128 x F4   (later: dqkv 128 x 3DT)
+  bf16* sDF = sGF + kTile * F4;               // 128 x F4   (later: dctx fp32 scratch)
+  bf16* sDQKV = sGF;
+  float* sDC = reinterpret_cast<float*>(sDF); // 128 x (DT+1)
+  bf16* sQKV = sDF + kTile * F4;              // 128 x QS bf16 (q, k, v for the group peers)
+  float* sP = reinterpret_cast<float*>(sQKV + kTile * QS);   // 128 x KG
+  float* sS = sP + kTile * KG;                                  // 128 x KG (dS)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sS + kTile * KG);
+  uint64_t* bar_w = bars;
+  uint64_t* bar_a = bars + 1;
+  uint64_t* bar_d = bars + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    sm100::mbar_init(bar_w, 1);
+    sm100::mbar_init(bar_a, 32 * kWorkers);
+    sm100::mbar_init(bar_d, 1);
+    sm100::fence_barrier_init();
+  }
+  if (warp == 0) sm100::tmem_alloc<512>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t T_DW2 = tmem;                // F4 rows x DT
+  const uint32_t T_DW1 = tmem + 32;           // F4 rows x XK   ([dW1ᵀ | db1])
+  const uint32_t T_DWO = tmem + 80;           // DT rows x XK   ([dWoᵀ | dbo])
+  const uint32_t T_DWQ = tmem + 128;          // 3DT rows x XK  ([dWqkvᵀ | dbqkv])
+  const uint32_t T_W0 = tmem + 176;           // 128: qkv, then f1
+  const uint32_t T_W1 = tmem + 304;           // 128: dgf
+  const uint32_t T_W2 = tmem + 432;           // 32:  o, dx1n, dctx, dxn
+  const long long ntiles = (a.T + kTile - 1) / kTile;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      sm100::mbar_arrive_expect_tx(bar_w, (nWf + nWb) * 2);
+      {
+        const uint8_t* src_f = reinterpret_cast<const uint8_t*>(a.wblob + bo.qkv[0]);
+        const uint8_t* src_b = reinterpret_cast<const uint8_t*>(a.wblob + bo.qkv_n[0]);
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     :: "r"(sm100::smem_u32(sWf)), "l"(src_f), "r"(nWf * 2), "r"(sm100::smem_u32(bar_w)) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     :: "r"(sm100::smem_u32(sWb)), "l"(src_b), "r"(nWb * 2), "r"(sm100::smem_u32(bar_w)) : "memory");
+      }
+      sm100::mbar_wait(bar_w, 0);
+      auto S = [](const void* p) { return sm100::smem_u32(p); };
+      uint32_t pa = 0;
+      auto wait_a = [&]() { sm100::mbar_wait(bar_a, pa); pa ^= 1; sm100::tc_fence_after(); };
+      bool first = true;
+      for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        wait_a();                                                           // xn, dX2
+        mma(T_W0, Opnd{S(sXN), XK, 0}, Opnd{S(w_qkv), DT, 0}, DT / 16, 3 * DT, false);
+        sm100::mma_commit(bar_d);
+        wait_a();                                                           // ctx
+        mma(T_W2, Opnd{S(sCTX), XK, 0}, Opnd{S(w_wo), DT, 0}, DT / 16, DT, false);
+        sm100::mma_commit(bar_d);
+        wait_a();                                                           // x1n
+        mma(T_W0, Opnd{S(sX1N), XK, 0}, Opnd{S(w_w1i), DT, 0}, DT / 16, F4, false);
+        mma(T_W1, Opnd{S(sDX2), DT, 0}, Opnd{S(w_w2i_n), DT, 0}, DT / 16, F4, false);
+        sm100::mma_commit(bar_d);
+        wait_a();                                                           // gf, df
+        mma(T_DW2, Opnd{S(sGF), F4, 1}, Opnd{S(sDX2), DT, 1}, kTile / 16, DT, !first);
+        mma(T_DW1, Opnd{S(sDF), F4, 1}, Opnd{S(sX1N), XK, 1}, kTile / 16, XK, !first);
+        mma(T_W2, Opnd{S(sDF), F4, 0}, Opnd{S(w_w1i_n), F4, 0}, F4 / 16, DT, false);
+        sm100::mma_commit(bar_d);
+        wait_a();                                                           // dx1
+        mma(T_W2, Opnd{S(sDX1), DT, 0}, Opnd{S(w_wo_n), DT, 0}, DT / 16, DT, false);
+        mma(T_DWO, Opnd{S(sDX1), DT, 1}, Opnd{S(sCTX), XK, 1}, kTile / 16, XK, !first);
+        sm100::mma_commit(bar_d);
+        wait_a();                                                           // dqkv
+        mma(T_W2, Opnd{S(sDQKV), 3 * DT, 0}, Opnd{S(w_qkv_n), 3 * DT, 0}, 3 * DT / 16, DT, false);
+        mma(T_DWQ, Opnd{S(sDQKV), 3 * DT, 1}, Opnd{S(sXN), XK, 1}, kTile / 16, XK, !first);
+        sm100::mma_commit(bar_d);
+        first = false;
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const uint32_t lo = (uint32_t)(q * 32) << 16;
+    const float scale = rsqrtf((float)DT);
+    const float* const* ib = a.inner_bias[0];
+    const float* const* ln = a.inner_ln[0];
+    uint32_t pd = 0;
+    auto signal = [&]() { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(bar_a); };
+    auto wait_d = [&]() { sm100::mbar_wait(bar_d, pd); pd ^= 1; sm100::tc_fence_after(); };
+    float cs_l1g = 0.f, cs_l1b = 0.f, cs_l2g = 0.f, cs_l2b = 0.f, cs_b2 = 0.f;   // lane c ↔ column c
+    int my_tiles = 0;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++my_tiles) {
+      const long long t = tile * kTile + row;
+      const bool in_range = t < a.T;
+      bool keep = false;
+      if (in_range) {
+        const int b = (int)(t / a.Lp), j = (int)(t % a.Lp);
+        const int n = min(max(a.n_events[b], 0), a.L);
+        keep = (j / a.K) >= (a.Lp - n) / a.K;
+      }
+      // ---- R0: x = h; LN1; dX2 = dmerged ⊙ keep
+      float h[DT], dx2[DT];
+#pragma unroll
+      for (int c = 0; c < DT; c += 4) {
+        float4 hv = make_float4(0.f, 0.f, 0.f, 0.f), dv = hv;
+        if (in_range) hv = reinterpret_cast<const float4*>(a.h_in + t * DT)[c / 4];
+        if (keep) dv = reinterpret_cast<const float4*>(a.dmerged + t * DT)[c / 4];
+        h[c] = hv.x; h[c + 1] = hv.y; h[c + 2] = hv.z; h[c + 3] = hv.w;
+        dx2[c] = dv.x; dx2[c + 1] = dv.y; dx2[c + 2] = dv.z; dx2[c + 3] = dv.w;
+      }
+      float xn[XK], inv1;
+      ln_row<DT>(h, ln[0], ln[1], xn, nullptr, inv1);
+#pragma unroll
+      for (int c = DT; c < XK; ++c) xn[c] = c == DT ? 1.f : 0.f;
+      store_row(sXN, row, XK, xn, XK);
+      store_row(sDX2, row, DT, dx2, DT);
+      signal();
+      // ---- R1: q, k, v; group attention (scratch keeps q|k|v (bf16) and P (fp32) for the peers)
+      wait_d();
+      float qv[DT], kvv[DT];
+      tmem_row<DT>(T_W0 + lo, qv);
+#pragma unroll
+      for (int c = 0; c < DT; ++c) qv[c] += __ldg(ib[0] + c);
+      bf16* qs = sQKV + row * QS;
+#pragma unroll
+      for (int c = 0; c < DT; ++c) qs[c] = __float2bfloat16(qv[c]);
+      tmem_row<DT>(T_W0 + lo + DT, kvv);
+#pragma unroll
+      for (int c = 0; c < DT; ++c) qs[DT + c] = __float2bfloat16(kvv[c] + __ldg(ib[1] + c));
+      tmem_row<DT>(T_W0 + lo + 2 * DT, kvv);
+#pragma unroll
+      for (int c = 0; c < DT; ++c) qs[2 * DT + c] = __float2bfloat16(kvv[c] + __ldg(ib[2] + c));
+      __syncwarp();
+      const int g0 = row - row % KG;
+      const int me = row - g0;
+      float p[KG];
+      {
+        float mx = -INFINITY;
+#pragma unroll
+        for (int jj = 0; jj < KG; ++jj) {
+          const bf16* kr = sQKV + (g0 + jj) * QS + DT;
+          float acc = 0.f;
+#pragma unroll
+          for (int c = 0; c < DT; ++c) acc = fmaf(qv[c], __bfloat162float(kr[c]), acc);
+          p[jj] = acc * scale;
+          mx = fmaxf(mx, p[jj]);
+        }
+        float tot = 0.f;
+#pragma unroll
+        for (int jj = 0; jj < KG; ++jj) { p[jj] = __expf(p[jj] - mx); tot += p[jj]; }
+        const float rinv = 1.f / tot;
+#pragma unroll
+        for (int jj = 0; jj < KG; ++jj) { p[jj] *= rinv; sP[row * KG + jj] = p[jj]; }
+      }
+      float ctx[XK];
+#pragma unroll
+      for (int c = 0; c < DT; ++c) {
+        float acc = 0.f;
+#pragma unroll
+        for (int jj = 0; jj < KG; ++jj) acc = fmaf(p[jj], __bfloat162float(sQKV[(g0 + jj) * QS + 2 * DT + c]), acc);
+        ctx[c] = acc;
+      }
+#pragma unroll
+      for (int c = DT; c < XK; ++c) ctx[c] = c == DT ? 1.f : 0.f;
+      store_row(sCTX, row, XK, ctx, XK);
+      signal();
+      // ---- R2: x1 = h + ctx·Wo + bo; LN2
+      wait_d();
+      float x1[DT];
+      tmem_row<DT>(T_W2 + lo, x1);
+#pragma unroll
+      for (int c = 0; c < DT; ++c) x1[c] += h[c] + __ldg(ib[3] + c);
+      float x1n[XK], inv2;
+      ln_row<DT>(x1, ln[2], ln[3], x1n, nullptr, inv2);
+#pragma unroll
+      for (int c = DT; c < XK; ++c) x1n[c] = c == DT ? 1.f : 0.f;
+      store_row(sX1N, row, XK, x1n, XK);
+      signal();
+      // ---- R3: FFN: gf = GELU(f1), df = (dX2·W2ᵀ) ⊙ GELU'(f1)
+      wait_d();
+#pragma unroll 1
+      for (int c0 = 0; c0 < F4; c0 += 32) {
+        float fv[32], gv[32];
+        tmem_row<32>(T_W0 + lo + c0, fv);
+        tmem_row<32>(T_W1 + lo + c0, gv);
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+          const float z = fv[u] + __ldg(ib[4] + c0 + u);
+          const float tt = tanh_fast(kGeluC * (z + kGeluA * z * z * z));
+          fv[u] = 0.5f * z * (1.f + tt);
+          gv[u] *= 0.5f * (1.f + tt) + 0.5f * z * (1.f - tt * tt) * kGeluC * (1.f + 3.f * kGeluA * z * z);
+        }
+        store_row(sGF, row, F4, fv, 32, c0);
+        store_row(sDF, row, F4, gv, 32, c0);
+      }
+      signal();
+      // ---- R4: LN2 backward → dx1 = dX2 + LN2ᵀ(dx1n)
+      wait_d();
+      float g[DT];
+      tmem_row<DT>(T_W2 + lo, g);                                     // dx1n
+      float mu2 = 0.f;
+#pragma unroll
+      for (int c = 0; c < DT; ++c) mu2 += x1[c];
+      mu2 *= 1.f / DT;
+      float xh[DT], m1 = 0.f, m2 = 0.f;
+#pragma unroll
+      for (int c = 0; c < DT; ++c) {
+        xh[c] = (x1[c] - mu2) * inv2;
+        const float gh = g[c] * __ldg(ln[2] + c);
+        m1 += gh;
+        m2 += gh * xh[c];
+      }
+      m1 *= 1.f / DT;
+      m2 *= 1.f / DT;
+      float dx1[DT], tmp[DT];
+#pragma unroll
+      for (int c = 0; c < DT; ++c) {
+        dx1[c] = dx2[c] + (g[c] * __ldg(ln[2] + c) - m1 - xh[c] * m2) * inv2;
+        tmp[c] = g[c] * xh[c];
+      }
+      cs_l2g += warp_colsum<DT>(tmp);
+      cs_l2b += warp_colsum<DT>(g);
+      cs_b2 += warp_colsum<DT>(dx2);
+      store_row(sDX1, row, DT, dx1, DT);
+      signal();
+      // ---- R5: dctx → group attention backward → dqkv
+      wait_d();
+      float dc[DT];
+      tmem_row<DT>(T_W2 + lo, dc);
+#pragma unroll
+      for (int c = 0; c < DT; ++c) sDC[row * (DT + 1) + c] = dc[c];
+      __syncwarp();
+      {
+        float dp[KG], D = 0.f;
+#pragma unroll
+        for (int jj = 0; jj < KG; ++jj) {
+          const bf16* vr = sQKV + (g0 + jj) * QS + 2 * DT;
+          float acc = 0.f;
+#pragma unroll
+          for (int c = 0; c < DT; ++c) acc = fmaf(dc[c], __bfloat162float(vr[c]), acc);
+          dp[jj] = acc;
+          D += acc * p[jj];
+        }
+#pragma unroll
+        for (int jj = 0; jj < KG; ++jj) sS[row * KG + jj] = p[jj] * (dp[jj] - D) * scale;
+      }
+      __syncwarp();
+      float dqkv[3 * DT];
+#pragma unroll
+      for (int c = 0; c < DT; ++c) {
+        float dq = 0.f, dk = 0.f, dv = 0.f;
+#pragma unroll
+        for (int jj = 0; jj < KG; ++jj) {
+          const bf16* pr = sQKV + (g0 + jj) * QS;
+          dq = fmaf(sS[row * KG + jj], __bfloat162float(pr[DT + c]), dq);
+          dk = fmaf(sS[(g0 + jj) * KG + me], __bfloat162float(pr[c]), dk);
+          dv = fmaf(sP[(g0 + jj) * KG + me], sDC[(g0 + jj) * (DT + 1) + c], dv);
+        }
+        dqkv[c] = dq;
+        dqkv[DT + c] = dk;
+        dqkv[2 * DT + c] = dv;
+      }
+      __syncwarp();
+      store_row(sDQKV, row, 3 * DT, dqkv, 3 * DT);
+      signal();
+      // ---- R6: LN1 backward → dh = dx1 + LN1ᵀ(dxn)
+      wait_d();
+      tmem_row<DT>(T_W2 + lo, g);                                     // dxn
+      float mu1 = 0.f;
+#pragma unroll
+      for (int c = 0; c < DT; ++c) mu1 += h[c];
+      mu1 *= 1.f / DT;
+      m1 = 0.f;
+      m2 = 0.f;
+#pragma unroll
+      for (int c = 0; c < DT; ++c) {
+        xh[c] = (h[c] - mu1) * inv1;
+        const float gh = g[c] * __ldg(ln[0] + c);
+        m1 += gh;
+        m2 += gh * xh[c];
+      }
+      m1 *= 1.f / DT;
+      m2 *= 1.f / DT;
+#pragma unroll
+      for (int c = 0; c < DT; ++c) {
+        dx1[c] += (g[c] * __ldg(ln[0] + c) - m1 - xh[c] * m2) * inv1;
+        tmp[c] = g[c] * xh[c];
+      }
+      cs_l1g += warp_colsum<DT>(tmp);
+      cs_l1b += warp_colsum<DT>(g);
+      if (in_range) {
+        float4* dst = reinterpret_cast<float4*>(a.dh_out + t * DT);
+#pragma unroll
+        for (int c = 0; c < DT; c += 4) dst[c / 4] = make_float4(dx1[c], dx1[c + 1], dx1[c + 2], dx1[c + 3]);
+      }
+    }
+    // ---- flush this CTA's accumulators (gradient slots: 0 w_q,1 b_q,2 w_k,3 b_k,4 w_v,5 b_v,
+    //      6 w_o,7 b_o,8 w1,9 b1,10 w2,11 b2,12 ln1_g,13 ln1_b,14 ln2_g,15 ln2_b)
+    if (my_tiles > 0) {
+      float* const* G = a.g_inner;
+      {   // dW2 [4d][d]: TMEM row f = hidden unit
+        float w[DT];
+        tmem_row<DT>(T_DW2 + lo, w);
+#pragma unroll
+        for (int c = 0; c < DT; ++c) atomicAdd(G[10] + row * DT + c, w[c]);
+      }
+      {   // [dW1ᵀ | db1]: row f = hidden unit
+        float w[XK];
+        tmem_row<XK>(T_DW1 + lo, w);
+#pragma unroll
+        for (int c = 0; c < DT; ++c) atomicAdd(G[8] + c * F4 + row, w[c]);
+        atomicAdd(G[9] + row, w[DT]);
+      }
+      {   // [dWoᵀ | dbo]: row c = output column of W_o (first DT rows valid)
+        float w[XK];
+        tmem_row<XK>(T_DWO + lo, w);
+        if (row < DT) {
+#pragma unroll
+          for (int k = 0; k < DT; ++k) atomicAdd(G[6] + k * DT + row, w[k]);
+          atomicAdd(G[7] + row, w[DT]);
+        }
+      }
+      {   // [dWqkvᵀ | dbqkv]: row o ∈ [0, 3d)
+        float w[XK];
+        tmem_row<XK>(T_DWQ + lo, w);
+        if (row < 3 * DT) {
+          const int which = row / DT, oc = row % DT;
+#pragma unroll
+          for (int k = 0; k < DT; ++k) atomicAdd(G[2 * which] + k * DT + oc, w[k]);
+          atomicAdd(G[2 * which + 1] + oc, w[DT]);
+        }
+      }
+      if (lane < DT) {
+        atomicAdd(G[12] + lane, cs_l1g);
+        atomicAdd(G[13] + lane, cs_l1b);
+        atomicAdd(G[14] + lane, cs_l2g);
+        atomicAdd(G[15] + lane, cs_l2b);
+        atomicAdd(G[11] + lane, cs_b2);
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) sm100::tmem_dealloc<512>(tmem);
+}
+
+template <int DT, int KG>
+int launch_inner_bwd(const FrontArgs& a, cudaStream_t st) {
+  constexpr int XK = DT + 16, F4 = 4 * DT, QS = 3 * DT + 2;
+  const int nW = (8 + 12) * DT * DT;
+  const int smem = nW * 2 + kTile * (3 * XK + 2 * DT + 2 * F4 + QS) * 2 + kTile * KG * 8 + 64;
+  if (smem > 227 * 1024) return (int)cudaErrorInvalidValue;
+  static int done = 0;
+  if (!done) {
+    cudaFuncSetAttribute(fe_inner_bwd_kernel<DT, KG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    done = 1;
+  }
+  const long long ntiles = (a.T + kTile - 1) / kTile;
+  const int grid = (int)std::min<long long>(ntiles, 148);
+  fe_inner_bwd_kernel<DT, KG><<<grid, kThreads, std::max(smem, 116 * 1024), st>>>(a);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+int frontend_inner_bwd(const FrontArgs& a, cudaStream_t st) {
+  if (a.inner_layers != 1) return (int)cudaErrorInvalidValue;
+  if (a.d == 32 && a.K == 4) return launch_inner_bwd<32, 4>(a, st);
+  if (a.d == 16 && a.K == 4) return launch_inner_bwd<16, 4>(a, st);
+  if (a.d == 32 && a.K == 8) return launch_inner_bwd<32, 8>(a, st);
+  if (a.d == 16 && a.K == 8) return launch_inner_bwd<16, 8>(a, st);
+  if (a.d == 32 && a.K == 2) return launch_inner_bwd<32, 2>(a, st);
+  if (a.d == 16 && a.K == 2) return launch_inner_bwd<16, 2>(a, st);
+  return (int)cudaErrorInvalidValue;
+}
+
+}  // namespace longer

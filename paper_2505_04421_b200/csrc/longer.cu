@@ -688,10 +688,23 @@ int backward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs) {
   globals_raw_bwd(ga, st);
   // InnerTrans backward (all-pad groups were zeroed after the last layer).  The fused forward
   // kept only its input h, so the per-stage activations are recomputed here first.
-  if (p.fused_fe && p.IL) TRY(inner_unfused_fwd(c, p));
   float* dxt = p.dmerged;
-  if (p.IL) mul_rows_inplace(dxt, (int)T, d, p.keep, st);
-  for (int i = p.IL - 1; i >= 0; --i) {
+  int first_unfused = p.IL - 1;
+  if (p.fused_fe && p.IL == 1) {
+    FrontArgs f = front_args(c, p, bt);
+    f.h_in = p.h; f.dmerged = p.dmerged; f.dh_out = p.t_dx;
+    const BlockOff& bo = o.inner[0];
+    const long long offs[16] = {bo.w_q, bo.b_q, bo.w_k, bo.b_k, bo.w_v, bo.b_v, bo.w_o, bo.b_o,
+                                bo.w1, bo.b1, bo.w2, bo.b2, bo.ln1_g, bo.ln1_b, bo.ln2_g, bo.ln2_b};
+    for (int i = 0; i < 16; ++i) f.g_inner[i] = c.g(offs[i]);
+    TRY(frontend_inner_bwd(f, st));
+    dxt = p.t_dx;
+    first_unfused = -1;
+  } else if (p.fused_fe && p.IL) {
+    TRY(inner_unfused_fwd(c, p));
+  }
+  if (first_unfused >= 0) mul_rows_inplace(dxt, (int)T, d, p.keep, st);
+  for (int i = first_unfused; i >= 0; --i) {
     const InnerBufs& b = p.in[i];
     const BlockOff& bo = o.inner[i];
     const float* xin = i == 0 ? p.h : p.in[i - 1].out;
