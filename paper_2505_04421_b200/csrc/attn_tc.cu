@@ -1,0 +1,372 @@
+// attn_tc.cu — cross-layer attention on the tensor cores (tcgen05), one CTA per (sample, head).
+//
+// _multi_head_attention + masked_softmax (pkg/src/longrec/attention.py:153-169,
+// pkg/src/longrec/tensors.py:323-351) for the first (cross) layer: the q = k + m query rows
+// (≤ 128, zero-padded to the UMMA M = 128 tile) against the v = G + m key rows, streamed in
+// chunks of 128 keys.  The structured visibility mask (VisRule) is evaluated in registers.
+//
+// Forward: two passes over the key chunks — pass 1 finds the exact row max / sum from S = QKᵀ in
+// TMEM, pass 2 writes normalised P (bf16) to smem and accumulates O += P·V in TMEM — so no
+// accumulator rescaling is needed; LSE and an fp32 copy of O are kept for the backward.
+// Backward (per chunk): S and dP = dO·Vᵀ in TMEM → dS = P ⊙ (dP − D) in smem →
+// dV = Pᵀ·dO, dK = dSᵀ·Q (thread = key row on readout), dQ += dS·K accumulated in TMEM.
+#include "fe_common.cuh"
+#include "ops.cuh"
+
+#include <algorithm>
+
+namespace longer {
+
+using namespace fe;
+
+namespace {
+
+constexpr int kC = 128;     // keys per chunk
+
+// thread `row` copies row `row` of a [rows x DH] bf16 matrix into a canonical K-major tile
+template <int DH>
+__device__ __forceinline__ void load_rows_bf16(bf16* tile, const bf16* src, int ld, int row, int nrows) {
+#pragma unroll
+  for (int c = 0; c < DH; c += 8) {
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (row < nrows) v = *reinterpret_cast<const uint4*>(src + (long long)row * ld + c);
+    *reinterpret_cast<uint4*>(tile + canon(row, c, DH)) = v;
+  }
+}
+
+template <int DH>
+__global__ void __launch_bounds__(kThreads, 1) xattn_fwd_kernel(AttnArgs a) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  bf16* sQ = reinterpret_cast<bf16*>(smem_raw);
+  bf16* sK = sQ + 128 * DH;
+  bf16* sV = sK + kC * DH;
+  bf16* sP = sV + kC * DH;                        // 128 x kC
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 128 * kC);
+  uint64_t* bar_a = bars;
+  uint64_t* bar_d = bars + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+  const int b = blockIdx.x / a.heads, hd = blockIdx.x % a.heads;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    sm100::mbar_init(bar_a, 32 * kWorkers);
+    sm100::mbar_init(bar_d, 1);
+    sm100::fence_barrier_init();
+  }
+  if (warp == 0) sm100::tmem_alloc<256>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t T_S = tmem, T_O = tmem + 128;
+  const int nchunk = (a.nk + kC - 1) / kC;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t aQ = sm100::smem_u32(sQ), aK = sm100::smem_u32(sK), aV = sm100::smem_u32(sV);
+      const uint32_t aP = sm100::smem_u32(sP);
+      uint32_t pa = 0;
+      auto wait_a = [&]() { sm100::mbar_wait(bar_a, pa); pa ^= 1; sm100::tc_fence_after(); };
+      for (int c = 0; c < nchunk; ++c) {            // pass 1: S for the statistics
+        wait_a();
+        mma(T_S, Opnd{aQ, DH, 0}, Opnd{aK, DH, 0}, DH / 16, kC, false);
+        sm100::mma_commit(bar_d);
+      }
+      for (int c = 0; c < nchunk; ++c) {            // pass 2: P, O += P·V
+        wait_a();
+        mma(T_S, Opnd{aQ, DH, 0}, Opnd{aK, DH, 0}, DH / 16, kC, false);
+        sm100::mma_commit(bar_d);
+        wait_a();
+        mma(T_O, Opnd{aP, kC, 0}, Opnd{aV, DH, 1}, kC / 16, DH, c > 0);
+        sm100::mma_commit(bar_d);
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const uint32_t lo = (uint32_t)(q * 32) << 16;
+    const float scale = rsqrtf((float)(a.D / a.heads));
+    const VisRule vis{a.k, a.G, a.ns, a.goff, a.npg[b]};
+    const bf16* Qb = a.Q + b * a.sq + hd * DH;
+    const bf16* Kb = a.Kp + b * a.sk + hd * DH;
+    const bf16* Vb = a.V + b * a.sv + hd * DH;
+    uint32_t pd = 0;
+    auto signal = [&]() { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(bar_a); };
+    auto wait_d = [&]() { sm100::mbar_wait(bar_d, pd); pd ^= 1; sm100::tc_fence_after(); };
+    load_rows_bf16<DH>(sQ, Qb, a.ldq, row, a.nq);
+    const bool qrow = row < a.nq;
+    float m = -INFINITY, l = 0.f;
+    for (int c = 0; c < nchunk; ++c) {
+      const int c0 = c * kC;
+      load_rows_bf16<DH>(sK, Kb + (long long)c0 * a.ldk, a.ldk, row, a.nk - c0);
+      signal();
+      wait_d();
+#pragma unroll 1
+      for (int j0 = 0; j0 < kC; j0 += 32) {
+        float s[32];
+        tmem_row<32>(T_S + lo + j0, s);
+        if (!qrow) continue;
+        float cm = -INFINITY;
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+          const int key = c0 + j0 + u;
+          s[u] = (key < a.nk && vis(row, key)) ? s[u] * scale : -INFINITY;
+          cm = fmaxf(cm, s[u]);
+        }
+        if (cm == -INFINITY) continue;
+        const float mn = fmaxf(m, cm);
+        float add = 0.f;
+#pragma unroll
+        for (int u = 0; u < 32; ++u) add += __expf(s[u] - mn);
+        l = l * __expf(m - mn) + add;
+        m = mn;
+      }
+    }
+    const float rl = l > 0.f ? 1.f / l : 0.f;
+    for (int c = 0; c < nchunk; ++c) {
+      const int c0 = c * kC;
+      load_rows_bf16<DH>(sK, Kb + (long long)c0 * a.ldk, a.ldk, row, a.nk - c0);
+      load_rows_bf16<DH>(sV, Vb + (long long)c0 * a.ldv, a.ldv, row, a.nk - c0);
+      signal();
+      wait_d();
+#pragma unroll 1
+      for (int j0 = 0; j0 < kC; j0 += 32) {
+        float s[32];
+        tmem_row<32>(T_S + lo + j0, s);
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+          const int key = c0 + j0 + u;
+          s[u] = (qrow && l > 0.f && key < a.nk && vis(row, key)) ? __expf(s[u] * scale - m) * rl : 0.f;
+        }
+        store_row(sP, row, kC, s, 32, j0);
+      }
+      signal();
+      wait_d();
+    }
+    float o[DH];
+    tmem_row<DH>(T_O + lo, o);
+    if (qrow) {
+      bf16* dst = a.ctx + b * a.sc + (long long)row * a.ldc + hd * DH;
+      float* dst32 = a.ctx32 + b * a.sc + (long long)row * a.ldc + hd * DH;
+#pragma unroll
+      for (int c = 0; c < DH; c += 8) {
+        uint4 pk;
+        pk.x = sm100::pack_bf16(o[c], o[c + 1]); pk.y = sm100::pack_bf16(o[c + 2], o[c + 3]);
+        pk.z = sm100::pack_bf16(o[c + 4], o[c + 5]); pk.w = sm100::pack_bf16(o[c + 6], o[c + 7]);
+        *reinterpret_cast<uint4*>(dst + c) = pk;
+        *reinterpret_cast<float4*>(dst32 + c) = make_float4(o[c], o[c + 1], o[c + 2], o[c + 3]);
+        *reinterpret_cast<float4*>(dst32 + c + 4) = make_float4(o[c + 4], o[c + 5], o[c + 6], o[c + 7]);
+      }
+      a.lse[((long long)b * a.heads + hd) * a.nq + row] = l > 0.f ? m + __logf(l) : -INFINITY;
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) sm100::tmem_dealloc<256>(tmem);
+}
+
+template <int DH>
+__global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  bf16* sQ = reinterpret_cast<bf16*>(smem_raw);
+  bf16* sdO = sQ + 128 * DH;
+  bf16* sK = sdO + 128 * DH;
+  bf16* sV = sK + kC * DH;
+  bf16* sP = sV + kC * DH;                        // 128 x kC
+  bf16* sdS = sP + 128 * kC;                      // 128 x kC  (pre-scaled by 1/sqrt(dh))
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sdS + 128 * kC);
+  uint64_t* bar_a = bars;
+  uint64_t* bar_d = bars + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+  const int b = blockIdx.x / a.heads, hd = blockIdx.x % a.heads;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    sm100::mbar_init(bar_a, 32 * kWorkers);
+    sm100::mbar_init(bar_d, 1);
+    sm100::fence_barrier_init();
+  }
+  if (warp == 0) sm100::tmem_alloc<512>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t T_A = tmem, T_B = tmem + 128, T_DQ = tmem + 256;
+  const int nchunk = (a.nk + kC - 1) / kC;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t aQ = sm100::smem_u32(sQ), adO = sm100::smem_u32(sdO), aK = sm100::smem_u32(sK);
+      const uint32_t aV = sm100::smem_u32(sV), aP = sm100::smem_u32(sP), adS = sm100::smem_u32(sdS);
+      uint32_t pa = 0;
+      auto wait_a = [&]() { sm100::mbar_wait(bar_a, pa); pa ^= 1; sm100::tc_fence_after(); };
+      for (int c = 0; c < nchunk; ++c) {                            // pass 1: D = Σ_j P·dP
+        wait_a();
+        mma(T_A, Opnd{aQ, DH, 0}, Opnd{aK, DH, 0}, DH / 16, kC, false);
+        mma(T_B, Opnd{adO, DH, 0}, Opnd{aV, DH, 0}, DH / 16, kC, false);
+        sm100::mma_commit(bar_d);
+      }
+      for (int c = 0; c < nchunk; ++c) {
+        wait_a();                                                   // K, V chunk (+ Q, dO)
+        mma(T_A, Opnd{aQ, DH, 0}, Opnd{aK, DH, 0}, DH / 16, kC, false);      // S
+        mma(T_B, Opnd{adO, DH, 0}, Opnd{aV, DH, 0}, DH / 16, kC, false);     // dP
+        sm100::mma_commit(bar_d);
+        wait_a();                                                   // P, dS
+        mma(T_A, Opnd{aP, kC, 1}, Opnd{adO, DH, 1}, 128 / 16, DH, false);    // dV = Pᵀ·dO
+        mma(T_B, Opnd{adS, kC, 1}, Opnd{aQ, DH, 1}, 128 / 16, DH, false);    // dK = dSᵀ·Q
+        mma(T_DQ, Opnd{adS, kC, 0}, Opnd{aK, DH, 1}, kC / 16, DH, c > 0);    // dQ += dS·K
+        sm100::mma_commit(bar_d);
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const uint32_t lo = (uint32_t)(q * 32) << 16;
+    const float scale = rsqrtf((float)(a.D / a.heads));
+    const VisRule vis{a.k, a.G, a.ns, a.goff, a.npg[b]};
+    const bf16* Qb = a.Q + b * a.sq + hd * DH;
+    const bf16* Kb = a.Kp + b * a.sk + hd * DH;
+    const bf16* Vb = a.V + b * a.sv + hd * DH;
+    uint32_t pd = 0;
+    auto signal = [&]() { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(bar_a); };
+    auto wait_d = [&]() { sm100::mbar_wait(bar_d, pd); pd ^= 1; sm100::tc_fence_after(); };
+    const bool qrow = row < a.nq;
+    load_rows_bf16<DH>(sQ, Qb, a.ldq, row, a.nq);
+    // dO (fp32) → bf16 tile
+    float Di = 0.f, lse = -INFINITY;
+    {
+      const float* dOr = a.dctx + b * a.sdc + (long long)row * a.lddc + hd * DH;
+#pragma unroll
+      for (int c = 0; c < DH; c += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = qrow ? dOr[c + u] : 0.f;
+        store_row(sdO, row, DH, v, 8, c);
+      }
+      if (qrow) lse = a.lse[((long long)b * a.heads + hd) * a.nq + row];
+    }
+    // pass 1: D_i = Σ_j P_ij dP_ij with exactly the P and dP of pass 2, so that Σ_j dS_ij = 0
+    // holds to rounding (D = rowsum(dO ⊙ O) would mix the bf16 roundings of dO, P and V).
+    for (int c = 0; c < nchunk; ++c) {
+      const int c0 = c * kC;
+      load_rows_bf16<DH>(sK, Kb + (long long)c0 * a.ldk, a.ldk, row, a.nk - c0);
+      load_rows_bf16<DH>(sV, Vb + (long long)c0 * a.ldv, a.ldv, row, a.nk - c0);
+      signal();
+      wait_d();
+#pragma unroll 1
+      for (int j0 = 0; j0 < kC; j0 += 32) {
+        float s[32], dp[32];
+        tmem_row<32>(T_A + lo + j0, s);
+        tmem_row<32>(T_B + lo + j0, dp);
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+          const int key = c0 + j0 + u;
+          const bool ok = qrow && lse != -INFINITY && key < a.nk && vis(row, key);
+          if (ok) Di = fmaf(__expf(s[u] * scale - lse), dp[u], Di);
+        }
+      }
+    }
+    for (int c = 0; c < nchunk; ++c) {
+      const int c0 = c * kC;
+      load_rows_bf16<DH>(sK, Kb + (long long)c0 * a.ldk, a.ldk, row, a.nk - c0);
+      load_rows_bf16<DH>(sV, Vb + (long long)c0 * a.ldv, a.ldv, row, a.nk - c0);
+      signal();
+      wait_d();
+#pragma unroll 1
+      for (int j0 = 0; j0 < kC; j0 += 32) {
+        float s[32], dp[32];
+        tmem_row<32>(T_A + lo + j0, s);
+        tmem_row<32>(T_B + lo + j0, dp);
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+          const int key = c0 + j0 + u;
+          const bool ok = qrow && lse != -INFINITY && key < a.nk && vis(row, key);
+          const float p = ok ? __expf(s[u] * scale - lse) : 0.f;
+          s[u] = p;
+          dp[u] = p * (dp[u] - Di) * scale;
+        }
+        store_row(sP, row, kC, s, 32, j0);
+        store_row(sdS, row, kC, dp, 32, j0);
+      }
+      signal();
+      wait_d();
+      // thread = key row: dV, dK of key c0 + row, 32 columns at a time
+      const bool krow = c0 + row < a.nk;
+      bf16* pv = a.dV + b * a.sdv + (long long)(c0 + row) * a.lddv + hd * DH;
+      bf16* pk = a.dK + b * a.sdk + (long long)(c0 + row) * a.lddk + hd * DH;
+#pragma unroll 1
+      for (int c1 = 0; c1 < DH; c1 += 32) {
+        float dv[32], dk[32];
+        tmem_row<32>(T_A + lo + c1, dv);
+        tmem_row<32>(T_B + lo + c1, dk);
+        if (!krow) continue;
+#pragma unroll
+        for (int cc = 0; cc < 32; cc += 8) {
+          uint4 x, y;
+          x.x = sm100::pack_bf16(dv[cc], dv[cc + 1]); x.y = sm100::pack_bf16(dv[cc + 2], dv[cc + 3]);
+          x.z = sm100::pack_bf16(dv[cc + 4], dv[cc + 5]); x.w = sm100::pack_bf16(dv[cc + 6], dv[cc + 7]);
+          y.x = sm100::pack_bf16(dk[cc], dk[cc + 1]); y.y = sm100::pack_bf16(dk[cc + 2], dk[cc + 3]);
+          y.z = sm100::pack_bf16(dk[cc + 4], dk[cc + 5]); y.w = sm100::pack_bf16(dk[cc + 6], dk[cc + 7]);
+          *reinterpret_cast<uint4*>(pv + c1 + cc) = x;
+          *reinterpret_cast<uint4*>(pk + c1 + cc) = y;
+        }
+      }
+    }
+    float dq[DH];
+    tmem_row<DH>(T_DQ + lo, dq);
+    if (qrow) {
+      bf16* pq = a.dQ + b * a.sdq + (long long)row * a.lddq + hd * DH;
+#pragma unroll
+      for (int cc = 0; cc < DH; cc += 8) {
+        uint4 x;
+        x.x = sm100::pack_bf16(dq[cc], dq[cc + 1]); x.y = sm100::pack_bf16(dq[cc + 2], dq[cc + 3]);
+        x.z = sm100::pack_bf16(dq[cc + 4], dq[cc + 5]); x.w = sm100::pack_bf16(dq[cc + 6], dq[cc + 7]);
+        *reinterpret_cast<uint4*>(pq + cc) = x;
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) sm100::tmem_dealloc<512>(tmem);
+}
+
+template <int DH>
+int launch_fwd(const AttnArgs& a, cudaStream_t st) {
+  const int smem = (128 * DH + 2 * kC * DH + 128 * kC) * 2 + 64;
+  static int done = 0;
+  if (!done) { cudaFuncSetAttribute(xattn_fwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); done = 1; }
+  xattn_fwd_kernel<DH><<<a.B * a.heads, kThreads, std::max(smem, 116 * 1024), st>>>(a);
+  return (int)cudaGetLastError();
+}
+
+template <int DH>
+int launch_bwd(const AttnArgs& a, cudaStream_t st) {
+  const int smem = (2 * 128 * DH + 2 * kC * DH + 2 * 128 * kC) * 2 + 64;
+  static int done = 0;
+  if (!done) { cudaFuncSetAttribute(xattn_bwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); done = 1; }
+  xattn_bwd_kernel<DH><<<a.B * a.heads, kThreads, std::max(smem, 116 * 1024), st>>>(a);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+int attn_tc_supported(const AttnArgs& a) {
+  const int dh = a.D / a.heads;
+  return a.nq <= 128 && (dh == 32 || dh == 64 || dh == 128);
+}
+
+int attn_tc_fwd(const AttnArgs& a, cudaStream_t st) {
+  const int dh = a.D / a.heads;
+  if (dh == 128) return launch_fwd<128>(a, st);
+  if (dh == 64) return launch_fwd<64>(a, st);
+  if (dh == 32) return launch_fwd<32>(a, st);
+  return (int)cudaErrorInvalidValue;
+}
+
+int attn_tc_bwd(const AttnArgs& a, cudaStream_t st) {
+  const int dh = a.D / a.heads;
+  if (dh == 128) return launch_bwd<128>(a, st);
+  if (dh == 64) return launch_bwd<64>(a, st);
+  if (dh == 32) return launch_bwd<32>(a, st);
+  return (int)cudaErrorInvalidValue;
+}
+
+}  // namespace longer

@@ -389,6 +389,12 @@ int pack_weights(const Plan& p, const float* params, void* ws, cudaStream_t st) 
 }
 
 // ------------------------------------------------------------------ forward
+bool use_attn_tc(const AttnArgs& a) {
+  const char* env = std::getenv("LONGER_ATTN_TC");
+  if (env && env[0] == '0') return false;
+  return attn_tc_supported(a) != 0;
+}
+
 // One pre-norm attention block over the q query rows (pkg/src/longrec/attention.py:172-212).
 int block_fwd(const Ctx& c, const BlockOff& bo, BlockBufs& b, const float* xq, bool cross, const bf16* Wqkv,
               const float* bqkv, const bf16* Wo, const bf16* W1, const bf16* W2) {
@@ -419,7 +425,7 @@ int block_fwd(const Ctx& c, const BlockOff& bo, BlockBufs& b, const float* xq, b
     a.V = b.qkv + 2 * D; a.ldv = 3 * D; a.sv = a.sq;
     a.nk = p.q; a.ns = p.k; a.goff = p.G - p.k;
   }
-  attn_fwd(a, st);
+  if (cross && use_attn_tc(a)) TRY(attn_tc_fwd(a, st)); else attn_fwd(a, st);
   TRY(lin_fwd(st, b.ctx, D, Q, Wo, D, D, c.w(bo.b_o), 0, b.x1, nullptr, nullptr, xq, D));
   layernorm_fwd(rows_plain(b.x1, D, Q), D, c.w(bo.ln2_g), c.w(bo.ln2_b), b.x1n, b.m2, b.r2, st);
   TRY(lin_fwd(st, b.x1n, D, Q, W1, D, 4 * D, c.w(bo.b1), EPI_GELU | EPI_SAVE_PRE, nullptr, b.gf, b.f1));
@@ -608,7 +614,7 @@ int block_bwd(const Ctx& c, const BlockOff& bo, const BlockBufs& b, const float*
     a.dK = p.dqkv + D; a.lddk = 3 * D; a.sdk = a.sdq;
     a.dV = p.dqkv + 2 * D; a.lddv = 3 * D; a.sdv = a.sdq;
   }
-  attn_bwd(a, st);
+  if (cross && use_attn_tc(a)) TRY(attn_tc_bwd(a, st)); else attn_bwd(a, st);
   if (cross) {
     TRY(lin_dx(st, p.dqkv, D, Q, Wqkv, D, D, D, p.dqn, D, nullptr, 0));
     TRY(lin_dw(st, b.qn, D, D, p.dqkv, D, D, Q, c.g(bo.w_q)));

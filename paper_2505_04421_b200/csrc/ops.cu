@@ -853,10 +853,17 @@ __global__ void head_fwd_kernel(HeadArgs a) {
       const float p = z >= 0.f ? 1.f / (1.f + e) : e / (1.f + e);
       a.probs[b] = p;
       if (a.loss_per) {
+        // bce with the reference's clamp p_c = clip(p, 1e-12, 1-1e-12) (tensors.py:551-571),
+        // evaluated in log-odds space: 1 - 1e-12 is not representable in fp32, but
+        // log p = -softplus(-z) and log(1-p) = -softplus(z) are, and clamping p at 1e-12 is
+        // clamping the log at log(1e-12); the clamp's zero-gradient region is |z| ≥ logit(1-1e-12).
         const float y = a.label[b];
-        const float pc = fminf(fmaxf(p, kProbEps), 1.f - kProbEps);
-        a.loss_per[b] = -(y * __logf(pc) + (1.f - y) * __logf(1.f - pc));
-        const bool inr = p > kProbEps && p < 1.f - kProbEps;
+        const float kLog12 = -27.631021115928547f;          // log(1e-12)
+        const float sp_pos = fmaxf(z, 0.f) + log1pf(__expf(-fabsf(z)));    // softplus(z)
+        const float sp_neg = sp_pos - z;                                   // softplus(-z)
+        const float log_p = fmaxf(-sp_neg, kLog12), log_q = fmaxf(-sp_pos, kLog12);
+        a.loss_per[b] = -(y * log_p + (1.f - y) * log_q);
+        const bool inr = fabsf(z) < 27.631021115928547f;
         a.dz[b] = inr ? (p - y) / (float)a.B : 0.f;
       }
     }

@@ -95,6 +95,10 @@ struct AttnArgs {
 };
 void attn_fwd(const AttnArgs& a, cudaStream_t st);
 void attn_bwd(const AttnArgs& a, cudaStream_t st);
+// tcgen05 versions for the cross layer (attn_tc.cu): q ≤ 128 query rows, head width 32/64/128
+int attn_tc_supported(const AttnArgs& a);
+int attn_tc_fwd(const AttnArgs& a, cudaStream_t st);
+int attn_tc_bwd(const AttnArgs& a, cudaStream_t st);
 
 // ---------------------------------------------------------------- globals + head
 struct GlobalsArgs {

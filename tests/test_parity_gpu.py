@@ -115,3 +115,21 @@ def test_matches_oracle_on_synthetic(kw, B, min_events):
     # inference entry point (fused front-end when the shape allows it)
     pf = model.forward(batch).cpu().numpy().astype(np.float64)
     assert np.max(np.abs(pf - p_ref)) <= 5e-3, np.abs(pf - p_ref)
+
+
+@pytest.mark.parametrize("bias", [20.0, 40.0, -40.0, -25.0])
+def test_saturated_logits_follow_the_reference_clamp(bias):
+    """p = sigmoid(z) saturates in fp32 long before the reference's 1e-12 clamp does; the loss and
+    the clamp's zero-gradient region must still follow tensors.py:551-571 (float64)."""
+    cfg = ModelConfig(L=48, d=8, K=2, k=6, N=1, n_users=40).validate()
+    from paper_2505_04421_b200.params import init_params
+    P = init_params(cfg, seed=0)
+    P["head.b2"] = P["head.b2"] + bias
+    batch = synthetic_batch(cfg, 4, seed=3)
+    p_ref, loss_ref, G = O.forward_backward(P, cfg, batch.as_dict())
+    model = _model(cfg, P)
+    p, loss, grads = _run(model, batch)
+    assert np.isfinite(loss)
+    assert abs(loss - loss_ref) <= 1e-3 * abs(loss_ref) + 1e-3, (loss, loss_ref)
+    assert_grads_close(grads, {n: G[n] for n in ("head.b2", "head.w2", "head.w1", "cross.w_v", "tables.item_table")},
+                       f"bias {bias}")
