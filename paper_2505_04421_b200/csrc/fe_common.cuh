@@ -24,11 +24,14 @@ __host__ __device__ __forceinline__ int canon(int row, int k, int Kdim) {
 }
 
 // element offsets of every weight image inside the packed blob (forward images WxT = [out][in],
-// backward images Wx_n = [in][out], both canonical K-major)
+// backward images Wx_n = [in][out], both canonical K-major).  Forward images whose activation
+// tile carries a ones column get one extra K row holding the bias ("bias-augmented", K = d + 16,
+// bias at k = d; for W_tp the bias sits in the spare feature column k = 31), so those biases are
+// added by the tensor core instead of the epilogue.
 struct BlobOff {
-  int tp, w1, w2;                       // forward: Wtpᵀ [d][32], W1ᵀ [2D][d], W2ᵀ [d][2D]
+  int tp, w1, w2;                       // forward: [Wtpᵀ|b] [d][32], [W1ᵀ|b1] [2D][d+16], W2ᵀ [d][2D]
   int tp_n, w1_n, w2_n;                 // backward: Wtp [32][d], W1 [d][2D], W2 [2D][d]
-  int qkv[8], wo[8], w1i[8], w2i[8];    // forward inner: [3d][d], [d][d], [4d][d], [d][4d]
+  int qkv[8], wo[8], w1i[8], w2i[8];    // forward inner: [3d][d+16], [d][d], [4d][d+16], [d][4d]
   int qkv_n[8], wo_n[8], w1i_n[8], w2i_n[8];  // backward inner: [d][3d], [d][d], [d][4d], [4d][d]
   int fwd_total, total;
 };
@@ -36,13 +39,14 @@ struct BlobOff {
 __host__ __device__ inline BlobOff blob_offsets(int d, int D, int IL) {
   BlobOff o;
   int off = 0;
+  const int XK = d + 16;
   o.tp = off; off += d * kFP;
-  o.w1 = off; off += 2 * D * d;
+  o.w1 = off; off += 2 * D * XK;
   o.w2 = off; off += d * 2 * D;
   for (int l = 0; l < IL; ++l) {
-    o.qkv[l] = off; off += 3 * d * d;
+    o.qkv[l] = off; off += 3 * d * XK;
     o.wo[l] = off; off += d * d;
-    o.w1i[l] = off; off += 4 * d * d;
+    o.w1i[l] = off; off += 4 * d * XK;
     o.w2i[l] = off; off += d * 4 * d;
   }
   o.fwd_total = off;

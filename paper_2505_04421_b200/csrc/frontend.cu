@@ -23,7 +23,7 @@ namespace {
 // ------------------------------------------------------------------ weight packing
 struct PackW {
   int n;
-  struct { long long src; int in, out, trans, n_off, k_off, Kdim, dst; } s[48];
+  struct { long long src; int in, out, trans, n_off, k_off, Kdim, dst; } s[96];
 };
 
 // trans = 1: image of Wᵀ ([out][in]: element (n=j, k=i) = W[i][j]); trans = 0: image of W as
@@ -88,6 +88,26 @@ __device__ __forceinline__ void featurise(const FrontArgs& a, const TokenInfo& t
   }
 }
 
+// table[id][0:width] += v[off : off+width] for every lane with id ≥ 0, summing lanes that share an id
+// with warp shuffles first (one shared atomic per distinct id and column).
+__device__ __forceinline__ void warp_scatter_add(float* table, int id, const float (&v)[kFP], int off, int width) {
+  const int lane = threadIdx.x & 31;
+  unsigned pending = __ballot_sync(0xffffffffu, id >= 0);
+  while (pending) {
+    const int leader = __ffs(pending) - 1;
+    const int key = __shfl_sync(0xffffffffu, id, leader);
+    const unsigned grp = __ballot_sync(0xffffffffu, id == key);
+#pragma unroll
+    for (int c = 0; c < kFP; ++c) {
+      if (c >= off && c < off + width) {                  // warp-uniform
+        const float s = warp_sum(id == key ? v[c] : 0.f);
+        if (lane == leader) atomicAdd(table + key * width + (c - off), s);
+      }
+    }
+    pending &= ~grp;
+  }
+}
+
 __device__ __forceinline__ void load_blob(uint8_t* dst_smem, const uint8_t* src, int bytes, uint64_t* bar) {
   for (int off = 0; off < bytes; off += 32768) {
     const int n = min(32768, bytes - off);
@@ -104,10 +124,11 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
   constexpr int D = DT * KG;
   constexpr int H2 = 2 * D;                        // token-MLP hidden width
   constexpr int nh = H2 / 128;                     // 128-column halves of the hidden
+  constexpr int XK = DT + 16;                      // activation tile row: [x | 1 | 0…] (bias column)
   const BlobOff bo = blob_offsets(DT, D, a.inner_layers);
   bf16* sW = reinterpret_cast<bf16*>(smem_raw);
-  bf16* sA = sW + ((bo.fwd_total + 63) & ~63);             // 128 x 32 bf16
-  bf16* sH = sA + kTile * kFP;                             // 128 x 128 bf16 (also fp32 k/v scratch)
+  bf16* sA = sW + ((bo.fwd_total + 63) & ~63);             // 128 x XK bf16 (feat uses 128 x 32)
+  bf16* sH = sA + kTile * XK;                              // 128 x 128 bf16 (also fp32 k/v scratch)
   float* sKV = reinterpret_cast<float*>(sH);               // 128 x (2*DT+1) fp32
   uint64_t* bars = reinterpret_cast<uint64_t*>(sH + kTile * 136);
   uint64_t* bar_w = bars;
@@ -141,27 +162,27 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
       auto W = [&](int off, int kdim) { return Opnd{wW + off * 2, kdim, 0}; };
       const uint32_t accH = tmem + 128;          // h / f2 accumulator columns
       for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        wait_a();                                // feat
+        wait_a();                                // [feat | 1]
         mma(tmem, Opnd{wA, kFP, 0}, W(bo.tp, kFP), kFP / 16, DT, false);
         sm100::mma_commit(bar_d);
-        wait_a();                                // x0
-        mma(tmem, Opnd{wA, DT, 0}, W(bo.w1, DT), DT / 16, 128, false);
+        wait_a();                                // [x0 | 1]
+        mma(tmem, Opnd{wA, XK, 0}, W(bo.w1, XK), XK / 16, 128, false);
         sm100::mma_commit(bar_d);
         for (int j = 0; j < nh; ++j) {
           wait_a();                              // GELU(a1 half j) in sH
           mma(accH, Opnd{wH, 128, 0}, W(bo.w2 + canon(0, 128 * j, H2), H2), 8, DT, j > 0);
-          if (j + 1 < nh) mma(tmem, Opnd{wA, DT, 0}, W(bo.w1 + canon(128 * (j + 1), 0, DT), DT), DT / 16, 128, false);
+          if (j + 1 < nh) mma(tmem, Opnd{wA, XK, 0}, W(bo.w1 + canon(128 * (j + 1), 0, XK), XK), XK / 16, 128, false);
           sm100::mma_commit(bar_d);
         }
         for (int l = 0; l < a.inner_layers; ++l) {
-          wait_a();                              // LN1(x)
-          mma(tmem, Opnd{wA, DT, 0}, W(bo.qkv[l], DT), DT / 16, 3 * DT, false);
+          wait_a();                              // [LN1(x) | 1]
+          mma(tmem, Opnd{wA, XK, 0}, W(bo.qkv[l], XK), XK / 16, 3 * DT, false);
           sm100::mma_commit(bar_d);
           wait_a();                              // ctx
-          mma(tmem, Opnd{wA, DT, 0}, W(bo.wo[l], DT), DT / 16, DT, false);
+          mma(tmem, Opnd{wA, XK, 0}, W(bo.wo[l], DT), DT / 16, DT, false);
           sm100::mma_commit(bar_d);
-          wait_a();                              // LN2(x1)
-          mma(tmem, Opnd{wA, DT, 0}, W(bo.w1i[l], DT), DT / 16, 4 * DT, false);
+          wait_a();                              // [LN2(x1) | 1]
+          mma(tmem, Opnd{wA, XK, 0}, W(bo.w1i[l], XK), XK / 16, 4 * DT, false);
           sm100::mma_commit(bar_d);
           wait_a();                              // GELU(f1)
           mma(accH, Opnd{wH, 4 * DT, 0}, W(bo.w2i[l], 4 * DT), 4 * DT / 16, DT, false);
@@ -178,6 +199,9 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
     uint32_t pd = 0;
     auto signal = [&]() { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(bar_a); };
     auto wait_d = [&]() { sm100::mbar_wait(bar_d, pd); pd ^= 1; sm100::tc_fence_after(); };
+    float b2[DT];                                  // narrow biases live in registers
+#pragma unroll
+    for (int c = 0; c < DT; ++c) b2[c] = __ldg(a.seq_b2 + c);
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const TokenInfo ti = token_info(a, tile, row);
       if (ti.in_range && ti.j == 0 && a.npg) a.npg[ti.b] = (a.Lp - ti.n) / a.K;
@@ -188,18 +212,32 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
       float v[kFP];
       int ids[3];
       featurise(a, ti, v, ids, true);
+      v[kFP - 1] = 1.f;                            // bias column (b_tp rides in the W_tp image)
       store_row(sA, row, kFP, v, kFP);
       signal();
-      // x0 = feat·W_tp + b_tp + abs_pos[recency]
-      float x[DT];
-      wait_d();
-      tmem_row<DT>(trow, x);
+      // abs-pos row: issued before waiting for the MMA so the gather overlaps it
+      float x[XK];
+      {
+        const float4* pp = reinterpret_cast<const float4*>(a.pos_tab + (long long)ti.rec * DT);
 #pragma unroll
-      for (int c = 0; c < DT; ++c)
-        x[c] = ti.real ? x[c] + __ldg(a.tok_b + c) + __ldg(a.pos_tab + (long long)ti.rec * DT + c) : 0.f;
-      store_row(sA, row, DT, x, DT);
+        for (int c = 0; c < DT; c += 4) {
+          const float4 p4 = __ldg(pp + c / 4);
+          x[c] = p4.x; x[c + 1] = p4.y; x[c + 2] = p4.z; x[c + 3] = p4.w;
+        }
+      }
+      // x0 = [feat | 1]·[W_tp ; b_tp] + abs_pos[recency]
+      wait_d();
+      {
+        float acc[DT];
+        tmem_row<DT>(trow, acc);
+#pragma unroll
+        for (int c = 0; c < DT; ++c) x[c] = ti.real ? x[c] + acc[c] : 0.f;
+      }
+#pragma unroll
+      for (int c = DT; c < XK; ++c) x[c] = c == DT ? 1.f : 0.f;
+      store_row(sA, row, XK, x, XK);
       signal();
-      // token MLP: GELU(x0·W1 + b1) (128-column halves → sH) · W2 accumulates in TMEM
+      // token MLP: GELU([x0 | 1]·[W1 ; b1]) (128-column halves → sH) · W2 accumulates in TMEM
       for (int hj = 0; hj < nh; ++hj) {
         wait_d();
 #pragma unroll 1
@@ -207,7 +245,7 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
           float hv[32];
           tmem_row<32>(trow + c0, hv);
 #pragma unroll
-          for (int u = 0; u < 32; ++u) hv[u] = gelu_f(hv[u] + __ldg(a.seq_b1 + 128 * hj + c0 + u));
+          for (int u = 0; u < 32; ++u) hv[u] = gelu_f(hv[u]);
           store_row(sH, row, 128, hv, 32, c0);
         }
         signal();
@@ -216,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
       float h[DT];
       tmem_row<DT>(trow + 128, h);
 #pragma unroll
-      for (int c = 0; c < DT; ++c) h[c] = ti.real ? h[c] + __ldg(a.seq_b2 + c) : 0.f;
+      for (int c = 0; c < DT; ++c) h[c] = ti.real ? h[c] + b2[c] : 0.f;
       if (a.h_out && ti.in_range) {
         float4* dst = reinterpret_cast<float4*>(a.h_out + ti.t * DT);
 #pragma unroll
@@ -225,24 +263,24 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
       for (int l = 0; l < a.inner_layers; ++l) {
         const float* const* ib = a.inner_bias[l];
         const float* const* ln = a.inner_ln[l];
-        float xn[DT], inv;
+        float xn[XK], inv;
         ln_row<DT>(h, ln[0], ln[1], xn, nullptr, inv);
-        store_row(sA, row, DT, xn, DT);
+#pragma unroll
+        for (int c = DT; c < XK; ++c) xn[c] = c == DT ? 1.f : 0.f;
+        store_row(sA, row, XK, xn, XK);
         signal();
         wait_d();
         float qv[DT];
-        tmem_row<DT>(trow, qv);
+        tmem_row<DT>(trow, qv);                    // q, k, v already carry their biases
         {
           float kv[DT];
           tmem_row<DT>(trow + DT, kv);
 #pragma unroll
-          for (int c = 0; c < DT; ++c) sKV[row * (2 * DT + 1) + c] = kv[c] + __ldg(ib[1] + c);
+          for (int c = 0; c < DT; ++c) sKV[row * (2 * DT + 1) + c] = kv[c];
           tmem_row<DT>(trow + 2 * DT, kv);
 #pragma unroll
-          for (int c = 0; c < DT; ++c) sKV[row * (2 * DT + 1) + DT + c] = kv[c] + __ldg(ib[2] + c);
+          for (int c = 0; c < DT; ++c) sKV[row * (2 * DT + 1) + DT + c] = kv[c];
         }
-#pragma unroll
-        for (int c = 0; c < DT; ++c) qv[c] += __ldg(ib[0] + c);
         __syncwarp();
         const int g0 = row - row % KG;
         float s[KG];
@@ -259,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
 #pragma unroll
         for (int jj = 0; jj < KG; ++jj) { s[jj] = __expf(s[jj] - mx); tot += s[jj]; }
         const float rinv = 1.f / tot;
-        float ctx[DT];
+        float ctx[XK];
 #pragma unroll
         for (int c = 0; c < DT; ++c) {
           float acc = 0.f;
@@ -267,8 +305,10 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
           for (int jj = 0; jj < KG; ++jj) acc = fmaf(s[jj], sKV[(g0 + jj) * (2 * DT + 1) + DT + c], acc);
           ctx[c] = acc * rinv;
         }
+#pragma unroll
+        for (int c = DT; c < XK; ++c) ctx[c] = 0.f;
         __syncwarp();
-        store_row(sA, row, DT, ctx, DT);
+        store_row(sA, row, XK, ctx, XK);
         signal();
         wait_d();
         float o[DT];
@@ -276,7 +316,9 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
 #pragma unroll
         for (int c = 0; c < DT; ++c) h[c] += o[c] + __ldg(ib[3] + c);       // x1
         ln_row<DT>(h, ln[2], ln[3], xn, nullptr, inv);
-        store_row(sA, row, DT, xn, DT);
+#pragma unroll
+        for (int c = DT; c < XK; ++c) xn[c] = c == DT ? 1.f : 0.f;
+        store_row(sA, row, XK, xn, XK);
         signal();
         wait_d();
 #pragma unroll 1
@@ -284,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
           float hv[32];
           tmem_row<32>(trow + c0, hv);
 #pragma unroll
-          for (int u = 0; u < 32; ++u) hv[u] = gelu_f(hv[u] + __ldg(ib[4] + c0 + u));
+          for (int u = 0; u < 32; ++u) hv[u] = gelu_f(hv[u]);
           store_row(sH, row, 4 * DT, hv, 32, c0);
         }
         signal();
@@ -324,10 +366,10 @@ __global__ void __launch_bounds__(kThreads, 1) fe_mlp_bwd_kernel(FrontArgs a) {
   const BlobOff bo = blob_offsets(DT, Dm, a.inner_layers);
   // smem carve-up
   bf16* sW = reinterpret_cast<bf16*>(smem_raw);                    // tp, w1 (fwd) + tp_n, w1_n, w2_n
-  const int n_tp = DT * kFP, n_w1 = H2 * DT;
+  const int n_tp = DT * kFP, n_w1 = H2 * DT, n_w1f = H2 * XK;
   bf16* w_tp = sW;
-  bf16* w_w1 = w_tp + n_tp;
-  bf16* w_tp_n = w_w1 + n_w1;
+  bf16* w_w1 = w_tp + n_tp;                    // [W1ᵀ | b1] image, K = XK
+  bf16* w_tp_n = w_w1 + n_w1f;
   bf16* w_w1_n = w_tp_n + n_tp;
   bf16* w_w2_n = w_w1_n + n_w1;
   bf16* sFeat = w_w2_n + n_w1;                 // 128 x 32
@@ -342,7 +384,8 @@ __global__ void __launch_bounds__(kThreads, 1) fe_mlp_bwd_kernel(FrontArgs a) {
   float* s_item = s_tab;
   float* s_act = s_item + (item_smem ? n_item : 0);
   float* s_time = s_act + n_act;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_time + n_time + 2);
+  float* s_b1 = s_time + n_time;                 // seq_b1 staged once (H2)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_b1 + H2 + 2);
   bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(bars) + 7) & ~uintptr_t(7));
   uint64_t* bar_w = bars;
   uint64_t* bar_a = bars + 1;
@@ -351,6 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1) fe_mlp_bwd_kernel(FrontArgs a) {
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < (item_smem ? n_item : 0) + n_act + n_time; i += blockDim.x) s_tab[i] = 0.f;
+  for (int i = threadIdx.x; i < H2; i += blockDim.x) s_b1[i] = a.seq_b1[i];
   if (threadIdx.x == 0) {
     sm100::mbar_init(bar_w, 1);
     sm100::mbar_init(bar_a, 32 * kWorkers);
@@ -374,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1) fe_mlp_bwd_kernel(FrontArgs a) {
 
   if (warp == 0) {
     if (lane == 0) {
-      const int b1 = (n_tp + n_w1) * 2, b2 = (n_tp + 2 * n_w1) * 2;
+      const int b1 = (n_tp + n_w1f) * 2, b2 = (n_tp + 2 * n_w1) * 2;
       sm100::mbar_arrive_expect_tx(bar_w, b1 + b2);
       load_blob(reinterpret_cast<uint8_t*>(w_tp), reinterpret_cast<const uint8_t*>(a.wblob + bo.tp), b1, bar_w);
       load_blob(reinterpret_cast<uint8_t*>(w_tp_n), reinterpret_cast<const uint8_t*>(a.wblob + bo.tp_n), b2, bar_w);
@@ -392,7 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1) fe_mlp_bwd_kernel(FrontArgs a) {
         sm100::mma_commit(bar_d);
         wait_a();                                                        // x0
         // hidden half 0: a1 (recompute) and dg1 = dh·W2ᵀ
-        mma(T_A1, Opnd{aX0, XK, 0}, Opnd{aW1, DT, 0}, DT / 16, 128, false);
+        mma(T_A1, Opnd{aX0, XK, 0}, Opnd{aW1, XK, 0}, XK / 16, 128, false);
         mma(T_G1, Opnd{aDH, DT, 0}, Opnd{aW2n, DT, 0}, DT / 16, 128, false);
         sm100::mma_commit(bar_d);
         for (int j = 0; j < nh; ++j) {
@@ -401,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, 1) fe_mlp_bwd_kernel(FrontArgs a) {
           mma(T_DW1 + j * XK, Opnd{aDA, 128, 1}, Opnd{aX0, XK, 1}, kTile / 16, XK, !first);
           mma(T_DX0, Opnd{aDA, 128, 0}, Opnd{aW1n + canon(0, 128 * j, H2) * 2, H2, 0}, 8, DT, j > 0);
           if (j + 1 < nh) {
-            mma(T_A1, Opnd{aX0, XK, 0}, Opnd{aW1 + canon(128 * (j + 1), 0, DT) * 2, DT, 0}, DT / 16, 128, false);
+            mma(T_A1, Opnd{aX0, XK, 0}, Opnd{aW1 + canon(128 * (j + 1), 0, XK) * 2, XK, 0}, XK / 16, 128, false);
             mma(T_G1, Opnd{aDH, DT, 0}, Opnd{aW2n + canon(128 * (j + 1), 0, DT) * 2, DT, 0}, DT / 16, 128, false);
           }
           sm100::mma_commit(bar_d);
@@ -427,6 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1) fe_mlp_bwd_kernel(FrontArgs a) {
       float v[kFP];
       int ids[3];
       featurise(a, ti, v, ids, false);
+      v[kFP - 1] = 1.f;                                                // bias column
       store_row(sFeat, row, kFP, v, kFP);
       float dh[DT];
       if (ti.real) {
@@ -449,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1) fe_mlp_bwd_kernel(FrontArgs a) {
       tmem_row<DT>(T_X0 + lane_off, x);
 #pragma unroll
       for (int c = 0; c < DT; ++c)
-        x[c] = ti.real ? x[c] + __ldg(a.tok_b + c) + __ldg(a.pos_tab + (long long)ti.rec * DT + c) : 0.f;
+        x[c] = ti.real ? x[c] + __ldg(a.pos_tab + (long long)ti.rec * DT + c) : 0.f;
 #pragma unroll
       for (int c = DT; c < DT + 16; ++c) x[c] = c == DT ? 1.f : 0.f;
       store_row(sX0, row, XK, x, XK);
@@ -463,7 +508,7 @@ __global__ void __launch_bounds__(kThreads, 1) fe_mlp_bwd_kernel(FrontArgs a) {
           tmem_row<32>(T_G1 + lane_off + c0, gv);
 #pragma unroll
           for (int u = 0; u < 32; ++u) {
-            const float z = av[u] + __ldg(a.seq_b1 + 128 * hj + c0 + u);
+            const float z = av[u];                                  // b1 added by the MMA
             const float t = tanh_fast(kGeluC * (z + kGeluA * z * z * z));
             av[u] = 0.5f * z * (1.f + t);
             gv[u] *= 0.5f * (1.f + t) + 0.5f * z * (1.f - t * t) * kGeluC * (1.f + 3.f * kGeluA * z * z);
@@ -489,15 +534,17 @@ __global__ void __launch_bounds__(kThreads, 1) fe_mlp_bwd_kernel(FrontArgs a) {
       wait_d();
       float df[kFP];
       tmem_row<kFP>(T_X0 + lane_off, df);
+      const int e1 = a.d_item, e2 = e1 + a.d_act;
       if (ti.real) {
-        const int e1 = a.d_item, e2 = e1 + a.d_act;
-        for (int c = 0; c < e1; ++c) {
-          if (item_smem) atomicAdd(s_item + ids[0] * a.d_item + c, df[c]);
-          else atomicAdd(a.g_item + ids[0] * a.d_item + c, df[c]);
-        }
-        for (int c = 0; c < a.d_act; ++c) atomicAdd(s_act + ids[1] * a.d_act + c, df[e1 + c]);
-        for (int c = 0; c < a.d_time; ++c) atomicAdd(s_time + ids[2] * a.d_time + c, df[e2 + c]);
+        float* gi = (item_smem ? s_item : a.g_item) + ids[0] * a.d_item;
+#pragma unroll
+        for (int c = 0; c < kFP; ++c)
+          if (c < e1) atomicAdd(gi + c, df[c]);
       }
+      // action / time-bucket rows repeat across consecutive events: aggregate equal ids in the
+      // warp before touching shared memory (a 4-row table would otherwise serialise 128 threads)
+      warp_scatter_add(s_act, ti.real ? ids[1] : -1, df, e1, a.d_act);
+      warp_scatter_add(s_time, ti.real ? ids[2] : -1, df, e2, a.d_time);
     }
     // ---------------- flush the CTA's accumulators
     if (my_tiles > 0) {
@@ -545,7 +592,7 @@ int frontend_supported(int d, int K, int D, int F, int inner_layers) {
   if (!(d == 16 || d == 32)) return 0;
   if (!(K == 2 || K == 4 || K == 8)) return 0;
   if ((2 * D) % 128 || 2 * D > 512) return 0;
-  if (F > kFP) return 0;
+  if (F > kFP - 1) return 0;     // column 31 of the feature tile carries the bias
   if (inner_layers > 8) return 0;
   return 1;
 }
@@ -564,8 +611,12 @@ void pack_frontend_weights(const float* params, long long tok_w, long long seq_w
     s.src = src; s.in = in; s.out = out; s.trans = trans; s.n_off = n_off; s.k_off = k_off; s.Kdim = Kdim; s.dst = dst;
   };
   // forward images (Wᵀ, K = in)
+  const int XK = d + 16;
+  // forward images (Wᵀ, K = in), bias-augmented where the activation tile carries a ones column
   add(tok_w, F, d, 1, 0, 0, kFP, o.tp);
-  add(seq_w1, d, 2 * D, 1, 0, 0, d, o.w1);
+  add(tok_w + (long long)F * d, 1, d, 1, 0, kFP - 1, kFP, o.tp);            // b_tp at k = 31
+  add(seq_w1, d, 2 * D, 1, 0, 0, XK, o.w1);
+  add(seq_w1 + (long long)d * 2 * D, 1, 2 * D, 1, 0, d, XK, o.w1);          // b1 at k = d
   add(seq_w2, 2 * D, d, 1, 0, 0, 2 * D, o.w2);
   // backward images (W, K = out)
   add(tok_w, F, d, 0, 0, 0, d, o.tp_n);
@@ -574,11 +625,15 @@ void pack_frontend_weights(const float* params, long long tok_w, long long seq_w
   for (int l = 0; l < IL; ++l) {
     const long long wq = inner_w[l][0], wk = inner_w[l][1], wv = inner_w[l][2], wo = inner_w[l][3];
     const long long w1 = wo + (long long)d * d + d, w2 = w1 + 4LL * d * d + 4 * d;   // reference order
-    add(wq, d, d, 1, 0, 0, d, o.qkv[l]);
-    add(wk, d, d, 1, d, 0, d, o.qkv[l]);
-    add(wv, d, d, 1, 2 * d, 0, d, o.qkv[l]);
+    add(wq, d, d, 1, 0, 0, XK, o.qkv[l]);
+    add(wk, d, d, 1, d, 0, XK, o.qkv[l]);
+    add(wv, d, d, 1, 2 * d, 0, XK, o.qkv[l]);
+    add(wq + (long long)d * d, 1, d, 1, 0, d, XK, o.qkv[l]);                 // b_q, b_k, b_v at k = d
+    add(wk + (long long)d * d, 1, d, 1, d, d, XK, o.qkv[l]);
+    add(wv + (long long)d * d, 1, d, 1, 2 * d, d, XK, o.qkv[l]);
     add(wo, d, d, 1, 0, 0, d, o.wo[l]);
-    add(w1, d, 4 * d, 1, 0, 0, d, o.w1i[l]);
+    add(w1, d, 4 * d, 1, 0, 0, XK, o.w1i[l]);
+    add(w1 + 4LL * d * d, 1, 4 * d, 1, 0, d, XK, o.w1i[l]);                  // b1 at k = d
     add(w2, 4 * d, d, 1, 0, 0, 4 * d, o.w2i[l]);
     add(wq, d, d, 0, 0, 0, 3 * d, o.qkv_n[l]);
     add(wk, d, d, 0, 0, d, 3 * d, o.qkv_n[l]);
@@ -593,7 +648,7 @@ void pack_frontend_weights(const float* params, long long tok_w, long long seq_w
 template <int DT, int KG>
 static int launch_fwd(const FrontArgs& a, cudaStream_t st) {
   const BlobOff bo = blob_offsets(DT, DT * KG, a.inner_layers);
-  const int smem = ((bo.fwd_total + 63) & ~63) * 2 + kTile * kFP * 2 + kTile * 136 * 2 + 64;
+  const int smem = ((bo.fwd_total + 63) & ~63) * 2 + kTile * std::max(DT + 16, kFP) * 2 + kTile * 136 * 2 + 64;
   static int done = 0;
   if (!done) {
     cudaFuncSetAttribute(fe_fwd_kernel<DT, KG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -623,7 +678,7 @@ static int launch_mlp_bwd(const FrontArgs& a, cudaStream_t st) {
   const int XK = DT + 16;
   const int n_item = a.vocab * a.d_item;
   const int tab = ((n_item <= 16384) ? n_item : 0) + a.n_actions * a.d_act + a.nb * a.d_time;
-  const int smem = (2 * DT * kFP + 3 * H2 * DT) * 2 + kTile * (kFP + XK + DT + 128 + 128 + DT) * 2 + tab * 4 + 128;
+  const int smem = (2 * DT * kFP + 2 * H2 * DT + H2 * XK) * 2 + kTile * (kFP + XK + DT + 128 + 128 + DT) * 2 + (tab + H2) * 4 + 128;
   if (smem > 227 * 1024) return (int)cudaErrorInvalidValue;
   static int done = 0;
   if (!done) {

@@ -26,11 +26,11 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
   const BlobOff bo = blob_offsets(DT, DT * KG, a.inner_layers);
   // weights: forward images [qkv | wo | w1i] and backward images [qkv_n | wo_n | w1i_n | w2i_n]
   bf16* sWf = reinterpret_cast<bf16*>(smem_raw);
-  const int nWf = 3 * DT * DT + DT * DT + 4 * DT * DT;
+  const int nWf = 3 * DT * XK + DT * DT + 4 * DT * XK;   // [Wqkvᵀ|b], Woᵀ, [W1ᵀ|b1]
   const int nWb = 3 * DT * DT + DT * DT + 4 * DT * DT + 4 * DT * DT;
   bf16* sWb = sWf + nWf;
   bf16* w_qkv = sWf;
-  bf16* w_wo = w_qkv + 3 * DT * DT;
+  bf16* w_wo = w_qkv + 3 * DT * XK;
   bf16* w_w1i = w_wo + DT * DT;
   bf16* w_qkv_n = sWb;
   bf16* w_wo_n = w_qkv_n + 3 * DT * DT;
@@ -93,13 +93,13 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
       bool first = true;
       for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         wait_a();                                                           // xn, dX2
-        mma(T_W0, Opnd{S(sXN), XK, 0}, Opnd{S(w_qkv), DT, 0}, DT / 16, 3 * DT, false);
+        mma(T_W0, Opnd{S(sXN), XK, 0}, Opnd{S(w_qkv), XK, 0}, XK / 16, 3 * DT, false);
         sm100::mma_commit(bar_d);
         wait_a();                                                           // ctx
         mma(T_W2, Opnd{S(sCTX), XK, 0}, Opnd{S(w_wo), DT, 0}, DT / 16, DT, false);
         sm100::mma_commit(bar_d);
         wait_a();                                                           // x1n
-        mma(T_W0, Opnd{S(sX1N), XK, 0}, Opnd{S(w_w1i), DT, 0}, DT / 16, F4, false);
+        mma(T_W0, Opnd{S(sX1N), XK, 0}, Opnd{S(w_w1i), XK, 0}, XK / 16, F4, false);
         mma(T_W1, Opnd{S(sDX2), DT, 0}, Opnd{S(w_w2i_n), DT, 0}, DT / 16, F4, false);
         sm100::mma_commit(bar_d);
         wait_a();                                                           // gf, df
@@ -160,17 +160,15 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
       wait_d();
       float qv[DT], kvv[DT];
       tmem_row<DT>(T_W0 + lo, qv);
-#pragma unroll
-      for (int c = 0; c < DT; ++c) qv[c] += __ldg(ib[0] + c);
       bf16* qs = sQKV + row * QS;
 #pragma unroll
       for (int c = 0; c < DT; ++c) qs[c] = __float2bfloat16(qv[c]);
       tmem_row<DT>(T_W0 + lo + DT, kvv);
 #pragma unroll
-      for (int c = 0; c < DT; ++c) qs[DT + c] = __float2bfloat16(kvv[c] + __ldg(ib[1] + c));
+      for (int c = 0; c < DT; ++c) qs[DT + c] = __float2bfloat16(kvv[c]);
       tmem_row<DT>(T_W0 + lo + 2 * DT, kvv);
 #pragma unroll
-      for (int c = 0; c < DT; ++c) qs[2 * DT + c] = __float2bfloat16(kvv[c] + __ldg(ib[2] + c));
+      for (int c = 0; c < DT; ++c) qs[2 * DT + c] = __float2bfloat16(kvv[c]);
       __syncwarp();
       const int g0 = row - row % KG;
       const int me = row - g0;
@@ -226,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
         tmem_row<32>(T_W1 + lo + c0, gv);
 #pragma unroll
         for (int u = 0; u < 32; ++u) {
-          const float z = fv[u] + __ldg(ib[4] + c0 + u);
+          const float z = fv[u];                                      // b1 added by the MMA
           const float tt = tanh_fast(kGeluC * (z + kGeluA * z * z * z));
           fv[u] = 0.5f * z * (1.f + tt);
           gv[u] *= 0.5f * (1.f + tt) + 0.5f * z * (1.f - tt * tt) * kGeluC * (1.f + 3.f * kGeluA * z * z);
@@ -388,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
 template <int DT, int KG>
 int launch_inner_bwd(const FrontArgs& a, cudaStream_t st) {
   constexpr int XK = DT + 16, F4 = 4 * DT, QS = 3 * DT + 2;
-  const int nW = (8 + 12) * DT * DT;
+  const int nW = 7 * DT * XK + DT * DT + 12 * DT * DT;
   const int smem = nW * 2 + kTile * (3 * XK + 2 * DT + 2 * F4 + QS) * 2 + kTile * KG * 8 + 64;
   if (smem > 227 * 1024) return (int)cudaErrorInvalidValue;
   static int done = 0;
