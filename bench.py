@@ -52,6 +52,43 @@ def flops_per_sample(cfg) -> int:
     return 6 * total
 
 
+def phase_flops(cfg, B):
+    """Algorithmic FLOPs of one launch of each probed fused kernel (recompute and padding excluded),
+    from the same MAC model as flops_per_sample."""
+    d, D, F, L = cfg.d, cfg.D, cfg.feat_width, cfg.L
+    q, v = cfg.k + cfg.m, cfg.merged_len + cfg.m
+    mlp = L * (F * d + 4 * d * D)
+    inner = cfg.inner_layers * (12 * cfg.L_padded * d * d + 2 * cfg.L_padded * cfg.K * d) \
+        if cfg.merge_mode == "inner" else 0
+    attn = 2 * q * v * D
+    return {"fe_fwd": 2 * B * (mlp + inner), "fe_inner_bwd": 4 * B * inner, "fe_mlp_bwd": 4 * B * mlp,
+            "xattn_fwd": 2 * B * attn, "xattn_bwd": 4 * B * attn}
+
+
+def count_graph_kernels(graph):
+    """Kernel nodes of the captured step graph, split into ours (longer::) and others."""
+    try:
+        from cuda.bindings import driver as drv
+        g = drv.CUgraph(graph.raw_cuda_graph())
+        err, _, n = drv.cuGraphGetNodes(g, 0)
+        err, nodes, n = drv.cuGraphGetNodes(g, n)
+        ours = other = 0
+        for node in nodes[:n]:
+            err, t = drv.cuGraphNodeGetType(node)
+            if t != drv.CUgraphNodeType.CU_GRAPH_NODE_TYPE_KERNEL:
+                continue
+            err, prm = drv.cuGraphKernelNodeGetParams(node)
+            err, name = drv.cuFuncGetName(prm.func)
+            nm = name.decode() if isinstance(name, bytes) else str(name)
+            if "longer" in nm:
+                ours += 1
+            else:
+                other += 1
+        return ours, other
+    except Exception as exc:  # pragma: no cover
+        return None, repr(exc)
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -199,6 +236,15 @@ def main():
         opt.step()
 
     stream = torch.cuda.current_stream(dev)
+    # timing probes around the fused kernels (graph-captured event records)
+    import ctypes
+    from paper_2505_04421_b200 import _lib as L_
+    probe_ev = {}
+    for name, ph in L_.PROBES.items():
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream); e1.record(stream)            # materialise the events
+        probe_ev[name] = (e0, e1)
+        L_.check(model._lib.longer_set_probe(ph, ctypes.c_void_p(e0.cuda_event), ctypes.c_void_p(e1.cuda_event)))
     # warm-up (eager) — also sets kernel attributes before capture
     for i in range(2):
         load(dev_batches[i % n_batches])
@@ -206,7 +252,7 @@ def main():
     torch.cuda.synchronize()
     graph = None
     if not args.no_graph:
-        graph = torch.cuda.CUDAGraph()
+        graph = torch.cuda.CUDAGraph(keep_graph=True)
         s = torch.cuda.Stream(dev)
         s.wait_stream(stream)
         with torch.cuda.stream(s):
@@ -216,6 +262,9 @@ def main():
         with torch.cuda.graph(graph):
             step_body()
         torch.cuda.synchronize()
+
+    if graph is not None:
+        graph.instantiate() if hasattr(graph, "instantiate") else None
 
     def run_step():
         if graph is not None:
@@ -238,12 +287,21 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    from cuda.bindings import runtime as rt
+    phase_ms = {k: 0.0 for k in probe_ev}
     for i in range(args.steps):
         load(dev_batches[i % n_batches])
         flush.fill_(i & 0xFF)
         ev[i][0].record(stream)
         run_step()
         ev[i][1].record(stream)
+        ev[i][1].synchronize()                      # per-step read of the kernel probes
+        for k, (e0, e1) in probe_ev.items():
+            err, t = rt.cudaEventElapsedTime(e0.cuda_event, e1.cuda_event)
+            if int(err) == 0:
+                phase_ms[k] += t
+            elif i == 0 and rank == 0:
+                print(f"probe {k}: {err}", file=sys.stderr)
     torch.cuda.synchronize()
     ms = sum(a.elapsed_time(b) for a, b in ev)
     if world > 1:
@@ -276,6 +334,21 @@ def main():
         burst, sustained, hbm, src = peaks()
         fps = flops_per_sample(cfg)
         achieved = value / world * fps / 1e12
+        pf = phase_flops(cfg, B)
+        dom = max(phase_ms, key=lambda k: phase_ms[k]) if phase_ms else None
+        kernels = {}
+        for k, tms in phase_ms.items():
+            if tms > 0:
+                avg = tms / args.steps
+                kernels[k] = {"ms_per_launch": avg, "tflops": pf[k] / (avg / 1e3) / 1e12,
+                              "share_of_step": avg / ms_step}
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "dram_traffic.json")) as fh:
+                traffic = json.load(fh).get(args.config, {}).get(dom)
+        except Exception:
+            pass
+        n_ours, n_other = count_graph_kernels(graph) if graph is not None else (None, None)
         line = {
             "metric": "samples/sec fwd+bwd at L=2000", "value": value, "unit": "samples/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -285,10 +358,17 @@ def main():
                        "per_gpu_batch": B, "parallelism": f"dp{world}", "l2": "flushed between steps",
                        "step": "fwd+bwd+allreduce+adam" if world > 1 else "fwd+bwd+adam",
                        "cuda_graph": graph is not None},
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": burst, "unit": "TFLOP/s",
-                         "frac": achieved / burst, "traffic": None, "peak_source": src,
-                         "scope": "whole step (algorithmic FLOPs = 6 x analysis.muladds_full_forward per sample)",
-                         "frac_of_sustained": achieved / sustained if sustained else None},
+            "roofline": ({"bound": "tensor", "kernel": dom, "achieved": kernels[dom]["tflops"], "peak": burst,
+                          "unit": "TFLOP/s", "frac": kernels[dom]["tflops"] / burst, "traffic": traffic,
+                          "peak_source": src, "ms_per_launch": kernels[dom]["ms_per_launch"],
+                          "flop_per_launch": pf[dom]} if dom in kernels else None),
+            "roofline_step": {"bound": "tensor", "achieved": achieved, "peak": burst, "unit": "TFLOP/s",
+                              "frac": achieved / burst, "peak_source": src,
+                              "scope": "whole step, algorithmic FLOPs = 6 x analysis.muladds_full_forward/sample",
+                              "frac_of_sustained": achieved / sustained if sustained else None},
+            "kernels": kernels,
+            "gpu_launches": (n_ours * args.steps) if n_ours is not None else None,
+            "gpu_launches_per_step": {"ours": n_ours, "torch_or_nccl": n_other},
             "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d_bytes,
                     "d2h_bytes_per_step": 4},
             "clocks": clk,

@@ -88,6 +88,12 @@ int longer_read_status(void* ws, int32_t* flags, void* stream);
 
 const char* longer_last_error(void);
 
+/* Diagnostics: record caller-owned CUDA events (cudaEvent_t) immediately before / after one fused
+ * kernel of subsequent calls, on the call's stream (graph-capturable).  phase: 0 front-end forward,
+ * 1 InnerTrans backward, 2 token-MLP/featuriser backward, 3 cross-attention forward,
+ * 4 cross-attention backward.  Null events disable the probe. */
+int longer_set_probe(int32_t phase, void* ev_begin, void* ev_end);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,7 +21,9 @@ _EXC = {LONGER_ECONFIG: ConfigError, LONGER_EDIM: DimensionError, LONGER_ELOOKUP
         LONGER_ENUMERIC: NumericalError, LONGER_ESTALE: StaleCacheError, LONGER_ECUDA: RuntimeError}
 
 SYMBOLS = ("longer_param_count", "longer_workspace_bytes", "longer_forward", "longer_forward_backward",
-           "longer_adam_step", "longer_read_status", "longer_last_error")
+           "longer_adam_step", "longer_read_status", "longer_last_error", "longer_set_probe")
+
+PROBES = {"fe_fwd": 0, "fe_inner_bwd": 1, "fe_mlp_bwd": 2, "xattn_fwd": 3, "xattn_bwd": 4}
 
 
 class LongerDims(ctypes.Structure):
@@ -65,6 +67,7 @@ def _declare(lib):
         "longer_forward_backward": [pd, vp, pb, vp, ctypes.c_size_t, vp, vp, vp, vp],
         "longer_adam_step": [vp, vp, vp, vp, i64, f32, i32, vp],
         "longer_read_status": [vp, ctypes.POINTER(i32), vp],
+        "longer_set_probe": [i32, vp, vp],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)

@@ -23,6 +23,21 @@ namespace {
 
 thread_local std::string g_err;
 
+// Timing probes (longer_set_probe): optional CUDA events recorded around the fused kernels, on the
+// launching stream (graph-capturable), so callers can time one kernel inside a whole step.
+enum Phase { PH_FE_FWD = 0, PH_FE_INNER_BWD = 1, PH_FE_MLP_BWD = 2, PH_XATTN_FWD = 3, PH_XATTN_BWD = 4, PH_N = 5 };
+cudaEvent_t g_probe[PH_N][2] = {};
+
+void probe(int ph, int which, cudaStream_t st) {
+  // External record: inside stream capture this becomes a real event-record node (a plain
+  // cudaEventRecord would only be a capture-internal dependency marker).
+  if (!g_probe[ph][which]) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(g_probe[ph][which], st, cudaEventRecordExternal);
+  else cudaEventRecord(g_probe[ph][which], st);
+}
+
 int fail(int code, const char* msg) {
   g_err = msg;
   return code;
@@ -425,7 +440,7 @@ int block_fwd(const Ctx& c, const BlockOff& bo, BlockBufs& b, const float* xq, b
     a.V = b.qkv + 2 * D; a.ldv = 3 * D; a.sv = a.sq;
     a.nk = p.q; a.ns = p.k; a.goff = p.G - p.k;
   }
-  if (cross && use_attn_tc(a)) TRY(attn_tc_fwd(a, st)); else attn_fwd(a, st);
+  if (cross && use_attn_tc(a)) { probe(PH_XATTN_FWD, 0, st); TRY(attn_tc_fwd(a, st)); probe(PH_XATTN_FWD, 1, st); } else attn_fwd(a, st);
   TRY(lin_fwd(st, b.ctx, D, Q, Wo, D, D, c.w(bo.b_o), 0, b.x1, nullptr, nullptr, xq, D));
   layernorm_fwd(rows_plain(b.x1, D, Q), D, c.w(bo.ln2_g), c.w(bo.ln2_b), b.x1n, b.m2, b.r2, st);
   TRY(lin_fwd(st, b.x1n, D, Q, W1, D, 4 * D, c.w(bo.b1), EPI_GELU | EPI_SAVE_PRE, nullptr, b.gf, b.f1));
@@ -531,7 +546,7 @@ int forward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs, fl
   (void)with_loss;
   TRY(pack_weights(p, c.P, p.ws, st));
   if (p.fused_fe) {
-    TRY(frontend_fused_fwd(c, p, bt));
+    probe(PH_FE_FWD, 0, c.st); TRY(frontend_fused_fwd(c, p, bt)); probe(PH_FE_FWD, 1, c.st);
   } else {
     TRY(frontend_unfused_fwd(c, p, bt));
   }
@@ -614,7 +629,7 @@ int block_bwd(const Ctx& c, const BlockOff& bo, const BlockBufs& b, const float*
     a.dK = p.dqkv + D; a.lddk = 3 * D; a.sdk = a.sdq;
     a.dV = p.dqkv + 2 * D; a.lddv = 3 * D; a.sdv = a.sdq;
   }
-  if (cross && use_attn_tc(a)) TRY(attn_tc_bwd(a, st)); else attn_bwd(a, st);
+  if (cross && use_attn_tc(a)) { probe(PH_XATTN_BWD, 0, st); TRY(attn_tc_bwd(a, st)); probe(PH_XATTN_BWD, 1, st); } else attn_bwd(a, st);
   if (cross) {
     TRY(lin_dx(st, p.dqkv, D, Q, Wqkv, D, D, D, p.dqn, D, nullptr, 0));
     TRY(lin_dw(st, b.qn, D, D, p.dqkv, D, D, Q, c.g(bo.w_q)));
@@ -703,7 +718,7 @@ int backward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs) {
     const long long offs[16] = {bo.w_q, bo.b_q, bo.w_k, bo.b_k, bo.w_v, bo.b_v, bo.w_o, bo.b_o,
                                 bo.w1, bo.b1, bo.w2, bo.b2, bo.ln1_g, bo.ln1_b, bo.ln2_g, bo.ln2_b};
     for (int i = 0; i < 16; ++i) f.g_inner[i] = c.g(offs[i]);
-    TRY(frontend_inner_bwd(f, st));
+    probe(PH_FE_INNER_BWD, 0, st); TRY(frontend_inner_bwd(f, st)); probe(PH_FE_INNER_BWD, 1, st);
     dxt = p.t_dx;
     first_unfused = -1;
   } else if (p.fused_fe && p.IL) {
@@ -745,7 +760,7 @@ int backward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs) {
   if (p.fused_fe) {
     FrontArgs f = front_args(c, p, bt);
     f.dh = dxt;
-    TRY(frontend_mlp_bwd(f, st));
+    probe(PH_FE_MLP_BWD, 0, st); TRY(frontend_mlp_bwd(f, st)); probe(PH_FE_MLP_BWD, 1, st);
     TRY((int)cudaGetLastError());
     return 0;
   }
@@ -846,3 +861,10 @@ extern "C" int longer_read_status(void* ws, int32_t* flags, void* stream) {
 }
 
 extern "C" const char* longer_last_error(void) { return g_err.c_str(); }
+
+extern "C" int longer_set_probe(int32_t phase, void* ev_begin, void* ev_end) {
+  if (phase < 0 || phase >= PH_N) return fail(LONGER_EDIM, "unknown probe phase");
+  g_probe[phase][0] = (cudaEvent_t)ev_begin;
+  g_probe[phase][1] = (cudaEvent_t)ev_end;
+  return 0;
+}
