@@ -24,7 +24,7 @@ struct Smem {
   static constexpr int A_BYTES = BM * BK * 2;        // 16 KB
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int TOTAL = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + kEpiWarps * 32 * 33 * 4;
+  static constexpr int TOTAL = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 template <int BN, int STAGES>
@@ -38,7 +38,6 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   uint64_t* empty = full + STAGES;
   uint64_t* tmem_full = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
-  float* stage_base = reinterpret_cast<float*>(smem + STAGES * S::STAGE_BYTES + 256);
 
   const int warp = threadIdx.x / 32;
   const int n0 = blockIdx.x * BN;
@@ -107,61 +106,113 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     }
   } else {
     // Epilogue warps e = 0..7: TMEM lane quarter q = warp % 4, column chunks c ≡ e/4 (mod 2).
-    // Each 32x32 accumulator block is transposed through a padded per-warp smem tile so every
-    // global load/store is row-contiguous across the warp; loads for 8 rows are issued before use.
+    // Thread = output row: the 32 accumulators of a chunk are processed in registers and every
+    // global access is a 16-byte vector (bf16 x 8 / fp32 x 4); flag tests run once per chunk.
     const int e = warp - 2;
     const int q = warp & 3;
     const int lane = threadIdx.x & 31;
-    float* stg = stage_base + e * 32 * 33;
     sm100::mbar_wait(tmem_full, 0);
     sm100::tc_fence_after();
     const uint32_t flags = g.flags;
-    const int row0 = m0 + q * 32;
-    const __nv_bfloat16* pre_in = reinterpret_cast<const __nv_bfloat16*>(g.pre_bf16);
+    const int row = m0 + q * 32 + lane;
+    const bool row_ok = row < g.M;
+    const float rmask = ((flags & EPI_ROWMASK) && row_ok) ? g.rowmask[row] : 1.f;
 #pragma unroll 1
     for (int c = (e >> 2) * 32; c < BN; c += 64) {
       uint32_t r[32];
       sm100::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + c, r);
       sm100::tmem_ld_wait();
+      const int nb = n0 + c;
+      if (!row_ok || nb >= g.N) continue;
+      float v[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = __uint_as_float(r[j]);
-      __syncwarp();
-      const int n = n0 + c + lane;
-      if (n0 + c < g.N && row0 < g.M) {
-        const bool col_ok = n < g.N;
-        const float bias_n = ((flags & EPI_BIAS) && col_ok) ? g.bias[n] : 0.f;
-#pragma unroll 1
-        for (int r0 = 0; r0 < 32; r0 += 8) {
-          float pv[8], rv[8], mv[8];
+      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+      if (nb + 32 <= g.N) {
+        if (flags & EPI_BIAS) {
+          const float4* bp = reinterpret_cast<const float4*>(g.bias + nb);
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int row = row0 + r0 + u;
-            const bool ok = col_ok && row < g.M;
-            pv[u] = ((flags & EPI_GELU_BWD) && ok) ? __bfloat162float(pre_in[(size_t)row * g.ldc_bf + n]) : 0.f;
-            rv[u] = ((flags & EPI_RESID) && ok) ? g.resid[(size_t)row * g.ldr + n] : 0.f;
-            mv[u] = ((flags & EPI_ROWMASK) && row < g.M) ? g.rowmask[row] : 1.f;
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int row = row0 + r0 + u;
-            if (!col_ok || row >= g.M) continue;
-            float v = stg[(r0 + u) * 33 + lane] + bias_n;
-            if (flags & EPI_SAVE_PRE)
-              reinterpret_cast<__nv_bfloat16*>(g.pre_bf16)[(size_t)row * g.ldc_bf + n] = __float2bfloat16(v);
-            if (flags & EPI_GELU) v = gelu_f(v);
-            if (flags & EPI_GELU_BWD) v *= gelu_grad_f(pv[u]);
-            v += rv[u];
-            v *= mv[u];
-            if (flags & EPI_OUT_F32) {
-              float* dst = g.C + (size_t)row * g.ldc + n;
-              if (flags & EPI_ATOMIC) atomicAdd(dst, v); else *dst = v;
-            }
-            if (flags & EPI_OUT_BF16)
-              reinterpret_cast<__nv_bfloat16*>(g.C_bf16)[(size_t)row * g.ldc_bf + n] = __float2bfloat16(v);
+          for (int j = 0; j < 8; ++j) {
+            const float4 b4 = __ldg(bp + j);
+            v[4 * j] += b4.x; v[4 * j + 1] += b4.y; v[4 * j + 2] += b4.z; v[4 * j + 3] += b4.w;
           }
         }
+        if (flags & EPI_SAVE_PRE) {
+          uint4* pp = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(g.pre_bf16) + (size_t)row * g.ldc_bf + nb);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            pp[j] = make_uint4(sm100::pack_bf16(v[8 * j], v[8 * j + 1]), sm100::pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                               sm100::pack_bf16(v[8 * j + 4], v[8 * j + 5]), sm100::pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+        }
+        if (flags & EPI_GELU) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
+        }
+        if (flags & EPI_GELU_BWD) {
+          const uint4* pp = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(g.pre_bf16) +
+                                                           (size_t)row * g.ldc_bf + nb);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint4 p4 = pp[j];
+            const uint32_t w[4] = {p4.x, p4.y, p4.z, p4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              v[8 * j + 2 * u] *= gelu_grad_f(sm100::bf16_lo(w[u]));
+              v[8 * j + 2 * u + 1] *= gelu_grad_f(sm100::bf16_hi(w[u]));
+            }
+          }
+        }
+        if (flags & EPI_RESID) {
+          const float4* rp = reinterpret_cast<const float4*>(g.resid + (size_t)row * g.ldr + nb);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 r4 = rp[j];
+            v[4 * j] += r4.x; v[4 * j + 1] += r4.y; v[4 * j + 2] += r4.z; v[4 * j + 3] += r4.w;
+          }
+        }
+        if (flags & EPI_ROWMASK) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] *= rmask;
+        }
+        if (flags & EPI_OUT_F32) {
+          float4* cp = reinterpret_cast<float4*>(g.C + (size_t)row * g.ldc + nb);
+          if (flags & EPI_ATOMIC) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) atomicAdd(cp + j, make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) cp[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          }
+        }
+        if (flags & EPI_OUT_BF16) {
+          uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(g.C_bf16) + (size_t)row * g.ldc_bf + nb);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            op[j] = make_uint4(sm100::pack_bf16(v[8 * j], v[8 * j + 1]), sm100::pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                               sm100::pack_bf16(v[8 * j + 4], v[8 * j + 5]), sm100::pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+        }
+      } else {
+        // ragged last chunk: scalar path
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int n = nb + j;
+          if (n >= g.N) continue;
+          float x = v[j];
+          if (flags & EPI_BIAS) x += g.bias[n];
+          if (flags & EPI_SAVE_PRE)
+            reinterpret_cast<__nv_bfloat16*>(g.pre_bf16)[(size_t)row * g.ldc_bf + n] = __float2bfloat16(x);
+          if (flags & EPI_GELU) x = gelu_f(x);
+          if (flags & EPI_GELU_BWD)
+            x *= gelu_grad_f(__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(g.pre_bf16)[(size_t)row * g.ldc_bf + n]));
+          if (flags & EPI_RESID) x += g.resid[(size_t)row * g.ldr + n];
+          x *= rmask;
+          if (flags & EPI_OUT_F32) {
+            float* dst = g.C + (size_t)row * g.ldc + n;
+            if (flags & EPI_ATOMIC) atomicAdd(dst, x); else *dst = x;
+          }
+          if (flags & EPI_OUT_BF16)
+            reinterpret_cast<__nv_bfloat16*>(g.C_bf16)[(size_t)row * g.ldc_bf + n] = __float2bfloat16(x);
+        }
       }
-      __syncwarp();
     }
   }
   sm100::tc_fence_before();
