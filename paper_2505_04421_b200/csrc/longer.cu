@@ -440,7 +440,13 @@ int block_fwd(const Ctx& c, const BlockOff& bo, BlockBufs& b, const float* xq, b
     a.V = b.qkv + 2 * D; a.ldv = 3 * D; a.sv = a.sq;
     a.nk = p.q; a.ns = p.k; a.goff = p.G - p.k;
   }
-  if (cross && use_attn_tc(a)) { probe(PH_XATTN_FWD, 0, st); TRY(attn_tc_fwd(a, st)); probe(PH_XATTN_FWD, 1, st); } else attn_fwd(a, st);
+  if (use_attn_tc(a)) {
+    if (cross) probe(PH_XATTN_FWD, 0, st);
+    TRY(attn_tc_fwd(a, st));
+    if (cross) probe(PH_XATTN_FWD, 1, st);
+  } else {
+    attn_fwd(a, st);
+  }
   TRY(lin_fwd(st, b.ctx, D, Q, Wo, D, D, c.w(bo.b_o), 0, b.x1, nullptr, nullptr, xq, D));
   layernorm_fwd(rows_plain(b.x1, D, Q), D, c.w(bo.ln2_g), c.w(bo.ln2_b), b.x1n, b.m2, b.r2, st);
   TRY(lin_fwd(st, b.x1n, D, Q, W1, D, 4 * D, c.w(bo.b1), EPI_GELU | EPI_SAVE_PRE, nullptr, b.gf, b.f1));
@@ -629,7 +635,13 @@ int block_bwd(const Ctx& c, const BlockOff& bo, const BlockBufs& b, const float*
     a.dK = p.dqkv + D; a.lddk = 3 * D; a.sdk = a.sdq;
     a.dV = p.dqkv + 2 * D; a.lddv = 3 * D; a.sdv = a.sdq;
   }
-  if (cross && use_attn_tc(a)) { probe(PH_XATTN_BWD, 0, st); TRY(attn_tc_bwd(a, st)); probe(PH_XATTN_BWD, 1, st); } else attn_bwd(a, st);
+  if (use_attn_tc(a)) {
+    if (cross) probe(PH_XATTN_BWD, 0, st);
+    TRY(attn_tc_bwd(a, st));
+    if (cross) probe(PH_XATTN_BWD, 1, st);
+  } else {
+    attn_bwd(a, st);
+  }
   if (cross) {
     TRY(lin_dx(st, p.dqkv, D, Q, Wqkv, D, D, D, p.dqn, D, nullptr, 0));
     TRY(lin_dw(st, b.qn, D, D, p.dqkv, D, D, Q, c.g(bo.w_q)));
