@@ -18,6 +18,7 @@ constexpr int kFP = 32;                 // featuriser K: F = d_item + d_act + d_
 constexpr int kTile = 128;              // tokens per tile (= UMMA M = TMEM lanes)
 constexpr int kWorkers = 4;
 constexpr int kThreads = 32 * (1 + kWorkers);
+constexpr int kThreads8 = 32 * (1 + 2 * kWorkers);   // MMA warp + 8 worker warps (two per lane quarter)
 
 __host__ __device__ __forceinline__ int canon(int row, int k, int Kdim) {
   return (row >> 3) * (Kdim * 8) + (k >> 3) * 64 + (row & 7) * 8 + (k & 7);

@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
 // and accumulate, in TMEM for the whole kernel, dW2 += g1ᵀ·dh, [dW1ᵀ | db1] += da1ᵀ·[x0 | 1],
 // dW_tpᵀ += dx0ᵀ·feat.  Table gradients are privatised in smem; abs-pos rows get global atomics.
 template <int DT>
-__global__ void __launch_bounds__(kThreads, 1) fe_mlp_bwd_kernel(FrontArgs a) {
+__global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   const int Dm = DT * a.K;
   const int H2 = 2 * Dm;
@@ -384,8 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1) fe_mlp_bwd_kernel(FrontArgs a) {
   float* s_item = s_tab;
   float* s_act = s_item + (item_smem ? n_item : 0);
   float* s_time = s_act + n_act;
-  float* s_b1 = s_time + n_time;                 // seq_b1 staged once (H2)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_b1 + H2 + 2);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_time + n_time + 2);
   bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(bars) + 7) & ~uintptr_t(7));
   uint64_t* bar_w = bars;
   uint64_t* bar_a = bars + 1;
@@ -394,10 +393,9 @@ __global__ void __launch_bounds__(kThreads, 1) fe_mlp_bwd_kernel(FrontArgs a) {
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < (item_smem ? n_item : 0) + n_act + n_time; i += blockDim.x) s_tab[i] = 0.f;
-  for (int i = threadIdx.x; i < H2; i += blockDim.x) s_b1[i] = a.seq_b1[i];
   if (threadIdx.x == 0) {
     sm100::mbar_init(bar_w, 1);
-    sm100::mbar_init(bar_a, 32 * kWorkers);
+    sm100::mbar_init(bar_a, 32 * 2 * kWorkers);
     sm100::mbar_init(bar_d, 1);
     sm100::fence_barrier_init();
   }
@@ -458,51 +456,73 @@ __global__ void __launch_bounds__(kThreads, 1) fe_mlp_bwd_kernel(FrontArgs a) {
       }
     }
   } else {
+    // 8 worker warps: two per TMEM lane quarter.  Group 0 (warps 1-4) and group 1 (warps 5-8) see the
+    // same 32 token rows; the wide GELU/GELU' stage is split by columns, the row-wise stages by task.
     const int q = warp & 3;
+    const int grp = (warp - 1) >> 2;
     const int row = q * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     uint32_t pd = 0;
     auto signal = [&]() { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(bar_a); };
     auto wait_d = [&]() { sm100::mbar_wait(bar_d, pd); pd ^= 1; sm100::tc_fence_after(); };
-    float acc_b2 = 0.f, acc_btp = 0.f;     // column sums (lane c ↔ column c)
+    float acc_b2 = 0.f, acc_btp = 0.f;     // column sums (lane c ↔ column c), group 1
     int my_tiles = 0;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++my_tiles) {
       const TokenInfo ti = token_info(a, tile, row);
-      float v[kFP];
-      int ids[3];
-      featurise(a, ti, v, ids, false);
-      v[kFP - 1] = 1.f;                                                // bias column
-      store_row(sFeat, row, kFP, v, kFP);
-      float dh[DT];
-      if (ti.real) {
-        const float4* src = reinterpret_cast<const float4*>(a.dh + ti.t * DT);
+      int ids[3] = {0, 0, 0};
+      if (grp == 0) {
+        float v[kFP];
+        featurise(a, ti, v, ids, false);
+        v[kFP - 1] = 1.f;                                              // bias column
+        store_row(sFeat, row, kFP, v, kFP);
+      } else {
+        if (ti.real) {
+          const long long src = (long long)ti.b * a.L + (ti.j - (a.Lp - a.L));
+          const int act = a.actions[src], dt = a.dt[src];
+          ids[1] = (act < 0 || act >= a.n_actions) ? 0 : act;
+          ids[2] = min(32 - __clz(max(dt, 0)), a.nb - 1);
+        }
+        float dh[DT];
+        if (ti.real) {
+          const float4* src = reinterpret_cast<const float4*>(a.dh + ti.t * DT);
+#pragma unroll
+          for (int c = 0; c < DT; c += 4) {
+            const float4 f4 = src[c / 4];
+            dh[c] = f4.x; dh[c + 1] = f4.y; dh[c + 2] = f4.z; dh[c + 3] = f4.w;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < DT; ++c) dh[c] = 0.f;
+        }
+        store_row(sDH, row, DT, dh, DT);
+        acc_b2 += warp_colsum<DT>(dh);                                 // db_seq2 = Σ dh
+      }
+      signal();
+      // x0 recompute (group 0; the abs-pos gather is issued before the MMA wait)
+      if (grp == 0) {
+        float x[DT + 16];
+        const float4* pp = reinterpret_cast<const float4*>(a.pos_tab + (long long)ti.rec * DT);
 #pragma unroll
         for (int c = 0; c < DT; c += 4) {
-          const float4 f4 = src[c / 4];
-          dh[c] = f4.x; dh[c + 1] = f4.y; dh[c + 2] = f4.z; dh[c + 3] = f4.w;
+          const float4 p4 = __ldg(pp + c / 4);
+          x[c] = p4.x; x[c + 1] = p4.y; x[c + 2] = p4.z; x[c + 3] = p4.w;
         }
+        wait_d();
+        float acc[DT];
+        tmem_row<DT>(T_X0 + lane_off, acc);
+#pragma unroll
+        for (int c = 0; c < DT; ++c) x[c] = ti.real ? x[c] + acc[c] : 0.f;
+#pragma unroll
+        for (int c = DT; c < DT + 16; ++c) x[c] = c == DT ? 1.f : 0.f;
+        store_row(sX0, row, XK, x, XK);
       } else {
-#pragma unroll
-        for (int c = 0; c < DT; ++c) dh[c] = 0.f;
+        wait_d();
       }
-      store_row(sDH, row, DT, dh, DT);
-      acc_b2 += warp_colsum<DT>(dh);                                   // db_seq2 = Σ dh
-      signal();
-      // x0 recompute
-      float x[DT + 16];
-      wait_d();
-      tmem_row<DT>(T_X0 + lane_off, x);
-#pragma unroll
-      for (int c = 0; c < DT; ++c)
-        x[c] = ti.real ? x[c] + __ldg(a.pos_tab + (long long)ti.rec * DT + c) : 0.f;
-#pragma unroll
-      for (int c = DT; c < DT + 16; ++c) x[c] = c == DT ? 1.f : 0.f;
-      store_row(sX0, row, XK, x, XK);
       signal();
       for (int hj = 0; hj < nh; ++hj) {
         wait_d();
 #pragma unroll 1
-        for (int c0 = 0; c0 < 128; c0 += 32) {
+        for (int c0 = 64 * grp; c0 < 64 * grp + 64; c0 += 32) {
           float av[32], gv[32];
           tmem_row<32>(T_A1 + lane_off + c0, av);
           tmem_row<32>(T_G1 + lane_off + c0, gv);
@@ -523,52 +543,60 @@ __global__ void __launch_bounds__(kThreads, 1) fe_mlp_bwd_kernel(FrontArgs a) {
       tmem_row<DT>(T_DX0 + lane_off, dx0);
 #pragma unroll
       for (int c = 0; c < DT; ++c) dx0[c] = ti.real ? dx0[c] : 0.f;
-      store_row(sDX0, row, DT, dx0, DT);
-      if (ti.real) {
-        float* gp = a.g_pos + (long long)ti.rec * DT;
+      if (grp == 0) {
+        store_row(sDX0, row, DT, dx0, DT);
+        if (ti.real) {
+          float* gp = a.g_pos + (long long)ti.rec * DT;
 #pragma unroll
-        for (int c = 0; c < DT; ++c) atomicAdd(gp + c, dx0[c]);
+          for (int c = 0; c < DT; ++c) atomicAdd(gp + c, dx0[c]);
+        }
+      } else {
+        acc_btp += warp_colsum<DT>(dx0);                               // db_tp = Σ dx0
       }
-      acc_btp += warp_colsum<DT>(dx0);                                 // db_tp = Σ dx0
       signal();
       wait_d();
       float df[kFP];
       tmem_row<kFP>(T_X0 + lane_off, df);
       const int e1 = a.d_item, e2 = e1 + a.d_act;
-      if (ti.real) {
-        float* gi = (item_smem ? s_item : a.g_item) + ids[0] * a.d_item;
+      if (grp == 0) {
+        if (ti.real) {
+          float* gi = (item_smem ? s_item : a.g_item) + ids[0] * a.d_item;
 #pragma unroll
-        for (int c = 0; c < kFP; ++c)
-          if (c < e1) atomicAdd(gi + c, df[c]);
+          for (int c = 0; c < kFP; ++c)
+            if (c < e1) atomicAdd(gi + c, df[c]);
+        }
+      } else {
+        // action / time-bucket rows repeat across consecutive events: aggregate equal ids in the
+        // warp before touching shared memory
+        warp_scatter_add(s_act, ti.real ? ids[1] : -1, df, e1, a.d_act);
+        warp_scatter_add(s_time, ti.real ? ids[2] : -1, df, e2, a.d_time);
       }
-      // action / time-bucket rows repeat across consecutive events: aggregate equal ids in the
-      // warp before touching shared memory (a 4-row table would otherwise serialise 128 threads)
-      warp_scatter_add(s_act, ti.real ? ids[1] : -1, df, e1, a.d_act);
-      warp_scatter_add(s_time, ti.real ? ids[2] : -1, df, e2, a.d_time);
     }
-    // ---------------- flush the CTA's accumulators
+    // ---------------- flush the CTA's accumulators (group 0: dW2, dW_tp; group 1: dW1, biases)
     if (my_tiles > 0) {
       for (int j = 0; j < nh; ++j) {
         const int f = 128 * j + row;                                   // hidden unit
-        float w2[DT];
-        tmem_row<DT>(T_DW2 + lane_off + j * DT, w2);
+        if (grp == 0) {
+          float w2[DT];
+          tmem_row<DT>(T_DW2 + lane_off + j * DT, w2);
 #pragma unroll
-        for (int c = 0; c < DT; ++c) atomicAdd(a.g_seq_w2 + (long long)f * DT + c, w2[c]);
-        float w1[DT + 16];
-        tmem_row<DT + 16>(T_DW1 + lane_off + j * XK, w1);
+          for (int c = 0; c < DT; ++c) atomicAdd(a.g_seq_w2 + (long long)f * DT + c, w2[c]);
+        } else {
+          float w1[DT + 16];
+          tmem_row<DT + 16>(T_DW1 + lane_off + j * XK, w1);
 #pragma unroll
-        for (int c = 0; c < DT; ++c) atomicAdd(a.g_seq_w1 + (long long)c * H2 + f, w1[c]);
-        atomicAdd(a.g_seq_b1 + f, w1[DT]);
+          for (int c = 0; c < DT; ++c) atomicAdd(a.g_seq_w1 + (long long)c * H2 + f, w1[c]);
+          atomicAdd(a.g_seq_b1 + f, w1[DT]);
+        }
       }
-      {
+      if (grp == 0) {
         float wt[kFP];
         tmem_row<kFP>(T_DWTP + lane_off, wt);                           // warp-collective load
         if (row < DT) {
           const int F = a.d_item + a.d_act + a.d_time;
           for (int k = 0; k < F; ++k) atomicAdd(a.g_tok_w + k * DT + row, wt[k]);
         }
-      }
-      if (lane < DT) {
+      } else if (lane < DT) {
         atomicAdd(a.g_seq_b2 + lane, acc_b2);
         atomicAdd(a.g_tok_b + lane, acc_btp);
       }
@@ -688,7 +716,7 @@ static int launch_mlp_bwd(const FrontArgs& a, cudaStream_t st) {
   const long long ntiles = (a.T + kTile - 1) / kTile;
   const int grid = (int)std::min<long long>(ntiles, 148);
   // > 113 KB of smem keeps one CTA per SM (the kernel allocates all 512 TMEM columns)
-  fe_mlp_bwd_kernel<DT><<<grid, kThreads, std::max(smem, 116 * 1024), st>>>(a);
+  fe_mlp_bwd_kernel<DT><<<grid, kThreads8, std::max(smem, 116 * 1024), st>>>(a);
   return (int)cudaGetLastError();
 }
 
