@@ -354,8 +354,12 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
 // ------------------------------------------------------------------ token-MLP + featuriser backward
 // Per tile: recompute feat, x0 and the hidden a1 (one 128-column half at a time), then
 //   da1 = (dh·W2ᵀ) ⊙ GELU'(a1),   dx0 = da1·W1ᵀ,   dfeat = dx0·W_tpᵀ
-// and accumulate, in TMEM for the whole kernel, dW2 += g1ᵀ·dh, [dW1ᵀ | db1] += da1ᵀ·[x0 | 1],
-// dW_tpᵀ += dx0ᵀ·feat.  Table gradients are privatised in smem; abs-pos rows get global atomics.
+// and accumulate, in TMEM for the whole kernel:
+//   dW2 += g1ᵀ·dh,   [dW1ᵀ | db1] += da1ᵀ·[x0 | 1],
+//   [dW_tpᵀ | db_tp ; · | db2] += [dx0 | dh]ᵀ·[feat | 1]       (bias sums from the ones column)
+//   Y += onehot([bucket | action])ᵀ·dx0                        (time / action table grads = Y·W_tpᵀ)
+// Tiles are column blocks of one sample (token position fixed per thread for the whole kernel), so
+// the abs-pos rows are loaded once and their gradient accumulates in shared memory.
 template <int DT>
 __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -372,19 +376,19 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
   bf16* w_tp_n = w_w1 + n_w1f;
   bf16* w_w1_n = w_tp_n + n_tp;
   bf16* w_w2_n = w_w1_n + n_w1;
-  bf16* sFeat = w_w2_n + n_w1;                 // 128 x 32
-  bf16* sX0 = sFeat + kTile * kFP;             // 128 x XK
+  bf16* sFeat = w_w2_n + n_w1;                 // 128 x 32   [feat | 1]
+  bf16* sX0 = sFeat + kTile * kFP;             // 128 x XK   [x0 | 1]
   bf16* sDH = sX0 + kTile * XK;                // 128 x DT
   bf16* sG = sDH + kTile * DT;                 // 128 x 128
   bf16* sDA = sG + kTile * 128;                // 128 x 128
-  bf16* sDX0 = sDA + kTile * 128;              // 128 x DT
-  float* s_tab = reinterpret_cast<float*>(sDX0 + kTile * DT);
-  const int n_item = a.vocab * a.d_item, n_act = a.n_actions * a.d_act, n_time = a.nb * a.d_time;
+  bf16* sDX0 = sDA + kTile * 128;              // 128 x 64   [dx0 | dh]
+  bf16* sOH = sDX0 + kTile * 64;               // 128 x 64   [onehot(bucket) | onehot(action)]
+  float* s_pos = reinterpret_cast<float*>(sOH + kTile * 64);        // 128 x (DT+1)
+  float* s_gpos = s_pos + kTile * (DT + 1);                         // 128 x (DT+1)
+  float* s_item = s_gpos + kTile * (DT + 1);
+  const int n_item = a.vocab * a.d_item;
   const bool item_smem = n_item <= 16384;
-  float* s_item = s_tab;
-  float* s_act = s_item + (item_smem ? n_item : 0);
-  float* s_time = s_act + n_act;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_time + n_time + 2);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_item + (item_smem ? n_item : 0) + 2);
   bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(bars) + 7) & ~uintptr_t(7));
   uint64_t* bar_w = bars;
   uint64_t* bar_a = bars + 1;
@@ -392,7 +396,17 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < (item_smem ? n_item : 0) + n_act + n_time; i += blockDim.x) s_tab[i] = 0.f;
+  // column-block tiling: this CTA owns token positions [cb*128, cb*128+128) of samples b0, b0+r, …
+  const int tps = (a.Lp + kTile - 1) / kTile;
+  const int r = gridDim.x / tps;
+  const int cb = blockIdx.x % tps, b0 = blockIdx.x / tps;
+  for (int i = threadIdx.x; i < (item_smem ? n_item : 0); i += blockDim.x) s_item[i] = 0.f;
+  for (int i = threadIdx.x; i < kTile * DT; i += blockDim.x) {
+    const int rr = i / DT, c = i % DT;
+    const int rec = a.Lp - 1 - (cb * kTile + rr);
+    s_pos[rr * (DT + 1) + c] = (rec >= 0 && rec < a.L) ? a.pos_tab[(long long)rec * DT + c] : 0.f;
+    s_gpos[rr * (DT + 1) + c] = 0.f;
+  }
   if (threadIdx.x == 0) {
     sm100::mbar_init(bar_w, 1);
     sm100::mbar_init(bar_a, 32 * 2 * kWorkers);
@@ -407,12 +421,11 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
   // TMEM columns
   const uint32_t T_DW2 = tmem;                         // nh x DT
   const uint32_t T_DW1 = tmem + nh * DT;               // nh x XK
-  const uint32_t T_DWTP = T_DW1 + nh * XK;             // kFP
-  const uint32_t T_X0 = T_DWTP + kFP;                  // DT (x0 acc), later dfeat (kFP)
-  const uint32_t T_DX0 = T_X0 + kFP;                   // DT
-  const uint32_t T_A1 = T_DX0 + 32;                    // 128
-  const uint32_t T_G1 = T_A1 + 128;                    // 128
-  const long long ntiles = (a.T + kTile - 1) / kTile;
+  const uint32_t T_DWTP = tmem + 160;                  // 32: [dWtpᵀ | db_tp] rows 0..DT, db2 rows DT..2DT (col 31)
+  const uint32_t T_Y = tmem + 192;                     // 32: onehotᵀ·dx0
+  const uint32_t T_X = tmem + 224;                     // 32: x0 acc → dx0 acc → dfeat
+  const uint32_t T_A1 = tmem + 256;                    // 128
+  const uint32_t T_G1 = tmem + 384;                    // 128
 
   if (warp == 0) {
     if (lane == 0) {
@@ -425,23 +438,23 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
       const uint32_t aW1n = sm100::smem_u32(w_w1_n), aW2n = sm100::smem_u32(w_w2_n);
       const uint32_t aFeat = sm100::smem_u32(sFeat), aX0 = sm100::smem_u32(sX0), aDH = sm100::smem_u32(sDH);
       const uint32_t aG = sm100::smem_u32(sG), aDA = sm100::smem_u32(sDA), aDX0 = sm100::smem_u32(sDX0);
+      const uint32_t aOH = sm100::smem_u32(sOH);
       uint32_t pa = 0;
       auto wait_a = [&]() { sm100::mbar_wait(bar_a, pa); pa ^= 1; sm100::tc_fence_after(); };
       bool first = true;
-      for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        wait_a();                                                        // feat, dh
-        mma(T_X0, Opnd{aFeat, kFP, 0}, Opnd{aTP, kFP, 0}, kFP / 16, DT, false);
+      for (int b = b0; b < a.B; b += r) {
+        wait_a();                                                        // feat, dh, onehot
+        mma(T_X, Opnd{aFeat, kFP, 0}, Opnd{aTP, kFP, 0}, kFP / 16, DT, false);
         sm100::mma_commit(bar_d);
         wait_a();                                                        // x0
-        // hidden half 0: a1 (recompute) and dg1 = dh·W2ᵀ
         mma(T_A1, Opnd{aX0, XK, 0}, Opnd{aW1, XK, 0}, XK / 16, 128, false);
         mma(T_G1, Opnd{aDH, DT, 0}, Opnd{aW2n, DT, 0}, DT / 16, 128, false);
         sm100::mma_commit(bar_d);
         for (int j = 0; j < nh; ++j) {
-          wait_a();                                                      // g1, da1 of half j in sG / sDA
+          wait_a();                                                      // g1, da1 of half j
           mma(T_DW2 + j * DT, Opnd{aG, 128, 1}, Opnd{aDH, DT, 1}, kTile / 16, DT, !first);
           mma(T_DW1 + j * XK, Opnd{aDA, 128, 1}, Opnd{aX0, XK, 1}, kTile / 16, XK, !first);
-          mma(T_DX0, Opnd{aDA, 128, 0}, Opnd{aW1n + canon(0, 128 * j, H2) * 2, H2, 0}, 8, DT, j > 0);
+          mma(T_X, Opnd{aDA, 128, 0}, Opnd{aW1n + canon(0, 128 * j, H2) * 2, H2, 0}, 8, DT, j > 0);
           if (j + 1 < nh) {
             mma(T_A1, Opnd{aX0, XK, 0}, Opnd{aW1 + canon(128 * (j + 1), 0, XK) * 2, XK, 0}, XK / 16, 128, false);
             mma(T_G1, Opnd{aDH, DT, 0}, Opnd{aW2n + canon(128 * (j + 1), 0, DT) * 2, DT, 0}, DT / 16, 128, false);
@@ -449,8 +462,9 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
           sm100::mma_commit(bar_d);
         }
         wait_a();                                                        // dx0 in sDX0
-        mma(T_DWTP, Opnd{aDX0, DT, 1}, Opnd{aFeat, kFP, 1}, kTile / 16, kFP, !first);
-        mma(T_X0, Opnd{aDX0, DT, 0}, Opnd{aTPn, DT, 0}, DT / 16, kFP, false);
+        mma(T_DWTP, Opnd{aDX0, 64, 1}, Opnd{aFeat, kFP, 1}, kTile / 16, kFP, !first);
+        mma(T_Y, Opnd{aOH, 64, 1}, Opnd{aDX0, 64, 1}, kTile / 16, DT, !first);
+        mma(T_X, Opnd{aDX0, 64, 0}, Opnd{aTPn, DT, 0}, DT / 16, kFP, false);
         sm100::mma_commit(bar_d);
         first = false;
       }
@@ -462,26 +476,32 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
     const int grp = (warp - 1) >> 2;
     const int row = q * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const int j = cb * kTile + row;                    // token position inside the sample (fixed)
+    const bool col_ok = j < a.Lp;
     uint32_t pd = 0;
     auto signal = [&]() { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(bar_a); };
     auto wait_d = [&]() { sm100::mbar_wait(bar_d, pd); pd ^= 1; sm100::tc_fence_after(); };
-    float acc_b2 = 0.f, acc_btp = 0.f;     // column sums (lane c ↔ column c), group 1
     int my_tiles = 0;
-    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++my_tiles) {
-      const TokenInfo ti = token_info(a, tile, row);
+    for (int b = b0; b < a.B; b += r, ++my_tiles) {
+      TokenInfo ti;
+      ti.b = b; ti.j = j;
+      ti.in_range = col_ok;
+      ti.t = (long long)b * a.Lp + j;
+      ti.n = min(max(a.n_events[b], 0), a.L);
+      ti.real = col_ok && j >= a.Lp - ti.n;
+      ti.keep = col_ok && (j / a.K) >= (a.Lp - ti.n) / a.K;
+      ti.rec = ti.real ? a.Lp - 1 - j : 0;
       int ids[3] = {0, 0, 0};
       if (grp == 0) {
         float v[kFP];
         featurise(a, ti, v, ids, false);
         v[kFP - 1] = 1.f;                                              // bias column
         store_row(sFeat, row, kFP, v, kFP);
+        float oh[64];
+#pragma unroll
+        for (int c = 0; c < 64; ++c) oh[c] = (ti.real && (c == ids[2] || c == 32 + ids[1])) ? 1.f : 0.f;
+        store_row(sOH, row, 64, oh, 64);
       } else {
-        if (ti.real) {
-          const long long src = (long long)ti.b * a.L + (ti.j - (a.Lp - a.L));
-          const int act = a.actions[src], dt = a.dt[src];
-          ids[1] = (act < 0 || act >= a.n_actions) ? 0 : act;
-          ids[2] = min(32 - __clz(max(dt, 0)), a.nb - 1);
-        }
         float dh[DT];
         if (ti.real) {
           const float4* src = reinterpret_cast<const float4*>(a.dh + ti.t * DT);
@@ -495,28 +515,18 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
           for (int c = 0; c < DT; ++c) dh[c] = 0.f;
         }
         store_row(sDH, row, DT, dh, DT);
-        acc_b2 += warp_colsum<DT>(dh);                                 // db_seq2 = Σ dh
+        store_row(sDX0, row, 64, dh, DT, 32);                          // [· | dh] for the db2 row sums
       }
       signal();
-      // x0 recompute (group 0; the abs-pos gather is issued before the MMA wait)
-      if (grp == 0) {
-        float x[DT + 16];
-        const float4* pp = reinterpret_cast<const float4*>(a.pos_tab + (long long)ti.rec * DT);
+      wait_d();
+      if (grp == 0) {                                                  // x0 recompute
+        float x[DT + 16], acc[DT];
+        tmem_row<DT>(T_X + lane_off, acc);
 #pragma unroll
-        for (int c = 0; c < DT; c += 4) {
-          const float4 p4 = __ldg(pp + c / 4);
-          x[c] = p4.x; x[c + 1] = p4.y; x[c + 2] = p4.z; x[c + 3] = p4.w;
-        }
-        wait_d();
-        float acc[DT];
-        tmem_row<DT>(T_X0 + lane_off, acc);
-#pragma unroll
-        for (int c = 0; c < DT; ++c) x[c] = ti.real ? x[c] + acc[c] : 0.f;
+        for (int c = 0; c < DT; ++c) x[c] = ti.real ? acc[c] + s_pos[row * (DT + 1) + c] : 0.f;
 #pragma unroll
         for (int c = DT; c < DT + 16; ++c) x[c] = c == DT ? 1.f : 0.f;
         store_row(sX0, row, XK, x, XK);
-      } else {
-        wait_d();
       }
       signal();
       for (int hj = 0; hj < nh; ++hj) {
@@ -539,76 +549,89 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
         signal();
       }
       wait_d();
-      float dx0[DT];
-      tmem_row<DT>(T_DX0 + lane_off, dx0);
-#pragma unroll
-      for (int c = 0; c < DT; ++c) dx0[c] = ti.real ? dx0[c] : 0.f;
       if (grp == 0) {
-        store_row(sDX0, row, DT, dx0, DT);
-        if (ti.real) {
-          float* gp = a.g_pos + (long long)ti.rec * DT;
+        float dx0[DT];
+        tmem_row<DT>(T_X + lane_off, dx0);
 #pragma unroll
-          for (int c = 0; c < DT; ++c) atomicAdd(gp + c, dx0[c]);
+        for (int c = 0; c < DT; ++c) {
+          dx0[c] = ti.real ? dx0[c] : 0.f;
+          s_gpos[row * (DT + 1) + c] += dx0[c];                        // abs-pos row of this position
         }
-      } else {
-        acc_btp += warp_colsum<DT>(dx0);                               // db_tp = Σ dx0
+        store_row(sDX0, row, 64, dx0, DT, 0);
       }
       signal();
       wait_d();
-      float df[kFP];
-      tmem_row<kFP>(T_X0 + lane_off, df);
-      const int e1 = a.d_item, e2 = e1 + a.d_act;
-      if (grp == 0) {
+      if (grp == 0) {                                                  // item rows: dfeat[:d_item]
+        float df[kFP];
+        tmem_row<kFP>(T_X + lane_off, df);
         if (ti.real) {
           float* gi = (item_smem ? s_item : a.g_item) + ids[0] * a.d_item;
 #pragma unroll
           for (int c = 0; c < kFP; ++c)
-            if (c < e1) atomicAdd(gi + c, df[c]);
+            if (c < a.d_item) atomicAdd(gi + c, df[c]);
         }
-      } else {
-        // action / time-bucket rows repeat across consecutive events: aggregate equal ids in the
-        // warp before touching shared memory
-        warp_scatter_add(s_act, ti.real ? ids[1] : -1, df, e1, a.d_act);
-        warp_scatter_add(s_time, ti.real ? ids[2] : -1, df, e2, a.d_time);
       }
     }
-    // ---------------- flush the CTA's accumulators (group 0: dW2, dW_tp; group 1: dW1, biases)
+    // ---------------- flush the CTA's accumulators
     if (my_tiles > 0) {
-      for (int j = 0; j < nh; ++j) {
-        const int f = 128 * j + row;                                   // hidden unit
+      const int F = a.d_item + a.d_act + a.d_time;
+      for (int jh = 0; jh < nh; ++jh) {
+        const int f = 128 * jh + row;                                  // hidden unit
         if (grp == 0) {
           float w2[DT];
-          tmem_row<DT>(T_DW2 + lane_off + j * DT, w2);
+          tmem_row<DT>(T_DW2 + lane_off + jh * DT, w2);
 #pragma unroll
           for (int c = 0; c < DT; ++c) atomicAdd(a.g_seq_w2 + (long long)f * DT + c, w2[c]);
         } else {
           float w1[DT + 16];
-          tmem_row<DT + 16>(T_DW1 + lane_off + j * XK, w1);
+          tmem_row<DT + 16>(T_DW1 + lane_off + jh * XK, w1);
 #pragma unroll
           for (int c = 0; c < DT; ++c) atomicAdd(a.g_seq_w1 + (long long)c * H2 + f, w1[c]);
           atomicAdd(a.g_seq_b1 + f, w1[DT]);
         }
       }
       if (grp == 0) {
+        // rows 0..DT-1: [dW_tpᵀ | db_tp]; rows 32..32+DT-1 (the dh half of sDX0): Σ dh (db2)
         float wt[kFP];
-        tmem_row<kFP>(T_DWTP + lane_off, wt);                           // warp-collective load
+        tmem_row<kFP>(T_DWTP + lane_off, wt);                          // warp-collective load
         if (row < DT) {
-          const int F = a.d_item + a.d_act + a.d_time;
           for (int k = 0; k < F; ++k) atomicAdd(a.g_tok_w + k * DT + row, wt[k]);
+          atomicAdd(a.g_tok_b + row, wt[kFP - 1]);
+        } else if (row >= 32 && row < 32 + DT) {
+          atomicAdd(a.g_seq_b2 + row - 32, wt[kFP - 1]);
         }
-      } else if (lane < DT) {
-        atomicAdd(a.g_seq_b2 + lane, acc_b2);
-        atomicAdd(a.g_tok_b + lane, acc_btp);
+      } else {
+        // Y rows: bucket b (0..31) and action 32+a: table grad = Y_row · W_tp[cols]ᵀ
+        float y[DT];
+        tmem_row<DT>(T_Y + lane_off, y);
+        const int e1 = a.d_item, e2 = e1 + a.d_act;
+        if (row < a.nb) {
+          for (int c = 0; c < a.d_time; ++c) {
+            float acc = 0.f;
+#pragma unroll
+            for (int k = 0; k < DT; ++k) acc = fmaf(y[k], a.tok_w[(e2 + c) * DT + k], acc);
+            atomicAdd(a.g_time + row * a.d_time + c, acc);
+          }
+        } else if (row >= 32 && row < 32 + a.n_actions) {
+          for (int c = 0; c < a.d_act; ++c) {
+            float acc = 0.f;
+#pragma unroll
+            for (int k = 0; k < DT; ++k) acc = fmaf(y[k], a.tok_w[(e1 + c) * DT + k], acc);
+            atomicAdd(a.g_act + (row - 32) * a.d_act + c, acc);
+          }
+        }
       }
     }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < (item_smem ? n_item : 0); i += blockDim.x)
     if (s_item[i] != 0.f) atomicAdd(a.g_item + i, s_item[i]);
-  for (int i = threadIdx.x; i < n_act; i += blockDim.x)
-    if (s_act[i] != 0.f) atomicAdd(a.g_act + i, s_act[i]);
-  for (int i = threadIdx.x; i < n_time; i += blockDim.x)
-    if (s_time[i] != 0.f) atomicAdd(a.g_time + i, s_time[i]);
+  for (int i = threadIdx.x; i < kTile * DT; i += blockDim.x) {
+    const int rr = i / DT, c = i % DT;
+    const int rec = a.Lp - 1 - (cb * kTile + rr);
+    const float v = s_gpos[rr * (DT + 1) + c];
+    if (rec >= 0 && rec < a.L && v != 0.f) atomicAdd(a.g_pos + (long long)rec * DT + c, v);
+  }
   sm100::tc_fence_before();
   __syncthreads();
   if (warp == 0) sm100::tmem_dealloc<512>(tmem);
@@ -705,18 +728,20 @@ static int launch_mlp_bwd(const FrontArgs& a, cudaStream_t st) {
   const int H2 = 2 * DT * a.K;
   const int XK = DT + 16;
   const int n_item = a.vocab * a.d_item;
-  const int tab = ((n_item <= 16384) ? n_item : 0) + a.n_actions * a.d_act + a.nb * a.d_time;
-  const int smem = (2 * DT * kFP + 2 * H2 * DT + H2 * XK) * 2 + kTile * (kFP + XK + DT + 128 + 128 + DT) * 2 + (tab + H2) * 4 + 128;
+  const int tab = (n_item <= 16384) ? n_item : 0;
+  const int smem = (2 * DT * kFP + 2 * H2 * DT + H2 * XK) * 2 + kTile * (kFP + XK + DT + 128 + 128 + 64 + 64) * 2 +
+                   (2 * kTile * (DT + 1) + tab) * 4 + 128;
   if (smem > 227 * 1024) return (int)cudaErrorInvalidValue;
   static int done = 0;
   if (!done) {
     cudaFuncSetAttribute(fe_mlp_bwd_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     done = 1;
   }
-  const long long ntiles = (a.T + kTile - 1) / kTile;
-  const int grid = (int)std::min<long long>(ntiles, 148);
+  // column-block tiling: grid = tiles-per-sample x replicas (≤ 148 CTAs, one per SM)
+  const int tps = (a.Lp + kTile - 1) / kTile;
+  const int r = std::max(1, std::min(a.B, 148 / tps));
   // > 113 KB of smem keeps one CTA per SM (the kernel allocates all 512 TMEM columns)
-  fe_mlp_bwd_kernel<DT><<<grid, kThreads8, std::max(smem, 116 * 1024), st>>>(a);
+  fe_mlp_bwd_kernel<DT><<<tps * r, kThreads8, std::max(smem, 116 * 1024), st>>>(a);
   return (int)cudaGetLastError();
 }
 

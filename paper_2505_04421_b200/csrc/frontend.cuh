@@ -19,7 +19,7 @@ struct FrontArgs {
   int B, L, Lp, K, d, d_item, d_act, d_time, nb, vocab, n_actions, inner_layers;
   long long T;                 // B * Lp tokens
   // fp32 master parameters (biases, tables)
-  const float *item_tab, *act_tab, *time_tab, *pos_tab, *tok_b, *seq_b1, *seq_b2;
+  const float *item_tab, *act_tab, *time_tab, *pos_tab, *tok_w, *tok_b, *seq_b1, *seq_b2;
   const float* inner_bias[8][6];   // per layer: b_q, b_k, b_v, b_o, b1, b2
   const float* inner_ln[8][4];     // per layer: ln1_g, ln1_b, ln2_g, ln2_b
   // packed bf16 weight blob (see pack_frontend_weights)

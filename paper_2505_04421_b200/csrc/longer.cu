@@ -512,7 +512,7 @@ FrontArgs front_args(const Ctx& c, const Plan& p, const LongerBatch& bt) {
   f.d_time = dm.d_time; f.nb = dm.n_time_buckets; f.vocab = dm.vocab; f.n_actions = dm.n_actions;
   f.inner_layers = p.IL; f.T = p.T;
   f.item_tab = c.w(o.item); f.act_tab = c.w(o.act); f.time_tab = c.w(o.time); f.pos_tab = c.w(o.pos);
-  f.tok_b = c.w(o.tok_b); f.seq_b1 = c.w(o.seq_b1); f.seq_b2 = c.w(o.seq_b2);
+  f.tok_w = c.w(o.tok_w); f.tok_b = c.w(o.tok_b); f.seq_b1 = c.w(o.seq_b1); f.seq_b2 = c.w(o.seq_b2);
   for (int l = 0; l < p.IL; ++l) {
     const BlockOff& b = o.inner[l];
     f.inner_bias[l][0] = c.w(b.b_q); f.inner_bias[l][1] = c.w(b.b_k); f.inner_bias[l][2] = c.w(b.b_v);
@@ -799,7 +799,7 @@ int backward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs) {
 bool use_fused(const Plan& p) {
   const char* env = std::getenv("LONGER_FUSED");
   if (env && env[0] == '0') return false;
-  return frontend_supported(p.d, p.K, p.D, p.F, p.IL) != 0;
+  return frontend_supported(p.d, p.K, p.D, p.F, p.IL) != 0 && p.dims.n_actions <= 32;
 }
 
 int check_call(const LongerDims* dims, size_t ws_bytes, Plan* out, void* ws) {
