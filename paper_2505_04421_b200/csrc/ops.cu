@@ -257,7 +257,7 @@ void layernorm_bwd(const RowMap& x, int W, const float* g, const float* mean, co
                    int ldy, const RowMapW& out, int accumulate, const float* rowmask, float* dgain, float* dbias,
                    cudaStream_t st) {
   const int rows = x.rows();
-  const int grid = std::min(cdiv(rows, 8), 148 * 8);
+  const int grid = std::min(cdiv(rows, 8), 148 * 2);
   if (W <= 32) ln_bwd_kernel<1><<<grid, 256, 0, st>>>(x, W, g, mean, rstd, dy, ldy, out, accumulate, rowmask, dgain, dbias);
   else if (W <= 64) ln_bwd_kernel<2><<<grid, 256, 0, st>>>(x, W, g, mean, rstd, dy, ldy, out, accumulate, rowmask, dgain, dbias);
   else if (W <= 128) ln_bwd_kernel<4><<<grid, 256, 0, st>>>(x, W, g, mean, rstd, dy, ldy, out, accumulate, rowmask, dgain, dbias);
@@ -274,27 +274,35 @@ __global__ void colsum_kernel(const T* __restrict__ x, int rows, int W, int ld, 
   const int r0 = blockIdx.x * rows_per_block;
   const int r1 = min(rows, r0 + rows_per_block);
   for (int c0 = 0; c0 < W; c0 += cpp) {
-    float acc = 0.f;
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
     const int c = c0 + tid % cpp;
-    if (tid < cpp * rpp && c < W)
-      for (int r = r0 + tid / cpp; r < r1; r += rpp) acc += ldf(x + (long long)r * ld + c);
-    red[tid] = acc;
+    if (tid < cpp * rpp && c < W) {
+      int r = r0 + tid / cpp;
+      for (; r + 3 * rpp < r1; r += 4 * rpp) {        // four independent loads in flight
+        a0 += ldf(x + (long long)r * ld + c);
+        a1 += ldf(x + (long long)(r + rpp) * ld + c);
+        a2 += ldf(x + (long long)(r + 2 * rpp) * ld + c);
+        a3 += ldf(x + (long long)(r + 3 * rpp) * ld + c);
+      }
+      for (; r < r1; r += rpp) a0 += ldf(x + (long long)r * ld + c);
+    }
+    red[tid] = (a0 + a1) + (a2 + a3);
     __syncthreads();
     if (tid < cpp && c0 + tid < W) {
-      float s = 0.f;
-      for (int q = 0; q < rpp; ++q) s += red[q * cpp + tid];
-      atomicAdd(&out[c0 + tid], s);
+      float sum = 0.f;
+      for (int qq = 0; qq < rpp; ++qq) sum += red[qq * cpp + tid];
+      atomicAdd(&out[c0 + tid], sum);
     }
     __syncthreads();
   }
 }
 
 void colsum_f32(const float* x, int rows, int W, int ld, float* out, cudaStream_t st) {
-  const int rpb = std::max(64, cdiv(rows, 148 * 4));
+  const int rpb = std::max(64, cdiv(rows, 148 * 2));
   colsum_kernel<float><<<cdiv(rows, rpb), 256, 0, st>>>(x, rows, W, ld, rpb, out);
 }
 void colsum_bf16(const bf16* x, int rows, int W, int ld, float* out, cudaStream_t st) {
-  const int rpb = std::max(64, cdiv(rows, 148 * 4));
+  const int rpb = std::max(64, cdiv(rows, 148 * 2));
   colsum_kernel<bf16><<<cdiv(rows, rpb), 256, 0, st>>>(x, rows, W, ld, rpb, out);
 }
 
@@ -836,11 +844,18 @@ __global__ void head_fwd_kernel(HeadArgs a) {
   __syncthreads();
   for (int i = threadIdx.x; i < HIN; i += blockDim.x) a.hin[(long long)b * HIN + i] = s_in[i];
   float* s_h = s_in + HIN;
-  for (int j = threadIdx.x; j < a.hh; j += blockDim.x) {
-    float acc = a.b1[j];
-    for (int i = 0; i < HIN; ++i) acc = fmaf(s_in[i], a.w1[i * a.hh + j], acc);
-    a.z1[(long long)b * a.hh + j] = acc;
-    s_h[j] = gelu_f(acc);
+  {
+    // warp w handles hidden units j ≡ w (mod warps); lanes split the HIN inputs, then reduce
+    const int wid = threadIdx.x / 32, lane = threadIdx.x & 31, nw = blockDim.x / 32;
+    for (int j = wid; j < a.hh; j += nw) {
+      float acc = 0.f;
+      for (int i = lane; i < HIN; i += 32) acc = fmaf(s_in[i], __ldg(a.w1 + i * a.hh + j), acc);
+      acc = warp_sum(acc) + a.b1[j];
+      if (lane == 0) {
+        a.z1[(long long)b * a.hh + j] = acc;
+        s_h[j] = gelu_f(acc);
+      }
+    }
   }
   __syncthreads();
   if (threadIdx.x < 32) {
@@ -924,28 +939,35 @@ __global__ void head_bwd_kernel(HeadArgs a) {
 }
 
 // head weight gradients: deterministic reductions over the batch (one thread per weight)
-__global__ void head_wgrad_kernel(HeadArgs a) {
+// head weight gradients: batch reductions split over gridDim.y sample slices (atomic combine)
+__global__ void head_wgrad_kernel(HeadArgs a, int per) {
   const int HIN = 4 * a.D + 2 * a.d;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   const int n_w1 = HIN * a.hh;
+  const int b0 = blockIdx.y * per, b1 = min(a.B, b0 + per);
   if (e < n_w1) {
     const int i = e / a.hh, j = e % a.hh;
-    float acc = 0.f;
-    for (int b = 0; b < a.B; ++b) acc = fmaf(a.hin[(long long)b * HIN + i], a.dz1[(long long)b * a.hh + j], acc);
-    a.g_w1[e] += acc;
+    float acc0 = 0.f, acc1 = 0.f;
+    int b = b0;
+    for (; b + 1 < b1; b += 2) {
+      acc0 = fmaf(a.hin[(long long)b * HIN + i], a.dz1[(long long)b * a.hh + j], acc0);
+      acc1 = fmaf(a.hin[(long long)(b + 1) * HIN + i], a.dz1[(long long)(b + 1) * a.hh + j], acc1);
+    }
+    if (b < b1) acc0 = fmaf(a.hin[(long long)b * HIN + i], a.dz1[(long long)b * a.hh + j], acc0);
+    atomicAdd(&a.g_w1[e], acc0 + acc1);
   } else if (e < n_w1 + a.hh) {
     const int j = e - n_w1;
     float acc = 0.f, acc2 = 0.f;
-    for (int b = 0; b < a.B; ++b) {
+    for (int b = b0; b < b1; ++b) {
       acc += a.dz1[(long long)b * a.hh + j];
       acc2 = fmaf(gelu_f(a.z1[(long long)b * a.hh + j]), a.dz[b], acc2);
     }
-    a.g_b1[j] += acc;
-    a.g_w2[j] += acc2;
+    atomicAdd(&a.g_b1[j], acc);
+    atomicAdd(&a.g_w2[j], acc2);
   } else if (e == n_w1 + a.hh) {
     float acc = 0.f;
-    for (int b = 0; b < a.B; ++b) acc += a.dz[b];
-    a.g_b2[0] += acc;
+    for (int b = b0; b < b1; ++b) acc += a.dz[b];
+    atomicAdd(&a.g_b2[0], acc);
   }
 }
 
@@ -953,7 +975,8 @@ void head_bwd(const HeadArgs& a, cudaStream_t st) {
   const int HIN = 4 * a.D + 2 * a.d;
   head_bwd_kernel<<<a.B, 128, 4 * (a.hh + HIN), st>>>(a);
   const int n = HIN * a.hh + a.hh + 1;
-  head_wgrad_kernel<<<cdiv(n, 128), 128, 0, st>>>(a);
+  const int per = 16;
+  head_wgrad_kernel<<<dim3(cdiv(n, 128), cdiv(a.B, per)), 128, 0, st>>>(a, per);
 }
 
 // ============================================================== parameters
