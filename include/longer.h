@@ -88,6 +88,27 @@ int longer_read_status(void* ws, int32_t* flags, void* stream);
 
 const char* longer_last_error(void);
 
+/* ---- Two-stage serving (pkg/src/longrec/serving.py:84-167) --------------------------------
+ * Stage 1, `longer_cache_build`, replaces build_cache (serving.py:84-144) for `dims->batch` users
+ * at once: the batch carries each user's events with dt measured from that user's scoring time
+ * (cand_item and label are ignored and may be null).  It stores, per user, everything that does
+ * not depend on the candidate: the cross layer's key/value rows of the merged sequence and the
+ * m-1 non-target globals, each self layer's key/value rows of the k+m-1 non-target queries
+ * (bf16, the exact rows the full forward feeds its attention), the last layer's CLS row and the
+ * user-side head features.  `cache` is caller-owned device memory of `longer_cache_bytes`.
+ * Stage 2, `longer_cache_score`, replaces score_with_cache (serving.py:147-167) for
+ * `candidates_per_user` candidates of every cached user (cand_items[u * C + j], probs likewise):
+ * only the target rows run through the blocks, against the cached rows plus their own key/value.
+ * Fingerprint / scoring-time staleness (StaleCacheError) is tracked by the host wrapper; the
+ * library checks that the cache size matches `dims` (LONGER_ESTALE otherwise). */
+int longer_cache_bytes(const LongerDims* dims, size_t* bytes);
+int longer_cache_build(const LongerDims* dims, const float* params, const LongerBatch* batch,
+                       void* ws, size_t ws_bytes, void* cache, size_t cache_bytes, void* stream);
+int longer_score_workspace_bytes(const LongerDims* dims, int32_t candidates_per_user, size_t* bytes);
+int longer_cache_score(const LongerDims* dims, const float* params, const void* cache,
+                       size_t cache_bytes, const int32_t* cand_items, int32_t candidates_per_user,
+                       void* ws, size_t ws_bytes, float* probs, void* stream);
+
 /* Diagnostics: record caller-owned CUDA events (cudaEvent_t) immediately before / after one fused
  * kernel of subsequent calls, on the call's stream (graph-capturable).  phase: 0 front-end forward,
  * 1 InnerTrans backward, 2 token-MLP/featuriser backward, 3 cross-attention forward,

@@ -21,7 +21,8 @@ _EXC = {LONGER_ECONFIG: ConfigError, LONGER_EDIM: DimensionError, LONGER_ELOOKUP
         LONGER_ENUMERIC: NumericalError, LONGER_ESTALE: StaleCacheError, LONGER_ECUDA: RuntimeError}
 
 SYMBOLS = ("longer_param_count", "longer_workspace_bytes", "longer_forward", "longer_forward_backward",
-           "longer_adam_step", "longer_read_status", "longer_last_error", "longer_set_probe")
+           "longer_adam_step", "longer_read_status", "longer_last_error", "longer_set_probe",
+           "longer_cache_bytes", "longer_cache_build", "longer_score_workspace_bytes", "longer_cache_score")
 
 PROBES = {"fe_fwd": 0, "fe_inner_bwd": 1, "fe_mlp_bwd": 2, "xattn_fwd": 3, "xattn_bwd": 4}
 
@@ -68,6 +69,10 @@ def _declare(lib):
         "longer_adam_step": [vp, vp, vp, vp, i64, f32, i32, vp],
         "longer_read_status": [vp, ctypes.POINTER(i32), vp],
         "longer_set_probe": [i32, vp, vp],
+        "longer_cache_bytes": [pd, ctypes.POINTER(ctypes.c_size_t)],
+        "longer_cache_build": [pd, vp, pb, vp, ctypes.c_size_t, vp, ctypes.c_size_t, vp],
+        "longer_score_workspace_bytes": [pd, i32, ctypes.POINTER(ctypes.c_size_t)],
+        "longer_cache_score": [pd, vp, vp, ctypes.c_size_t, vp, i32, vp, ctypes.c_size_t, vp, vp],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)

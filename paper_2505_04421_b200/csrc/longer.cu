@@ -16,6 +16,8 @@
 #include "longer.h"
 #include "ops.cuh"
 #include "frontend.cuh"
+#include "serve.cuh"
+#include <algorithm>
 #include <cstdlib>
 
 namespace longer {
@@ -158,6 +160,7 @@ struct Plan {
   ParamOff po;
   int* status;
   int32_t* npg;
+  int32_t* cand0;  // placeholder candidates of a cache build
   Packed pk;
   // tokens
   bf16 *feat, *x0, *a1, *g1;
@@ -187,8 +190,7 @@ struct Plan {
   size_t bytes;
 };
 
-Plan make_plan(const LongerDims& d, void* ws) {
-  Plan p{};
+void plan_dims(Plan& p, const LongerDims& d, void* ws) {
   p.dims = d;
   p.ws = ws;
   p.B = d.batch; p.L = d.L; p.K = d.K; p.d = d.d;
@@ -199,14 +201,10 @@ Plan make_plan(const LongerDims& d, void* ws) {
   p.HIN = 4 * p.D + 2 * d.d;
   p.T = (long long)p.B * p.Lp;
   p.po = param_offsets(d);
-  Bump a{reinterpret_cast<char*>(ws)};
-  const long long T = p.T;
-  const int B = p.B, D = p.D, q = p.q, v = p.v, m = p.m, dd = p.d;
-  const long long Q = (long long)B * q, V = (long long)B * v, M = (long long)B * m;
-  p.status = a.take<int>(64);
-  p.npg = a.take<int32_t>(B);
-  p.wblob = a.take<bf16>(frontend_blob_bytes(dd, D, p.IL) / 2 + 64);
-  // packed weights
+}
+
+void take_packed(Plan& p, Bump& a) {
+  const int D = p.D, dd = p.d;
   p.pk.seq_w1 = a.take<bf16>(dd * 2 * D); p.pk.seq_w2 = a.take<bf16>(2 * D * dd);
   p.pk.glob_w1 = a.take<bf16>(D * 2 * D); p.pk.glob_w2 = a.take<bf16>(2 * D * D);
   for (int i = 0; i < p.IL; ++i) {
@@ -219,6 +217,20 @@ Plan make_plan(const LongerDims& d, void* ws) {
     p.pk.s_wqkv[i] = a.take<bf16>(D * 3 * D); p.pk.s_bqkv[i] = a.take<float>(3 * D);
     p.pk.s_wo[i] = a.take<bf16>(D * D); p.pk.s_w1[i] = a.take<bf16>(D * 4 * D); p.pk.s_w2[i] = a.take<bf16>(4 * D * D);
   }
+}
+
+Plan make_plan(const LongerDims& d, void* ws) {
+  Plan p{};
+  plan_dims(p, d, ws);
+  Bump a{reinterpret_cast<char*>(ws)};
+  const long long T = p.T;
+  const int B = p.B, D = p.D, q = p.q, v = p.v, m = p.m, dd = p.d;
+  const long long Q = (long long)B * q, V = (long long)B * v, M = (long long)B * m;
+  p.status = a.take<int>(64);
+  p.npg = a.take<int32_t>(B);
+  p.cand0 = a.take<int32_t>(B);
+  p.wblob = a.take<bf16>(frontend_blob_bytes(dd, D, p.IL) / 2 + 64);
+  take_packed(p, a);
   // tokens
   p.feat = a.take<bf16>(T * p.FP); p.x0 = a.take<bf16>(T * dd);
   p.real = a.take<float>(T); p.keep = a.take<float>(T);
@@ -812,6 +824,175 @@ int check_call(const LongerDims* dims, size_t ws_bytes, Plan* out, void* ws) {
   return 0;
 }
 
+// ------------------------------------------------------------------ serving (serving.py:84-167)
+// Cache of U users (dims.batch), in one caller-owned buffer:
+//   xkv  [U][v-1][2D] bf16  cross-layer [K | V] of the merged rows + the m-1 non-target globals
+//   skv  [N][U][q-1][2D]    each self layer's [K | V] of the k seq queries + m-1 non-target globals
+//   cls  [U][D] f32         CLS row of the last layer output (serving.py:141)
+//   ud   [U][2d] f32        [uid_emb | profile_emb] (user_side_features)
+//   npg  [U] i32            all-pad merged groups (the target's key mask, serving.py:137-139)
+struct CacheLayout {
+  size_t xkv, skv, cls, ud, npg, bytes;
+  long long xrows, srows;
+};
+
+CacheLayout cache_layout(const Plan& p) {
+  CacheLayout c{};
+  const size_t U = p.B, D = p.D;
+  c.xrows = p.v - 1;
+  c.srows = p.q - 1;
+  size_t off = 0;
+  auto take = [&](size_t n) { off = (off + 255) & ~size_t(255); size_t r = off; off += n; return r; };
+  c.xkv = take(U * c.xrows * 2 * D * 2);
+  c.skv = take((size_t)p.N * U * c.srows * 2 * D * 2);
+  c.cls = take(U * D * 4);
+  c.ud = take(U * 2 * p.d * 4);
+  c.npg = take(U * 4);
+  c.bytes = (off + 255) & ~size_t(255);
+  return c;
+}
+
+// Stage 1: the ordinary forward with a placeholder candidate, then keep the candidate-free rows.
+// The visibility rule hides the target row from every other row (attention.py:49-87), so these
+// rows are bit-identical to the ones the full forward of any candidate computes.
+int cache_build(const Ctx& c, const Plan& p, const LongerBatch& user_batch, char* cache) {
+  cudaStream_t st = c.st;
+  const int D = p.D;
+  LongerBatch bt = user_batch;
+  TRY((int)cudaMemsetAsync(p.cand0, 0, sizeof(int32_t) * p.B, st));
+  bt.cand_item = p.cand0;
+  bt.label = nullptr;
+  TRY(forward(c, p, bt, p.loss_per, nullptr, 0));
+  const CacheLayout L = cache_layout(p);
+  copy_rows_bf16(p.KV, (long long)p.v * 2 * D, 2 * D, 0, reinterpret_cast<bf16*>(cache + L.xkv), L.xrows * 2 * D,
+                 (int)L.xrows, 2 * D, p.B, st);
+  for (int i = 0; i < p.N; ++i) {
+    bf16* dst = reinterpret_cast<bf16*>(cache + L.skv) + (size_t)i * p.B * L.srows * 2 * D;
+    copy_rows_bf16(p.sb[i].qkv, (long long)p.q * 3 * D, 3 * D, D, dst, L.srows * 2 * D, (int)L.srows, 2 * D, p.B,
+                   st);
+  }
+  CacheUserArgs u{};
+  u.x_last = p.N ? p.sb[p.N - 1].out : p.cb.out;
+  u.U = p.B; u.q = p.q; u.k = p.k; u.D = D; u.d = p.d;
+  u.uid = user_batch.uid; u.profile = user_batch.profile; u.npg = p.npg;
+  u.uid_tab = c.w(p.po.uid); u.prof_tab = c.w(p.po.prof);
+  u.cls = reinterpret_cast<float*>(cache + L.cls);
+  u.ud = reinterpret_cast<float*>(cache + L.ud);
+  u.npg_out = reinterpret_cast<int32_t*>(cache + L.npg);
+  cache_users(u, st);
+  TRY((int)cudaGetLastError());
+  return 0;
+}
+
+struct ScorePlan {
+  Plan p;                      // dims (batch = users), packed weights, status
+  int C;
+  long long R;                 // users x candidates target rows
+  bf16 *raw_bf, *gg, *qn, *qkv, *ctx, *x1n, *gf;
+  float *x, *y, *m1, *r1, *x1, *m2, *r2;
+  size_t bytes;
+};
+
+ScorePlan make_score_plan(const LongerDims& d, int C, void* ws) {
+  ScorePlan s{};
+  plan_dims(s.p, d, ws);
+  Bump a{reinterpret_cast<char*>(ws)};
+  s.p.status = a.take<int>(64);
+  take_packed(s.p, a);
+  s.C = C;
+  s.R = (long long)d.batch * C;
+  const long long R = s.R;
+  const int D = s.p.D;
+  s.raw_bf = a.take<bf16>(R * D); s.gg = a.take<bf16>(R * 2 * D);
+  s.x = a.take<float>(R * D); s.y = a.take<float>(R * D);
+  s.qn = a.take<bf16>(R * D); s.m1 = a.take<float>(R); s.r1 = a.take<float>(R);
+  s.qkv = a.take<bf16>(R * 3 * D); s.ctx = a.take<bf16>(R * D);
+  s.x1 = a.take<float>(R * D); s.x1n = a.take<bf16>(R * D); s.m2 = a.take<float>(R); s.r2 = a.take<float>(R);
+  s.gf = a.take<bf16>(R * 4 * D);
+  s.bytes = a.off + 256;
+  return s;
+}
+
+// Y[rows, out] (bf16, row stride ldy) = X·W + bias
+int lin_fwd_ld(cudaStream_t st, const bf16* X, int ldx, long long rows, const bf16* W, int in, int out,
+               const float* bias, bf16* Y, int ldy) {
+  GemmArgs g = G_(X, ldx, 0, W, out, 1, rows, out, in);
+  g.flags = EPI_BIAS | EPI_OUT_BF16;
+  g.bias = bias; g.C_bf16 = Y; g.ldc_bf = ldy;
+  return gemm_launch(g, st);
+}
+
+// attention_block_cached (attention.py:215-236) for all R target rows: x → out.
+int serve_block(const Ctx& c, const ScorePlan& s, const BlockOff& bo, const float* x, float* out, bool cross,
+                const bf16* kv, int nk, int ns, int goff, const int32_t* npg, const bf16* Wqkv, const float* bqkv,
+                const bf16* Wo, const bf16* W1, const bf16* W2) {
+  const Plan& p = s.p;
+  cudaStream_t st = c.st;
+  const int D = p.D;
+  const long long R = s.R;
+  layernorm_fwd(rows_plain(x, D, R), D, c.w(bo.ln1_g), c.w(bo.ln1_b), s.qn, s.m1, s.r1, st);
+  if (cross) {   // cross weights are packed as W_q and [W_k | W_v]
+    TRY(lin_fwd_ld(st, s.qn, D, R, p.pk.c_wq, D, D, c.w(bo.b_q), s.qkv, 3 * D));
+    TRY(lin_fwd_ld(st, s.qn, D, R, p.pk.c_wkv, D, 2 * D, p.pk.c_bkv, s.qkv + D, 3 * D));
+  } else {
+    TRY(lin_fwd_ld(st, s.qn, D, R, Wqkv, D, 3 * D, bqkv, s.qkv, 3 * D));
+  }
+  ServeAttnArgs a{};
+  a.Q = s.qkv; a.ldq = 3 * D;
+  a.Kown = s.qkv + D; a.Vown = s.qkv + 2 * D; a.ldown = 3 * D;
+  a.K = kv; a.ldk = 2 * D; a.sk = (long long)nk * 2 * D;
+  a.V = kv + D; a.ldv = 2 * D; a.sv = a.sk;
+  a.U = p.B; a.C = s.C; a.nk = nk; a.ns = ns; a.goff = goff; a.D = D; a.heads = p.heads; a.npg = npg;
+  a.ctx = s.ctx; a.ldc = D;
+  TRY(serve_attn(a, st));
+  TRY(lin_fwd(st, s.ctx, D, R, Wo, D, D, c.w(bo.b_o), 0, s.x1, nullptr, nullptr, x, D));
+  layernorm_fwd(rows_plain(s.x1, D, R), D, c.w(bo.ln2_g), c.w(bo.ln2_b), s.x1n, s.m2, s.r2, st);
+  TRY(lin_fwd(st, s.x1n, D, R, W1, D, 4 * D, c.w(bo.b1), EPI_GELU, nullptr, s.gf, nullptr));
+  TRY(lin_fwd(st, s.gf, 4 * D, R, W2, 4 * D, D, c.w(bo.b2), 0, out, nullptr, nullptr, s.x1, D));
+  return 0;
+}
+
+// Stage 2: candidates → target global rows → cross + N self blocks against the cache → head.
+int cache_score(const Ctx& c, const ScorePlan& s, const char* cache, const int32_t* cand, float* probs) {
+  const Plan& p = s.p;
+  cudaStream_t st = c.st;
+  const ParamOff& o = p.po;
+  const LongerDims& dm = p.dims;
+  const int D = p.D;
+  const long long R = s.R;
+  const CacheLayout L = cache_layout(p);
+  TRY(pack_weights(p, c.P, p.ws, st));
+  TargetArgs t{};
+  t.cand = cand; t.R = R; t.d = p.d; t.D = D; t.d_item = dm.d_item; t.d_act = dm.d_act; t.d_time = dm.d_time;
+  t.vocab = dm.vocab; t.item_tab = c.w(o.item); t.time_tab = c.w(o.time); t.tok_w = c.w(o.tok_w);
+  t.tok_b = c.w(o.tok_b); t.lift_w = c.w(o.lift_w); t.lift_b = c.w(o.lift_b); t.raw_bf = s.raw_bf;
+  t.status = p.status;
+  target_rows(t, st);
+  TRY(lin_fwd(st, s.raw_bf, D, R, p.pk.glob_w1, D, 2 * D, c.w(o.glob_b1), EPI_GELU, nullptr, s.gg, nullptr));
+  TRY(lin_fwd(st, s.gg, 2 * D, R, p.pk.glob_w2, 2 * D, D, c.w(o.glob_b2), 0, s.x, nullptr, nullptr));
+  const int32_t* npg = reinterpret_cast<const int32_t*>(cache + L.npg);
+  float* x = s.x;
+  float* y = s.y;
+  TRY(serve_block(c, s, o.cross, x, y, true, reinterpret_cast<const bf16*>(cache + L.xkv), (int)L.xrows, p.G, 0, npg,
+                  nullptr, nullptr, p.pk.c_wo, p.pk.c_w1, p.pk.c_w2));
+  std::swap(x, y);
+  for (int i = 0; i < p.N; ++i) {
+    const bf16* kv = reinterpret_cast<const bf16*>(cache + L.skv) + (size_t)i * p.B * L.srows * 2 * D;
+    TRY(serve_block(c, s, o.self_[i], x, y, false, kv, (int)L.srows, p.k, p.G - p.k, npg, p.pk.s_wqkv[i],
+                    p.pk.s_bqkv[i], p.pk.s_wo[i], p.pk.s_w1[i], p.pk.s_w2[i]));
+    std::swap(x, y);
+  }
+  ServeHeadArgs h{};
+  h.x = x; h.R = R; h.C = s.C; h.D = D; h.d = p.d; h.hh = p.hh;
+  h.cls = reinterpret_cast<const float*>(cache + L.cls);
+  h.ud = reinterpret_cast<const float*>(cache + L.ud);
+  h.w1 = c.w(o.head_w1); h.b1 = c.w(o.head_b1); h.w2 = c.w(o.head_w2); h.b2 = c.w(o.head_b2);
+  h.probs = probs;
+  serve_head(h, st);
+  TRY((int)cudaGetLastError());
+  return 0;
+}
+
 }  // namespace
 }  // namespace longer
 
@@ -873,6 +1054,54 @@ extern "C" int longer_read_status(void* ws, int32_t* flags, void* stream) {
 }
 
 extern "C" const char* longer_last_error(void) { return g_err.c_str(); }
+
+extern "C" int longer_cache_bytes(const LongerDims* dims, size_t* bytes) {
+  if (!dims || !bytes) return fail(LONGER_EDIM, "null argument");
+  int rc = validate(*dims);
+  if (rc) return rc;
+  Plan p{};
+  plan_dims(p, *dims, nullptr);
+  *bytes = cache_layout(p).bytes;
+  return 0;
+}
+
+extern "C" int longer_cache_build(const LongerDims* dims, const float* params, const LongerBatch* batch, void* ws,
+                                  size_t ws_bytes, void* cache, size_t cache_bytes, void* stream) {
+  static Plan p;
+  int rc = check_call(dims, ws_bytes, &p, ws);
+  if (rc) return rc;
+  if (!batch || !cache) return fail(LONGER_EDIM, "null batch or cache");
+  if (cache_bytes < cache_layout(p).bytes) return fail(LONGER_EDIM, "cache buffer too small");
+  p.fused_fe = use_fused(p);
+  Ctx c{p, params, nullptr, (cudaStream_t)stream};
+  return cache_build(c, p, *batch, reinterpret_cast<char*>(cache));
+}
+
+extern "C" int longer_score_workspace_bytes(const LongerDims* dims, int32_t candidates_per_user, size_t* bytes) {
+  if (!dims || !bytes) return fail(LONGER_EDIM, "null argument");
+  int rc = validate(*dims);
+  if (rc) return rc;
+  if (candidates_per_user < 1) return fail(LONGER_EDIM, "candidates_per_user must be >= 1");
+  *bytes = make_score_plan(*dims, candidates_per_user, nullptr).bytes;
+  return 0;
+}
+
+extern "C" int longer_cache_score(const LongerDims* dims, const float* params, const void* cache, size_t cache_bytes,
+                                  const int32_t* cand_items, int32_t candidates_per_user, void* ws, size_t ws_bytes,
+                                  float* probs, void* stream) {
+  if (!dims || !cache || !cand_items || !probs) return fail(LONGER_EDIM, "null argument");
+  int rc = validate(*dims);
+  if (rc) return rc;
+  if (candidates_per_user < 1) return fail(LONGER_EDIM, "candidates_per_user must be >= 1");
+  static ScorePlan s;
+  s = make_score_plan(*dims, candidates_per_user, ws);
+  if (ws_bytes < s.bytes) return fail(LONGER_EDIM, "workspace too small");
+  if (reinterpret_cast<uintptr_t>(ws) & 255) return fail(LONGER_EDIM, "workspace must be 256-byte aligned");
+  if (cache_bytes != cache_layout(s.p).bytes)
+    return fail(LONGER_ESTALE, "cache was built for different dimensions (rebuild it)");
+  Ctx c{s.p, params, nullptr, (cudaStream_t)stream};
+  return cache_score(c, s, reinterpret_cast<const char*>(cache), cand_items, probs);
+}
 
 extern "C" int longer_set_probe(int32_t phase, void* ev_begin, void* ev_end) {
   if (phase < 0 || phase >= PH_N) return fail(LONGER_EDIM, "unknown probe phase");

@@ -11,7 +11,8 @@ from oracle import longer_oracle as O
 from paper_2505_04421_b200.config import ModelConfig
 from paper_2505_04421_b200.params import init_params, param_shapes
 
-GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+GOLDEN = sorted(p for p in glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz"))
+                if not os.path.basename(p).startswith("serving_"))
 
 
 def load_golden(path):
