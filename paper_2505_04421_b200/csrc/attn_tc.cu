@@ -36,6 +36,8 @@ __device__ __forceinline__ void load_rows_bf16(bf16* tile, const bf16* src, int 
 
 template <int DH>
 __global__ void __launch_bounds__(kThreads, 1) xattn_fwd_kernel(AttnArgs a) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   bf16* sQ = reinterpret_cast<bf16*>(smem_raw);
   bf16* sK = sQ + 128 * DH;
@@ -166,6 +168,8 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_fwd_kernel(AttnArgs a) {
 
 template <int DH>
 __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   bf16* sQ = reinterpret_cast<bf16*>(smem_raw);
   bf16* sdO = sQ + 128 * DH;
@@ -333,7 +337,7 @@ int launch_fwd(const AttnArgs& a, cudaStream_t st) {
   const int smem = (128 * DH + 2 * kC * DH + 128 * kC) * 2 + 64;
   static int done = 0;
   if (!done) { cudaFuncSetAttribute(xattn_fwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); done = 1; }
-  xattn_fwd_kernel<DH><<<a.B * a.heads, kThreads, std::max(smem, 116 * 1024), st>>>(a);
+  launch(xattn_fwd_kernel<DH>, a.B * a.heads, kThreads, std::max(smem, 116 * 1024), st, a);
   return (int)cudaGetLastError();
 }
 
@@ -342,7 +346,7 @@ int launch_bwd(const AttnArgs& a, cudaStream_t st) {
   const int smem = (2 * 128 * DH + 2 * kC * DH + 2 * 128 * kC) * 2 + 64;
   static int done = 0;
   if (!done) { cudaFuncSetAttribute(xattn_bwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); done = 1; }
-  xattn_bwd_kernel<DH><<<a.B * a.heads, kThreads, std::max(smem, 116 * 1024), st>>>(a);
+  launch(xattn_bwd_kernel<DH>, a.B * a.heads, kThreads, std::max(smem, 116 * 1024), st, a);
   return (int)cudaGetLastError();
 }
 

@@ -4,9 +4,47 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+#include <utility>
+
 namespace longer {
 
 typedef __nv_bfloat16 bf16;
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every kernel of the library is launched with programmatic stream serialisation: the next kernel
+// of the step may be scheduled while this one drains, runs its prologue (barrier init, TMEM
+// allocation, tensor-map prefetch), then blocks in pdl_wait() until its predecessor has finished
+// and its writes are visible.  Rules that keep this safe: pdl_wait() precedes every global-memory
+// access of a kernel; kernels that allocate TMEM call pdl_trigger() only after their allocation (a
+// waiting dependent never holds TMEM that a not-yet-allocated predecessor CTA needs).
+// LONGER_PDL=0 disables the attribute (plain stream order).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("LONGER_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v != 0;
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 constexpr float kGeluC = 0.7978845608028654f;  // sqrt(2/pi)   (pkg/src/longrec/tensors.py:36)
 constexpr float kGeluA = 0.044715f;            //              (pkg/src/longrec/tensors.py:37)

@@ -29,6 +29,8 @@ struct PackW {
 // trans = 1: image of Wᵀ ([out][in]: element (n=j, k=i) = W[i][j]); trans = 0: image of W as
 // [in][out] (element (n=i, k=j) = W[i][j]).  W is the fp32 master [in, out] row-major.
 __global__ void pack_canon_kernel(const float* __restrict__ params, PackW pw, bf16* blob) {
+  pdl_trigger();
+  pdl_wait();
   const auto s = pw.s[blockIdx.y];
   const int n_el = s.in * s.out;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n_el; e += gridDim.x * blockDim.x) {
@@ -120,6 +122,8 @@ __device__ __forceinline__ void load_blob(uint8_t* dst_smem, const uint8_t* src,
 // ------------------------------------------------------------------ forward kernel
 template <int DT, int KG>
 __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   constexpr int D = DT * KG;
   constexpr int H2 = 2 * D;                        // token-MLP hidden width
@@ -362,6 +366,8 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
 // the abs-pos rows are loaded once and their gradient accumulates in shared memory.
 template <int DT>
 __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   const int Dm = DT * a.K;
   const int H2 = 2 * Dm;
@@ -693,7 +699,7 @@ void pack_frontend_weights(const float* params, long long tok_w, long long seq_w
     add(w1, d, 4 * d, 0, 0, 0, 4 * d, o.w1i_n[l]);
     add(w2, 4 * d, d, 0, 0, 0, d, o.w2i_n[l]);
   }
-  pack_canon_kernel<<<dim3(16, pw.n), 256, 0, st>>>(params, pw, blob);
+  launch(pack_canon_kernel, dim3(16, pw.n), 256, 0, st, params, pw, blob);
 }
 
 template <int DT, int KG>
@@ -708,7 +714,7 @@ static int launch_fwd(const FrontArgs& a, cudaStream_t st) {
   const long long ntiles = (a.T + kTile - 1) / kTile;
   const int per_sm = smem <= 113 * 1024 ? 2 : 1;
   const int grid = (int)std::min<long long>(ntiles, per_sm * 148);
-  fe_fwd_kernel<DT, KG><<<grid, kThreads, smem, st>>>(a);
+  launch(fe_fwd_kernel<DT, KG>, grid, kThreads, smem, st, a);
   return (int)cudaGetLastError();
 }
 
@@ -741,7 +747,7 @@ static int launch_mlp_bwd(const FrontArgs& a, cudaStream_t st) {
   const int tps = (a.Lp + kTile - 1) / kTile;
   const int r = std::max(1, std::min(a.B, 148 / tps));
   // > 113 KB of smem keeps one CTA per SM (the kernel allocates all 512 TMEM columns)
-  fe_mlp_bwd_kernel<DT><<<tps * r, kThreads8, std::max(smem, 116 * 1024), st>>>(a);
+  launch(fe_mlp_bwd_kernel<DT>, tps * r, kThreads8, std::max(smem, 116 * 1024), st, a);
   return (int)cudaGetLastError();
 }
 

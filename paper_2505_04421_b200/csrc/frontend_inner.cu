@@ -19,6 +19,8 @@ namespace {
 
 template <int DT, int KG>
 __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   constexpr int XK = DT + 16;                 // activation rows carrying a ones column
   constexpr int F4 = 4 * DT;
@@ -396,7 +398,7 @@ int launch_inner_bwd(const FrontArgs& a, cudaStream_t st) {
   }
   const long long ntiles = (a.T + kTile - 1) / kTile;
   const int grid = (int)std::min<long long>(ntiles, 148);
-  fe_inner_bwd_kernel<DT, KG><<<grid, kThreads, std::max(smem, 116 * 1024), st>>>(a);
+  launch(fe_inner_bwd_kernel<DT, KG>, grid, kThreads, std::max(smem, 116 * 1024), st, a);
   return (int)cudaGetLastError();
 }
 

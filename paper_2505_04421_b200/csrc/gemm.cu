@@ -31,6 +31,8 @@ template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
             GemmArgs g, int kb_per_split) {
+  pdl_trigger();
+  pdl_wait();
   using S = Smem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -229,7 +231,7 @@ int launch_cfg(const GemmArgs& g, const CUtensorMap& tA, const CUtensorMap& tB, 
     cudaFuncSetAttribute(gemm_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr_set = true;
   }
-  gemm_kernel<BN, STAGES><<<grid, kThreads, smem, st>>>(tA, tB, g, kb_per);
+  launch(gemm_kernel<BN, STAGES>, grid, kThreads, smem, st, tA, tB, g, kb_per);
   return (int)cudaGetLastError();
 }
 

@@ -2,6 +2,7 @@
 // layer norms, bias/column reductions, grouped + hybrid attention, global tokens, head + BCE,
 // parameter packing and Adam.  Each kernel cites the reference function it restates.
 #include "ops.cuh"
+#include "sm100.cuh"
 
 #include <math.h>
 #include <algorithm>
@@ -16,6 +17,8 @@ inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 // _event_features + abs-pos add (pkg/src/longrec/inputs.py:434-444, :474-476) and the pad
 // bookkeeping of encode_events / merge (inputs.py:457-482, merge.py:45-62). One thread/token.
 __global__ void embed_fwd_kernel(EmbedArgs a) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float sw[];                    // tok_w [F*d] + tok_b [d]
   const int F = a.d_item + a.d_act + a.d_time;
   for (int i = threadIdx.x; i < F * a.d + a.d; i += blockDim.x)
@@ -65,12 +68,14 @@ void embed_fwd(const EmbedArgs& a, cudaStream_t st) {
   const long long T = (long long)a.B * a.Lp;
   const int F = a.d_item + a.d_act + a.d_time;
   const int smem = (F * a.d + a.d) * 4;
-  embed_fwd_kernel<<<cdiv(T, 256), 256, smem, st>>>(a);
+  launch(embed_fwd_kernel, cdiv(T, 256), 256, smem, st, a);
 }
 
 // Backward of the featuriser: dfeat = dx0·W_tpᵀ scattered into the item/action/time tables with
 // shared-memory privatised accumulators (gather_rows bw = np.add.at, tensors.py:505-510).
 __global__ void embed_bwd_kernel(EmbedBwdArgs a, int tokens_per_block, int item_in_smem) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float sm[];
   const int F = a.d_item + a.d_act + a.d_time;
   float* s_w = sm;                                   // F*d
@@ -120,6 +125,8 @@ __global__ void embed_bwd_kernel(EmbedBwdArgs a, int tokens_per_block, int item_
 // abs_pos_table gradient: row r collects dx0 of the token with recency r of every sample —
 // a deterministic strided column reduction instead of scatter atomics.
 __global__ void pos_grad_kernel(EmbedBwdArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;                     // recency row
   for (int c = threadIdx.x; c < a.d; c += blockDim.x) {
     float acc = 0.f;
@@ -139,14 +146,42 @@ void embed_bwd(const EmbedBwdArgs& a, cudaStream_t st) {
   const int tpb = 4096;
   static int attr_done = 0;
   if (!attr_done) { cudaFuncSetAttribute(embed_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024); attr_done = 1; }
-  embed_bwd_kernel<<<cdiv(T, tpb), 256, smem, st>>>(a, tpb, item_in_smem);
-  pos_grad_kernel<<<a.L, 32 * cdiv(a.d, 32), 0, st>>>(a);
+  launch(embed_bwd_kernel, cdiv(T, tpb), 256, smem, st, a, tpb, item_in_smem);
+  launch(pos_grad_kernel, a.L, 32 * cdiv(a.d, 32), 0, st, a);
 }
 
 // ============================================================== layer norm
-template <int VPT>
+// One warp per row.  Contiguous mode (W == 32·VPT, aligned rows): lane owns columns
+// [lane·VPT, lane·VPT + VPT) and moves them with one 8/16/32-byte access; otherwise strided.
+template <int VPT, bool CONTIG>
+__device__ __forceinline__ int ln_col(int lane, int u) { return CONTIG ? lane * VPT + u : lane + 32 * u; }
+
+template <int VPT, bool CONTIG>
+__device__ __forceinline__ void ln_load(const float* __restrict__ p, int lane, int W, float* v) {
+  if constexpr (CONTIG && VPT == 8) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p + lane * 8));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(p + lane * 8 + 4));
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else if constexpr (CONTIG && VPT == 4) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p + lane * 4));
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  } else if constexpr (CONTIG && VPT == 2) {
+    const float2 a = __ldg(reinterpret_cast<const float2*>(p + lane * 2));
+    v[0] = a.x; v[1] = a.y;
+  } else {
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) {
+      const int c = ln_col<VPT, CONTIG>(lane, u);
+      v[u] = c < W ? p[c] : 0.f;
+    }
+  }
+}
+
+template <int VPT, bool CONTIG>
 __global__ void ln_fwd_kernel(RowMap x, int W, const float* __restrict__ g, const float* __restrict__ bta,
                               bf16* y, float* mean, float* rstd) {
+  pdl_trigger();
+  pdl_wait();
   const int warps = blockDim.x / 32;
   const int row = blockIdx.x * warps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
@@ -156,54 +191,88 @@ __global__ void ln_fwd_kernel(RowMap x, int W, const float* __restrict__ g, cons
   const float* src = j < x.na ? x.A + (long long)(b * x.a_rows + x.a_off + j) * x.lda
                               : x.Bsrc + (long long)(b * x.nb + j - x.na) * x.ldb;
   float v[VPT];
+  ln_load<VPT, CONTIG>(src, lane, W, v);
   float s = 0.f;
 #pragma unroll
-  for (int u = 0; u < VPT; ++u) {
-    const int c = lane + 32 * u;
-    v[u] = c < W ? src[c] : 0.f;
-    s += v[u];
-  }
+  for (int u = 0; u < VPT; ++u) s += v[u];
   const float mu = warp_sum(s) / W;
   float q = 0.f;
 #pragma unroll
   for (int u = 0; u < VPT; ++u) {
-    const int c = lane + 32 * u;
+    const int c = ln_col<VPT, CONTIG>(lane, u);
     const float dv = c < W ? v[u] - mu : 0.f;
     q += dv * dv;
   }
   const float var = warp_sum(q) / W;
   const float inv = rsqrtf(var + kLnEps);
+  bf16* dst = y + (long long)row * W;
+  if constexpr (CONTIG && VPT >= 2) {
+    float gg[VPT], bb[VPT];
 #pragma unroll
-  for (int u = 0; u < VPT; ++u) {
-    const int c = lane + 32 * u;
-    if (c < W) y[(long long)row * W + c] = __float2bfloat16((v[u] - mu) * inv * g[c] + bta[c]);
+    for (int u = 0; u < VPT; ++u) { gg[u] = g[lane * VPT + u]; bb[u] = bta[lane * VPT + u]; }
+    uint32_t w[VPT / 2];
+#pragma unroll
+    for (int u = 0; u < VPT; u += 2)
+      w[u / 2] = sm100::pack_bf16((v[u] - mu) * inv * gg[u] + bb[u], (v[u + 1] - mu) * inv * gg[u + 1] + bb[u + 1]);
+    if constexpr (VPT == 8) *reinterpret_cast<uint4*>(dst + lane * 8) = make_uint4(w[0], w[1], w[2], w[3]);
+    else if constexpr (VPT == 4) *reinterpret_cast<uint2*>(dst + lane * 4) = make_uint2(w[0], w[1]);
+    else *reinterpret_cast<uint32_t*>(dst + lane * 2) = w[0];
+  } else {
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) {
+      const int c = ln_col<VPT, CONTIG>(lane, u);
+      if (c < W) dst[c] = __float2bfloat16((v[u] - mu) * inv * g[c] + bta[c]);
+    }
   }
   if (lane == 0) { mean[row] = mu; rstd[row] = inv; }
 }
 
+namespace {
+bool ln_contig(int W, int vpt, const void* p0, int ld0, const void* p1, int ld1) {
+  if (W != 32 * vpt || vpt == 1) return false;
+  auto al = [&](const void* p, int ld) {
+    return !p || ((reinterpret_cast<uintptr_t>(p) % (4 * vpt)) == 0 && ld % vpt == 0);
+  };
+  return al(p0, ld0) && al(p1, ld1);
+}
+}  // namespace
+
 void layernorm_fwd(const RowMap& x, int W, const float* g, const float* b, bf16* y, float* mean, float* rstd,
                    cudaStream_t st) {
   const int rows = x.rows();
+  if (rows <= 0) return;
   const int grid = cdiv(rows, 8);
-  if (W <= 32) ln_fwd_kernel<1><<<grid, 256, 0, st>>>(x, W, g, b, y, mean, rstd);
-  else if (W <= 64) ln_fwd_kernel<2><<<grid, 256, 0, st>>>(x, W, g, b, y, mean, rstd);
-  else if (W <= 128) ln_fwd_kernel<4><<<grid, 256, 0, st>>>(x, W, g, b, y, mean, rstd);
-  else ln_fwd_kernel<8><<<grid, 256, 0, st>>>(x, W, g, b, y, mean, rstd);
+  const int vpt = W <= 32 ? 1 : W <= 64 ? 2 : W <= 128 ? 4 : 8;
+  const bool ct = ln_contig(W, vpt, x.A, x.lda, x.nb ? x.Bsrc : nullptr, x.ldb);
+#define LNF(V) (ct ? launch(ln_fwd_kernel<V, true>, grid, 256, 0, st, x, W, g, b, y, mean, rstd) \
+                   : launch(ln_fwd_kernel<V, false>, grid, 256, 0, st, x, W, g, b, y, mean, rstd))
+  if (vpt == 1) launch(ln_fwd_kernel<1, false>, grid, 256, 0, st, x, W, g, b, y, mean, rstd);
+  else if (vpt == 2) LNF(2);
+  else if (vpt == 4) LNF(4);
+  else LNF(8);
+#undef LNF
 }
 
 // LN backward (pkg/src/longrec/tensors.py:368-378): dx = (ĝ − mean ĝ − x̂·mean(ĝx̂))·σ⁻¹, ĝ = dy·g
-template <int VPT>
+template <int VPT, bool CONTIG>
 __global__ void ln_bwd_kernel(RowMap x, int W, const float* __restrict__ g, const float* __restrict__ mean,
                               const float* __restrict__ rstd, const float* __restrict__ dy, int ldy, RowMapW out,
                               int accumulate, const float* rowmask, float* dgain, float* dbias) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float sg[8][VPT * 32], sb[8][VPT * 32];
   const int warps = blockDim.x / 32;
   const int wid = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int rows = x.rows();
   const int per = x.na + x.nb;
-  float pg[VPT], pb[VPT];
+  float pg[VPT], pb[VPT], gv[VPT];
 #pragma unroll
   for (int u = 0; u < VPT; ++u) { pg[u] = 0.f; pb[u] = 0.f; }
+#pragma unroll
+  for (int u = 0; u < VPT; ++u) {
+    const int c = ln_col<VPT, CONTIG>(lane, u);
+    gv[u] = c < W ? g[c] : 0.f;
+  }
   for (int row = blockIdx.x * warps + wid; row < rows; row += gridDim.x * warps) {
     const int b = row / per, j = row % per;
     const float* src = j < x.na ? x.A + (long long)(b * x.a_rows + x.a_off + j) * x.lda
@@ -211,17 +280,18 @@ __global__ void ln_bwd_kernel(RowMap x, int W, const float* __restrict__ g, cons
     float* dst = j < out.na ? out.A + (long long)(b * out.a_rows + out.a_off + j) * out.lda
                             : out.Bsrc + (long long)(b * out.nb + j - out.na) * out.ldb;
     const float mu = mean[row], inv = rstd[row];
-    float xh[VPT], gh[VPT];
+    float xh[VPT], gh[VPT], dyv[VPT];
+    ln_load<VPT, CONTIG>(src, lane, W, xh);
+    ln_load<VPT, CONTIG>(dy + (long long)row * ldy, lane, W, dyv);
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int u = 0; u < VPT; ++u) {
-      const int c = lane + 32 * u;
+      const int c = ln_col<VPT, CONTIG>(lane, u);
       if (c < W) {
-        const float dyv = dy[(long long)row * ldy + c];
-        xh[u] = (src[c] - mu) * inv;
-        gh[u] = dyv * g[c];
-        pg[u] += dyv * xh[u];
-        pb[u] += dyv;
+        xh[u] = (xh[u] - mu) * inv;
+        gh[u] = dyv[u] * gv[u];
+        pg[u] += dyv[u] * xh[u];
+        pb[u] += dyv[u];
       } else {
         xh[u] = 0.f; gh[u] = 0.f;
       }
@@ -230,19 +300,35 @@ __global__ void ln_bwd_kernel(RowMap x, int W, const float* __restrict__ g, cons
     }
     const float m1 = warp_sum(s1) / W, m2 = warp_sum(s2) / W;
     const float rm = rowmask ? rowmask[row] : 1.f;
+    float o[VPT];
+    if (accumulate) ln_load<VPT, CONTIG>(dst, lane, W, o);
 #pragma unroll
     for (int u = 0; u < VPT; ++u) {
-      const int c = lane + 32 * u;
-      if (c < W) {
-        float v = (gh[u] - m1 - xh[u] * m2) * inv;
-        if (accumulate) v += dst[c];
-        dst[c] = v * rm;
+      float v = (gh[u] - m1 - xh[u] * m2) * inv;
+      if (accumulate) v += o[u];
+      o[u] = v * rm;
+    }
+    if constexpr (CONTIG && VPT == 8) {
+      reinterpret_cast<float4*>(dst + lane * 8)[0] = make_float4(o[0], o[1], o[2], o[3]);
+      reinterpret_cast<float4*>(dst + lane * 8)[1] = make_float4(o[4], o[5], o[6], o[7]);
+    } else if constexpr (CONTIG && VPT == 4) {
+      *reinterpret_cast<float4*>(dst + lane * 4) = make_float4(o[0], o[1], o[2], o[3]);
+    } else if constexpr (CONTIG && VPT == 2) {
+      *reinterpret_cast<float2*>(dst + lane * 2) = make_float2(o[0], o[1]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < VPT; ++u) {
+        const int c = ln_col<VPT, CONTIG>(lane, u);
+        if (c < W) dst[c] = o[u];
       }
     }
   }
   if (dgain) {
 #pragma unroll
-    for (int u = 0; u < VPT; ++u) { sg[wid][lane + 32 * u] = pg[u]; sb[wid][lane + 32 * u] = pb[u]; }
+    for (int u = 0; u < VPT; ++u) {
+      const int c = ln_col<VPT, CONTIG>(lane, u);
+      sg[wid][c] = pg[u]; sb[wid][c] = pb[u];
+    }
     __syncthreads();
     for (int c = threadIdx.x; c < W; c += blockDim.x) {
       float a = 0.f, bb = 0.f;
@@ -257,16 +343,26 @@ void layernorm_bwd(const RowMap& x, int W, const float* g, const float* mean, co
                    int ldy, const RowMapW& out, int accumulate, const float* rowmask, float* dgain, float* dbias,
                    cudaStream_t st) {
   const int rows = x.rows();
-  const int grid = std::min(cdiv(rows, 8), 148 * 2);
-  if (W <= 32) ln_bwd_kernel<1><<<grid, 256, 0, st>>>(x, W, g, mean, rstd, dy, ldy, out, accumulate, rowmask, dgain, dbias);
-  else if (W <= 64) ln_bwd_kernel<2><<<grid, 256, 0, st>>>(x, W, g, mean, rstd, dy, ldy, out, accumulate, rowmask, dgain, dbias);
-  else if (W <= 128) ln_bwd_kernel<4><<<grid, 256, 0, st>>>(x, W, g, mean, rstd, dy, ldy, out, accumulate, rowmask, dgain, dbias);
-  else ln_bwd_kernel<8><<<grid, 256, 0, st>>>(x, W, g, mean, rstd, dy, ldy, out, accumulate, rowmask, dgain, dbias);
+  if (rows <= 0) return;
+  const int grid = std::min(cdiv(rows, 8), 148 * 8);
+  const int vpt = W <= 32 ? 1 : W <= 64 ? 2 : W <= 128 ? 4 : 8;
+  const bool ct = ln_contig(W, vpt, x.A, x.lda, x.nb ? x.Bsrc : nullptr, x.ldb) &&
+                  ln_contig(W, vpt, out.A, out.lda, out.nb ? out.Bsrc : nullptr, out.ldb) &&
+                  ln_contig(W, vpt, dy, ldy, nullptr, 0);
+#define LNB(V) (ct ? launch(ln_bwd_kernel<V, true>, grid, 256, 0, st, x, W, g, mean, rstd, dy, ldy, out, accumulate, rowmask, dgain, dbias) \
+                   : launch(ln_bwd_kernel<V, false>, grid, 256, 0, st, x, W, g, mean, rstd, dy, ldy, out, accumulate, rowmask, dgain, dbias))
+  if (vpt == 1) launch(ln_bwd_kernel<1, false>, grid, 256, 0, st, x, W, g, mean, rstd, dy, ldy, out, accumulate, rowmask, dgain, dbias);
+  else if (vpt == 2) LNB(2);
+  else if (vpt == 4) LNB(4);
+  else LNB(8);
+#undef LNB
 }
 
 // ============================================================== reductions / copies
 template <typename T>
 __global__ void colsum_kernel(const T* __restrict__ x, int rows, int W, int ld, int rows_per_block, float* out) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float red[256];
   const int cpp = W < 256 ? W : 256;
   const int rpp = 256 / cpp;
@@ -297,16 +393,84 @@ __global__ void colsum_kernel(const T* __restrict__ x, int rows, int W, int ld, 
   }
 }
 
+// Vectorised column sums: a thread owns 8 consecutive columns (one 16/32-byte load per row),
+// W/8 threads cover a row, 256/(W/8) rows are read concurrently and each thread keeps 4 rows in
+// flight; per-block partials are reduced in shared memory, then one atomic per column per block.
+__device__ __forceinline__ void load8(const float* p, float* v) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p)), b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void load8(const bf16* p, float* v) {
+  const uint4 a = __ldg(reinterpret_cast<const uint4*>(p));
+  const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) { v[2 * i] = sm100::bf16_lo(w[i]); v[2 * i + 1] = sm100::bf16_hi(w[i]); }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) colsum8_kernel(const T* __restrict__ x, int rows, int W, int ld,
+                                                      int rows_per_block, float* out) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ float red[256 * 8];
+  const int tpr = W / 8, rpp = 256 / tpr;
+  const int tid = threadIdx.x;
+  const int cg = tid % tpr, rg = tid / tpr;
+  const int r0 = blockIdx.x * rows_per_block, r1 = min(rows, r0 + rows_per_block);
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (rg < rpp) {
+    int r = r0 + rg;
+    for (; r + 3 * rpp < r1; r += 4 * rpp) {
+      float v0[8], v1[8], v2[8], v3[8];
+      load8(x + (long long)r * ld + cg * 8, v0);
+      load8(x + (long long)(r + rpp) * ld + cg * 8, v1);
+      load8(x + (long long)(r + 2 * rpp) * ld + cg * 8, v2);
+      load8(x + (long long)(r + 3 * rpp) * ld + cg * 8, v3);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] += (v0[i] + v1[i]) + (v2[i] + v3[i]);
+    }
+    for (; r < r1; r += rpp) {
+      float v0[8];
+      load8(x + (long long)r * ld + cg * 8, v0);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] += v0[i];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) red[tid * 8 + i] = acc[i];     // = red[rg][cg*8+i] (row-group major)
+  __syncthreads();
+  for (int c = tid; c < W; c += 256) {
+    float s = 0.f;
+    for (int q = 0; q < rpp; ++q) s += red[q * W + c];
+    atomicAdd(&out[c], s);
+  }
+}
+
+template <typename T>
+void colsum_launch(const T* x, int rows, int W, int ld, float* out, cudaStream_t st) {
+  if (rows <= 0) return;
+  const bool vec = W % 8 == 0 && W <= 2048 && 256 % (W / 8) == 0 && ld % 8 == 0 &&
+                   (reinterpret_cast<uintptr_t>(x) % 16) == 0;
+  if (vec) {
+    const int rpp = 256 / (W / 8);
+    const int rpb = std::max(rpp * 8, cdiv(rows, 148 * 8) / rpp * rpp);
+    launch(colsum8_kernel<T>, cdiv(rows, rpb), 256, 0, st, x, rows, W, ld, rpb, out);
+  } else {
+    const int rpb = std::max(64, cdiv(rows, 148 * 2));
+    launch(colsum_kernel<T>, cdiv(rows, rpb), 256, 0, st, x, rows, W, ld, rpb, out);
+  }
+}
+
 void colsum_f32(const float* x, int rows, int W, int ld, float* out, cudaStream_t st) {
-  const int rpb = std::max(64, cdiv(rows, 148 * 2));
-  colsum_kernel<float><<<cdiv(rows, rpb), 256, 0, st>>>(x, rows, W, ld, rpb, out);
+  colsum_launch<float>(x, rows, W, ld, out, st);
 }
 void colsum_bf16(const bf16* x, int rows, int W, int ld, float* out, cudaStream_t st) {
-  const int rpb = std::max(64, cdiv(rows, 148 * 2));
-  colsum_kernel<bf16><<<cdiv(rows, rpb), 256, 0, st>>>(x, rows, W, ld, rpb, out);
+  colsum_launch<bf16>(x, rows, W, ld, out, st);
 }
 
 __global__ void cast_rows_kernel(const float* x, int rows, int W, int ldx, bf16* y, int ldy, const float* rowmask) {
+  pdl_trigger();
+  pdl_wait();
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (long long)rows * W) return;
   const int r = (int)(i / W), c = (int)(i % W);
@@ -316,22 +480,26 @@ __global__ void cast_rows_kernel(const float* x, int rows, int W, int ldx, bf16*
 }
 void cast_rows_bf16(const float* x, int rows, int W, int ldx, bf16* y, int ldy, const float* rowmask, cudaStream_t st) {
   const long long n = (long long)rows * W;
-  if (n) cast_rows_kernel<<<cdiv(n, 256), 256, 0, st>>>(x, rows, W, ldx, y, ldy, rowmask);
+  if (n) launch(cast_rows_kernel, cdiv(n, 256), 256, 0, st, x, rows, W, ldx, y, ldy, rowmask);
 }
 
 __global__ void mul_rows_kernel(float* x, int rows, int W, const float* rowmask) {
+  pdl_trigger();
+  pdl_wait();
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (long long)rows * W) return;
   x[i] *= rowmask[i / W];
 }
 void mul_rows_inplace(float* x, int rows, int W, const float* rowmask, cudaStream_t st) {
   const long long n = (long long)rows * W;
-  if (n) mul_rows_kernel<<<cdiv(n, 256), 256, 0, st>>>(x, rows, W, rowmask);
+  if (n) launch(mul_rows_kernel, cdiv(n, 256), 256, 0, st, x, rows, W, rowmask);
 }
 
 template <int ADD>
 __global__ void move_rows_kernel(const float* src, int batch, int src_rows, int src_off, int n, float* dst,
                                  int dst_rows, int dst_off, int W) {
+  pdl_trigger();
+  pdl_wait();
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (long long)batch * n * W) return;
   const int c = (int)(i % W);
@@ -344,12 +512,12 @@ __global__ void move_rows_kernel(const float* src, int batch, int src_rows, int 
 void gather_rows_f32(const float* src, int batch, int src_rows, int src_off, int n, float* dst, int dst_rows,
                      int dst_off, int W, cudaStream_t st) {
   const long long tot = (long long)batch * n * W;
-  if (tot) move_rows_kernel<0><<<cdiv(tot, 256), 256, 0, st>>>(src, batch, src_rows, src_off, n, dst, dst_rows, dst_off, W);
+  if (tot) launch(move_rows_kernel<0>, cdiv(tot, 256), 256, 0, st, src, batch, src_rows, src_off, n, dst, dst_rows, dst_off, W);
 }
 void add_rows_f32(const float* src, int batch, int src_rows, int src_off, int n, float* dst, int dst_rows,
                   int dst_off, int W, cudaStream_t st) {
   const long long tot = (long long)batch * n * W;
-  if (tot) move_rows_kernel<1><<<cdiv(tot, 256), 256, 0, st>>>(src, batch, src_rows, src_off, n, dst, dst_rows, dst_off, W);
+  if (tot) launch(move_rows_kernel<1>, cdiv(tot, 256), 256, 0, st, src, batch, src_rows, src_off, n, dst, dst_rows, dst_off, W);
 }
 
 // ============================================================== grouped attention (InnerTrans)
@@ -359,6 +527,8 @@ void add_rows_f32(const float* src, int batch, int src_rows, int src_off, int n,
 // shared memory with coalesced stores.
 template <int KT>
 __global__ void group_attn_fwd_kernel(const float* __restrict__ qkv, int T, int Kr, int w, bf16* ctx, float* probs) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float sm[];
   const int K = KT > 0 ? KT : Kr;
   const int TT = (blockDim.x / K) * K;                   // tokens per tile (whole groups)
@@ -406,6 +576,8 @@ __global__ void group_attn_fwd_kernel(const float* __restrict__ qkv, int T, int 
 template <int KT>
 __global__ void group_attn_bwd_kernel(const float* __restrict__ qkv, const float* __restrict__ probs,
                                       const float* __restrict__ dctx, int T, int Kr, int w, bf16* dqkv) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float sm[];
   const int K = KT > 0 ? KT : Kr;
   const int TT = (blockDim.x / K) * K;
@@ -475,10 +647,10 @@ void group_attn_fwd(const float* qkv, int T, int K, int w, bf16* ctx, float* pro
     done = 1;
   }
   const int grid = cdiv(T, TT);
-  if (K == 2) group_attn_fwd_kernel<2><<<grid, 128, smem, st>>>(qkv, T, K, w, ctx, probs);
-  else if (K == 4) group_attn_fwd_kernel<4><<<grid, 128, smem, st>>>(qkv, T, K, w, ctx, probs);
-  else if (K == 8) group_attn_fwd_kernel<8><<<grid, 128, smem, st>>>(qkv, T, K, w, ctx, probs);
-  else group_attn_fwd_kernel<0><<<grid, 128, smem, st>>>(qkv, T, K, w, ctx, probs);
+  if (K == 2) launch(group_attn_fwd_kernel<2>, grid, 128, smem, st, qkv, T, K, w, ctx, probs);
+  else if (K == 4) launch(group_attn_fwd_kernel<4>, grid, 128, smem, st, qkv, T, K, w, ctx, probs);
+  else if (K == 8) launch(group_attn_fwd_kernel<8>, grid, 128, smem, st, qkv, T, K, w, ctx, probs);
+  else launch(group_attn_fwd_kernel<0>, grid, 128, smem, st, qkv, T, K, w, ctx, probs);
 }
 void group_attn_bwd(const float* qkv, const float* probs, const float* dctx, int T, int K, int w, bf16* dqkv,
                     cudaStream_t st) {
@@ -493,10 +665,10 @@ void group_attn_bwd(const float* qkv, const float* probs, const float* dctx, int
     done = 1;
   }
   const int grid = cdiv(T, TT);
-  if (K == 2) group_attn_bwd_kernel<2><<<grid, 128, smem, st>>>(qkv, probs, dctx, T, K, w, dqkv);
-  else if (K == 4) group_attn_bwd_kernel<4><<<grid, 128, smem, st>>>(qkv, probs, dctx, T, K, w, dqkv);
-  else if (K == 8) group_attn_bwd_kernel<8><<<grid, 128, smem, st>>>(qkv, probs, dctx, T, K, w, dqkv);
-  else group_attn_bwd_kernel<0><<<grid, 128, smem, st>>>(qkv, probs, dctx, T, K, w, dqkv);
+  if (K == 2) launch(group_attn_bwd_kernel<2>, grid, 128, smem, st, qkv, probs, dctx, T, K, w, dqkv);
+  else if (K == 4) launch(group_attn_bwd_kernel<4>, grid, 128, smem, st, qkv, probs, dctx, T, K, w, dqkv);
+  else if (K == 8) launch(group_attn_bwd_kernel<8>, grid, 128, smem, st, qkv, probs, dctx, T, K, w, dqkv);
+  else launch(group_attn_bwd_kernel<0>, grid, 128, smem, st, qkv, probs, dctx, T, K, w, dqkv);
 }
 
 // ============================================================== hybrid attention
@@ -506,6 +678,8 @@ void group_attn_bwd(const float* qkv, const float* probs, const float* dctx, int
 constexpr int kAttnChunk = 64;
 
 __global__ void attn_fwd_kernel(AttnArgs a) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float sm[];
   const int b = blockIdx.x / a.heads, h = blockIdx.x % a.heads;
   const int dh = a.D / a.heads;
@@ -595,12 +769,14 @@ void attn_fwd(const AttnArgs& a, cudaStream_t st) {
   static int done = 0;
   if (!done) { cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); done = 1; }
   const int threads = std::min(1024, 32 * std::max(4, (a.nq + 7) / 8));
-  attn_fwd_kernel<<<a.B * a.heads, threads, smem, st>>>(a);
+  launch(attn_fwd_kernel, a.B * a.heads, threads, smem, st, a);
 }
 
 // Backward (masked_softmax bw p⊙(g−Σg⊙p), tensors.py:346-349; matmul bws, tensors.py:219-244).
 // P is recomputed from the saved log-sum-exp; dQ accumulates in smem across key chunks.
 __global__ void attn_bwd_kernel(AttnArgs a) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float sm[];
   const int b = blockIdx.x / a.heads, h = blockIdx.x % a.heads;
   const int dh = a.D / a.heads;
@@ -692,13 +868,15 @@ void attn_bwd(const AttnArgs& a, cudaStream_t st) {
   const int smem = 4 * (3 * a.nq * ldp + 2 * kAttnChunk * ldp + 2 * a.nq * kAttnChunk + 2 * a.nq);
   static int done = 0;
   if (!done) { cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); done = 1; }
-  attn_bwd_kernel<<<a.B * a.heads, 256, smem, st>>>(a);
+  launch(attn_bwd_kernel, a.B * a.heads, 256, smem, st, a);
 }
 
 // ============================================================== global tokens
 // nontarget_global_tokens / target_global_token raw rows (pkg/src/longrec/inputs.py:500-537),
 // before the shared global MLP (which runs as tcgen05 GEMMs).  One CTA per sample.
 __global__ void globals_raw_fwd_kernel(GlobalsArgs a) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float s_u[64], s_tf[64], s_td[64];
   const int b = blockIdx.x;
   const int F = a.d_item + a.d_act + a.d_time;
@@ -738,12 +916,14 @@ __global__ void globals_raw_fwd_kernel(GlobalsArgs a) {
 }
 
 void globals_raw_fwd(const GlobalsArgs& a, cudaStream_t st) {
-  globals_raw_fwd_kernel<<<a.B, 128, 0, st>>>(a);
+  launch(globals_raw_fwd_kernel, a.B, 128, 0, st, a);
 }
 
 // Backward of the raw global rows: lift / token-projection / cls / table gradients, accumulated
 // per CTA in shared memory over a slice of samples, then flushed with one atomic per entry.
 __global__ void globals_raw_bwd_kernel(GlobalsArgs a, int per_block) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float sm[];
   const int F = a.d_item + a.d_act + a.d_time;
   float* s_lw = sm;                       // d*D
@@ -819,73 +999,103 @@ void globals_raw_bwd(const GlobalsArgs& a, cudaStream_t st) {
   const int smem = 4 * (a.d * a.D + a.D + (a.m - 2) * a.D + F * a.d + a.d + 3 * 64 + 64);
   static int done = 0;
   if (!done) { cudaFuncSetAttribute(globals_raw_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); done = 1; }
-  const int per = std::max(1, cdiv(a.B, 64));
-  globals_raw_bwd_kernel<<<cdiv(a.B, per), 256, smem, st>>>(a, per);
+  const int per = std::max(1, cdiv(a.B, 148));
+  launch(globals_raw_bwd_kernel, cdiv(a.B, per), 256, smem, st, a, per);
 }
 
 // ============================================================== head + BCE
 // Head of forward_tensor (pkg/src/longrec/model.py:346-362): [t, c, t⊙c, t⊙t, u_d] → GELU MLP →
-// sigmoid; BCE with the 1e-12 clamp (tensors.py:551-571).  One CTA per sample.
-__global__ void head_fwd_kernel(HeadArgs a) {
-  extern __shared__ float s_in[];                  // HIN + hh
-  const int b = blockIdx.x;
-  const int D = a.D, HIN = 4 * D + 2 * a.d;
-  const float* t = a.x + ((long long)b * a.q + a.k + a.m - 1) * D;
-  const float* c = a.x + ((long long)b * a.q + a.k + 1) * D;
-  const int uid = a.uid[b], prof = a.profile[b];
-  for (int i = threadIdx.x; i < D; i += blockDim.x) {
+// sigmoid; BCE with the 1e-12 clamp (tensors.py:551-571).  One warp per sample: lanes own hidden
+// units (coalesced W1 rows, the input row broadcast from shared memory).
+constexpr int kHeadWarps = 8;
+
+// W1 [HIN, hh] staged in shared memory with row stride hh+1: conflict-free both for lanes over
+// hidden units (forward) and lanes over inputs (backward).
+__device__ __forceinline__ void stage_w1(const float* __restrict__ w1, int HIN, int hh, float* s_w) {
+  const int n = HIN * hh;
+#pragma unroll 8
+  for (int e = threadIdx.x; e < n; e += blockDim.x) s_w[(e / hh) * (hh + 1) + e % hh] = __ldg(w1 + e);
+  __syncthreads();
+}
+
+__device__ __forceinline__ void head_row(const float* x, int b, int q, int k, int m, int D, int d, const int32_t* uid,
+                                         const int32_t* profile, const float* uid_tab, const float* prof_tab,
+                                         float* s_in, int lane) {
+  const float* t = x + ((long long)b * q + k + m - 1) * D;
+  const float* c = x + ((long long)b * q + k + 1) * D;
+  for (int i = lane; i < D; i += 32) {
     const float tv = t[i], cv = c[i];
     s_in[i] = tv; s_in[D + i] = cv; s_in[2 * D + i] = tv * cv; s_in[3 * D + i] = tv * tv;
   }
-  for (int i = threadIdx.x; i < a.d; i += blockDim.x) {
-    s_in[4 * D + i] = a.uid_tab[(long long)uid * a.d + i];
-    s_in[4 * D + a.d + i] = a.prof_tab[(long long)prof * a.d + i];
+  const int u = uid[b], pr = profile[b];
+  for (int i = lane; i < d; i += 32) {
+    s_in[4 * D + i] = uid_tab[(long long)u * d + i];
+    s_in[4 * D + d + i] = prof_tab[(long long)pr * d + i];
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < HIN; i += blockDim.x) a.hin[(long long)b * HIN + i] = s_in[i];
-  float* s_h = s_in + HIN;
-  {
-    // warp w handles hidden units j ≡ w (mod warps); lanes split the HIN inputs, then reduce
-    const int wid = threadIdx.x / 32, lane = threadIdx.x & 31, nw = blockDim.x / 32;
-    for (int j = wid; j < a.hh; j += nw) {
-      float acc = 0.f;
-      for (int i = lane; i < HIN; i += 32) acc = fmaf(s_in[i], __ldg(a.w1 + i * a.hh + j), acc);
-      acc = warp_sum(acc) + a.b1[j];
-      if (lane == 0) {
-        a.z1[(long long)b * a.hh + j] = acc;
-        s_h[j] = gelu_f(acc);
-      }
+  __syncwarp();
+}
+
+template <bool STAGE>
+__global__ void head_fwd_kernel(HeadArgs a) {
+  pdl_trigger();
+  pdl_wait();
+  extern __shared__ float smem_h[];
+  const int D = a.D, HIN = 4 * D + 2 * a.d;
+  const int wid = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int ws = STAGE ? a.hh + 1 : a.hh;
+  const float* W1 = a.w1;
+  float* s_base = smem_h;
+  if constexpr (STAGE) {
+    stage_w1(a.w1, HIN, a.hh, smem_h);
+    W1 = smem_h;
+    s_base = smem_h + HIN * ws;
+  }
+  const int b = blockIdx.x * kHeadWarps + wid;
+  if (b >= a.B) return;
+  float* s_in = s_base + wid * HIN;
+  head_row(a.x, b, a.q, a.k, a.m, D, a.d, a.uid, a.profile, a.uid_tab, a.prof_tab, s_in, lane);
+  for (int i = lane; i < HIN; i += 32) a.hin[(long long)b * HIN + i] = s_in[i];
+  float zpart = 0.f;
+  for (int j = lane; j < a.hh; j += 32) {
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    int i = 0;
+    for (; i + 3 < HIN; i += 4) {
+      a0 = fmaf(s_in[i], W1[i * ws + j], a0);
+      a1 = fmaf(s_in[i + 1], W1[(i + 1) * ws + j], a1);
+      a2 = fmaf(s_in[i + 2], W1[(i + 2) * ws + j], a2);
+      a3 = fmaf(s_in[i + 3], W1[(i + 3) * ws + j], a3);
     }
+    for (; i < HIN; ++i) a0 = fmaf(s_in[i], W1[i * ws + j], a0);
+    const float z1 = (a0 + a1) + (a2 + a3) + a.b1[j];
+    a.z1[(long long)b * a.hh + j] = z1;
+    zpart = fmaf(gelu_f(z1), a.w2[j], zpart);
   }
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    float acc = 0.f;
-    for (int j = threadIdx.x; j < a.hh; j += 32) acc = fmaf(s_h[j], a.w2[j], acc);
-    acc = warp_sum(acc);
-    if (threadIdx.x == 0) {
-      const float z = acc + a.b2[0];
-      const float e = __expf(-fabsf(z));
-      const float p = z >= 0.f ? 1.f / (1.f + e) : e / (1.f + e);
-      a.probs[b] = p;
-      if (a.loss_per) {
-        // bce with the reference's clamp p_c = clip(p, 1e-12, 1-1e-12) (tensors.py:551-571),
-        // evaluated in log-odds space: 1 - 1e-12 is not representable in fp32, but
-        // log p = -softplus(-z) and log(1-p) = -softplus(z) are, and clamping p at 1e-12 is
-        // clamping the log at log(1e-12); the clamp's zero-gradient region is |z| ≥ logit(1-1e-12).
-        const float y = a.label[b];
-        const float kLog12 = -27.631021115928547f;          // log(1e-12)
-        const float sp_pos = fmaxf(z, 0.f) + log1pf(__expf(-fabsf(z)));    // softplus(z)
-        const float sp_neg = sp_pos - z;                                   // softplus(-z)
-        const float log_p = fmaxf(-sp_neg, kLog12), log_q = fmaxf(-sp_pos, kLog12);
-        a.loss_per[b] = -(y * log_p + (1.f - y) * log_q);
-        const bool inr = fabsf(z) < 27.631021115928547f;
-        a.dz[b] = inr ? (p - y) / (float)a.B : 0.f;
-      }
+  const float acc = warp_sum(zpart);
+  if (lane == 0) {
+    const float z = acc + a.b2[0];
+    const float e = __expf(-fabsf(z));
+    const float p = z >= 0.f ? 1.f / (1.f + e) : e / (1.f + e);
+    a.probs[b] = p;
+    if (a.loss_per) {
+      // bce with the reference's clamp p_c = clip(p, 1e-12, 1-1e-12) (tensors.py:551-571),
+      // evaluated in log-odds space: 1 - 1e-12 is not representable in fp32, but
+      // log p = -softplus(-z) and log(1-p) = -softplus(z) are, and clamping p at 1e-12 is
+      // clamping the log at log(1e-12); the clamp's zero-gradient region is |z| ≥ logit(1-1e-12).
+      const float y = a.label[b];
+      const float kLog12 = -27.631021115928547f;          // log(1e-12)
+      const float sp_pos = fmaxf(z, 0.f) + log1pf(__expf(-fabsf(z)));    // softplus(z)
+      const float sp_neg = sp_pos - z;                                   // softplus(-z)
+      const float log_p = fmaxf(-sp_neg, kLog12), log_q = fmaxf(-sp_pos, kLog12);
+      a.loss_per[b] = -(y * log_p + (1.f - y) * log_q);
+      const bool inr = fabsf(z) < 27.631021115928547f;
+      a.dz[b] = inr ? (p - y) / (float)a.B : 0.f;
     }
   }
 }
 
 __global__ void loss_mean_kernel(const float* loss_per, int B, float* loss) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float red[256];
   float s = 0.f;
   for (int i = threadIdx.x; i < B; i += blockDim.x) s += loss_per[i];
@@ -898,41 +1108,75 @@ __global__ void loss_mean_kernel(const float* loss_per, int B, float* loss) {
   if (threadIdx.x == 0) loss[0] = red[0] / (float)B;
 }
 
+namespace {
+int head_smem_w1(const HeadArgs& a) { return 4 * (4 * a.D + 2 * a.d) * (a.hh + 1); }
+constexpr int kHeadSmemMax = 200 * 1024;
+}  // namespace
+
 void head_fwd(const HeadArgs& a, int with_loss, cudaStream_t st) {
-  const int smem = 4 * (4 * a.D + 2 * a.d + a.hh);
-  head_fwd_kernel<<<a.B, 128, smem, st>>>(a);
-  if (with_loss) loss_mean_kernel<<<1, 256, 0, st>>>(a.loss_per, a.B, a.loss);
+  const int smem = 4 * kHeadWarps * (4 * a.D + 2 * a.d);
+  const bool stage = smem + head_smem_w1(a) <= kHeadSmemMax;
+  if (stage) {
+    static int done = 0;
+    if (!done) { cudaFuncSetAttribute(head_fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHeadSmemMax); done = 1; }
+    launch(head_fwd_kernel<true>, cdiv(a.B, kHeadWarps), 32 * kHeadWarps, smem + head_smem_w1(a), st, a);
+  } else {
+    launch(head_fwd_kernel<false>, cdiv(a.B, kHeadWarps), 32 * kHeadWarps, smem, st, a);
+  }
+  if (with_loss) launch(loss_mean_kernel, 1, 256, 0, st, a.loss_per, a.B, a.loss);
 }
 
+// Head backward, one warp per sample: dz1 = dz·w2⊙GELU'(z1) (lanes = hidden units), then
+// dhin = W1·dz1 with lanes over the inputs, W1 rows read as float4 runs.
+template <bool STAGE>
 __global__ void head_bwd_kernel(HeadArgs a) {
-  extern __shared__ float s[];
-  const int b = blockIdx.x;
+  pdl_trigger();
+  pdl_wait();
+  extern __shared__ float smem_h[];
   const int D = a.D, HIN = 4 * D + 2 * a.d;
-  float* s_dz1 = s;              // hh
-  float* s_dhin = s + a.hh;      // HIN
+  const int wid = threadIdx.x / 32, lane = threadIdx.x & 31;
+  float* s_base = smem_h;
+  if constexpr (STAGE) {
+    stage_w1(a.w1, HIN, a.hh, smem_h);
+    s_base = smem_h + HIN * (a.hh + 1);
+  }
+  const int b = blockIdx.x * kHeadWarps + wid;
+  if (b >= a.B) return;
+  float* s_dz1 = s_base + wid * (a.hh + HIN);
+  float* s_dhin = s_dz1 + a.hh;
   const float dz = a.dz[b];
-  for (int j = threadIdx.x; j < a.hh; j += blockDim.x) {
+  for (int j = lane; j < a.hh; j += 32) {
     const float v = dz * a.w2[j] * gelu_grad_f(a.z1[(long long)b * a.hh + j]);
     s_dz1[j] = v;
     a.dz1[(long long)b * a.hh + j] = v;
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < HIN; i += blockDim.x) {
+  __syncwarp();
+  const bool vec = !STAGE && (a.hh % 4) == 0 && (reinterpret_cast<uintptr_t>(a.w1) & 15) == 0;
+  for (int i = lane; i < HIN; i += 32) {
+    const float* wr = STAGE ? smem_h + i * (a.hh + 1) : a.w1 + (long long)i * a.hh;
     float acc = 0.f;
-    for (int j = 0; j < a.hh; ++j) acc = fmaf(s_dz1[j], a.w1[i * a.hh + j], acc);
+    if (vec) {
+      for (int j = 0; j < a.hh; j += 4) {
+        const float4 w = __ldg(reinterpret_cast<const float4*>(wr + j));
+        acc = fmaf(s_dz1[j], w.x, acc); acc = fmaf(s_dz1[j + 1], w.y, acc);
+        acc = fmaf(s_dz1[j + 2], w.z, acc); acc = fmaf(s_dz1[j + 3], w.w, acc);
+      }
+    } else {
+      for (int j = 0; j < a.hh; ++j) acc = fmaf(s_dz1[j], wr[j], acc);
+    }
     s_dhin[i] = acc;
   }
-  __syncthreads();
+  __syncwarp();
   const float* hin = a.hin + (long long)b * HIN;
   float* dt = a.dx + ((long long)b * a.q + a.k + a.m - 1) * D;
   float* dc = a.dx + ((long long)b * a.q + a.k + 1) * D;
-  for (int i = threadIdx.x; i < D; i += blockDim.x) {
+  for (int i = lane; i < D; i += 32) {
     const float t = hin[i], c = hin[D + i];
     dt[i] = s_dhin[i] + s_dhin[2 * D + i] * c + 2.f * s_dhin[3 * D + i] * t;
     dc[i] = s_dhin[D + i] + s_dhin[2 * D + i] * t;
   }
   const int uid = a.uid[b], prof = a.profile[b];
-  for (int i = threadIdx.x; i < a.d; i += blockDim.x) {
+  for (int i = lane; i < a.d; i += 32) {
     atomicAdd(&a.g_uid[(long long)uid * a.d + i], s_dhin[4 * D + i]);
     atomicAdd(&a.g_prof[(long long)prof * a.d + i], s_dhin[4 * D + a.d + i]);
   }
@@ -941,6 +1185,8 @@ __global__ void head_bwd_kernel(HeadArgs a) {
 // head weight gradients: deterministic reductions over the batch (one thread per weight)
 // head weight gradients: batch reductions split over gridDim.y sample slices (atomic combine)
 __global__ void head_wgrad_kernel(HeadArgs a, int per) {
+  pdl_trigger();
+  pdl_wait();
   const int HIN = 4 * a.D + 2 * a.d;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   const int n_w1 = HIN * a.hh;
@@ -973,14 +1219,23 @@ __global__ void head_wgrad_kernel(HeadArgs a, int per) {
 
 void head_bwd(const HeadArgs& a, cudaStream_t st) {
   const int HIN = 4 * a.D + 2 * a.d;
-  head_bwd_kernel<<<a.B, 128, 4 * (a.hh + HIN), st>>>(a);
+  const int smem = 4 * kHeadWarps * (a.hh + HIN);
+  if (smem + head_smem_w1(a) <= kHeadSmemMax) {
+    static int done = 0;
+    if (!done) { cudaFuncSetAttribute(head_bwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHeadSmemMax); done = 1; }
+    launch(head_bwd_kernel<true>, cdiv(a.B, kHeadWarps), 32 * kHeadWarps, smem + head_smem_w1(a), st, a);
+  } else {
+    launch(head_bwd_kernel<false>, cdiv(a.B, kHeadWarps), 32 * kHeadWarps, smem, st, a);
+  }
   const int n = HIN * a.hh + a.hh + 1;
   const int per = 16;
-  head_wgrad_kernel<<<dim3(cdiv(n, 128), cdiv(a.B, per)), 128, 0, st>>>(a, per);
+  launch(head_wgrad_kernel, dim3(cdiv(n, 128), cdiv(a.B, per)), 128, 0, st, a, per);
 }
 
 // ============================================================== parameters
 __global__ void pack_kernel(const float* __restrict__ params, const PackList specs, void* dst) {
+  pdl_trigger();
+  pdl_wait();
   const CopySpec s = specs.s[blockIdx.y];
   const long long n = (long long)s.rows * s.cols;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
@@ -993,11 +1248,13 @@ __global__ void pack_kernel(const float* __restrict__ params, const PackList spe
 }
 
 void pack_params(const float* params, const PackList& specs, void* dst_base, cudaStream_t st) {
-  if (specs.n) pack_kernel<<<dim3(64, specs.n), 256, 0, st>>>(params, specs, dst_base);
+  if (specs.n) launch(pack_kernel, dim3(64, specs.n), 256, 0, st, params, specs, dst_base);
 }
 
 // Adam (pkg/src/longrec/model.py:467-482)
 __global__ void adam_kernel(float* p, const float* g, float* m, float* v, long long n, float lr, float c1, float c2) {
+  pdl_trigger();
+  pdl_wait();
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const float gi = g[i];
     const float mi = 0.9f * m[i] + 0.1f * gi;
@@ -1010,7 +1267,7 @@ __global__ void adam_kernel(float* p, const float* g, float* m, float* v, long l
 
 void adam_step(float* p, const float* g, float* m, float* v, long long n, float lr, int t, cudaStream_t st) {
   const float c1 = (float)(1.0 - pow(0.9, t)), c2 = (float)(1.0 - pow(0.999, t));
-  adam_kernel<<<148 * 8, 256, 0, st>>>(p, g, m, v, n, lr, c1, c2);
+  launch(adam_kernel, 148 * 8, 256, 0, st, p, g, m, v, n, lr, c1, c2);
 }
 
 }  // namespace longer

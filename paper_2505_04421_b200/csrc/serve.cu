@@ -22,6 +22,8 @@ inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 // ------------------------------------------------------------------ row copies
 __global__ void copy_rows_bf16_kernel(const bf16* src, long long s_stride, int s_ld, int s_col, bf16* dst,
                                       long long d_stride, int rows, int cols, int batch) {
+  pdl_trigger();
+  pdl_wait();
   const long long n = (long long)batch * rows * cols;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
     const int c = (int)(e % cols);
@@ -34,12 +36,14 @@ __global__ void copy_rows_bf16_kernel(const bf16* src, long long s_stride, int s
 void copy_rows_bf16(const bf16* src, long long s_stride, int s_ld, int s_col, bf16* dst, long long d_stride, int rows,
                     int cols, int batch, cudaStream_t st) {
   const long long n = (long long)batch * rows * cols;
-  if (n) copy_rows_bf16_kernel<<<std::min(cdiv(n, 256), 148 * 16), 256, 0, st>>>(src, s_stride, s_ld, s_col, dst,
+  if (n) launch(copy_rows_bf16_kernel, std::min(cdiv(n, 256), 148 * 16), 256, 0, st, src, s_stride, s_ld, s_col, dst,
                                                                                    d_stride, rows, cols, batch);
 }
 
 // per user: CLS output of the last layer, user-side head features [uid_emb | profile_emb], npg
 __global__ void cache_user_kernel(CacheUserArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const int u = blockIdx.x;
   const float* cls = a.x_last + ((long long)u * a.q + a.k + 1) * a.D;
   for (int c = threadIdx.x; c < a.D; c += blockDim.x) a.cls[(long long)u * a.D + c] = cls[c];
@@ -51,12 +55,14 @@ __global__ void cache_user_kernel(CacheUserArgs a) {
   if (threadIdx.x == 0) a.npg_out[u] = a.npg[u];
 }
 
-void cache_users(const CacheUserArgs& a, cudaStream_t st) { cache_user_kernel<<<a.U, 128, 0, st>>>(a); }
+void cache_users(const CacheUserArgs& a, cudaStream_t st) { launch(cache_user_kernel, a.U, 128, 0, st, a); }
 
 // ------------------------------------------------------------------ target rows
 // target_global_token (pkg/src/longrec/inputs.py:500-512) before the global MLP:
 // [item_emb | 0_act | time_emb[0]] · W_tp + b_tp → · lift_w + lift_b, one CTA per candidate row.
 __global__ void target_rows_kernel(TargetArgs a) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float s_tf[64], s_td[64];
   const long long r = blockIdx.x;
   const int F = a.d_item + a.d_act + a.d_time;
@@ -83,7 +89,7 @@ __global__ void target_rows_kernel(TargetArgs a) {
 }
 
 void target_rows(const TargetArgs& a, cudaStream_t st) {
-  if (a.R) target_rows_kernel<<<(unsigned)a.R, 128, 0, st>>>(a);
+  if (a.R) launch(target_rows_kernel, (unsigned)a.R, 128, 0, st, a);
 }
 
 // ------------------------------------------------------------------ cached attention
@@ -92,6 +98,8 @@ void target_rows(const TargetArgs& a, cudaStream_t st) {
 // Exact two-pass softmax; S = Q·K_cacheᵀ on the tensor core (TMEM), the own key in registers.
 template <int DH>
 __global__ void __launch_bounds__(kThreads, 1) serve_attn_kernel(ServeAttnArgs a) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   constexpr int kC = 128;
   bf16* sQ = reinterpret_cast<bf16*>(smem_raw);
@@ -255,7 +263,7 @@ int launch_serve(const ServeAttnArgs& a, cudaStream_t st) {
   static int done = 0;
   if (!done) { cudaFuncSetAttribute(serve_attn_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); done = 1; }
   const int tiles = (a.C + 127) / 128;
-  serve_attn_kernel<DH><<<a.U * tiles * a.heads, kThreads, std::max(smem, 116 * 1024), st>>>(a);
+  launch(serve_attn_kernel<DH>, a.U * tiles * a.heads, kThreads, std::max(smem, 116 * 1024), st, a);
   return (int)cudaGetLastError();
 }
 
@@ -263,6 +271,8 @@ int launch_serve(const ServeAttnArgs& a, cudaStream_t st) {
 // one warp per (candidate row, head); lanes stride the keys for the statistics and split the
 // head dims for P·V.
 __global__ void serve_attn_simt_kernel(ServeAttnArgs a) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float s_q[];                       // [warps][dh]
   const int dh = a.D / a.heads;
   const int wib = threadIdx.x / 32, lane = threadIdx.x & 31;
@@ -330,7 +340,7 @@ int serve_attn(const ServeAttnArgs& a, cudaStream_t st) {
   if (dh == 32) return launch_serve<32>(a, st);
   if (dh > 256) return (int)cudaErrorInvalidValue;
   const long long tasks = (long long)a.U * a.C * a.heads;
-  serve_attn_simt_kernel<<<(unsigned)((tasks + 3) / 4), 128, 4 * dh * sizeof(float), st>>>(a);
+  launch(serve_attn_simt_kernel, (unsigned)((tasks + 3) / 4), 128, 4 * dh * sizeof(float), st, a);
   return (int)cudaGetLastError();
 }
 
@@ -338,6 +348,8 @@ int serve_attn(const ServeAttnArgs& a, cudaStream_t st) {
 // head of forward_tensor (pkg/src/longrec/model.py:346-362) with the cached CLS row and user-side
 // features of the candidate's user (score_with_cache, serving.py:160-166).
 __global__ void serve_head_kernel(ServeHeadArgs a) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float s_in[];
   const long long r = blockIdx.x;
   const int u = (int)(r / a.C);
@@ -373,7 +385,7 @@ __global__ void serve_head_kernel(ServeHeadArgs a) {
 
 void serve_head(const ServeHeadArgs& a, cudaStream_t st) {
   const int smem = 4 * (4 * a.D + 2 * a.d + a.hh);
-  if (a.R) serve_head_kernel<<<(unsigned)a.R, 128, smem, st>>>(a);
+  if (a.R) launch(serve_head_kernel, (unsigned)a.R, 128, smem, st, a);
 }
 
 }  // namespace longer
