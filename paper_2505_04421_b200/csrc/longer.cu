@@ -40,6 +40,52 @@ void probe(int ph, int which, cudaStream_t st) {
   else cudaEventRecord(g_probe[ph][which], st);
 }
 
+// Side stream for the weight-gradient branch: dW GEMMs and bias column sums only feed the
+// gradient buffer, so they run beside the critical dX chain (fork after their inputs exist, one
+// join at the end of the call).  Inside stream capture the fork/join become graph edges.
+// LONGER_SIDE=0 runs everything on the caller's stream.
+struct Side {
+  int dev = -1;
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+};
+Side g_side[16];
+
+cudaStream_t side_stream(cudaStream_t main) {
+  const char* env = std::getenv("LONGER_SIDE");
+  if (env && env[0] == '0') return main;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Side& sd = g_side[dev & 15];
+  if (!sd.s) {
+    cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&sd.fork_ev, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&sd.join_ev, cudaEventDisableTiming);
+    sd.dev = dev;
+  }
+  return sd.s;
+}
+
+// side stream waits for everything enqueued on main so far
+void fork_side(cudaStream_t main, cudaStream_t side) {
+  if (side == main) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Side& sd = g_side[dev & 15];
+  cudaEventRecord(sd.fork_ev, main);
+  cudaStreamWaitEvent(side, sd.fork_ev, 0);
+}
+
+// main waits for everything enqueued on the side stream so far
+void join_side(cudaStream_t main, cudaStream_t side) {
+  if (side == main) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Side& sd = g_side[dev & 15];
+  cudaEventRecord(sd.join_ev, side);
+  cudaStreamWaitEvent(main, sd.join_ev, 0);
+}
+
 int fail(int code, const char* msg) {
   g_err = msg;
   return code;
@@ -135,6 +181,9 @@ struct Bump {
 struct BlockBufs {            // one attention block over the q query rows
   bf16 *qn, *qkv, *ctx, *x1n, *f1, *gf;
   float *m1, *r1, *lse, *x1, *m2, *r2, *out, *ctx32;
+  // backward, per block (the weight-gradient side stream reads them while the main stream moves on)
+  float *g_dx, *g_dx1n, *g_dx1, *g_dctx, *g_dqn;    // g_dx = dL/d(block output)
+  bf16 *g_dx_bf, *g_df1, *g_dx1_bf, *g_dqkv;
 };
 struct InnerBufs {            // one InnerTrans layer over T tokens
   bf16 *xn, *ctx, *x1n, *f1, *gf;
@@ -177,9 +226,8 @@ struct Plan {
   BlockBufs sb[kMaxSelf];
   // head
   float *hin, *z1, *loss_per, *dz, *dz1;
-  // backward scratch (query rows)
-  float *dx, *dx1n, *dx1, *dctx, *dqn, *dO;
-  bf16 *dx_bf, *df1, *dx1_bf, *dqkv;
+  // backward scratch (query rows; per-block scratch lives in BlockBufs)
+  float* dO;
   float* dkn;
   bf16* dKV;
   float *dmerged, *dglob, *draw;
@@ -256,6 +304,10 @@ Plan make_plan(const LongerDims& d, void* ws) {
     b.qkv = a.take<bf16>(Q * qkv_cols); b.ctx = a.take<bf16>(Q * D); b.lse = a.take<float>(Q * p.heads); b.ctx32 = a.take<float>(Q * D);
     b.x1 = a.take<float>(Q * D); b.x1n = a.take<bf16>(Q * D); b.m2 = a.take<float>(Q); b.r2 = a.take<float>(Q);
     b.f1 = a.take<bf16>(Q * 4 * D); b.gf = a.take<bf16>(Q * 4 * D); b.out = a.take<float>(Q * D);
+    b.g_dx = a.take<float>(Q * D); b.g_dx1n = a.take<float>(Q * D); b.g_dx1 = a.take<float>(Q * D);
+    b.g_dctx = a.take<float>(Q * D); b.g_dqn = a.take<float>(Q * D);
+    b.g_dx_bf = a.take<bf16>(Q * D); b.g_df1 = a.take<bf16>(Q * 4 * D); b.g_dx1_bf = a.take<bf16>(Q * D);
+    b.g_dqkv = a.take<bf16>(Q * qkv_cols);
   };
   block_bufs(p.cb, D);
   for (int i = 0; i < p.N; ++i) block_bufs(p.sb[i], 3 * D);
@@ -263,10 +315,7 @@ Plan make_plan(const LongerDims& d, void* ws) {
   p.hin = a.take<float>((long long)B * p.HIN); p.z1 = a.take<float>((long long)B * p.hh);
   p.loss_per = a.take<float>(B); p.dz = a.take<float>(B); p.dz1 = a.take<float>((long long)B * p.hh);
   // backward (query rows)
-  p.dx = a.take<float>(Q * D); p.dx1n = a.take<float>(Q * D); p.dx1 = a.take<float>(Q * D);
-  p.dctx = a.take<float>(Q * D); p.dqn = a.take<float>(Q * D); p.dO = a.take<float>(Q * D);
-  p.dx_bf = a.take<bf16>(Q * D); p.df1 = a.take<bf16>(Q * 4 * D); p.dx1_bf = a.take<bf16>(Q * D);
-  p.dqkv = a.take<bf16>(Q * 3 * D);
+  p.dO = a.take<float>(Q * D);
   p.dkn = a.take<float>(V * D); p.dKV = a.take<bf16>(V * 2 * D);
   p.dmerged = a.take<float>(T * dd); p.dglob = a.take<float>(M * D); p.draw = a.take<float>(M * D);
   p.dglob_bf = a.take<bf16>(M * D); p.dga = a.take<bf16>(M * 2 * D);
@@ -601,41 +650,48 @@ int forward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs, fl
   return 0;
 }
 
-// Backward of one attention block; dout in p.dx, d(x_q) written back to p.dx (self) or into
-// dmerged / dglob (cross).  (pkg/src/longrec/attention.py:172-212 + tensors.py backward closures)
-int block_bwd(const Ctx& c, const BlockOff& bo, const BlockBufs& b, const float* xq, bool cross, const bf16* Wqkv,
-              const bf16* Wo, const bf16* W1, const bf16* W2) {
+// Backward of one attention block (pkg/src/longrec/attention.py:172-212 + tensors.py backward
+// closures).  dL/d(out) is in b.g_dx (fp32) / b.g_dx_bf (bf16).  The critical dX chain runs on
+// c.st; every weight gradient and bias column sum goes to the side stream ss.
+//   self:  dL/d(x_q) → nxt_dx / nxt_dx_bf (the previous block's g_dx), with the column sums of it
+//          accumulated into nxt_b2 (that block's FFN output bias gradient).
+//   cross: dL/d(merged rows) → p.dmerged, dL/d(global rows) → p.dglob.
+int block_bwd(const Ctx& c, cudaStream_t ss, const BlockOff& bo, const BlockBufs& b, const float* xq, bool cross,
+              const bf16* Wqkv, const bf16* Wo, const bf16* W1, const bf16* W2, float* nxt_dx, bf16* nxt_dx_bf,
+              float* nxt_b2) {
   const Plan& p = c.p;
   cudaStream_t st = c.st;
   const int D = p.D;
   const long long Q = (long long)p.B * p.q, V = (long long)p.B * p.v;
-  cast_rows_bf16(p.dx, (int)Q, D, D, p.dx_bf, D, nullptr, st);
   // FFN + residual
-  TRY(lin_dx(st, p.dx_bf, D, Q, W2, D, 4 * D, D, nullptr, 0, p.df1, 4 * D, b.f1));
-  TRY(lin_dw(st, b.gf, 4 * D, 4 * D, p.dx_bf, D, D, Q, c.g(bo.w2)));
-  colsum_f32(p.dx, (int)Q, D, D, c.g(bo.b2), st);
-  TRY(lin_dx(st, p.df1, 4 * D, Q, W1, 4 * D, D, 4 * D, p.dx1n, D, nullptr, 0));
-  TRY(lin_dw(st, b.x1n, D, D, p.df1, 4 * D, 4 * D, Q, c.g(bo.w1)));
-  colsum_bf16(p.df1, (int)Q, 4 * D, 4 * D, c.g(bo.b1), st);
-  TRY((int)cudaMemcpyAsync(p.dx1, p.dx, Q * D * 4, cudaMemcpyDeviceToDevice, st));
-  layernorm_bwd(rows_plain(b.x1, D, Q), D, c.w(bo.ln2_g), b.m2, b.r2, p.dx1n, D, rows_plain_w(p.dx1, D, Q), 1,
-                nullptr, c.g(bo.ln2_g), c.g(bo.ln2_b), st);
-  cast_rows_bf16(p.dx1, (int)Q, D, D, p.dx1_bf, D, nullptr, st);
-  // output projection + residual
-  TRY(lin_dx(st, p.dx1_bf, D, Q, Wo, D, D, D, p.dctx, D, nullptr, 0));
-  TRY(lin_dw(st, b.ctx, D, D, p.dx1_bf, D, D, Q, c.g(bo.w_o)));
-  colsum_f32(p.dx1, (int)Q, D, D, c.g(bo.b_o), st);
+  fork_side(st, ss);
+  TRY(lin_dw(ss, b.gf, 4 * D, 4 * D, b.g_dx_bf, D, D, Q, c.g(bo.w2)));
+  TRY(lin_dx(st, b.g_dx_bf, D, Q, W2, D, 4 * D, D, nullptr, 0, b.g_df1, 4 * D, b.f1));
+  fork_side(st, ss);
+  TRY(lin_dw(ss, b.x1n, D, D, b.g_df1, 4 * D, 4 * D, Q, c.g(bo.w1)));
+  colsum_bf16(b.g_df1, (int)Q, 4 * D, 4 * D, c.g(bo.b1), ss);
+  TRY(lin_dx(st, b.g_df1, 4 * D, Q, W1, 4 * D, D, 4 * D, b.g_dx1n, D, nullptr, 0));
+  {
+    LnBwdExtra ex;
+    ex.addend = b.g_dx; ex.out_bf = b.g_dx1_bf; ex.colsum_out = c.g(bo.b_o);
+    layernorm_bwd(rows_plain(b.x1, D, Q), D, c.w(bo.ln2_g), b.m2, b.r2, b.g_dx1n, D, rows_plain_w(b.g_dx1, D, Q), 0,
+                  nullptr, c.g(bo.ln2_g), c.g(bo.ln2_b), st, ex);
+  }
+  // output projection
+  fork_side(st, ss);
+  TRY(lin_dw(ss, b.ctx, D, D, b.g_dx1_bf, D, D, Q, c.g(bo.w_o)));
+  TRY(lin_dx(st, b.g_dx1_bf, D, Q, Wo, D, D, D, b.g_dctx, D, nullptr, 0));
   // attention
   AttnArgs a{};
   a.nq = p.q; a.D = D; a.heads = p.heads; a.k = p.k; a.G = p.G; a.npg = p.npg; a.B = p.B;
   a.ctx = b.ctx; a.ldc = D; a.sc = (long long)p.q * D; a.lse = b.lse; a.ctx32 = b.ctx32;
-  a.dctx = p.dctx; a.lddc = D; a.sdc = (long long)p.q * D; a.ctx_in = b.ctx;
+  a.dctx = b.g_dctx; a.lddc = D; a.sdc = (long long)p.q * D; a.ctx_in = b.ctx;
   if (cross) {
     a.Q = b.qkv; a.ldq = D; a.sq = (long long)p.q * D;
     a.Kp = p.KV; a.ldk = 2 * D; a.sk = (long long)p.v * 2 * D;
     a.V = p.KV + D; a.ldv = 2 * D; a.sv = a.sk;
     a.nk = p.v; a.ns = p.G; a.goff = 0;
-    a.dQ = p.dqkv; a.lddq = D; a.sdq = (long long)p.q * D;
+    a.dQ = b.g_dqkv; a.lddq = D; a.sdq = (long long)p.q * D;
     a.dK = p.dKV; a.lddk = 2 * D; a.sdk = (long long)p.v * 2 * D;
     a.dV = p.dKV + D; a.lddv = 2 * D; a.sdv = a.sdk;
   } else {
@@ -643,9 +699,9 @@ int block_bwd(const Ctx& c, const BlockOff& bo, const BlockBufs& b, const float*
     a.Kp = b.qkv + D; a.ldk = 3 * D; a.sk = a.sq;
     a.V = b.qkv + 2 * D; a.ldv = 3 * D; a.sv = a.sq;
     a.nk = p.q; a.ns = p.k; a.goff = p.G - p.k;
-    a.dQ = p.dqkv; a.lddq = 3 * D; a.sdq = (long long)p.q * 3 * D;
-    a.dK = p.dqkv + D; a.lddk = 3 * D; a.sdk = a.sdq;
-    a.dV = p.dqkv + 2 * D; a.lddv = 3 * D; a.sdv = a.sdq;
+    a.dQ = b.g_dqkv; a.lddq = 3 * D; a.sdq = (long long)p.q * 3 * D;
+    a.dK = b.g_dqkv + D; a.lddk = 3 * D; a.sdk = a.sdq;
+    a.dV = b.g_dqkv + 2 * D; a.lddv = 3 * D; a.sdv = a.sdq;
   }
   if (use_attn_tc(a)) {
     if (cross) probe(PH_XATTN_BWD, 0, st);
@@ -654,15 +710,16 @@ int block_bwd(const Ctx& c, const BlockOff& bo, const BlockBufs& b, const float*
   } else {
     attn_bwd(a, st);
   }
+  fork_side(st, ss);
   if (cross) {
-    TRY(lin_dx(st, p.dqkv, D, Q, Wqkv, D, D, D, p.dqn, D, nullptr, 0));
-    TRY(lin_dw(st, b.qn, D, D, p.dqkv, D, D, Q, c.g(bo.w_q)));
-    colsum_bf16(p.dqkv, (int)Q, D, D, c.g(bo.b_q), st);
+    TRY(lin_dw(ss, b.qn, D, D, b.g_dqkv, D, D, Q, c.g(bo.w_q)));
+    colsum_bf16(b.g_dqkv, (int)Q, D, D, c.g(bo.b_q), ss);
+    TRY(lin_dw(ss, p.kn, D, D, p.dKV, 2 * D, D, V, c.g(bo.w_k)));
+    TRY(lin_dw(ss, p.kn, D, D, p.dKV + D, 2 * D, D, V, c.g(bo.w_v)));
+    colsum_bf16(p.dKV, (int)V, D, 2 * D, c.g(bo.b_k), ss);
+    colsum_bf16(p.dKV + D, (int)V, D, 2 * D, c.g(bo.b_v), ss);
+    TRY(lin_dx(st, b.g_dqkv, D, Q, Wqkv, D, D, D, b.g_dqn, D, nullptr, 0));
     TRY(lin_dx(st, p.dKV, 2 * D, V, p.pk.c_wkv, 2 * D, D, 2 * D, p.dkn, D, nullptr, 0));
-    TRY(lin_dw(st, p.kn, D, D, p.dKV, 2 * D, D, V, c.g(bo.w_k)));
-    TRY(lin_dw(st, p.kn, D, D, p.dKV + D, 2 * D, D, V, c.g(bo.w_v)));
-    colsum_bf16(p.dKV, (int)V, D, 2 * D, c.g(bo.b_k), st);
-    colsum_bf16(p.dKV + D, (int)V, D, 2 * D, c.g(bo.b_v), st);
     RowMap r{};
     r.A = p.merged; r.lda = D; r.a_rows = p.G; r.a_off = 0; r.na = p.G; r.Bsrc = p.glob; r.ldb = D; r.nb = p.m;
     r.batch = p.B;
@@ -670,22 +727,24 @@ int block_bwd(const Ctx& c, const BlockOff& bo, const BlockBufs& b, const float*
     rw.A = p.dmerged; rw.lda = D; rw.a_rows = p.G; rw.a_off = 0; rw.na = p.G; rw.Bsrc = p.dglob; rw.ldb = D;
     rw.nb = p.m; rw.batch = p.B;
     layernorm_bwd(r, D, c.w(bo.ln1_g), p.mk, p.rk, p.dkn, D, rw, 0, nullptr, c.g(bo.ln1_g), c.g(bo.ln1_b), st);
-    TRY((int)cudaMemcpyAsync(p.dO, p.dx1, Q * D * 4, cudaMemcpyDeviceToDevice, st));
-    layernorm_bwd(rows_plain(xq, D, Q), D, c.w(bo.ln1_g), b.m1, b.r1, p.dqn, D, rows_plain_w(p.dO, D, Q), 1,
-                  nullptr, c.g(bo.ln1_g), c.g(bo.ln1_b), st);
+    LnBwdExtra ex;
+    ex.addend = b.g_dx1;
+    layernorm_bwd(rows_plain(xq, D, Q), D, c.w(bo.ln1_g), b.m1, b.r1, b.g_dqn, D, rows_plain_w(p.dO, D, Q), 0,
+                  nullptr, c.g(bo.ln1_g), c.g(bo.ln1_b), st, ex);
     add_rows_f32(p.dO, p.B, p.q, 0, p.k, p.dmerged, p.G, p.G - p.k, D, st);
     add_rows_f32(p.dO, p.B, p.q, p.k, p.m, p.dglob, p.m, 0, D, st);
   } else {
-    TRY(lin_dx(st, p.dqkv, 3 * D, Q, Wqkv, 3 * D, D, 3 * D, p.dqn, D, nullptr, 0));
     for (int j = 0; j < 3; ++j) {
       const long long wo = j == 0 ? bo.w_q : (j == 1 ? bo.w_k : bo.w_v);
       const long long bb = j == 0 ? bo.b_q : (j == 1 ? bo.b_k : bo.b_v);
-      TRY(lin_dw(st, b.qn, D, D, p.dqkv + j * D, 3 * D, D, Q, c.g(wo)));
-      colsum_bf16(p.dqkv + j * D, (int)Q, D, 3 * D, c.g(bb), st);
+      TRY(lin_dw(ss, b.qn, D, D, b.g_dqkv + j * D, 3 * D, D, Q, c.g(wo)));
+      colsum_bf16(b.g_dqkv + j * D, (int)Q, D, 3 * D, c.g(bb), ss);
     }
-    TRY((int)cudaMemcpyAsync(p.dx, p.dx1, Q * D * 4, cudaMemcpyDeviceToDevice, st));
-    layernorm_bwd(rows_plain(xq, D, Q), D, c.w(bo.ln1_g), b.m1, b.r1, p.dqn, D, rows_plain_w(p.dx, D, Q), 1,
-                  nullptr, c.g(bo.ln1_g), c.g(bo.ln1_b), st);
+    TRY(lin_dx(st, b.g_dqkv, 3 * D, Q, Wqkv, 3 * D, D, 3 * D, b.g_dqn, D, nullptr, 0));
+    LnBwdExtra ex;
+    ex.addend = b.g_dx1; ex.out_bf = nxt_dx_bf; ex.colsum_out = nxt_b2;
+    layernorm_bwd(rows_plain(xq, D, Q), D, c.w(bo.ln1_g), b.m1, b.r1, b.g_dqn, D, rows_plain_w(nxt_dx, D, Q), 0,
+                  nullptr, c.g(bo.ln1_g), c.g(bo.ln1_b), st, ex);
   }
   return 0;
 }
@@ -696,8 +755,11 @@ int backward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs) {
   const LongerDims& dm = p.dims;
   const int d = p.d, D = p.D;
   const long long T = p.T, M = (long long)p.B * p.m, Q = (long long)p.B * p.q;
+  const cudaStream_t ss = side_stream(st);
+  const BlockBufs& last = p.N ? p.sb[p.N - 1] : p.cb;
   TRY((int)cudaMemsetAsync(c.G, 0, o.total * 4, st));
-  TRY((int)cudaMemsetAsync(p.dx, 0, Q * D * 4, st));
+  TRY((int)cudaMemsetAsync(last.g_dx, 0, Q * D * 4, st));
+  TRY((int)cudaMemsetAsync(last.g_dx_bf, 0, Q * D * 2, st));
   // head (model.py:346-362) → dx rows k+m-1 (target) and k+1 (CLS)
   HeadArgs h{};
   h.x = p.N ? p.sb[p.N - 1].out : p.cb.out;
@@ -705,23 +767,30 @@ int backward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs) {
   h.uid = bt.uid; h.profile = bt.profile; h.label = bt.label;
   h.uid_tab = c.w(o.uid); h.prof_tab = c.w(o.prof);
   h.w1 = c.w(o.head_w1); h.b1 = c.w(o.head_b1); h.w2 = c.w(o.head_w2); h.b2 = c.w(o.head_b2);
-  h.hin = p.hin; h.z1 = p.z1; h.probs = probs; h.dz = p.dz; h.dz1 = p.dz1; h.dx = p.dx;
+  h.hin = p.hin; h.z1 = p.z1; h.probs = probs; h.dz = p.dz; h.dz1 = p.dz1; h.dx = last.g_dx; h.dx_bf = last.g_dx_bf;
   h.g_w1 = c.g(o.head_w1); h.g_b1 = c.g(o.head_b1); h.g_w2 = c.g(o.head_w2); h.g_b2 = c.g(o.head_b2);
   h.g_uid = c.g(o.uid); h.g_prof = c.g(o.prof);
   head_bwd(h, st);
+  fork_side(st, ss);
+  colsum_f32(last.g_dx, (int)Q, D, D, c.g(p.N ? o.self_[p.N - 1].b2 : o.cross.b2), ss);
   for (int i = p.N - 1; i >= 0; --i) {
     const float* xin = i == 0 ? p.cb.out : p.sb[i - 1].out;
-    TRY(block_bwd(c, o.self_[i], p.sb[i], xin, false, p.pk.s_wqkv[i], p.pk.s_wo[i], p.pk.s_w1[i], p.pk.s_w2[i]));
+    const BlockBufs& nb = i == 0 ? p.cb : p.sb[i - 1];
+    TRY(block_bwd(c, ss, o.self_[i], p.sb[i], xin, false, p.pk.s_wqkv[i], p.pk.s_wo[i], p.pk.s_w1[i], p.pk.s_w2[i],
+                  nb.g_dx, nb.g_dx_bf, c.g(i == 0 ? o.cross.b2 : o.self_[i - 1].b2)));
   }
-  TRY(block_bwd(c, o.cross, p.cb, p.O, true, p.pk.c_wq, p.pk.c_wo, p.pk.c_w1, p.pk.c_w2));
+  TRY(block_bwd(c, ss, o.cross, p.cb, p.O, true, p.pk.c_wq, p.pk.c_wo, p.pk.c_w1, p.pk.c_w2, nullptr, nullptr,
+                nullptr));
   // global-token MLP and raw rows
   cast_rows_bf16(p.dglob, (int)M, D, D, p.dglob_bf, D, nullptr, st);
+  fork_side(st, ss);
+  TRY(lin_dw(ss, p.gg, 2 * D, 2 * D, p.dglob_bf, D, D, M, c.g(o.glob_w2)));
+  colsum_f32(p.dglob, (int)M, D, D, c.g(o.glob_b2), ss);
   TRY(lin_dx(st, p.dglob_bf, D, M, p.pk.glob_w2, D, 2 * D, D, nullptr, 0, p.dga, 2 * D, p.ga));
-  TRY(lin_dw(st, p.gg, 2 * D, 2 * D, p.dglob_bf, D, D, M, c.g(o.glob_w2)));
-  colsum_f32(p.dglob, (int)M, D, D, c.g(o.glob_b2), st);
+  fork_side(st, ss);
+  TRY(lin_dw(ss, p.raw_bf, D, D, p.dga, 2 * D, 2 * D, M, c.g(o.glob_w1)));
+  colsum_bf16(p.dga, (int)M, 2 * D, 2 * D, c.g(o.glob_b1), ss);
   TRY(lin_dx(st, p.dga, 2 * D, M, p.pk.glob_w1, 2 * D, D, 2 * D, p.draw, D, nullptr, 0));
-  TRY(lin_dw(st, p.raw_bf, D, D, p.dga, 2 * D, 2 * D, M, c.g(o.glob_w1)));
-  colsum_bf16(p.dga, (int)M, 2 * D, 2 * D, c.g(o.glob_b1), st);
   GlobalsArgs ga{};
   ga.uid = bt.uid; ga.cand_item = bt.cand_item; ga.B = p.B; ga.m = p.m; ga.d = d; ga.D = D;
   ga.d_item = dm.d_item; ga.d_act = dm.d_act; ga.d_time = dm.d_time;
@@ -785,6 +854,7 @@ int backward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs) {
     FrontArgs f = front_args(c, p, bt);
     f.dh = dxt;
     probe(PH_FE_MLP_BWD, 0, st); TRY(frontend_mlp_bwd(f, st)); probe(PH_FE_MLP_BWD, 1, st);
+    join_side(st, ss);
     TRY((int)cudaGetLastError());
     return 0;
   }
@@ -804,6 +874,7 @@ int backward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs) {
   eb.tok_w = c.w(o.tok_w); eb.dx0 = p.dx0;
   eb.g_item = c.g(o.item); eb.g_act = c.g(o.act); eb.g_time = c.g(o.time); eb.g_pos = c.g(o.pos);
   embed_bwd(eb, st);
+  join_side(st, ss);
   TRY((int)cudaGetLastError());
   return 0;
 }

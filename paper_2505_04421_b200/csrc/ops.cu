@@ -257,17 +257,17 @@ void layernorm_fwd(const RowMap& x, int W, const float* g, const float* b, bf16*
 template <int VPT, bool CONTIG>
 __global__ void ln_bwd_kernel(RowMap x, int W, const float* __restrict__ g, const float* __restrict__ mean,
                               const float* __restrict__ rstd, const float* __restrict__ dy, int ldy, RowMapW out,
-                              int accumulate, const float* rowmask, float* dgain, float* dbias) {
+                              int accumulate, const float* rowmask, float* dgain, float* dbias, LnBwdExtra ex) {
   pdl_trigger();
   pdl_wait();
-  __shared__ float sg[8][VPT * 32], sb[8][VPT * 32];
+  __shared__ float sg[8][VPT * 32], sb[8][VPT * 32], sc[8][VPT * 32];
   const int warps = blockDim.x / 32;
   const int wid = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int rows = x.rows();
   const int per = x.na + x.nb;
-  float pg[VPT], pb[VPT], gv[VPT];
+  float pg[VPT], pb[VPT], pc[VPT], gv[VPT];
 #pragma unroll
-  for (int u = 0; u < VPT; ++u) { pg[u] = 0.f; pb[u] = 0.f; }
+  for (int u = 0; u < VPT; ++u) { pg[u] = 0.f; pb[u] = 0.f; pc[u] = 0.f; }
 #pragma unroll
   for (int u = 0; u < VPT; ++u) {
     const int c = ln_col<VPT, CONTIG>(lane, u);
@@ -300,13 +300,33 @@ __global__ void ln_bwd_kernel(RowMap x, int W, const float* __restrict__ g, cons
     }
     const float m1 = warp_sum(s1) / W, m2 = warp_sum(s2) / W;
     const float rm = rowmask ? rowmask[row] : 1.f;
-    float o[VPT];
+    float o[VPT], ad[VPT];
     if (accumulate) ln_load<VPT, CONTIG>(dst, lane, W, o);
+    if (ex.addend) ln_load<VPT, CONTIG>(ex.addend + (long long)row * W, lane, W, ad);
 #pragma unroll
     for (int u = 0; u < VPT; ++u) {
       float v = (gh[u] - m1 - xh[u] * m2) * inv;
       if (accumulate) v += o[u];
+      if (ex.addend) v += ad[u];
       o[u] = v * rm;
+      pc[u] += o[u];
+    }
+    if (ex.out_bf) {
+      bf16* ob = ex.out_bf + (long long)row * W;
+      if constexpr (CONTIG && VPT >= 2) {
+        uint32_t w[VPT / 2];
+#pragma unroll
+        for (int u = 0; u < VPT; u += 2) w[u / 2] = sm100::pack_bf16(o[u], o[u + 1]);
+        if constexpr (VPT == 8) *reinterpret_cast<uint4*>(ob + lane * 8) = make_uint4(w[0], w[1], w[2], w[3]);
+        else if constexpr (VPT == 4) *reinterpret_cast<uint2*>(ob + lane * 4) = make_uint2(w[0], w[1]);
+        else *reinterpret_cast<uint32_t*>(ob + lane * 2) = w[0];
+      } else {
+#pragma unroll
+        for (int u = 0; u < VPT; ++u) {
+          const int c = ln_col<VPT, CONTIG>(lane, u);
+          if (c < W) ob[c] = __float2bfloat16(o[u]);
+        }
+      }
     }
     if constexpr (CONTIG && VPT == 8) {
       reinterpret_cast<float4*>(dst + lane * 8)[0] = make_float4(o[0], o[1], o[2], o[3]);
@@ -323,35 +343,37 @@ __global__ void ln_bwd_kernel(RowMap x, int W, const float* __restrict__ g, cons
       }
     }
   }
-  if (dgain) {
+  if (dgain || ex.colsum_out) {
 #pragma unroll
     for (int u = 0; u < VPT; ++u) {
       const int c = ln_col<VPT, CONTIG>(lane, u);
-      sg[wid][c] = pg[u]; sb[wid][c] = pb[u];
+      sg[wid][c] = pg[u]; sb[wid][c] = pb[u]; sc[wid][c] = pc[u];
     }
     __syncthreads();
     for (int c = threadIdx.x; c < W; c += blockDim.x) {
-      float a = 0.f, bb = 0.f;
-      for (int w = 0; w < warps; ++w) { a += sg[w][c]; bb += sb[w][c]; }
-      atomicAdd(&dgain[c], a);
-      atomicAdd(&dbias[c], bb);
+      float a = 0.f, bb = 0.f, cc = 0.f;
+      for (int w = 0; w < warps; ++w) { a += sg[w][c]; bb += sb[w][c]; cc += sc[w][c]; }
+      if (dgain) { atomicAdd(&dgain[c], a); atomicAdd(&dbias[c], bb); }
+      if (ex.colsum_out) atomicAdd(&ex.colsum_out[c], cc);
     }
   }
 }
 
 void layernorm_bwd(const RowMap& x, int W, const float* g, const float* mean, const float* rstd, const float* dy,
                    int ldy, const RowMapW& out, int accumulate, const float* rowmask, float* dgain, float* dbias,
-                   cudaStream_t st) {
+                   cudaStream_t st, LnBwdExtra ex) {
   const int rows = x.rows();
   if (rows <= 0) return;
-  const int grid = std::min(cdiv(rows, 8), 148 * 8);
+  // ~32 rows per 8-warp block: enough blocks to cover the SMs, few enough that the per-block
+  // atomic flush of the column partials stays cheap
+  const int grid = std::max(1, std::min(cdiv(rows, 32), 148 * 8));
   const int vpt = W <= 32 ? 1 : W <= 64 ? 2 : W <= 128 ? 4 : 8;
   const bool ct = ln_contig(W, vpt, x.A, x.lda, x.nb ? x.Bsrc : nullptr, x.ldb) &&
                   ln_contig(W, vpt, out.A, out.lda, out.nb ? out.Bsrc : nullptr, out.ldb) &&
                   ln_contig(W, vpt, dy, ldy, nullptr, 0);
-#define LNB(V) (ct ? launch(ln_bwd_kernel<V, true>, grid, 256, 0, st, x, W, g, mean, rstd, dy, ldy, out, accumulate, rowmask, dgain, dbias) \
-                   : launch(ln_bwd_kernel<V, false>, grid, 256, 0, st, x, W, g, mean, rstd, dy, ldy, out, accumulate, rowmask, dgain, dbias))
-  if (vpt == 1) launch(ln_bwd_kernel<1, false>, grid, 256, 0, st, x, W, g, mean, rstd, dy, ldy, out, accumulate, rowmask, dgain, dbias);
+#define LNB(V) (ct ? launch(ln_bwd_kernel<V, true>, grid, 256, 0, st, x, W, g, mean, rstd, dy, ldy, out, accumulate, rowmask, dgain, dbias, ex) \
+                   : launch(ln_bwd_kernel<V, false>, grid, 256, 0, st, x, W, g, mean, rstd, dy, ldy, out, accumulate, rowmask, dgain, dbias, ex))
+  if (vpt == 1) launch(ln_bwd_kernel<1, false>, grid, 256, 0, st, x, W, g, mean, rstd, dy, ldy, out, accumulate, rowmask, dgain, dbias, ex);
   else if (vpt == 2) LNB(2);
   else if (vpt == 4) LNB(4);
   else LNB(8);
@@ -1170,10 +1192,15 @@ __global__ void head_bwd_kernel(HeadArgs a) {
   const float* hin = a.hin + (long long)b * HIN;
   float* dt = a.dx + ((long long)b * a.q + a.k + a.m - 1) * D;
   float* dc = a.dx + ((long long)b * a.q + a.k + 1) * D;
+  bf16* dtb = a.dx_bf ? a.dx_bf + ((long long)b * a.q + a.k + a.m - 1) * D : nullptr;
+  bf16* dcb = a.dx_bf ? a.dx_bf + ((long long)b * a.q + a.k + 1) * D : nullptr;
   for (int i = lane; i < D; i += 32) {
     const float t = hin[i], c = hin[D + i];
-    dt[i] = s_dhin[i] + s_dhin[2 * D + i] * c + 2.f * s_dhin[3 * D + i] * t;
-    dc[i] = s_dhin[D + i] + s_dhin[2 * D + i] * t;
+    const float vt = s_dhin[i] + s_dhin[2 * D + i] * c + 2.f * s_dhin[3 * D + i] * t;
+    const float vc = s_dhin[D + i] + s_dhin[2 * D + i] * t;
+    dt[i] = vt;
+    dc[i] = vc;
+    if (dtb) { dtb[i] = __float2bfloat16(vt); dcb[i] = __float2bfloat16(vc); }
   }
   const int uid = a.uid[b], prof = a.profile[b];
   for (int i = lane; i < a.d; i += 32) {

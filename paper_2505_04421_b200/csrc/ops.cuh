@@ -51,9 +51,18 @@ struct RowMapW {
   float* Bsrc; int ldb; int nb;
   int batch;
 };
+// Optional extras of the LN backward (plain row indexing, row stride W):
+//   addend     out += addend[row]           (the residual branch's gradient)
+//   out_bf     bf16 copy of out              (the next GEMM's operand)
+//   colsum_out += column sums of out         (the bias gradient of the linear layer feeding out)
+struct LnBwdExtra {
+  const float* addend = nullptr;
+  bf16* out_bf = nullptr;
+  float* colsum_out = nullptr;
+};
 void layernorm_bwd(const RowMap& x, int W, const float* g, const float* mean, const float* rstd,
                    const float* dy, int ldy, const RowMapW& out, int accumulate, const float* rowmask,
-                   float* dgain, float* dbias, cudaStream_t st);
+                   float* dgain, float* dbias, cudaStream_t st, LnBwdExtra ex = LnBwdExtra());
 
 // column sums of a [rows, W] matrix (fp32 or bf16), atomically added to out[W]
 void colsum_f32(const float* x, int rows, int W, int ld, float* out, cudaStream_t st);
@@ -128,6 +137,7 @@ struct HeadArgs {
   float* loss;         // [1] batch mean
   // backward
   float* dx;           // [B*q, D]  (zeroed by caller) ← head grads into rows k+m-1 and k+1
+  bf16* dx_bf;         // optional bf16 copy of dx (zeroed by caller), same two rows written
   float *g_w1, *g_b1, *g_w2, *g_b2, *g_uid, *g_prof;
   float* dz1;          // [B, hh] scratch
 };
