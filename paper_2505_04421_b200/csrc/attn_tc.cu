@@ -34,16 +34,47 @@ __device__ __forceinline__ void load_rows_bf16(bf16* tile, const bf16* src, int 
   }
 }
 
+// Query i sits in tile row qrow_of(i) = (i % 4)·32 + i / 4, so the q ≤ 128 queries of a sample are
+// spread over all four TMEM lane quadrants (= all four worker warps) instead of crowding warp 0.
+__device__ __forceinline__ int query_of_row(int row) { return (row & 31) * 4 + (row >> 5); }
+
+// The visible keys of one query row form ONE interval [lo, hi) of the key index (VisRule):
+//   sequence query i < k (group gq = G-k+i): non-pad sequence keys up to its own group;
+//   global query of rank r: every non-pad sequence key, then the globals of rank ≤ r.
+__device__ __forceinline__ void vis_interval(const VisRule& v, int i, int nk, int& lo, int& hi) {
+  lo = max(0, v.npg - v.goff);
+  if (i < v.k) {
+    const int gq = v.G - v.k + i;
+    hi = gq < v.npg ? 0 : min(v.ns, gq - v.goff + 1);
+  } else {
+    hi = v.ns + (i - v.k) + 1;
+  }
+  hi = min(hi, nk);
+  if (hi < lo) hi = lo;
+}
+// bit v set ⇔ key j0 + v ∈ [lo, hi)
+__device__ __forceinline__ uint32_t vis_bits(int lo, int hi, int j0) {
+  const int a = max(lo - j0, 0), b = min(hi - j0, 32);
+  if (b <= a) return 0u;
+  const uint32_t mb = b >= 32 ? 0xffffffffu : ((1u << b) - 1u);
+  return mb & ~((1u << a) - 1u);
+}
+
+// Forward, ONE pass over the key chunks: S = Q·K_cᵀ in TMEM; the workers keep a running max m
+// and sum l per row and write P̃ = exp(s − m) (bf16) over the dead K tile; O += P̃·V_c accumulates
+// in TMEM.  When a chunk raises a row's max by more than kRescale the row's O is rescaled in TMEM
+// (tcgen05.ld/st) — rare after the first chunk; below that threshold P̃ ≤ e^kRescale stays exact
+// enough in bf16 and fp32.  O/l, the fp32 copy and lse = m + log l are written at the end.
+// Shared memory: Q + K|P + V (96 KB at head width 128) → two CTAs per SM.
+constexpr float kRescale = 8.f;
+
 template <int DH>
-__global__ void __launch_bounds__(kThreads, 1) xattn_fwd_kernel(AttnArgs a) {
-  pdl_trigger();
-  pdl_wait();
+__global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   bf16* sQ = reinterpret_cast<bf16*>(smem_raw);
-  bf16* sK = sQ + 128 * DH;
-  bf16* sV = sK + kC * DH;
-  bf16* sP = sV + kC * DH;                        // 128 x kC
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 128 * kC);
+  bf16* sKP = sQ + 128 * DH;                      // K chunk (kC x DH), then P (128 x kC)
+  bf16* sV = sKP + 128 * kC;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kC * DH);
   uint64_t* bar_a = bars;
   uint64_t* bar_d = bars + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
@@ -59,106 +90,122 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_fwd_kernel(AttnArgs a) {
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
   const uint32_t T_S = tmem, T_O = tmem + 128;
   const int nchunk = (a.nk + kC - 1) / kC;
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint32_t aQ = sm100::smem_u32(sQ), aK = sm100::smem_u32(sK), aV = sm100::smem_u32(sV);
-      const uint32_t aP = sm100::smem_u32(sP);
+      const uint32_t aQ = sm100::smem_u32(sQ), aKP = sm100::smem_u32(sKP), aV = sm100::smem_u32(sV);
       uint32_t pa = 0;
       auto wait_a = [&]() { sm100::mbar_wait(bar_a, pa); pa ^= 1; sm100::tc_fence_after(); };
-      for (int c = 0; c < nchunk; ++c) {            // pass 1: S for the statistics
-        wait_a();
-        mma(T_S, Opnd{aQ, DH, 0}, Opnd{aK, DH, 0}, DH / 16, kC, false);
+      for (int c = 0; c < nchunk; ++c) {
+        wait_a();                                   // K_c, V_c staged
+        mma(T_S, Opnd{aQ, DH, 0}, Opnd{aKP, DH, 0}, DH / 16, kC, false);
         sm100::mma_commit(bar_d);
-      }
-      for (int c = 0; c < nchunk; ++c) {            // pass 2: P, O += P·V
-        wait_a();
-        mma(T_S, Opnd{aQ, DH, 0}, Opnd{aK, DH, 0}, DH / 16, kC, false);
-        sm100::mma_commit(bar_d);
-        wait_a();
-        mma(T_O, Opnd{aP, kC, 0}, Opnd{aV, DH, 1}, kC / 16, DH, c > 0);
+        wait_a();                                   // P_c staged (and O rescaled)
+        mma(T_O, Opnd{aKP, kC, 0}, Opnd{aV, DH, 1}, kC / 16, DH, c > 0);
         sm100::mma_commit(bar_d);
       }
     }
   } else {
     const int q = warp & 3;
     const int row = q * 32 + lane;
-    const uint32_t lo = (uint32_t)(q * 32) << 16;
+    const int qi = query_of_row(row);
+    const uint32_t lo_lane = (uint32_t)(q * 32) << 16;
     const float scale = rsqrtf((float)(a.D / a.heads));
     const VisRule vis{a.k, a.G, a.ns, a.goff, a.npg[b]};
+    const bool qrow = qi < a.nq;
+    int vlo = 0, vhi = 0;
+    if (qrow) vis_interval(vis, qi, a.nk, vlo, vhi);
     const bf16* Qb = a.Q + b * a.sq + hd * DH;
     const bf16* Kb = a.Kp + b * a.sk + hd * DH;
     const bf16* Vb = a.V + b * a.sv + hd * DH;
     uint32_t pd = 0;
     auto signal = [&]() { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(bar_a); };
     auto wait_d = [&]() { sm100::mbar_wait(bar_d, pd); pd ^= 1; sm100::tc_fence_after(); };
-    load_rows_bf16<DH>(sQ, Qb, a.ldq, row, a.nq);
-    const bool qrow = row < a.nq;
+#pragma unroll
+    for (int c = 0; c < DH; c += 8) {
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (qrow) v = *reinterpret_cast<const uint4*>(Qb + (long long)qi * a.ldq + c);
+      *reinterpret_cast<uint4*>(sQ + canon(row, c, DH)) = v;
+    }
     float m = -INFINITY, l = 0.f;
     for (int c = 0; c < nchunk; ++c) {
       const int c0 = c * kC;
-      load_rows_bf16<DH>(sK, Kb + (long long)c0 * a.ldk, a.ldk, row, a.nk - c0);
-      signal();
-      wait_d();
-#pragma unroll 1
-      for (int j0 = 0; j0 < kC; j0 += 32) {
-        float s[32];
-        tmem_row<32>(T_S + lo + j0, s);
-        if (!qrow) continue;
-        float cm = -INFINITY;
-#pragma unroll
-        for (int u = 0; u < 32; ++u) {
-          const int key = c0 + j0 + u;
-          s[u] = (key < a.nk && vis(row, key)) ? s[u] * scale : -INFINITY;
-          cm = fmaxf(cm, s[u]);
-        }
-        if (cm == -INFINITY) continue;
-        const float mn = fmaxf(m, cm);
-        float add = 0.f;
-#pragma unroll
-        for (int u = 0; u < 32; ++u) add += __expf(s[u] - mn);
-        l = l * __expf(m - mn) + add;
-        m = mn;
-      }
-    }
-    const float rl = l > 0.f ? 1.f / l : 0.f;
-    for (int c = 0; c < nchunk; ++c) {
-      const int c0 = c * kC;
-      load_rows_bf16<DH>(sK, Kb + (long long)c0 * a.ldk, a.ldk, row, a.nk - c0);
+      load_rows_bf16<DH>(sKP, Kb + (long long)c0 * a.ldk, a.ldk, row, a.nk - c0);
       load_rows_bf16<DH>(sV, Vb + (long long)c0 * a.ldv, a.ldv, row, a.nk - c0);
       signal();
-      wait_d();
+      wait_d();                                     // S_c ready (K tile dead)
+      float cm = -INFINITY;
 #pragma unroll 1
       for (int j0 = 0; j0 < kC; j0 += 32) {
         float s[32];
-        tmem_row<32>(T_S + lo + j0, s);
+        tmem_row<32>(T_S + lo_lane + j0, s);
+        const uint32_t bits = vis_bits(vlo, vhi, c0 + j0);
+        if (bits) {
+#pragma unroll
+          for (int u = 0; u < 32; ++u)
+            if (bits & (1u << u)) cm = fmaxf(cm, s[u]);
+        }
+      }
+      cm *= scale;
+      const bool raise = cm > m + kRescale || (m == -INFINITY && cm != -INFINITY);
+      float factor = 1.f;
+      if (raise) {
+        factor = m == -INFINITY ? 0.f : __expf(m - cm);
+        l *= factor;
+        m = cm;
+      }
+      if (c > 0 && __any_sync(0xffffffffu, raise)) {
+#pragma unroll 1
+        for (int cc = 0; cc < DH; cc += 32) {
+          uint32_t r[32];
+          sm100::tmem_ld32(T_O + lo_lane + cc, r);
+          sm100::tmem_ld_wait();
+#pragma unroll
+          for (int u = 0; u < 32; ++u) r[u] = __float_as_uint(__uint_as_float(r[u]) * factor);
+          sm100::tmem_st32(T_O + lo_lane + cc, r);
+        }
+        sm100::tmem_st_wait();
+      }
+#pragma unroll 1
+      for (int j0 = 0; j0 < kC; j0 += 32) {
+        float s[32];
+        tmem_row<32>(T_S + lo_lane + j0, s);
+        const uint32_t bits = vis_bits(vlo, vhi, c0 + j0);
+        float add = 0.f;
 #pragma unroll
         for (int u = 0; u < 32; ++u) {
-          const int key = c0 + j0 + u;
-          s[u] = (qrow && l > 0.f && key < a.nk && vis(row, key)) ? __expf(s[u] * scale - m) * rl : 0.f;
+          s[u] = (bits & (1u << u)) ? __expf(fmaf(s[u], scale, -m)) : 0.f;
+          add += s[u];
         }
-        store_row(sP, row, kC, s, 32, j0);
+        l += add;
+        store_row(sKP, row, kC, s, 32, j0);
       }
       signal();
-      wait_d();
+      wait_d();                                     // O += P·V done: K|P and V tiles free
     }
     float o[DH];
-    tmem_row<DH>(T_O + lo, o);
+    tmem_row<DH>(T_O + lo_lane, o);
     if (qrow) {
-      bf16* dst = a.ctx + b * a.sc + (long long)row * a.ldc + hd * DH;
-      float* dst32 = a.ctx32 + b * a.sc + (long long)row * a.ldc + hd * DH;
+      const float rl = l > 0.f ? 1.f / l : 0.f;
+      bf16* dst = a.ctx + b * a.sc + (long long)qi * a.ldc + hd * DH;
+      float* dst32 = a.ctx32 + b * a.sc + (long long)qi * a.ldc + hd * DH;
 #pragma unroll
       for (int c = 0; c < DH; c += 8) {
+        float w[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) w[u] = o[c + u] * rl;
         uint4 pk;
-        pk.x = sm100::pack_bf16(o[c], o[c + 1]); pk.y = sm100::pack_bf16(o[c + 2], o[c + 3]);
-        pk.z = sm100::pack_bf16(o[c + 4], o[c + 5]); pk.w = sm100::pack_bf16(o[c + 6], o[c + 7]);
+        pk.x = sm100::pack_bf16(w[0], w[1]); pk.y = sm100::pack_bf16(w[2], w[3]);
+        pk.z = sm100::pack_bf16(w[4], w[5]); pk.w = sm100::pack_bf16(w[6], w[7]);
         *reinterpret_cast<uint4*>(dst + c) = pk;
-        *reinterpret_cast<float4*>(dst32 + c) = make_float4(o[c], o[c + 1], o[c + 2], o[c + 3]);
-        *reinterpret_cast<float4*>(dst32 + c + 4) = make_float4(o[c + 4], o[c + 5], o[c + 6], o[c + 7]);
+        *reinterpret_cast<float4*>(dst32 + c) = make_float4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<float4*>(dst32 + c + 4) = make_float4(w[4], w[5], w[6], w[7]);
       }
-      a.lse[((long long)b * a.heads + hd) * a.nq + row] = l > 0.f ? m + __logf(l) : -INFINITY;
+      a.lse[((long long)b * a.heads + hd) * a.nq + qi] = l > 0.f ? m + __logf(l) : -INFINITY;
     }
   }
   sm100::tc_fence_before();
@@ -334,10 +381,10 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
 
 template <int DH>
 int launch_fwd(const AttnArgs& a, cudaStream_t st) {
-  const int smem = (128 * DH + 2 * kC * DH + 128 * kC) * 2 + 64;
+  const int smem = (128 * DH + 128 * kC + kC * DH) * 2 + 64;
   static int done = 0;
   if (!done) { cudaFuncSetAttribute(xattn_fwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); done = 1; }
-  launch(xattn_fwd_kernel<DH>, a.B * a.heads, kThreads, std::max(smem, 116 * 1024), st, a);
+  launch(xattn_fwd_kernel<DH>, a.B * a.heads, kThreads, std::max(smem, 80 * 1024), st, a);
   return (int)cudaGetLastError();
 }
 
