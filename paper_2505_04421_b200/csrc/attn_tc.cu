@@ -215,8 +215,6 @@ __global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a) {
 
 template <int DH>
 __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
-  pdl_trigger();
-  pdl_wait();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   bf16* sQ = reinterpret_cast<bf16*>(smem_raw);
   bf16* sdO = sQ + 128 * DH;
@@ -240,6 +238,8 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
   const uint32_t T_A = tmem, T_B = tmem + 128, T_DQ = tmem + 256;
   const int nchunk = (a.nk + kC - 1) / kC;
 
@@ -279,21 +279,34 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
     uint32_t pd = 0;
     auto signal = [&]() { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(bar_a); };
     auto wait_d = [&]() { sm100::mbar_wait(bar_d, pd); pd ^= 1; sm100::tc_fence_after(); };
-    const bool qrow = row < a.nq;
-    load_rows_bf16<DH>(sQ, Qb, a.ldq, row, a.nq);
+    const int qi = query_of_row(row);
+    const bool qrow = qi < a.nq;
+#pragma unroll
+    for (int c = 0; c < DH; c += 8) {
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (qrow) v = *reinterpret_cast<const uint4*>(Qb + (long long)qi * a.ldq + c);
+      *reinterpret_cast<uint4*>(sQ + canon(row, c, DH)) = v;
+    }
     // dO (fp32) → bf16 tile
     float Di = 0.f, lse = -INFINITY;
     {
-      const float* dOr = a.dctx + b * a.sdc + (long long)row * a.lddc + hd * DH;
+      const float* dOr = a.dctx + b * a.sdc + (long long)qi * a.lddc + hd * DH;
 #pragma unroll
       for (int c = 0; c < DH; c += 8) {
         float v[8];
+        if (qrow) {
+          const float4 x = *reinterpret_cast<const float4*>(dOr + c), y = *reinterpret_cast<const float4*>(dOr + c + 4);
+          v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w; v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+        } else {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = qrow ? dOr[c + u] : 0.f;
+          for (int u = 0; u < 8; ++u) v[u] = 0.f;
+        }
         store_row(sdO, row, DH, v, 8, c);
       }
-      if (qrow) lse = a.lse[((long long)b * a.heads + hd) * a.nq + row];
+      if (qrow) lse = a.lse[((long long)b * a.heads + hd) * a.nq + qi];
     }
+    int vlo = 0, vhi = 0;
+    if (qrow && lse != -INFINITY) vis_interval(vis, qi, a.nk, vlo, vhi);
     // pass 1: D_i = Σ_j P_ij dP_ij with exactly the P and dP of pass 2, so that Σ_j dS_ij = 0
     // holds to rounding (D = rowsum(dO ⊙ O) would mix the bf16 roundings of dO, P and V).
     for (int c = 0; c < nchunk; ++c) {
@@ -307,11 +320,11 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
         float s[32], dp[32];
         tmem_row<32>(T_A + lo + j0, s);
         tmem_row<32>(T_B + lo + j0, dp);
+        const uint32_t bits = vis_bits(vlo, vhi, c0 + j0);
+        if (bits) {
 #pragma unroll
-        for (int u = 0; u < 32; ++u) {
-          const int key = c0 + j0 + u;
-          const bool ok = qrow && lse != -INFINITY && key < a.nk && vis(row, key);
-          if (ok) Di = fmaf(__expf(s[u] * scale - lse), dp[u], Di);
+          for (int u = 0; u < 32; ++u)
+            if (bits & (1u << u)) Di = fmaf(__expf(fmaf(s[u], scale, -lse)), dp[u], Di);
         }
       }
     }
@@ -326,11 +339,10 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
         float s[32], dp[32];
         tmem_row<32>(T_A + lo + j0, s);
         tmem_row<32>(T_B + lo + j0, dp);
+        const uint32_t bits = vis_bits(vlo, vhi, c0 + j0);
 #pragma unroll
         for (int u = 0; u < 32; ++u) {
-          const int key = c0 + j0 + u;
-          const bool ok = qrow && lse != -INFINITY && key < a.nk && vis(row, key);
-          const float p = ok ? __expf(s[u] * scale - lse) : 0.f;
+          const float p = (bits & (1u << u)) ? __expf(fmaf(s[u], scale, -lse)) : 0.f;
           s[u] = p;
           dp[u] = p * (dp[u] - Di) * scale;
         }
@@ -364,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
     float dq[DH];
     tmem_row<DH>(T_DQ + lo, dq);
     if (qrow) {
-      bf16* pq = a.dQ + b * a.sdq + (long long)row * a.lddq + hd * DH;
+      bf16* pq = a.dQ + b * a.sdq + (long long)qi * a.lddq + hd * DH;
 #pragma unroll
       for (int cc = 0; cc < DH; cc += 8) {
         uint4 x;

@@ -122,8 +122,6 @@ __device__ __forceinline__ void load_blob(uint8_t* dst_smem, const uint8_t* src,
 // ------------------------------------------------------------------ forward kernel
 template <int DT, int KG>
 __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
-  pdl_trigger();
-  pdl_wait();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   constexpr int D = DT * KG;
   constexpr int H2 = 2 * D;                        // token-MLP hidden width
@@ -152,6 +150,8 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
   const long long ntiles = (a.T + kTile - 1) / kTile;
 
   if (warp == 0) {
@@ -366,7 +366,6 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
 // the abs-pos rows are loaded once and their gradient accumulates in shared memory.
 template <int DT>
 __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
-  pdl_trigger();
   pdl_wait();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   const int Dm = DT * a.K;
@@ -424,6 +423,7 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
   // TMEM columns
   const uint32_t T_DW2 = tmem;                         // nh x DT
   const uint32_t T_DW1 = tmem + nh * DT;               // nh x XK

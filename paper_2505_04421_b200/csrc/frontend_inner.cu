@@ -19,8 +19,6 @@ namespace {
 
 template <int DT, int KG>
 __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) {
-  pdl_trigger();
-  pdl_wait();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   constexpr int XK = DT + 16;                 // activation rows carrying a ones column
   constexpr int F4 = 4 * DT;
@@ -68,6 +66,8 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
   const uint32_t T_DW2 = tmem;                // F4 rows x DT
   const uint32_t T_DW1 = tmem + 32;           // F4 rows x XK   ([dW1ᵀ | db1])
   const uint32_t T_DWO = tmem + 80;           // DT rows x XK   ([dWoᵀ | dbo])

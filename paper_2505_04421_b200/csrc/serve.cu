@@ -98,8 +98,6 @@ void target_rows(const TargetArgs& a, cudaStream_t st) {
 // Exact two-pass softmax; S = Q·K_cacheᵀ on the tensor core (TMEM), the own key in registers.
 template <int DH>
 __global__ void __launch_bounds__(kThreads, 1) serve_attn_kernel(ServeAttnArgs a) {
-  pdl_trigger();
-  pdl_wait();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   constexpr int kC = 128;
   bf16* sQ = reinterpret_cast<bf16*>(smem_raw);
@@ -125,6 +123,8 @@ __global__ void __launch_bounds__(kThreads, 1) serve_attn_kernel(ServeAttnArgs a
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
   const uint32_t T_S = tmem, T_O = tmem + 128;
   const int nchunk = (a.nk + kC - 1) / kC;
   if (warp == 0) {
