@@ -137,6 +137,22 @@ __device__ __forceinline__ void ln_row(const float* x, const float* g, const flo
 
 // Column sums of a warp's 32 rows: on return lane c holds Σ_rows v[c] (c < W; W ∈ {16, 32}).
 // Recursive halving, 31 shuffles for W = 32.
+// ln_row with the gain / bias vectors in shared memory (plain loads; ln_row uses the read-only path)
+template <int DT>
+__device__ __forceinline__ void ln_row_s(const float* x, const float* g, const float* b, float* y, float& inv_out) {
+  float mu = 0.f;
+#pragma unroll
+  for (int c = 0; c < DT; ++c) mu += x[c];
+  mu *= 1.f / DT;
+  float var = 0.f;
+#pragma unroll
+  for (int c = 0; c < DT; ++c) { const float t = x[c] - mu; var += t * t; }
+  const float inv = rsqrtf(var * (1.f / DT) + kLnEps);
+  inv_out = inv;
+#pragma unroll
+  for (int c = 0; c < DT; ++c) y[c] = (x[c] - mu) * inv * g[c] + b[c];
+}
+
 template <int W>
 __device__ __forceinline__ float warp_colsum(float (&v)[W]) {
   const int lane = threadIdx.x & 31;

@@ -119,20 +119,43 @@ __device__ __forceinline__ void load_blob(uint8_t* dst_smem, const uint8_t* src,
   }
 }
 
+// InnerTrans k|v scratch: row r holds [k | v] (2·DT bf16) as 16-byte chunks, chunk index XOR-ed
+// with the row so that the group peers' rows (same chunk, consecutive rows) hit distinct banks.
+template <int DT>
+__device__ __forceinline__ void kv_store(bf16* skv, int row, const float* kv) {
+  constexpr int CPR = 2 * DT / 8;
+#pragma unroll
+  for (int ch = 0; ch < CPR; ++ch) {
+    uint4 w;
+    w.x = sm100::pack_bf16(kv[8 * ch], kv[8 * ch + 1]); w.y = sm100::pack_bf16(kv[8 * ch + 2], kv[8 * ch + 3]);
+    w.z = sm100::pack_bf16(kv[8 * ch + 4], kv[8 * ch + 5]); w.w = sm100::pack_bf16(kv[8 * ch + 6], kv[8 * ch + 7]);
+    *reinterpret_cast<uint4*>(skv + row * 2 * DT + ((ch ^ (row % CPR)) * 8)) = w;
+  }
+}
+template <int DT>
+__device__ __forceinline__ void kv_load8(const bf16* skv, int row, int col, float* out) {
+  constexpr int CPR = 2 * DT / 8;
+  const uint4 w = *reinterpret_cast<const uint4*>(skv + row * 2 * DT + (((col / 8) ^ (row % CPR)) * 8));
+  out[0] = sm100::bf16_lo(w.x); out[1] = sm100::bf16_hi(w.x); out[2] = sm100::bf16_lo(w.y); out[3] = sm100::bf16_hi(w.y);
+  out[4] = sm100::bf16_lo(w.z); out[5] = sm100::bf16_hi(w.z); out[6] = sm100::bf16_lo(w.w); out[7] = sm100::bf16_hi(w.w);
+}
+
 // ------------------------------------------------------------------ forward kernel
 template <int DT, int KG>
 __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   constexpr int D = DT * KG;
   constexpr int H2 = 2 * D;                        // token-MLP hidden width
-  constexpr int nh = H2 / 128;                     // 128-column halves of the hidden
+  constexpr int nh = H2 / 64;                      // 64-column parts of the hidden
+  constexpr int nf = 4 * DT / 64;                  // 64-column parts of the InnerTrans FFN hidden
   constexpr int XK = DT + 16;                      // activation tile row: [x | 1 | 0…] (bias column)
   const BlobOff bo = blob_offsets(DT, D, a.inner_layers);
   bf16* sW = reinterpret_cast<bf16*>(smem_raw);
   bf16* sA = sW + ((bo.fwd_total + 63) & ~63);             // 128 x XK bf16 (feat uses 128 x 32)
-  bf16* sH = sA + kTile * XK;                              // 128 x 128 bf16 (also fp32 k/v scratch)
-  float* sKV = reinterpret_cast<float*>(sH);               // 128 x (2*DT+1) fp32
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sH + kTile * 136);
+  bf16* sH = sA + kTile * XK;                              // 128 x 64 bf16 hidden part (also k|v scratch)
+  bf16* sKV = sH;                                          // 128 x 2DT bf16, 16-byte chunks XOR-swizzled
+  float* s_par = reinterpret_cast<float*>(sH + kTile * 64);   // [IL][ln1_g, ln1_b, b_o, ln2_g, ln2_b, b2][DT]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_par + a.inner_layers * 6 * DT);
   uint64_t* bar_w = bars;
   uint64_t* bar_a = bars + 1;
   uint64_t* bar_d = bars + 2;
@@ -152,6 +175,13 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
   const uint32_t tmem = *tmem_slot;
   pdl_trigger();
   pdl_wait();
+  for (int i = threadIdx.x; i < a.inner_layers * 6 * DT; i += blockDim.x) {
+    const int l = i / (6 * DT), v = (i / DT) % 6, c = i % DT;
+    const float* src = v == 0 ? a.inner_ln[l][0] : v == 1 ? a.inner_ln[l][1] : v == 2 ? a.inner_bias[l][3]
+                     : v == 3 ? a.inner_ln[l][2] : v == 4 ? a.inner_ln[l][3] : a.inner_bias[l][5];
+    s_par[i] = src[c];
+  }
+  __syncthreads();
   const long long ntiles = (a.T + kTile - 1) / kTile;
 
   if (warp == 0) {
@@ -170,12 +200,12 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
         mma(tmem, Opnd{wA, kFP, 0}, W(bo.tp, kFP), kFP / 16, DT, false);
         sm100::mma_commit(bar_d);
         wait_a();                                // [x0 | 1]
-        mma(tmem, Opnd{wA, XK, 0}, W(bo.w1, XK), XK / 16, 128, false);
+        mma(tmem, Opnd{wA, XK, 0}, W(bo.w1, XK), XK / 16, 64, false);
         sm100::mma_commit(bar_d);
         for (int j = 0; j < nh; ++j) {
-          wait_a();                              // GELU(a1 half j) in sH
-          mma(accH, Opnd{wH, 128, 0}, W(bo.w2 + canon(0, 128 * j, H2), H2), 8, DT, j > 0);
-          if (j + 1 < nh) mma(tmem, Opnd{wA, XK, 0}, W(bo.w1 + canon(128 * (j + 1), 0, XK), XK), XK / 16, 128, false);
+          wait_a();                              // GELU(a1 part j) in sH
+          mma(accH, Opnd{wH, 64, 0}, W(bo.w2 + canon(0, 64 * j, H2), H2), 4, DT, j > 0);
+          if (j + 1 < nh) mma(tmem, Opnd{wA, XK, 0}, W(bo.w1 + canon(64 * (j + 1), 0, XK), XK), XK / 16, 64, false);
           sm100::mma_commit(bar_d);
         }
         for (int l = 0; l < a.inner_layers; ++l) {
@@ -186,11 +216,14 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
           mma(tmem, Opnd{wA, XK, 0}, W(bo.wo[l], DT), DT / 16, DT, false);
           sm100::mma_commit(bar_d);
           wait_a();                              // [LN2(x1) | 1]
-          mma(tmem, Opnd{wA, XK, 0}, W(bo.w1i[l], XK), XK / 16, 4 * DT, false);
+          mma(tmem, Opnd{wA, XK, 0}, W(bo.w1i[l], XK), XK / 16, 64, false);
           sm100::mma_commit(bar_d);
-          wait_a();                              // GELU(f1)
-          mma(accH, Opnd{wH, 4 * DT, 0}, W(bo.w2i[l], 4 * DT), 4 * DT / 16, DT, false);
-          sm100::mma_commit(bar_d);
+          for (int j = 0; j < nf; ++j) {
+            wait_a();                            // GELU(f1 part j) in sH
+            mma(accH, Opnd{wH, 64, 0}, W(bo.w2i[l] + canon(0, 64 * j, 4 * DT), 4 * DT), 4, DT, j > 0);
+            if (j + 1 < nf) mma(tmem, Opnd{wA, XK, 0}, W(bo.w1i[l] + canon(64 * (j + 1), 0, XK), XK), XK / 16, 64, false);
+            sm100::mma_commit(bar_d);
+          }
         }
       }
     }
@@ -241,16 +274,16 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
       for (int c = DT; c < XK; ++c) x[c] = c == DT ? 1.f : 0.f;
       store_row(sA, row, XK, x, XK);
       signal();
-      // token MLP: GELU([x0 | 1]·[W1 ; b1]) (128-column halves → sH) · W2 accumulates in TMEM
+      // token MLP: GELU([x0 | 1]·[W1 ; b1]) (64-column parts → sH) · W2 accumulates in TMEM
       for (int hj = 0; hj < nh; ++hj) {
         wait_d();
-#pragma unroll 1
-        for (int c0 = 0; c0 < 128; c0 += 32) {
+#pragma unroll
+        for (int c0 = 0; c0 < 64; c0 += 32) {
           float hv[32];
           tmem_row<32>(trow + c0, hv);
 #pragma unroll
           for (int u = 0; u < 32; ++u) hv[u] = gelu_f(hv[u]);
-          store_row(sH, row, 128, hv, 32, c0);
+          store_row(sH, row, 64, hv, 32, c0);
         }
         signal();
       }
@@ -265,10 +298,9 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
         for (int c = 0; c < DT; c += 4) dst[c / 4] = make_float4(h[c], h[c + 1], h[c + 2], h[c + 3]);
       }
       for (int l = 0; l < a.inner_layers; ++l) {
-        const float* const* ib = a.inner_bias[l];
-        const float* const* ln = a.inner_ln[l];
+        const float* par = s_par + l * 6 * DT;
         float xn[XK], inv;
-        ln_row<DT>(h, ln[0], ln[1], xn, nullptr, inv);
+        ln_row_s<DT>(h, par, par + DT, xn, inv);
 #pragma unroll
         for (int c = DT; c < XK; ++c) xn[c] = c == DT ? 1.f : 0.f;
         store_row(sA, row, XK, xn, XK);
@@ -277,13 +309,10 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
         float qv[DT];
         tmem_row<DT>(trow, qv);                    // q, k, v already carry their biases
         {
-          float kv[DT];
+          float kv[2 * DT];
           tmem_row<DT>(trow + DT, kv);
-#pragma unroll
-          for (int c = 0; c < DT; ++c) sKV[row * (2 * DT + 1) + c] = kv[c];
-          tmem_row<DT>(trow + 2 * DT, kv);
-#pragma unroll
-          for (int c = 0; c < DT; ++c) sKV[row * (2 * DT + 1) + DT + c] = kv[c];
+          tmem_row<DT>(trow + 2 * DT, kv + DT);
+          kv_store<DT>(sKV, row, kv);
         }
         __syncwarp();
         const int g0 = row - row % KG;
@@ -293,7 +322,12 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
         for (int jj = 0; jj < KG; ++jj) {
           float acc = 0.f;
 #pragma unroll
-          for (int c = 0; c < DT; ++c) acc = fmaf(qv[c], sKV[(g0 + jj) * (2 * DT + 1) + c], acc);
+          for (int c = 0; c < DT; c += 8) {
+            float kk[8];
+            kv_load8<DT>(sKV, g0 + jj, c, kk);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = fmaf(qv[c + u], kk[u], acc);
+          }
           s[jj] = acc * scale_in;
           mx = fmaxf(mx, s[jj]);
         }
@@ -303,12 +337,19 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
         const float rinv = 1.f / tot;
         float ctx[XK];
 #pragma unroll
-        for (int c = 0; c < DT; ++c) {
-          float acc = 0.f;
+        for (int c = 0; c < DT; ++c) ctx[c] = 0.f;
 #pragma unroll
-          for (int jj = 0; jj < KG; ++jj) acc = fmaf(s[jj], sKV[(g0 + jj) * (2 * DT + 1) + DT + c], acc);
-          ctx[c] = acc * rinv;
+        for (int jj = 0; jj < KG; ++jj) {
+#pragma unroll
+          for (int c = 0; c < DT; c += 8) {
+            float vv[8];
+            kv_load8<DT>(sKV, g0 + jj, DT + c, vv);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) ctx[c + u] = fmaf(s[jj], vv[u], ctx[c + u]);
+          }
         }
+#pragma unroll
+        for (int c = 0; c < DT; ++c) ctx[c] *= rinv;
 #pragma unroll
         for (int c = DT; c < XK; ++c) ctx[c] = 0.f;
         __syncwarp();
@@ -318,26 +359,28 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
         float o[DT];
         tmem_row<DT>(trow, o);
 #pragma unroll
-        for (int c = 0; c < DT; ++c) h[c] += o[c] + __ldg(ib[3] + c);       // x1
-        ln_row<DT>(h, ln[2], ln[3], xn, nullptr, inv);
+        for (int c = 0; c < DT; ++c) h[c] += o[c] + par[2 * DT + c];      // x1
+        ln_row_s<DT>(h, par + 3 * DT, par + 4 * DT, xn, inv);
 #pragma unroll
         for (int c = DT; c < XK; ++c) xn[c] = c == DT ? 1.f : 0.f;
         store_row(sA, row, XK, xn, XK);
         signal();
-        wait_d();
-#pragma unroll 1
-        for (int c0 = 0; c0 < 4 * DT; c0 += 32) {
-          float hv[32];
-          tmem_row<32>(trow + c0, hv);
+        for (int fj = 0; fj < nf; ++fj) {
+          wait_d();
 #pragma unroll
-          for (int u = 0; u < 32; ++u) hv[u] = gelu_f(hv[u]);
-          store_row(sH, row, 4 * DT, hv, 32, c0);
+          for (int c0 = 0; c0 < 64; c0 += 32) {
+            float hv[32];
+            tmem_row<32>(trow + c0, hv);
+#pragma unroll
+            for (int u = 0; u < 32; ++u) hv[u] = gelu_f(hv[u]);
+            store_row(sH, row, 64, hv, 32, c0);
+          }
+          signal();
         }
-        signal();
         wait_d();
         tmem_row<DT>(trow + 128, o);
 #pragma unroll
-        for (int c = 0; c < DT; ++c) h[c] += o[c] + __ldg(ib[5] + c);       // x2
+        for (int c = 0; c < DT; ++c) h[c] += o[c] + par[5 * DT + c];      // x2
       }
       if (a.inner_layers > 0 && !ti.keep) {
 #pragma unroll
@@ -705,7 +748,8 @@ void pack_frontend_weights(const float* params, long long tok_w, long long seq_w
 template <int DT, int KG>
 static int launch_fwd(const FrontArgs& a, cudaStream_t st) {
   const BlobOff bo = blob_offsets(DT, DT * KG, a.inner_layers);
-  const int smem = ((bo.fwd_total + 63) & ~63) * 2 + kTile * std::max(DT + 16, kFP) * 2 + kTile * 136 * 2 + 64;
+  const int smem = ((bo.fwd_total + 63) & ~63) * 2 + kTile * std::max(DT + 16, kFP) * 2 + kTile * 64 * 2 +
+                   a.inner_layers * 6 * DT * 4 + 64;
   static int done = 0;
   if (!done) {
     cudaFuncSetAttribute(fe_fwd_kernel<DT, KG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
