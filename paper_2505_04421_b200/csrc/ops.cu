@@ -273,16 +273,39 @@ __global__ void ln_bwd_kernel(RowMap x, int W, const float* __restrict__ g, cons
     const int c = ln_col<VPT, CONTIG>(lane, u);
     gv[u] = c < W ? g[c] : 0.f;
   }
-  for (int row = blockIdx.x * warps + wid; row < rows; row += gridDim.x * warps) {
+  // software-pipelined over the warp's rows: every input of row r + stride is loaded before row r
+  // is reduced and stored, so each warp keeps two rows of loads in flight
+  struct RowIn {
+    float x[VPT], dy[VPT], o[VPT], ad[VPT];
+    float mu, inv, rm;
+    float* dst;
+  };
+  auto load_row = [&](int row, RowIn& R) {
     const int b = row / per, j = row % per;
     const float* src = j < x.na ? x.A + (long long)(b * x.a_rows + x.a_off + j) * x.lda
                                 : x.Bsrc + (long long)(b * x.nb + j - x.na) * x.ldb;
-    float* dst = j < out.na ? out.A + (long long)(b * out.a_rows + out.a_off + j) * out.lda
-                            : out.Bsrc + (long long)(b * out.nb + j - out.na) * out.ldb;
-    const float mu = mean[row], inv = rstd[row];
+    R.dst = j < out.na ? out.A + (long long)(b * out.a_rows + out.a_off + j) * out.lda
+                       : out.Bsrc + (long long)(b * out.nb + j - out.na) * out.ldb;
+    R.mu = mean[row];
+    R.inv = rstd[row];
+    R.rm = rowmask ? rowmask[row] : 1.f;
+    ln_load<VPT, CONTIG>(src, lane, W, R.x);
+    ln_load<VPT, CONTIG>(dy + (long long)row * ldy, lane, W, R.dy);
+    if (accumulate) ln_load<VPT, CONTIG>(R.dst, lane, W, R.o);
+    if (ex.addend) ln_load<VPT, CONTIG>(ex.addend + (long long)row * W, lane, W, R.ad);
+  };
+  const int stride = gridDim.x * warps;
+  int row = blockIdx.x * warps + wid;
+  RowIn cur;
+  if (row < rows) load_row(row, cur);
+  for (; row < rows; row += stride) {
+    RowIn nxt;
+    if (row + stride < rows) load_row(row + stride, nxt);
+    const float mu = cur.mu, inv = cur.inv, rm = cur.rm;
+    float* dst = cur.dst;
     float xh[VPT], gh[VPT], dyv[VPT];
-    ln_load<VPT, CONTIG>(src, lane, W, xh);
-    ln_load<VPT, CONTIG>(dy + (long long)row * ldy, lane, W, dyv);
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) { xh[u] = cur.x[u]; dyv[u] = cur.dy[u]; }
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int u = 0; u < VPT; ++u) {
@@ -299,15 +322,12 @@ __global__ void ln_bwd_kernel(RowMap x, int W, const float* __restrict__ g, cons
       s2 += gh[u] * xh[u];
     }
     const float m1 = warp_sum(s1) / W, m2 = warp_sum(s2) / W;
-    const float rm = rowmask ? rowmask[row] : 1.f;
-    float o[VPT], ad[VPT];
-    if (accumulate) ln_load<VPT, CONTIG>(dst, lane, W, o);
-    if (ex.addend) ln_load<VPT, CONTIG>(ex.addend + (long long)row * W, lane, W, ad);
+    float o[VPT];
 #pragma unroll
     for (int u = 0; u < VPT; ++u) {
       float v = (gh[u] - m1 - xh[u] * m2) * inv;
-      if (accumulate) v += o[u];
-      if (ex.addend) v += ad[u];
+      if (accumulate) v += cur.o[u];
+      if (ex.addend) v += cur.ad[u];
       o[u] = v * rm;
       pc[u] += o[u];
     }
@@ -342,6 +362,7 @@ __global__ void ln_bwd_kernel(RowMap x, int W, const float* __restrict__ g, cons
         if (c < W) dst[c] = o[u];
       }
     }
+    cur = nxt;
   }
   if (dgain || ex.colsum_out) {
 #pragma unroll
@@ -1035,8 +1056,30 @@ constexpr int kHeadWarps = 8;
 // hidden units (forward) and lanes over inputs (backward).
 __device__ __forceinline__ void stage_w1(const float* __restrict__ w1, int HIN, int hh, float* s_w) {
   const int n = HIN * hh;
+  if ((reinterpret_cast<uintptr_t>(w1) & 15) == 0 && (hh & 3) == 0) {
+    // 16-byte loads, eight in flight per thread before their (scalar, padded-stride) stores
+    const int n4 = n / 4;
+    for (int e0 = threadIdx.x; e0 < n4; e0 += 8 * blockDim.x) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * blockDim.x;
+        if (e < n4) v[u] = __ldg(reinterpret_cast<const float4*>(w1) + e);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * blockDim.x;
+        if (e < n4) {
+          const int i = (4 * e) / hh, j = (4 * e) % hh;
+          float* d = s_w + i * (hh + 1) + j;
+          d[0] = v[u].x; d[1] = v[u].y; d[2] = v[u].z; d[3] = v[u].w;
+        }
+      }
+    }
+  } else {
 #pragma unroll 8
-  for (int e = threadIdx.x; e < n; e += blockDim.x) s_w[(e / hh) * (hh + 1) + e % hh] = __ldg(w1 + e);
+    for (int e = threadIdx.x; e < n; e += blockDim.x) s_w[(e / hh) * (hh + 1) + e % hh] = __ldg(w1 + e);
+  }
   __syncthreads();
 }
 
