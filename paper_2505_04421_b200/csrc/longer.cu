@@ -483,13 +483,9 @@ int block_fwd(const Ctx& c, const BlockOff& bo, BlockBufs& b, const float* xq, b
   a.nq = p.q; a.D = D; a.heads = p.heads; a.k = p.k; a.G = p.G; a.npg = p.npg; a.B = p.B;
   a.ctx = b.ctx; a.ldc = D; a.sc = (long long)p.q * D; a.lse = b.lse; a.ctx32 = b.ctx32;
   if (cross) {
-    // R = [merged; globals] → LN1 (same ln1 params) → [K | V] projection over all v rows
-    RowMap r{};
-    r.A = p.merged; r.lda = D; r.a_rows = p.G; r.a_off = 0; r.na = p.G; r.Bsrc = p.glob; r.ldb = D; r.nb = p.m;
-    r.batch = p.B;
-    layernorm_fwd(r, D, c.w(bo.ln1_g), c.w(bo.ln1_b), p.kn, p.mk, p.rk, st);
+    // K/V rows: LN1 + [K | V] projection were forked onto the side stream by forward()
     TRY(lin_fwd(st, b.qn, D, Q, Wqkv, D, D, c.w(bo.b_q), 0, nullptr, b.qkv, nullptr));
-    TRY(lin_fwd(st, p.kn, D, (long long)p.B * p.v, p.pk.c_wkv, D, 2 * D, p.pk.c_bkv, 0, nullptr, p.KV, nullptr));
+    join_side(st, side_stream(st));
     a.Q = b.qkv; a.ldq = D; a.sq = (long long)p.q * D;
     a.Kp = p.KV; a.ldk = 2 * D; a.sk = (long long)p.v * 2 * D;
     a.V = p.KV + D; a.ldv = 2 * D; a.sv = (long long)p.v * 2 * D;
@@ -628,6 +624,17 @@ int forward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs, fl
   TRY(lin_fwd(st, p.raw_bf, D, M, p.pk.glob_w1, D, 2 * D, c.w(o.glob_b1), EPI_GELU | EPI_SAVE_PRE, nullptr, p.gg, p.ga));
   TRY(lin_fwd(st, p.gg, 2 * D, M, p.pk.glob_w2, 2 * D, D, c.w(o.glob_b2), 0, p.glob, nullptr, nullptr));
   // composite queries O = [merged[G-k:]; globals] (model.py:317-319)
+  {
+    // R = [merged; globals] → cross LN1 → [K | V] over all B·v rows, on the side stream while the
+    // main stream builds the q query rows (joined in block_fwd before the attention)
+    const cudaStream_t ss = side_stream(st);
+    fork_side(st, ss);
+    RowMap r{};
+    r.A = p.merged; r.lda = D; r.a_rows = p.G; r.a_off = 0; r.na = p.G; r.Bsrc = p.glob; r.ldb = D; r.nb = p.m;
+    r.batch = p.B;
+    layernorm_fwd(r, D, c.w(o.cross.ln1_g), c.w(o.cross.ln1_b), p.kn, p.mk, p.rk, ss);
+    TRY(lin_fwd(ss, p.kn, D, (long long)p.B * p.v, p.pk.c_wkv, D, 2 * D, p.pk.c_bkv, 0, nullptr, p.KV, nullptr));
+  }
   gather_rows_f32(p.merged, p.B, p.G, p.G - p.k, p.k, p.O, p.q, 0, D, st);
   gather_rows_f32(p.glob, p.B, p.m, 0, p.m, p.O, p.q, p.k, D, st);
   Plan& pm = const_cast<Plan&>(p);
