@@ -335,8 +335,12 @@ def main():
         achieved = value / world * fps / 1e12
         pf = phase_flops(cfg, B)
         dom = max(phase_ms, key=lambda k: phase_ms[k]) if phase_ms else None
-        kernels = {}
+        kernels, sections = {}, {}
         for k, tms in phase_ms.items():
+            if k not in pf:
+                if tms > 0:
+                    sections[k] = {"ms": tms / args.steps, "share_of_step": tms / args.steps / ms_step}
+                continue
             if tms > 0:
                 avg = tms / args.steps
                 kernels[k] = {"ms_per_launch": avg, "tflops": pf[k] / (avg / 1e3) / 1e12,
@@ -366,6 +370,7 @@ def main():
                               "scope": "whole step, algorithmic FLOPs = 6 x analysis.muladds_full_forward/sample",
                               "frac_of_sustained": achieved / sustained if sustained else None},
             "kernels": kernels,
+            "sections": sections,
             "gpu_launches": (n_ours * args.steps) if n_ours is not None else None,
             "gpu_launches_per_step": {"ours": n_ours, "torch_or_nccl": n_other},
             "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d_bytes,

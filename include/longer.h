@@ -112,7 +112,8 @@ int longer_cache_score(const LongerDims* dims, const float* params, const void* 
 /* Diagnostics: record caller-owned CUDA events (cudaEvent_t) immediately before / after one fused
  * kernel of subsequent calls, on the call's stream (graph-capturable).  phase: 0 front-end forward,
  * 1 InnerTrans backward, 2 token-MLP/featuriser backward, 3 cross-attention forward,
- * 4 cross-attention backward.  Null events disable the probe. */
+ * 4 cross-attention backward; sections: 5 forward after the front-end (globals, blocks, head),
+ * 6 backward before the front-end (head, blocks, globals).  Null events disable the probe. */
 int longer_set_probe(int32_t phase, void* ev_begin, void* ev_end);
 
 #ifdef __cplusplus

@@ -24,7 +24,8 @@ SYMBOLS = ("longer_param_count", "longer_workspace_bytes", "longer_forward", "lo
            "longer_adam_step", "longer_read_status", "longer_last_error", "longer_set_probe",
            "longer_cache_bytes", "longer_cache_build", "longer_score_workspace_bytes", "longer_cache_score")
 
-PROBES = {"fe_fwd": 0, "fe_inner_bwd": 1, "fe_mlp_bwd": 2, "xattn_fwd": 3, "xattn_bwd": 4}
+PROBES = {"fe_fwd": 0, "fe_inner_bwd": 1, "fe_mlp_bwd": 2, "xattn_fwd": 3, "xattn_bwd": 4,
+          "fwd_rows": 5, "bwd_rows": 6}   # the last two bracket sections, not single kernels
 
 
 class LongerDims(ctypes.Structure):

@@ -27,7 +27,8 @@ thread_local std::string g_err;
 
 // Timing probes (longer_set_probe): optional CUDA events recorded around the fused kernels, on the
 // launching stream (graph-capturable), so callers can time one kernel inside a whole step.
-enum Phase { PH_FE_FWD = 0, PH_FE_INNER_BWD = 1, PH_FE_MLP_BWD = 2, PH_XATTN_FWD = 3, PH_XATTN_BWD = 4, PH_N = 5 };
+enum Phase { PH_FE_FWD = 0, PH_FE_INNER_BWD = 1, PH_FE_MLP_BWD = 2, PH_XATTN_FWD = 3, PH_XATTN_BWD = 4,
+             PH_FWD_ROWS = 5, PH_BWD_ROWS = 6, PH_N = 7 };
 cudaEvent_t g_probe[PH_N][2] = {};
 
 void probe(int ph, int which, cudaStream_t st) {
@@ -610,6 +611,7 @@ int forward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs, fl
   TRY(pack_weights(p, c.P, p.ws, st));
   if (p.fused_fe) {
     probe(PH_FE_FWD, 0, c.st); TRY(frontend_fused_fwd(c, p, bt)); probe(PH_FE_FWD, 1, c.st);
+    probe(PH_FWD_ROWS, 0, c.st);
   } else {
     TRY(frontend_unfused_fwd(c, p, bt));
   }
@@ -653,6 +655,7 @@ int forward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs, fl
   h.hin = p.hin; h.z1 = p.z1; h.probs = probs;
   h.loss_per = with_loss ? p.loss_per : nullptr; h.dz = p.dz; h.loss = loss;
   head_fwd(h, with_loss, st);
+  if (p.fused_fe) probe(PH_FWD_ROWS, 1, st);
   TRY((int)cudaGetLastError());
   return 0;
 }
@@ -764,6 +767,7 @@ int backward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs) {
   const long long T = p.T, M = (long long)p.B * p.m, Q = (long long)p.B * p.q;
   const cudaStream_t ss = side_stream(st);
   const BlockBufs& last = p.N ? p.sb[p.N - 1] : p.cb;
+  probe(PH_BWD_ROWS, 0, st);
   TRY((int)cudaMemsetAsync(c.G, 0, o.total * 4, st));
   TRY((int)cudaMemsetAsync(last.g_dx, 0, Q * D * 4, st));
   TRY((int)cudaMemsetAsync(last.g_dx_bf, 0, Q * D * 2, st));
@@ -811,6 +815,7 @@ int backward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs) {
   // kept only its input h, so the per-stage activations are recomputed here first.
   float* dxt = p.dmerged;
   int first_unfused = p.IL - 1;
+  probe(PH_BWD_ROWS, 1, st);
   if (p.fused_fe && p.IL == 1) {
     FrontArgs f = front_args(c, p, bt);
     f.h_in = p.h; f.dmerged = p.dmerged; f.dh_out = p.t_dx;
