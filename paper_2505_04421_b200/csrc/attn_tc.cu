@@ -330,8 +330,10 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
     }
     for (int c = 0; c < nchunk; ++c) {
       const int c0 = c * kC;
-      load_rows_bf16<DH>(sK, Kb + (long long)c0 * a.ldk, a.ldk, row, a.nk - c0);
-      load_rows_bf16<DH>(sV, Vb + (long long)c0 * a.ldv, a.ldv, row, a.nk - c0);
+      if (nchunk > 1) {                 // a single chunk is still resident from pass 1
+        load_rows_bf16<DH>(sK, Kb + (long long)c0 * a.ldk, a.ldk, row, a.nk - c0);
+        load_rows_bf16<DH>(sV, Vb + (long long)c0 * a.ldv, a.ldv, row, a.nk - c0);
+      }
       signal();
       wait_d();
 #pragma unroll 1
