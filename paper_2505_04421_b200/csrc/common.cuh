@@ -56,15 +56,28 @@ __device__ __forceinline__ float tanh_fast(float x) {
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// tanh-GELU (pkg/src/longrec/tensors.py:292-304)
+// tanh-GELU (pkg/src/longrec/tensors.py:292-304), written as FFMA chains:
+//   u = x·c(1 + a x²),  t = tanh(u),  gelu = h + h·t (h = x/2),
+//   gelu' = (1 + t)/2 + h (1 − t²) c (1 + 3a x²)
 __device__ __forceinline__ float gelu_f(float x) {
-  float t = tanh_fast(kGeluC * (x + kGeluA * x * x * x));
-  return 0.5f * x * (1.0f + t);
+  const float x2 = x * x;
+  const float t = tanh_fast(x * fmaf(x2, kGeluC * kGeluA, kGeluC));
+  const float h = 0.5f * x;
+  return fmaf(h, t, h);
 }
 __device__ __forceinline__ float gelu_grad_f(float x) {
-  float t = tanh_fast(kGeluC * (x + kGeluA * x * x * x));
-  float du = kGeluC * (1.0f + 3.0f * kGeluA * x * x);
-  return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * du;
+  const float x2 = x * x;
+  const float t = tanh_fast(x * fmaf(x2, kGeluC * kGeluA, kGeluC));
+  const float h = 0.5f * x;
+  return fmaf(h * fmaf(-t, t, 1.f), fmaf(x2, 3.f * kGeluC * kGeluA, kGeluC), fmaf(0.5f, t, 0.5f));
+}
+// both at once: returns gelu(x), writes gelu'(x)
+__device__ __forceinline__ float gelu_and_grad(float x, float& grad) {
+  const float x2 = x * x;
+  const float t = tanh_fast(x * fmaf(x2, kGeluC * kGeluA, kGeluC));
+  const float h = 0.5f * x;
+  grad = fmaf(h * fmaf(-t, t, 1.f), fmaf(x2, 3.f * kGeluC * kGeluA, kGeluC), fmaf(0.5f, t, 0.5f));
+  return fmaf(h, t, h);
 }
 
 __device__ __forceinline__ float warp_sum(float v) {

@@ -587,10 +587,9 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
           tmem_row<32>(T_G1 + lane_off + c0, gv);
 #pragma unroll
           for (int u = 0; u < 32; ++u) {
-            const float z = av[u];                                  // b1 added by the MMA
-            const float t = tanh_fast(kGeluC * (z + kGeluA * z * z * z));
-            av[u] = 0.5f * z * (1.f + t);
-            gv[u] *= 0.5f * (1.f + t) + 0.5f * z * (1.f - t * t) * kGeluC * (1.f + 3.f * kGeluA * z * z);
+            float gd;                                               // b1 added by the MMA
+            av[u] = gelu_and_grad(av[u], gd);
+            gv[u] *= gd;
           }
           store_row(sG, row, 128, av, 32, c0);
           store_row(sDA, row, 128, gv, 32, c0);

@@ -226,10 +226,9 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
         tmem_row<32>(T_W1 + lo + c0, gv);
 #pragma unroll
         for (int u = 0; u < 32; ++u) {
-          const float z = fv[u];                                      // b1 added by the MMA
-          const float tt = tanh_fast(kGeluC * (z + kGeluA * z * z * z));
-          fv[u] = 0.5f * z * (1.f + tt);
-          gv[u] *= 0.5f * (1.f + tt) + 0.5f * z * (1.f - tt * tt) * kGeluC * (1.f + 3.f * kGeluA * z * z);
+          float gd;                                                   // b1 added by the MMA
+          fv[u] = gelu_and_grad(fv[u], gd);
+          gv[u] *= gd;
         }
         store_row(sGF, row, F4, fv, 32, c0);
         store_row(sDF, row, F4, gv, 32, c0);
