@@ -696,6 +696,11 @@ int frontend_supported(int d, int K, int D, int F, int inner_layers) {
   return 1;
 }
 
+int frontend_mlp_bwd_supported(int d, int K, int D) {
+  (void)d; (void)K;
+  return 2 * D <= 256;
+}
+
 int frontend_blob_bytes(int d, int D, int inner_layers) { return blob_offsets(d, D, inner_layers).total * 2; }
 
 void pack_frontend_weights(const float* params, long long tok_w, long long seq_w1, long long seq_w2,

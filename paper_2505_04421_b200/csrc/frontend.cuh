@@ -49,6 +49,8 @@ void pack_frontend_weights(const float* params, long long tok_w, long long seq_w
                            cudaStream_t st);
 
 int frontend_supported(int d, int K, int D, int F, int inner_layers);
+// the fused token-MLP backward additionally needs 2D ≤ 256 (TMEM / shared-memory budget)
+int frontend_mlp_bwd_supported(int d, int K, int D);
 int frontend_fwd(const FrontArgs& a, cudaStream_t st);
 // token-MLP + featuriser backward: dh → all front-end MLP/featuriser/table/pos gradients
 int frontend_mlp_bwd(const FrontArgs& a, cudaStream_t st);

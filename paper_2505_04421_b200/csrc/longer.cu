@@ -344,10 +344,18 @@ struct Ctx {
   float* g(long long off) const { return G + off; }
 };
 
-#define TRY(expr)                                   \
-  do {                                              \
-    int _rc = (expr);                               \
-    if (_rc) return fail(LONGER_ECUDA, #expr);      \
+// On failure: the innermost failing call (with the CUDA error text) first, then its callers.
+#define TRY(expr)                                                                         \
+  do {                                                                                    \
+    int _rc = (expr);                                                                     \
+    if (_rc) {                                                                            \
+      if (g_err.empty()) {                                                                \
+        g_err = std::string(#expr) + ": " + cudaGetErrorString((cudaError_t)_rc);         \
+      } else {                                                                            \
+        g_err += std::string(" | in ") + #expr;                                           \
+      }                                                                                   \
+      return LONGER_ECUDA;                                                                \
+    }                                                                                     \
   } while (0)
 
 // C[M,N] (=|+=) epi(A[M,K]·B[K,N]); majors: a_mn / b_mn as in gemm.cuh
@@ -514,9 +522,17 @@ int block_fwd(const Ctx& c, const BlockOff& bo, BlockBufs& b, const float* xq, b
 
 int inner_unfused_fwd(const Ctx& c, const Plan& p);
 
+// Featuriser + token MLP with per-stage kernels (keeps feat, x0, a1, g1 for the per-stage backward).
+int mlp_unfused_fwd(const Ctx& c, const Plan& p, const LongerBatch& bt);
+
 // Unfused front-end: featuriser kernel + tcgen05 GEMMs per stage; keeps every activation the
 // unfused backward needs.
 int frontend_unfused_fwd(const Ctx& c, const Plan& p, const LongerBatch& bt) {
+  TRY(mlp_unfused_fwd(c, p, bt));
+  return inner_unfused_fwd(c, p);
+}
+
+int mlp_unfused_fwd(const Ctx& c, const Plan& p, const LongerBatch& bt) {
   cudaStream_t st = c.st;
   const ParamOff& o = p.po;
   const LongerDims& dm = p.dims;
@@ -534,7 +550,7 @@ int frontend_unfused_fwd(const Ctx& c, const Plan& p, const LongerBatch& bt) {
   // per-token input MLP (inputs.py:447-449); pad rows zeroed (inputs.py:478-481)
   TRY(lin_fwd(st, p.x0, d, T, p.pk.seq_w1, d, 2 * D, c.w(o.seq_b1), EPI_GELU | EPI_SAVE_PRE, nullptr, p.g1, p.a1));
   TRY(lin_fwd(st, p.g1, 2 * D, T, p.pk.seq_w2, 2 * D, d, c.w(o.seq_b2), 0, p.h, nullptr, nullptr, nullptr, 0, p.real));
-  return inner_unfused_fwd(c, p);
+  return 0;
 }
 
 // InnerTrans merge (merge.py:83-112) from p.h with per-stage kernels, keeping every activation
@@ -862,7 +878,10 @@ int backward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs) {
     dxt = p.t_dx;
   }
   // token MLP + featuriser (inputs.py:434-482); only real tokens carry gradient
-  if (p.fused_fe) {
+  if (p.fused_fe && !frontend_mlp_bwd_supported(p.d, p.K, p.D)) {
+    // widths the fused MLP backward does not take: recompute the MLP activations per stage
+    TRY(mlp_unfused_fwd(c, p, bt));
+  } else if (p.fused_fe) {
     FrontArgs f = front_args(c, p, bt);
     f.dh = dxt;
     probe(PH_FE_MLP_BWD, 0, st); TRY(frontend_mlp_bwd(f, st)); probe(PH_FE_MLP_BWD, 1, st);
@@ -898,6 +917,7 @@ bool use_fused(const Plan& p) {
 }
 
 int check_call(const LongerDims* dims, size_t ws_bytes, Plan* out, void* ws) {
+  g_err.clear();
   if (!dims) return fail(LONGER_EDIM, "null dims");
   int rc = validate(*dims);
   if (rc) return rc;
@@ -1172,6 +1192,7 @@ extern "C" int longer_score_workspace_bytes(const LongerDims* dims, int32_t cand
 extern "C" int longer_cache_score(const LongerDims* dims, const float* params, const void* cache, size_t cache_bytes,
                                   const int32_t* cand_items, int32_t candidates_per_user, void* ws, size_t ws_bytes,
                                   float* probs, void* stream) {
+  g_err.clear();
   if (!dims || !cache || !cand_items || !probs) return fail(LONGER_EDIM, "null argument");
   int rc = validate(*dims);
   if (rc) return rc;

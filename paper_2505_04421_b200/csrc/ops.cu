@@ -817,7 +817,7 @@ void attn_fwd(const AttnArgs& a, cudaStream_t st) {
 
 // Backward (masked_softmax bw p⊙(g−Σg⊙p), tensors.py:346-349; matmul bws, tensors.py:219-244).
 // P is recomputed from the saved log-sum-exp; dQ accumulates in smem across key chunks.
-__global__ void attn_bwd_kernel(AttnArgs a) {
+__global__ void attn_bwd_kernel(AttnArgs a, int C) {
   pdl_trigger();
   pdl_wait();
   extern __shared__ float sm[];
@@ -829,10 +829,10 @@ __global__ void attn_bwd_kernel(AttnArgs a) {
   float* sdO = sQ + nq * ldp;              // nq*ldp
   float* sdQ = sdO + nq * ldp;             // nq*ldp
   float* sK = sdQ + nq * ldp;              // C*ldp
-  float* sV = sK + kAttnChunk * ldp;       // C*ldp
-  float* sP = sV + kAttnChunk * ldp;       // nq*C
-  float* sdS = sP + nq * kAttnChunk;       // nq*C
-  float* sDi = sdS + nq * kAttnChunk;      // nq
+  float* sV = sK + C * ldp;       // C*ldp
+  float* sP = sV + C * ldp;       // nq*C
+  float* sdS = sP + nq * C;       // nq*C
+  float* sDi = sdS + nq * C;      // nq
   float* sL = sDi + nq;                    // nq
   const float scale = rsqrtf((float)dh);
   const VisRule vis{a.k, a.G, a.ns, a.goff, a.npg[b]};
@@ -855,8 +855,8 @@ __global__ void attn_bwd_kernel(AttnArgs a) {
     s = warp_sum(s);
     if (lane == 0) { sDi[i] = s; sL[i] = a.lse[((long long)b * a.heads + h) * nq + i]; }
   }
-  for (int c0 = 0; c0 < a.nk; c0 += kAttnChunk) {
-    const int cn = min(kAttnChunk, a.nk - c0);
+  for (int c0 = 0; c0 < a.nk; c0 += C) {
+    const int cn = min(C, a.nk - c0);
     __syncthreads();
     for (int i = threadIdx.x; i < cn * dh; i += blockDim.x) {
       const int r = i / dh, c = i % dh;
@@ -864,8 +864,8 @@ __global__ void attn_bwd_kernel(AttnArgs a) {
       sV[r * ldp + c] = __bfloat162float(Vg[(long long)(c0 + r) * a.ldv + c]);
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < nq * kAttnChunk; e += blockDim.x) {
-      const int i = e / kAttnChunk, j = e % kAttnChunk;
+    for (int e = threadIdx.x; e < nq * C; e += blockDim.x) {
+      const int i = e / C, j = e % C;
       float p = 0.f, ds = 0.f;
       if (j < cn && sL[i] != -INFINITY && vis(i, c0 + j)) {
         float s = 0.f, dp = 0.f;
@@ -876,8 +876,8 @@ __global__ void attn_bwd_kernel(AttnArgs a) {
         p = __expf(s - sL[i]);
         ds = p * (dp - sDi[i]);
       }
-      sP[i * kAttnChunk + j] = p;
-      sdS[i * kAttnChunk + j] = ds;
+      sP[i * C + j] = p;
+      sdS[i * C + j] = ds;
     }
     __syncthreads();
     // dV[j] = Σ_i P[i,j] dO[i];  dK[j] = scale Σ_i dS[i,j] Q̃[i]/scale... (sQ is pre-scaled: Q̃ = scale·Q)
@@ -885,8 +885,8 @@ __global__ void attn_bwd_kernel(AttnArgs a) {
       const int j = e / dh, c = e % dh;
       float dv = 0.f, dk = 0.f;
       for (int i = 0; i < nq; ++i) {
-        dv = fmaf(sP[i * kAttnChunk + j], sdO[i * ldp + c], dv);
-        dk = fmaf(sdS[i * kAttnChunk + j], sQ[i * ldp + c], dk);
+        dv = fmaf(sP[i * C + j], sdO[i * ldp + c], dv);
+        dk = fmaf(sdS[i * C + j], sQ[i * ldp + c], dk);
       }
       a.dV[b * a.sdv + (long long)(c0 + j) * a.lddv + h * dh + c] = __float2bfloat16(dv);
       a.dK[b * a.sdk + (long long)(c0 + j) * a.lddk + h * dh + c] = __float2bfloat16(dk);
@@ -894,7 +894,7 @@ __global__ void attn_bwd_kernel(AttnArgs a) {
     for (int e = threadIdx.x; e < nq * dh; e += blockDim.x) {
       const int i = e / dh, c = e % dh;
       float dq = 0.f;
-      for (int j = 0; j < cn; ++j) dq = fmaf(sdS[i * kAttnChunk + j], sK[j * ldp + c], dq);
+      for (int j = 0; j < cn; ++j) dq = fmaf(sdS[i * C + j], sK[j * ldp + c], dq);
       sdQ[i * ldp + c] += dq * scale;
     }
   }
@@ -908,10 +908,14 @@ __global__ void attn_bwd_kernel(AttnArgs a) {
 void attn_bwd(const AttnArgs& a, cudaStream_t st) {
   const int dh = a.D / a.heads;
   const int ldp = dh + 1;
-  const int smem = 4 * (3 * a.nq * ldp + 2 * kAttnChunk * ldp + 2 * a.nq * kAttnChunk + 2 * a.nq);
+  // key chunk: 64 unless the head width needs a smaller one to fit shared memory (e.g. 256)
+  int C = kAttnChunk;
+  auto smem_for = [&](int c) { return 4 * (3 * a.nq * ldp + 2 * c * ldp + 2 * a.nq * c + 2 * a.nq); };
+  while (C > 8 && smem_for(C) > 220 * 1024) C /= 2;
+  const int smem = smem_for(C);
   static int done = 0;
   if (!done) { cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); done = 1; }
-  launch(attn_bwd_kernel, a.B * a.heads, 256, smem, st, a);
+  launch(attn_bwd_kernel, a.B * a.heads, 256, smem, st, a, C);
 }
 
 // ============================================================== global tokens
