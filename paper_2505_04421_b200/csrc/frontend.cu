@@ -155,7 +155,8 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
   bf16* sH = sA + kTile * XK;                              // 128 x 64 bf16 hidden part (also k|v scratch)
   bf16* sKV = sH;                                          // 128 x 2DT bf16, 16-byte chunks XOR-swizzled
   float* s_par = reinterpret_cast<float*>(sH + kTile * 64);   // [IL][ln1_g, ln1_b, b_o, ln2_g, ln2_b, b2][DT]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_par + a.inner_layers * 6 * DT);
+  float* s_kn = s_par + a.inner_layers * 6 * DT;              // cross LN1 [gain | bias] (2D) for the kn epilogue
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_kn + 2 * D);
   uint64_t* bar_w = bars;
   uint64_t* bar_a = bars + 1;
   uint64_t* bar_d = bars + 2;
@@ -181,6 +182,8 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
                      : v == 3 ? a.inner_ln[l][2] : v == 4 ? a.inner_ln[l][3] : a.inner_bias[l][5];
     s_par[i] = src[c];
   }
+  if (a.kn)
+    for (int i = threadIdx.x; i < 2 * D; i += blockDim.x) s_kn[i] = i < D ? a.kn_g[i] : a.kn_b[i - D];
   __syncthreads();
   const long long ntiles = (a.T + kTile - 1) / kTile;
 
@@ -390,6 +393,43 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
         float4* dst = reinterpret_cast<float4*>(a.merged + ti.t * DT);
 #pragma unroll
         for (int c = 0; c < DT; c += 4) dst[c / 4] = make_float4(h[c], h[c + 1], h[c + 2], h[c + 3]);
+      }
+      if (a.kn) {
+        // cross LN1 of the merged row = the KG consecutive tokens of this group (adjacent lanes)
+        float s1 = 0.f;
+#pragma unroll
+        for (int c = 0; c < DT; ++c) s1 += h[c];
+#pragma unroll
+        for (int o2 = 1; o2 < KG; o2 <<= 1) s1 += __shfl_xor_sync(0xffffffffu, s1, o2);
+        const float mu = s1 * (1.f / D);
+        float s2 = 0.f;
+#pragma unroll
+        for (int c = 0; c < DT; ++c) { const float t = h[c] - mu; s2 += t * t; }
+#pragma unroll
+        for (int o2 = 1; o2 < KG; o2 <<= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o2);
+        const float inv = rsqrtf(s2 * (1.f / D) + kLnEps);
+        if (ti.in_range) {
+          const int part = ti.j % KG;
+          const long long krow = (long long)ti.b * a.v + ti.j / KG;
+          bf16* dst = a.kn + krow * D + part * DT;
+          const float* gk = s_kn + part * DT;
+          const float* bk = s_kn + D + part * DT;
+#pragma unroll
+          for (int c = 0; c < DT; c += 8) {
+            const float4 g0 = *reinterpret_cast<const float4*>(gk + c), g1 = *reinterpret_cast<const float4*>(gk + c + 4);
+            const float4 b0 = *reinterpret_cast<const float4*>(bk + c), b1 = *reinterpret_cast<const float4*>(bk + c + 4);
+            const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+            const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+            float y[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) y[u] = fmaf((h[c + u] - mu) * inv, gg[u], bb[u]);
+            uint4 w;
+            w.x = sm100::pack_bf16(y[0], y[1]); w.y = sm100::pack_bf16(y[2], y[3]);
+            w.z = sm100::pack_bf16(y[4], y[5]); w.w = sm100::pack_bf16(y[6], y[7]);
+            *reinterpret_cast<uint4*>(dst + c) = w;
+          }
+          if (part == 0) { a.kn_mean[krow] = mu; a.kn_rstd[krow] = inv; }
+        }
       }
     }
   }
@@ -753,7 +793,7 @@ template <int DT, int KG>
 static int launch_fwd(const FrontArgs& a, cudaStream_t st) {
   const BlobOff bo = blob_offsets(DT, DT * KG, a.inner_layers);
   const int smem = ((bo.fwd_total + 63) & ~63) * 2 + kTile * std::max(DT + 16, kFP) * 2 + kTile * 64 * 2 +
-                   a.inner_layers * 6 * DT * 4 + 64;
+                   a.inner_layers * 6 * DT * 4 + 2 * DT * KG * 4 + 64;
   static int done = 0;
   if (!done) {
     cudaFuncSetAttribute(fe_fwd_kernel<DT, KG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);

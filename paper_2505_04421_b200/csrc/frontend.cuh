@@ -30,6 +30,12 @@ struct FrontArgs {
   int* status;
   int32_t* npg;                // [B] all-pad merged groups per sample
   float *real_out, *keep_out;  // [T] token is real / token's group is not all-pad (or null)
+  // optional fused epilogue: the cross block's LN1 of every merged row (a group of K tokens),
+  // written as the bf16 K/V-projection operand kn[b*v + g] with its mean / rstd
+  const float *kn_g, *kn_b;
+  bf16* kn;
+  float *kn_mean, *kn_rstd;
+  int v;                       // rows per sample in kn (G + m)
   // backward
   const float* dh;             // [T, d] gradient w.r.t. the token-MLP output (MLP backward input)
   float *g_tok_w, *g_tok_b, *g_seq_w1, *g_seq_b1, *g_seq_w2, *g_seq_b2;

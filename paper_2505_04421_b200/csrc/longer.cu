@@ -614,7 +614,11 @@ int frontend_fused_fwd(const Ctx& c, const Plan& p, const LongerBatch& bt) {
     iw[l][0] = o.inner[l].w_q; iw[l][1] = o.inner[l].w_k; iw[l][2] = o.inner[l].w_v; iw[l][3] = o.inner[l].w_o;
   }
   pack_frontend_weights(c.P, o.tok_w, o.seq_w1, o.seq_w2, iw, p.d, p.D, p.F, p.IL, p.wblob, c.st);
-  return frontend_fwd(front_args(c, p, bt), c.st);
+  FrontArgs f = front_args(c, p, bt);
+  // epilogue: the cross block's LN1 of the merged rows straight into the K/V operand (kn)
+  f.kn = p.kn; f.kn_g = c.w(o.cross.ln1_g); f.kn_b = c.w(o.cross.ln1_b);
+  f.kn_mean = p.mk; f.kn_rstd = p.rk; f.v = p.v;
+  return frontend_fwd(f, c.st);
 }
 
 int forward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs, float* loss, int with_loss) {
@@ -648,7 +652,12 @@ int forward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs, fl
     const cudaStream_t ss = side_stream(st);
     fork_side(st, ss);
     RowMap r{};
-    r.A = p.merged; r.lda = D; r.a_rows = p.G; r.a_off = 0; r.na = p.G; r.Bsrc = p.glob; r.ldb = D; r.nb = p.m;
+    if (p.fused_fe) {          // merged rows were normalised by the fused front-end; globals only
+      r.A = p.glob; r.lda = D; r.a_rows = p.m; r.a_off = 0; r.na = p.m; r.Bsrc = nullptr; r.ldb = D; r.nb = 0;
+      r.o_per = p.v; r.o_off = p.G;
+    } else {
+      r.A = p.merged; r.lda = D; r.a_rows = p.G; r.a_off = 0; r.na = p.G; r.Bsrc = p.glob; r.ldb = D; r.nb = p.m;
+    }
     r.batch = p.B;
     layernorm_fwd(r, D, c.w(o.cross.ln1_g), c.w(o.cross.ln1_b), p.kn, p.mk, p.rk, ss);
     TRY(lin_fwd(ss, p.kn, D, (long long)p.B * p.v, p.pk.c_wkv, D, 2 * D, p.pk.c_bkv, 0, nullptr, p.KV, nullptr));

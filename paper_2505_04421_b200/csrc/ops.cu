@@ -205,7 +205,8 @@ __global__ void ln_fwd_kernel(RowMap x, int W, const float* __restrict__ g, cons
   }
   const float var = warp_sum(q) / W;
   const float inv = rsqrtf(var + kLnEps);
-  bf16* dst = y + (long long)row * W;
+  const int orow = x.out_row(row);
+  bf16* dst = y + (long long)orow * W;
   if constexpr (CONTIG && VPT >= 2) {
     float gg[VPT], bb[VPT];
 #pragma unroll
@@ -224,7 +225,7 @@ __global__ void ln_fwd_kernel(RowMap x, int W, const float* __restrict__ g, cons
       if (c < W) dst[c] = __float2bfloat16((v[u] - mu) * inv * g[c] + bta[c]);
     }
   }
-  if (lane == 0) { mean[row] = mu; rstd[row] = inv; }
+  if (lane == 0) { mean[orow] = mu; rstd[orow] = inv; }
 }
 
 namespace {

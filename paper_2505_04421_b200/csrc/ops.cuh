@@ -40,7 +40,12 @@ struct RowMap {
   const float* A; int lda; int a_rows; int a_off; int na;
   const float* Bsrc; int ldb; int nb;
   int batch;
+  // layernorm_fwd output placement: row b*(na+nb)+j goes to b*o_per + o_off + j (o_per = 0: same row)
+  int o_per, o_off;
   __host__ __device__ int rows() const { return batch * (na + nb); }
+  __host__ __device__ int out_row(int row) const {
+    return o_per ? (row / (na + nb)) * o_per + o_off + row % (na + nb) : row;
+  }
 };
 // y = LN(x)·g + b  → bf16 [rows, W]; mean/rstd saved
 void layernorm_fwd(const RowMap& x, int W, const float* g, const float* b, bf16* y, float* mean, float* rstd,
