@@ -605,17 +605,30 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
         }
         store_row(sDH, row, DT, dh, DT);
         store_row(sDX0, row, 64, dh, DT, 32);                          // [· | dh] for the db2 row sums
+        if (ti.real) {                                                 // item id for the dfeat split
+          const int it = a.items[(long long)ti.b * a.L + (ti.j - (a.Lp - a.L))];
+          ids[0] = (it < 0 || it >= a.vocab) ? 0 : it;
+        }
       }
       signal();
       wait_d();
-      if (grp == 0) {                                                  // x0 recompute
-        float x[DT + 16], acc[DT];
-        tmem_row<DT>(T_X + lane_off, acc);
+      // x0 recompute; with DT = 32 the two groups take 16 columns each
+      constexpr int XH = (DT % 32 == 0) ? DT / 2 : DT;
+      if (XH < DT || grp == 0) {
+        const int c0 = XH < DT ? grp * XH : 0;
+        float x[XH], acc[XH];
+        tmem_row<XH>(T_X + lane_off + c0, acc);
 #pragma unroll
-        for (int c = 0; c < DT; ++c) x[c] = ti.real ? acc[c] + s_pos[row * (DT + 1) + c] : 0.f;
+        for (int c = 0; c < XH; ++c) x[c] = ti.real ? acc[c] + s_pos[row * (DT + 1) + c0 + c] : 0.f;
+        store_row(sX0, row, XK, x, XH, c0);
+      }
+      if (grp == 1 || XH == DT) {
+        if (grp == (XH < DT ? 1 : 0)) {
+          float pad[16];
 #pragma unroll
-        for (int c = DT; c < DT + 16; ++c) x[c] = c == DT ? 1.f : 0.f;
-        store_row(sX0, row, XK, x, XK);
+          for (int c = 0; c < 16; ++c) pad[c] = c == 0 ? 1.f : 0.f;    // [· | 1 | 0…] bias column
+          store_row(sX0, row, XK, pad, 16, DT);
+        }
       }
       signal();
       for (int hj = 0; hj < nh; ++hj) {
@@ -637,26 +650,27 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
         signal();
       }
       wait_d();
-      if (grp == 0) {
-        float dx0[DT];
-        tmem_row<DT>(T_X + lane_off, dx0);
+      if (XH < DT || grp == 0) {
+        const int c0 = XH < DT ? grp * XH : 0;
+        float dx0[XH];
+        tmem_row<XH>(T_X + lane_off + c0, dx0);
 #pragma unroll
-        for (int c = 0; c < DT; ++c) {
+        for (int c = 0; c < XH; ++c) {
           dx0[c] = ti.real ? dx0[c] : 0.f;
-          s_gpos[row * (DT + 1) + c] += dx0[c];                        // abs-pos row of this position
+          s_gpos[row * (DT + 1) + c0 + c] += dx0[c];                   // abs-pos row of this position
         }
-        store_row(sDX0, row, 64, dx0, DT, 0);
+        store_row(sDX0, row, 64, dx0, XH, c0);
       }
       signal();
       wait_d();
-      if (grp == 0) {                                                  // item rows: dfeat[:d_item]
+      {                                                                // item rows: dfeat[:d_item]
         float df[kFP];
         tmem_row<kFP>(T_X + lane_off, df);
         if (ti.real) {
           float* gi = (item_smem ? s_item : a.g_item) + ids[0] * a.d_item;
 #pragma unroll
           for (int c = 0; c < kFP; ++c)
-            if (c < a.d_item) atomicAdd(gi + c, df[c]);
+            if (c < a.d_item && (c & 1) == grp) atomicAdd(gi + c, df[c]);
         }
       }
     }
