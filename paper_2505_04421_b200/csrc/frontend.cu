@@ -65,14 +65,14 @@ __device__ __forceinline__ TokenInfo token_info(const FrontArgs& a, long long ti
   return ti;
 }
 
-// featuriser: concat(item, action, time-bucket embeddings), zero-padded to kFP columns
-__device__ __forceinline__ void featurise(const FrontArgs& a, const TokenInfo& ti, float* v, int* ids, bool flag) {
+// featuriser: concat(item, action, time-bucket embeddings), zero-padded to kFP columns, from the
+// token's raw (item, action, Δt) — loaded by the caller, possibly a tile ahead
+__device__ __forceinline__ void featurise_raw(const FrontArgs& a, const TokenInfo& ti, int item, int act, int dt,
+                                              float* v, int* ids, bool flag) {
 #pragma unroll
   for (int c = 0; c < kFP; ++c) v[c] = 0.f;
   ids[0] = ids[1] = ids[2] = 0;
   if (!ti.real) return;
-  const long long src = (long long)ti.b * a.L + (ti.j - (a.Lp - a.L));
-  int item = a.items[src], act = a.actions[src], dt = a.dt[src];
   int bad = 0;
   if (item < 0 || item >= a.vocab) { bad |= 1; item = 0; }
   if (act < 0 || act >= a.n_actions) { bad |= 1; act = 0; }
@@ -88,6 +88,15 @@ __device__ __forceinline__ void featurise(const FrontArgs& a, const TokenInfo& t
                             : a.time_tab + bucket * a.d_time + (c - e2);
     v[c] = c < e3 ? __ldg(p) : 0.f;
   }
+}
+
+__device__ __forceinline__ void featurise(const FrontArgs& a, const TokenInfo& ti, float* v, int* ids, bool flag) {
+  int item = 0, act = 0, dt = 0;
+  if (ti.real) {
+    const long long src = (long long)ti.b * a.L + (ti.j - (a.Lp - a.L));
+    item = a.items[src]; act = a.actions[src]; dt = a.dt[src];
+  }
+  featurise_raw(a, ti, item, act, dt, v, ids, flag);
 }
 
 // table[id][0:width] += v[off : off+width] for every lane with id ≥ 0, summing lanes that share an id
@@ -570,20 +579,42 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
     uint32_t pd = 0;
     auto signal = [&]() { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(bar_a); };
     auto wait_d = [&]() { sm100::mbar_wait(bar_d, pd); pd ^= 1; sm100::tc_fence_after(); };
+    // the next sample's raw inputs (n_events, ids, dh) are loaded a tile ahead, right after the
+    // current tile's first stage, so their latency overlaps the MMA round trips
+    int n_pf = 0, item_pf = 0, act_pf = 0, dt_pf = 0;
+    float dh_pf[DT];
+    auto prefetch = [&](int bb) {
+      n_pf = a.n_events[bb];
+      if (!col_ok) return;
+      const long long src = (long long)bb * a.L + max(j - (a.Lp - a.L), 0);
+      item_pf = a.items[src];
+      if (grp == 0) {
+        act_pf = a.actions[src];
+        dt_pf = a.dt[src];
+      } else {
+        const float4* srcd = reinterpret_cast<const float4*>(a.dh + ((long long)bb * a.Lp + j) * DT);
+#pragma unroll
+        for (int c = 0; c < DT; c += 4) {
+          const float4 f4 = srcd[c / 4];
+          dh_pf[c] = f4.x; dh_pf[c + 1] = f4.y; dh_pf[c + 2] = f4.z; dh_pf[c + 3] = f4.w;
+        }
+      }
+    };
+    if (b0 < a.B) prefetch(b0);
     int my_tiles = 0;
     for (int b = b0; b < a.B; b += r, ++my_tiles) {
       TokenInfo ti;
       ti.b = b; ti.j = j;
       ti.in_range = col_ok;
       ti.t = (long long)b * a.Lp + j;
-      ti.n = min(max(a.n_events[b], 0), a.L);
+      ti.n = min(max(n_pf, 0), a.L);
       ti.real = col_ok && j >= a.Lp - ti.n;
       ti.keep = col_ok && (j / a.K) >= (a.Lp - ti.n) / a.K;
       ti.rec = ti.real ? a.Lp - 1 - j : 0;
       int ids[3] = {0, 0, 0};
       if (grp == 0) {
         float v[kFP];
-        featurise(a, ti, v, ids, false);
+        featurise_raw(a, ti, item_pf, act_pf, dt_pf, v, ids, false);
         v[kFP - 1] = 1.f;                                              // bias column
         store_row(sFeat, row, kFP, v, kFP);
         float oh[64];
@@ -592,25 +623,14 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
         store_row(sOH, row, 64, oh, 64);
       } else {
         float dh[DT];
-        if (ti.real) {
-          const float4* src = reinterpret_cast<const float4*>(a.dh + ti.t * DT);
 #pragma unroll
-          for (int c = 0; c < DT; c += 4) {
-            const float4 f4 = src[c / 4];
-            dh[c] = f4.x; dh[c + 1] = f4.y; dh[c + 2] = f4.z; dh[c + 3] = f4.w;
-          }
-        } else {
-#pragma unroll
-          for (int c = 0; c < DT; ++c) dh[c] = 0.f;
-        }
+        for (int c = 0; c < DT; ++c) dh[c] = ti.real ? dh_pf[c] : 0.f;
         store_row(sDH, row, DT, dh, DT);
         store_row(sDX0, row, 64, dh, DT, 32);                          // [· | dh] for the db2 row sums
-        if (ti.real) {                                                 // item id for the dfeat split
-          const int it = a.items[(long long)ti.b * a.L + (ti.j - (a.Lp - a.L))];
-          ids[0] = (it < 0 || it >= a.vocab) ? 0 : it;
-        }
+        if (ti.real) ids[0] = (item_pf < 0 || item_pf >= a.vocab) ? 0 : item_pf;   // for the dfeat split
       }
       signal();
+      if (b + r < a.B) prefetch(b + r);
       wait_d();
       // x0 recompute; with DT = 32 the two groups take 16 columns each
       constexpr int XH = (DT % 32 == 0) ? DT / 2 : DT;
