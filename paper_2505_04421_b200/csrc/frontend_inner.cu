@@ -48,7 +48,8 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
   bf16* sQKV = sDF + kTile * F4;              // 128 x QS bf16 (q, k, v for the group peers)
   float* sP = reinterpret_cast<float*>(sQKV + kTile * QS);   // 128 x KG
   float* sS = sP + kTile * KG;                                  // 128 x KG (dS)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sS + kTile * KG);
+  float* s_par = sS + kTile * KG;             // [ln1_g, ln1_b, b_o, ln2_g, ln2_b] x DT
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_par + 5 * DT);
   uint64_t* bar_w = bars;
   uint64_t* bar_a = bars + 1;
   uint64_t* bar_d = bars + 2;
@@ -68,6 +69,13 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
   const uint32_t tmem = *tmem_slot;
   pdl_trigger();
   pdl_wait();
+  for (int i = threadIdx.x; i < 5 * DT; i += blockDim.x) {
+    const int v = i / DT, c = i % DT;
+    const float* src = v == 0 ? a.inner_ln[0][0] : v == 1 ? a.inner_ln[0][1] : v == 2 ? a.inner_bias[0][3]
+                     : v == 3 ? a.inner_ln[0][2] : a.inner_ln[0][3];
+    s_par[i] = src[c];
+  }
+  __syncthreads();
   const uint32_t T_DW2 = tmem;                // F4 rows x DT
   const uint32_t T_DW1 = tmem + 32;           // F4 rows x XK   ([dW1ᵀ | db1])
   const uint32_t T_DWO = tmem + 80;           // DT rows x XK   ([dWoᵀ | dbo])
@@ -125,8 +133,11 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
     const int row = q * 32 + lane;
     const uint32_t lo = (uint32_t)(q * 32) << 16;
     const float scale = rsqrtf((float)DT);
-    const float* const* ib = a.inner_bias[0];
-    const float* const* ln = a.inner_ln[0];
+    const float* lg1 = s_par;                   // layer vectors staged in shared memory
+    const float* lb1 = s_par + DT;
+    const float* bo_ = s_par + 2 * DT;
+    const float* lg2 = s_par + 3 * DT;
+    const float* lb2 = s_par + 4 * DT;
     uint32_t pd = 0;
     auto signal = [&]() { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(bar_a); };
     auto wait_d = [&]() { sm100::mbar_wait(bar_d, pd); pd ^= 1; sm100::tc_fence_after(); };
@@ -152,7 +163,7 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
         dx2[c] = dv.x; dx2[c + 1] = dv.y; dx2[c + 2] = dv.z; dx2[c + 3] = dv.w;
       }
       float xn[XK], inv1;
-      ln_row<DT>(h, ln[0], ln[1], xn, nullptr, inv1);
+      ln_row_s<DT>(h, lg1, lb1, xn, inv1);
 #pragma unroll
       for (int c = DT; c < XK; ++c) xn[c] = c == DT ? 1.f : 0.f;
       store_row(sXN, row, XK, xn, XK);
@@ -210,9 +221,9 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
       float x1[DT];
       tmem_row<DT>(T_W2 + lo, x1);
 #pragma unroll
-      for (int c = 0; c < DT; ++c) x1[c] += h[c] + __ldg(ib[3] + c);
+      for (int c = 0; c < DT; ++c) x1[c] += h[c] + bo_[c];
       float x1n[XK], inv2;
-      ln_row<DT>(x1, ln[2], ln[3], x1n, nullptr, inv2);
+      ln_row_s<DT>(x1, lg2, lb2, x1n, inv2);
 #pragma unroll
       for (int c = DT; c < XK; ++c) x1n[c] = c == DT ? 1.f : 0.f;
       store_row(sX1N, row, XK, x1n, XK);
@@ -246,7 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
 #pragma unroll
       for (int c = 0; c < DT; ++c) {
         xh[c] = (x1[c] - mu2) * inv2;
-        const float gh = g[c] * __ldg(ln[2] + c);
+        const float gh = g[c] * lg2[c];
         m1 += gh;
         m2 += gh * xh[c];
       }
@@ -255,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
       float dx1[DT], tmp[DT];
 #pragma unroll
       for (int c = 0; c < DT; ++c) {
-        dx1[c] = dx2[c] + (g[c] * __ldg(ln[2] + c) - m1 - xh[c] * m2) * inv2;
+        dx1[c] = dx2[c] + (g[c] * lg2[c] - m1 - xh[c] * m2) * inv2;
         tmp[c] = g[c] * xh[c];
       }
       cs_l2g += warp_colsum<DT>(tmp);
@@ -315,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
 #pragma unroll
       for (int c = 0; c < DT; ++c) {
         xh[c] = (h[c] - mu1) * inv1;
-        const float gh = g[c] * __ldg(ln[0] + c);
+        const float gh = g[c] * lg1[c];
         m1 += gh;
         m2 += gh * xh[c];
       }
@@ -323,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
       m2 *= 1.f / DT;
 #pragma unroll
       for (int c = 0; c < DT; ++c) {
-        dx1[c] += (g[c] * __ldg(ln[0] + c) - m1 - xh[c] * m2) * inv1;
+        dx1[c] += (g[c] * lg1[c] - m1 - xh[c] * m2) * inv1;
         tmp[c] = g[c] * xh[c];
       }
       cs_l1g += warp_colsum<DT>(tmp);
@@ -388,7 +399,7 @@ template <int DT, int KG>
 int launch_inner_bwd(const FrontArgs& a, cudaStream_t st) {
   constexpr int XK = DT + 16, F4 = 4 * DT, QS = 3 * DT + 2;
   const int nW = 7 * DT * XK + DT * DT + 12 * DT * DT;
-  const int smem = nW * 2 + kTile * (3 * XK + 2 * DT + 2 * F4 + QS) * 2 + kTile * KG * 8 + 64;
+  const int smem = nW * 2 + kTile * (3 * XK + 2 * DT + 2 * F4 + QS) * 2 + kTile * KG * 8 + 5 * DT * 4 + 64;
   if (smem > 227 * 1024) return (int)cudaErrorInvalidValue;
   static int done = 0;
   if (!done) {
