@@ -256,10 +256,12 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
         sm100::mma_commit(bar_d);
       }
       for (int c = 0; c < nchunk; ++c) {
-        wait_a();                                                   // K, V chunk (+ Q, dO)
-        mma(T_A, Opnd{aQ, DH, 0}, Opnd{aK, DH, 0}, DH / 16, kC, false);      // S
-        mma(T_B, Opnd{adO, DH, 0}, Opnd{aV, DH, 0}, DH / 16, kC, false);     // dP
-        sm100::mma_commit(bar_d);
+        if (nchunk > 1) {           // a single chunk's S and dP are still in TMEM from pass 1
+          wait_a();                                                 // K, V chunk (+ Q, dO)
+          mma(T_A, Opnd{aQ, DH, 0}, Opnd{aK, DH, 0}, DH / 16, kC, false);    // S
+          mma(T_B, Opnd{adO, DH, 0}, Opnd{aV, DH, 0}, DH / 16, kC, false);   // dP
+          sm100::mma_commit(bar_d);
+        }
         wait_a();                                                   // P, dS
         mma(T_A, Opnd{aP, kC, 1}, Opnd{adO, DH, 1}, 128 / 16, DH, false);    // dV = Pᵀ·dO
         mma(T_B, Opnd{adS, kC, 1}, Opnd{aQ, DH, 1}, 128 / 16, DH, false);    // dK = dSᵀ·Q
@@ -330,12 +332,12 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
     }
     for (int c = 0; c < nchunk; ++c) {
       const int c0 = c * kC;
-      if (nchunk > 1) {                 // a single chunk is still resident from pass 1
+      if (nchunk > 1) {                 // a single chunk (K, V, S, dP) is still resident from pass 1
         load_rows_bf16<DH>(sK, Kb + (long long)c0 * a.ldk, a.ldk, row, a.nk - c0);
         load_rows_bf16<DH>(sV, Vb + (long long)c0 * a.ldv, a.ldv, row, a.nk - c0);
+        signal();
+        wait_d();
       }
-      signal();
-      wait_d();
 #pragma unroll 1
       for (int j0 = 0; j0 < kC; j0 += 32) {
         float s[32], dp[32];
