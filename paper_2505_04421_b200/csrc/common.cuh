@@ -31,6 +31,17 @@ inline bool pdl_enabled() {
   return v != 0;
 }
 
+// The weight-gradient side stream (longer.cu) launches at the lowest priority and everything else
+// at the highest, so the block scheduler serves the critical dX chain first when both are ready.
+inline cudaStream_t g_side_stream = nullptr;
+
+inline void launch_priorities(int& lo, int& hi) {
+  static int l = 1, h = 1;
+  if (l == 1) cudaDeviceGetStreamPriorityRange(&l, &h);
+  lo = l;
+  hi = h;
+}
+
 template <typename... KArgs, typename... Args>
 inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
   cudaLaunchConfig_t cfg{};
@@ -38,11 +49,20 @@ inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  int lo = 0, hi = 0;
+  launch_priorities(lo, hi);
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  at[n].id = cudaLaunchAttributePriority;
+  at[n].val.priority = (st != nullptr && st == g_side_stream) ? lo : hi;
+  ++n;
+  if (pdl_enabled()) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = n;
   cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 

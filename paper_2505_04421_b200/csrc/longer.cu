@@ -60,6 +60,7 @@ cudaStream_t side_stream(cudaStream_t main) {
   Side& sd = g_side[dev & 15];
   if (!sd.s) {
     cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking);
+    g_side_stream = sd.s;
     cudaEventCreateWithFlags(&sd.fork_ev, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&sd.join_ev, cudaEventDisableTiming);
     sd.dev = dev;
