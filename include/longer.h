@@ -76,6 +76,12 @@ int longer_forward_backward(const LongerDims* dims, const float* params, const L
                             void* ws, size_t ws_bytes, float* probs, float* loss, float* grads,
                             void* stream);
 
+/* Vector-Jacobian product of the most recent longer_forward on the same ws / batch / params (the
+ * torch.autograd bridge): grads (overwritten) = (dprobs/dparams)ᵀ · dprobs, using the
+ * activations that forward left in `ws`. */
+int longer_backward(const LongerDims* dims, const float* params, const LongerBatch* batch, void* ws,
+                    size_t ws_bytes, const float* probs, const float* dprobs, float* grads, void* stream);
+
 /* In-place Adam on the flat buffers (beta1 .9, beta2 .999, eps 1e-8, bias-corrected, step t>=1).
  * m, v: fp32 [count] moments (caller-zeroed before step 1). */
 int longer_adam_step(float* params, const float* grads, float* m, float* v, int64_t count, float lr,

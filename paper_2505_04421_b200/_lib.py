@@ -22,7 +22,8 @@ _EXC = {LONGER_ECONFIG: ConfigError, LONGER_EDIM: DimensionError, LONGER_ELOOKUP
 
 SYMBOLS = ("longer_param_count", "longer_workspace_bytes", "longer_forward", "longer_forward_backward",
            "longer_adam_step", "longer_read_status", "longer_last_error", "longer_set_probe",
-           "longer_cache_bytes", "longer_cache_build", "longer_score_workspace_bytes", "longer_cache_score")
+           "longer_cache_bytes", "longer_cache_build", "longer_score_workspace_bytes", "longer_cache_score",
+           "longer_backward")
 
 PROBES = {"fe_fwd": 0, "fe_inner_bwd": 1, "fe_mlp_bwd": 2, "xattn_fwd": 3, "xattn_bwd": 4,
           "fwd_rows": 5, "bwd_rows": 6}   # the last two bracket sections, not single kernels
@@ -67,6 +68,7 @@ def _declare(lib):
         "longer_workspace_bytes": [pd, ctypes.POINTER(ctypes.c_size_t)],
         "longer_forward": [pd, vp, pb, vp, ctypes.c_size_t, vp, vp],
         "longer_forward_backward": [pd, vp, pb, vp, ctypes.c_size_t, vp, vp, vp, vp],
+        "longer_backward": [pd, vp, pb, vp, ctypes.c_size_t, vp, vp, vp, vp],
         "longer_adam_step": [vp, vp, vp, vp, i64, f32, i32, vp],
         "longer_read_status": [vp, ctypes.POINTER(i32), vp],
         "longer_set_probe": [i32, vp, vp],

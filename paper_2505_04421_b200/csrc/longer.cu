@@ -1150,6 +1150,18 @@ extern "C" int longer_forward_backward(const LongerDims* dims, const float* para
   return backward(c, p, *batch, probs);
 }
 
+extern "C" int longer_backward(const LongerDims* dims, const float* params, const LongerBatch* batch, void* ws,
+                               size_t ws_bytes, const float* probs, const float* dprobs, float* grads, void* stream) {
+  static Plan p;
+  int rc = check_call(dims, ws_bytes, &p, ws);
+  if (rc) return rc;
+  if (!batch || !probs || !dprobs || !grads) return fail(LONGER_EDIM, "null argument");
+  p.fused_fe = use_fused(p);
+  Ctx c{p, params, grads, (cudaStream_t)stream};
+  dz_from_dprobs(probs, dprobs, p.B, p.dz, c.st);     // dL/dz = dL/dp · p(1 − p)
+  return backward(c, p, *batch, const_cast<float*>(probs));
+}
+
 extern "C" int longer_adam_step(float* params, const float* grads, float* m, float* v, int64_t count, float lr,
                                 int32_t t, void* stream) {
   if (t < 1) return fail(LONGER_ECONFIG, "Adam step counter must be >= 1");

@@ -1307,6 +1307,20 @@ void head_bwd(const HeadArgs& a, cudaStream_t st) {
   launch(head_wgrad_kernel, dim3(cdiv(n, 128), cdiv(a.B, per)), 128, 0, st, a, per);
 }
 
+__global__ void dz_from_dprobs_kernel(const float* probs, const float* dprobs, int B, float* dz) {
+  pdl_trigger();
+  pdl_wait();
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B) {
+    const float pb = probs[b];
+    dz[b] = dprobs[b] * pb * (1.f - pb);
+  }
+}
+
+void dz_from_dprobs(const float* probs, const float* dprobs, int B, float* dz, cudaStream_t st) {
+  launch(dz_from_dprobs_kernel, cdiv(B, 256), 256, 0, st, probs, dprobs, B, dz);
+}
+
 // ============================================================== parameters
 __global__ void pack_kernel(const float* __restrict__ params, const PackList specs, void* dst) {
   pdl_trigger();

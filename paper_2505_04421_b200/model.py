@@ -149,6 +149,7 @@ class LongerModel:
         B = b.size
         base, nbytes = self._workspace(B)
         probs = self._probs[B]
+        self._fwd_gen = getattr(self, "_fwd_gen", 0) + 1
         rc = self._lib.longer_forward(ctypes.byref(_lib.dims_of(self.cfg, B)), ctypes.c_void_p(self.flat.data_ptr()),
                                       ctypes.byref(self._struct(b)), ctypes.c_void_p(base), nbytes,
                                       ctypes.c_void_p(probs.data_ptr()), self._stream())
@@ -156,6 +157,33 @@ class LongerModel:
         if sync_check:
             self.read_status(B)
         return probs
+
+    def vjp(self, batch, probs, dprobs):
+        """(dprobs/dparams)ᵀ·dprobs into ``grad_flat`` (overwritten) for the batch the most recent
+        ``forward`` ran on (its activations are still in the workspace); returns ``grad_flat``."""
+        torch = _torch()
+        b = self.to_device_batch(batch)
+        B = b.size
+        base, nbytes = self._workspace(B)
+        dprobs = dprobs.to(device=self.device, dtype=torch.float32).contiguous()
+        probs = probs.to(device=self.device, dtype=torch.float32).contiguous()
+        _lib.check(self._lib.longer_backward(
+            ctypes.byref(_lib.dims_of(self.cfg, B)), ctypes.c_void_p(self.flat.data_ptr()),
+            ctypes.byref(self._struct(b)), ctypes.c_void_p(base), nbytes, ctypes.c_void_p(probs.data_ptr()),
+            ctypes.c_void_p(dprobs.data_ptr()), ctypes.c_void_p(self.grad_flat.data_ptr()), self._stream()))
+        return self.grad_flat
+
+    def autograd_params(self):
+        """A leaf tensor aliasing the flat fp32 master parameters, for ``LongerFunction``: after
+        ``loss.backward()`` its ``.grad`` holds d(loss)/d(params) in ``params()`` order."""
+        if getattr(self, "_leaf", None) is None:
+            self._leaf = self.flat.detach().requires_grad_(True)
+        return self._leaf
+
+    def probs(self, batch):
+        """Differentiable ``[B]`` probabilities (``torch.autograd`` bridge)."""
+        b = self.to_device_batch(batch)
+        return LongerFunction.apply(self.autograd_params(), self, b)
 
     def score(self, sample: Sample) -> float:
         return float(self.forward([sample], sync_check=True)[0].item())
@@ -169,6 +197,7 @@ class LongerModel:
         B = b.size
         base, nbytes = self._workspace(B)
         probs = self._probs[B]
+        self._fwd_gen = getattr(self, "_fwd_gen", 0) + 1
         rc = self._lib.longer_forward_backward(
             ctypes.byref(_lib.dims_of(self.cfg, B)), ctypes.c_void_p(self.flat.data_ptr()),
             ctypes.byref(self._struct(b)), ctypes.c_void_p(base), nbytes, ctypes.c_void_p(probs.data_ptr()),
@@ -198,6 +227,35 @@ class LongerModel:
         model.load_params(named)
         model.param_version = version
         return model
+
+
+def _autograd_base():
+    import torch
+    return torch.autograd.Function
+
+
+class LongerFunction(_autograd_base()):
+    """``probs = LongerFunction.apply(flat_params, model, batch)``: the LONGER forward as a
+    ``torch.autograd.Function``.  Forward = ``longer_forward``; backward = ``longer_backward``, the
+    vector-Jacobian product against the activations the forward left in the model's workspace —
+    so a forward must be followed by its backward before the next forward of the same batch size
+    on the same model (checked)."""
+
+    @staticmethod
+    def forward(ctx, flat, model, batch):
+        probs = model.forward(batch).clone()
+        ctx.model, ctx.batch, ctx.gen = model, batch, model._fwd_gen
+        ctx.save_for_backward(probs)
+        return probs
+
+    @staticmethod
+    def backward(ctx, dprobs):
+        model = ctx.model
+        if getattr(model, "_fwd_gen", None) != ctx.gen:
+            raise RuntimeError("another LongerModel forward ran since this one; its activations are gone")
+        (probs,) = ctx.saved_tensors
+        grads = model.vjp(ctx.batch, probs, dprobs).clone()
+        return grads, None, None
 
 
 class Adam:

@@ -138,3 +138,36 @@ def test_saturated_logits_follow_the_reference_clamp(bias):
     assert abs(loss - loss_ref) <= 1e-3 * abs(loss_ref) + 1e-3, (loss, loss_ref)
     assert_grads_close(grads, {n: G[n] for n in ("head.b2", "head.w2", "head.w1", "cross.w_v", "tables.item_table")},
                        f"bias {bias}")
+
+
+def test_autograd_bridge_matches_training_step():
+    """torch.autograd path (LongerFunction → longer_backward VJP) ≡ the fused training step for the
+    same BCE loss away from the clamp region, and against the oracle."""
+    import torch
+    cfg = ModelConfig(L=256, d=16, K=4, k=16, N=1, m=3).validate()
+    from paper_2505_04421_b200.params import init_params
+    rng = np.random.default_rng(11)
+    P = {n: a + 0.02 * rng.standard_normal(a.shape) for n, a in init_params(cfg, seed=0).items()}
+    batch = synthetic_batch(cfg, 6, seed=5, min_events=60)
+    model = _model(cfg, P)
+    _, _, G_step = _run(model, batch)
+    probs = model.probs(batch)
+    y = torch.from_numpy(np.asarray(batch.label)).cuda()
+    loss = torch.nn.functional.binary_cross_entropy(probs, y)
+    loss.backward()
+    flat = model.autograd_params().grad.detach().cpu().numpy().astype(np.float64)
+    off = 0
+    G_ag = {}
+    for name, shape in model.shapes.items():
+        n = int(np.prod(shape))
+        G_ag[name] = flat[off:off + n].reshape(shape)
+        off += n
+    for name in G_step:
+        np.testing.assert_allclose(G_ag[name], G_step[name], rtol=2e-3, atol=1e-6, err_msg=name)
+    _, _, G_ref = O.forward_backward(P, cfg, batch.as_dict())
+    assert_grads_close(G_ag, G_ref, "autograd")
+    # a second forward invalidates the first one's saved activations
+    p1 = model.probs(batch)
+    model.forward(batch)
+    with pytest.raises(RuntimeError):
+        p1.sum().backward()
