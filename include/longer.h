@@ -45,7 +45,7 @@ typedef struct LongerDims {
   int32_t L, d, K, m, k, N, heads;
   int32_t merge_inner;      /* 0 = "concat", 1 = "inner" */
   int32_t inner_layers;
-  int32_t query_strategy;   /* 0 = "recent" (the only strategy on the device path) */
+  int32_t query_strategy;   /* 0 recent, 1 uniform, 2 learnable, 3 recent_uniform (config.py order) */
   int32_t head_hidden, d_item, d_act, d_time, n_time_buckets;
   int32_t vocab, n_actions, n_users, n_profiles;
   int32_t batch;            /* samples in this call */

@@ -130,17 +130,70 @@ def recent_query_groups(cfg):
     return np.arange(G - cfg.k, G)
 
 
-def cross_mask(cfg, npg):
+def _ceil_div(a, b):
+    return -(-a // b)
+
+
+def query_groups(cfg, npg):
+    """Merged-group index of every sequence query, [B, k] (``select_queries``,
+    pkg/src/longrec/model.py:58-123, all four strategies).  Pad groups are the prefix
+    0..npg-1; a chosen pad group is a pad query.  For "learnable" every row is a bank vector at
+    the top grid position (returned as G-1) and is never pad."""
+    G, k = cfg.merged_len, cfg.k
+    B = npg.shape[0]
+    out = np.zeros((B, k), dtype=np.int64)
+    for b in range(B):
+        fv = int(npg[b])
+        nonpad = np.arange(fv, G)
+        n_m = nonpad.size
+        if cfg.query_strategy == "learnable":
+            out[b] = G - 1
+            continue
+        if n_m <= k:
+            fill = k - n_m
+            chosen = list(range(fv - fill, fv)) + list(nonpad)
+        elif cfg.query_strategy == "recent":
+            chosen = list(nonpad[-k:])
+        elif cfg.query_strategy == "uniform":
+            chosen = [int(nonpad[_ceil_div((j + 1) * n_m, k) - 1]) for j in range(k)]
+        elif cfg.query_strategy == "recent_uniform":
+            r = _ceil_div(k, 2)
+            u = k - r
+            picked = set(int(i) for i in nonpad[-r:])
+            prefix = nonpad[:n_m - r]
+            plen = prefix.size
+            for j in range(u):
+                picked.add(int(prefix[_ceil_div((j + 1) * plen, u) - 1]))
+            for idx in reversed(nonpad):
+                if len(picked) >= k:
+                    break
+                picked.add(int(idx))
+            chosen = sorted(picked)
+        else:
+            raise NotImplementedError(cfg.query_strategy)
+        out[b] = np.sort(np.asarray(chosen, dtype=np.int64))
+    return out
+
+
+def query_pad(cfg, npg, qg):
+    """[B, k] pad flags of the sequence queries (never for "learnable")."""
+    if cfg.query_strategy == "learnable":
+        return np.zeros(qg.shape, dtype=bool)
+    return qg < npg[:, None]
+
+
+def cross_mask(cfg, npg, qg=None):
     """Visibility of the first layer, [B, q, v] (pkg/src/longrec/attention.py:49-87 with the
     metadata of pkg/src/longrec/model.py:275-293)."""
     G, k, m = cfg.merged_len, cfg.k, cfg.m
     B = npg.shape[0]
-    qg = recent_query_groups(cfg)
+    if qg is None:
+        qg = np.broadcast_to(recent_query_groups(cfg), (B, k))
     keyg = np.arange(G)
     vis = np.zeros((B, k + m, G + m), dtype=bool)
     nonpad_key = keyg[None, :] >= npg[:, None]                      # [B, G]
-    qpad = qg[None, :] < npg[:, None]                               # [B, k]
-    seq = nonpad_key[:, None, :] & (keyg[None, None, :] <= qg[None, :, None]) & ~qpad[:, :, None]
+    qpad = query_pad(cfg, npg, qg)                                  # [B, k]
+    seq = nonpad_key[:, None, :] & (keyg[None, None, :] <= qg[:, :, None]) & ~qpad[:, :, None]
     vis[:, :k, :G] = seq
     vis[:, k:, :G] = nonpad_key[:, None, :]
     r = np.arange(m)
@@ -148,15 +201,16 @@ def cross_mask(cfg, npg):
     return vis
 
 
-def self_mask(cfg, npg):
-    """Visibility among the q retained rows, [B, q, q]."""
+def self_mask(cfg, npg, qg=None):
+    """Visibility among the q retained rows, [B, q, q] (positions of the sequence queries are their
+    groups; equal positions see each other, as for the "learnable" bank)."""
     k, m = cfg.k, cfg.m
     B = npg.shape[0]
-    qg = recent_query_groups(cfg)
-    qpad = qg[None, :] < npg[:, None]                               # [B, k]
+    if qg is None:
+        qg = np.broadcast_to(recent_query_groups(cfg), (B, k))
+    qpad = query_pad(cfg, npg, qg)                                  # [B, k]
     vis = np.zeros((B, k + m, k + m), dtype=bool)
-    ii = np.arange(k)
-    seq = (ii[None, :] <= ii[:, None])[None] & ~qpad[:, None, :] & ~qpad[:, :, None]
+    seq = (qg[:, None, :] <= qg[:, :, None]) & ~qpad[:, None, :] & ~qpad[:, :, None]
     vis[:, :k, :k] = seq
     vis[:, k:, :k] = ~qpad[:, None, :]
     r = np.arange(m)
@@ -314,10 +368,8 @@ def inner_bwd(P, cfg, dx, cache, grads):
 def forward(P, cfg, batch):
     """Batched ``LongRecModel.forward_tensor`` (pkg/src/longrec/model.py:307-363).
 
-    Returns (p [B], cache).  Only the "recent" query strategy is restated.
+    Returns (p [B], cache).  All four query strategies (``query_groups``).
     """
-    if cfg.query_strategy != "recent":
-        raise NotImplementedError("oracle restates the 'recent' query strategy")
     items = np.asarray(batch["items"], dtype=np.int64)
     actions = np.asarray(batch["actions"], dtype=np.int64)
     dt = np.asarray(batch["dt"], dtype=np.int64)
@@ -365,11 +417,15 @@ def forward(P, cfg, batch):
     gg, gt = gelu_fwd(ga)
     glob = lin(gg, P["tables.mlp.glob_w2"], P["tables.mlp.glob_b2"])
     # composite queries and keys (model.py:317-320)
-    qg = recent_query_groups(cfg)
-    O = np.concatenate([merged[:, qg], glob], axis=1)
+    qg = query_groups(cfg, npg)                                                   # [B, k]
+    if cfg.query_strategy == "learnable":
+        qrows = np.broadcast_to(P["query_bank"], (B, k, D))
+    else:
+        qrows = np.take_along_axis(merged, qg[:, :, None], axis=1)
+    O = np.concatenate([qrows, glob], axis=1)
     R = np.concatenate([merged, glob], axis=1)
-    vis1 = cross_mask(cfg, npg)
-    viss = self_mask(cfg, npg)
+    vis1 = cross_mask(cfg, npg, qg)
+    viss = self_mask(cfg, npg, qg)
     x, c_cross = block_fwd(P, "cross.", O, R, vis1, cfg.heads, False)
     c_self = []
     for i in range(cfg.N):
@@ -386,7 +442,7 @@ def forward(P, cfg, batch):
     p = sigmoid(z)
     cache = dict(it=it, ac=ac, bucket=bucket, rec=rec, real=real, feat=feat, x0=x0, a1=a1, g1=g1, t1=t1,
                  inner=inner_cache, npg=npg, uid=uid, prof=prof, cand=cand, uid_emb=uid_emb, td=td, tfeat=tfeat,
-                 raw=raw, ga=ga, gg=gg, gt=gt, c_cross=c_cross, c_self=c_self, x=x, t=t, cl=cl, hin=hin,
+                 raw=raw, ga=ga, gg=gg, gt=gt, c_cross=c_cross, c_self=c_self, x=x, t=t, cl=cl, hin=hin, qg=qg,
                  z1=z1, hg=hg, ht=ht, z=z, p=p)
     return p, cache
 
@@ -427,7 +483,12 @@ def backward(P, cfg, batch, cache):
         dx, _ = block_bwd(P, f"self.{i}.", dx, cache["c_self"][i], grads)
     dO, dR = block_bwd(P, "cross.", dx, cache["c_cross"], grads)
     dmerged = dR[:, :G].copy()
-    dmerged[:, recent_query_groups(cfg)] += dO[:, :k]
+    if cfg.query_strategy == "learnable":
+        _acc(grads, "query_bank", dO[:, :k].sum(axis=0))
+    else:
+        qg = cache["qg"]
+        for b in range(dO.shape[0]):
+            np.add.at(dmerged[b], qg[b], dO[b, :k])
     dglob = dR[:, G:] + dO[:, k:]
     # global MLP and its inputs
     dgg = lin_bwd(dglob, cache["gg"], P["tables.mlp.glob_w2"], grads, "tables.mlp.glob_w2", "tables.mlp.glob_b2")

@@ -38,15 +38,21 @@ __device__ __forceinline__ void load_rows_bf16(bf16* tile, const bf16* src, int 
 // spread over all four TMEM lane quadrants (= all four worker warps) instead of crowding warp 0.
 __device__ __forceinline__ int query_of_row(int row) { return (row & 31) * 4 + (row >> 5); }
 
-// The visible keys of one query row form ONE interval [lo, hi) of the key index (VisRule):
-//   sequence query i < k (group gq = G-k+i): non-pad sequence keys up to its own group;
+// The visible keys of one query row form ONE interval [lo, hi) of the key index (VisRule; the query
+// groups are sorted, so "key group ≤ query group" is "key index ≤ query index" in the self layers):
+//   sequence query: non-pad sequence keys up to its own group (pad query: none);
 //   global query of rank r: every non-pad sequence key, then the globals of rank ≤ r.
 __device__ __forceinline__ void vis_interval(const VisRule& v, int i, int nk, int& lo, int& hi) {
-  lo = max(0, v.npg - v.goff);
+  const int slo = v.self_keys ? v.jpad() : v.npg;          // first non-pad sequence key
   if (i < v.k) {
-    const int gq = v.G - v.k + i;
-    hi = gq < v.npg ? 0 : min(v.ns, gq - v.goff + 1);
+    if (v.qpad(i)) {
+      lo = hi = 0;
+      return;
+    }
+    lo = slo;
+    hi = v.self_keys ? (v.learn ? v.k : i + 1) : v.qgroup(i) + 1;
   } else {
+    lo = slo;
     hi = v.ns + (i - v.k) + 1;
   }
   hi = min(hi, nk);
@@ -115,7 +121,8 @@ __global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a) {
     const int qi = query_of_row(row);
     const uint32_t lo_lane = (uint32_t)(q * 32) << 16;
     const float scale = rsqrtf((float)(a.D / a.heads));
-    const VisRule vis{a.k, a.G, a.ns, a.goff, a.npg[b]};
+    const VisRule vis{a.k, a.G, a.ns, a.goff, a.npg[b], a.qg ? a.qg + (long long)b * a.k : nullptr, a.learn,
+                     a.self_keys};
     const bool qrow = qi < a.nq;
     int vlo = 0, vhi = 0;
     if (qrow) vis_interval(vis, qi, a.nk, vlo, vhi);
@@ -274,7 +281,8 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
     const int row = q * 32 + lane;
     const uint32_t lo = (uint32_t)(q * 32) << 16;
     const float scale = rsqrtf((float)(a.D / a.heads));
-    const VisRule vis{a.k, a.G, a.ns, a.goff, a.npg[b]};
+    const VisRule vis{a.k, a.G, a.ns, a.goff, a.npg[b], a.qg ? a.qg + (long long)b * a.k : nullptr, a.learn,
+                     a.self_keys};
     const bf16* Qb = a.Q + b * a.sq + hd * DH;
     const bf16* Kb = a.Kp + b * a.sk + hd * DH;
     const bf16* Vb = a.V + b * a.sv + hd * DH;

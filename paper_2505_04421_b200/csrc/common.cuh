@@ -117,21 +117,29 @@ __device__ __forceinline__ void stf(float* p, float v) { *p = v; }
 __device__ __forceinline__ void stf(bf16* p, float v) { *p = __float2bfloat16(v); }
 
 // Visibility rule of the hybrid attention (pkg/src/longrec/attention.py:49-87 with the
-// metadata of pkg/src/longrec/model.py:275-293, "recent" query strategy):
-//   queries: i < k  → sequence query of merged group G-k+i;  i >= k → global of rank i-k
-//   keys:    j < ns → sequence key of merged group goff+j;    j >= ns → global of rank j-ns
-//   (cross layer: ns = G, goff = 0;   self layers: ns = k, goff = G-k)
-//   a group is pad iff group < npg (pad groups form a prefix of the left-padded grid).
+// metadata of pkg/src/longrec/model.py:275-293), for every query strategy:
+//   queries: i < k → sequence query at merged group qgroup(i);  i >= k → global of rank i-k
+//   keys:    j < ns → sequence key;  j >= ns → global of rank j-ns
+//     cross layer (self_keys = 0): sequence key j is merged group j (ns = G)
+//     self layers (self_keys = 1): sequence key j is sequence query j (ns = k)
+//   a merged group is pad iff group < npg (pad groups form a prefix of the left-padded grid).
+// qg = this sample's sorted query groups (nullptr: "recent", G-k+i); learn = the "learnable" bank
+// (every bank row sits at the top grid position and is never pad).
 struct VisRule {
   int k, G, ns, goff, npg;
+  const int32_t* qg;
+  int learn, self_keys;
+  __device__ __forceinline__ int qgroup(int i) const { return learn ? G - 1 : (qg ? qg[i] : G - k + i); }
+  __device__ __forceinline__ bool qpad(int i) const { return !learn && qgroup(i) < npg; }
+  // number of pad sequence queries (always the first ones: the query groups are sorted)
+  __device__ __forceinline__ int jpad() const { return learn ? 0 : max(0, k - (G - npg)); }
   __device__ __forceinline__ bool operator()(int i, int j) const {
     if (i < k) {
-      const int gq = G - k + i;
-      if (gq < npg || j >= ns) return false;
-      const int gk = goff + j;
-      return gk >= npg && gk <= gq;
+      if (qpad(i) || j >= ns) return false;
+      if (self_keys) return !qpad(j) && qgroup(j) <= qgroup(i);
+      return j >= npg && j <= qgroup(i);
     }
-    if (j < ns) return goff + j >= npg;
+    if (j < ns) return self_keys ? !qpad(j) : j >= npg;
     return (j - ns) <= (i - k);
   }
 };

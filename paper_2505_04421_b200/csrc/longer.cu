@@ -93,6 +93,9 @@ int fail(int code, const char* msg) {
   return code;
 }
 
+// query strategies (config.py QUERY_STRATEGIES order)
+enum QueryStrategy { QS_RECENT = 0, QS_UNIFORM = 1, QS_LEARNABLE = 2, QS_RECENT_UNIFORM = 3 };
+
 // ------------------------------------------------------------------ parameter offsets
 constexpr int kMaxInner = 8;
 constexpr int kMaxSelf = 16;
@@ -105,6 +108,7 @@ struct ParamOff {
   long long item, act, time, uid, prof, pos, cls;
   long long tok_w, tok_b, seq_w1, seq_b1, seq_w2, seq_b2, lift_w, lift_b, glob_w1, glob_b1, glob_w2, glob_b2;
   BlockOff inner[kMaxInner], cross, self_[kMaxSelf];
+  long long qbank;             // "learnable" query bank [k, D] (-1 otherwise)
   long long head_w1, head_b1, head_w2, head_b2;
   long long total;
 };
@@ -140,6 +144,7 @@ ParamOff param_offsets(const LongerDims& d) {
     for (int i = 0; i < d.inner_layers; ++i) o.inner[i] = block(d.d);
   o.cross = block(D);
   for (int i = 0; i < d.N; ++i) o.self_[i] = block(D);
+  o.qbank = d.query_strategy == QS_LEARNABLE ? take((long long)d.k * D) : -1;
   const long long hin = 4 * D + 2 * d.d;
   o.head_w1 = take(hin * d.head_hidden); o.head_b1 = take(d.head_hidden);
   o.head_w2 = take(d.head_hidden); o.head_b2 = take(1);
@@ -151,9 +156,9 @@ int validate(const LongerDims& d) {
   if (d.L < 1 || d.d < 1 || d.K < 1) return fail(LONGER_ECONFIG, "L, d, K must all be >= 1");
   if (d.m < 3) return fail(LONGER_ECONFIG, "m must be >= 3 (UID, at least one CLS, target)");
   if (d.N < 1 || d.k < 1) return fail(LONGER_ECONFIG, "N and k must be >= 1");
-  if (d.query_strategy != 0) return fail(LONGER_ECONFIG, "device path implements the 'recent' query strategy");
+  if (d.query_strategy < 0 || d.query_strategy > 3) return fail(LONGER_ECONFIG, "unknown query strategy");
   const int Lp = (d.L + d.K - 1) / d.K * d.K, G = Lp / d.K, D = d.K * d.d;
-  if (d.k > G) return fail(LONGER_ECONFIG, "k exceeds merged length");
+  if (d.k > G && d.query_strategy != QS_LEARNABLE) return fail(LONGER_ECONFIG, "k exceeds merged length");
   if (d.heads < 1 || D % d.heads) return fail(LONGER_ECONFIG, "D not divisible by heads");
   if (d.d % 8) return fail(LONGER_ECONFIG, "device path needs d % 8 == 0 (16-byte TMA rows)");
   if (D / d.heads > 256) return fail(LONGER_ECONFIG, "head width D/heads must be <= 256");
@@ -212,6 +217,8 @@ struct Plan {
   int* status;
   int32_t* npg;
   int32_t* cand0;  // placeholder candidates of a cache build
+  int32_t* qg;     // [B, k] query groups (uniform / recent_uniform)
+  int qs;          // query strategy
   Packed pk;
   // tokens
   bf16 *feat, *x0, *a1, *g1;
@@ -251,6 +258,7 @@ void plan_dims(Plan& p, const LongerDims& d, void* ws) {
   p.HIN = 4 * p.D + 2 * d.d;
   p.T = (long long)p.B * p.Lp;
   p.po = param_offsets(d);
+  p.qs = d.query_strategy;
 }
 
 void take_packed(Plan& p, Bump& a) {
@@ -279,6 +287,7 @@ Plan make_plan(const LongerDims& d, void* ws) {
   p.status = a.take<int>(64);
   p.npg = a.take<int32_t>(B);
   p.cand0 = a.take<int32_t>(B);
+  p.qg = a.take<int32_t>((long long)B * d.k);
   p.wblob = a.take<bf16>(frontend_blob_bytes(dd, D, p.IL) / 2 + 64);
   take_packed(p, a);
   // tokens
@@ -491,6 +500,8 @@ int block_fwd(const Ctx& c, const BlockOff& bo, BlockBufs& b, const float* xq, b
   layernorm_fwd(rows_plain(xq, D, Q), D, c.w(bo.ln1_g), c.w(bo.ln1_b), b.qn, b.m1, b.r1, st);
   AttnArgs a{};
   a.nq = p.q; a.D = D; a.heads = p.heads; a.k = p.k; a.G = p.G; a.npg = p.npg; a.B = p.B;
+  a.qg = (p.qs == QS_UNIFORM || p.qs == QS_RECENT_UNIFORM) ? p.qg : nullptr;
+  a.learn = p.qs == QS_LEARNABLE; a.self_keys = cross ? 0 : 1;
   a.ctx = b.ctx; a.ldc = D; a.sc = (long long)p.q * D; a.lse = b.lse; a.ctx32 = b.ctx32;
   if (cross) {
     // K/V rows: LN1 + [K | V] projection were forked onto the side stream by forward()
@@ -663,7 +674,14 @@ int forward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs, fl
     layernorm_fwd(r, D, c.w(o.cross.ln1_g), c.w(o.cross.ln1_b), p.kn, p.mk, p.rk, ss);
     TRY(lin_fwd(ss, p.kn, D, (long long)p.B * p.v, p.pk.c_wkv, D, 2 * D, p.pk.c_bkv, 0, nullptr, p.KV, nullptr));
   }
-  gather_rows_f32(p.merged, p.B, p.G, p.G - p.k, p.k, p.O, p.q, 0, D, st);
+  // sequence queries (select_queries, model.py:58-123)
+  if (p.qs == QS_RECENT) {
+    gather_rows_f32(p.merged, p.B, p.G, p.G - p.k, p.k, p.O, p.q, 0, D, st);
+  } else {
+    if (p.qs != QS_LEARNABLE) select_queries(p.npg, p.B, p.G, p.k, p.qs, p.qg, st);
+    gather_query_rows(p.merged, p.qs == QS_LEARNABLE ? nullptr : p.qg, p.qs == QS_LEARNABLE ? c.w(o.qbank) : nullptr,
+                      p.B, p.G, p.k, D, p.O, p.q, st);
+  }
   gather_rows_f32(p.glob, p.B, p.m, 0, p.m, p.O, p.q, p.k, D, st);
   Plan& pm = const_cast<Plan&>(p);
   TRY(block_fwd(c, o.cross, pm.cb, p.O, true, p.pk.c_wq, nullptr, p.pk.c_wo, p.pk.c_w1, p.pk.c_w2));
@@ -720,6 +738,8 @@ int block_bwd(const Ctx& c, cudaStream_t ss, const BlockOff& bo, const BlockBufs
   // attention
   AttnArgs a{};
   a.nq = p.q; a.D = D; a.heads = p.heads; a.k = p.k; a.G = p.G; a.npg = p.npg; a.B = p.B;
+  a.qg = (p.qs == QS_UNIFORM || p.qs == QS_RECENT_UNIFORM) ? p.qg : nullptr;
+  a.learn = p.qs == QS_LEARNABLE; a.self_keys = cross ? 0 : 1;
   a.ctx = b.ctx; a.ldc = D; a.sc = (long long)p.q * D; a.lse = b.lse; a.ctx32 = b.ctx32;
   a.dctx = b.g_dctx; a.lddc = D; a.sdc = (long long)p.q * D; a.ctx_in = b.ctx;
   if (cross) {
@@ -767,7 +787,11 @@ int block_bwd(const Ctx& c, cudaStream_t ss, const BlockOff& bo, const BlockBufs
     ex.addend = b.g_dx1;
     layernorm_bwd(rows_plain(xq, D, Q), D, c.w(bo.ln1_g), b.m1, b.r1, b.g_dqn, D, rows_plain_w(p.dO, D, Q), 0,
                   nullptr, c.g(bo.ln1_g), c.g(bo.ln1_b), st, ex);
-    add_rows_f32(p.dO, p.B, p.q, 0, p.k, p.dmerged, p.G, p.G - p.k, D, st);
+    if (p.qs == QS_RECENT)
+      add_rows_f32(p.dO, p.B, p.q, 0, p.k, p.dmerged, p.G, p.G - p.k, D, st);
+    else
+      scatter_query_rows(p.dO, p.q, p.qg, p.B, p.G, p.k, D, p.dmerged,
+                         p.qs == QS_LEARNABLE ? c.g(p.po.qbank) : nullptr, st);
     add_rows_f32(p.dO, p.B, p.q, p.k, p.m, p.dglob, p.m, 0, D, st);
   } else {
     for (int j = 0; j < 3; ++j) {
@@ -1091,7 +1115,9 @@ int cache_score(const Ctx& c, const ScorePlan& s, const char* cache, const int32
   std::swap(x, y);
   for (int i = 0; i < p.N; ++i) {
     const bf16* kv = reinterpret_cast<const bf16*>(cache + L.skv) + (size_t)i * p.B * L.srows * 2 * D;
-    TRY(serve_block(c, s, o.self_[i], x, y, false, kv, (int)L.srows, p.k, p.G - p.k, npg, p.pk.s_wqkv[i],
+    // the target sees every non-pad sequence query: key j is pad iff (G-k)+j < npg, never for the bank
+    const int goff = p.qs == QS_LEARNABLE ? p.G : p.G - p.k;
+    TRY(serve_block(c, s, o.self_[i], x, y, false, kv, (int)L.srows, p.k, goff, npg, p.pk.s_wqkv[i],
                     p.pk.s_bqkv[i], p.pk.s_wo[i], p.pk.s_w1[i], p.pk.s_w2[i]));
     std::swap(x, y);
   }

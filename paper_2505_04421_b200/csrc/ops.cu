@@ -733,7 +733,8 @@ __global__ void attn_fwd_kernel(AttnArgs a) {
   float* sV = sK + kAttnChunk * ldp;
   const int wid = threadIdx.x / 32, lane = threadIdx.x & 31, nw = blockDim.x / 32;
   const float scale = rsqrtf((float)dh);
-  const VisRule vis{a.k, a.G, a.ns, a.goff, a.npg[b]};
+  const VisRule vis{a.k, a.G, a.ns, a.goff, a.npg[b], a.qg ? a.qg + (long long)b * a.k : nullptr, a.learn,
+                     a.self_keys};
   const bf16* Q = a.Q + b * a.sq + h * dh;
   const bf16* Kg = a.Kp + b * a.sk + h * dh;
   const bf16* Vg = a.V + b * a.sv + h * dh;
@@ -836,7 +837,8 @@ __global__ void attn_bwd_kernel(AttnArgs a, int C) {
   float* sDi = sdS + nq * C;      // nq
   float* sL = sDi + nq;                    // nq
   const float scale = rsqrtf((float)dh);
-  const VisRule vis{a.k, a.G, a.ns, a.goff, a.npg[b]};
+  const VisRule vis{a.k, a.G, a.ns, a.goff, a.npg[b], a.qg ? a.qg + (long long)b * a.k : nullptr, a.learn,
+                     a.self_keys};
   const bf16* Q = a.Q + b * a.sq + h * dh;
   const bf16* Kg = a.Kp + b * a.sk + h * dh;
   const bf16* Vg = a.V + b * a.sv + h * dh;
@@ -1049,6 +1051,105 @@ void globals_raw_bwd(const GlobalsArgs& a, cudaStream_t st) {
   if (!done) { cudaFuncSetAttribute(globals_raw_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); done = 1; }
   const int per = std::max(1, cdiv(a.B, 148));
   launch(globals_raw_bwd_kernel, cdiv(a.B, per), 256, smem, st, a, per);
+}
+
+// ============================================================== query selection (model.py:58-123)
+// One thread per sample; a bitmap over the merged groups (≤ 8192) realises recent_uniform's set
+// with deduplication and newest-first backfill, then emits the picks in group order.
+__global__ void select_queries_kernel(const int32_t* npg, int B, int G, int k, int strategy, int32_t* qg) {
+  pdl_trigger();
+  pdl_wait();
+  extern __shared__ uint32_t s_bits[];
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  const int words = (G + 31) / 32;
+  uint32_t* bits = s_bits + threadIdx.x * words;
+  if (b >= B) return;
+  int32_t* out = qg + (long long)b * k;
+  const int fv = min(max(npg[b], 0), G);
+  const int nm = G - fv;
+  auto cdiv_i = [](long long x, long long y) { return (int)((x + y - 1) / y); };
+  if (nm <= k || strategy == 0) {                 // pad fill + all non-pad == the k newest groups
+    for (int j = 0; j < k; ++j) out[j] = G - k + j;
+    return;
+  }
+  if (strategy == 1) {                             // uniform
+    for (int j = 0; j < k; ++j) out[j] = fv + cdiv_i((long long)(j + 1) * nm, k) - 1;
+    return;
+  }
+  // recent_uniform
+  for (int w = 0; w < words; ++w) bits[w] = 0u;
+  const int r = (k + 1) / 2, u = k - r;
+  int cnt = 0;
+  auto pick = [&](int g) {
+    const uint32_t m = 1u << (g & 31);
+    if (!(bits[g >> 5] & m)) { bits[g >> 5] |= m; ++cnt; }
+  };
+  for (int g = G - r; g < G; ++g) pick(g);
+  const int plen = nm - r;
+  for (int j = 0; j < u; ++j) pick(fv + cdiv_i((long long)(j + 1) * plen, u) - 1);
+  for (int g = G - 1; g >= fv && cnt < k; --g) pick(g);
+  int o = 0;
+  for (int g = fv; g < G && o < k; ++g)
+    if (bits[g >> 5] & (1u << (g & 31))) out[o++] = g;
+}
+
+void select_queries(const int32_t* npg, int B, int G, int k, int strategy, int32_t* qg, cudaStream_t st) {
+  const int words = (G + 31) / 32;
+  const int per = std::max(1, std::min(64, (48 * 1024) / (words * 4)));
+  launch(select_queries_kernel, cdiv(B, per), per, (size_t)per * words * 4, st, npg, B, G, k, strategy, qg);
+}
+
+__global__ void gather_query_rows_kernel(const float* merged, const int32_t* qg, const float* bank, int B, int G,
+                                         int k, int W, float* O, int q) {
+  pdl_trigger();
+  pdl_wait();
+  const long long n = (long long)B * k * W;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(e % W);
+    const long long bi = e / W;
+    const int i = (int)(bi % k), b = (int)(bi / k);
+    const float v = bank ? bank[(long long)i * W + c] : merged[((long long)b * G + qg[bi]) * W + c];
+    O[((long long)b * q + i) * W + c] = v;
+  }
+}
+
+void gather_query_rows(const float* merged, const int32_t* qg, const float* bank, int B, int G, int k, int W,
+                       float* O, int q, cudaStream_t st) {
+  const long long n = (long long)B * k * W;
+  if (n) launch(gather_query_rows_kernel, std::min(cdiv(n, 256), 148 * 16), 256, 0, st, merged, qg, bank, B, G, k, W, O, q);
+}
+
+__global__ void scatter_query_rows_kernel(const float* dO, int q, const int32_t* qg, int B, int G, int k, int W,
+                                          float* dmerged, float* g_bank) {
+  pdl_trigger();
+  pdl_wait();
+  if (g_bank) {                                    // Σ over samples, one thread per (i, c)
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= k * W) return;
+    const int i = e / W, c = e % W;
+    float acc = 0.f;
+    for (int b = 0; b < B; ++b) acc += dO[((long long)b * q + i) * W + c];
+    g_bank[e] += acc;
+    return;
+  }
+  const long long n = (long long)B * k * W;        // query groups of one sample are distinct
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(e % W);
+    const long long bi = e / W;
+    const int i = (int)(bi % k), b = (int)(bi / k);
+    dmerged[((long long)b * G + qg[bi]) * W + c] += dO[((long long)b * q + i) * W + c];
+  }
+}
+
+void scatter_query_rows(const float* dO, int q, const int32_t* qg, int B, int G, int k, int W, float* dmerged,
+                        float* g_bank, cudaStream_t st) {
+  if (g_bank) {
+    launch(scatter_query_rows_kernel, cdiv((long long)k * W, 256), 256, 0, st, dO, q, qg, B, G, k, W, dmerged, g_bank);
+  } else {
+    const long long n = (long long)B * k * W;
+    if (n) launch(scatter_query_rows_kernel, std::min(cdiv(n, 256), 148 * 16), 256, 0, st, dO, q, qg, B, G, k, W,
+                  dmerged, g_bank);
+  }
 }
 
 // ============================================================== head + BCE

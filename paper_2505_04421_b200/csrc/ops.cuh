@@ -95,6 +95,8 @@ struct AttnArgs {
   const bf16* V; int ldv; long long sv;
   int nq, nk, D, heads;
   int k, G, ns, goff;                        // VisRule parameters
+  const int32_t* qg;                         // [B, k] query groups (nullptr: "recent")
+  int learn, self_keys;                      // "learnable" bank; self layer (keys = query rows)
   const int32_t* npg;                        // [B] pad groups
   int B;
   bf16* ctx; int ldc; long long sc;          // fwd out (GEMM operand)
@@ -113,6 +115,17 @@ void attn_bwd(const AttnArgs& a, cudaStream_t st);
 int attn_tc_supported(const AttnArgs& a);
 int attn_tc_fwd(const AttnArgs& a, cudaStream_t st);
 int attn_tc_bwd(const AttnArgs& a, cudaStream_t st);
+
+// ---------------------------------------------------------------- query selection (model.py:58-123)
+// qg[b, 0..k) = the merged groups of sample b's sequence queries for strategy
+// 1 = uniform, 3 = recent_uniform (0 = recent and 2 = learnable need no table)
+void select_queries(const int32_t* npg, int B, int G, int k, int strategy, int32_t* qg, cudaStream_t st);
+// O[b, i] = merged[b, qg[b, i]] (or bank[i] when bank != nullptr), rows of width W, i < k
+void gather_query_rows(const float* merged, const int32_t* qg, const float* bank, int B, int G, int k, int W,
+                       float* O, int q, cudaStream_t st);
+// dmerged[b, qg[b, i]] += dO[b, i]  (or g_bank[i] += Σ_b dO[b, i] when g_bank != nullptr)
+void scatter_query_rows(const float* dO, int q, const int32_t* qg, int B, int G, int k, int W, float* dmerged,
+                        float* g_bank, cudaStream_t st);
 
 // ---------------------------------------------------------------- globals + head
 struct GlobalsArgs {

@@ -42,8 +42,6 @@ class LongerModel:
     def __init__(self, cfg: ModelConfig, seed: int = 0, device: str = "cuda") -> None:
         torch = _torch()
         cfg.validate()
-        if cfg.query_strategy != "recent":
-            raise ConfigError("the B200 path implements the 'recent' query strategy")
         if cfg.d % 8:
             raise ConfigError("the B200 path needs d % 8 == 0 (16-byte rows for TMA)")
         self.cfg = cfg

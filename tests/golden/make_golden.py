@@ -49,6 +49,17 @@ CASES = {
     "gpu_d8_h2": (dict(L=30, d=8, K=4, m=4, k=5, N=2, heads=2, merge_mode="inner", inner_layers=2,
                        head_hidden=16, n_users=50, vocab=60), [30, 17, 5, 0, 40, 12], 11),
     "gpu_concat_d8": (dict(L=48, d=8, K=2, k=6, N=3, n_users=40), [48, 20, 3, 48], 12),
+    # the other query strategies (pkg/src/longrec/model.py:58-123): non-contiguous query groups,
+    # pad queries when fewer than k non-pad groups exist, a learned query bank
+    "qs_uniform": (dict(TINY, L=30, K=2, k=5, query_strategy="uniform"), [30, 17, 9, 4, 0], 13),
+    "qs_recent_uniform": (dict(TINY, L=30, K=2, k=5, query_strategy="recent_uniform"), [30, 17, 9, 4, 0], 14),
+    "qs_learnable": (dict(TINY, L=30, K=2, k=5, query_strategy="learnable", merge_mode="inner"), [30, 11, 2, 0], 15),
+    "gpu_d8_uniform": (dict(L=64, d=8, K=4, m=4, k=6, N=2, heads=2, merge_mode="inner", query_strategy="uniform",
+                            head_hidden=16, n_users=50, vocab=60), [64, 41, 13, 5, 0], 16),
+    "gpu_d8_recent_uniform": (dict(L=64, d=8, K=2, m=3, k=7, N=2, query_strategy="recent_uniform",
+                                   n_users=50, vocab=60), [64, 30, 11, 64], 17),
+    "gpu_d8_learnable": (dict(L=48, d=8, K=4, m=3, k=5, N=2, query_strategy="learnable", merge_mode="inner",
+                              n_users=50, vocab=60), [48, 20, 3, 0], 18),
 }
 
 

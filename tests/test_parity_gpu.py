@@ -100,6 +100,10 @@ C2 = dict(L=2000, d=32, K=4, k=32, N=2, m=3, merge_mode="inner")
     (dict(L=256, d=16, K=4, k=16, N=1, m=3), 8, 100),
     # c5 widths (D = 256, K = 8): per-stage MLP backward fallback, head width 256 (SIMT attention)
     (dict(L=96, d=32, K=8, k=4, N=2, m=3, merge_mode="inner"), 3, 20),
+    # the other query strategies at the c2 widths, mixed lengths (pad queries included)
+    (dict(C2, L=512, query_strategy="uniform"), 4, 1),
+    (dict(C2, L=512, query_strategy="recent_uniform", merge_mode="concat"), 4, 1),
+    (dict(C2, L=512, query_strategy="learnable"), 4, 1),
     # D = 256 with two heads: tensor-core attention at head width 128
     (dict(L=96, d=32, K=8, k=4, N=1, m=3, heads=2, merge_mode="inner"), 3, 20),
 ])

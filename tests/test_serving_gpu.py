@@ -144,3 +144,20 @@ def test_score_request():
         S.score_request(model, store, S.ScoreRequest(1, [Candidate(1, ts), Candidate(2, ts + 1)]))
     empty = S.score_request(model, store, S.ScoreRequest(2, []))
     assert empty.probabilities == []
+
+
+@pytest.mark.parametrize("strategy", ["uniform", "recent_uniform", "learnable"])
+def test_cached_scores_other_query_strategies(strategy):
+    """Cached scoring ≡ the full forward for the non-"recent" query sets."""
+    from paper_2505_04421_b200 import serving as S
+    cfg = ModelConfig(L=256, d=16, K=4, k=16, N=2, m=3, query_strategy=strategy).validate()
+    model = _model(cfg, None, seed=7)
+    samples = synthetic_samples(cfg, 6, seed=12)
+    samples = [Sample(s.events[:n], s.user_features, Candidate(0, s.candidate.timestamp), 0)
+               for s, n in zip(samples, [256, 200, 90, 40, 9, 0])]
+    users = tensorize(samples, cfg)
+    cand = np.random.default_rng(2).integers(cfg.vocab, size=(6, 8)).astype(np.int32)
+    cache = S.build_caches_batch(model, users, [s.candidate.timestamp for s in samples])
+    p = S.score_candidates(model, cache, cand).cpu().numpy()
+    pf = model.forward(_expand(users, cand)).cpu().numpy().reshape(cand.shape)
+    assert np.max(np.abs(p - pf)) <= 2e-3, np.abs(p - pf)
