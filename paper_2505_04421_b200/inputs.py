@@ -11,6 +11,9 @@ at ``n_time_buckets - 1 <= 31``, clamping deltas to int32 max is exact.
 """
 from __future__ import annotations
 
+import gzip
+import json
+
 from dataclasses import dataclass
 from typing import Optional, Sequence
 
@@ -43,10 +46,86 @@ class Candidate:
 
 @dataclass(frozen=True)
 class Sample:
+    """One training record (pkg/src/longrec/inputs.py:55-100): ordered events, user features,
+    candidate, label.  Same JSON record layout as the reference."""
+
     events: tuple
     user_features: UserFeatures
     candidate: Candidate
     label: int
+
+    def validate(self, L_max: Optional[int] = None) -> "Sample":
+        ts = [e.timestamp for e in self.events]
+        if any(a > b for a, b in zip(ts, ts[1:])):
+            raise ConfigError("events must be sorted non-decreasing by timestamp")
+        if ts and ts[-1] > self.candidate.timestamp:
+            raise ConfigError("event timestamps must not exceed the candidate timestamp")
+        if L_max is not None and len(self.events) > L_max:
+            raise ConfigError(f"sample has {len(self.events)} events > L_max={L_max}")
+        if self.label not in (0, 1):
+            raise ConfigError("label must be 0 or 1")
+        return self
+
+    def to_json_dict(self) -> dict:
+        return {
+            "events": [{"item_id": e.item_id, "action_type": e.action_type, "timestamp": e.timestamp}
+                       for e in self.events],
+            "user_features": {"uid": self.user_features.uid,
+                              "profile_bucket": self.user_features.profile_bucket},
+            "candidate": {"item_id": self.candidate.item_id, "timestamp": self.candidate.timestamp},
+            "label": self.label,
+        }
+
+    @classmethod
+    def from_json_dict(cls, rec: dict) -> "Sample":
+        return cls(events=tuple(Event(e["item_id"], e["action_type"], e["timestamp"]) for e in rec["events"]),
+                   user_features=UserFeatures(rec["user_features"]["uid"], rec["user_features"]["profile_bucket"]),
+                   candidate=Candidate(rec["candidate"]["item_id"], rec["candidate"]["timestamp"]),
+                   label=int(rec["label"]))
+
+
+@dataclass
+class Dataset:
+    """Samples of a JSONL file (pkg/src/longrec/inputs.py:103-119)."""
+
+    samples: list
+
+    def __len__(self) -> int:
+        return len(self.samples)
+
+    def labels(self) -> np.ndarray:
+        return np.array([s.label for s in self.samples], dtype=np.int64)
+
+    def batches(self, cfg: ModelConfig, batch_size: int, pin: bool = True):
+        """Host ``Batch``es (pinned for async H2D) of ``batch_size`` samples, in file order."""
+        for i in range(0, len(self.samples), batch_size):
+            b = tensorize(self.samples[i:i + batch_size], cfg)
+            yield b.pin() if pin else b
+
+
+def save_dataset(dataset: Dataset, path: str) -> None:
+    """Newline-delimited JSON, one sample per line; ``.gz`` compresses (inputs.py:279-285)."""
+    opener = gzip.open if str(path).endswith(".gz") else open
+    with opener(path, "wt", encoding="utf-8") as fh:
+        for smp in dataset.samples:
+            fh.write(json.dumps(smp.to_json_dict(), separators=(",", ":")))
+            fh.write("\n")
+
+
+def load_dataset(path: str, L_max: Optional[int] = None) -> Dataset:
+    """Read a reference JSONL dataset (inputs.py:288-301), validating every record."""
+    opener = gzip.open if str(path).endswith(".gz") else open
+    samples = []
+    with opener(path, "rt", encoding="utf-8") as fh:
+        for line in fh:
+            line = line.strip()
+            if not line:
+                continue
+            try:
+                samples.append(Sample.from_json_dict(json.loads(line)).validate(L_max))
+            except (KeyError, TypeError, json.JSONDecodeError) as exc:
+                raise ConfigError(f"malformed dataset record: {exc}") from exc
+    return Dataset(samples)
 
 
 @dataclass
