@@ -244,13 +244,19 @@ def main():
         e0.record(stream); e1.record(stream)            # materialise the events
         probe_ev[name] = (e0, e1)
         L_.check(model._lib.longer_set_probe(ph, ctypes.c_void_p(e0.cuda_event), ctypes.c_void_p(e1.cuda_event)))
+    def mark(msg):
+        if os.environ.get("BENCH_TRACE"):
+            print(f"[bench] {msg}", file=sys.stderr, flush=True)
+
     # warm-up (eager) — also sets kernel attributes before capture
+    mark("eager warm-up")
     for i in range(2):
         load(dev_batches[i % n_batches])
         step_body()
     torch.cuda.synchronize()
     graph = None
     if not args.no_graph:
+        mark("capture")
         graph = torch.cuda.CUDAGraph(keep_graph=True)
         s = torch.cuda.Stream(dev)
         s.wait_stream(stream)
@@ -279,9 +285,11 @@ def main():
     if world > 1:
         dist.barrier()
 
+    mark("graph warm-up done")
     # ---------------- timed region: device step, inputs resident, L2 flushed between steps
     clocks = ClockSampler(local)
-    clocks.start()
+    if not os.environ.get("BENCH_NO_CLOCKS"):
+        clocks.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     torch.cuda.synchronize()
     if world > 1:
@@ -305,7 +313,9 @@ def main():
     ms = sum(a.elapsed_time(b) for a, b in ev)
     if world > 1:
         dist.barrier()
+    mark("timed region done")
     clk = clocks.stop()
+    mark("clocks stopped")
 
     # ---------------- e2e: pinned host batch → H2D, step, loss D2H, every step
     loss_host = torch.zeros(1, dtype=torch.float32).pin_memory()
@@ -314,10 +324,13 @@ def main():
     for i in range(args.steps):
         e2e_ev[i][0].record(stream)
         load(host[i % n_batches])
+        mark(f"e2e {i} loaded")
         run_step()
+        mark(f"e2e {i} replayed")
         loss_host.copy_(model._loss, non_blocking=True)
         e2e_ev[i][1].record(stream)
         e2e_ev[i][1].synchronize()
+        mark(f"e2e {i} synced")
     e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev)
 
     t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=dev)

@@ -77,9 +77,11 @@ constexpr float kRescale = 8.f;
 template <int DH>
 __global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
+  constexpr int KP = kC * DH > 128 * kC ? kC * DH : 128 * kC;
+  constexpr uint32_t TCOLS = DH > 128 ? 512 : 256;
   bf16* sQ = reinterpret_cast<bf16*>(smem_raw);
   bf16* sKP = sQ + 128 * DH;                      // K chunk (kC x DH), then P (128 x kC)
-  bf16* sV = sKP + 128 * kC;
+  bf16* sV = sKP + KP;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kC * DH);
   uint64_t* bar_a = bars;
   uint64_t* bar_d = bars + 1;
@@ -91,7 +93,7 @@ __global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a) {
     sm100::mbar_init(bar_d, 1);
     sm100::fence_barrier_init();
   }
-  if (warp == 0) sm100::tmem_alloc<256>(tmem_slot);
+  if (warp == 0) sm100::tmem_alloc<TCOLS>(tmem_slot);
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
@@ -194,42 +196,50 @@ __global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a) {
       signal();
       wait_d();                                     // O += P·V done: K|P and V tiles free
     }
-    float o[DH];
-    tmem_row<DH>(T_O + lo_lane, o);
-    if (qrow) {
-      const float rl = l > 0.f ? 1.f / l : 0.f;
-      bf16* dst = a.ctx + b * a.sc + (long long)qi * a.ldc + hd * DH;
-      float* dst32 = a.ctx32 + b * a.sc + (long long)qi * a.ldc + hd * DH;
+    const float rl = l > 0.f ? 1.f / l : 0.f;
+    bf16* dst = a.ctx + b * a.sc + (long long)qi * a.ldc + hd * DH;
+    float* dst32 = a.ctx32 + b * a.sc + (long long)qi * a.ldc + hd * DH;
+#pragma unroll 1
+    for (int c0 = 0; c0 < DH; c0 += 32) {
+      float o[32];
+      tmem_row<32>(T_O + lo_lane + c0, o);
+      if (!qrow) continue;
 #pragma unroll
-      for (int c = 0; c < DH; c += 8) {
+      for (int c = 0; c < 32; c += 8) {
         float w[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) w[u] = o[c + u] * rl;
         uint4 pk;
         pk.x = sm100::pack_bf16(w[0], w[1]); pk.y = sm100::pack_bf16(w[2], w[3]);
         pk.z = sm100::pack_bf16(w[4], w[5]); pk.w = sm100::pack_bf16(w[6], w[7]);
-        *reinterpret_cast<uint4*>(dst + c) = pk;
-        *reinterpret_cast<float4*>(dst32 + c) = make_float4(w[0], w[1], w[2], w[3]);
-        *reinterpret_cast<float4*>(dst32 + c + 4) = make_float4(w[4], w[5], w[6], w[7]);
+        *reinterpret_cast<uint4*>(dst + c0 + c) = pk;
+        *reinterpret_cast<float4*>(dst32 + c0 + c) = make_float4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<float4*>(dst32 + c0 + c + 4) = make_float4(w[4], w[5], w[6], w[7]);
       }
-      a.lse[((long long)b * a.heads + hd) * a.nq + qi] = l > 0.f ? m + __logf(l) : -INFINITY;
     }
+    if (qrow) a.lse[((long long)b * a.heads + hd) * a.nq + qi] = l > 0.f ? m + __logf(l) : -INFINITY;
   }
   sm100::tc_fence_before();
   __syncthreads();
-  if (warp == 0) sm100::tmem_dealloc<256>(tmem);
+  if (warp == 0) sm100::tmem_dealloc<TCOLS>(tmem);
 }
 
+// Head width 256 (BIG): the 512 TMEM columns hold S|dV-half, dP|dK-half and dQ (256); dV and dK come
+// out in two 128-column halves.  Shared memory keeps only QR = 64 query rows of Q, dO, P and dS
+// (nq ≤ 64, identity row order): the M = 128 MMAs read rows 64..127 from the next buffer and
+// produce rows that are never read, and the K = query contractions stop at 64.
 template <int DH>
 __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
+  constexpr bool BIG = DH > 128;
+  constexpr int QR = BIG ? 64 : 128;              // stored query rows
   bf16* sQ = reinterpret_cast<bf16*>(smem_raw);
-  bf16* sdO = sQ + 128 * DH;
-  bf16* sK = sdO + 128 * DH;
+  bf16* sdO = sQ + QR * DH;
+  bf16* sK = sdO + QR * DH;
   bf16* sV = sK + kC * DH;
-  bf16* sP = sV + kC * DH;                        // 128 x kC
-  bf16* sdS = sP + 128 * kC;                      // 128 x kC  (pre-scaled by 1/sqrt(dh))
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sdS + 128 * kC);
+  bf16* sdS = sV + kC * DH;                       // QR x kC  (pre-scaled by 1/sqrt(dh))
+  bf16* sP = sdS + QR * kC;                       // QR x kC  (after dS: dS's M-row overread stays in smem)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + QR * kC);
   uint64_t* bar_a = bars;
   uint64_t* bar_d = bars + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
@@ -262,6 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
         mma(T_B, Opnd{adO, DH, 0}, Opnd{aV, DH, 0}, DH / 16, kC, false);
         sm100::mma_commit(bar_d);
       }
+      constexpr int NH = BIG ? 2 : 1, NW = DH / NH;                // dV / dK column halves
       for (int c = 0; c < nchunk; ++c) {
         if (nchunk > 1) {           // a single chunk's S and dP are still in TMEM from pass 1
           wait_a();                                                 // K, V chunk (+ Q, dO)
@@ -269,11 +280,16 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
           mma(T_B, Opnd{adO, DH, 0}, Opnd{aV, DH, 0}, DH / 16, kC, false);   // dP
           sm100::mma_commit(bar_d);
         }
-        wait_a();                                                   // P, dS
-        mma(T_A, Opnd{aP, kC, 1}, Opnd{adO, DH, 1}, 128 / 16, DH, false);    // dV = Pᵀ·dO
-        mma(T_B, Opnd{adS, kC, 1}, Opnd{aQ, DH, 1}, 128 / 16, DH, false);    // dK = dSᵀ·Q
-        mma(T_DQ, Opnd{adS, kC, 0}, Opnd{aK, DH, 1}, kC / 16, DH, c > 0);    // dQ += dS·K
-        sm100::mma_commit(bar_d);
+        for (int h = 0; h < NH; ++h) {
+          wait_a();                                                 // P, dS (h = 1: halves read out)
+          const uint32_t co = (uint32_t)h * NW * 16;                // byte offset of column half h
+          mma(T_A, Opnd{aP, kC, 1}, Opnd{adO + co, DH, 1}, QR / 16, NW, false);   // dV = Pᵀ·dO
+          mma(T_B, Opnd{adS, kC, 1}, Opnd{aQ + co, DH, 1}, QR / 16, NW, false);   // dK = dSᵀ·Q
+          if (h == 0)
+            for (int hq = 0; hq < NH; ++hq)                                        // dQ += dS·K
+              mma(T_DQ + hq * NW, Opnd{adS, kC, 0}, Opnd{aK + (uint32_t)hq * NW * 16, DH, 1}, kC / 16, NW, c > 0);
+          sm100::mma_commit(bar_d);
+        }
       }
     }
   } else {
@@ -289,13 +305,15 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
     uint32_t pd = 0;
     auto signal = [&]() { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(bar_a); };
     auto wait_d = [&]() { sm100::mbar_wait(bar_d, pd); pd ^= 1; sm100::tc_fence_after(); };
-    const int qi = query_of_row(row);
+    const int qi = BIG ? row : query_of_row(row);
     const bool qrow = qi < a.nq;
+    if (!BIG || row < QR) {
 #pragma unroll
-    for (int c = 0; c < DH; c += 8) {
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (qrow) v = *reinterpret_cast<const uint4*>(Qb + (long long)qi * a.ldq + c);
-      *reinterpret_cast<uint4*>(sQ + canon(row, c, DH)) = v;
+      for (int c = 0; c < DH; c += 8) {
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (qrow) v = *reinterpret_cast<const uint4*>(Qb + (long long)qi * a.ldq + c);
+        *reinterpret_cast<uint4*>(sQ + canon(row, c, DH)) = v;
+      }
     }
     // dO (fp32) → bf16 tile
     float Di = 0.f, lse = -INFINITY;
@@ -303,6 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
       const float* dOr = a.dctx + b * a.sdc + (long long)qi * a.lddc + hd * DH;
 #pragma unroll
       for (int c = 0; c < DH; c += 8) {
+        if (BIG && row >= QR) break;
         float v[8];
         if (qrow) {
           const float4 x = *reinterpret_cast<const float4*>(dOr + c), y = *reinterpret_cast<const float4*>(dOr + c + 4);
@@ -358,43 +377,50 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
           s[u] = p;
           dp[u] = p * (dp[u] - Di) * scale;
         }
-        store_row(sP, row, kC, s, 32, j0);
-        store_row(sdS, row, kC, dp, 32, j0);
+        if (!BIG || row < QR) {
+          store_row(sP, row, kC, s, 32, j0);
+          store_row(sdS, row, kC, dp, 32, j0);
+        }
       }
-      signal();
-      wait_d();
-      // thread = key row: dV, dK of key c0 + row, 32 columns at a time
+      // thread = key row: dV, dK of key c0 + row, 32 columns at a time (BIG: two 128-column halves)
       const bool krow = c0 + row < a.nk;
       bf16* pv = a.dV + b * a.sdv + (long long)(c0 + row) * a.lddv + hd * DH;
       bf16* pk = a.dK + b * a.sdk + (long long)(c0 + row) * a.lddk + hd * DH;
+      constexpr int NH = BIG ? 2 : 1, NW = DH / NH;
+      for (int h = 0; h < NH; ++h) {
+        signal();
+        wait_d();
 #pragma unroll 1
-      for (int c1 = 0; c1 < DH; c1 += 32) {
-        float dv[32], dk[32];
-        tmem_row<32>(T_A + lo + c1, dv);
-        tmem_row<32>(T_B + lo + c1, dk);
-        if (!krow) continue;
+        for (int c1 = 0; c1 < NW; c1 += 32) {
+          float dv[32], dk[32];
+          tmem_row<32>(T_A + lo + c1, dv);
+          tmem_row<32>(T_B + lo + c1, dk);
+          if (!krow) continue;
 #pragma unroll
-        for (int cc = 0; cc < 32; cc += 8) {
-          uint4 x, y;
-          x.x = sm100::pack_bf16(dv[cc], dv[cc + 1]); x.y = sm100::pack_bf16(dv[cc + 2], dv[cc + 3]);
-          x.z = sm100::pack_bf16(dv[cc + 4], dv[cc + 5]); x.w = sm100::pack_bf16(dv[cc + 6], dv[cc + 7]);
-          y.x = sm100::pack_bf16(dk[cc], dk[cc + 1]); y.y = sm100::pack_bf16(dk[cc + 2], dk[cc + 3]);
-          y.z = sm100::pack_bf16(dk[cc + 4], dk[cc + 5]); y.w = sm100::pack_bf16(dk[cc + 6], dk[cc + 7]);
-          *reinterpret_cast<uint4*>(pv + c1 + cc) = x;
-          *reinterpret_cast<uint4*>(pk + c1 + cc) = y;
+          for (int cc = 0; cc < 32; cc += 8) {
+            uint4 x, y;
+            x.x = sm100::pack_bf16(dv[cc], dv[cc + 1]); x.y = sm100::pack_bf16(dv[cc + 2], dv[cc + 3]);
+            x.z = sm100::pack_bf16(dv[cc + 4], dv[cc + 5]); x.w = sm100::pack_bf16(dv[cc + 6], dv[cc + 7]);
+            y.x = sm100::pack_bf16(dk[cc], dk[cc + 1]); y.y = sm100::pack_bf16(dk[cc + 2], dk[cc + 3]);
+            y.z = sm100::pack_bf16(dk[cc + 4], dk[cc + 5]); y.w = sm100::pack_bf16(dk[cc + 6], dk[cc + 7]);
+            *reinterpret_cast<uint4*>(pv + h * NW + c1 + cc) = x;
+            *reinterpret_cast<uint4*>(pk + h * NW + c1 + cc) = y;
+          }
         }
       }
     }
-    float dq[DH];
-    tmem_row<DH>(T_DQ + lo, dq);
-    if (qrow) {
-      bf16* pq = a.dQ + b * a.sdq + (long long)qi * a.lddq + hd * DH;
+    bf16* pq = a.dQ + b * a.sdq + (long long)qi * a.lddq + hd * DH;
+#pragma unroll 1
+    for (int c0 = 0; c0 < DH; c0 += 32) {
+      float dq[32];
+      tmem_row<32>(T_DQ + lo + c0, dq);
+      if (!qrow) continue;
 #pragma unroll
-      for (int cc = 0; cc < DH; cc += 8) {
+      for (int cc = 0; cc < 32; cc += 8) {
         uint4 x;
         x.x = sm100::pack_bf16(dq[cc], dq[cc + 1]); x.y = sm100::pack_bf16(dq[cc + 2], dq[cc + 3]);
         x.z = sm100::pack_bf16(dq[cc + 4], dq[cc + 5]); x.w = sm100::pack_bf16(dq[cc + 6], dq[cc + 7]);
-        *reinterpret_cast<uint4*>(pq + cc) = x;
+        *reinterpret_cast<uint4*>(pq + c0 + cc) = x;
       }
     }
   }
@@ -405,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
 
 template <int DH>
 int launch_fwd(const AttnArgs& a, cudaStream_t st) {
-  const int smem = (128 * DH + 128 * kC + kC * DH) * 2 + 64;
+  const int smem = (128 * DH + std::max(128 * kC, kC * DH) + kC * DH) * 2 + 64;
   static int done = 0;
   if (!done) { cudaFuncSetAttribute(xattn_fwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); done = 1; }
   launch(xattn_fwd_kernel<DH>, a.B * a.heads, kThreads, std::max(smem, 80 * 1024), st, a);
@@ -414,7 +440,8 @@ int launch_fwd(const AttnArgs& a, cudaStream_t st) {
 
 template <int DH>
 int launch_bwd(const AttnArgs& a, cudaStream_t st) {
-  const int smem = (2 * 128 * DH + 2 * kC * DH + 2 * 128 * kC) * 2 + 64;
+  const int QR = DH > 128 ? 64 : 128;
+  const int smem = (2 * QR * DH + 2 * kC * DH + 2 * QR * kC) * 2 + 64;
   static int done = 0;
   if (!done) { cudaFuncSetAttribute(xattn_bwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); done = 1; }
   launch(xattn_bwd_kernel<DH>, a.B * a.heads, kThreads, std::max(smem, 116 * 1024), st, a);
@@ -425,11 +452,12 @@ int launch_bwd(const AttnArgs& a, cudaStream_t st) {
 
 int attn_tc_supported(const AttnArgs& a) {
   const int dh = a.D / a.heads;
-  return a.nq <= 128 && (dh == 32 || dh == 64 || dh == 128);
+  return (a.nq <= 128 && (dh == 32 || dh == 64 || dh == 128)) || (a.nq <= 64 && dh == 256);
 }
 
 int attn_tc_fwd(const AttnArgs& a, cudaStream_t st) {
   const int dh = a.D / a.heads;
+  if (dh == 256) return launch_fwd<256>(a, st);
   if (dh == 128) return launch_fwd<128>(a, st);
   if (dh == 64) return launch_fwd<64>(a, st);
   if (dh == 32) return launch_fwd<32>(a, st);
@@ -438,6 +466,7 @@ int attn_tc_fwd(const AttnArgs& a, cudaStream_t st) {
 
 int attn_tc_bwd(const AttnArgs& a, cudaStream_t st) {
   const int dh = a.D / a.heads;
+  if (dh == 256) return launch_bwd<256>(a, st);
   if (dh == 128) return launch_bwd<128>(a, st);
   if (dh == 64) return launch_bwd<64>(a, st);
   if (dh == 32) return launch_bwd<32>(a, st);

@@ -37,7 +37,11 @@ inline cudaStream_t g_side_stream = nullptr;
 
 inline void launch_priorities(int& lo, int& hi) {
   static int l = 1, h = 1;
-  if (l == 1) cudaDeviceGetStreamPriorityRange(&l, &h);
+  if (l == 1) {
+    cudaDeviceGetStreamPriorityRange(&l, &h);
+    const char* e = std::getenv("LONGER_PRIO");
+    if (e && e[0] == '0') h = l;                 // all launches at the default priority
+  }
   lo = l;
   hi = h;
 }
@@ -53,9 +57,11 @@ inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
   launch_priorities(lo, hi);
   cudaLaunchAttribute at[2];
   int n = 0;
-  at[n].id = cudaLaunchAttributePriority;
-  at[n].val.priority = (st != nullptr && st == g_side_stream) ? lo : hi;
-  ++n;
+  if (hi != lo) {
+    at[n].id = cudaLaunchAttributePriority;
+    at[n].val.priority = (st != nullptr && st == g_side_stream) ? lo : hi;
+    ++n;
+  }
   if (pdl_enabled()) {
     at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[n].val.programmaticStreamSerializationAllowed = 1;
