@@ -169,13 +169,18 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
   uint64_t* bar_w = bars;
   uint64_t* bar_a = bars + 1;
   uint64_t* bar_d = bars + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3);
+  uint64_t* bar_p = bars + 3;                              // [2] MMA → workers: a1 part in TMEM buffer 0 / 1
+  uint64_t* bar_h = bars + 5;                              // MMA → workers: a W2 part has consumed sH
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     sm100::mbar_init(bar_w, 1);
     sm100::mbar_init(bar_a, 32 * kWorkers);
     sm100::mbar_init(bar_d, 1);
+    sm100::mbar_init(&bar_p[0], 1);
+    sm100::mbar_init(&bar_p[1], 1);
+    sm100::mbar_init(bar_h, 1);
     sm100::fence_barrier_init();
   }
   if (warp == 0) sm100::tmem_alloc<256>(tmem_slot);
@@ -211,14 +216,25 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
         wait_a();                                // [feat | 1]
         mma(tmem, Opnd{wA, kFP, 0}, W(bo.tp, kFP), kFP / 16, DT, false);
         sm100::mma_commit(bar_d);
+        // token MLP: a1 parts run two ahead of the workers in TMEM columns [0,64) / [64,128), each
+        // buffer with its own barrier.  A buffer's next commit needs every worker's signal of the
+        // part after the one it waited for, so no barrier completes twice before a worker's wait
+        // (parity aliasing would hang); W2 parts commit to bar_h the same way.
         wait_a();                                // [x0 | 1]
         mma(tmem, Opnd{wA, XK, 0}, W(bo.w1, XK), XK / 16, 64, false);
-        sm100::mma_commit(bar_d);
+        sm100::mma_commit(&bar_p[0]);
+        if (nh > 1) {
+          mma(tmem + 64, Opnd{wA, XK, 0}, W(bo.w1 + canon(64, 0, XK), XK), XK / 16, 64, false);
+          sm100::mma_commit(&bar_p[1]);
+        }
         for (int j = 0; j < nh; ++j) {
           wait_a();                              // GELU(a1 part j) in sH
           mma(accH, Opnd{wH, 64, 0}, W(bo.w2 + canon(0, 64 * j, H2), H2), 4, DT, j > 0);
-          if (j + 1 < nh) mma(tmem, Opnd{wA, XK, 0}, W(bo.w1 + canon(64 * (j + 1), 0, XK), XK), XK / 16, 64, false);
-          sm100::mma_commit(bar_d);
+          sm100::mma_commit(bar_h);
+          if (j + 2 < nh) {
+            mma(tmem + 64 * (j & 1), Opnd{wA, XK, 0}, W(bo.w1 + canon(64 * (j + 2), 0, XK), XK), XK / 16, 64, false);
+            sm100::mma_commit(&bar_p[j & 1]);
+          }
         }
         for (int l = 0; l < a.inner_layers; ++l) {
           wait_a();                              // [LN1(x) | 1]
@@ -248,6 +264,12 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
     uint32_t pd = 0;
     auto signal = [&]() { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(bar_a); };
     auto wait_d = [&]() { sm100::mbar_wait(bar_d, pd); pd ^= 1; sm100::tc_fence_after(); };
+    uint32_t pp0 = 0, pp1 = 0, ph = 0;
+    auto wait_p = [&](int buf) {
+      if (buf) { sm100::mbar_wait(&bar_p[1], pp1); pp1 ^= 1; } else { sm100::mbar_wait(&bar_p[0], pp0); pp0 ^= 1; }
+      sm100::tc_fence_after();
+    };
+    auto wait_h = [&]() { sm100::mbar_wait(bar_h, ph); ph ^= 1; sm100::tc_fence_after(); };
     float b2[DT];                                  // narrow biases live in registers
 #pragma unroll
     for (int c = 0; c < DT; ++c) b2[c] = __ldg(a.seq_b2 + c);
@@ -288,18 +310,19 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
       signal();
       // token MLP: GELU([x0 | 1]·[W1 ; b1]) (64-column parts → sH) · W2 accumulates in TMEM
       for (int hj = 0; hj < nh; ++hj) {
-        wait_d();
+        wait_p(hj & 1);                          // a1 part hj
+        if (hj > 0) wait_h();                    // W2 of the previous part has read sH
 #pragma unroll
         for (int c0 = 0; c0 < 64; c0 += 32) {
           float hv[32];
-          tmem_row<32>(trow + c0, hv);
+          tmem_row<32>(trow + 64 * (hj & 1) + c0, hv);
 #pragma unroll
           for (int u = 0; u < 32; ++u) hv[u] = gelu_f(hv[u]);
           store_row(sH, row, 64, hv, 32, c0);
         }
         signal();
       }
-      wait_d();
+      wait_h();
       float h[DT];
       tmem_row<DT>(trow + 128, h);
 #pragma unroll
