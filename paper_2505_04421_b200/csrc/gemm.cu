@@ -263,9 +263,15 @@ int launch_bn(const GemmArgs& g, cudaStream_t st) {
 int gemm_launch(const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0) return 0;
   if (g.split_k != 1 && !(g.flags & EPI_ATOMIC)) return (int)cudaErrorInvalidValue;
+  // Widest tile that still gives the 148 SMs work: the query-row GEMMs (M = 8,960 → 70 row
+  // tiles) would otherwise leave half the machine idle at N ≤ 128.
+  const long long mt = (g.M + BM - 1) / BM;
+  auto tiles = [&](int bn) { return mt * ((g.N + bn - 1) / bn); };
+  const bool split = (g.flags & EPI_ATOMIC) != 0;           // split-K fills the machine itself
   if (g.N <= 64) return launch_bn<64>(g, st);
-  if (g.N <= 128) return launch_bn<128>(g, st);
-  return launch_bn<256>(g, st);
+  if (g.N <= 128) return (split || tiles(128) >= 120) ? launch_bn<128>(g, st) : launch_bn<64>(g, st);
+  if (split || tiles(256) >= 120) return launch_bn<256>(g, st);
+  return tiles(128) >= 120 ? launch_bn<128>(g, st) : launch_bn<64>(g, st);
 }
 
 }  // namespace longer
