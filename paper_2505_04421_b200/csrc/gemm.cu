@@ -27,32 +27,42 @@ struct Smem {
   static constexpr int TOTAL = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
+// Persistent: a CTA walks work items w = blockIdx.x + i·gridDim.x over (n-tile, m-tile, k-split).
+// The TMA ring runs continuously across items and the accumulator is double-buffered in TMEM
+// (2·BN columns), so the MMAs and loads of item i+1 overlap the epilogue of item i.
+//   tmem_full[b]  MMA → epilogue: buffer b holds a finished item (b = local item index & 1)
+//   tmem_empty[b] epilogue → MMA: buffer b drained (8 arrivals, one per epilogue warp)
+// Each buffer's barriers alternate strictly, so no phase can be skipped.
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-            GemmArgs g, int kb_per_split) {
+            GemmArgs g, int kb_per_split, int n_tiles, int m_tiles, int n_items) {
   using S = Smem<BN, STAGES>;
+  constexpr uint32_t TCOLS = 2 * BN < 32 ? 32 : 2 * BN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tmem_full = empty + STAGES;            // [2]
+  uint64_t* tmem_empty = tmem_full + 2;            // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x / 32;
-  const int n0 = blockIdx.x * BN;
-  const int m0 = blockIdx.y * BM;
   const int nkb_total = (g.K + BK - 1) / BK;
-  const int kb_begin = blockIdx.z * kb_per_split;
-  const int kb_end = min(nkb_total, kb_begin + kb_per_split);
-  const int nkb = kb_end - kb_begin;
+  auto item = [&](int w, int& n0, int& m0, int& kb_begin, int& nkb) {
+    const int x = w % n_tiles, y = (w / n_tiles) % m_tiles, z = w / (n_tiles * m_tiles);
+    n0 = x * BN;
+    m0 = y * BM;
+    kb_begin = z * kb_per_split;
+    nkb = min(nkb_total, kb_begin + kb_per_split) - kb_begin;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], 1); }
-    sm100::mbar_init(tmem_full, 1);
+    for (int b = 0; b < 2; ++b) { sm100::mbar_init(&tmem_full[b], 1); sm100::mbar_init(&tmem_empty[b], kEpiWarps); }
     sm100::fence_barrier_init();
   }
-  if (warp == 1) sm100::tmem_alloc<(BN < 32 ? 32 : BN)>(tmem_slot);
+  if (warp == 1) sm100::tmem_alloc<TCOLS>(tmem_slot);
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
@@ -64,47 +74,63 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     if (sm100::elect_one()) {
       sm100::tma_prefetch(&tmA);
       sm100::tma_prefetch(&tmB);
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % STAGES, round = i / STAGES;
-        if (i >= STAGES) sm100::mbar_wait(&empty[s], (round - 1) & 1);
-        uint8_t* sa = smem + s * S::STAGE_BYTES;
-        uint8_t* sb = sa + S::A_BYTES;
-        sm100::mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
-        const int k0 = (kb_begin + i) * BK;
-        if (!g.a_mn_major) {
-          sm100::tma_load_2d(sa, &tmA, &full[s], k0, m0);
-        } else {
-          sm100::tma_load_2d(sa, &tmA, &full[s], m0, k0);
-          sm100::tma_load_2d(sa + 8192, &tmA, &full[s], m0 + 64, k0);
-        }
-        if (!g.b_mn_major) {
-          sm100::tma_load_2d(sb, &tmB, &full[s], k0, n0);
-        } else {
+      int it = 0;
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+        int n0, m0, kb_begin, nkb;
+        item(w, n0, m0, kb_begin, nkb);
+        for (int i = 0; i < nkb; ++i, ++it) {
+          const int s = it % STAGES, round = it / STAGES;
+          if (it >= STAGES) sm100::mbar_wait(&empty[s], (round - 1) & 1);
+          uint8_t* sa = smem + s * S::STAGE_BYTES;
+          uint8_t* sb = sa + S::A_BYTES;
+          sm100::mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
+          const int k0 = (kb_begin + i) * BK;
+          if (!g.a_mn_major) {
+            sm100::tma_load_2d(sa, &tmA, &full[s], k0, m0);
+          } else {
+            sm100::tma_load_2d(sa, &tmA, &full[s], m0, k0);
+            sm100::tma_load_2d(sa + 8192, &tmA, &full[s], m0 + 64, k0);
+          }
+          if (!g.b_mn_major) {
+            sm100::tma_load_2d(sb, &tmB, &full[s], k0, n0);
+          } else {
 #pragma unroll
-          for (int j = 0; j < BN / 64; ++j) sm100::tma_load_2d(sb + j * 8192, &tmB, &full[s], n0 + 64 * j, k0);
+            for (int j = 0; j < BN / 64; ++j) sm100::tma_load_2d(sb + j * 8192, &tmB, &full[s], n0 + 64 * j, k0);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (sm100::elect_one()) {
       const uint32_t idesc = sm100::make_idesc_bf16(BM, BN, g.a_mn_major, g.b_mn_major);
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % STAGES, round = i / STAGES;
-        sm100::mbar_wait(&full[s], round & 1);
-        sm100::tc_fence_after();
-        const uint32_t sa = sm100::smem_u32(smem + s * S::STAGE_BYTES);
-        const uint32_t sb = sa + S::A_BYTES;
-#pragma unroll
-        for (int kk = 0; kk < BK / 16; ++kk) {
-          uint64_t ad = g.a_mn_major ? sm100::make_sdesc(sa + kk * 2048, 8192, 1024, sm100::LAYOUT_SW128)
-                                     : sm100::make_sdesc(sa + kk * 32, 16, 1024, sm100::LAYOUT_SW128);
-          uint64_t bd = g.b_mn_major ? sm100::make_sdesc(sb + kk * 2048, 8192, 1024, sm100::LAYOUT_SW128)
-                                     : sm100::make_sdesc(sb + kk * 32, 16, 1024, sm100::LAYOUT_SW128);
-          sm100::mma_bf16(tmem, ad, bd, idesc, (i | kk) != 0);
+      int it = 0, j = 0;
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++j) {
+        int n0, m0, kb_begin, nkb;
+        item(w, n0, m0, kb_begin, nkb);
+        const int buf = j & 1;
+        if (j >= 2) {                                 // the epilogue has drained this buffer
+          sm100::mbar_wait(&tmem_empty[buf], ((j >> 1) - 1) & 1);
+          sm100::tc_fence_after();
         }
-        sm100::mma_commit(&empty[s]);
+        const uint32_t acc = tmem + (uint32_t)(buf * BN);
+        for (int i = 0; i < nkb; ++i, ++it) {
+          const int s = it % STAGES, round = it / STAGES;
+          sm100::mbar_wait(&full[s], round & 1);
+          sm100::tc_fence_after();
+          const uint32_t sa = sm100::smem_u32(smem + s * S::STAGE_BYTES);
+          const uint32_t sb = sa + S::A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            uint64_t ad = g.a_mn_major ? sm100::make_sdesc(sa + kk * 2048, 8192, 1024, sm100::LAYOUT_SW128)
+                                       : sm100::make_sdesc(sa + kk * 32, 16, 1024, sm100::LAYOUT_SW128);
+            uint64_t bd = g.b_mn_major ? sm100::make_sdesc(sb + kk * 2048, 8192, 1024, sm100::LAYOUT_SW128)
+                                       : sm100::make_sdesc(sb + kk * 32, 16, 1024, sm100::LAYOUT_SW128);
+            sm100::mma_bf16(acc, ad, bd, idesc, (i | kk) != 0);
+          }
+          sm100::mma_commit(&empty[s]);
+        }
+        sm100::mma_commit(&tmem_full[buf]);
       }
-      sm100::mma_commit(tmem_full);
     }
   } else {
     // Epilogue warps e = 0..7: TMEM lane quarter q = warp % 4, column chunks c ≡ e/4 (mod 2).
@@ -113,8 +139,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const int e = warp - 2;
     const int q = warp & 3;
     const int lane = threadIdx.x & 31;
-    sm100::mbar_wait(tmem_full, 0);
+    int j = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++j) {
+    int n0, m0, kb_begin_unused, nkb_unused;
+    item(w, n0, m0, kb_begin_unused, nkb_unused);
+    const int buf = j & 1;
+    sm100::mbar_wait(&tmem_full[buf], (j >> 1) & 1);
     sm100::tc_fence_after();
+    const uint32_t tmem_acc = tmem + (uint32_t)(buf * BN);
     const uint32_t flags = g.flags;
     const int row = m0 + q * 32 + lane;
     const bool row_ok = row < g.M;
@@ -122,7 +154,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 #pragma unroll 1
     for (int c = (e >> 2) * 32; c < BN; c += 64) {
       uint32_t r[32];
-      sm100::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + c, r);
+      sm100::tmem_ld32(tmem_acc + ((uint32_t)(q * 32) << 16) + c, r);
       sm100::tmem_ld_wait();
       const int nb = n0 + c;
       if (!row_ok || nb >= g.N) continue;
@@ -216,10 +248,15 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         }
       }
     }
+    // this item's accumulator is drained: hand the buffer back to the MMA warp
+    sm100::tc_fence_before();
+    __syncwarp();
+    if (lane == 0) sm100::mbar_arrive(&tmem_empty[buf]);
+    }
   }
   sm100::tc_fence_before();
   __syncthreads();
-  if (warp == 1) sm100::tmem_dealloc<(BN < 32 ? 32 : BN)>(tmem);
+  if (warp == 1) sm100::tmem_dealloc<(2 * BN < 32 ? 32 : 2 * BN)>(tmem);
 }
 
 template <int BN, int STAGES>
@@ -231,7 +268,10 @@ int launch_cfg(const GemmArgs& g, const CUtensorMap& tA, const CUtensorMap& tB, 
     cudaFuncSetAttribute(gemm_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr_set = true;
   }
-  launch(gemm_kernel<BN, STAGES>, grid, kThreads, smem, st, tA, tB, g, kb_per);
+  const int n_items = (int)(grid.x * grid.y * grid.z);
+  const int ctas = std::min(n_items, 148);
+  launch(gemm_kernel<BN, STAGES>, dim3(ctas), kThreads, smem, st, tA, tB, g, kb_per, (int)grid.x, (int)grid.y,
+         n_items);
   return (int)cudaGetLastError();
 }
 

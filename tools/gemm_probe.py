@@ -8,7 +8,8 @@ sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
 from paper_2505_04421_b200 import _lib  # noqa: E402
 
 lib = _lib.load()
-shapes = [(8960, 512, 128, 0, 1), (512000, 256, 32, 0, 1), (512000, 32, 256, 0, 1), (128, 256, 512000, 1, 1)]
+shapes = [(8960, 512, 128, 0, 1), (8960, 128, 128, 0, 1), (8960, 128, 512, 0, 1), (128768, 256, 128, 0, 1),
+          (128768, 128, 256, 0, 0), (128, 256, 128768, 1, 1)]
 for M, N, K, amn, bmn in shapes:
     A = torch.randn(M, K, device="cuda").bfloat16()
     B = torch.randn(K, N, device="cuda").bfloat16()
