@@ -228,8 +228,11 @@ __global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a) {
 // out in two 128-column halves.  Shared memory keeps only QR = 64 query rows of Q, dO, P and dS
 // (nq ≤ 64, identity row order): the M = 128 MMAs read rows 64..127 from the next buffer and
 // produce rows that are never read, and the K = query contractions stop at 64.
+// Eight worker warps, two per TMEM lane quadrant: the pair shares its 32 rows and splits the
+// columns (key columns of S / dP, head columns of the loads and the dV / dK / dQ read-outs); the
+// row sums D_i meet once in shared memory after pass 1.
 template <int DH>
-__global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
+__global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   constexpr bool BIG = DH > 128;
   constexpr int QR = BIG ? 64 : 128;              // stored query rows
@@ -239,14 +242,15 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
   bf16* sV = sK + kC * DH;
   bf16* sdS = sV + kC * DH;                       // QR x kC  (pre-scaled by 1/sqrt(dh))
   bf16* sP = sdS + QR * kC;                       // QR x kC  (after dS: dS's M-row overread stays in smem)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + QR * kC);
+  float* sDp = reinterpret_cast<float*>(sP + QR * kC);       // [2][128] partial D_i of the two groups
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sDp + 256);
   uint64_t* bar_a = bars;
   uint64_t* bar_d = bars + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
   const int b = blockIdx.x / a.heads, hd = blockIdx.x % a.heads;
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    sm100::mbar_init(bar_a, 32 * kWorkers);
+    sm100::mbar_init(bar_a, 32 * 2 * kWorkers);
     sm100::mbar_init(bar_d, 1);
     sm100::fence_barrier_init();
   }
@@ -294,8 +298,15 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
     }
   } else {
     const int q = warp & 3;
+    const int grp = (warp - 1) >> 2;                 // column half of this warp pair
     const int row = q * 32 + lane;
     const uint32_t lo = (uint32_t)(q * 32) << 16;
+    constexpr int HC = DH / 2;                       // head columns per group
+    // read-out columns (32 at a time) of this group for dV / dK (per half) and dQ; at DH = 32 the
+    // first group reads all of them
+    constexpr int RW = BIG ? DH / 4 : (DH >= 64 ? DH / 2 : DH);       // dV / dK (per half)
+    const int r0 = DH >= 64 ? grp * RW : 0, r1 = DH >= 64 ? r0 + RW : (grp == 0 ? DH : 0);
+    const int q0 = DH >= 64 ? grp * HC : 0, q1 = DH >= 64 ? q0 + HC : (grp == 0 ? DH : 0);   // dQ
     const float scale = rsqrtf((float)(a.D / a.heads));
     const VisRule vis{a.k, a.G, a.ns, a.goff, a.npg[b], a.qg ? a.qg + (long long)b * a.k : nullptr, a.learn,
                      a.self_keys};
@@ -305,11 +316,20 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
     uint32_t pd = 0;
     auto signal = [&]() { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(bar_a); };
     auto wait_d = [&]() { sm100::mbar_wait(bar_d, pd); pd ^= 1; sm100::tc_fence_after(); };
+    // this group's half of a K / V chunk: key row `row`, head columns [grp·HC, grp·HC + HC)
+    auto load_half = [&](bf16* tile, const bf16* src, int ld, int nrows) {
+#pragma unroll
+      for (int c = 0; c < HC; c += 8) {
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (row < nrows) v = *reinterpret_cast<const uint4*>(src + (long long)row * ld + grp * HC + c);
+        *reinterpret_cast<uint4*>(tile + canon(row, grp * HC + c, DH)) = v;
+      }
+    };
     const int qi = BIG ? row : query_of_row(row);
     const bool qrow = qi < a.nq;
     if (!BIG || row < QR) {
 #pragma unroll
-      for (int c = 0; c < DH; c += 8) {
+      for (int c = grp * HC; c < grp * HC + HC; c += 8) {
         uint4 v = make_uint4(0, 0, 0, 0);
         if (qrow) v = *reinterpret_cast<const uint4*>(Qb + (long long)qi * a.ldq + c);
         *reinterpret_cast<uint4*>(sQ + canon(row, c, DH)) = v;
@@ -320,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
     {
       const float* dOr = a.dctx + b * a.sdc + (long long)qi * a.lddc + hd * DH;
 #pragma unroll
-      for (int c = 0; c < DH; c += 8) {
+      for (int c = grp * HC; c < grp * HC + HC; c += 8) {
         if (BIG && row >= QR) break;
         float v[8];
         if (qrow) {
@@ -340,12 +360,12 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
     // holds to rounding (D = rowsum(dO ⊙ O) would mix the bf16 roundings of dO, P and V).
     for (int c = 0; c < nchunk; ++c) {
       const int c0 = c * kC;
-      load_rows_bf16<DH>(sK, Kb + (long long)c0 * a.ldk, a.ldk, row, a.nk - c0);
-      load_rows_bf16<DH>(sV, Vb + (long long)c0 * a.ldv, a.ldv, row, a.nk - c0);
+      load_half(sK, Kb + (long long)c0 * a.ldk, a.ldk, a.nk - c0);
+      load_half(sV, Vb + (long long)c0 * a.ldv, a.ldv, a.nk - c0);
       signal();
       wait_d();
 #pragma unroll 1
-      for (int j0 = 0; j0 < kC; j0 += 32) {
+      for (int j0 = grp * (kC / 2); j0 < grp * (kC / 2) + kC / 2; j0 += 32) {
         float s[32], dp[32];
         tmem_row<32>(T_A + lo + j0, s);
         tmem_row<32>(T_B + lo + j0, dp);
@@ -357,16 +377,19 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
         }
       }
     }
+    sDp[grp * 128 + row] = Di;                       // combine the two column halves of D_i
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    Di = sDp[row] + sDp[128 + row];
     for (int c = 0; c < nchunk; ++c) {
       const int c0 = c * kC;
       if (nchunk > 1) {                 // a single chunk (K, V, S, dP) is still resident from pass 1
-        load_rows_bf16<DH>(sK, Kb + (long long)c0 * a.ldk, a.ldk, row, a.nk - c0);
-        load_rows_bf16<DH>(sV, Vb + (long long)c0 * a.ldv, a.ldv, row, a.nk - c0);
+        load_half(sK, Kb + (long long)c0 * a.ldk, a.ldk, a.nk - c0);
+        load_half(sV, Vb + (long long)c0 * a.ldv, a.ldv, a.nk - c0);
         signal();
         wait_d();
       }
 #pragma unroll 1
-      for (int j0 = 0; j0 < kC; j0 += 32) {
+      for (int j0 = grp * (kC / 2); j0 < grp * (kC / 2) + kC / 2; j0 += 32) {
         float s[32], dp[32];
         tmem_row<32>(T_A + lo + j0, s);
         tmem_row<32>(T_B + lo + j0, dp);
@@ -391,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
         signal();
         wait_d();
 #pragma unroll 1
-        for (int c1 = 0; c1 < NW; c1 += 32) {
+        for (int c1 = r0; c1 < r1; c1 += 32) {
           float dv[32], dk[32];
           tmem_row<32>(T_A + lo + c1, dv);
           tmem_row<32>(T_B + lo + c1, dk);
@@ -411,7 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1) xattn_bwd_kernel(AttnArgs a) {
     }
     bf16* pq = a.dQ + b * a.sdq + (long long)qi * a.lddq + hd * DH;
 #pragma unroll 1
-    for (int c0 = 0; c0 < DH; c0 += 32) {
+    for (int c0 = q0; c0 < q1; c0 += 32) {
       float dq[32];
       tmem_row<32>(T_DQ + lo + c0, dq);
       if (!qrow) continue;
@@ -441,10 +464,10 @@ int launch_fwd(const AttnArgs& a, cudaStream_t st) {
 template <int DH>
 int launch_bwd(const AttnArgs& a, cudaStream_t st) {
   const int QR = DH > 128 ? 64 : 128;
-  const int smem = (2 * QR * DH + 2 * kC * DH + 2 * QR * kC) * 2 + 64;
+  const int smem = (2 * QR * DH + 2 * kC * DH + 2 * QR * kC) * 2 + 256 * 4 + 64;
   static int done = 0;
   if (!done) { cudaFuncSetAttribute(xattn_bwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); done = 1; }
-  launch(xattn_bwd_kernel<DH>, a.B * a.heads, kThreads, std::max(smem, 116 * 1024), st, a);
+  launch(xattn_bwd_kernel<DH>, a.B * a.heads, kThreads8, std::max(smem, 116 * 1024), st, a);
   return (int)cudaGetLastError();
 }
 
