@@ -12,8 +12,10 @@
 // dV = Pᵀ·dO, dK = dSᵀ·Q (thread = key row on readout), dQ += dS·K accumulated in TMEM.
 #include "fe_common.cuh"
 #include "ops.cuh"
+#include "tma.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace longer {
 
@@ -231,12 +233,16 @@ __global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a) {
 // Eight worker warps, two per TMEM lane quadrant: the pair shares its 32 rows and splits the
 // columns (key columns of S / dP, head columns of the loads and the dV / dK / dQ read-outs); the
 // row sums D_i meet once in shared memory after pass 1.
-template <int DH>
-__global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a) {
+// TMA (head width ≥ 64): the MMA thread streams each K / V chunk with 3-D tensor maps ([sample]
+// [key][column], rows past the sample's keys read as zero) into 128-byte-swizzled tiles, issuing
+// the next chunk as soon as the MMAs reading the current one have completed.
+template <int DH, bool TMA>
+__global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, const __grid_constant__ CUtensorMap tmK,
+                                                                  const __grid_constant__ CUtensorMap tmV) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   constexpr bool BIG = DH > 128;
   constexpr int QR = BIG ? 64 : 128;              // stored query rows
-  bf16* sQ = reinterpret_cast<bf16*>(smem_raw);
+  bf16* sQ = reinterpret_cast<bf16*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   bf16* sdO = sQ + QR * DH;
   bf16* sK = sdO + QR * DH;
   bf16* sV = sK + kC * DH;
@@ -246,12 +252,16 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(sDp + 256);
   uint64_t* bar_a = bars;
   uint64_t* bar_d = bars + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+  uint64_t* bar_kv = bars + 2;                    // TMA: K / V chunk landed
+  uint64_t* bar_m = bars + 3;                     // TMA: the MMAs reading the chunk are done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
   const int b = blockIdx.x / a.heads, hd = blockIdx.x % a.heads;
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     sm100::mbar_init(bar_a, 32 * 2 * kWorkers);
     sm100::mbar_init(bar_d, 1);
+    sm100::mbar_init(bar_kv, 1);
+    sm100::mbar_init(bar_m, 1);
     sm100::fence_barrier_init();
   }
   if (warp == 0) sm100::tmem_alloc<512>(tmem_slot);
@@ -268,20 +278,51 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a) {
     if (lane == 0) {
       const uint32_t aQ = sm100::smem_u32(sQ), adO = sm100::smem_u32(sdO), aK = sm100::smem_u32(sK);
       const uint32_t aV = sm100::smem_u32(sV), aP = sm100::smem_u32(sP), adS = sm100::smem_u32(sdS);
-      uint32_t pa = 0;
+      uint32_t pa = 0, pkv = 0, pm = 0;
       auto wait_a = [&]() { sm100::mbar_wait(bar_a, pa); pa ^= 1; sm100::tc_fence_after(); };
+      auto load_kv = [&](int c) {
+        sm100::mbar_arrive_expect_tx(bar_kv, 2 * kC * DH * 2);
+#pragma unroll
+        for (int i = 0; i < DH / 64; ++i) {
+          sm100::tma_load_3d(sK + i * kC * 64, &tmK, bar_kv, hd * DH + 64 * i, c * kC, b);
+          sm100::tma_load_3d(sV + i * kC * 64, &tmV, bar_kv, hd * DH + 64 * i, c * kC, b);
+        }
+      };
+      auto wait_kv = [&]() { sm100::mbar_wait(bar_kv, pkv); pkv ^= 1; };
+      auto mma_done = [&]() { sm100::mma_commit(bar_m); sm100::mbar_wait(bar_m, pm); pm ^= 1; };
+      // S = Q·Kᵀ and dP = dO·Vᵀ of the resident chunk
+      auto mma_s_dp = [&]() {
+        if constexpr (TMA) {
+          mma(T_A, Opnd{aQ, DH, 0}, OpndSW{aK, kC, 0}, DH / 16, kC, false);
+          mma(T_B, Opnd{adO, DH, 0}, OpndSW{aV, kC, 0}, DH / 16, kC, false);
+        } else {
+          mma(T_A, Opnd{aQ, DH, 0}, Opnd{aK, DH, 0}, DH / 16, kC, false);
+          mma(T_B, Opnd{adO, DH, 0}, Opnd{aV, DH, 0}, DH / 16, kC, false);
+        }
+      };
+      if constexpr (TMA) {
+        sm100::tma_prefetch(&tmK);
+        sm100::tma_prefetch(&tmV);
+        load_kv(0);
+      }
       for (int c = 0; c < nchunk; ++c) {                            // pass 1: D = Σ_j P·dP
         wait_a();
-        mma(T_A, Opnd{aQ, DH, 0}, Opnd{aK, DH, 0}, DH / 16, kC, false);
-        mma(T_B, Opnd{adO, DH, 0}, Opnd{aV, DH, 0}, DH / 16, kC, false);
+        if constexpr (TMA) wait_kv();
+        mma_s_dp();
         sm100::mma_commit(bar_d);
+        if constexpr (TMA) {
+          if (nchunk > 1) {                                         // next chunk (pass 2: chunk 0)
+            mma_done();
+            load_kv(c + 1 < nchunk ? c + 1 : 0);
+          }
+        }
       }
       constexpr int NH = BIG ? 2 : 1, NW = DH / NH;                // dV / dK column halves
       for (int c = 0; c < nchunk; ++c) {
         if (nchunk > 1) {           // a single chunk's S and dP are still in TMEM from pass 1
           wait_a();                                                 // K, V chunk (+ Q, dO)
-          mma(T_A, Opnd{aQ, DH, 0}, Opnd{aK, DH, 0}, DH / 16, kC, false);    // S
-          mma(T_B, Opnd{adO, DH, 0}, Opnd{aV, DH, 0}, DH / 16, kC, false);   // dP
+          if constexpr (TMA) wait_kv();
+          mma_s_dp();
           sm100::mma_commit(bar_d);
         }
         for (int h = 0; h < NH; ++h) {
@@ -290,9 +331,20 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a) {
           mma(T_A, Opnd{aP, kC, 1}, Opnd{adO + co, DH, 1}, QR / 16, NW, false);   // dV = Pᵀ·dO
           mma(T_B, Opnd{adS, kC, 1}, Opnd{aQ + co, DH, 1}, QR / 16, NW, false);   // dK = dSᵀ·Q
           if (h == 0)
-            for (int hq = 0; hq < NH; ++hq)                                        // dQ += dS·K
-              mma(T_DQ + hq * NW, Opnd{adS, kC, 0}, Opnd{aK + (uint32_t)hq * NW * 16, DH, 1}, kC / 16, NW, c > 0);
+            for (int hq = 0; hq < NH; ++hq) {                                      // dQ += dS·K
+              if constexpr (TMA)
+                mma(T_DQ + hq * NW, Opnd{adS, kC, 0}, OpndSW{aK + (uint32_t)hq * (NW / 64) * kC * 128, kC, 1},
+                    kC / 16, NW, c > 0);
+              else
+                mma(T_DQ + hq * NW, Opnd{adS, kC, 0}, Opnd{aK + (uint32_t)hq * NW * 16, DH, 1}, kC / 16, NW, c > 0);
+            }
           sm100::mma_commit(bar_d);
+        }
+        if constexpr (TMA) {
+          if (nchunk > 1 && c + 1 < nchunk) {
+            mma_done();
+            load_kv(c + 1);
+          }
         }
       }
     }
@@ -360,8 +412,10 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a) {
     // holds to rounding (D = rowsum(dO ⊙ O) would mix the bf16 roundings of dO, P and V).
     for (int c = 0; c < nchunk; ++c) {
       const int c0 = c * kC;
-      load_half(sK, Kb + (long long)c0 * a.ldk, a.ldk, a.nk - c0);
-      load_half(sV, Vb + (long long)c0 * a.ldv, a.ldv, a.nk - c0);
+      if constexpr (!TMA) {
+        load_half(sK, Kb + (long long)c0 * a.ldk, a.ldk, a.nk - c0);
+        load_half(sV, Vb + (long long)c0 * a.ldv, a.ldv, a.nk - c0);
+      }
       signal();
       wait_d();
 #pragma unroll 1
@@ -383,8 +437,10 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a) {
     for (int c = 0; c < nchunk; ++c) {
       const int c0 = c * kC;
       if (nchunk > 1) {                 // a single chunk (K, V, S, dP) is still resident from pass 1
-        load_half(sK, Kb + (long long)c0 * a.ldk, a.ldk, a.nk - c0);
-        load_half(sV, Vb + (long long)c0 * a.ldv, a.ldv, a.nk - c0);
+        if constexpr (!TMA) {
+          load_half(sK, Kb + (long long)c0 * a.ldk, a.ldk, a.nk - c0);
+          load_half(sV, Vb + (long long)c0 * a.ldv, a.ldv, a.nk - c0);
+        }
         signal();
         wait_d();
       }
@@ -461,14 +517,39 @@ int launch_fwd(const AttnArgs& a, cudaStream_t st) {
   return (int)cudaGetLastError();
 }
 
+template <int DH, bool TMA>
+int launch_bwd_t(const AttnArgs& a, const CUtensorMap& tK, const CUtensorMap& tV, cudaStream_t st) {
+  const int QR = DH > 128 ? 64 : 128;
+  const int smem = (2 * QR * DH + 2 * kC * DH + 2 * QR * kC) * 2 + 256 * 4 + 64 + 1024;
+  static int done = 0;
+  if (!done) {
+    cudaFuncSetAttribute(xattn_bwd_kernel<DH, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    done = 1;
+  }
+  launch(xattn_bwd_kernel<DH, TMA>, a.B * a.heads, kThreads8, std::max(smem, 116 * 1024), st, a, tK, tV);
+  return (int)cudaGetLastError();
+}
+
+// K / V tensor maps [B][nk][D] over the strided projections; falls back to thread loads when the
+// strides or base addresses do not meet TMA's 16-byte rules.
 template <int DH>
 int launch_bwd(const AttnArgs& a, cudaStream_t st) {
-  const int QR = DH > 128 ? 64 : 128;
-  const int smem = (2 * QR * DH + 2 * kC * DH + 2 * QR * kC) * 2 + 256 * 4 + 64;
-  static int done = 0;
-  if (!done) { cudaFuncSetAttribute(xattn_bwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); done = 1; }
-  launch(xattn_bwd_kernel<DH>, a.B * a.heads, kThreads8, std::max(smem, 116 * 1024), st, a);
-  return (int)cudaGetLastError();
+  CUtensorMap tK{}, tV{};
+  const char* env = std::getenv("LONGER_ATTN_TMA");                 // LONGER_ATTN_TMA=0: thread loads
+  bool tma_ok = DH >= 64 && !(env && env[0] == '0');
+  auto aligned = [](const void* p, long long ld, long long sb) {
+    return (reinterpret_cast<uintptr_t>(p) & 15) == 0 && ld % 8 == 0 && sb % 8 == 0;
+  };
+  if (tma_ok) tma_ok = aligned(a.Kp, a.ldk, a.sk) && aligned(a.V, a.ldv, a.sv);
+  if (tma_ok) {
+    const long long cols = (long long)a.heads * DH;
+    tma_ok = tma::encode_3d_bf16(&tK, a.Kp, cols, a.nk, a.B, a.ldk, a.sk, 64, kC) == 0 &&
+             tma::encode_3d_bf16(&tV, a.V, cols, a.nk, a.B, a.ldv, a.sv, 64, kC) == 0;
+  }
+  if constexpr (DH >= 64) {
+    if (tma_ok) return launch_bwd_t<DH, true>(a, tK, tV, st);
+  }
+  return launch_bwd_t<DH, false>(a, tK, tV, st);
 }
 
 }  // namespace

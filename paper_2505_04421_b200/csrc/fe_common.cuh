@@ -88,8 +88,22 @@ struct Opnd {
   }
 };
 
+// Operand view of a [rows][64·nb] tile written by TMA as nb column blocks of 64 (128-byte swizzle,
+// block stride rows·128 bytes).  mn = 0: K-major (contraction over the columns, N = rows);
+// mn = 1: MN-major (contraction over the rows, N = the columns).
+struct OpndSW {
+  uint32_t addr;
+  int rows;
+  int mn;
+  __device__ __forceinline__ uint64_t desc(int ks) const {
+    return mn ? sm100::make_sdesc(addr + ks * 2048, rows * 128, 1024, sm100::LAYOUT_SW128)
+              : sm100::make_sdesc(addr + (ks >> 2) * rows * 128 + (ks & 3) * 32, 16, 1024, sm100::LAYOUT_SW128);
+  }
+};
+
 // D[tmem, 128 x N] (+)= A · B over `kslices` K-slices of 16 (single thread)
-__device__ __forceinline__ void mma(uint32_t tmem_d, const Opnd& A, const Opnd& B, int kslices, int N, bool acc) {
+template <class OA, class OB>
+__device__ __forceinline__ void mma(uint32_t tmem_d, const OA& A, const OB& B, int kslices, int N, bool acc) {
   const uint32_t idesc = sm100::make_idesc_bf16(128, N, A.mn, B.mn);
   for (int ks = 0; ks < kslices; ++ks)
     sm100::mma_bf16(tmem_d, A.desc(ks), B.desc(ks), idesc, (acc || ks > 0) ? 1u : 0u);

@@ -39,5 +39,21 @@ inline int encode_2d_bf16(CUtensorMap* m, const void* base, long long dim0, long
   return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
 }
 
+// 3-D bf16 tensor [dim2][dim1][dim0]: strides ld1, ld2 elements (multiples of 8); box box0 x box1 x 1.
+inline int encode_3d_bf16(CUtensorMap* m, const void* base, long long dim0, long long dim1, long long dim2,
+                          long long ld1, long long ld2, int box0, int box1,
+                          CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return (int)cudaErrorNotSupported;
+  cuuint64_t dims[3] = {(cuuint64_t)dim0, (cuuint64_t)dim1, (cuuint64_t)dim2};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld1 * 2), (cuuint64_t)(ld2 * 2)};
+  cuuint32_t box[3] = {(cuuint32_t)box0, (cuuint32_t)box1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
+}
+
 }  // namespace tma
 }  // namespace longer
