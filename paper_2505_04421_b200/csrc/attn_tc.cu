@@ -76,23 +76,30 @@ __device__ __forceinline__ uint32_t vis_bits(int lo, int hi, int j0) {
 // Shared memory: Q + K|P + V (96 KB at head width 128) → two CTAs per SM.
 constexpr float kRescale = 8.f;
 
-template <int DH>
-__global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a) {
+// TMA (head width ≥ 64): K / V chunks arrive by 3-D TMA into 128-byte-swizzled tiles, the next
+// chunk issued by the MMA thread as soon as O += P·V of the current one has completed.
+template <int DH, bool TMA>
+__global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a, const __grid_constant__ CUtensorMap tmK,
+                                                                 const __grid_constant__ CUtensorMap tmV) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   constexpr int KP = kC * DH > 128 * kC ? kC * DH : 128 * kC;
   constexpr uint32_t TCOLS = DH > 128 ? 512 : 256;
-  bf16* sQ = reinterpret_cast<bf16*>(smem_raw);
+  bf16* sQ = reinterpret_cast<bf16*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   bf16* sKP = sQ + 128 * DH;                      // K chunk (kC x DH), then P (128 x kC)
   bf16* sV = sKP + KP;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kC * DH);
   uint64_t* bar_a = bars;
   uint64_t* bar_d = bars + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+  uint64_t* bar_kv = bars + 2;
+  uint64_t* bar_m = bars + 3;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
   const int b = blockIdx.x / a.heads, hd = blockIdx.x % a.heads;
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     sm100::mbar_init(bar_a, 32 * kWorkers);
     sm100::mbar_init(bar_d, 1);
+    sm100::mbar_init(bar_kv, 1);
+    sm100::mbar_init(bar_m, 1);
     sm100::fence_barrier_init();
   }
   if (warp == 0) sm100::tmem_alloc<TCOLS>(tmem_slot);
@@ -108,15 +115,45 @@ __global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a) {
   if (warp == 0) {
     if (lane == 0) {
       const uint32_t aQ = sm100::smem_u32(sQ), aKP = sm100::smem_u32(sKP), aV = sm100::smem_u32(sV);
-      uint32_t pa = 0;
+      uint32_t pa = 0, pkv = 0, pm = 0;
       auto wait_a = [&]() { sm100::mbar_wait(bar_a, pa); pa ^= 1; sm100::tc_fence_after(); };
+      auto load_kv = [&](int c) {
+        sm100::mbar_arrive_expect_tx(bar_kv, 2 * kC * DH * 2);
+#pragma unroll
+        for (int i = 0; i < DH / 64; ++i) {
+          sm100::tma_load_3d(sKP + i * kC * 64, &tmK, bar_kv, hd * DH + 64 * i, c * kC, b);
+          sm100::tma_load_3d(sV + i * kC * 64, &tmV, bar_kv, hd * DH + 64 * i, c * kC, b);
+        }
+      };
+      if constexpr (TMA) {
+        sm100::tma_prefetch(&tmK);
+        sm100::tma_prefetch(&tmV);
+        load_kv(0);
+      }
       for (int c = 0; c < nchunk; ++c) {
-        wait_a();                                   // K_c, V_c staged
-        mma(T_S, Opnd{aQ, DH, 0}, Opnd{aKP, DH, 0}, DH / 16, kC, false);
+        wait_a();                                   // K_c, V_c staged (TMA: Q staged, TMEM S free)
+        if constexpr (TMA) {
+          sm100::mbar_wait(bar_kv, pkv);
+          pkv ^= 1;
+          mma(T_S, Opnd{aQ, DH, 0}, OpndSW{aKP, kC, 0}, DH / 16, kC, false);
+        } else {
+          mma(T_S, Opnd{aQ, DH, 0}, Opnd{aKP, DH, 0}, DH / 16, kC, false);
+        }
         sm100::mma_commit(bar_d);
         wait_a();                                   // P_c staged (and O rescaled)
-        mma(T_O, Opnd{aKP, kC, 0}, Opnd{aV, DH, 1}, kC / 16, DH, c > 0);
+        if constexpr (TMA)
+          mma(T_O, Opnd{aKP, kC, 0}, OpndSW{aV, kC, 1}, kC / 16, DH, c > 0);
+        else
+          mma(T_O, Opnd{aKP, kC, 0}, Opnd{aV, DH, 1}, kC / 16, DH, c > 0);
         sm100::mma_commit(bar_d);
+        if constexpr (TMA) {
+          if (c + 1 < nchunk) {                     // K|P and V free once O += P·V has completed
+            sm100::mma_commit(bar_m);
+            sm100::mbar_wait(bar_m, pm);
+            pm ^= 1;
+            load_kv(c + 1);
+          }
+        }
       }
     }
   } else {
@@ -145,8 +182,10 @@ __global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a) {
     float m = -INFINITY, l = 0.f;
     for (int c = 0; c < nchunk; ++c) {
       const int c0 = c * kC;
-      load_rows_bf16<DH>(sKP, Kb + (long long)c0 * a.ldk, a.ldk, row, a.nk - c0);
-      load_rows_bf16<DH>(sV, Vb + (long long)c0 * a.ldv, a.ldv, row, a.nk - c0);
+      if constexpr (!TMA) {
+        load_rows_bf16<DH>(sKP, Kb + (long long)c0 * a.ldk, a.ldk, row, a.nk - c0);
+        load_rows_bf16<DH>(sV, Vb + (long long)c0 * a.ldv, a.ldv, row, a.nk - c0);
+      }
       signal();
       wait_d();                                     // S_c ready (K tile dead)
       float cm = -INFINITY;
@@ -508,13 +547,40 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
   if (warp == 0) sm100::tmem_dealloc<512>(tmem);
 }
 
+// K / V tensor maps [B][nk][D] over the strided projections (false: the strides or base addresses
+// miss TMA's 16-byte rules, or LONGER_ATTN_TMA=0 → thread loads).
+template <int DH>
+bool kv_maps(const AttnArgs& a, CUtensorMap& tK, CUtensorMap& tV) {
+  const char* env = std::getenv("LONGER_ATTN_TMA");
+  if (DH < 64 || (env && env[0] == '0')) return false;
+  auto aligned = [](const void* p, long long ld, long long sb) {
+    return (reinterpret_cast<uintptr_t>(p) & 15) == 0 && ld % 8 == 0 && sb % 8 == 0;
+  };
+  if (!aligned(a.Kp, a.ldk, a.sk) || !aligned(a.V, a.ldv, a.sv)) return false;
+  const long long cols = (long long)a.heads * DH;
+  return tma::encode_3d_bf16(&tK, a.Kp, cols, a.nk, a.B, a.ldk, a.sk, 64, kC) == 0 &&
+         tma::encode_3d_bf16(&tV, a.V, cols, a.nk, a.B, a.ldv, a.sv, 64, kC) == 0;
+}
+
+template <int DH, bool TMA>
+int launch_fwd_t(const AttnArgs& a, const CUtensorMap& tK, const CUtensorMap& tV, cudaStream_t st) {
+  const int smem = (128 * DH + std::max(128 * kC, kC * DH) + kC * DH) * 2 + 64 + 1024;
+  static int done = 0;
+  if (!done) {
+    cudaFuncSetAttribute(xattn_fwd_kernel<DH, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    done = 1;
+  }
+  launch(xattn_fwd_kernel<DH, TMA>, a.B * a.heads, kThreads, std::max(smem, 80 * 1024), st, a, tK, tV);
+  return (int)cudaGetLastError();
+}
+
 template <int DH>
 int launch_fwd(const AttnArgs& a, cudaStream_t st) {
-  const int smem = (128 * DH + std::max(128 * kC, kC * DH) + kC * DH) * 2 + 64;
-  static int done = 0;
-  if (!done) { cudaFuncSetAttribute(xattn_fwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); done = 1; }
-  launch(xattn_fwd_kernel<DH>, a.B * a.heads, kThreads, std::max(smem, 80 * 1024), st, a);
-  return (int)cudaGetLastError();
+  CUtensorMap tK{}, tV{};
+  if constexpr (DH >= 64) {
+    if (kv_maps<DH>(a, tK, tV)) return launch_fwd_t<DH, true>(a, tK, tV, st);
+  }
+  return launch_fwd_t<DH, false>(a, tK, tV, st);
 }
 
 template <int DH, bool TMA>
@@ -530,24 +596,11 @@ int launch_bwd_t(const AttnArgs& a, const CUtensorMap& tK, const CUtensorMap& tV
   return (int)cudaGetLastError();
 }
 
-// K / V tensor maps [B][nk][D] over the strided projections; falls back to thread loads when the
-// strides or base addresses do not meet TMA's 16-byte rules.
 template <int DH>
 int launch_bwd(const AttnArgs& a, cudaStream_t st) {
   CUtensorMap tK{}, tV{};
-  const char* env = std::getenv("LONGER_ATTN_TMA");                 // LONGER_ATTN_TMA=0: thread loads
-  bool tma_ok = DH >= 64 && !(env && env[0] == '0');
-  auto aligned = [](const void* p, long long ld, long long sb) {
-    return (reinterpret_cast<uintptr_t>(p) & 15) == 0 && ld % 8 == 0 && sb % 8 == 0;
-  };
-  if (tma_ok) tma_ok = aligned(a.Kp, a.ldk, a.sk) && aligned(a.V, a.ldv, a.sv);
-  if (tma_ok) {
-    const long long cols = (long long)a.heads * DH;
-    tma_ok = tma::encode_3d_bf16(&tK, a.Kp, cols, a.nk, a.B, a.ldk, a.sk, 64, kC) == 0 &&
-             tma::encode_3d_bf16(&tV, a.V, cols, a.nk, a.B, a.ldv, a.sv, 64, kC) == 0;
-  }
   if constexpr (DH >= 64) {
-    if (tma_ok) return launch_bwd_t<DH, true>(a, tK, tV, st);
+    if (kv_maps<DH>(a, tK, tV)) return launch_bwd_t<DH, true>(a, tK, tV, st);
   }
   return launch_bwd_t<DH, false>(a, tK, tV, st);
 }
