@@ -13,6 +13,7 @@
 #include "fe_common.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace longer {
 
@@ -507,7 +508,7 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
   float* s_gpos = s_pos + kTile * (DT + 1);                         // 128 x (DT+1)
   float* s_item = s_gpos + kTile * (DT + 1);
   const int n_item = a.vocab * a.d_item;
-  const bool item_smem = n_item <= 16384;
+  const bool item_smem = a.item_smem && n_item <= 16384;
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_item + (item_smem ? n_item : 0) + 2);
   bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(bars) + 7) & ~uintptr_t(7));
   uint64_t* bar_w = bars;
@@ -879,7 +880,10 @@ static int launch_mlp_bwd(const FrontArgs& a, cudaStream_t st) {
   const int H2 = 2 * DT * a.K;
   const int XK = DT + 16;
   const int n_item = a.vocab * a.d_item;
-  const int tab = (n_item <= 16384) ? n_item : 0;
+  const char* env = std::getenv("LONGER_ITEM_SMEM");
+  FrontArgs b = a;
+  b.item_smem = !(env && env[0] == '0');
+  const int tab = (b.item_smem && n_item <= 16384) ? n_item : 0;
   const int smem = (2 * DT * kFP + 2 * H2 * DT + H2 * XK) * 2 + kTile * (kFP + XK + DT + 128 + 128 + 64 + 64) * 2 +
                    (2 * kTile * (DT + 1) + tab) * 4 + 128;
   if (smem > 227 * 1024) return (int)cudaErrorInvalidValue;
@@ -892,7 +896,7 @@ static int launch_mlp_bwd(const FrontArgs& a, cudaStream_t st) {
   const int tps = (a.Lp + kTile - 1) / kTile;
   const int r = std::max(1, std::min(a.B, 148 / tps));
   // > 113 KB of smem keeps one CTA per SM (the kernel allocates all 512 TMEM columns)
-  launch(fe_mlp_bwd_kernel<DT>, tps * r, kThreads8, std::max(smem, 116 * 1024), st, a);
+  launch(fe_mlp_bwd_kernel<DT>, tps * r, kThreads8, std::max(smem, 116 * 1024), st, b);
   return (int)cudaGetLastError();
 }
 

@@ -17,6 +17,7 @@ struct FrontArgs {
   // batch
   const int32_t *items, *actions, *dt, *n_events;
   int B, L, Lp, K, d, d_item, d_act, d_time, nb, vocab, n_actions, inner_layers;
+  int item_smem = 1;           // fe_mlp_bwd: stage the item-table gradient in shared memory when it fits
   long long T;                 // B * Lp tokens
   // fp32 master parameters (biases, tables)
   const float *item_tab, *act_tab, *time_tab, *pos_tab, *tok_w, *tok_b, *seq_b1, *seq_b2;
