@@ -347,7 +347,8 @@ def main():
         fps = flops_per_sample(cfg)
         achieved = value / world * fps / 1e12
         pf = phase_flops(cfg, B)
-        dom = max(phase_ms, key=lambda k: phase_ms[k]) if phase_ms else None
+        kern_ms = {k: v for k, v in phase_ms.items() if k in pf}         # sections are not kernels
+        dom = max(kern_ms, key=lambda k: kern_ms[k]) if kern_ms else None
         kernels, sections = {}, {}
         for k, tms in phase_ms.items():
             if k not in pf:
