@@ -9,6 +9,7 @@
 #include "common.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace longer {
 
@@ -24,7 +25,8 @@ struct Smem {
   static constexpr int A_BYTES = BM * BK * 2;        // 16 KB
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int TOTAL = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int STG_BYTES = 4096;             // per epilogue warp: a 32 x 32 fp32 chunk
+  static constexpr int TOTAL = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + 8 * STG_BYTES;
 };
 
 // Persistent: a CTA walks work items w = blockIdx.x + i·gridDim.x over (n-tile, m-tile, k-split).
@@ -139,6 +141,41 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const int e = warp - 2;
     const int q = warp & 3;
     const int lane = threadIdx.x & 31;
+    // Staged stores: the warp's 32 rows x 32 columns go through its own smem buffer (XOR-swizzled
+    // 16-byte segments, conflict-free both ways) and leave as whole 64 / 128-byte row segments, so
+    // each store instruction fills its sectors instead of writing 16 bytes into 32 different rows.
+    uint4* stg = reinterpret_cast<uint4*>(smem + STAGES * S::STAGE_BYTES + 256 + e * S::STG_BYTES);
+    const bool staged = g.staged != 0;
+    auto store_bf16 = [&](void* base, int ld, int m_base, int nb, const float* v) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        stg[lane * 4 + (j ^ ((lane >> 1) & 3))] =
+            make_uint4(sm100::pack_bf16(v[8 * j], v[8 * j + 1]), sm100::pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                       sm100::pack_bf16(v[8 * j + 4], v[8 * j + 5]), sm100::pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int r = k * 8 + (lane >> 2), sgm = lane & 3;
+        const uint4 val = stg[r * 4 + (sgm ^ ((r >> 1) & 3))];
+        if (m_base + r < g.M)
+          *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(base) + (size_t)(m_base + r) * ld + nb + sgm * 8) = val;
+      }
+      __syncwarp();
+    };
+    auto store_f32 = [&](float* base, int ld, int m_base, int nb, const float* v) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        stg[lane * 8 + (j ^ (lane & 7))] = make_uint4(__float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+                                                      __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int r = k * 4 + (lane >> 3), sgm = lane & 7;
+        const uint4 val = stg[r * 8 + (sgm ^ (r & 7))];
+        if (m_base + r < g.M) *reinterpret_cast<uint4*>(base + (size_t)(m_base + r) * ld + nb + sgm * 4) = val;
+      }
+      __syncwarp();
+    };
     int j = 0;
     for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++j) {
     int n0, m0, kb_begin_unused, nkb_unused;
@@ -157,10 +194,68 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       sm100::tmem_ld32(tmem_acc + ((uint32_t)(q * 32) << 16) + c, r);
       sm100::tmem_ld_wait();
       const int nb = n0 + c;
-      if (!row_ok || nb >= g.N) continue;
+      if (nb >= g.N) continue;                                   // warp-uniform
+      const int m_base = m0 + q * 32;
       float v[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+      if (staged && nb + 32 <= g.N) {
+        // warp-collective path: rows past M compute on zeros and are never stored
+        if (flags & EPI_BIAS) {
+          const float4* bp = reinterpret_cast<const float4*>(g.bias + nb);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 b4 = __ldg(bp + j);
+            v[4 * j] += b4.x; v[4 * j + 1] += b4.y; v[4 * j + 2] += b4.z; v[4 * j + 3] += b4.w;
+          }
+        }
+        if (flags & EPI_SAVE_PRE) store_bf16(g.pre_bf16, g.ldc_bf, m_base, nb, v);
+        if (flags & EPI_GELU) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
+        }
+        if ((flags & EPI_GELU_BWD) && row_ok) {
+          const uint4* pp = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(g.pre_bf16) +
+                                                           (size_t)row * g.ldc_bf + nb);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint4 p4 = pp[j];
+            const uint32_t w[4] = {p4.x, p4.y, p4.z, p4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              v[8 * j + 2 * u] *= gelu_grad_f(sm100::bf16_lo(w[u]));
+              v[8 * j + 2 * u + 1] *= gelu_grad_f(sm100::bf16_hi(w[u]));
+            }
+          }
+        }
+        if ((flags & EPI_RESID) && row_ok) {
+          const float4* rp = reinterpret_cast<const float4*>(g.resid + (size_t)row * g.ldr + nb);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 r4 = rp[j];
+            v[4 * j] += r4.x; v[4 * j + 1] += r4.y; v[4 * j + 2] += r4.z; v[4 * j + 3] += r4.w;
+          }
+        }
+        if (flags & EPI_ROWMASK) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] *= rmask;
+        }
+        if (flags & EPI_OUT_F32) {
+          if (flags & EPI_ATOMIC) {
+            if (row_ok) {
+              float4* cp = reinterpret_cast<float4*>(g.C + (size_t)row * g.ldc + nb);
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                atomicAdd(cp + j, make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+            }
+          } else {
+            store_f32(g.C, g.ldc, m_base, nb, v);
+          }
+        }
+        if (flags & EPI_OUT_BF16) store_bf16(g.C_bf16, g.ldc_bf, m_base, nb, v);
+        continue;
+      }
+      if (!row_ok) continue;
       if (nb + 32 <= g.N) {
         if (flags & EPI_BIAS) {
           const float4* bp = reinterpret_cast<const float4*>(g.bias + nb);
@@ -270,7 +365,16 @@ int launch_cfg(const GemmArgs& g, const CUtensorMap& tA, const CUtensorMap& tB, 
   }
   const int n_items = (int)(grid.x * grid.y * grid.z);
   const int ctas = std::min(n_items, 148);
-  launch(gemm_kernel<BN, STAGES>, dim3(ctas), kThreads, smem, st, tA, tB, g, kb_per, (int)grid.x, (int)grid.y,
+  GemmArgs ga = g;
+  if (ga.staged < 0) {
+    static int env = -1;
+    if (env < 0) {
+      const char* e = std::getenv("LONGER_GEMM_STAGE");
+      env = (e && e[0] == '0') ? 0 : 1;
+    }
+    ga.staged = env;
+  }
+  launch(gemm_kernel<BN, STAGES>, dim3(ctas), kThreads, smem, st, tA, tB, ga, kb_per, (int)grid.x, (int)grid.y,
          n_items);
   return (int)cudaGetLastError();
 }
