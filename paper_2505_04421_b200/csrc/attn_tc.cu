@@ -36,6 +36,21 @@ __device__ __forceinline__ void load_rows_bf16(bf16* tile, const bf16* src, int 
   }
 }
 
+// packed key row j = key j % nk of sample b0 + j / nk (zero past the P samples / the batch)
+template <int DH>
+__device__ __forceinline__ void load_key_packed(bf16* tile, const bf16* base, int ld, long long sb, int row, int nk,
+                                                int b0, int pack, int B) {
+  const int s = row / nk, j = row % nk;
+  const bool ok = s < pack && b0 + s < B;
+  const bf16* src = base + (long long)(b0 + s) * sb + (long long)j * ld;
+#pragma unroll
+  for (int c = 0; c < DH; c += 8) {
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (ok) v = *reinterpret_cast<const uint4*>(src + c);
+    *reinterpret_cast<uint4*>(tile + canon(row, c, DH)) = v;
+  }
+}
+
 // Query i sits in tile row qrow_of(i) = (i % 4)·32 + i / 4, so the q ≤ 128 queries of a sample are
 // spread over all four TMEM lane quadrants (= all four worker warps) instead of crowding warp 0.
 __device__ __forceinline__ int query_of_row(int row) { return (row & 31) * 4 + (row >> 5); }
@@ -78,9 +93,13 @@ constexpr float kRescale = 8.f;
 
 // TMA (head width ≥ 64): K / V chunks arrive by 3-D TMA into 128-byte-swizzled tiles, the next
 // chunk issued by the MMA thread as soon as O += P·V of the current one has completed.
+// Packing (pack = P > 1, self layers): P samples share one CTA — tile row r is query r % nq of
+// sample r / nq, key column j is key j % nk of sample j / nk (P·nq ≤ 128, P·nk ≤ 128: one chunk),
+// and a row sees only its own sample's key interval, shifted by (r / nq)·nk.  K / V then come
+// from a 2-D tensor map over the contiguous [B·nk] key rows.
 template <int DH, bool TMA>
 __global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a, const __grid_constant__ CUtensorMap tmK,
-                                                                 const __grid_constant__ CUtensorMap tmV) {
+                                                                 const __grid_constant__ CUtensorMap tmV, int pack) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   constexpr int KP = kC * DH > 128 * kC ? kC * DH : 128 * kC;
   constexpr uint32_t TCOLS = DH > 128 ? 512 : 256;
@@ -93,7 +112,7 @@ __global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a, cons
   uint64_t* bar_kv = bars + 2;
   uint64_t* bar_m = bars + 3;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
-  const int b = blockIdx.x / a.heads, hd = blockIdx.x % a.heads;
+  const int b0 = (blockIdx.x / a.heads) * pack, hd = blockIdx.x % a.heads;
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     sm100::mbar_init(bar_a, 32 * kWorkers);
@@ -121,8 +140,13 @@ __global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a, cons
         sm100::mbar_arrive_expect_tx(bar_kv, 2 * kC * DH * 2);
 #pragma unroll
         for (int i = 0; i < DH / 64; ++i) {
-          sm100::tma_load_3d(sKP + i * kC * 64, &tmK, bar_kv, hd * DH + 64 * i, c * kC, b);
-          sm100::tma_load_3d(sV + i * kC * 64, &tmV, bar_kv, hd * DH + 64 * i, c * kC, b);
+          if (pack > 1) {
+            sm100::tma_load_2d(sKP + i * kC * 64, &tmK, bar_kv, hd * DH + 64 * i, b0 * a.nk);
+            sm100::tma_load_2d(sV + i * kC * 64, &tmV, bar_kv, hd * DH + 64 * i, b0 * a.nk);
+          } else {
+            sm100::tma_load_3d(sKP + i * kC * 64, &tmK, bar_kv, hd * DH + 64 * i, c * kC, b0);
+            sm100::tma_load_3d(sV + i * kC * 64, &tmV, bar_kv, hd * DH + 64 * i, c * kC, b0);
+          }
         }
       };
       if constexpr (TMA) {
@@ -159,17 +183,23 @@ __global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a, cons
   } else {
     const int q = warp & 3;
     const int row = q * 32 + lane;
-    const int qi = query_of_row(row);
+    const int sr = pack > 1 ? row / a.nq : 0;                  // packed sample of this row
+    const int qi = pack > 1 ? row % a.nq : query_of_row(row);
+    const int b = min(b0 + sr, a.B - 1);
     const uint32_t lo_lane = (uint32_t)(q * 32) << 16;
     const float scale = rsqrtf((float)(a.D / a.heads));
     const VisRule vis{a.k, a.G, a.ns, a.goff, a.npg[b], a.qg ? a.qg + (long long)b * a.k : nullptr, a.learn,
                      a.self_keys};
-    const bool qrow = qi < a.nq;
+    const bool qrow = qi < a.nq && sr < pack && b0 + sr < a.B;
     int vlo = 0, vhi = 0;
-    if (qrow) vis_interval(vis, qi, a.nk, vlo, vhi);
+    if (qrow) {
+      vis_interval(vis, qi, a.nk, vlo, vhi);
+      vlo += sr * a.nk;
+      vhi += sr * a.nk;
+    }
     const bf16* Qb = a.Q + b * a.sq + hd * DH;
-    const bf16* Kb = a.Kp + b * a.sk + hd * DH;
-    const bf16* Vb = a.V + b * a.sv + hd * DH;
+    const bf16* Kb = a.Kp + b0 * a.sk + hd * DH;
+    const bf16* Vb = a.V + b0 * a.sv + hd * DH;
     uint32_t pd = 0;
     auto signal = [&]() { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(bar_a); };
     auto wait_d = [&]() { sm100::mbar_wait(bar_d, pd); pd ^= 1; sm100::tc_fence_after(); };
@@ -183,8 +213,13 @@ __global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a, cons
     for (int c = 0; c < nchunk; ++c) {
       const int c0 = c * kC;
       if constexpr (!TMA) {
-        load_rows_bf16<DH>(sKP, Kb + (long long)c0 * a.ldk, a.ldk, row, a.nk - c0);
-        load_rows_bf16<DH>(sV, Vb + (long long)c0 * a.ldv, a.ldv, row, a.nk - c0);
+        if (pack > 1) {
+          load_key_packed<DH>(sKP, a.Kp + hd * DH, a.ldk, a.sk, row, a.nk, b0, pack, a.B);
+          load_key_packed<DH>(sV, a.V + hd * DH, a.ldv, a.sv, row, a.nk, b0, pack, a.B);
+        } else {
+          load_rows_bf16<DH>(sKP, Kb + (long long)c0 * a.ldk, a.ldk, row, a.nk - c0);
+          load_rows_bf16<DH>(sV, Vb + (long long)c0 * a.ldv, a.ldv, row, a.nk - c0);
+        }
       }
       signal();
       wait_d();                                     // S_c ready (K tile dead)
@@ -275,9 +310,10 @@ __global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a, cons
 // TMA (head width ≥ 64): the MMA thread streams each K / V chunk with 3-D tensor maps ([sample]
 // [key][column], rows past the sample's keys read as zero) into 128-byte-swizzled tiles, issuing
 // the next chunk as soon as the MMAs reading the current one have completed.
+// Packing as in the forward (pack > 1: non-BIG only; key rows of dV / dK map back to their samples).
 template <int DH, bool TMA>
 __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, const __grid_constant__ CUtensorMap tmK,
-                                                                  const __grid_constant__ CUtensorMap tmV) {
+                                                                  const __grid_constant__ CUtensorMap tmV, int pack) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   constexpr bool BIG = DH > 128;
   constexpr int QR = BIG ? 64 : 128;              // stored query rows
@@ -294,7 +330,7 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
   uint64_t* bar_kv = bars + 2;                    // TMA: K / V chunk landed
   uint64_t* bar_m = bars + 3;                     // TMA: the MMAs reading the chunk are done
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
-  const int b = blockIdx.x / a.heads, hd = blockIdx.x % a.heads;
+  const int b0 = (blockIdx.x / a.heads) * pack, hd = blockIdx.x % a.heads;
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     sm100::mbar_init(bar_a, 32 * 2 * kWorkers);
@@ -323,8 +359,13 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
         sm100::mbar_arrive_expect_tx(bar_kv, 2 * kC * DH * 2);
 #pragma unroll
         for (int i = 0; i < DH / 64; ++i) {
-          sm100::tma_load_3d(sK + i * kC * 64, &tmK, bar_kv, hd * DH + 64 * i, c * kC, b);
-          sm100::tma_load_3d(sV + i * kC * 64, &tmV, bar_kv, hd * DH + 64 * i, c * kC, b);
+          if (pack > 1) {
+            sm100::tma_load_2d(sK + i * kC * 64, &tmK, bar_kv, hd * DH + 64 * i, b0 * a.nk);
+            sm100::tma_load_2d(sV + i * kC * 64, &tmV, bar_kv, hd * DH + 64 * i, b0 * a.nk);
+          } else {
+            sm100::tma_load_3d(sK + i * kC * 64, &tmK, bar_kv, hd * DH + 64 * i, c * kC, b0);
+            sm100::tma_load_3d(sV + i * kC * 64, &tmV, bar_kv, hd * DH + 64 * i, c * kC, b0);
+          }
         }
       };
       auto wait_kv = [&]() { sm100::mbar_wait(bar_kv, pkv); pkv ^= 1; };
@@ -399,11 +440,13 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
     const int r0 = DH >= 64 ? grp * RW : 0, r1 = DH >= 64 ? r0 + RW : (grp == 0 ? DH : 0);
     const int q0 = DH >= 64 ? grp * HC : 0, q1 = DH >= 64 ? q0 + HC : (grp == 0 ? DH : 0);   // dQ
     const float scale = rsqrtf((float)(a.D / a.heads));
+    const int sr = pack > 1 ? row / a.nq : 0;                  // packed sample of this query row
+    const int b = min(b0 + sr, a.B - 1);
     const VisRule vis{a.k, a.G, a.ns, a.goff, a.npg[b], a.qg ? a.qg + (long long)b * a.k : nullptr, a.learn,
                      a.self_keys};
     const bf16* Qb = a.Q + b * a.sq + hd * DH;
-    const bf16* Kb = a.Kp + b * a.sk + hd * DH;
-    const bf16* Vb = a.V + b * a.sv + hd * DH;
+    const bf16* Kb = a.Kp + b0 * a.sk + hd * DH;
+    const bf16* Vb = a.V + b0 * a.sv + hd * DH;
     uint32_t pd = 0;
     auto signal = [&]() { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(bar_a); };
     auto wait_d = [&]() { sm100::mbar_wait(bar_d, pd); pd ^= 1; sm100::tc_fence_after(); };
@@ -416,8 +459,8 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
         *reinterpret_cast<uint4*>(tile + canon(row, grp * HC + c, DH)) = v;
       }
     };
-    const int qi = BIG ? row : query_of_row(row);
-    const bool qrow = qi < a.nq;
+    const int qi = pack > 1 ? row % a.nq : (BIG ? row : query_of_row(row));
+    const bool qrow = qi < a.nq && sr < pack && b0 + sr < a.B;
     if (!BIG || row < QR) {
 #pragma unroll
       for (int c = grp * HC; c < grp * HC + HC; c += 8) {
@@ -446,14 +489,35 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
       if (qrow) lse = a.lse[((long long)b * a.heads + hd) * a.nq + qi];
     }
     int vlo = 0, vhi = 0;
-    if (qrow && lse != -INFINITY) vis_interval(vis, qi, a.nk, vlo, vhi);
+    if (qrow && lse != -INFINITY) {
+      vis_interval(vis, qi, a.nk, vlo, vhi);
+      vlo += sr * a.nk;
+      vhi += sr * a.nk;
+    }
+    // this group's half of the packed key row `row` (pack > 1)
+    auto load_half_packed = [&](bf16* tile, const bf16* base, int ld, long long sb) {
+      const int s2 = row / a.nk, j = row % a.nk;
+      const bool ok = s2 < pack && b0 + s2 < a.B;
+      const bf16* src = base + (long long)(b0 + s2) * sb + (long long)j * ld + hd * DH;
+#pragma unroll
+      for (int c = 0; c < HC; c += 8) {
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (ok) v = *reinterpret_cast<const uint4*>(src + grp * HC + c);
+        *reinterpret_cast<uint4*>(tile + canon(row, grp * HC + c, DH)) = v;
+      }
+    };
     // pass 1: D_i = Σ_j P_ij dP_ij with exactly the P and dP of pass 2, so that Σ_j dS_ij = 0
     // holds to rounding (D = rowsum(dO ⊙ O) would mix the bf16 roundings of dO, P and V).
     for (int c = 0; c < nchunk; ++c) {
       const int c0 = c * kC;
       if constexpr (!TMA) {
-        load_half(sK, Kb + (long long)c0 * a.ldk, a.ldk, a.nk - c0);
-        load_half(sV, Vb + (long long)c0 * a.ldv, a.ldv, a.nk - c0);
+        if (pack > 1) {
+          load_half_packed(sK, a.Kp, a.ldk, a.sk);
+          load_half_packed(sV, a.V, a.ldv, a.sv);
+        } else {
+          load_half(sK, Kb + (long long)c0 * a.ldk, a.ldk, a.nk - c0);
+          load_half(sV, Vb + (long long)c0 * a.ldv, a.ldv, a.nk - c0);
+        }
       }
       signal();
       wait_d();
@@ -501,9 +565,11 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
         }
       }
       // thread = key row: dV, dK of key c0 + row, 32 columns at a time (BIG: two 128-column halves)
-      const bool krow = c0 + row < a.nk;
-      bf16* pv = a.dV + b * a.sdv + (long long)(c0 + row) * a.lddv + hd * DH;
-      bf16* pk = a.dK + b * a.sdk + (long long)(c0 + row) * a.lddk + hd * DH;
+      // key row → (sample, key): packed rows map back to their own sample
+      const int ks = pack > 1 ? row / a.nk : 0, kj = pack > 1 ? row % a.nk : c0 + row;
+      const bool krow = pack > 1 ? (ks < pack && b0 + ks < a.B) : (c0 + row < a.nk);
+      bf16* pv = a.dV + (long long)(b0 + ks) * a.sdv + (long long)kj * a.lddv + hd * DH;
+      bf16* pk = a.dK + (long long)(b0 + ks) * a.sdk + (long long)kj * a.lddk + hd * DH;
       constexpr int NH = BIG ? 2 : 1, NW = DH / NH;
       for (int h = 0; h < NH; ++h) {
         signal();
@@ -550,7 +616,7 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
 // K / V tensor maps [B][nk][D] over the strided projections (false: the strides or base addresses
 // miss TMA's 16-byte rules, or LONGER_ATTN_TMA=0 → thread loads).
 template <int DH>
-bool kv_maps(const AttnArgs& a, CUtensorMap& tK, CUtensorMap& tV) {
+bool kv_maps(const AttnArgs& a, int pack, CUtensorMap& tK, CUtensorMap& tV) {
   const char* env = std::getenv("LONGER_ATTN_TMA");
   if (DH < 64 || (env && env[0] == '0')) return false;
   auto aligned = [](const void* p, long long ld, long long sb) {
@@ -558,33 +624,52 @@ bool kv_maps(const AttnArgs& a, CUtensorMap& tK, CUtensorMap& tV) {
   };
   if (!aligned(a.Kp, a.ldk, a.sk) || !aligned(a.V, a.ldv, a.sv)) return false;
   const long long cols = (long long)a.heads * DH;
+  if (pack > 1)                                   // contiguous key rows of all samples (checked)
+    return tma::encode_2d_bf16(&tK, a.Kp, cols, (long long)a.B * a.nk, a.ldk, 64, kC) == 0 &&
+           tma::encode_2d_bf16(&tV, a.V, cols, (long long)a.B * a.nk, a.ldv, 64, kC) == 0;
   return tma::encode_3d_bf16(&tK, a.Kp, cols, a.nk, a.B, a.ldk, a.sk, 64, kC) == 0 &&
          tma::encode_3d_bf16(&tV, a.V, cols, a.nk, a.B, a.ldv, a.sv, 64, kC) == 0;
 }
 
+// samples per CTA: self-layer shapes whose queries and keys of several samples fit one tile
+// (key rows contiguous across samples for the 2-D tensor map); LONGER_ATTN_PACK=0 disables.
+template <int DH>
+int pack_of(const AttnArgs& a) {
+  const char* env = std::getenv("LONGER_ATTN_PACK");             // 0: off, 2: also in the forward
+  if (DH > 128 || (env && env[0] == '0') || a.nq > 64 || a.nk > 64) return 1;
+  if (a.sk != (long long)a.nk * a.ldk || a.sv != (long long)a.nk * a.ldv) return 1;
+  const int p = std::min(kC / a.nk, 128 / a.nq);
+  return std::max(1, std::min(p, a.B));
+}
+
 template <int DH, bool TMA>
-int launch_fwd_t(const AttnArgs& a, const CUtensorMap& tK, const CUtensorMap& tV, cudaStream_t st) {
+int launch_fwd_t(const AttnArgs& a, const CUtensorMap& tK, const CUtensorMap& tV, int pack, cudaStream_t st) {
   const int smem = (128 * DH + std::max(128 * kC, kC * DH) + kC * DH) * 2 + 64 + 1024;
   static int done = 0;
   if (!done) {
     cudaFuncSetAttribute(xattn_fwd_kernel<DH, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     done = 1;
   }
-  launch(xattn_fwd_kernel<DH, TMA>, a.B * a.heads, kThreads, std::max(smem, 80 * 1024), st, a, tK, tV);
+  launch(xattn_fwd_kernel<DH, TMA>, ((a.B + pack - 1) / pack) * a.heads, kThreads, std::max(smem, 80 * 1024), st, a,
+         tK, tV, pack);
   return (int)cudaGetLastError();
 }
 
 template <int DH>
 int launch_fwd(const AttnArgs& a, cudaStream_t st) {
   CUtensorMap tK{}, tV{};
+  // the forward runs two CTAs per SM, so B·heads ≤ 296 CTAs are already one wave: packing would
+  // only idle SMs (measured +10 µs per step); LONGER_ATTN_PACK=2 forces it for testing
+  const char* env = std::getenv("LONGER_ATTN_PACK");
+  const int pack = (env && env[0] == '2') ? pack_of<DH>(a) : 1;
   if constexpr (DH >= 64) {
-    if (kv_maps<DH>(a, tK, tV)) return launch_fwd_t<DH, true>(a, tK, tV, st);
+    if (kv_maps<DH>(a, pack, tK, tV)) return launch_fwd_t<DH, true>(a, tK, tV, pack, st);
   }
-  return launch_fwd_t<DH, false>(a, tK, tV, st);
+  return launch_fwd_t<DH, false>(a, tK, tV, pack, st);
 }
 
 template <int DH, bool TMA>
-int launch_bwd_t(const AttnArgs& a, const CUtensorMap& tK, const CUtensorMap& tV, cudaStream_t st) {
+int launch_bwd_t(const AttnArgs& a, const CUtensorMap& tK, const CUtensorMap& tV, int pack, cudaStream_t st) {
   const int QR = DH > 128 ? 64 : 128;
   const int smem = (2 * QR * DH + 2 * kC * DH + 2 * QR * kC) * 2 + 256 * 4 + 64 + 1024;
   static int done = 0;
@@ -592,17 +677,19 @@ int launch_bwd_t(const AttnArgs& a, const CUtensorMap& tK, const CUtensorMap& tV
     cudaFuncSetAttribute(xattn_bwd_kernel<DH, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     done = 1;
   }
-  launch(xattn_bwd_kernel<DH, TMA>, a.B * a.heads, kThreads8, std::max(smem, 116 * 1024), st, a, tK, tV);
+  launch(xattn_bwd_kernel<DH, TMA>, ((a.B + pack - 1) / pack) * a.heads, kThreads8, std::max(smem, 116 * 1024), st, a,
+         tK, tV, pack);
   return (int)cudaGetLastError();
 }
 
 template <int DH>
 int launch_bwd(const AttnArgs& a, cudaStream_t st) {
   CUtensorMap tK{}, tV{};
+  const int pack = pack_of<DH>(a);
   if constexpr (DH >= 64) {
-    if (kv_maps<DH>(a, tK, tV)) return launch_bwd_t<DH, true>(a, tK, tV, st);
+    if (kv_maps<DH>(a, pack, tK, tV)) return launch_bwd_t<DH, true>(a, tK, tV, pack, st);
   }
-  return launch_bwd_t<DH, false>(a, tK, tV, st);
+  return launch_bwd_t<DH, false>(a, tK, tV, pack, st);
 }
 
 }  // namespace

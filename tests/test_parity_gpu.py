@@ -126,6 +126,28 @@ def test_matches_oracle_on_synthetic(kw, B, min_events):
     assert np.max(np.abs(pf - p_ref)) <= 5e-3, np.abs(pf - p_ref)
 
 
+@pytest.mark.parametrize("pack,tma", [("0", "1"), ("2", "1"), ("2", "0"), ("1", "0")])
+def test_attention_variants_match_oracle(pack, tma, monkeypatch):
+    """Every tensor-core attention variant (read per launch): samples packed per CTA in the
+    self layers (LONGER_ATTN_PACK: 0 off, 1 backward only = default, 2 forward too) x K/V by TMA or
+    by thread loads (LONGER_ATTN_TMA), at the c2 widths with mixed lengths, a query strategy that
+    gathers query groups, and B = 4 (a partly filled packed CTA)."""
+    monkeypatch.setenv("LONGER_ATTN_PACK", pack)
+    monkeypatch.setenv("LONGER_ATTN_TMA", tma)
+    cfg = ModelConfig(**dict(C2, L=512, query_strategy="uniform")).validate()
+    from paper_2505_04421_b200.params import init_params
+    P = init_params(cfg, seed=0)
+    rng = np.random.default_rng(5)
+    P = {n: a + 0.02 * rng.standard_normal(a.shape) for n, a in P.items()}
+    batch = synthetic_batch(cfg, 4, seed=11, min_events=1)
+    p_ref, loss_ref, G = O.forward_backward(P, cfg, batch.as_dict())
+    model = _model(cfg, P)
+    p, loss, grads = _run(model, batch)
+    assert np.max(np.abs(p - p_ref)) <= 5e-3
+    assert abs(loss - loss_ref) <= loss_tol(p_ref, batch.label)
+    assert_grads_close(grads, G, f"pack={pack} tma={tma}")
+
+
 @pytest.mark.parametrize("bias", [20.0, 40.0, -40.0, -25.0])
 def test_saturated_logits_follow_the_reference_clamp(bias):
     """p = sigmoid(z) saturates in fp32 long before the reference's 1e-12 clamp does; the loss and
