@@ -711,10 +711,45 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
         float df[kFP];
         tmem_row<kFP>(T_X + lane_off, df);
         if (ti.real) {
-          float* gi = (item_smem ? s_item : a.g_item) + ids[0] * a.d_item;
+          if (item_smem && (a.d_item & 3) == 0 && (reinterpret_cast<uintptr_t>(s_item) & 15) == 0) {
+            // shared-memory float adds are CAS loops on sm_100: one 128-bit CAS per 4 columns
+            // (quads alternate between the two warp groups)
+            uint4* gi = reinterpret_cast<uint4*>(s_item + ids[0] * a.d_item);
 #pragma unroll
-          for (int c = 0; c < kFP; ++c)
-            if (c < a.d_item && (c & 1) == grp) atomicAdd(gi + c, df[c]);
+            for (int c = 0; c + 3 < kFP; c += 4) {
+              if (c >= a.d_item || ((c >> 2) & 1) != grp) continue;
+              uint4* addr = gi + (c >> 2);
+              uint4 old = *addr, assumed;
+              do {
+                assumed = old;
+                const uint4 nw = make_uint4(__float_as_uint(__uint_as_float(assumed.x) + df[c]),
+                                            __float_as_uint(__uint_as_float(assumed.y) + df[c + 1]),
+                                            __float_as_uint(__uint_as_float(assumed.z) + df[c + 2]),
+                                            __float_as_uint(__uint_as_float(assumed.w) + df[c + 3]));
+                old = sm100::atom_cas128_shared(addr, assumed, nw);
+              } while (old.x != assumed.x || old.y != assumed.y || old.z != assumed.z || old.w != assumed.w);
+            }
+          } else if (item_smem && (a.d_item & 1) == 0) {
+            // one 64-bit CAS per column pair (pairs alternate between the two warp groups)
+            unsigned long long* gi = reinterpret_cast<unsigned long long*>(s_item + ids[0] * a.d_item);
+#pragma unroll
+            for (int c = 0; c + 1 < kFP; c += 2) {
+              if (c >= a.d_item || ((c >> 1) & 1) != grp) continue;
+              unsigned long long* addr = gi + (c >> 1);
+              unsigned long long old = *addr, assumed;
+              do {
+                assumed = old;
+                const float2 cur = *reinterpret_cast<const float2*>(&assumed);
+                const float2 nw = make_float2(cur.x + df[c], cur.y + df[c + 1]);
+                old = atomicCAS(addr, assumed, *reinterpret_cast<const unsigned long long*>(&nw));
+              } while (old != assumed);
+            }
+          } else {
+            float* gi = (item_smem ? s_item : a.g_item) + ids[0] * a.d_item;
+#pragma unroll
+            for (int c = 0; c < kFP; ++c)
+              if (c < a.d_item && (c & 1) == grp) atomicAdd(gi + c, df[c]);
+          }
         }
       }
     }

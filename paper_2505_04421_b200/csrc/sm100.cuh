@@ -90,6 +90,22 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* m
       : "memory");
 }
 
+// 128-bit compare-and-swap on shared memory (ATOMS.CAS.128); returns the previous 16 bytes.
+__device__ __forceinline__ uint4 atom_cas128_shared(void* smem_addr, uint4 cmp, uint4 val) {
+  unsigned long long olo, ohi;
+  const unsigned long long clo = ((unsigned long long)cmp.y << 32) | cmp.x, chi = ((unsigned long long)cmp.w << 32) | cmp.z;
+  const unsigned long long nlo = ((unsigned long long)val.y << 32) | val.x, nhi = ((unsigned long long)val.w << 32) | val.z;
+  asm volatile("{\n\t.reg .b128 c, n, d;\n\t"
+               "mov.b128 c, {%2, %3};\n\t"
+               "mov.b128 n, {%4, %5};\n\t"
+               "atom.shared.cas.b128 d, [%6], c, n;\n\t"
+               "mov.b128 {%0, %1}, d;\n\t}"
+               : "=l"(olo), "=l"(ohi)
+               : "l"(clo), "l"(chi), "l"(nlo), "l"(nhi), "r"(smem_u32(smem_addr))
+               : "memory");
+  return make_uint4((uint32_t)olo, (uint32_t)(olo >> 32), (uint32_t)ohi, (uint32_t)(ohi >> 32));
+}
+
 // ------------------------------------------------------------------ TMEM
 template <uint32_t NCOLS>
 __device__ __forceinline__ void tmem_alloc(uint32_t* smem_slot) {  // whole warp
