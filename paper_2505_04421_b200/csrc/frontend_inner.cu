@@ -17,12 +17,54 @@ using namespace fe;
 
 namespace {
 
+// 16-byte vector helpers over bf16 scratch rows (8 values per shared-memory access)
+template <int N>
+__device__ __forceinline__ void store8_bf16(bf16* dst, const float* v) {
+#pragma unroll
+  for (int c = 0; c < N; c += 8)
+    *reinterpret_cast<uint4*>(dst + c) =
+        make_uint4(sm100::pack_bf16(v[c], v[c + 1]), sm100::pack_bf16(v[c + 2], v[c + 3]),
+                   sm100::pack_bf16(v[c + 4], v[c + 5]), sm100::pack_bf16(v[c + 6], v[c + 7]));
+}
+// Σ_c x[c]·row[c], summed in c order
+template <int N>
+__device__ __forceinline__ float dot8_bf16(const float* x, const bf16* row) {
+  float acc = 0.f;
+#pragma unroll
+  for (int c = 0; c < N; c += 8) {
+    const uint4 u = *reinterpret_cast<const uint4*>(row + c);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      acc = fmaf(x[c + 2 * t], sm100::bf16_lo(w[t]), acc);
+      acc = fmaf(x[c + 2 * t + 1], sm100::bf16_hi(w[t]), acc);
+    }
+  }
+  return acc;
+}
+// y[c] += a·row[c]
+template <int N>
+__device__ __forceinline__ void axpy8_bf16(float* y, float a, const bf16* row) {
+#pragma unroll
+  for (int c = 0; c < N; c += 8) {
+    const uint4 u = *reinterpret_cast<const uint4*>(row + c);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      y[c + 2 * t] = fmaf(a, sm100::bf16_lo(w[t]), y[c + 2 * t]);
+      y[c + 2 * t + 1] = fmaf(a, sm100::bf16_hi(w[t]), y[c + 2 * t + 1]);
+    }
+  }
+}
+
 template <int DT, int KG>
 __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   constexpr int XK = DT + 16;                 // activation rows carrying a ones column
   constexpr int F4 = 4 * DT;
-  constexpr int QS = 3 * DT + 2;              // bf16 q|k|v scratch row (padded)
+  constexpr int QS = 3 * DT + 8;              // bf16 q|k|v scratch row (16-byte rows; rows 4 apart
+                                              // fall in different bank groups)
+  constexpr int DCS = DT + 4;                 // fp32 dctx scratch row
   const BlobOff bo = blob_offsets(DT, DT * KG, a.inner_layers);
   // weights: forward images [qkv | wo | w1i] and backward images [qkv_n | wo_n | w1i_n | w2i_n]
   bf16* sWf = reinterpret_cast<bf16*>(smem_raw);
@@ -44,7 +86,7 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
   bf16* sGF = sDX1 + kTile * DT;              // 128 x F4   (later: dqkv 128 x 3DT)
   bf16* sDF = sGF + kTile * F4;               // 128 x F4   (later: dctx fp32 scratch)
   bf16* sDQKV = sGF;
-  float* sDC = reinterpret_cast<float*>(sDF); // 128 x (DT+1)
+  float* sDC = reinterpret_cast<float*>(sDF); // 128 x DCS
   bf16* sQKV = sDF + kTile * F4;              // 128 x QS bf16 (q, k, v for the group peers)
   float* sP = reinterpret_cast<float*>(sQKV + kTile * QS);   // 128 x KG
   float* sS = sP + kTile * KG;                                  // 128 x KG (dS)
@@ -174,14 +216,11 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
       float qv[DT], kvv[DT];
       tmem_row<DT>(T_W0 + lo, qv);
       bf16* qs = sQKV + row * QS;
-#pragma unroll
-      for (int c = 0; c < DT; ++c) qs[c] = __float2bfloat16(qv[c]);
+      store8_bf16<DT>(qs, qv);
       tmem_row<DT>(T_W0 + lo + DT, kvv);
-#pragma unroll
-      for (int c = 0; c < DT; ++c) qs[DT + c] = __float2bfloat16(kvv[c]);
+      store8_bf16<DT>(qs + DT, kvv);
       tmem_row<DT>(T_W0 + lo + 2 * DT, kvv);
-#pragma unroll
-      for (int c = 0; c < DT; ++c) qs[2 * DT + c] = __float2bfloat16(kvv[c]);
+      store8_bf16<DT>(qs + 2 * DT, kvv);
       __syncwarp();
       const int g0 = row - row % KG;
       const int me = row - g0;
@@ -190,10 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
         float mx = -INFINITY;
 #pragma unroll
         for (int jj = 0; jj < KG; ++jj) {
-          const bf16* kr = sQKV + (g0 + jj) * QS + DT;
-          float acc = 0.f;
-#pragma unroll
-          for (int c = 0; c < DT; ++c) acc = fmaf(qv[c], __bfloat162float(kr[c]), acc);
+          const float acc = dot8_bf16<DT>(qv, sQKV + (g0 + jj) * QS + DT);
           p[jj] = acc * scale;
           mx = fmaxf(mx, p[jj]);
         }
@@ -206,12 +242,9 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
       }
       float ctx[XK];
 #pragma unroll
-      for (int c = 0; c < DT; ++c) {
-        float acc = 0.f;
+      for (int c = 0; c < DT; ++c) ctx[c] = 0.f;
 #pragma unroll
-        for (int jj = 0; jj < KG; ++jj) acc = fmaf(p[jj], __bfloat162float(sQKV[(g0 + jj) * QS + 2 * DT + c]), acc);
-        ctx[c] = acc;
-      }
+      for (int jj = 0; jj < KG; ++jj) axpy8_bf16<DT>(ctx, p[jj], sQKV + (g0 + jj) * QS + 2 * DT);
 #pragma unroll
       for (int c = DT; c < XK; ++c) ctx[c] = c == DT ? 1.f : 0.f;
       store_row(sCTX, row, XK, ctx, XK);
@@ -279,16 +312,14 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
       float dc[DT];
       tmem_row<DT>(T_W2 + lo, dc);
 #pragma unroll
-      for (int c = 0; c < DT; ++c) sDC[row * (DT + 1) + c] = dc[c];
+      for (int c = 0; c < DT; c += 4)
+        *reinterpret_cast<float4*>(sDC + row * DCS + c) = make_float4(dc[c], dc[c + 1], dc[c + 2], dc[c + 3]);
       __syncwarp();
       {
         float dp[KG], D = 0.f;
 #pragma unroll
         for (int jj = 0; jj < KG; ++jj) {
-          const bf16* vr = sQKV + (g0 + jj) * QS + 2 * DT;
-          float acc = 0.f;
-#pragma unroll
-          for (int c = 0; c < DT; ++c) acc = fmaf(dc[c], __bfloat162float(vr[c]), acc);
+          const float acc = dot8_bf16<DT>(dc, sQKV + (g0 + jj) * QS + 2 * DT);
           dp[jj] = acc;
           D += acc * p[jj];
         }
@@ -298,18 +329,22 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
       __syncwarp();
       float dqkv[3 * DT];
 #pragma unroll
-      for (int c = 0; c < DT; ++c) {
-        float dq = 0.f, dk = 0.f, dv = 0.f;
+      for (int c = 0; c < 3 * DT; ++c) dqkv[c] = 0.f;
 #pragma unroll
-        for (int jj = 0; jj < KG; ++jj) {
-          const bf16* pr = sQKV + (g0 + jj) * QS;
-          dq = fmaf(sS[row * KG + jj], __bfloat162float(pr[DT + c]), dq);
-          dk = fmaf(sS[(g0 + jj) * KG + me], __bfloat162float(pr[c]), dk);
-          dv = fmaf(sP[(g0 + jj) * KG + me], sDC[(g0 + jj) * (DT + 1) + c], dv);
+      for (int jj = 0; jj < KG; ++jj) {           // same per-element summation order as a c-outer loop
+        const bf16* pr = sQKV + (g0 + jj) * QS;
+        axpy8_bf16<DT>(dqkv, sS[row * KG + jj], pr + DT);                  // dq += dS_ij k_j
+        axpy8_bf16<DT>(dqkv + DT, sS[(g0 + jj) * KG + me], pr);            // dk += dS_ji q_j
+        const float pj = sP[(g0 + jj) * KG + me];                          // dv += P_ji dctx_j
+        const float* dcr = sDC + (g0 + jj) * DCS;
+#pragma unroll
+        for (int c = 0; c < DT; c += 4) {
+          const float4 d4 = *reinterpret_cast<const float4*>(dcr + c);
+          dqkv[2 * DT + c] = fmaf(pj, d4.x, dqkv[2 * DT + c]);
+          dqkv[2 * DT + c + 1] = fmaf(pj, d4.y, dqkv[2 * DT + c + 1]);
+          dqkv[2 * DT + c + 2] = fmaf(pj, d4.z, dqkv[2 * DT + c + 2]);
+          dqkv[2 * DT + c + 3] = fmaf(pj, d4.w, dqkv[2 * DT + c + 3]);
         }
-        dqkv[c] = dq;
-        dqkv[DT + c] = dk;
-        dqkv[2 * DT + c] = dv;
       }
       __syncwarp();
       store_row(sDQKV, row, 3 * DT, dqkv, 3 * DT);
@@ -397,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
 
 template <int DT, int KG>
 int launch_inner_bwd(const FrontArgs& a, cudaStream_t st) {
-  constexpr int XK = DT + 16, F4 = 4 * DT, QS = 3 * DT + 2;
+  constexpr int XK = DT + 16, F4 = 4 * DT, QS = 3 * DT + 8;
   const int nW = 7 * DT * XK + DT * DT + 12 * DT * DT;
   const int smem = nW * 2 + kTile * (3 * XK + 2 * DT + 2 * F4 + QS) * 2 + kTile * KG * 8 + 5 * DT * 4 + 64;
   if (smem > 227 * 1024) return (int)cudaErrorInvalidValue;
