@@ -574,14 +574,22 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
         sm100::mma_commit(bar_d);
         for (int j = 0; j < nh; ++j) {
           wait_a();                                                      // g1, da1 of half j
-          mma(T_DW2 + j * DT, Opnd{aG, 128, 1}, Opnd{aDH, DT, 1}, kTile / 16, DT, !first);
-          mma(T_DW1 + j * XK, Opnd{aDA, 128, 1}, Opnd{aX0, XK, 1}, kTile / 16, XK, !first);
-          mma(T_X, Opnd{aDA, 128, 0}, Opnd{aW1n + canon(0, 128 * j, H2) * 2, H2, 0}, 8, DT, j > 0);
           if (j + 1 < nh) {
+            mma(T_DW2 + j * DT, Opnd{aG, 128, 1}, Opnd{aDH, DT, 1}, kTile / 16, DT, !first);
+            mma(T_DW1 + j * XK, Opnd{aDA, 128, 1}, Opnd{aX0, XK, 1}, kTile / 16, XK, !first);
+            mma(T_X, Opnd{aDA, 128, 0}, Opnd{aW1n + canon(0, 128 * j, H2) * 2, H2, 0}, 8, DT, j > 0);
             mma(T_A1, Opnd{aX0, XK, 0}, Opnd{aW1 + canon(128 * (j + 1), 0, XK) * 2, XK, 0}, XK / 16, 128, false);
             mma(T_G1, Opnd{aDH, DT, 0}, Opnd{aW2n + canon(128 * (j + 1), 0, DT) * 2, DT, 0}, DT / 16, 128, false);
+            sm100::mma_commit(bar_d);
+          } else {
+            // last half: the workers only wait for dx0 (T_X); the weight-gradient MMAs run on
+            // behind that commit (sG / sDA / sDH / sX0 are next rewritten after the tile's final
+            // commit, which covers them)
+            mma(T_X, Opnd{aDA, 128, 0}, Opnd{aW1n + canon(0, 128 * j, H2) * 2, H2, 0}, 8, DT, j > 0);
+            sm100::mma_commit(bar_d);
+            mma(T_DW2 + j * DT, Opnd{aG, 128, 1}, Opnd{aDH, DT, 1}, kTile / 16, DT, !first);
+            mma(T_DW1 + j * XK, Opnd{aDA, 128, 1}, Opnd{aX0, XK, 1}, kTile / 16, XK, !first);
           }
-          sm100::mma_commit(bar_d);
         }
         wait_a();                                                        // dx0 in sDX0
         mma(T_DWTP, Opnd{aDX0, 64, 1}, Opnd{aFeat, kFP, 1}, kTile / 16, kFP, !first);

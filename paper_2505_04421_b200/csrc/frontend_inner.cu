@@ -154,15 +154,18 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
         mma(T_W0, Opnd{S(sX1N), XK, 0}, Opnd{S(w_w1i), XK, 0}, XK / 16, F4, false);
         mma(T_W1, Opnd{S(sDX2), DT, 0}, Opnd{S(w_w2i_n), DT, 0}, DT / 16, F4, false);
         sm100::mma_commit(bar_d);
+        // The workers wait only for the dX product of each stage; the weight-gradient MMAs queue
+        // behind that commit and are covered by the next one, which precedes any rewrite of
+        // their operands (sGF / sDF are reused as dqkv / dctx scratch only after the dx1 commit).
         wait_a();                                                           // gf, df
-        mma(T_DW2, Opnd{S(sGF), F4, 1}, Opnd{S(sDX2), DT, 1}, kTile / 16, DT, !first);
-        mma(T_DW1, Opnd{S(sDF), F4, 1}, Opnd{S(sX1N), XK, 1}, kTile / 16, XK, !first);
         mma(T_W2, Opnd{S(sDF), F4, 0}, Opnd{S(w_w1i_n), F4, 0}, F4 / 16, DT, false);
         sm100::mma_commit(bar_d);
+        mma(T_DW2, Opnd{S(sGF), F4, 1}, Opnd{S(sDX2), DT, 1}, kTile / 16, DT, !first);
+        mma(T_DW1, Opnd{S(sDF), F4, 1}, Opnd{S(sX1N), XK, 1}, kTile / 16, XK, !first);
         wait_a();                                                           // dx1
         mma(T_W2, Opnd{S(sDX1), DT, 0}, Opnd{S(w_wo_n), DT, 0}, DT / 16, DT, false);
-        mma(T_DWO, Opnd{S(sDX1), DT, 1}, Opnd{S(sCTX), XK, 1}, kTile / 16, XK, !first);
         sm100::mma_commit(bar_d);
+        mma(T_DWO, Opnd{S(sDX1), DT, 1}, Opnd{S(sCTX), XK, 1}, kTile / 16, XK, !first);
         wait_a();                                                           // dqkv
         mma(T_W2, Opnd{S(sDQKV), 3 * DT, 0}, Opnd{S(w_qkv_n), 3 * DT, 0}, 3 * DT / 16, DT, false);
         mma(T_DWQ, Opnd{S(sDQKV), 3 * DT, 1}, Opnd{S(sXN), XK, 1}, kTile / 16, XK, !first);
