@@ -48,7 +48,7 @@ void probe(int ph, int which, cudaStream_t st) {
 struct Side {
   int dev = -1;
   cudaStream_t s = nullptr;
-  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr, mark_ev = nullptr;
 };
 Side g_side[16];
 
@@ -63,6 +63,7 @@ cudaStream_t side_stream(cudaStream_t main) {
     g_side_stream = sd.s;
     cudaEventCreateWithFlags(&sd.fork_ev, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&sd.join_ev, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&sd.mark_ev, cudaEventDisableTiming);
     sd.dev = dev;
   }
   return sd.s;
@@ -86,6 +87,20 @@ void join_side(cudaStream_t main, cudaStream_t side) {
   Side& sd = g_side[dev & 15];
   cudaEventRecord(sd.join_ev, side);
   cudaStreamWaitEvent(main, sd.join_ev, 0);
+}
+
+// a point on the side stream that main waits for later (mark_side now, wait_mark at the consumer)
+void mark_side(cudaStream_t main, cudaStream_t side) {
+  if (side == main) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaEventRecord(g_side[dev & 15].mark_ev, side);
+}
+void wait_mark(cudaStream_t main, cudaStream_t side) {
+  if (side == main) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaStreamWaitEvent(main, g_side[dev & 15].mark_ev, 0);
 }
 
 int fail(int code, const char* msg) {
@@ -641,27 +656,30 @@ int forward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs, fl
   const long long M = (long long)p.B * p.m;
   (void)with_loss;
   TRY(pack_weights(p, c.P, p.ws, st));
-  if (p.fused_fe) {
-    probe(PH_FE_FWD, 0, c.st); TRY(frontend_fused_fwd(c, p, bt)); probe(PH_FE_FWD, 1, c.st);
-    probe(PH_FWD_ROWS, 0, c.st);
-  } else {
-    TRY(frontend_unfused_fwd(c, p, bt));
-  }
-  // global tokens (inputs.py:500-537)
+  // global tokens (inputs.py:500-537): independent of the sequence front-end, so they run on the
+  // side stream beside it; main waits for them only where the query rows take the globals
+  const cudaStream_t ss = side_stream(st);
+  fork_side(st, ss);
   GlobalsArgs ga{};
   ga.uid = bt.uid; ga.cand_item = bt.cand_item; ga.B = p.B; ga.m = p.m; ga.d = d; ga.D = D;
   ga.d_item = dm.d_item; ga.d_act = dm.d_act; ga.d_time = dm.d_time;
   ga.uid_tab = c.w(o.uid); ga.item_tab = c.w(o.item); ga.time_tab = c.w(o.time); ga.cls = c.w(o.cls);
   ga.tok_w = c.w(o.tok_w); ga.tok_b = c.w(o.tok_b); ga.lift_w = c.w(o.lift_w); ga.lift_b = c.w(o.lift_b);
   ga.raw = p.raw; ga.raw_bf = p.raw_bf; ga.td = p.td;
-  globals_raw_fwd(ga, st);
-  TRY(lin_fwd(st, p.raw_bf, D, M, p.pk.glob_w1, D, 2 * D, c.w(o.glob_b1), EPI_GELU | EPI_SAVE_PRE, nullptr, p.gg, p.ga));
-  TRY(lin_fwd(st, p.gg, 2 * D, M, p.pk.glob_w2, 2 * D, D, c.w(o.glob_b2), 0, p.glob, nullptr, nullptr));
+  globals_raw_fwd(ga, ss);
+  TRY(lin_fwd(ss, p.raw_bf, D, M, p.pk.glob_w1, D, 2 * D, c.w(o.glob_b1), EPI_GELU | EPI_SAVE_PRE, nullptr, p.gg, p.ga));
+  TRY(lin_fwd(ss, p.gg, 2 * D, M, p.pk.glob_w2, 2 * D, D, c.w(o.glob_b2), 0, p.glob, nullptr, nullptr));
+  mark_side(st, ss);
+  if (p.fused_fe) {
+    probe(PH_FE_FWD, 0, c.st); TRY(frontend_fused_fwd(c, p, bt)); probe(PH_FE_FWD, 1, c.st);
+    probe(PH_FWD_ROWS, 0, c.st);
+  } else {
+    TRY(frontend_unfused_fwd(c, p, bt));
+  }
   // composite queries O = [merged[G-k:]; globals] (model.py:317-319)
   {
-    // R = [merged; globals] → cross LN1 → [K | V] over all B·v rows, on the side stream while the
-    // main stream builds the q query rows (joined in block_fwd before the attention)
-    const cudaStream_t ss = side_stream(st);
+    // R = [merged; globals] → cross LN1 → [K | V] over all B·v rows, on the side stream (after the
+    // globals) while the main stream builds the q query rows (joined in block_fwd before the attention)
     fork_side(st, ss);
     RowMap r{};
     if (p.fused_fe) {          // merged rows were normalised by the fused front-end; globals only
@@ -682,6 +700,7 @@ int forward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs, fl
     gather_query_rows(p.merged, p.qs == QS_LEARNABLE ? nullptr : p.qg, p.qs == QS_LEARNABLE ? c.w(o.qbank) : nullptr,
                       p.B, p.G, p.k, D, p.O, p.q, st);
   }
+  wait_mark(st, ss);                                   // the global rows
   gather_rows_f32(p.glob, p.B, p.m, 0, p.m, p.O, p.q, p.k, D, st);
   Plan& pm = const_cast<Plan&>(p);
   TRY(block_fwd(c, o.cross, pm.cb, p.O, true, p.pk.c_wq, nullptr, p.pk.c_wo, p.pk.c_w1, p.pk.c_w2));
