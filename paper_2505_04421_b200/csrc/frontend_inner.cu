@@ -10,6 +10,7 @@
 #include "frontend.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace longer {
 
@@ -57,14 +58,19 @@ __device__ __forceinline__ void axpy8_bf16(float* y, float a, const bf16* row) {
   }
 }
 
-template <int DT, int KG>
-__global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) {
+// NG worker groups: NG = 2 puts two warps on each TMEM lane quadrant (8 workers), each owning half
+// of the row's columns (HD = DT / NG); row statistics (LN moments, attention scores, the dP dot
+// products, LN-backward sums) meet through a small shared-memory exchange between the pair.
+template <int DT, int KG, int NG>
+__global__ void __launch_bounds__(32 * (1 + kWorkers * NG), 1) fe_inner_bwd_kernel(FrontArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   constexpr int XK = DT + 16;                 // activation rows carrying a ones column
   constexpr int F4 = 4 * DT;
   constexpr int QS = 3 * DT + 8;              // bf16 q|k|v scratch row (16-byte rows; rows 4 apart
                                               // fall in different bank groups)
   constexpr int DCS = DT + 4;                 // fp32 dctx scratch row
+  constexpr int HD = DT / NG;                 // columns per worker warp
+  constexpr int FH = F4 / NG;                 // FFN hidden columns per worker warp
   const BlobOff bo = blob_offsets(DT, DT * KG, a.inner_layers);
   // weights: forward images [qkv | wo | w1i] and backward images [qkv_n | wo_n | w1i_n | w2i_n]
   bf16* sWf = reinterpret_cast<bf16*>(smem_raw);
@@ -88,10 +94,11 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
   bf16* sDQKV = sGF;
   float* sDC = reinterpret_cast<float*>(sDF); // 128 x DCS
   bf16* sQKV = sDF + kTile * F4;              // 128 x QS bf16 (q, k, v for the group peers)
-  float* sP = reinterpret_cast<float*>(sQKV + kTile * QS);   // 128 x KG
-  float* sS = sP + kTile * KG;                                  // 128 x KG (dS)
-  float* s_par = sS + kTile * KG;             // [ln1_g, ln1_b, b_o, ln2_g, ln2_b] x DT
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_par + 5 * DT);
+  float* sP = reinterpret_cast<float*>(sQKV + kTile * QS);   // NG x 128 x KG (one copy per group)
+  float* sS = sP + NG * kTile * KG;                             // NG x 128 x KG (dS)
+  float* s_par = sS + NG * kTile * KG;        // [ln1_g, ln1_b, b_o, ln2_g, ln2_b] x DT
+  float* sX = s_par + 5 * DT;                 // NG = 2: [2 parity][2 group][128][8] exchange slots
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sX + (NG > 1 ? 2 * NG * kTile * 8 : 0));
   uint64_t* bar_w = bars;
   uint64_t* bar_a = bars + 1;
   uint64_t* bar_d = bars + 2;
@@ -100,7 +107,7 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     sm100::mbar_init(bar_w, 1);
-    sm100::mbar_init(bar_a, 32 * kWorkers);
+    sm100::mbar_init(bar_a, 32 * kWorkers * NG);
     sm100::mbar_init(bar_d, 1);
     sm100::fence_barrier_init();
   }
@@ -175,6 +182,8 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
     }
   } else {
     const int q = warp & 3;
+    const int grp = (warp - 1) >> 2;           // column half (NG = 2) of this warp
+    const int c0 = grp * HD;
     const int row = q * 32 + lane;
     const uint32_t lo = (uint32_t)(q * 32) << 16;
     const float scale = rsqrtf((float)DT);
@@ -183,10 +192,50 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
     const float* bo_ = s_par + 2 * DT;
     const float* lg2 = s_par + 3 * DT;
     const float* lb2 = s_par + 4 * DT;
+    float* sPg = sP + grp * kTile * KG;         // this group's copy of P and dS
+    float* sSg = sS + grp * kTile * KG;
     uint32_t pd = 0;
     auto signal = [&]() { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(bar_a); };
     auto wait_d = [&]() { sm100::mbar_wait(bar_d, pd); pd ^= 1; sm100::tc_fence_after(); };
-    float cs_l1g = 0.f, cs_l1b = 0.f, cs_l2g = 0.f, cs_l2b = 0.f, cs_b2 = 0.f;   // lane c ↔ column c
+    // v[0..n) += the pair's partials (a + b == b + a: both warps get bit-identical sums).  Slots
+    // alternate by parity, so one barrier per exchange also protects the slot's reuse.
+    int xpar = 0;
+    auto xsum = [&](float* v, int n) {
+      if constexpr (NG > 1) {
+        float* mine = sX + ((xpar * NG + grp) * kTile + row) * 8;
+        const float* other = sX + ((xpar * NG + (grp ^ 1)) * kTile + row) * 8;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (i < n) mine[i] = v[i];
+        asm volatile("bar.sync %0, 64;" :: "r"(1 + q) : "memory");
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (i < n) v[i] += other[i];
+        xpar ^= 1;
+      }
+    };
+    // LN moments of the row (two-pass, as the reference): mean, then the centred variance
+    auto ln_stats = [&](const float* x, float& mu, float& inv) {
+      float sm = 0.f;
+#pragma unroll
+      for (int c = 0; c < HD; ++c) sm += x[c];
+      xsum(&sm, 1);
+      mu = sm * (1.f / DT);
+      float vs = 0.f;
+#pragma unroll
+      for (int c = 0; c < HD; ++c) { const float t = x[c] - mu; vs += t * t; }
+      xsum(&vs, 1);
+      inv = rsqrtf(vs * (1.f / DT) + kLnEps);
+    };
+    auto ones_col = [&](bf16* tile) {           // [· | 1 | 0…] bias column of an XK-wide operand
+      if (grp == NG - 1) {
+        float pad[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) pad[c] = c == 0 ? 1.f : 0.f;
+        store_row(tile, row, XK, pad, 16, DT);
+      }
+    };
+    float cs_l1g = 0.f, cs_l1b = 0.f, cs_l2g = 0.f, cs_l2b = 0.f, cs_b2 = 0.f;   // lane c ↔ column c0 + c
     int my_tiles = 0;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++my_tiles) {
       const long long t = tile * kTile + row;
@@ -198,233 +247,243 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
         keep = (j / a.K) >= (a.Lp - n) / a.K;
       }
       // ---- R0: x = h; LN1; dX2 = dmerged ⊙ keep
-      float h[DT], dx2[DT];
+      float h[HD], dx2[HD];
 #pragma unroll
-      for (int c = 0; c < DT; c += 4) {
+      for (int c = 0; c < HD; c += 4) {
         float4 hv = make_float4(0.f, 0.f, 0.f, 0.f), dv = hv;
-        if (in_range) hv = reinterpret_cast<const float4*>(a.h_in + t * DT)[c / 4];
-        if (keep) dv = reinterpret_cast<const float4*>(a.dmerged + t * DT)[c / 4];
+        if (in_range) hv = *reinterpret_cast<const float4*>(a.h_in + t * DT + c0 + c);
+        if (keep) dv = *reinterpret_cast<const float4*>(a.dmerged + t * DT + c0 + c);
         h[c] = hv.x; h[c + 1] = hv.y; h[c + 2] = hv.z; h[c + 3] = hv.w;
         dx2[c] = dv.x; dx2[c + 1] = dv.y; dx2[c + 2] = dv.z; dx2[c + 3] = dv.w;
       }
-      float xn[XK], inv1;
-      ln_row_s<DT>(h, lg1, lb1, xn, inv1);
+      float mu1, inv1;
+      ln_stats(h, mu1, inv1);
+      {
+        float xn[HD];
 #pragma unroll
-      for (int c = DT; c < XK; ++c) xn[c] = c == DT ? 1.f : 0.f;
-      store_row(sXN, row, XK, xn, XK);
-      store_row(sDX2, row, DT, dx2, DT);
+        for (int c = 0; c < HD; ++c) xn[c] = (h[c] - mu1) * inv1 * lg1[c0 + c] + lb1[c0 + c];
+        store_row(sXN, row, XK, xn, HD, c0);
+      }
+      ones_col(sXN);
+      store_row(sDX2, row, DT, dx2, HD, c0);
       signal();
       // ---- R1: q, k, v; group attention (scratch keeps q|k|v (bf16) and P (fp32) for the peers)
       wait_d();
-      float qv[DT], kvv[DT];
-      tmem_row<DT>(T_W0 + lo, qv);
-      bf16* qs = sQKV + row * QS;
-      store8_bf16<DT>(qs, qv);
-      tmem_row<DT>(T_W0 + lo + DT, kvv);
-      store8_bf16<DT>(qs + DT, kvv);
-      tmem_row<DT>(T_W0 + lo + 2 * DT, kvv);
-      store8_bf16<DT>(qs + 2 * DT, kvv);
+      float qv[HD];
+      {
+        float kvv[HD];
+        tmem_row<HD>(T_W0 + lo + c0, qv);
+        bf16* qs = sQKV + row * QS;
+        store8_bf16<HD>(qs + c0, qv);
+        tmem_row<HD>(T_W0 + lo + DT + c0, kvv);
+        store8_bf16<HD>(qs + DT + c0, kvv);
+        tmem_row<HD>(T_W0 + lo + 2 * DT + c0, kvv);
+        store8_bf16<HD>(qs + 2 * DT + c0, kvv);
+      }
       __syncwarp();
       const int g0 = row - row % KG;
       const int me = row - g0;
       float p[KG];
       {
+#pragma unroll
+        for (int jj = 0; jj < KG; ++jj) p[jj] = dot8_bf16<HD>(qv, sQKV + (g0 + jj) * QS + DT + c0);
+        xsum(p, KG);
         float mx = -INFINITY;
 #pragma unroll
-        for (int jj = 0; jj < KG; ++jj) {
-          const float acc = dot8_bf16<DT>(qv, sQKV + (g0 + jj) * QS + DT);
-          p[jj] = acc * scale;
-          mx = fmaxf(mx, p[jj]);
-        }
+        for (int jj = 0; jj < KG; ++jj) { p[jj] *= scale; mx = fmaxf(mx, p[jj]); }
         float tot = 0.f;
 #pragma unroll
         for (int jj = 0; jj < KG; ++jj) { p[jj] = __expf(p[jj] - mx); tot += p[jj]; }
         const float rinv = 1.f / tot;
 #pragma unroll
-        for (int jj = 0; jj < KG; ++jj) { p[jj] *= rinv; sP[row * KG + jj] = p[jj]; }
+        for (int jj = 0; jj < KG; ++jj) { p[jj] *= rinv; sPg[row * KG + jj] = p[jj]; }
       }
-      float ctx[XK];
+      {
+        float ctx[HD];
 #pragma unroll
-      for (int c = 0; c < DT; ++c) ctx[c] = 0.f;
+        for (int c = 0; c < HD; ++c) ctx[c] = 0.f;
 #pragma unroll
-      for (int jj = 0; jj < KG; ++jj) axpy8_bf16<DT>(ctx, p[jj], sQKV + (g0 + jj) * QS + 2 * DT);
-#pragma unroll
-      for (int c = DT; c < XK; ++c) ctx[c] = c == DT ? 1.f : 0.f;
-      store_row(sCTX, row, XK, ctx, XK);
+        for (int jj = 0; jj < KG; ++jj) axpy8_bf16<HD>(ctx, p[jj], sQKV + (g0 + jj) * QS + 2 * DT + c0);
+        store_row(sCTX, row, XK, ctx, HD, c0);
+      }
+      ones_col(sCTX);
       signal();
       // ---- R2: x1 = h + ctx·Wo + bo; LN2
       wait_d();
-      float x1[DT];
-      tmem_row<DT>(T_W2 + lo, x1);
+      float x1[HD];
+      tmem_row<HD>(T_W2 + lo + c0, x1);
 #pragma unroll
-      for (int c = 0; c < DT; ++c) x1[c] += h[c] + bo_[c];
-      float x1n[XK], inv2;
-      ln_row_s<DT>(x1, lg2, lb2, x1n, inv2);
+      for (int c = 0; c < HD; ++c) x1[c] += h[c] + bo_[c0 + c];
+      float mu2, inv2;
+      ln_stats(x1, mu2, inv2);
+      {
+        float x1n[HD];
 #pragma unroll
-      for (int c = DT; c < XK; ++c) x1n[c] = c == DT ? 1.f : 0.f;
-      store_row(sX1N, row, XK, x1n, XK);
+        for (int c = 0; c < HD; ++c) x1n[c] = (x1[c] - mu2) * inv2 * lg2[c0 + c] + lb2[c0 + c];
+        store_row(sX1N, row, XK, x1n, HD, c0);
+      }
+      ones_col(sX1N);
       signal();
-      // ---- R3: FFN: gf = GELU(f1), df = (dX2·W2ᵀ) ⊙ GELU'(f1)
+      // ---- R3: FFN: gf = GELU(f1), df = (dX2·W2ᵀ) ⊙ GELU'(f1)   (this warp: FH hidden columns)
       wait_d();
 #pragma unroll 1
-      for (int c0 = 0; c0 < F4; c0 += 32) {
+      for (int cc = grp * FH; cc < grp * FH + FH; cc += 32) {
         float fv[32], gv[32];
-        tmem_row<32>(T_W0 + lo + c0, fv);
-        tmem_row<32>(T_W1 + lo + c0, gv);
+        tmem_row<32>(T_W0 + lo + cc, fv);
+        tmem_row<32>(T_W1 + lo + cc, gv);
 #pragma unroll
         for (int u = 0; u < 32; ++u) {
           float gd;                                                   // b1 added by the MMA
           fv[u] = gelu_and_grad(fv[u], gd);
           gv[u] *= gd;
         }
-        store_row(sGF, row, F4, fv, 32, c0);
-        store_row(sDF, row, F4, gv, 32, c0);
+        store_row(sGF, row, F4, fv, 32, cc);
+        store_row(sDF, row, F4, gv, 32, cc);
       }
       signal();
       // ---- R4: LN2 backward → dx1 = dX2 + LN2ᵀ(dx1n)
       wait_d();
-      float g[DT];
-      tmem_row<DT>(T_W2 + lo, g);                                     // dx1n
-      float mu2 = 0.f;
+      float g[HD], xh[HD], dx1[HD], tmp[HD];
+      tmem_row<HD>(T_W2 + lo + c0, g);                                // dx1n
+      {
+        float m[2] = {0.f, 0.f};
 #pragma unroll
-      for (int c = 0; c < DT; ++c) mu2 += x1[c];
-      mu2 *= 1.f / DT;
-      float xh[DT], m1 = 0.f, m2 = 0.f;
+        for (int c = 0; c < HD; ++c) {
+          xh[c] = (x1[c] - mu2) * inv2;
+          const float gh = g[c] * lg2[c0 + c];
+          m[0] += gh;
+          m[1] += gh * xh[c];
+        }
+        xsum(m, 2);
+        const float m1 = m[0] * (1.f / DT), m2 = m[1] * (1.f / DT);
 #pragma unroll
-      for (int c = 0; c < DT; ++c) {
-        xh[c] = (x1[c] - mu2) * inv2;
-        const float gh = g[c] * lg2[c];
-        m1 += gh;
-        m2 += gh * xh[c];
+        for (int c = 0; c < HD; ++c) {
+          dx1[c] = dx2[c] + (g[c] * lg2[c0 + c] - m1 - xh[c] * m2) * inv2;
+          tmp[c] = g[c] * xh[c];
+        }
       }
-      m1 *= 1.f / DT;
-      m2 *= 1.f / DT;
-      float dx1[DT], tmp[DT];
-#pragma unroll
-      for (int c = 0; c < DT; ++c) {
-        dx1[c] = dx2[c] + (g[c] * lg2[c] - m1 - xh[c] * m2) * inv2;
-        tmp[c] = g[c] * xh[c];
-      }
-      cs_l2g += warp_colsum<DT>(tmp);
-      cs_l2b += warp_colsum<DT>(g);
-      cs_b2 += warp_colsum<DT>(dx2);
-      store_row(sDX1, row, DT, dx1, DT);
+      cs_l2g += warp_colsum<HD>(tmp);
+      cs_l2b += warp_colsum<HD>(g);
+      cs_b2 += warp_colsum<HD>(dx2);
+      store_row(sDX1, row, DT, dx1, HD, c0);
       signal();
       // ---- R5: dctx → group attention backward → dqkv
       wait_d();
-      float dc[DT];
-      tmem_row<DT>(T_W2 + lo, dc);
+      {
+        float dc[HD];
+        tmem_row<HD>(T_W2 + lo + c0, dc);
 #pragma unroll
-      for (int c = 0; c < DT; c += 4)
-        *reinterpret_cast<float4*>(sDC + row * DCS + c) = make_float4(dc[c], dc[c + 1], dc[c + 2], dc[c + 3]);
+        for (int c = 0; c < HD; c += 4)
+          *reinterpret_cast<float4*>(sDC + row * DCS + c0 + c) = make_float4(dc[c], dc[c + 1], dc[c + 2], dc[c + 3]);
+        float dp[KG];
+#pragma unroll
+        for (int jj = 0; jj < KG; ++jj) dp[jj] = dot8_bf16<HD>(dc, sQKV + (g0 + jj) * QS + 2 * DT + c0);
+        xsum(dp, KG);
+        float D = 0.f;
+#pragma unroll
+        for (int jj = 0; jj < KG; ++jj) D += dp[jj] * p[jj];
+#pragma unroll
+        for (int jj = 0; jj < KG; ++jj) sSg[row * KG + jj] = p[jj] * (dp[jj] - D) * scale;
+      }
       __syncwarp();
       {
-        float dp[KG], D = 0.f;
+        float dqkv[3 * HD];
 #pragma unroll
-        for (int jj = 0; jj < KG; ++jj) {
-          const float acc = dot8_bf16<DT>(dc, sQKV + (g0 + jj) * QS + 2 * DT);
-          dp[jj] = acc;
-          D += acc * p[jj];
+        for (int c = 0; c < 3 * HD; ++c) dqkv[c] = 0.f;
+#pragma unroll
+        for (int jj = 0; jj < KG; ++jj) {         // same per-element summation order as a c-outer loop
+          const bf16* pr = sQKV + (g0 + jj) * QS;
+          axpy8_bf16<HD>(dqkv, sSg[row * KG + jj], pr + DT + c0);           // dq += dS_ij k_j
+          axpy8_bf16<HD>(dqkv + HD, sSg[(g0 + jj) * KG + me], pr + c0);     // dk += dS_ji q_j
+          const float pj = sPg[(g0 + jj) * KG + me];                        // dv += P_ji dctx_j
+          const float* dcr = sDC + (g0 + jj) * DCS + c0;
+#pragma unroll
+          for (int c = 0; c < HD; c += 4) {
+            const float4 d4 = *reinterpret_cast<const float4*>(dcr + c);
+            dqkv[2 * HD + c] = fmaf(pj, d4.x, dqkv[2 * HD + c]);
+            dqkv[2 * HD + c + 1] = fmaf(pj, d4.y, dqkv[2 * HD + c + 1]);
+            dqkv[2 * HD + c + 2] = fmaf(pj, d4.z, dqkv[2 * HD + c + 2]);
+            dqkv[2 * HD + c + 3] = fmaf(pj, d4.w, dqkv[2 * HD + c + 3]);
+          }
         }
-#pragma unroll
-        for (int jj = 0; jj < KG; ++jj) sS[row * KG + jj] = p[jj] * (dp[jj] - D) * scale;
+        __syncwarp();
+        store_row(sDQKV, row, 3 * DT, dqkv, HD, c0);
+        store_row(sDQKV, row, 3 * DT, dqkv + HD, HD, DT + c0);
+        store_row(sDQKV, row, 3 * DT, dqkv + 2 * HD, HD, 2 * DT + c0);
       }
-      __syncwarp();
-      float dqkv[3 * DT];
-#pragma unroll
-      for (int c = 0; c < 3 * DT; ++c) dqkv[c] = 0.f;
-#pragma unroll
-      for (int jj = 0; jj < KG; ++jj) {           // same per-element summation order as a c-outer loop
-        const bf16* pr = sQKV + (g0 + jj) * QS;
-        axpy8_bf16<DT>(dqkv, sS[row * KG + jj], pr + DT);                  // dq += dS_ij k_j
-        axpy8_bf16<DT>(dqkv + DT, sS[(g0 + jj) * KG + me], pr);            // dk += dS_ji q_j
-        const float pj = sP[(g0 + jj) * KG + me];                          // dv += P_ji dctx_j
-        const float* dcr = sDC + (g0 + jj) * DCS;
-#pragma unroll
-        for (int c = 0; c < DT; c += 4) {
-          const float4 d4 = *reinterpret_cast<const float4*>(dcr + c);
-          dqkv[2 * DT + c] = fmaf(pj, d4.x, dqkv[2 * DT + c]);
-          dqkv[2 * DT + c + 1] = fmaf(pj, d4.y, dqkv[2 * DT + c + 1]);
-          dqkv[2 * DT + c + 2] = fmaf(pj, d4.z, dqkv[2 * DT + c + 2]);
-          dqkv[2 * DT + c + 3] = fmaf(pj, d4.w, dqkv[2 * DT + c + 3]);
-        }
-      }
-      __syncwarp();
-      store_row(sDQKV, row, 3 * DT, dqkv, 3 * DT);
       signal();
       // ---- R6: LN1 backward → dh = dx1 + LN1ᵀ(dxn)
       wait_d();
-      tmem_row<DT>(T_W2 + lo, g);                                     // dxn
-      float mu1 = 0.f;
+      tmem_row<HD>(T_W2 + lo + c0, g);                                // dxn
+      {
+        float m[2] = {0.f, 0.f};
 #pragma unroll
-      for (int c = 0; c < DT; ++c) mu1 += h[c];
-      mu1 *= 1.f / DT;
-      m1 = 0.f;
-      m2 = 0.f;
+        for (int c = 0; c < HD; ++c) {
+          xh[c] = (h[c] - mu1) * inv1;
+          const float gh = g[c] * lg1[c0 + c];
+          m[0] += gh;
+          m[1] += gh * xh[c];
+        }
+        xsum(m, 2);
+        const float m1 = m[0] * (1.f / DT), m2 = m[1] * (1.f / DT);
 #pragma unroll
-      for (int c = 0; c < DT; ++c) {
-        xh[c] = (h[c] - mu1) * inv1;
-        const float gh = g[c] * lg1[c];
-        m1 += gh;
-        m2 += gh * xh[c];
+        for (int c = 0; c < HD; ++c) {
+          dx1[c] += (g[c] * lg1[c0 + c] - m1 - xh[c] * m2) * inv1;
+          tmp[c] = g[c] * xh[c];
+        }
       }
-      m1 *= 1.f / DT;
-      m2 *= 1.f / DT;
-#pragma unroll
-      for (int c = 0; c < DT; ++c) {
-        dx1[c] += (g[c] * lg1[c] - m1 - xh[c] * m2) * inv1;
-        tmp[c] = g[c] * xh[c];
-      }
-      cs_l1g += warp_colsum<DT>(tmp);
-      cs_l1b += warp_colsum<DT>(g);
+      cs_l1g += warp_colsum<HD>(tmp);
+      cs_l1b += warp_colsum<HD>(g);
       if (in_range) {
-        float4* dst = reinterpret_cast<float4*>(a.dh_out + t * DT);
 #pragma unroll
-        for (int c = 0; c < DT; c += 4) dst[c / 4] = make_float4(dx1[c], dx1[c + 1], dx1[c + 2], dx1[c + 3]);
+        for (int c = 0; c < HD; c += 4)
+          *reinterpret_cast<float4*>(a.dh_out + t * DT + c0 + c) = make_float4(dx1[c], dx1[c + 1], dx1[c + 2], dx1[c + 3]);
       }
     }
     // ---- flush this CTA's accumulators (gradient slots: 0 w_q,1 b_q,2 w_k,3 b_k,4 w_v,5 b_v,
-    //      6 w_o,7 b_o,8 w1,9 b1,10 w2,11 b2,12 ln1_g,13 ln1_b,14 ln2_g,15 ln2_b)
+    //      6 w_o,7 b_o,8 w1,9 b1,10 w2,11 b2,12 ln1_g,13 ln1_b,14 ln2_g,15 ln2_b); each warp
+    //      flushes its column half, the last group the bias column
     if (my_tiles > 0) {
       float* const* G = a.g_inner;
+      const bool bias_col = grp == NG - 1;
+      float w[HD], wb[16];
       {   // dW2 [4d][d]: TMEM row f = hidden unit
-        float w[DT];
-        tmem_row<DT>(T_DW2 + lo, w);
+        tmem_row<HD>(T_DW2 + lo + c0, w);
 #pragma unroll
-        for (int c = 0; c < DT; ++c) atomicAdd(G[10] + row * DT + c, w[c]);
+        for (int c = 0; c < HD; ++c) atomicAdd(G[10] + row * DT + c0 + c, w[c]);
       }
       {   // [dW1ᵀ | db1]: row f = hidden unit
-        float w[XK];
-        tmem_row<XK>(T_DW1 + lo, w);
+        tmem_row<HD>(T_DW1 + lo + c0, w);
+        tmem_row<16>(T_DW1 + lo + DT, wb);
 #pragma unroll
-        for (int c = 0; c < DT; ++c) atomicAdd(G[8] + c * F4 + row, w[c]);
-        atomicAdd(G[9] + row, w[DT]);
+        for (int c = 0; c < HD; ++c) atomicAdd(G[8] + (c0 + c) * F4 + row, w[c]);
+        if (bias_col) atomicAdd(G[9] + row, wb[0]);
       }
       {   // [dWoᵀ | dbo]: row c = output column of W_o (first DT rows valid)
-        float w[XK];
-        tmem_row<XK>(T_DWO + lo, w);
+        tmem_row<HD>(T_DWO + lo + c0, w);
+        tmem_row<16>(T_DWO + lo + DT, wb);
         if (row < DT) {
 #pragma unroll
-          for (int k = 0; k < DT; ++k) atomicAdd(G[6] + k * DT + row, w[k]);
-          atomicAdd(G[7] + row, w[DT]);
+          for (int k = 0; k < HD; ++k) atomicAdd(G[6] + (c0 + k) * DT + row, w[k]);
+          if (bias_col) atomicAdd(G[7] + row, wb[0]);
         }
       }
       {   // [dWqkvᵀ | dbqkv]: row o ∈ [0, 3d)
-        float w[XK];
-        tmem_row<XK>(T_DWQ + lo, w);
+        tmem_row<HD>(T_DWQ + lo + c0, w);
+        tmem_row<16>(T_DWQ + lo + DT, wb);
         if (row < 3 * DT) {
           const int which = row / DT, oc = row % DT;
 #pragma unroll
-          for (int k = 0; k < DT; ++k) atomicAdd(G[2 * which] + k * DT + oc, w[k]);
-          atomicAdd(G[2 * which + 1] + oc, w[DT]);
+          for (int k = 0; k < HD; ++k) atomicAdd(G[2 * which] + (c0 + k) * DT + oc, w[k]);
+          if (bias_col) atomicAdd(G[2 * which + 1] + oc, wb[0]);
         }
       }
-      if (lane < DT) {
-        atomicAdd(G[12] + lane, cs_l1g);
-        atomicAdd(G[13] + lane, cs_l1b);
-        atomicAdd(G[14] + lane, cs_l2g);
-        atomicAdd(G[15] + lane, cs_l2b);
-        atomicAdd(G[11] + lane, cs_b2);
+      if (lane < HD) {
+        atomicAdd(G[12] + c0 + lane, cs_l1g);
+        atomicAdd(G[13] + c0 + lane, cs_l1b);
+        atomicAdd(G[14] + c0 + lane, cs_l2g);
+        atomicAdd(G[15] + c0 + lane, cs_l2b);
+        atomicAdd(G[11] + c0 + lane, cs_b2);
       }
     }
   }
@@ -433,21 +492,32 @@ __global__ void __launch_bounds__(kThreads, 1) fe_inner_bwd_kernel(FrontArgs a) 
   if (warp == 0) sm100::tmem_dealloc<512>(tmem);
 }
 
-template <int DT, int KG>
-int launch_inner_bwd(const FrontArgs& a, cudaStream_t st) {
+template <int DT, int KG, int NG>
+int launch_inner_bwd_ng(const FrontArgs& a, cudaStream_t st) {
   constexpr int XK = DT + 16, F4 = 4 * DT, QS = 3 * DT + 8;
   const int nW = 7 * DT * XK + DT * DT + 12 * DT * DT;
-  const int smem = nW * 2 + kTile * (3 * XK + 2 * DT + 2 * F4 + QS) * 2 + kTile * KG * 8 + 5 * DT * 4 + 64;
+  const int smem = nW * 2 + kTile * (3 * XK + 2 * DT + 2 * F4 + QS) * 2 + NG * kTile * KG * 8 + 5 * DT * 4 +
+                   (NG > 1 ? 2 * NG * kTile * 8 * 4 : 0) + 64;
   if (smem > 227 * 1024) return (int)cudaErrorInvalidValue;
   static int done = 0;
   if (!done) {
-    cudaFuncSetAttribute(fe_inner_bwd_kernel<DT, KG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(fe_inner_bwd_kernel<DT, KG, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     done = 1;
   }
   const long long ntiles = (a.T + kTile - 1) / kTile;
   const int grid = (int)std::min<long long>(ntiles, 148);
-  launch(fe_inner_bwd_kernel<DT, KG>, grid, kThreads, std::max(smem, 116 * 1024), st, a);
+  launch(fe_inner_bwd_kernel<DT, KG, NG>, grid, 32 * (1 + kWorkers * NG), std::max(smem, 116 * 1024), st, a);
   return (int)cudaGetLastError();
+}
+
+// head width 32: eight workers (column pairs) unless LONGER_INNER_NG=1
+template <int DT, int KG>
+int launch_inner_bwd(const FrontArgs& a, cudaStream_t st) {
+  if constexpr (DT == 32) {
+    const char* env = std::getenv("LONGER_INNER_NG");
+    if (!(env && env[0] == '1')) return launch_inner_bwd_ng<DT, KG, 2>(a, st);
+  }
+  return launch_inner_bwd_ng<DT, KG, 1>(a, st);
 }
 
 }  // namespace
