@@ -794,14 +794,16 @@ int block_bwd(const Ctx& c, cudaStream_t ss, const BlockOff& bo, const BlockBufs
     colsum_bf16(p.dKV, (int)V, D, 2 * D, c.g(bo.b_k), ss);
     colsum_bf16(p.dKV + D, (int)V, D, 2 * D, c.g(bo.b_v), ss);
     TRY(lin_dx(st, b.g_dqkv, D, Q, Wqkv, D, D, D, b.g_dqn, D, nullptr, 0));
-    TRY(lin_dx(st, p.dKV, 2 * D, V, p.pk.c_wkv, 2 * D, D, 2 * D, p.dkn, D, nullptr, 0));
+    // dK|dV → d(kn) in bf16 (it only feeds the HBM-bound LN backward below), in p.dkn's storage
+    bf16* dkn_bf = reinterpret_cast<bf16*>(p.dkn);
+    TRY(lin_dx(st, p.dKV, 2 * D, V, p.pk.c_wkv, 2 * D, D, 2 * D, nullptr, 0, dkn_bf, D));
     RowMap r{};
     r.A = p.merged; r.lda = D; r.a_rows = p.G; r.a_off = 0; r.na = p.G; r.Bsrc = p.glob; r.ldb = D; r.nb = p.m;
     r.batch = p.B;
     RowMapW rw{};
     rw.A = p.dmerged; rw.lda = D; rw.a_rows = p.G; rw.a_off = 0; rw.na = p.G; rw.Bsrc = p.dglob; rw.ldb = D;
     rw.nb = p.m; rw.batch = p.B;
-    layernorm_bwd(r, D, c.w(bo.ln1_g), p.mk, p.rk, p.dkn, D, rw, 0, nullptr, c.g(bo.ln1_g), c.g(bo.ln1_b), st);
+    layernorm_bwd(r, D, c.w(bo.ln1_g), p.mk, p.rk, dkn_bf, D, rw, c.g(bo.ln1_g), c.g(bo.ln1_b), st);
     LnBwdExtra ex;
     ex.addend = b.g_dx1;
     layernorm_bwd(rows_plain(xq, D, Q), D, c.w(bo.ln1_g), b.m1, b.r1, b.g_dqn, D, rows_plain_w(p.dO, D, Q), 0,

@@ -178,6 +178,25 @@ __device__ __forceinline__ void ln_load(const float* __restrict__ p, int lane, i
 }
 
 template <int VPT, bool CONTIG>
+__device__ __forceinline__ void ln_load(const bf16* __restrict__ p, int lane, int W, float* v) {
+  if constexpr (CONTIG && VPT == 8) {
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(p + lane * 8));
+    const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) { v[2 * t] = sm100::bf16_lo(w[t]); v[2 * t + 1] = sm100::bf16_hi(w[t]); }
+  } else if constexpr (CONTIG && VPT == 4) {
+    const uint2 a = __ldg(reinterpret_cast<const uint2*>(p + lane * 4));
+    v[0] = sm100::bf16_lo(a.x); v[1] = sm100::bf16_hi(a.x); v[2] = sm100::bf16_lo(a.y); v[3] = sm100::bf16_hi(a.y);
+  } else {
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) {
+      const int c = ln_col<VPT, CONTIG>(lane, u);
+      v[u] = c < W ? __bfloat162float(p[c]) : 0.f;
+    }
+  }
+}
+
+template <int VPT, bool CONTIG>
 __global__ void ln_fwd_kernel(RowMap x, int W, const float* __restrict__ g, const float* __restrict__ bta,
                               bf16* y, float* mean, float* rstd) {
   pdl_trigger();
@@ -255,9 +274,9 @@ void layernorm_fwd(const RowMap& x, int W, const float* g, const float* b, bf16*
 }
 
 // LN backward (pkg/src/longrec/tensors.py:368-378): dx = (ĝ − mean ĝ − x̂·mean(ĝx̂))·σ⁻¹, ĝ = dy·g
-template <int VPT, bool CONTIG>
+template <int VPT, bool CONTIG, typename TY = float>
 __global__ void ln_bwd_kernel(RowMap x, int W, const float* __restrict__ g, const float* __restrict__ mean,
-                              const float* __restrict__ rstd, const float* __restrict__ dy, int ldy, RowMapW out,
+                              const float* __restrict__ rstd, const TY* __restrict__ dy, int ldy, RowMapW out,
                               int accumulate, const float* rowmask, float* dgain, float* dbias, LnBwdExtra ex) {
   pdl_trigger();
   pdl_wait();
@@ -379,6 +398,26 @@ __global__ void ln_bwd_kernel(RowMap x, int W, const float* __restrict__ g, cons
       if (ex.colsum_out) atomicAdd(&ex.colsum_out[c], cc);
     }
   }
+}
+
+// bf16 dy (a dX GEMM written in bf16: half the bytes of the HBM-bound K/V-row LN backward)
+void layernorm_bwd(const RowMap& x, int W, const float* g, const float* mean, const float* rstd, const bf16* dy,
+                   int ldy, const RowMapW& out, float* dgain, float* dbias, cudaStream_t st) {
+  const int rows = x.rows();
+  if (rows <= 0) return;
+  const int grid = std::max(1, std::min(cdiv(rows, 32), 148 * 8));
+  const bool ct = W == 128 && ln_contig(W, 4, x.A, x.lda, x.nb ? x.Bsrc : nullptr, x.ldb) &&
+                  ln_contig(W, 4, out.A, out.lda, out.nb ? out.Bsrc : nullptr, out.ldb) && ldy % 4 == 0 &&
+                  (reinterpret_cast<uintptr_t>(dy) & 7) == 0;
+  if (ct)
+    launch(ln_bwd_kernel<4, true, bf16>, grid, 256, 0, st, x, W, g, mean, rstd, dy, ldy, out, 0,
+           static_cast<const float*>(nullptr), dgain, dbias, LnBwdExtra());
+  else if (W <= 128)
+    launch(ln_bwd_kernel<4, false, bf16>, grid, 256, 0, st, x, W, g, mean, rstd, dy, ldy, out, 0,
+           static_cast<const float*>(nullptr), dgain, dbias, LnBwdExtra());
+  else
+    launch(ln_bwd_kernel<8, false, bf16>, grid, 256, 0, st, x, W, g, mean, rstd, dy, ldy, out, 0,
+           static_cast<const float*>(nullptr), dgain, dbias, LnBwdExtra());
 }
 
 void layernorm_bwd(const RowMap& x, int W, const float* g, const float* mean, const float* rstd, const float* dy,

@@ -69,6 +69,10 @@ void layernorm_bwd(const RowMap& x, int W, const float* g, const float* mean, co
                    const float* dy, int ldy, const RowMapW& out, int accumulate, const float* rowmask,
                    float* dgain, float* dbias, cudaStream_t st, LnBwdExtra ex = LnBwdExtra());
 
+// the same with a bf16 dy and no extras (W ≤ 256)
+void layernorm_bwd(const RowMap& x, int W, const float* g, const float* mean, const float* rstd,
+                   const bf16* dy, int ldy, const RowMapW& out, float* dgain, float* dbias, cudaStream_t st);
+
 // column sums of a [rows, W] matrix (fp32 or bf16), atomically added to out[W]
 void colsum_f32(const float* x, int rows, int W, int ld, float* out, cudaStream_t st);
 void colsum_bf16(const bf16* x, int rows, int W, int ld, float* out, cudaStream_t st);
