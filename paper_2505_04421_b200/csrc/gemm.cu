@@ -181,10 +181,19 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     int n0, m0, kb_begin_unused, nkb_unused;
     item(w, n0, m0, kb_begin_unused, nkb_unused);
     const int buf = j & 1;
+    const uint32_t flags = g.flags;
+    // bias of this warp's column chunks, one value per lane (broadcast by shuffles below), loaded
+    // before the accumulator wait so the load latency hides behind the MMAs
+    constexpr int NCH = (BN + 63) / 64;
+    float bias_l[NCH];
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+      const int col = n0 + (e >> 2) * 32 + 64 * k + lane;
+      bias_l[k] = ((flags & EPI_BIAS) && col < g.N) ? __ldg(g.bias + col) : 0.f;
+    }
     sm100::mbar_wait(&tmem_full[buf], (j >> 1) & 1);
     sm100::tc_fence_after();
     const uint32_t tmem_acc = tmem + (uint32_t)(buf * BN);
-    const uint32_t flags = g.flags;
     const int row = m0 + q * 32 + lane;
     const bool row_ok = row < g.M;
     const float rmask = ((flags & EPI_ROWMASK) && row_ok) ? g.rowmask[row] : 1.f;
@@ -202,12 +211,12 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       if (staged && nb + 32 <= g.N) {
         // warp-collective path: rows past M compute on zeros and are never stored
         if (flags & EPI_BIAS) {
-          const float4* bp = reinterpret_cast<const float4*>(g.bias + nb);
+          float bl = bias_l[0];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float4 b4 = __ldg(bp + j);
-            v[4 * j] += b4.x; v[4 * j + 1] += b4.y; v[4 * j + 2] += b4.z; v[4 * j + 3] += b4.w;
-          }
+          for (int k = 1; k < NCH; ++k)
+            if (c == (e >> 2) * 32 + 64 * k) bl = bias_l[k];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] += __shfl_sync(0xffffffffu, bl, j);
         }
         if (flags & EPI_SAVE_PRE) store_bf16(g.pre_bf16, g.ldc_bf, m_base, nb, v);
         if (flags & EPI_GELU) {
