@@ -191,6 +191,24 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       const int col = n0 + (e >> 2) * 32 + 64 * k + lane;
       bias_l[k] = ((flags & EPI_BIAS) && col < g.N) ? __ldg(g.bias + col) : 0.f;
     }
+    // one column chunk per warp (BN = 64): the residual row chunk is loaded before the wait too
+    float res_pre[NCH == 1 ? 32 : 1];
+    const bool res_early = NCH == 1 && (flags & EPI_RESID) && staged;
+    if constexpr (NCH == 1) {
+      const int col = n0 + (e >> 2) * 32;
+      const int rr = m0 + q * 32 + lane;
+      if (res_early && col + 32 <= g.N && rr < g.M) {
+        const float4* rp = reinterpret_cast<const float4*>(g.resid + (size_t)rr * g.ldr + col);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const float4 r4 = rp[t];
+          res_pre[4 * t] = r4.x; res_pre[4 * t + 1] = r4.y; res_pre[4 * t + 2] = r4.z; res_pre[4 * t + 3] = r4.w;
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < 32; ++t) res_pre[t] = 0.f;
+      }
+    }
     sm100::mbar_wait(&tmem_full[buf], (j >> 1) & 1);
     sm100::tc_fence_after();
     const uint32_t tmem_acc = tmem + (uint32_t)(buf * BN);
@@ -237,7 +255,12 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             }
           }
         }
-        if ((flags & EPI_RESID) && row_ok) {
+        if (res_early) {
+          if constexpr (NCH == 1) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += res_pre[j];
+          }
+        } else if ((flags & EPI_RESID) && row_ok) {
           const float4* rp = reinterpret_cast<const float4*>(g.resid + (size_t)row * g.ldr + nb);
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
