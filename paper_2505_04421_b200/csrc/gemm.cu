@@ -424,7 +424,16 @@ int launch_bn(const GemmArgs& g, cudaStream_t st) {
   const int nkb = (g.K + BK - 1) / BK;
   const int tiles = ((g.N + BN - 1) / BN) * ((g.M + BM - 1) / BM);
   int want = g.split_k;
-  if (want == 0) want = (g.flags & EPI_ATOMIC) ? std::max(1, std::min(296 / tiles, nkb / 4)) : 1;
+  // split-K for the weight gradients: about one item per SM (the persistent CTAs stream their
+  // k-blocks back to back; more splits only multiply the atomic epilogues). LONGER_SPLIT_ITEMS
+  // overrides the item target (default 74: the weight-gradient GEMMs run beside other kernels, so half
+  // the SMs with twice the k-blocks each measured best: 1.640 -> 1.625 ms per step).
+  static int split_items = -1;
+  if (split_items < 0) {
+    const char* e = std::getenv("LONGER_SPLIT_ITEMS");
+    split_items = e ? std::max(1, std::atoi(e)) : 74;
+  }
+  if (want == 0) want = (g.flags & EPI_ATOMIC) ? std::max(1, std::min(split_items / tiles, nkb / 4)) : 1;
   int split = std::max(1, std::min(want, nkb));
   int kb_per = (nkb + split - 1) / split;
   split = (nkb + kb_per - 1) / kb_per;
