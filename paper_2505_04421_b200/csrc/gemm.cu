@@ -424,10 +424,10 @@ int launch_bn(const GemmArgs& g, cudaStream_t st) {
   const int nkb = (g.K + BK - 1) / BK;
   const int tiles = ((g.N + BN - 1) / BN) * ((g.M + BM - 1) / BM);
   int want = g.split_k;
-  // split-K for the weight gradients: about one item per SM (the persistent CTAs stream their
-  // k-blocks back to back; more splits only multiply the atomic epilogues). LONGER_SPLIT_ITEMS
-  // overrides the item target (default 74: the weight-gradient GEMMs run beside other kernels, so half
-  // the SMs with twice the k-blocks each measured best: 1.640 -> 1.625 ms per step).
+  // split-K for the weight gradients: about 74 items (the persistent CTAs stream their k-blocks back
+  // to back; more splits only multiply the atomic epilogues, and these GEMMs run beside other
+  // kernels on the side stream: 296 → 148 → 74 items measured 1.648 → 1.640 → 1.625 ms per step).
+  // LONGER_SPLIT_ITEMS overrides the target.
   static int split_items = -1;
   if (split_items < 0) {
     const char* e = std::getenv("LONGER_SPLIT_ITEMS");
