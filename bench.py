@@ -223,13 +223,14 @@ def main():
     host = [synthetic_batch(cfg, B, seed=100 + rank * 17 + i).pin() for i in range(n_batches)]
     dev_batches = [h.to(dev) for h in host]
     static = synthetic_batch(cfg, B, seed=1).to(dev)          # graph input slot
+    static2 = synthetic_batch(cfg, B, seed=2).to(dev)         # second slot (e2e double buffering)
 
     def load(b):
         for f in type(b).FIELDS:
             getattr(static, f).copy_(getattr(b, f), non_blocking=True)
 
-    def step_body():
-        model.loss_backward(static, check=False)
+    def step_body(batch=None):
+        model.loss_backward(static if batch is None else batch, check=False)
         if world > 1:
             dist.all_reduce(model.grad_flat)
             model.grad_flat.mul_(1.0 / world)
@@ -268,15 +269,22 @@ def main():
         with torch.cuda.graph(graph):
             step_body()
         torch.cuda.synchronize()
+        # the same step reading the second input slot: the e2e loop alternates slots, so the H2D of
+        # step i+1 lands directly in the slot the next graph reads (no device-side copy)
+        graph2 = torch.cuda.CUDAGraph(keep_graph=True)
+        with torch.cuda.graph(graph2):
+            step_body(static2)
+        torch.cuda.synchronize()
 
     if graph is not None:
         graph.instantiate() if hasattr(graph, "instantiate") else None
+        graph2.instantiate() if hasattr(graph2, "instantiate") else None
 
-    def run_step():
+    def run_step(slot=0):
         if graph is not None:
-            graph.replay()
+            (graph if slot == 0 else graph2).replay()
         else:
-            step_body()
+            step_body(static if slot == 0 else static2)
 
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
     for i in range(args.warmup):
@@ -320,11 +328,11 @@ def main():
 
     # ---------------- e2e: pinned host batch → H2D, step, loss D2H, every step
     # The usual input pipeline: step i+1's batch is copied host→device on a copy stream while step
-    # i runs (two device staging slots), the step starts with a device copy of its slot into the
-    # graph's input tensors, and the host reads step i's loss (pinned D2H) once step i+1 is queued.
+    # i runs, into the second of two input slots (one captured graph per slot, so no device-side
+    # copy), and the host reads step i's loss (pinned D2H) once step i+1 is queued.
     # One span from before the first H2D to after the last loss read, so every copy is inside it.
     copy_stream = torch.cuda.Stream(dev)
-    stage = [synthetic_batch(cfg, B, seed=2 + j).to(dev) for j in range(2)]
+    stage = [static, static2]
     copied = [torch.cuda.Event() for _ in range(2)]
     consumed = [None, None]
     loss_host = torch.zeros(args.steps, dtype=torch.float32).pin_memory()
@@ -352,11 +360,10 @@ def main():
         if i + 1 < args.steps:
             h2d(i + 1)
         stream.wait_event(copied[i % 2])
-        load(stage[i % 2])
-        consumed[i % 2] = torch.cuda.Event()
-        consumed[i % 2].record(stream)
         mark(f"e2e {i} loaded")
-        run_step()
+        run_step(i % 2)
+        consumed[i % 2] = torch.cuda.Event()                # the step has read its slot
+        consumed[i % 2].record(stream)
         mark(f"e2e {i} replayed")
         loss_host[i : i + 1].copy_(model._loss.view(1), non_blocking=True)
         loss_ev[i].record(stream)
@@ -427,7 +434,7 @@ def main():
             "gpu_launches_per_step": {"ours": n_ours, "torch_or_nccl": n_other},
             "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d_bytes,
                     "d2h_bytes_per_step": 4, "ms_per_step": e2e_ms / args.steps,
-                    "pipeline": "pinned H2D of step i+1 on a copy stream overlaps step i; loss of every step "
+                    "pipeline": "pinned H2D of step i+1 on a copy stream (into the other of two graph input slots) overlaps step i; loss of every step "
                                 "read on the host; one span from the first H2D to the last loss read"},
             "clocks": clk,
         }
