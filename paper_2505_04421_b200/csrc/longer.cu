@@ -655,11 +655,14 @@ int forward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs, fl
   const int d = p.d, D = p.D;
   const long long M = (long long)p.B * p.m;
   (void)with_loss;
-  TRY(pack_weights(p, c.P, p.ws, st));
   // global tokens (inputs.py:500-537): independent of the sequence front-end, so they run on the
-  // side stream beside it; main waits for them only where the query rows take the globals
+  // side stream beside it; main waits for them only where the query rows take the globals.  With
+  // the fused front-end (its own weight blob) the bf16 GEMM operand copies are packed there too:
+  // the main stream first needs them after that wait.
   const cudaStream_t ss = side_stream(st);
+  if (!p.fused_fe) TRY(pack_weights(p, c.P, p.ws, st));
   fork_side(st, ss);
+  if (p.fused_fe) TRY(pack_weights(p, c.P, p.ws, ss));
   GlobalsArgs ga{};
   ga.uid = bt.uid; ga.cand_item = bt.cand_item; ga.B = p.B; ga.m = p.m; ga.d = d; ga.D = D;
   ga.d_item = dm.d_item; ga.d_act = dm.d_act; ga.d_time = dm.d_time;
