@@ -400,6 +400,85 @@ __global__ void ln_bwd_kernel(RowMap x, int W, const float* __restrict__ g, cons
   }
 }
 
+// Lean LN backward for W = 128 with a bf16 dy and no extras: a warp takes R rows at a time (all
+// their loads issued before any reduction), lane owns 4 contiguous columns; gain / bias partials
+// stay in registers and are flushed once per block.
+template <int R>
+__global__ void __launch_bounds__(256) ln_bwd128_kernel(RowMap x, const float* __restrict__ g,
+                                                        const float* __restrict__ mean,
+                                                        const float* __restrict__ rstd, const bf16* __restrict__ dy,
+                                                        int ldy, RowMapW out, float* dgain, float* dbias) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ float sg[8][128], sb[8][128];
+  const int wid = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int rows = x.rows();
+  const int per = x.na + x.nb;
+  const float4 gv = __ldg(reinterpret_cast<const float4*>(g) + lane);
+  float pg[4] = {0.f, 0.f, 0.f, 0.f}, pb[4] = {0.f, 0.f, 0.f, 0.f};
+  const int stride = gridDim.x * 8 * R;
+  for (int r0 = (blockIdx.x * 8 + wid) * R; r0 < rows; r0 += stride) {
+    float4 xv[R];
+    uint2 dv[R];
+    float mu[R], inv[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int row = r0 + i;
+      if (row < rows) {
+        const int b = row / per, j = row % per;
+        const float* src = j < x.na ? x.A + (long long)(b * x.a_rows + x.a_off + j) * x.lda
+                                    : x.Bsrc + (long long)(b * x.nb + j - x.na) * x.ldb;
+        xv[i] = __ldg(reinterpret_cast<const float4*>(src) + lane);
+        dv[i] = __ldg(reinterpret_cast<const uint2*>(dy + (long long)row * ldy) + lane);
+        mu[i] = mean[row];
+        inv[i] = rstd[row];
+      } else {
+        xv[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        dv[i] = make_uint2(0, 0);
+        mu[i] = 0.f;
+        inv[i] = 0.f;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int row = r0 + i;
+      const float xr[4] = {xv[i].x, xv[i].y, xv[i].z, xv[i].w};
+      const float d[4] = {sm100::bf16_lo(dv[i].x), sm100::bf16_hi(dv[i].x), sm100::bf16_lo(dv[i].y),
+                          sm100::bf16_hi(dv[i].y)};
+      const float gg[4] = {gv.x, gv.y, gv.z, gv.w};
+      float xh[4], gh[4], s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        xh[u] = (xr[u] - mu[i]) * inv[i];
+        gh[u] = d[u] * gg[u];
+        s1 += gh[u];
+        s2 += gh[u] * xh[u];
+        if (row < rows) { pg[u] += d[u] * xh[u]; pb[u] += d[u]; }
+      }
+      const float m1 = warp_sum(s1) * (1.f / 128), m2 = warp_sum(s2) * (1.f / 128);
+      if (row < rows) {
+        const int b = row / per, j = row % per;
+        float* dst = j < out.na ? out.A + (long long)(b * out.a_rows + out.a_off + j) * out.lda
+                                : out.Bsrc + (long long)(b * out.nb + j - out.na) * out.ldb;
+        float o[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) o[u] = (gh[u] - m1 - xh[u] * m2) * inv[i];
+        reinterpret_cast<float4*>(dst)[lane] = make_float4(o[0], o[1], o[2], o[3]);
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) { sg[wid][lane * 4 + u] = pg[u]; sb[wid][lane * 4 + u] = pb[u]; }
+  __syncthreads();
+  if (threadIdx.x < 128) {
+    float a = 0.f, bb = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) { a += sg[w][threadIdx.x]; bb += sb[w][threadIdx.x]; }
+    atomicAdd(&dgain[threadIdx.x], a);
+    atomicAdd(&dbias[threadIdx.x], bb);
+  }
+}
+
 // bf16 dy (a dX GEMM written in bf16: half the bytes of the HBM-bound K/V-row LN backward)
 void layernorm_bwd(const RowMap& x, int W, const float* g, const float* mean, const float* rstd, const bf16* dy,
                    int ldy, const RowMapW& out, float* dgain, float* dbias, cudaStream_t st) {
@@ -409,7 +488,16 @@ void layernorm_bwd(const RowMap& x, int W, const float* g, const float* mean, co
   const bool ct = W == 128 && ln_contig(W, 4, x.A, x.lda, x.nb ? x.Bsrc : nullptr, x.ldb) &&
                   ln_contig(W, 4, out.A, out.lda, out.nb ? out.Bsrc : nullptr, out.ldb) && ldy % 4 == 0 &&
                   (reinterpret_cast<uintptr_t>(dy) & 7) == 0;
-  if (ct)
+  static int lean = -1;
+  if (lean < 0) {
+    const char* e = std::getenv("LONGER_LN_LEAN");
+    lean = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (ct && lean) {
+    constexpr int R = 4;
+    const int grid2 = std::max(1, std::min(cdiv(rows, 8 * R * 4), 148 * 3));   // 3 blocks fit per SM
+    launch(ln_bwd128_kernel<R>, grid2, 256, 0, st, x, g, mean, rstd, dy, ldy, out, dgain, dbias);
+  } else if (ct)
     launch(ln_bwd_kernel<4, true, bf16>, grid, 256, 0, st, x, W, g, mean, rstd, dy, ldy, out, 0,
            static_cast<const float*>(nullptr), dgain, dbias, LnBwdExtra());
   else if (W <= 128)
