@@ -403,11 +403,27 @@ __global__ void ln_bwd_kernel(RowMap x, int W, const float* __restrict__ g, cons
 // Lean LN backward for W = 128 with a bf16 dy and no extras: a warp takes R rows at a time (all
 // their loads issued before any reduction), lane owns 4 contiguous columns; gain / bias partials
 // stay in registers and are flushed once per block.
-template <int R>
+template <typename TY>
+__device__ __forceinline__ void ld4(const TY* p, int lane, float* d);
+template <>
+__device__ __forceinline__ void ld4<bf16>(const bf16* p, int lane, float* d) {
+  const uint2 v = __ldg(reinterpret_cast<const uint2*>(p) + lane);
+  d[0] = sm100::bf16_lo(v.x); d[1] = sm100::bf16_hi(v.x); d[2] = sm100::bf16_lo(v.y); d[3] = sm100::bf16_hi(v.y);
+}
+template <>
+__device__ __forceinline__ void ld4<float>(const float* p, int lane, float* d) {
+  const float4 v = __ldg(reinterpret_cast<const float4*>(p) + lane);
+  d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+}
+
+// optional per-row operands of the query-row LN backward: + addend (fp32), bf16 copy of the
+// output, column sums of the output (the next bias gradient)
+template <int R, typename TY, bool EX>
 __global__ void __launch_bounds__(256) ln_bwd128_kernel(RowMap x, const float* __restrict__ g,
                                                         const float* __restrict__ mean,
-                                                        const float* __restrict__ rstd, const bf16* __restrict__ dy,
-                                                        int ldy, RowMapW out, float* dgain, float* dbias) {
+                                                        const float* __restrict__ rstd, const TY* __restrict__ dy,
+                                                        int ldy, RowMapW out, float* dgain, float* dbias,
+                                                        LnBwdExtra ex) {
   pdl_trigger();
   pdl_wait();
   __shared__ float sg[8][128], sb[8][128];
@@ -415,11 +431,11 @@ __global__ void __launch_bounds__(256) ln_bwd128_kernel(RowMap x, const float* _
   const int rows = x.rows();
   const int per = x.na + x.nb;
   const float4 gv = __ldg(reinterpret_cast<const float4*>(g) + lane);
-  float pg[4] = {0.f, 0.f, 0.f, 0.f}, pb[4] = {0.f, 0.f, 0.f, 0.f};
+  float pg[4] = {0.f, 0.f, 0.f, 0.f}, pb[4] = {0.f, 0.f, 0.f, 0.f}, pc[4] = {0.f, 0.f, 0.f, 0.f};
   const int stride = gridDim.x * 8 * R;
   for (int r0 = (blockIdx.x * 8 + wid) * R; r0 < rows; r0 += stride) {
     float4 xv[R];
-    uint2 dv[R];
+    float dv[R][4], ad[R][4];
     float mu[R], inv[R];
 #pragma unroll
     for (int i = 0; i < R; ++i) {
@@ -429,12 +445,14 @@ __global__ void __launch_bounds__(256) ln_bwd128_kernel(RowMap x, const float* _
         const float* src = j < x.na ? x.A + (long long)(b * x.a_rows + x.a_off + j) * x.lda
                                     : x.Bsrc + (long long)(b * x.nb + j - x.na) * x.ldb;
         xv[i] = __ldg(reinterpret_cast<const float4*>(src) + lane);
-        dv[i] = __ldg(reinterpret_cast<const uint2*>(dy + (long long)row * ldy) + lane);
+        ld4<TY>(dy + (long long)row * ldy, lane, dv[i]);
+        if (EX && ex.addend) ld4<float>(ex.addend + (long long)row * 128, lane, ad[i]);
         mu[i] = mean[row];
         inv[i] = rstd[row];
       } else {
         xv[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        dv[i] = make_uint2(0, 0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { dv[i][u] = 0.f; ad[i][u] = 0.f; }
         mu[i] = 0.f;
         inv[i] = 0.f;
       }
@@ -443,8 +461,7 @@ __global__ void __launch_bounds__(256) ln_bwd128_kernel(RowMap x, const float* _
     for (int i = 0; i < R; ++i) {
       const int row = r0 + i;
       const float xr[4] = {xv[i].x, xv[i].y, xv[i].z, xv[i].w};
-      const float d[4] = {sm100::bf16_lo(dv[i].x), sm100::bf16_hi(dv[i].x), sm100::bf16_lo(dv[i].y),
-                          sm100::bf16_hi(dv[i].y)};
+      const float* d = dv[i];
       const float gg[4] = {gv.x, gv.y, gv.z, gv.w};
       float xh[4], gh[4], s1 = 0.f, s2 = 0.f;
 #pragma unroll
@@ -462,21 +479,40 @@ __global__ void __launch_bounds__(256) ln_bwd128_kernel(RowMap x, const float* _
                                 : out.Bsrc + (long long)(b * out.nb + j - out.na) * out.ldb;
         float o[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) o[u] = (gh[u] - m1 - xh[u] * m2) * inv[i];
+        for (int u = 0; u < 4; ++u) {
+          o[u] = (gh[u] - m1 - xh[u] * m2) * inv[i];
+          if (EX && ex.addend) o[u] += ad[i][u];
+          if (EX) pc[u] += o[u];
+        }
         reinterpret_cast<float4*>(dst)[lane] = make_float4(o[0], o[1], o[2], o[3]);
+        if (EX && ex.out_bf)
+          reinterpret_cast<uint2*>(ex.out_bf + (long long)row * 128)[lane] =
+              make_uint2(sm100::pack_bf16(o[0], o[1]), sm100::pack_bf16(o[2], o[3]));
       }
     }
   }
+  __shared__ float sc[8][128];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) { sg[wid][lane * 4 + u] = pg[u]; sb[wid][lane * 4 + u] = pb[u]; }
+  for (int u = 0; u < 4; ++u) {
+    sg[wid][lane * 4 + u] = pg[u]; sb[wid][lane * 4 + u] = pb[u]; sc[wid][lane * 4 + u] = pc[u];
+  }
   __syncthreads();
   if (threadIdx.x < 128) {
-    float a = 0.f, bb = 0.f;
+    float a = 0.f, bb = 0.f, cc = 0.f;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) { a += sg[w][threadIdx.x]; bb += sb[w][threadIdx.x]; }
-    atomicAdd(&dgain[threadIdx.x], a);
-    atomicAdd(&dbias[threadIdx.x], bb);
+    for (int w = 0; w < 8; ++w) { a += sg[w][threadIdx.x]; bb += sb[w][threadIdx.x]; cc += sc[w][threadIdx.x]; }
+    if (dgain) { atomicAdd(&dgain[threadIdx.x], a); atomicAdd(&dbias[threadIdx.x], bb); }
+    if (EX && ex.colsum_out) atomicAdd(&ex.colsum_out[threadIdx.x], cc);
   }
+}
+
+static int ln_lean() {
+  static int lean = -1;
+  if (lean < 0) {
+    const char* e = std::getenv("LONGER_LN_LEAN");
+    lean = (e && e[0] == '0') ? 0 : 1;
+  }
+  return lean;
 }
 
 // bf16 dy (a dX GEMM written in bf16: half the bytes of the HBM-bound K/V-row LN backward)
@@ -488,15 +524,10 @@ void layernorm_bwd(const RowMap& x, int W, const float* g, const float* mean, co
   const bool ct = W == 128 && ln_contig(W, 4, x.A, x.lda, x.nb ? x.Bsrc : nullptr, x.ldb) &&
                   ln_contig(W, 4, out.A, out.lda, out.nb ? out.Bsrc : nullptr, out.ldb) && ldy % 4 == 0 &&
                   (reinterpret_cast<uintptr_t>(dy) & 7) == 0;
-  static int lean = -1;
-  if (lean < 0) {
-    const char* e = std::getenv("LONGER_LN_LEAN");
-    lean = (e && e[0] == '0') ? 0 : 1;
-  }
-  if (ct && lean) {
+  if (ct && ln_lean()) {
     constexpr int R = 4;
-    const int grid2 = std::max(1, std::min(cdiv(rows, 8 * R * 4), 148 * 3));   // 3 blocks fit per SM
-    launch(ln_bwd128_kernel<R>, grid2, 256, 0, st, x, g, mean, rstd, dy, ldy, out, dgain, dbias);
+    const int grid2 = std::max(1, std::min(cdiv(rows, 8 * R), 148 * 3));        // 3 blocks fit per SM
+    launch(ln_bwd128_kernel<R, bf16, false>, grid2, 256, 0, st, x, g, mean, rstd, dy, ldy, out, dgain, dbias, LnBwdExtra());
   } else if (ct)
     launch(ln_bwd_kernel<4, true, bf16>, grid, 256, 0, st, x, W, g, mean, rstd, dy, ldy, out, 0,
            static_cast<const float*>(nullptr), dgain, dbias, LnBwdExtra());
@@ -520,6 +551,7 @@ void layernorm_bwd(const RowMap& x, int W, const float* g, const float* mean, co
   const bool ct = ln_contig(W, vpt, x.A, x.lda, x.nb ? x.Bsrc : nullptr, x.ldb) &&
                   ln_contig(W, vpt, out.A, out.lda, out.nb ? out.Bsrc : nullptr, out.ldb) &&
                   ln_contig(W, vpt, dy, ldy, nullptr, 0);
+
 #define LNB(V) (ct ? launch(ln_bwd_kernel<V, true>, grid, 256, 0, st, x, W, g, mean, rstd, dy, ldy, out, accumulate, rowmask, dgain, dbias, ex) \
                    : launch(ln_bwd_kernel<V, false>, grid, 256, 0, st, x, W, g, mean, rstd, dy, ldy, out, accumulate, rowmask, dgain, dbias, ex))
   if (vpt == 1) launch(ln_bwd_kernel<1, false>, grid, 256, 0, st, x, W, g, mean, rstd, dy, ldy, out, accumulate, rowmask, dgain, dbias, ex);
