@@ -225,6 +225,9 @@ struct Plan {
   LongerDims dims;
   void* ws;
   bool fused_fe;   // fused front-end kernel (frontend.cu) for this call
+  bool compact_head = false;   // last self block's row-wise tail on the two head rows only
+  float *hc_x, *hc_g, *hc_dctx;   // compact [2B, D] buffers of that tail
+  bf16 *hc_ctx, *hc_g_bf;
   bf16* wblob;     // its canonical-layout weight blob
   int B, L, Lp, d, K, G, D, m, k, q, v, N, heads, inner, IL, hh, F, FP, HIN;
   long long T;
@@ -340,6 +343,8 @@ Plan make_plan(const LongerDims& d, void* ws) {
   // head
   p.hin = a.take<float>((long long)B * p.HIN); p.z1 = a.take<float>((long long)B * p.hh);
   p.loss_per = a.take<float>(B); p.dz = a.take<float>(B); p.dz1 = a.take<float>((long long)B * p.hh);
+  p.hc_x = a.take<float>(2LL * B * D); p.hc_g = a.take<float>(2LL * B * D); p.hc_dctx = a.take<float>(2LL * B * D);
+  p.hc_ctx = a.take<bf16>(2LL * B * D); p.hc_g_bf = a.take<bf16>(2LL * B * D);
   // backward (query rows)
   p.dO = a.take<float>(Q * D);
   p.dkn = a.take<float>(V * D); p.dKV = a.take<bf16>(V * 2 * D);
@@ -507,7 +512,7 @@ bool use_attn_tc(const AttnArgs& a) {
 
 // One pre-norm attention block over the q query rows (pkg/src/longrec/attention.py:172-212).
 int block_fwd(const Ctx& c, const BlockOff& bo, BlockBufs& b, const float* xq, bool cross, const bf16* Wqkv,
-              const float* bqkv, const bf16* Wo, const bf16* W1, const bf16* W2) {
+              const float* bqkv, const bf16* Wo, const bf16* W1, const bf16* W2, bool compact = false) {
   const Plan& p = c.p;
   cudaStream_t st = c.st;
   const int D = p.D;
@@ -540,10 +545,21 @@ int block_fwd(const Ctx& c, const BlockOff& bo, BlockBufs& b, const float* xq, b
   } else {
     attn_fwd(a, st);
   }
-  TRY(lin_fwd(st, b.ctx, D, Q, Wo, D, D, c.w(bo.b_o), 0, b.x1, nullptr, nullptr, xq, D));
-  layernorm_fwd(rows_plain(b.x1, D, Q), D, c.w(bo.ln2_g), c.w(bo.ln2_b), b.x1n, b.m2, b.r2, st);
-  TRY(lin_fwd(st, b.x1n, D, Q, W1, D, 4 * D, c.w(bo.b1), EPI_GELU | EPI_SAVE_PRE, nullptr, b.gf, b.f1));
-  TRY(lin_fwd(st, b.gf, 4 * D, Q, W2, 4 * D, D, c.w(bo.b2), 0, b.out, nullptr, nullptr, b.x1, D));
+  // compact: only the two rows the head reads leave the last block (model.py:346-362), so its
+  // row-wise tail (W_o + residual, LN2, FFN) runs on [2B, D] gathered rows
+  const long long R = compact ? 2LL * p.B : Q;
+  const bf16* ctx_rows = b.ctx;
+  const float* res_rows = xq;
+  if (compact) {
+    head_rows_gather_bf16(b.ctx, p.hc_ctx, p.B, p.q, p.k + 1, p.k + p.m - 1, D, st);
+    head_rows_gather_f32(xq, p.hc_x, p.B, p.q, p.k + 1, p.k + p.m - 1, D, st);
+    ctx_rows = p.hc_ctx;
+    res_rows = p.hc_x;
+  }
+  TRY(lin_fwd(st, ctx_rows, D, R, Wo, D, D, c.w(bo.b_o), 0, b.x1, nullptr, nullptr, res_rows, D));
+  layernorm_fwd(rows_plain(b.x1, D, R), D, c.w(bo.ln2_g), c.w(bo.ln2_b), b.x1n, b.m2, b.r2, st);
+  TRY(lin_fwd(st, b.x1n, D, R, W1, D, 4 * D, c.w(bo.b1), EPI_GELU | EPI_SAVE_PRE, nullptr, b.gf, b.f1));
+  TRY(lin_fwd(st, b.gf, 4 * D, R, W2, 4 * D, D, c.w(bo.b2), 0, b.out, nullptr, nullptr, b.x1, D));
   return 0;
 }
 
@@ -710,11 +726,12 @@ int forward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs, fl
   const float* xl = p.cb.out;
   for (int i = 0; i < p.N; ++i) {
     TRY(block_fwd(c, o.self_[i], pm.sb[i], xl, false, p.pk.s_wqkv[i], p.pk.s_bqkv[i], p.pk.s_wo[i], p.pk.s_w1[i],
-                  p.pk.s_w2[i]));
+                  p.pk.s_w2[i], p.compact_head && i == p.N - 1));
     xl = p.sb[i].out;
   }
   HeadArgs h{};
   h.x = xl; h.B = p.B; h.q = p.q; h.k = p.k; h.m = p.m; h.D = D; h.d = d; h.hh = p.hh;
+  if (p.compact_head) { h.q = 2; h.k = -1; h.m = 3; }   // rows k+1, k+m−1 → compact rows 0, 1
   h.uid = bt.uid; h.profile = bt.profile; h.label = bt.label;
   h.uid_tab = c.w(o.uid); h.prof_tab = c.w(o.prof);
   h.w1 = c.w(o.head_w1); h.b1 = c.w(o.head_b1); h.w2 = c.w(o.head_w2); h.b2 = c.w(o.head_b2);
@@ -734,29 +751,38 @@ int forward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs, fl
 //   cross: dL/d(merged rows) → p.dmerged, dL/d(global rows) → p.dglob.
 int block_bwd(const Ctx& c, cudaStream_t ss, const BlockOff& bo, const BlockBufs& b, const float* xq, bool cross,
               const bf16* Wqkv, const bf16* Wo, const bf16* W1, const bf16* W2, float* nxt_dx, bf16* nxt_dx_bf,
-              float* nxt_b2) {
+              float* nxt_b2, bool compact = false) {
   const Plan& p = c.p;
   cudaStream_t st = c.st;
   const int D = p.D;
   const long long Q = (long long)p.B * p.q, V = (long long)p.B * p.v;
-  // FFN + residual
+  // FFN + residual (compact: the last block's tail ran on the two head rows per sample)
+  const long long R = compact ? 2LL * p.B : Q;
+  float* dx1_rows = compact ? p.hc_g : b.g_dx1;
+  bf16* dx1_bf_rows = compact ? p.hc_g_bf : b.g_dx1_bf;
   fork_side(st, ss);
-  TRY(lin_dw(ss, b.gf, 4 * D, 4 * D, b.g_dx_bf, D, D, Q, c.g(bo.w2)));
-  TRY(lin_dx(st, b.g_dx_bf, D, Q, W2, D, 4 * D, D, nullptr, 0, b.g_df1, 4 * D, b.f1));
+  TRY(lin_dw(ss, b.gf, 4 * D, 4 * D, b.g_dx_bf, D, D, R, c.g(bo.w2)));
+  TRY(lin_dx(st, b.g_dx_bf, D, R, W2, D, 4 * D, D, nullptr, 0, b.g_df1, 4 * D, b.f1));
   fork_side(st, ss);
-  TRY(lin_dw(ss, b.x1n, D, D, b.g_df1, 4 * D, 4 * D, Q, c.g(bo.w1)));
-  colsum_bf16(b.g_df1, (int)Q, 4 * D, 4 * D, c.g(bo.b1), ss);
-  TRY(lin_dx(st, b.g_df1, 4 * D, Q, W1, 4 * D, D, 4 * D, b.g_dx1n, D, nullptr, 0));
+  TRY(lin_dw(ss, b.x1n, D, D, b.g_df1, 4 * D, 4 * D, R, c.g(bo.w1)));
+  colsum_bf16(b.g_df1, (int)R, 4 * D, 4 * D, c.g(bo.b1), ss);
+  TRY(lin_dx(st, b.g_df1, 4 * D, R, W1, 4 * D, D, 4 * D, b.g_dx1n, D, nullptr, 0));
   {
     LnBwdExtra ex;
-    ex.addend = b.g_dx; ex.out_bf = b.g_dx1_bf; ex.colsum_out = c.g(bo.b_o);
-    layernorm_bwd(rows_plain(b.x1, D, Q), D, c.w(bo.ln2_g), b.m2, b.r2, b.g_dx1n, D, rows_plain_w(b.g_dx1, D, Q), 0,
+    ex.addend = b.g_dx; ex.out_bf = dx1_bf_rows; ex.colsum_out = c.g(bo.b_o);
+    layernorm_bwd(rows_plain(b.x1, D, R), D, c.w(bo.ln2_g), b.m2, b.r2, b.g_dx1n, D, rows_plain_w(dx1_rows, D, R), 0,
                   nullptr, c.g(bo.ln2_g), c.g(bo.ln2_b), st, ex);
   }
   // output projection
   fork_side(st, ss);
-  TRY(lin_dw(ss, b.ctx, D, D, b.g_dx1_bf, D, D, Q, c.g(bo.w_o)));
-  TRY(lin_dx(st, b.g_dx1_bf, D, Q, Wo, D, D, D, b.g_dctx, D, nullptr, 0));
+  TRY(lin_dw(ss, compact ? p.hc_ctx : b.ctx, D, D, dx1_bf_rows, D, D, R, c.g(bo.w_o)));
+  TRY(lin_dx(st, dx1_bf_rows, D, R, Wo, D, D, D, compact ? p.hc_dctx : b.g_dctx, D, nullptr, 0));
+  if (compact) {   // back to full [B·q, D] rows (zero elsewhere) for the attention and LN1 backward
+    TRY((int)cudaMemsetAsync(b.g_dctx, 0, Q * D * 4, st));
+    head_rows_scatter_f32(p.hc_dctx, b.g_dctx, p.B, p.q, p.k + 1, p.k + p.m - 1, D, st);
+    TRY((int)cudaMemsetAsync(b.g_dx1, 0, Q * D * 4, st));
+    head_rows_scatter_f32(p.hc_g, b.g_dx1, p.B, p.q, p.k + 1, p.k + p.m - 1, D, st);
+  }
   // attention
   AttnArgs a{};
   a.nq = p.q; a.D = D; a.heads = p.heads; a.k = p.k; a.G = p.G; a.npg = p.npg; a.B = p.B;
@@ -849,6 +875,7 @@ int backward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs) {
   HeadArgs h{};
   h.x = p.N ? p.sb[p.N - 1].out : p.cb.out;
   h.B = p.B; h.q = p.q; h.k = p.k; h.m = p.m; h.D = D; h.d = d; h.hh = p.hh;
+  if (p.compact_head) { h.q = 2; h.k = -1; h.m = 3; }
   h.uid = bt.uid; h.profile = bt.profile; h.label = bt.label;
   h.uid_tab = c.w(o.uid); h.prof_tab = c.w(o.prof);
   h.w1 = c.w(o.head_w1); h.b1 = c.w(o.head_b1); h.w2 = c.w(o.head_w2); h.b2 = c.w(o.head_b2);
@@ -857,12 +884,12 @@ int backward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs) {
   h.g_uid = c.g(o.uid); h.g_prof = c.g(o.prof);
   head_bwd(h, st);
   fork_side(st, ss);
-  colsum_f32(last.g_dx, (int)Q, D, D, c.g(p.N ? o.self_[p.N - 1].b2 : o.cross.b2), ss);
+  colsum_f32(last.g_dx, (int)(p.compact_head ? 2LL * p.B : Q), D, D, c.g(p.N ? o.self_[p.N - 1].b2 : o.cross.b2), ss);
   for (int i = p.N - 1; i >= 0; --i) {
     const float* xin = i == 0 ? p.cb.out : p.sb[i - 1].out;
     const BlockBufs& nb = i == 0 ? p.cb : p.sb[i - 1];
     TRY(block_bwd(c, ss, o.self_[i], p.sb[i], xin, false, p.pk.s_wqkv[i], p.pk.s_wo[i], p.pk.s_w1[i], p.pk.s_w2[i],
-                  nb.g_dx, nb.g_dx_bf, c.g(i == 0 ? o.cross.b2 : o.self_[i - 1].b2)));
+                  nb.g_dx, nb.g_dx_bf, c.g(i == 0 ? o.cross.b2 : o.self_[i - 1].b2), p.compact_head && i == p.N - 1));
   }
   TRY(block_bwd(c, ss, o.cross, p.cb, p.O, true, p.pk.c_wq, p.pk.c_wo, p.pk.c_w1, p.pk.c_w2, nullptr, nullptr,
                 nullptr));
@@ -1177,12 +1204,20 @@ extern "C" int longer_workspace_bytes(const LongerDims* dims, size_t* bytes) {
   return 0;
 }
 
+// training / inference entry points run the last self block's tail on the two head rows
+// (LONGER_HEAD_ROWS=0: all rows); the serving cache build keeps every row (it caches them)
+static bool compact_head_ok(const Plan& p) {
+  const char* e = std::getenv("LONGER_HEAD_ROWS");
+  return p.N >= 1 && p.m >= 3 && !(e && e[0] == '0');
+}
+
 extern "C" int longer_forward(const LongerDims* dims, const float* params, const LongerBatch* batch, void* ws,
                               size_t ws_bytes, float* probs, void* stream) {
   static Plan p;   // large struct; one driving thread per device (see longer.h)
   int rc = check_call(dims, ws_bytes, &p, ws);
   if (rc) return rc;
   p.fused_fe = use_fused(p);
+  p.compact_head = compact_head_ok(p);
   Ctx c{p, params, nullptr, (cudaStream_t)stream};
   return forward(c, p, *batch, probs, nullptr, 0);
 }
@@ -1194,6 +1229,7 @@ extern "C" int longer_forward_backward(const LongerDims* dims, const float* para
   int rc = check_call(dims, ws_bytes, &p, ws);
   p.fused_fe = use_fused(p);
   if (rc) return rc;
+  p.compact_head = compact_head_ok(p);
   Ctx c{p, params, grads, (cudaStream_t)stream};
   rc = forward(c, p, *batch, probs, loss, 1);
   if (rc) return rc;
@@ -1207,6 +1243,7 @@ extern "C" int longer_backward(const LongerDims* dims, const float* params, cons
   if (rc) return rc;
   if (!batch || !probs || !dprobs || !grads) return fail(LONGER_EDIM, "null argument");
   p.fused_fe = use_fused(p);
+  p.compact_head = compact_head_ok(p);
   Ctx c{p, params, grads, (cudaStream_t)stream};
   dz_from_dprobs(probs, dprobs, p.B, p.dz, c.st);     // dL/dz = dL/dp · p(1 − p)
   return backward(c, p, *batch, const_cast<float*>(probs));

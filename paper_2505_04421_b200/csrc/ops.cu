@@ -1619,4 +1619,32 @@ void adam_step(float* p, const float* g, float* m, float* v, long long n, float 
   launch(adam_kernel, 148 * 8, 256, 0, st, p, g, m, v, n, lr, c1, c2);
 }
 
+
+// ============================================================== head rows of the last block
+// The head reads only rows k+1 (CLS) and k+m−1 (target) of the last block's output
+// (pkg/src/longrec/model.py:346-362), so that block's row-wise tail runs on those two rows per
+// sample: compact row 2b + 0 ↔ full row b·q + k+1, compact row 2b + 1 ↔ full row b·q + k+m−1.
+template <typename T, bool GATHER>
+__global__ void head_rows_kernel(const T* __restrict__ src, T* __restrict__ dst, int B, int q, int r0, int r1,
+                                 int W) {
+  pdl_trigger();
+  pdl_wait();
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)2 * B * W) return;
+  const int c = (int)(i % W), r = (int)(i / W);
+  const long long full = (long long)(r >> 1) * q + ((r & 1) ? r1 : r0);
+  if (GATHER) dst[(long long)r * W + c] = src[full * W + c];
+  else dst[full * W + c] = src[(long long)r * W + c];
+}
+
+void head_rows_gather_f32(const float* full, float* compact, int B, int q, int r0, int r1, int W, cudaStream_t st) {
+  launch(head_rows_kernel<float, true>, cdiv((long long)2 * B * W, 256), 256, 0, st, full, compact, B, q, r0, r1, W);
+}
+void head_rows_gather_bf16(const bf16* full, bf16* compact, int B, int q, int r0, int r1, int W, cudaStream_t st) {
+  launch(head_rows_kernel<bf16, true>, cdiv((long long)2 * B * W, 256), 256, 0, st, full, compact, B, q, r0, r1, W);
+}
+void head_rows_scatter_f32(const float* compact, float* full, int B, int q, int r0, int r1, int W, cudaStream_t st) {
+  launch(head_rows_kernel<float, false>, cdiv((long long)2 * B * W, 256), 256, 0, st, compact, full, B, q, r0, r1, W);
+}
+
 }  // namespace longer

@@ -167,6 +167,11 @@ void head_fwd(const HeadArgs& a, int with_loss, cudaStream_t st);
 // dz[b] = dprobs[b] · p(1 − p): the head's logit gradient for an arbitrary upstream dL/dp
 void dz_from_dprobs(const float* probs, const float* dprobs, int B, float* dz, cudaStream_t st);
 void head_bwd(const HeadArgs& a, cudaStream_t st);
+// the two head rows of each sample (r0 = k+1, r1 = k+m−1) between a full [B·q, W] buffer and a
+// compact [2B, W] one
+void head_rows_gather_f32(const float* full, float* compact, int B, int q, int r0, int r1, int W, cudaStream_t st);
+void head_rows_gather_bf16(const bf16* full, bf16* compact, int B, int q, int r0, int r1, int W, cudaStream_t st);
+void head_rows_scatter_f32(const float* compact, float* full, int B, int q, int r0, int r1, int W, cudaStream_t st);
 
 // ---------------------------------------------------------------- weights
 // Packs fp32 master parameters into the bf16 / fp32 operand layouts the kernels use.

@@ -148,6 +148,28 @@ def test_attention_variants_match_oracle(pack, tma, monkeypatch):
     assert_grads_close(grads, G, f"pack={pack} tma={tma}")
 
 
+@pytest.mark.parametrize("head_rows", ["1", "0"])
+def test_last_block_head_rows_match_oracle(head_rows, monkeypatch):
+    """The last self block's row-wise tail on the two head rows only (default) and on all rows
+    (LONGER_HEAD_ROWS=0) both match the oracle, forward and backward, at N = 1 and N = 2."""
+    monkeypatch.setenv("LONGER_HEAD_ROWS", head_rows)
+    for kw in (dict(C2, L=512), dict(C2, L=512, N=1, m=4)):
+        cfg = ModelConfig(**kw).validate()
+        from paper_2505_04421_b200.params import init_params
+        P = init_params(cfg, seed=0)
+        rng = np.random.default_rng(8)
+        P = {n: a + 0.02 * rng.standard_normal(a.shape) for n, a in P.items()}
+        batch = synthetic_batch(cfg, 5, seed=17, min_events=1)
+        p_ref, loss_ref, G = O.forward_backward(P, cfg, batch.as_dict())
+        model = _model(cfg, P)
+        p, loss, grads = _run(model, batch)
+        assert np.max(np.abs(p - p_ref)) <= 5e-3
+        assert abs(loss - loss_ref) <= loss_tol(p_ref, batch.label)
+        assert_grads_close(grads, G, f"head_rows={head_rows} {kw}")
+        pf = model.forward(batch).cpu().numpy().astype(np.float64)
+        assert np.max(np.abs(pf - p_ref)) <= 5e-3
+
+
 @pytest.mark.parametrize("bias", [20.0, 40.0, -40.0, -25.0])
 def test_saturated_logits_follow_the_reference_clamp(bias):
     """p = sigmoid(z) saturates in fp32 long before the reference's 1e-12 clamp does; the loss and
