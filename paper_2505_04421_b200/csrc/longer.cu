@@ -778,9 +778,7 @@ int block_bwd(const Ctx& c, cudaStream_t ss, const BlockOff& bo, const BlockBufs
   TRY(lin_dw(ss, compact ? p.hc_ctx : b.ctx, D, D, dx1_bf_rows, D, D, R, c.g(bo.w_o)));
   TRY(lin_dx(st, dx1_bf_rows, D, R, Wo, D, D, D, compact ? p.hc_dctx : b.g_dctx, D, nullptr, 0));
   if (compact) {   // back to full [B·q, D] rows (zero elsewhere) for the attention and LN1 backward
-    TRY((int)cudaMemsetAsync(b.g_dctx, 0, Q * D * 4, st));
     head_rows_scatter_f32(p.hc_dctx, b.g_dctx, p.B, p.q, p.k + 1, p.k + p.m - 1, D, st);
-    TRY((int)cudaMemsetAsync(b.g_dx1, 0, Q * D * 4, st));
     head_rows_scatter_f32(p.hc_g, b.g_dx1, p.B, p.q, p.k + 1, p.k + p.m - 1, D, st);
   }
   // attention

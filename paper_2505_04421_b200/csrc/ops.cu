@@ -1643,8 +1643,30 @@ void head_rows_gather_f32(const float* full, float* compact, int B, int q, int r
 void head_rows_gather_bf16(const bf16* full, bf16* compact, int B, int q, int r0, int r1, int W, cudaStream_t st) {
   launch(head_rows_kernel<bf16, true>, cdiv((long long)2 * B * W, 256), 256, 0, st, full, compact, B, q, r0, r1, W);
 }
+// full[B·q, W] = the compact rows at their places, zero elsewhere (one pass, no separate memset)
+__global__ void head_rows_expand_kernel(const float* __restrict__ compact, float* __restrict__ full, int B, int q,
+                                        int r0, int r1, int W) {
+  pdl_trigger();
+  pdl_wait();
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)B * q * W / 4) return;
+  const long long e = i * 4;
+  const int c = (int)(e % W);
+  const long long row = e / W;
+  const int b = (int)(row / q), j = (int)(row % q);
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (j == r0 || j == r1)
+    v = *reinterpret_cast<const float4*>(compact + ((long long)2 * b + (j == r1 ? 1 : 0)) * W + c);
+  *reinterpret_cast<float4*>(full + e) = v;
+}
+
 void head_rows_scatter_f32(const float* compact, float* full, int B, int q, int r0, int r1, int W, cudaStream_t st) {
-  launch(head_rows_kernel<float, false>, cdiv((long long)2 * B * W, 256), 256, 0, st, compact, full, B, q, r0, r1, W);
+  if (W % 4 == 0) {
+    launch(head_rows_expand_kernel, cdiv((long long)B * q * W / 4, 256), 256, 0, st, compact, full, B, q, r0, r1, W);
+  } else {
+    cudaMemsetAsync(full, 0, (size_t)B * q * W * 4, st);
+    launch(head_rows_kernel<float, false>, cdiv((long long)2 * B * W, 256), 256, 0, st, compact, full, B, q, r0, r1, W);
+  }
 }
 
 }  // namespace longer

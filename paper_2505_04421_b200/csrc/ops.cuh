@@ -168,7 +168,7 @@ void head_fwd(const HeadArgs& a, int with_loss, cudaStream_t st);
 void dz_from_dprobs(const float* probs, const float* dprobs, int B, float* dz, cudaStream_t st);
 void head_bwd(const HeadArgs& a, cudaStream_t st);
 // the two head rows of each sample (r0 = k+1, r1 = k+m−1) between a full [B·q, W] buffer and a
-// compact [2B, W] one
+// compact [2B, W] one (the scatter writes every row of `full`: zero outside the head rows)
 void head_rows_gather_f32(const float* full, float* compact, int B, int q, int r0, int r1, int W, cudaStream_t st);
 void head_rows_gather_bf16(const bf16* full, bf16* compact, int B, int q, int r0, int r1, int W, cudaStream_t st);
 void head_rows_scatter_f32(const float* compact, float* full, int B, int q, int r0, int r1, int W, cudaStream_t st);
