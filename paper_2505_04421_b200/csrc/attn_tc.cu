@@ -1,15 +1,17 @@
-// attn_tc.cu — cross-layer attention on the tensor cores (tcgen05), one CTA per (sample, head).
+// attn_tc.cu — attention of the cross and self layers on the tensor cores (tcgen05), one CTA per
+// (sample, head) — or per three samples in the self-layer backward.
 //
 // _multi_head_attention + masked_softmax (pkg/src/longrec/attention.py:153-169,
-// pkg/src/longrec/tensors.py:323-351) for the first (cross) layer: the q = k + m query rows
-// (≤ 128, zero-padded to the UMMA M = 128 tile) against the v = G + m key rows, streamed in
-// chunks of 128 keys.  The structured visibility mask (VisRule) is evaluated in registers.
+// pkg/src/longrec/tensors.py:323-351): the q = k + m query rows (≤ 128, zero-padded to the UMMA
+// M = 128 tile) against the key rows (cross: v = G + m; self: the q rows themselves), streamed in
+// chunks of 128 keys by 3-D TMA.  The structured visibility mask (VisRule) is one key interval per
+// query row, evaluated in registers.
 //
-// Forward: two passes over the key chunks — pass 1 finds the exact row max / sum from S = QKᵀ in
-// TMEM, pass 2 writes normalised P (bf16) to smem and accumulates O += P·V in TMEM — so no
-// accumulator rescaling is needed; LSE and an fp32 copy of O are kept for the backward.
-// Backward (per chunk): S and dP = dO·Vᵀ in TMEM → dS = P ⊙ (dP − D) in smem →
-// dV = Pᵀ·dO, dK = dSᵀ·Q (thread = key row on readout), dQ += dS·K accumulated in TMEM.
+// Forward: one pass over the key chunks with a running max / sum per row and O += P̃·V in TMEM
+// (rescaled in TMEM only when the max grows by more than kRescale); LSE and an fp32 copy of O are
+// kept for the backward.
+// Backward: pass 1 D_i = Σ_j P·dP; pass 2 per chunk S and dP = dO·Vᵀ in TMEM → dS = P ⊙ (dP − D) in
+// smem → dV = Pᵀ·dO, dK = dSᵀ·Q (thread = key row on readout), dQ += dS·K accumulated in TMEM.
 #include "fe_common.cuh"
 #include "ops.cuh"
 #include "tma.cuh"
