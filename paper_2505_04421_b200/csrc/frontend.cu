@@ -5,8 +5,8 @@
 // grouped_attention (pkg/src/longrec/tensors.py:406-444), for 128-token tiles; and the backward of
 // the token MLP + featuriser (tensors.py bw closures of linear/gelu/gather_rows).
 //
-// CTA = warp 0 (TMEM owner + single-thread MMA issuer) + 4 worker warps (thread = token row =
-// TMEM lane).  Per stage: workers write the A tile → mbarrier → one thread issues tcgen05.mma
+// CTA = warp 0 (TMEM owner + single-thread MMA issuer) + 4 worker warps (fe_fwd, two CTAs per SM)
+// or 8 (fe_mlp_bwd, two per lane quadrant); thread = token row = TMEM lane.  Per stage: workers write the A tile → mbarrier → one thread issues tcgen05.mma
 // (M = 128) against smem-resident weights → tcgen05.commit → workers read the fp32 accumulator
 // from TMEM and apply bias / GELU / LN / group attention in registers.
 #include "frontend.cuh"

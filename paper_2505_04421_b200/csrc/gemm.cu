@@ -1,8 +1,8 @@
 // gemm.cu — generic tcgen05 GEMM with fused epilogues. See gemm.cuh for the contract.
 //
-// CTA = 1 TMA warp + 1 MMA warp (also owns TMEM) + 8 epilogue warps.  The smem ring depth is a
-// template parameter chosen from the K extent (1, 2 or 4 stages) so that the short-K GEMMs of the
-// token pipeline keep 2-3 CTAs per SM and overlap one CTA's epilogue with another's MMA.
+// CTA = 1 TMA warp + 1 MMA warp (also owns TMEM) + 8 epilogue warps, persistent over work items
+// with a double-buffered TMEM accumulator.  The smem ring depth is a template parameter chosen from
+// the K extent (1, 2 or 4 stages); the epilogue stores go through a per-warp smem transpose.
 #include "gemm.cuh"
 #include "sm100.cuh"
 #include "tma.cuh"

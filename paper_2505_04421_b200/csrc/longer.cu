@@ -1,10 +1,12 @@
 // longer.cu — C ABI (include/longer.h) and the native step orchestrator.
 //
-// One call runs a whole batch through the LONGER encoder on one stream:
-//   pack weights → featurise tokens → token MLP → [InnerTrans] → global tokens → cross block →
-//   N self blocks → head + BCE  (forward, pkg/src/longrec/model.py:307-363)
-// and, for training, the exact reverse sweep (pkg/src/longrec/tensors.py:141-175).
-// Dense contractions go through the tcgen05 GEMM (gemm.cu), everything else through ops.cu.
+// One call runs a whole batch through the LONGER encoder on the caller's stream (plus a side
+// stream for work off the critical chain, joined before return):
+//   fused front-end (featuriser → token MLP → InnerTrans, frontend.cu) ‖ global tokens → cross
+//   block → N self blocks → head + BCE  (forward, pkg/src/longrec/model.py:307-363)
+// and, for training, the exact reverse sweep (pkg/src/longrec/tensors.py:141-175) with the weight
+// gradients on the side stream.  Row-level contractions go through the tcgen05 GEMM (gemm.cu),
+// attention through attn_tc.cu, the rest through ops.cu.
 #include <cuda_runtime.h>
 
 #include <cstdio>
