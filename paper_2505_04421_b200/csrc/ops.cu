@@ -1315,7 +1315,7 @@ void scatter_query_rows(const float* dO, int q, const int32_t* qg, int B, int G,
 // Head of forward_tensor (pkg/src/longrec/model.py:346-362): [t, c, t⊙c, t⊙t, u_d] → GELU MLP →
 // sigmoid; BCE with the 1e-12 clamp (tensors.py:551-571).  One warp per sample: lanes own hidden
 // units (coalesced W1 rows, the input row broadcast from shared memory).
-constexpr int kHeadWarps = 8;
+constexpr int kHeadWarps = 4;
 
 // W1 [HIN, hh] staged in shared memory with row stride hh+1: conflict-free both for lanes over
 // hidden units (forward) and lanes over inputs (backward).
