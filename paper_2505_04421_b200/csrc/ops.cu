@@ -712,15 +712,45 @@ __global__ void move_rows_kernel(const float* src, int batch, int src_rows, int 
   float* d = dst + ((long long)b * dst_rows + dst_off + j) * W + c;
   if (ADD) *d += v; else *d = v;
 }
+// 16-byte version (W % 4 == 0, 16-byte aligned bases)
+template <int ADD>
+__global__ void move_rows4_kernel(const float4* src, int batch, int src_rows, int src_off, int n, float4* dst,
+                                  int dst_rows, int dst_off, int W4) {
+  pdl_trigger();
+  pdl_wait();
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)batch * n * W4) return;
+  const int c = (int)(i % W4);
+  const long long r = i / W4;
+  const int b = (int)(r / n), j = (int)(r % n);
+  const float4 v = src[((long long)b * src_rows + src_off + j) * W4 + c];
+  float4* d = dst + ((long long)b * dst_rows + dst_off + j) * W4 + c;
+  if (ADD) {
+    float4 o = *d;
+    o.x += v.x; o.y += v.y; o.z += v.z; o.w += v.w;
+    *d = o;
+  } else {
+    *d = v;
+  }
+}
+template <int ADD>
+static void move_rows(const float* src, int batch, int src_rows, int src_off, int n, float* dst, int dst_rows,
+                      int dst_off, int W, cudaStream_t st) {
+  const long long tot = (long long)batch * n * W;
+  if (!tot) return;
+  if (W % 4 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0)
+    launch(move_rows4_kernel<ADD>, cdiv(tot / 4, 256), 256, 0, st, reinterpret_cast<const float4*>(src), batch,
+           src_rows, src_off, n, reinterpret_cast<float4*>(dst), dst_rows, dst_off, W / 4);
+  else
+    launch(move_rows_kernel<ADD>, cdiv(tot, 256), 256, 0, st, src, batch, src_rows, src_off, n, dst, dst_rows, dst_off, W);
+}
 void gather_rows_f32(const float* src, int batch, int src_rows, int src_off, int n, float* dst, int dst_rows,
                      int dst_off, int W, cudaStream_t st) {
-  const long long tot = (long long)batch * n * W;
-  if (tot) launch(move_rows_kernel<0>, cdiv(tot, 256), 256, 0, st, src, batch, src_rows, src_off, n, dst, dst_rows, dst_off, W);
+  move_rows<0>(src, batch, src_rows, src_off, n, dst, dst_rows, dst_off, W, st);
 }
 void add_rows_f32(const float* src, int batch, int src_rows, int src_off, int n, float* dst, int dst_rows,
                   int dst_off, int W, cudaStream_t st) {
-  const long long tot = (long long)batch * n * W;
-  if (tot) launch(move_rows_kernel<1>, cdiv(tot, 256), 256, 0, st, src, batch, src_rows, src_off, n, dst, dst_rows, dst_off, W);
+  move_rows<1>(src, batch, src_rows, src_off, n, dst, dst_rows, dst_off, W, st);
 }
 
 // ============================================================== grouped attention (InnerTrans)
