@@ -1681,11 +1681,20 @@ __global__ void head_rows_kernel(const T* __restrict__ src, T* __restrict__ dst,
   else dst[full * W + c] = src[(long long)r * W + c];
 }
 
+// gathers move 16-byte vectors when the row width allows (W·sizeof(T) % 16 == 0, aligned bases)
 void head_rows_gather_f32(const float* full, float* compact, int B, int q, int r0, int r1, int W, cudaStream_t st) {
-  launch(head_rows_kernel<float, true>, cdiv((long long)2 * B * W, 256), 256, 0, st, full, compact, B, q, r0, r1, W);
+  if (W % 4 == 0 && (reinterpret_cast<uintptr_t>(full) & 15) == 0 && (reinterpret_cast<uintptr_t>(compact) & 15) == 0)
+    launch(head_rows_kernel<uint4, true>, cdiv((long long)2 * B * W / 4, 256), 256, 0, st,
+           reinterpret_cast<const uint4*>(full), reinterpret_cast<uint4*>(compact), B, q, r0, r1, W / 4);
+  else
+    launch(head_rows_kernel<float, true>, cdiv((long long)2 * B * W, 256), 256, 0, st, full, compact, B, q, r0, r1, W);
 }
 void head_rows_gather_bf16(const bf16* full, bf16* compact, int B, int q, int r0, int r1, int W, cudaStream_t st) {
-  launch(head_rows_kernel<bf16, true>, cdiv((long long)2 * B * W, 256), 256, 0, st, full, compact, B, q, r0, r1, W);
+  if (W % 8 == 0 && (reinterpret_cast<uintptr_t>(full) & 15) == 0 && (reinterpret_cast<uintptr_t>(compact) & 15) == 0)
+    launch(head_rows_kernel<uint4, true>, cdiv((long long)2 * B * W / 8, 256), 256, 0, st,
+           reinterpret_cast<const uint4*>(full), reinterpret_cast<uint4*>(compact), B, q, r0, r1, W / 8);
+  else
+    launch(head_rows_kernel<bf16, true>, cdiv((long long)2 * B * W, 256), 256, 0, st, full, compact, B, q, r0, r1, W);
 }
 // full[B·q, W] = the compact rows at their places, zero elsewhere (one pass, no separate memset)
 __global__ void head_rows_expand_kernel(const float* __restrict__ compact, float* __restrict__ full, int B, int q,
