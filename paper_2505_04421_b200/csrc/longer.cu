@@ -739,7 +739,12 @@ int forward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs, fl
   h.w1 = c.w(o.head_w1); h.b1 = c.w(o.head_b1); h.w2 = c.w(o.head_w2); h.b2 = c.w(o.head_b2);
   h.hin = p.hin; h.z1 = p.z1; h.probs = probs;
   h.loss_per = with_loss ? p.loss_per : nullptr; h.dz = p.dz; h.loss = loss;
-  head_fwd(h, with_loss, st);
+  head_fwd(h, 0, st);
+  if (with_loss) {          // the scalar loss feeds nothing on the device: off the critical chain
+    fork_side(st, ss);
+    loss_mean(p.loss_per, p.B, loss, ss);
+    if (!c.G) join_side(st, ss);   // forward-only call: joined before return
+  }
   if (p.fused_fe) probe(PH_FWD_ROWS, 1, st);
   TRY((int)cudaGetLastError());
   return 0;

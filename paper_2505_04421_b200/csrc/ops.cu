@@ -1487,6 +1487,10 @@ int head_smem_w1(const HeadArgs& a) { return 4 * (4 * a.D + 2 * a.d) * (a.hh + 1
 constexpr int kHeadSmemMax = 200 * 1024;
 }  // namespace
 
+void loss_mean(const float* loss_per, int B, float* loss, cudaStream_t st) {
+  launch(loss_mean_kernel, 1, 256, 0, st, loss_per, B, loss);
+}
+
 void head_fwd(const HeadArgs& a, int with_loss, cudaStream_t st) {
   const int smem = 4 * kHeadWarps * (4 * a.D + 2 * a.d);
   const bool stage = smem + head_smem_w1(a) <= kHeadSmemMax;
@@ -1497,7 +1501,7 @@ void head_fwd(const HeadArgs& a, int with_loss, cudaStream_t st) {
   } else {
     launch(head_fwd_kernel<false>, cdiv(a.B, kHeadWarps), 32 * kHeadWarps, smem, st, a);
   }
-  if (with_loss) launch(loss_mean_kernel, 1, 256, 0, st, a.loss_per, a.B, a.loss);
+  if (with_loss) loss_mean(a.loss_per, a.B, a.loss, st);
 }
 
 // Head backward, one warp per sample: dz1 = dz·w2⊙GELU'(z1) (lanes = hidden units), then

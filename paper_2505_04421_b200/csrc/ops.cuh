@@ -164,6 +164,7 @@ struct HeadArgs {
   float* dz1;          // [B, hh] scratch
 };
 void head_fwd(const HeadArgs& a, int with_loss, cudaStream_t st);
+void loss_mean(const float* loss_per, int B, float* loss, cudaStream_t st);   // batch-mean BCE
 // dz[b] = dprobs[b] · p(1 − p): the head's logit gradient for an arbitrary upstream dL/dp
 void dz_from_dprobs(const float* probs, const float* dprobs, int B, float* dz, cudaStream_t st);
 void head_bwd(const HeadArgs& a, cudaStream_t st);
