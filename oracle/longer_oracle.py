@@ -536,3 +536,18 @@ def forward_backward(P, cfg, batch):
     p, cache = forward(P, cfg, batch)
     loss = bce_mean(p, batch["label"])
     return p, loss, backward(P, cfg, batch, cache)
+
+
+# ----------------------------------------------------------------- optimizer
+def adam_step(params, grads, m, v, t, lr):
+    """Adam.step (pkg/src/longrec/model.py:467-482): beta1 = 0.9, beta2 = 0.999, eps = 1e-8, bias
+    corrections with the step counter t (>= 1).  Arrays are updated in place (float64)."""
+    b1, b2, eps = 0.9, 0.999, 1e-8
+    c1 = 1.0 - b1 ** t
+    c2 = 1.0 - b2 ** t
+    m *= b1
+    m += (1 - b1) * grads
+    v *= b2
+    v += (1 - b2) * grads * grads
+    params -= lr * (m / c1) / (np.sqrt(v / c2) + eps)
+

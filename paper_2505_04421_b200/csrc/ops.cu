@@ -1662,9 +1662,38 @@ __global__ void adam_kernel(float* p, const float* g, float* m, float* v, long l
   }
 }
 
+// same per-element arithmetic, four elements per 16-byte access (aligned buffers, n % 4 == 0)
+__global__ void adam4_kernel(float4* p, const float4* g, float4* m, float4* v, long long n4, float lr, float c1,
+                             float c2) {
+  pdl_trigger();
+  pdl_wait();
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    const float4 g4 = g[i];
+    float4 m4 = m[i], v4 = v[i], p4 = p[i];
+    float* pm = &m4.x; float* pv = &v4.x; float* pp = &p4.x;
+    const float* pg = &g4.x;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float gi = pg[u];
+      const float mi = 0.9f * pm[u] + 0.1f * gi;
+      const float vi = 0.999f * pv[u] + 0.001f * gi * gi;
+      pm[u] = mi;
+      pv[u] = vi;
+      pp[u] -= lr * (mi / c1) / (sqrtf(vi / c2) + 1e-8f);
+    }
+    m[i] = m4; v[i] = v4; p[i] = p4;
+  }
+}
+
 void adam_step(float* p, const float* g, float* m, float* v, long long n, float lr, int t, cudaStream_t st) {
   const float c1 = (float)(1.0 - pow(0.9, t)), c2 = (float)(1.0 - pow(0.999, t));
-  launch(adam_kernel, 148 * 8, 256, 0, st, p, g, m, v, n, lr, c1, c2);
+  const bool vec = n % 4 == 0 && ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(g) |
+                                   reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(v)) & 15) == 0;
+  if (vec)
+    launch(adam4_kernel, 148 * 4, 256, 0, st, reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
+           reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), n / 4, lr, c1, c2);
+  else
+    launch(adam_kernel, 148 * 8, 256, 0, st, p, g, m, v, n, lr, c1, c2);
 }
 
 

@@ -7,7 +7,8 @@
   pkg/tests/test_attention.py:216-250); the candidate does reach p (test_model.py:100-109);
 * samples are independent: p of a sample does not depend on the rest of the batch (bit-identical);
 * very short histories (every sequence query a pad query → fully masked attention rows, whose
-  context is exactly 0, pkg/tests/test_tensors.py:110-112) match the oracle.
+  context is exactly 0, pkg/tests/test_tensors.py:110-112) match the oracle;
+* the fused Adam step follows Adam.step (pkg/src/longrec/model.py:467-482).
 """
 import numpy as np
 import pytest
@@ -104,3 +105,26 @@ def test_short_histories_match_oracle(n_events):
     from test_parity_gpu import assert_grads_close, loss_tol
     assert abs(loss - loss_ref) <= loss_tol(p_ref, b.label)
     assert_grads_close(grads, G, f"n_events={n_events}")
+
+
+def test_adam_matches_reference_update():
+    """longer_adam_step against Adam.step of the reference (model.py:467-482, restated as
+    oracle.adam_step) over several steps with changing gradients; fp32 state vs float64."""
+    import torch
+    from paper_2505_04421_b200.model import Adam
+    cfg = ModelConfig(**dict(C2, L=256)).validate()
+    model = _model(cfg)
+    rng = np.random.default_rng(2)
+    n = model.flat.numel()
+    p_ref = rng.standard_normal(n) * 0.1
+    m_ref, v_ref = np.zeros(n), np.zeros(n)
+    model.flat.copy_(torch.from_numpy(p_ref.astype(np.float32)))
+    p_ref = model.flat.cpu().numpy().astype(np.float64)          # start from the fp32 values
+    opt = Adam(model, 1e-3)
+    for t in range(1, 6):
+        g = rng.standard_normal(n) * (0.01 * t)
+        model.grad_flat.copy_(torch.from_numpy(g.astype(np.float32)))
+        opt.step()
+        O.adam_step(p_ref, g.astype(np.float32).astype(np.float64), m_ref, v_ref, t, 1e-3)
+    got = model.flat.cpu().numpy().astype(np.float64)
+    np.testing.assert_allclose(got, p_ref, rtol=0, atol=2e-6)
