@@ -49,3 +49,29 @@ def test_time_bucket_known_answers():
     # pkg/tests/test_inputs.py:93-106 and SPEC.md: 3601 s → 12, 0 → 0, 2^40 → 31
     assert O.time_bucket(np.array([3601, 0, 2 ** 40, 1, 2, 3, 4]), 32).tolist() == [12, 0, 31, 1, 2, 2, 3]
     assert O.time_bucket(np.array([2 ** 40]), 8).tolist() == [7]
+
+
+REF_SRC = "/root/reference/pkg/src"
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference package not present")
+def test_oracle_adam_matches_reference_adam():
+    """oracle.adam_step against longrec's own Adam.step (pkg/src/longrec/model.py:453-482)."""
+    import sys
+    sys.path.insert(0, REF_SRC)
+    try:
+        from longrec.model import Adam as RefAdam
+        from longrec.tensors import Tensor
+    finally:
+        sys.path.remove(REF_SRC)
+    rng = np.random.default_rng(1)
+    w = Tensor(rng.standard_normal((7, 5)))
+    ref = RefAdam([("w", w)], lr=3e-3)
+    p = w.data.copy()
+    m, v = np.zeros_like(p), np.zeros_like(p)
+    for t in range(1, 5):
+        g = rng.standard_normal(p.shape)
+        w.grad = g.copy()
+        ref.step()
+        O.adam_step(p, g, m, v, t, 3e-3)
+        np.testing.assert_allclose(p, w.data, rtol=0, atol=1e-15)
