@@ -506,6 +506,148 @@ __global__ void __launch_bounds__(256) ln_bwd128_kernel(RowMap x, const float* _
   }
 }
 
+// Pipelined lean LN backward (W = 128, bf16 dy, no extras): each warp streams its rows through an
+// S-stage ring of shared memory with per-lane cp.async (16 B of x, 8 B of dy per lane and row, the
+// row statistics by lanes 0..R-1), so S-1 groups of R rows stay in flight while the current group
+// is reduced — deep memory-level parallelism without holding the rows in registers.
+__device__ __forceinline__ void cpa16(void* s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(s)), "l"(g));
+}
+__device__ __forceinline__ void cpa8(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(s)), "l"(g));
+}
+__device__ __forceinline__ void cpa4(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(s)), "l"(g));
+}
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int R, int S>
+struct LnAsync {
+  static constexpr int STAGE = R * 768 + 32 * 4;   // x rows fp32 | dy rows bf16 | mean[R], rstd[R]
+  static constexpr int SMEM = 8 * S * STAGE;
+};
+
+template <int R, int S>
+__global__ void __launch_bounds__(256) ln_bwd128_async_kernel(RowMap x, const float* __restrict__ g,
+                                                              const float* __restrict__ mean,
+                                                              const float* __restrict__ rstd,
+                                                              const bf16* __restrict__ dy, int ldy, RowMapW out,
+                                                              float* dgain, float* dbias) {
+  pdl_trigger();
+  pdl_wait();
+  using L = LnAsync<R, S>;
+  extern __shared__ __align__(16) uint8_t lsm[];
+  __shared__ float sg[8][128], sb[8][128];
+  const int wid = threadIdx.x / 32, lane = threadIdx.x & 31;
+  uint8_t* wbase = lsm + wid * S * L::STAGE;
+  const int rows = x.rows();
+  const int per = x.na + x.nb;
+  const float4 gv = __ldg(reinterpret_cast<const float4*>(g) + lane);
+  float pg[4] = {0.f, 0.f, 0.f, 0.f}, pb[4] = {0.f, 0.f, 0.f, 0.f};
+  const int stride = gridDim.x * 8 * R;
+  const int first = (blockIdx.x * 8 + wid) * R;
+  auto issue = [&](int r0, int s) {
+    uint8_t* sp = wbase + s * L::STAGE;
+    float* sx = reinterpret_cast<float*>(sp);
+    bf16* sd = reinterpret_cast<bf16*>(sp + R * 512);
+    float* ss = reinterpret_cast<float*>(sp + R * 768);
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int row = r0 + i;
+      if (row < rows) {
+        const int b = row / per, j = row % per;
+        const float* src = j < x.na ? x.A + (long long)(b * x.a_rows + x.a_off + j) * x.lda
+                                    : x.Bsrc + (long long)(b * x.nb + j - x.na) * x.ldb;
+        cpa16(sx + i * 128 + lane * 4, src + lane * 4);
+        cpa8(sd + i * 128 + lane * 4, dy + (long long)row * ldy + lane * 4);
+      }
+    }
+    if (lane < R && r0 + lane < rows) {
+      cpa4(ss + lane, mean + r0 + lane);
+      cpa4(ss + R + lane, rstd + r0 + lane);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) issue(first + s * stride, s);
+  int it = 0;
+  for (int r0 = first; r0 < rows; r0 += stride, ++it) {
+    __syncwarp();                                   // every lane is done with the stage refilled next
+    issue(r0 + (S - 1) * stride, (it + S - 1) % S);
+    cpa_wait<S - 1>();
+    __syncwarp();                                   // the statistics copied by lanes 0..R-1
+    const uint8_t* sp = wbase + (it % S) * L::STAGE;
+    const float* sx = reinterpret_cast<const float*>(sp);
+    const bf16* sd = reinterpret_cast<const bf16*>(sp + R * 512);
+    const float* ss = reinterpret_cast<const float*>(sp + R * 768);
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int row = r0 + i;
+      if (row >= rows) break;
+      const float4 xv = *reinterpret_cast<const float4*>(sx + i * 128 + lane * 4);
+      const uint2 dvv = *reinterpret_cast<const uint2*>(sd + i * 128 + lane * 4);
+      const float mu = ss[i], inv = ss[R + i];
+      const float xr[4] = {xv.x, xv.y, xv.z, xv.w};
+      const float d[4] = {sm100::bf16_lo(dvv.x), sm100::bf16_hi(dvv.x), sm100::bf16_lo(dvv.y), sm100::bf16_hi(dvv.y)};
+      const float gg[4] = {gv.x, gv.y, gv.z, gv.w};
+      float xh[4], gh[4], s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        xh[u] = (xr[u] - mu) * inv;
+        gh[u] = d[u] * gg[u];
+        s1 += gh[u];
+        s2 += gh[u] * xh[u];
+        pg[u] += d[u] * xh[u];
+        pb[u] += d[u];
+      }
+      const float m1 = warp_sum(s1) * (1.f / 128), m2 = warp_sum(s2) * (1.f / 128);
+      const int b = row / per, j = row % per;
+      float* dst = j < out.na ? out.A + (long long)(b * out.a_rows + out.a_off + j) * out.lda
+                              : out.Bsrc + (long long)(b * out.nb + j - out.na) * out.ldb;
+      float o[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) o[u] = (gh[u] - m1 - xh[u] * m2) * inv;
+      reinterpret_cast<float4*>(dst)[lane] = make_float4(o[0], o[1], o[2], o[3]);
+    }
+  }
+  cpa_wait<0>();
+#pragma unroll
+  for (int u = 0; u < 4; ++u) { sg[wid][lane * 4 + u] = pg[u]; sb[wid][lane * 4 + u] = pb[u]; }
+  __syncthreads();
+  if (threadIdx.x < 128) {
+    float a = 0.f, bb = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) { a += sg[w][threadIdx.x]; bb += sb[w][threadIdx.x]; }
+    if (dgain) { atomicAdd(&dgain[threadIdx.x], a); atomicAdd(&dbias[threadIdx.x], bb); }
+  }
+}
+
+template <int R, int S>
+static void launch_ln_async(int bps, const RowMap& x, const float* g, const float* mean, const float* rstd,
+                            const bf16* dy, int ldy, const RowMapW& out, float* dgain, float* dbias,
+                            cudaStream_t st) {
+  constexpr int smem = LnAsync<R, S>::SMEM;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(ln_bwd128_async_kernel<R, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  const int grid = std::max(1, std::min(cdiv(x.rows(), 8 * R), 148 * bps));
+  launch(ln_bwd128_async_kernel<R, S>, grid, 256, smem, st, x, g, mean, rstd, dy, ldy, out, dgain, dbias);
+}
+
+// 0: register version (ln_bwd128_kernel); 1: R=2, S=4 at 3 blocks/SM; 2: R=2, S=3 at 4 blocks/SM;
+// 3: R=4, S=3 at 2 blocks/SM
+static int ln_async() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("LONGER_LN_ASYNC");
+    v = e ? std::atoi(e) : 1;
+  }
+  return v;
+}
+
 static int ln_lean() {
   static int lean = -1;
   if (lean < 0) {
@@ -524,7 +666,14 @@ void layernorm_bwd(const RowMap& x, int W, const float* g, const float* mean, co
   const bool ct = W == 128 && ln_contig(W, 4, x.A, x.lda, x.nb ? x.Bsrc : nullptr, x.ldb) &&
                   ln_contig(W, 4, out.A, out.lda, out.nb ? out.Bsrc : nullptr, out.ldb) && ldy % 4 == 0 &&
                   (reinterpret_cast<uintptr_t>(dy) & 7) == 0;
-  if (ct && ln_lean()) {
+  const int la = ln_async();
+  if (ct && ln_lean() && la == 1) {
+    launch_ln_async<2, 4>(3, x, g, mean, rstd, dy, ldy, out, dgain, dbias, st);
+  } else if (ct && ln_lean() && la == 2) {
+    launch_ln_async<2, 3>(4, x, g, mean, rstd, dy, ldy, out, dgain, dbias, st);
+  } else if (ct && ln_lean() && la == 3) {
+    launch_ln_async<4, 3>(2, x, g, mean, rstd, dy, ldy, out, dgain, dbias, st);
+  } else if (ct && ln_lean()) {
     constexpr int R = 4;
     const int grid2 = std::max(1, std::min(cdiv(rows, 8 * R), 148 * 3));        // 3 blocks fit per SM
     launch(ln_bwd128_kernel<R, bf16, false>, grid2, 256, 0, st, x, g, mean, rstd, dy, ldy, out, dgain, dbias, LnBwdExtra());
