@@ -547,6 +547,14 @@ __global__ void __launch_bounds__(256) ln_bwd128_async_kernel(RowMap x, const fl
   float pg[4] = {0.f, 0.f, 0.f, 0.f}, pb[4] = {0.f, 0.f, 0.f, 0.f};
   const int stride = gridDim.x * 8 * R;
   const int first = (blockIdx.x * 8 + wid) * R;
+  // row → (sample, row in sample) without an integer division: (row + ½)/per is ≥ ½/per away from
+  // an integer, far above the fp32 rounding at these sizes; one correction step makes it exact
+  const float inv_per = 1.f / (float)per;
+  auto split = [&](int row, int& b, int& j) {
+    b = (int)(((float)row + 0.5f) * inv_per);
+    j = row - b * per;
+    if (j < 0) { --b; j += per; } else if (j >= per) { ++b; j -= per; }
+  };
   auto issue = [&](int r0, int s) {
     uint8_t* sp = wbase + s * L::STAGE;
     float* sx = reinterpret_cast<float*>(sp);
@@ -556,7 +564,8 @@ __global__ void __launch_bounds__(256) ln_bwd128_async_kernel(RowMap x, const fl
     for (int i = 0; i < R; ++i) {
       const int row = r0 + i;
       if (row < rows) {
-        const int b = row / per, j = row % per;
+        int b, j;
+        split(row, b, j);
         const float* src = j < x.na ? x.A + (long long)(b * x.a_rows + x.a_off + j) * x.lda
                                     : x.Bsrc + (long long)(b * x.nb + j - x.na) * x.ldb;
         cpa16(sx + i * 128 + lane * 4, src + lane * 4);
@@ -601,8 +610,15 @@ __global__ void __launch_bounds__(256) ln_bwd128_async_kernel(RowMap x, const fl
         pg[u] += d[u] * xh[u];
         pb[u] += d[u];
       }
-      const float m1 = warp_sum(s1) * (1.f / 128), m2 = warp_sum(s2) * (1.f / 128);
-      const int b = row / per, j = row % per;
+      // both row sums in 7 shuffles: after the first exchange lanes 0-15 carry s1, lanes 16-31 s2
+      float kp = (lane & 16) ? s2 : s1;
+      kp += __shfl_xor_sync(0xffffffffu, (lane & 16) ? s1 : s2, 16);
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) kp += __shfl_xor_sync(0xffffffffu, kp, o);
+      const float m1 = __shfl_sync(0xffffffffu, kp, 0) * (1.f / 128);
+      const float m2 = __shfl_sync(0xffffffffu, kp, 16) * (1.f / 128);
+      int b, j;
+      split(row, b, j);
       float* dst = j < out.na ? out.A + (long long)(b * out.a_rows + out.a_off + j) * out.lda
                               : out.Bsrc + (long long)(b * out.nb + j - out.na) * out.ldb;
       float o[4];
@@ -695,7 +711,12 @@ void layernorm_bwd(const RowMap& x, int W, const float* g, const float* mean, co
   if (rows <= 0) return;
   // ~32 rows per 8-warp block: enough blocks to cover the SMs, few enough that the per-block
   // atomic flush of the column partials stays cheap
-  const int grid = std::max(1, std::min(cdiv(rows, 32), 148 * 8));
+  static int rpb = -1;
+  if (rpb < 0) {
+    const char* e = std::getenv("LONGER_LN_RPB");
+    rpb = e ? std::max(8, std::atoi(e)) : 32;
+  }
+  const int grid = std::max(1, std::min(cdiv(rows, rpb), 148 * 8));
   const int vpt = W <= 32 ? 1 : W <= 64 ? 2 : W <= 128 ? 4 : 8;
   const bool ct = ln_contig(W, vpt, x.A, x.lda, x.nb ? x.Bsrc : nullptr, x.ldb) &&
                   ln_contig(W, vpt, out.A, out.lda, out.nb ? out.Bsrc : nullptr, out.ldb) &&
