@@ -293,8 +293,8 @@ __global__ void ln_bwd_kernel(RowMap x, int W, const float* __restrict__ g, cons
     const int c = ln_col<VPT, CONTIG>(lane, u);
     gv[u] = c < W ? g[c] : 0.f;
   }
-  // software-pipelined over the warp's rows: every input of row r + stride is loaded before row r
-  // is reduced and stored, so each warp keeps two rows of loads in flight
+  // software-pipelined over the warp's rows: the inputs of the next rows are loaded before row r
+  // is reduced and stored
   struct RowIn {
     float x[VPT], dy[VPT], o[VPT], ad[VPT];
     float mu, inv, rm;
@@ -316,11 +316,18 @@ __global__ void ln_bwd_kernel(RowMap x, int W, const float* __restrict__ g, cons
   };
   const int stride = gridDim.x * warps;
   int row = blockIdx.x * warps + wid;
-  RowIn cur;
+  // VPT ≤ 4: three rows in flight (the warp's next two rows load while this one is reduced)
+  constexpr bool DEEP = VPT <= 4;
+  RowIn cur, nxt;
   if (row < rows) load_row(row, cur);
+  if (DEEP && row + stride < rows) load_row(row + stride, nxt);
   for (; row < rows; row += stride) {
-    RowIn nxt;
-    if (row + stride < rows) load_row(row + stride, nxt);
+    RowIn nn;
+    if (DEEP) {
+      if (row + 2 * stride < rows) load_row(row + 2 * stride, nn);
+    } else if (row + stride < rows) {
+      load_row(row + stride, nxt);
+    }
     const float mu = cur.mu, inv = cur.inv, rm = cur.rm;
     float* dst = cur.dst;
     float xh[VPT], gh[VPT], dyv[VPT];
@@ -383,6 +390,7 @@ __global__ void ln_bwd_kernel(RowMap x, int W, const float* __restrict__ g, cons
       }
     }
     cur = nxt;
+    if (DEEP) nxt = nn;
   }
   if (dgain || ex.colsum_out) {
 #pragma unroll
