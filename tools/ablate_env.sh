@@ -31,6 +31,9 @@ run LONGER_PRIO=0 LONGER_PRIO=0
 run LONGER_PDL=0 LONGER_PDL=0
 run LONGER_SIDE=0 LONGER_SIDE=0
 run LONGER_LN_LEAN=0 LONGER_LN_LEAN=0
+run LONGER_LN_ASYNC=0 LONGER_LN_ASYNC=0
+run LONGER_LN_ASYNC=1 LONGER_LN_ASYNC=1
+run LONGER_LN_RPB=16 LONGER_LN_RPB=16
 run LONGER_ATTN_TC=0 LONGER_ATTN_TC=0
 run LONGER_FUSED=0 LONGER_FUSED=0
 run default_again X=1
