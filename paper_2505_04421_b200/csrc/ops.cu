@@ -805,13 +805,10 @@ static void launch_ln_async(int bps, const RowMap& x, const float* g, const floa
 
 // 0: register version (ln_bwd128_kernel); 1: R=2, S=4 at 3 blocks/SM; 2: R=2, S=3 at 4 blocks/SM;
 // 3: R=4, S=3 at 2 blocks/SM; 4 / 5: half-warp rows (ln_bwd128_hw_kernel) R=2, S=4 / R=4, S=3
+// (read per launch, so a test can switch variants within one process)
 static int ln_async() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("LONGER_LN_ASYNC");
-    v = e ? std::atoi(e) : 5;
-  }
-  return v;
+  const char* e = std::getenv("LONGER_LN_ASYNC");
+  return e ? std::atoi(e) : 5;
 }
 
 static int ln_lean() {

@@ -148,6 +148,26 @@ def test_attention_variants_match_oracle(pack, tma, monkeypatch):
     assert_grads_close(grads, G, f"pack={pack} tma={tma}")
 
 
+@pytest.mark.parametrize("variant", ["0", "1", "2", "3", "4", "5"])
+def test_kv_layernorm_backward_variants_match_oracle(variant, monkeypatch):
+    """Every K/V-row LayerNorm backward variant (LONGER_LN_ASYNC, read per launch: 0 register rows,
+    1-3 full-warp cp.async rings, 4-5 half-warp rings = default) matches the oracle, with mixed
+    lengths and B = 5 so the last ring stage holds a partial group of rows."""
+    monkeypatch.setenv("LONGER_LN_ASYNC", variant)
+    cfg = ModelConfig(**dict(C2, L=512)).validate()
+    from paper_2505_04421_b200.params import init_params
+    P = init_params(cfg, seed=0)
+    rng = np.random.default_rng(9)
+    P = {n: a + 0.02 * rng.standard_normal(a.shape) for n, a in P.items()}
+    batch = synthetic_batch(cfg, 5, seed=23, min_events=1)
+    p_ref, loss_ref, G = O.forward_backward(P, cfg, batch.as_dict())
+    model = _model(cfg, P)
+    p, loss, grads = _run(model, batch)
+    assert np.max(np.abs(p - p_ref)) <= 5e-3
+    assert abs(loss - loss_ref) <= loss_tol(p_ref, batch.label)
+    assert_grads_close(grads, G, f"ln_async={variant}")
+
+
 @pytest.mark.parametrize("head_rows", ["1", "0"])
 def test_last_block_head_rows_match_oracle(head_rows, monkeypatch):
     """The last self block's row-wise tail on the two head rows only (default) and on all rows
