@@ -449,14 +449,22 @@ int gemm_launch(const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0) return 0;
   if (g.split_k != 1 && !(g.flags & EPI_ATOMIC)) return (int)cudaErrorInvalidValue;
   // Widest tile that still gives the 148 SMs work: the query-row GEMMs (M = 8,960 → 70 row
-  // tiles) would otherwise leave half the machine idle at N ≤ 128.
+  // tiles) would otherwise leave half the machine idle at N ≤ 128.  "Enough work" is ≥ 200 tiles:
+  // the query-row QKV / FFN-up GEMMs (N = 384 / 512) then take 128-wide tiles (210 / 280 items
+  // over 148 CTAs, the TMEM double buffer overlapping epilogues) instead of 140 256-wide ones
+  // (step 1.574 → 1.570 ms; 60 / 120 / 300 measured slower).
   const long long mt = (g.M + BM - 1) / BM;
   auto tiles = [&](int bn) { return mt * ((g.N + bn - 1) / bn); };
   const bool split = (g.flags & EPI_ATOMIC) != 0;           // split-K fills the machine itself
   if (g.N <= 64) return launch_bn<64>(g, st);
-  if (g.N <= 128) return (split || tiles(128) >= 120) ? launch_bn<128>(g, st) : launch_bn<64>(g, st);
-  if (split || tiles(256) >= 120) return launch_bn<256>(g, st);
-  return tiles(128) >= 120 ? launch_bn<128>(g, st) : launch_bn<64>(g, st);
+  static int min_tiles = -1;                                // LONGER_GEMM_MIN_TILES overrides (testing)
+  if (min_tiles < 0) {
+    const char* e = std::getenv("LONGER_GEMM_MIN_TILES");
+    min_tiles = e ? std::max(1, std::atoi(e)) : 200;
+  }
+  if (g.N <= 128) return (split || tiles(128) >= min_tiles) ? launch_bn<128>(g, st) : launch_bn<64>(g, st);
+  if (split || tiles(256) >= min_tiles) return launch_bn<256>(g, st);
+  return tiles(128) >= min_tiles ? launch_bn<128>(g, st) : launch_bn<64>(g, st);
 }
 
 }  // namespace longer
