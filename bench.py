@@ -10,9 +10,12 @@ device step with CUDA events (inputs resident in HBM, L2 flushed between steps);
 same step with the batch copied from pinned host memory and the loss read back every step.
 
 `--impl reference` times the CPU reference algorithm (the float64 oracle port of longrec in
-oracle/, all host threads) on a bounded sample of the same workload.
+oracle/, one single-threaded worker process per host core) on a bounded sample of the same step.
 
-Launch: python bench.py [--gpus N --steps K --warmup W]; N>1 under torch.distributed.run.
+Launch: python bench.py [--gpus N --steps K --warmup W]; with N > 1 and no torchrun environment the
+script relaunches itself under torch.distributed.run (one rank per GPU, NCCL); the step is then
+routed through paper_2505_04421_b200.dp.DataParallel (two gradient buckets, the first reduced on a
+communication stream beside the front-end backward).  `--config c4` measures serving instead.
 """
 from __future__ import annotations
 
@@ -143,44 +146,73 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(good)}
 
 
-def cpu_reference_rate(cfg, n_samples: int, seed: int = 1):
-    """Float64 oracle port of the reference algorithm, one batch of n_samples (all BLAS threads)."""
-    import numpy as np
-    from oracle import longer_oracle as O
-    from paper_2505_04421_b200 import init_params, synthetic_batch
-    P = init_params(cfg, 0)
-    batch = synthetic_batch(cfg, n_samples, seed=seed).as_dict()
-    O.forward_backward(P, cfg, {k: v[:1] for k, v in batch.items()})   # warm-up
-    t0 = time.perf_counter()
-    O.forward_backward(P, cfg, batch)
-    dt = time.perf_counter() - t0
-    return n_samples / dt, dt
+def cpu_samples_default() -> int:
+    return 4 * (os.cpu_count() or 1)
+
+
+def cpu_pool_rate(cfg, n_samples: int, steps: int = 1, warmup: int = 1, seed: int = 1):
+    """The reference algorithm on the host's cores: the float64 oracle port of longrec (pinned to
+    the reference's own outputs, tests/test_oracle.py), one single-threaded worker process per
+    core, each step = fwd + bwd of n_samples sharded over the workers + gradient sum + Adam
+    (oracle/cpu_pool.py).  Returns (samples/s over the timed steps, seconds per step, workers)."""
+    from oracle.cpu_pool import CpuPool
+    from paper_2505_04421_b200 import synthetic_batch
+    pool = CpuPool(cfg)
+    try:
+        for i in range(warmup):
+            pool.step(synthetic_batch(cfg, n_samples, seed=seed + i).as_dict())
+        total = 0.0
+        for i in range(steps):
+            batch = synthetic_batch(cfg, n_samples, seed=seed + warmup + i).as_dict()
+            t0 = time.perf_counter()
+            pool.step(batch)
+            total += time.perf_counter() - t0
+    finally:
+        pool.close()
+    return n_samples * steps / total, total / steps, pool.workers
+
+
+def cpu_baseline_entry(cfg, n_samples, steps, warmup):
+    from oracle.cpu_pool import cpu_model_name
+    rate, sec, workers = cpu_pool_rate(cfg, n_samples, steps, warmup)
+    return {"value": rate, "unit": "samples/s", "cores": workers, "kind": "port",
+            "cpu_model": cpu_model_name(), "threads_per_worker": 1,
+            "sample": f"{n_samples} samples/step ({sec:.2f} s/step, {steps} timed steps): fwd+bwd of the float64 "
+                      f"oracle port of longrec sharded over {workers} single-threaded worker processes, "
+                      f"gradient sum, Adam"}
 
 
 def run_reference(args, cfg):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    """--impl reference: the reference's CPU algorithm (the oracle port) on all host cores, on the
+    same config and metric; rank 0 only under torchrun."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
-    import numpy as np  # noqa: F401
-    sample = args.cpu_samples
-    rates, total = [], 0.0
-    for i in range(args.warmup + args.steps):
-        r, dt = cpu_reference_rate(cfg, sample, seed=1 + i)
-        if i >= args.warmup:
-            rates.append(r)
-            total += dt
-    value = sample * len(rates) / total
+    n = args.cpu_samples or cpu_samples_default()
+    base = cpu_baseline_entry(cfg, n, args.steps, args.warmup)
+    value = base["value"]
     line = {
         "impl": "reference", "metric": "samples/sec fwd+bwd at L=2000", "value": value, "unit": "samples/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / len(rates), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * n / value, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, **CONFIGS[args.config], "samples_per_step": sample},
-        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": os.cpu_count(), "kind": "port",
-                         "sample": f"{sample} samples/step, float64 NumPy oracle port of longrec fwd+bwd"},
+        "config": {"workload": args.config, **CONFIGS[args.config], "samples_per_step": n},
+        "cpu_baseline": base,
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def relaunch_under_torchrun(args) -> int:
+    """`bench.py --gpus N` without a torchrun environment: start N ranks (one per GPU) on this node
+    with the same arguments, NCCL init logging on, and return their exit code."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=dict(os.environ))
 
 
 def main():
@@ -191,7 +223,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2_inner", choices=sorted(CONFIGS))
     ap.add_argument("--batch", type=int, default=256, help="samples per GPU per step")
-    ap.add_argument("--cpu-samples", type=int, default=8)
+    ap.add_argument("--cpu-samples", type=int, default=0, help="CPU arm samples per step (0: 4 x cores)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -202,6 +234,10 @@ def main():
     if args.impl == "reference":
         run_reference(args, cfg)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
+    if int(os.environ.get("WORLD_SIZE", "1")) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE', '1')}")
 
     import torch
     import torch.distributed as dist
@@ -213,6 +249,9 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
+        # NCCL's init lines (rank / nranks / transport) on the log, for the rank-count check
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     B = args.batch
@@ -229,11 +268,15 @@ def main():
         for f in type(b).FIELDS:
             getattr(static, f).copy_(getattr(b, f), non_blocking=True)
 
+    from paper_2505_04421_b200.dp import DataParallel
+    dpm = DataParallel(model) if world > 1 else None
+
     def step_body(batch=None):
-        model.loss_backward(static if batch is None else batch, check=False)
-        if world > 1:
-            dist.all_reduce(model.grad_flat)
-            model.grad_flat.mul_(1.0 / world)
+        b = static if batch is None else batch
+        if dpm is not None:            # shard's fwd+bwd, early-bucket allreduce beside the front-end bwd
+            dpm.loss_backward(b, check=False)
+        else:
+            model.loss_backward(b, check=False)
         opt.step()
 
     stream = torch.cuda.current_stream(dev)
@@ -256,29 +299,35 @@ def main():
         load(dev_batches[i % n_batches])
         step_body()
     torch.cuda.synchronize()
-    graph = None
+    graph = graph2 = None
+    graph_note = "disabled (--no-graph)" if args.no_graph else "captured"
     if not args.no_graph:
         mark("capture")
-        graph = torch.cuda.CUDAGraph(keep_graph=True)
-        s = torch.cuda.Stream(dev)
-        s.wait_stream(stream)
-        with torch.cuda.stream(s):
-            step_body()
-        stream.wait_stream(s)
-        torch.cuda.synchronize()
-        with torch.cuda.graph(graph):
-            step_body()
-        torch.cuda.synchronize()
-        # the same step reading the second input slot: the e2e loop alternates slots, so the H2D of
-        # step i+1 lands directly in the slot the next graph reads (no device-side copy)
-        graph2 = torch.cuda.CUDAGraph(keep_graph=True)
-        with torch.cuda.graph(graph2):
-            step_body(static2)
-        torch.cuda.synchronize()
-
-    if graph is not None:
-        graph.instantiate() if hasattr(graph, "instantiate") else None
-        graph2.instantiate() if hasattr(graph2, "instantiate") else None
+        try:
+            s = torch.cuda.Stream(dev)
+            s.wait_stream(stream)
+            with torch.cuda.stream(s):
+                step_body()
+            stream.wait_stream(s)
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph(keep_graph=True)
+            with torch.cuda.graph(graph):
+                step_body()
+            torch.cuda.synchronize()
+            # the same step reading the second input slot: the e2e loop alternates slots, so the H2D
+            # of step i+1 lands directly in the slot the next graph reads (no device-side copy)
+            graph2 = torch.cuda.CUDAGraph(keep_graph=True)
+            with torch.cuda.graph(graph2):
+                step_body(static2)
+            torch.cuda.synchronize()
+            for g in (graph, graph2):
+                if hasattr(g, "instantiate"):
+                    g.instantiate()
+        except Exception as exc:          # e.g. a collective that refuses capture: run eagerly
+            graph = graph2 = None
+            graph_note = f"capture failed, eager steps ({type(exc).__name__}: {exc})"[:300]
+            print(f"[bench] rank {rank}: {graph_note}", file=sys.stderr, flush=True)
+            torch.cuda.synchronize()
 
     def run_step(slot=0):
         if graph is not None:
@@ -419,7 +468,7 @@ def main():
             "config": {"workload": args.config, **CONFIGS[args.config], "global_batch": world * B,
                        "per_gpu_batch": B, "parallelism": f"dp{world}", "l2": "flushed between steps",
                        "step": "fwd+bwd+allreduce+adam" if world > 1 else "fwd+bwd+adam",
-                       "cuda_graph": graph is not None},
+                       "cuda_graph": graph is not None, "cuda_graph_note": graph_note},
             "roofline": ({"bound": "tensor", "kernel": dom, "achieved": kernels[dom]["tflops"], "peak": burst,
                           "unit": "TFLOP/s", "frac": kernels[dom]["tflops"] / burst, "traffic": traffic,
                           "peak_source": src, "ms_per_launch": kernels[dom]["ms_per_launch"],
@@ -438,12 +487,9 @@ def main():
                                 "read on the host; one span from the first H2D to the last loss read"},
             "clocks": clk,
         }
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:
             try:
-                r, dt = cpu_reference_rate(cfg, args.cpu_samples)
-                line["cpu_baseline"] = {"value": r, "unit": "samples/s", "cores": os.cpu_count(), "kind": "port",
-                                        "sample": f"{args.cpu_samples} samples, one fwd+bwd of the float64 oracle "
-                                                  f"port ({dt:.1f} s)"}
+                line["cpu_baseline"] = cpu_baseline_entry(cfg, args.cpu_samples or cpu_samples_default(), 2, 1)
             except Exception as exc:  # pragma: no cover
                 line["cpu_baseline"] = {"value": None, "error": str(exc)}
         print(json.dumps(line), flush=True)

@@ -19,8 +19,12 @@
  *   - `ws` is scratch of at least `longer_workspace_bytes` bytes (256-byte aligned).
  *   - Return value: 0 on success, otherwise a LONGER_E* code; `longer_last_error()` gives text.
  *     Codes map 1:1 onto the reference exception classes (pkg/src/longrec/errors.py:8-29).
- *   - One thread drives one stream per device; calls are stream-ordered and graph-capturable
- *     (no host synchronisation inside).
+ *   - Calls are stream-ordered and graph-capturable (no host synchronisation inside) and
+ *     re-entrant: all per-call state lives in `ws` or on the stack; the only process-wide state
+ *     is the per-(kernel, device) shared-memory attribute cache.  The weight-gradient side
+ *     stream, its fork/join events, the LONGER_* tuning switches (read at every call) and the
+ *     diagnostic probes are per calling thread, so two threads may drive two models (or two
+ *     devices) concurrently, each with its own workspace.
  */
 #ifndef LONGER_H_
 #define LONGER_H_
@@ -71,6 +75,22 @@ int longer_workspace_bytes(const LongerDims* dims, size_t* bytes);
 int longer_forward(const LongerDims* dims, const float* params, const LongerBatch* batch,
                    void* ws, size_t ws_bytes, float* probs, void* stream);
 
+/* Activation trace of a forward (the reference's ForwardTrace, pkg/src/longrec/model.py:129-143,
+ * :365-372): device pointers into `ws`, valid until the next call on the same workspace. */
+typedef struct LongerTrace {
+  const float* h;              /* [B, Lp, d] token-MLP output, left zero rows for pad events */
+  const float* merged;         /* [B, G, D] merged sequence (InnerTrans / concat) */
+  const int32_t* query_groups; /* [B, k] merged group of each sequence query; null: "recent"
+                                  (G-k+i) or "learnable" (bank rows, no group) */
+  const float* layers[17];     /* [B, q, D] output of the cross block, then of each self block */
+  const float* head_input;     /* [B, head_width] [t, c, t*c, t*t, uid_emb, profile_emb] */
+  int32_t n_layers, Lp, G, q, head_width;
+} LongerTrace;
+
+/* longer_forward that also keeps every row of every layer and returns where the activations are. */
+int longer_forward_trace(const LongerDims* dims, const float* params, const LongerBatch* batch,
+                         void* ws, size_t ws_bytes, float* probs, LongerTrace* trace, void* stream);
+
 /* Training step body: probs[B], loss[0] = batch-mean BCE, grads (overwritten) = dloss/dparams. */
 int longer_forward_backward(const LongerDims* dims, const float* params, const LongerBatch* batch,
                             void* ws, size_t ws_bytes, float* probs, float* loss, float* grads,
@@ -114,6 +134,16 @@ int longer_score_workspace_bytes(const LongerDims* dims, int32_t candidates_per_
 int longer_cache_score(const LongerDims* dims, const float* params, const void* cache,
                        size_t cache_bytes, const int32_t* cand_items, int32_t candidates_per_user,
                        void* ws, size_t ws_bytes, float* probs, void* stream);
+
+/* Overlapped data-parallel gradient reduction.  grads[early_begin, count) — the
+ * cross and self blocks, the query bank and the head, about 2/3 of the parameters — are final
+ * before the front-end backward starts.  With an event set (caller-owned cudaEvent_t, per calling
+ * thread; null disables), longer_forward_backward / longer_backward record it at that point, on a
+ * stream that has joined all prior work of the call, so a communication stream can wait on it and
+ * reduce that range while the front-end backward runs; the rest is final when the call's stream
+ * reaches the end of the call. */
+int longer_grad_early_begin(const LongerDims* dims, int64_t* begin);
+int longer_set_grad_event(void* ev);
 
 /* Diagnostics: record caller-owned CUDA events (cudaEvent_t) immediately before / after one fused
  * kernel of subsequent calls, on the call's stream (graph-capturable).  phase: 0 front-end forward,

@@ -427,10 +427,11 @@ def forward(P, cfg, batch):
     vis1 = cross_mask(cfg, npg, qg)
     viss = self_mask(cfg, npg, qg)
     x, c_cross = block_fwd(P, "cross.", O, R, vis1, cfg.heads, False)
-    c_self = []
+    c_self, layers = [], [x]
     for i in range(cfg.N):
         x, c = block_fwd(P, f"self.{i}.", x, x, viss, cfg.heads, True)
         c_self.append(c)
+        layers.append(x)
     # head (model.py:346-362)
     t = x[:, k + m - 1]
     cl = x[:, k + 1]
@@ -443,7 +444,7 @@ def forward(P, cfg, batch):
     cache = dict(it=it, ac=ac, bucket=bucket, rec=rec, real=real, feat=feat, x0=x0, a1=a1, g1=g1, t1=t1,
                  inner=inner_cache, npg=npg, uid=uid, prof=prof, cand=cand, uid_emb=uid_emb, td=td, tfeat=tfeat,
                  raw=raw, ga=ga, gg=gg, gt=gt, c_cross=c_cross, c_self=c_self, x=x, t=t, cl=cl, hin=hin, qg=qg,
-                 z1=z1, hg=hg, ht=ht, z=z, p=p)
+                 z1=z1, hg=hg, ht=ht, z=z, p=p, h=h, merged=merged, layers=layers)
     return p, cache
 
 

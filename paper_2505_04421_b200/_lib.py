@@ -23,7 +23,7 @@ _EXC = {LONGER_ECONFIG: ConfigError, LONGER_EDIM: DimensionError, LONGER_ELOOKUP
 SYMBOLS = ("longer_param_count", "longer_workspace_bytes", "longer_forward", "longer_forward_backward",
            "longer_adam_step", "longer_read_status", "longer_last_error", "longer_set_probe",
            "longer_cache_bytes", "longer_cache_build", "longer_score_workspace_bytes", "longer_cache_score",
-           "longer_backward")
+           "longer_backward", "longer_forward_trace", "longer_grad_early_begin", "longer_set_grad_event")
 
 PROBES = {"fe_fwd": 0, "fe_inner_bwd": 1, "fe_mlp_bwd": 2, "xattn_fwd": 3, "xattn_bwd": 4,
           "fwd_rows": 5, "bwd_rows": 6}   # the last two bracket sections, not single kernels
@@ -39,6 +39,13 @@ class LongerDims(ctypes.Structure):
 class LongerBatch(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in (
         "items", "actions", "dt", "n_events", "uid", "profile", "cand_item", "label")]
+
+
+class LongerTrace(ctypes.Structure):
+    _fields_ = [("h", ctypes.c_void_p), ("merged", ctypes.c_void_p), ("query_groups", ctypes.c_void_p),
+                ("layers", ctypes.c_void_p * 17), ("head_input", ctypes.c_void_p),
+                ("n_layers", ctypes.c_int32), ("Lp", ctypes.c_int32), ("G", ctypes.c_int32),
+                ("q", ctypes.c_int32), ("head_width", ctypes.c_int32)]
 
 
 def so_path() -> Path:
@@ -69,9 +76,12 @@ def _declare(lib):
         "longer_forward": [pd, vp, pb, vp, ctypes.c_size_t, vp, vp],
         "longer_forward_backward": [pd, vp, pb, vp, ctypes.c_size_t, vp, vp, vp, vp],
         "longer_backward": [pd, vp, pb, vp, ctypes.c_size_t, vp, vp, vp, vp],
+        "longer_forward_trace": [pd, vp, pb, vp, ctypes.c_size_t, vp, ctypes.POINTER(LongerTrace), vp],
         "longer_adam_step": [vp, vp, vp, vp, i64, f32, i32, vp],
         "longer_read_status": [vp, ctypes.POINTER(i32), vp],
         "longer_set_probe": [i32, vp, vp],
+        "longer_grad_early_begin": [pd, ctypes.POINTER(i64)],
+        "longer_set_grad_event": [vp],
         "longer_cache_bytes": [pd, ctypes.POINTER(ctypes.c_size_t)],
         "longer_cache_build": [pd, vp, pb, vp, ctypes.c_size_t, vp, ctypes.c_size_t, vp],
         "longer_score_workspace_bytes": [pd, i32, ctypes.POINTER(ctypes.c_size_t)],
@@ -86,6 +96,9 @@ def _declare(lib):
     if hasattr(lib, "longer_test_gemm"):
         lib.longer_test_gemm.restype = ctypes.c_int
         lib.longer_test_gemm.argtypes = [vp, i32, i32, vp, i32, i32, vp, i32, i32, i32, i32, vp]
+    if hasattr(lib, "longer_test_layernorm"):
+        lib.longer_test_layernorm.restype = ctypes.c_int
+        lib.longer_test_layernorm.argtypes = [vp, i32, i32, vp, vp, vp, vp, vp, vp]
 
 
 def check(rc: int) -> None:

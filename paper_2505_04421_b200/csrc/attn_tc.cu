@@ -619,8 +619,7 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
 // miss TMA's 16-byte rules, or LONGER_ATTN_TMA=0 → thread loads).
 template <int DH>
 bool kv_maps(const AttnArgs& a, int pack, CUtensorMap& tK, CUtensorMap& tV) {
-  const char* env = std::getenv("LONGER_ATTN_TMA");
-  if (DH < 64 || (env && env[0] == '0')) return false;
+  if (DH < 64 || !g_knobs.attn_tma) return false;
   auto aligned = [](const void* p, long long ld, long long sb) {
     return (reinterpret_cast<uintptr_t>(p) & 15) == 0 && ld % 8 == 0 && sb % 8 == 0;
   };
@@ -637,8 +636,7 @@ bool kv_maps(const AttnArgs& a, int pack, CUtensorMap& tK, CUtensorMap& tV) {
 // (key rows contiguous across samples for the 2-D tensor map); LONGER_ATTN_PACK=0 disables.
 template <int DH>
 int pack_of(const AttnArgs& a) {
-  const char* env = std::getenv("LONGER_ATTN_PACK");             // 0: off, 2: also in the forward
-  if (DH > 128 || (env && env[0] == '0') || a.nq > 64 || a.nk > 64) return 1;
+  if (DH > 128 || g_knobs.attn_pack == 0 || a.nq > 64 || a.nk > 64) return 1;
   if (a.sk != (long long)a.nk * a.ldk || a.sv != (long long)a.nk * a.ldv) return 1;
   const int p = std::min(kC / a.nk, 128 / a.nq);
   return std::max(1, std::min(p, a.B));
@@ -647,11 +645,7 @@ int pack_of(const AttnArgs& a) {
 template <int DH, bool TMA>
 int launch_fwd_t(const AttnArgs& a, const CUtensorMap& tK, const CUtensorMap& tV, int pack, cudaStream_t st) {
   const int smem = (128 * DH + std::max(128 * kC, kC * DH) + kC * DH) * 2 + 64 + 1024;
-  static int done = 0;
-  if (!done) {
-    cudaFuncSetAttribute(xattn_fwd_kernel<DH, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    done = 1;
-  }
+  smem_attr(xattn_fwd_kernel<DH, TMA>, 227 * 1024);
   launch(xattn_fwd_kernel<DH, TMA>, ((a.B + pack - 1) / pack) * a.heads, kThreads, std::max(smem, 80 * 1024), st, a,
          tK, tV, pack);
   return (int)cudaGetLastError();
@@ -662,8 +656,7 @@ int launch_fwd(const AttnArgs& a, cudaStream_t st) {
   CUtensorMap tK{}, tV{};
   // the forward runs two CTAs per SM, so B·heads ≤ 296 CTAs are already one wave: packing would
   // only idle SMs (measured +10 µs per step); LONGER_ATTN_PACK=2 forces it for testing
-  const char* env = std::getenv("LONGER_ATTN_PACK");
-  const int pack = (env && env[0] == '2') ? pack_of<DH>(a) : 1;
+  const int pack = g_knobs.attn_pack == 2 ? pack_of<DH>(a) : 1;
   if constexpr (DH >= 64) {
     if (kv_maps<DH>(a, pack, tK, tV)) return launch_fwd_t<DH, true>(a, tK, tV, pack, st);
   }
@@ -674,11 +667,7 @@ template <int DH, bool TMA>
 int launch_bwd_t(const AttnArgs& a, const CUtensorMap& tK, const CUtensorMap& tV, int pack, cudaStream_t st) {
   const int QR = DH > 128 ? 64 : 128;
   const int smem = (2 * QR * DH + 2 * kC * DH + 2 * QR * kC) * 2 + 256 * 4 + 64 + 1024;
-  static int done = 0;
-  if (!done) {
-    cudaFuncSetAttribute(xattn_bwd_kernel<DH, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    done = 1;
-  }
+  smem_attr(xattn_bwd_kernel<DH, TMA>, 227 * 1024);
   launch(xattn_bwd_kernel<DH, TMA>, ((a.B + pack - 1) / pack) * a.heads, kThreads8, std::max(smem, 116 * 1024), st, a,
          tK, tV, pack);
   return (int)cudaGetLastError();

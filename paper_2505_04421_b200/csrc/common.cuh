@@ -5,6 +5,8 @@
 #include <stdint.h>
 
 #include <cstdlib>
+#include <mutex>
+#include <set>
 #include <utility>
 
 namespace longer {
@@ -22,28 +24,86 @@ typedef __nv_bfloat16 bf16;
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-inline bool pdl_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("LONGER_PDL");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v != 0;
+// Tuning / ablation switches (environment, LONGER_*).  Read into thread-local storage at every
+// C-ABI entry (refresh_knobs), so a test can toggle them between calls and two threads driving
+// the library never share them.  Defaults are the measured-best settings.
+struct Knobs {
+  int pdl = 1;             // LONGER_PDL: programmatic dependent launch
+  int prio = 1;            // LONGER_PRIO: side stream at the lowest launch priority
+  int side = 1;            // LONGER_SIDE: weight-gradient side stream
+  int fused = 1;           // LONGER_FUSED: fused front-end kernels
+  int attn_tc = 1;         // LONGER_ATTN_TC: tensor-core attention
+  int attn_tma = 1;        // LONGER_ATTN_TMA: K/V by TMA
+  int attn_pack = 1;       // LONGER_ATTN_PACK: 0 off, 1 backward, 2 forward too
+  int head_rows = 1;       // LONGER_HEAD_ROWS: last block's row-wise tail on the two head rows
+  int gemm_stage = 1;      // LONGER_GEMM_STAGE: smem-staged GEMM epilogue stores
+  int split_items = 74;    // LONGER_SPLIT_ITEMS: split-K work-item target of the weight gradients
+  int gemm_min_tiles = 200;  // LONGER_GEMM_MIN_TILES: fewest items a wider GEMM tile must give
+  int fe_grid = 0;         // LONGER_FE_GRID: cap on the fused front-end grids (0: the full machine)
+  int item_smem = 1;       // LONGER_ITEM_SMEM: item-table gradient staged in shared memory
+};
+
+inline int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return (e && *e) ? std::atoi(e) : dflt;
 }
 
-// The weight-gradient side stream (longer.cu) launches at the lowest priority and everything else
-// at the highest, so the block scheduler serves the critical dX chain first when both are ready.
-inline cudaStream_t g_side_stream = nullptr;
+inline Knobs read_knobs() {
+  Knobs k;
+  k.pdl = env_int("LONGER_PDL", 1);
+  k.prio = env_int("LONGER_PRIO", 1);
+  k.side = env_int("LONGER_SIDE", 1);
+  k.fused = env_int("LONGER_FUSED", 1);
+  k.attn_tc = env_int("LONGER_ATTN_TC", 1);
+  k.attn_tma = env_int("LONGER_ATTN_TMA", 1);
+  k.attn_pack = env_int("LONGER_ATTN_PACK", 1);
+  k.head_rows = env_int("LONGER_HEAD_ROWS", 1);
+  k.gemm_stage = env_int("LONGER_GEMM_STAGE", 1);
+  k.split_items = env_int("LONGER_SPLIT_ITEMS", 74);
+  k.gemm_min_tiles = env_int("LONGER_GEMM_MIN_TILES", 200);
+  k.fe_grid = env_int("LONGER_FE_GRID", 0);
+  k.item_smem = env_int("LONGER_ITEM_SMEM", 1);
+  if (k.split_items < 1) k.split_items = 1;
+  if (k.gemm_min_tiles < 1) k.gemm_min_tiles = 1;
+  return k;
+}
+
+inline thread_local Knobs g_knobs = read_knobs();
+inline void refresh_knobs() { g_knobs = read_knobs(); }
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the limit is a
+// per-device setting, so a process driving several GPUs raises it on each of them.
+inline void smem_attr(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.insert({kernel, dev}).second)
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+template <typename... KArgs>
+inline void smem_attr(void (*kernel)(KArgs...), int bytes) {
+  smem_attr(reinterpret_cast<const void*>(kernel), bytes);
+}
+
+// The weight-gradient side streams (longer.cu, one per device and driving thread) launch at the
+// lowest priority and everything else at the highest, so the block scheduler serves the critical
+// dX chain first when both are ready.
+inline thread_local cudaStream_t g_side_streams[16] = {};
+inline bool is_side_stream(cudaStream_t st) {
+  if (!st) return false;
+  for (cudaStream_t s : g_side_streams)
+    if (s == st) return true;
+  return false;
+}
 
 inline void launch_priorities(int& lo, int& hi) {
-  static int l = 1, h = 1;
-  if (l == 1) {
-    cudaDeviceGetStreamPriorityRange(&l, &h);
-    const char* e = std::getenv("LONGER_PRIO");
-    if (e && e[0] == '0') h = l;                 // all launches at the default priority
-  }
+  static int l = 0, h = 0;
+  static std::once_flag once;
+  std::call_once(once, [] { cudaDeviceGetStreamPriorityRange(&l, &h); });
   lo = l;
-  hi = h;
+  hi = g_knobs.prio ? h : l;                   // LONGER_PRIO=0: all launches at the default priority
 }
 
 template <typename... KArgs, typename... Args>
@@ -59,10 +119,10 @@ inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
   int n = 0;
   if (hi != lo) {
     at[n].id = cudaLaunchAttributePriority;
-    at[n].val.priority = (st != nullptr && st == g_side_stream) ? lo : hi;
+    at[n].val.priority = is_side_stream(st) ? lo : hi;
     ++n;
   }
-  if (pdl_enabled()) {
+  if (g_knobs.pdl) {
     at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[n].val.programmaticStreamSerializationAllowed = 1;
     ++n;

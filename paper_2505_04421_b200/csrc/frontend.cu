@@ -895,14 +895,11 @@ static int launch_fwd(const FrontArgs& a, cudaStream_t st) {
   const BlobOff bo = blob_offsets(DT, DT * KG, a.inner_layers);
   const int smem = ((bo.fwd_total + 63) & ~63) * 2 + kTile * std::max(DT + 16, kFP) * 2 + kTile * 64 * 2 +
                    a.inner_layers * 6 * DT * 4 + 2 * DT * KG * 4 + 64;
-  static int done = 0;
-  if (!done) {
-    cudaFuncSetAttribute(fe_fwd_kernel<DT, KG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    done = 1;
-  }
+  smem_attr(fe_fwd_kernel<DT, KG>, 227 * 1024);
   const long long ntiles = (a.T + kTile - 1) / kTile;
   const int per_sm = smem <= 113 * 1024 ? 2 : 1;
-  const int grid = (int)std::min<long long>(ntiles, per_sm * 148);
+  int grid = (int)std::min<long long>(ntiles, per_sm * 148);
+  if (g_knobs.fe_grid > 0) grid = std::min(grid, g_knobs.fe_grid);   // testing: many tiles per CTA
   launch(fe_fwd_kernel<DT, KG>, grid, kThreads, smem, st, a);
   return (int)cudaGetLastError();
 }
@@ -923,21 +920,17 @@ static int launch_mlp_bwd(const FrontArgs& a, cudaStream_t st) {
   const int H2 = 2 * DT * a.K;
   const int XK = DT + 16;
   const int n_item = a.vocab * a.d_item;
-  const char* env = std::getenv("LONGER_ITEM_SMEM");
   FrontArgs b = a;
-  b.item_smem = !(env && env[0] == '0');
+  b.item_smem = g_knobs.item_smem != 0;
   const int tab = (b.item_smem && n_item <= 16384) ? n_item : 0;
   const int smem = (2 * DT * kFP + 2 * H2 * DT + H2 * XK) * 2 + kTile * (kFP + XK + DT + 128 + 128 + 64 + 64) * 2 +
                    (2 * kTile * (DT + 1) + tab) * 4 + 128;
   if (smem > 227 * 1024) return (int)cudaErrorInvalidValue;
-  static int done = 0;
-  if (!done) {
-    cudaFuncSetAttribute(fe_mlp_bwd_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    done = 1;
-  }
+  smem_attr(fe_mlp_bwd_kernel<DT>, 227 * 1024);
   // column-block tiling: grid = tiles-per-sample x replicas (≤ 148 CTAs, one per SM)
   const int tps = (a.Lp + kTile - 1) / kTile;
-  const int r = std::max(1, std::min(a.B, 148 / tps));
+  int r = std::max(1, std::min(a.B, 148 / tps));
+  if (g_knobs.fe_grid > 0) r = std::max(1, std::min(r, g_knobs.fe_grid / tps));   // testing: many tiles per CTA
   // > 113 KB of smem keeps one CTA per SM (the kernel allocates all 512 TMEM columns)
   launch(fe_mlp_bwd_kernel<DT>, tps * r, kThreads8, std::max(smem, 116 * 1024), st, b);
   return (int)cudaGetLastError();

@@ -499,25 +499,18 @@ int launch_inner_bwd_ng(const FrontArgs& a, cudaStream_t st) {
   const int smem = nW * 2 + kTile * (3 * XK + 2 * DT + 2 * F4 + QS) * 2 + NG * kTile * KG * 8 + 5 * DT * 4 +
                    (NG > 1 ? 2 * NG * kTile * 8 * 4 : 0) + 64;
   if (smem > 227 * 1024) return (int)cudaErrorInvalidValue;
-  static int done = 0;
-  if (!done) {
-    cudaFuncSetAttribute(fe_inner_bwd_kernel<DT, KG, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    done = 1;
-  }
+  smem_attr(fe_inner_bwd_kernel<DT, KG, NG>, 227 * 1024);
   const long long ntiles = (a.T + kTile - 1) / kTile;
-  const int grid = (int)std::min<long long>(ntiles, 148);
+  int grid = (int)std::min<long long>(ntiles, 148);
+  if (g_knobs.fe_grid > 0) grid = std::min(grid, g_knobs.fe_grid);   // testing: many tiles per CTA
   launch(fe_inner_bwd_kernel<DT, KG, NG>, grid, 32 * (1 + kWorkers * NG), std::max(smem, 116 * 1024), st, a);
   return (int)cudaGetLastError();
 }
 
-// head width 32: eight workers (column pairs) unless LONGER_INNER_NG=1
+// head width 32: eight workers (column pairs); 16: four
 template <int DT, int KG>
 int launch_inner_bwd(const FrontArgs& a, cudaStream_t st) {
-  if constexpr (DT == 32) {
-    const char* env = std::getenv("LONGER_INNER_NG");
-    if (!(env && env[0] == '1')) return launch_inner_bwd_ng<DT, KG, 2>(a, st);
-  }
-  return launch_inner_bwd_ng<DT, KG, 1>(a, st);
+  return launch_inner_bwd_ng<DT, KG, DT == 32 ? 2 : 1>(a, st);
 }
 
 }  // namespace

@@ -390,22 +390,11 @@ template <int BN, int STAGES>
 int launch_cfg(const GemmArgs& g, const CUtensorMap& tA, const CUtensorMap& tB, dim3 grid, int kb_per,
                cudaStream_t st) {
   const int smem = Smem<BN, STAGES>::TOTAL;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(gemm_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr_set = true;
-  }
+  smem_attr(gemm_kernel<BN, STAGES>, smem);
   const int n_items = (int)(grid.x * grid.y * grid.z);
   const int ctas = std::min(n_items, 148);
   GemmArgs ga = g;
-  if (ga.staged < 0) {
-    static int env = -1;
-    if (env < 0) {
-      const char* e = std::getenv("LONGER_GEMM_STAGE");
-      env = (e && e[0] == '0') ? 0 : 1;
-    }
-    ga.staged = env;
-  }
+  if (ga.staged < 0) ga.staged = g_knobs.gemm_stage ? 1 : 0;
   launch(gemm_kernel<BN, STAGES>, dim3(ctas), kThreads, smem, st, tA, tB, ga, kb_per, (int)grid.x, (int)grid.y,
          n_items);
   return (int)cudaGetLastError();
@@ -428,11 +417,7 @@ int launch_bn(const GemmArgs& g, cudaStream_t st) {
   // to back; more splits only multiply the atomic epilogues, and these GEMMs run beside other
   // kernels on the side stream: 296 → 148 → 74 items measured 1.648 → 1.640 → 1.625 ms per step).
   // LONGER_SPLIT_ITEMS overrides the target.
-  static int split_items = -1;
-  if (split_items < 0) {
-    const char* e = std::getenv("LONGER_SPLIT_ITEMS");
-    split_items = e ? std::max(1, std::atoi(e)) : 74;
-  }
+  const int split_items = g_knobs.split_items;
   if (want == 0) want = (g.flags & EPI_ATOMIC) ? std::max(1, std::min(split_items / tiles, nkb / 4)) : 1;
   int split = std::max(1, std::min(want, nkb));
   int kb_per = (nkb + split - 1) / split;
@@ -457,12 +442,10 @@ int gemm_launch(const GemmArgs& g, cudaStream_t st) {
   auto tiles = [&](int bn) { return mt * ((g.N + bn - 1) / bn); };
   const bool split = (g.flags & EPI_ATOMIC) != 0;           // split-K fills the machine itself
   if (g.N <= 64) return launch_bn<64>(g, st);
-  static int min_tiles = -1;                                // LONGER_GEMM_MIN_TILES overrides (testing)
-  if (min_tiles < 0) {
-    const char* e = std::getenv("LONGER_GEMM_MIN_TILES");
-    min_tiles = e ? std::max(1, std::atoi(e)) : 200;
-  }
-  if (g.N <= 128) return (split || tiles(128) >= min_tiles) ? launch_bn<128>(g, st) : launch_bn<64>(g, st);
+  // LONGER_GEMM_MIN_TILES overrides both thresholds (read per call; 1 forces the widest tile)
+  const int min_tiles = g_knobs.gemm_min_tiles;
+  const int min_tiles128 = std::min(min_tiles, 120);        // N <= 128: 120 (measured in round 1)
+  if (g.N <= 128) return (split || tiles(128) >= min_tiles128) ? launch_bn<128>(g, st) : launch_bn<64>(g, st);
   if (split || tiles(256) >= min_tiles) return launch_bn<256>(g, st);
   return tiles(128) >= min_tiles ? launch_bn<128>(g, st) : launch_bn<64>(g, st);
 }

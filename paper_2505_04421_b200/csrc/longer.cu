@@ -31,7 +31,13 @@ thread_local std::string g_err;
 // launching stream (graph-capturable), so callers can time one kernel inside a whole step.
 enum Phase { PH_FE_FWD = 0, PH_FE_INNER_BWD = 1, PH_FE_MLP_BWD = 2, PH_XATTN_FWD = 3, PH_XATTN_BWD = 4,
              PH_FWD_ROWS = 5, PH_BWD_ROWS = 6, PH_N = 7 };
-cudaEvent_t g_probe[PH_N][2] = {};
+thread_local cudaEvent_t g_probe[PH_N][2] = {};   // set by longer_set_probe on the driving thread
+
+// Early-gradient event (longer_set_grad_event): recorded once grads[cross, total) are final.
+thread_local cudaEvent_t g_grad_event = nullptr;
+
+// (inside a stream capture a plain record is a capture-internal node other streams may wait on)
+void record_event(cudaEvent_t ev, cudaStream_t st) { cudaEventRecord(ev, st); }
 
 void probe(int ph, int which, cudaStream_t st) {
   // External record: inside stream capture this becomes a real event-record node (a plain
@@ -52,17 +58,16 @@ struct Side {
   cudaStream_t s = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr, mark_ev = nullptr;
 };
-Side g_side[16];
+thread_local Side g_side[16];     // per device and driving thread: calls never share events
 
 cudaStream_t side_stream(cudaStream_t main) {
-  const char* env = std::getenv("LONGER_SIDE");
-  if (env && env[0] == '0') return main;
+  if (!g_knobs.side) return main;
   int dev = 0;
   cudaGetDevice(&dev);
   Side& sd = g_side[dev & 15];
   if (!sd.s) {
     cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking);
-    g_side_stream = sd.s;
+    g_side_streams[dev & 15] = sd.s;
     cudaEventCreateWithFlags(&sd.fork_ev, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&sd.join_ev, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&sd.mark_ev, cudaEventDisableTiming);
@@ -238,6 +243,7 @@ struct Plan {
   int32_t* npg;
   int32_t* cand0;  // placeholder candidates of a cache build
   int32_t* qg;     // [B, k] query groups (uniform / recent_uniform)
+  int32_t* ids;    // [3, B] range-checked uid / profile / candidate item (check_sample_ids)
   int qs;          // query strategy
   Packed pk;
   // tokens
@@ -308,6 +314,7 @@ Plan make_plan(const LongerDims& d, void* ws) {
   p.npg = a.take<int32_t>(B);
   p.cand0 = a.take<int32_t>(B);
   p.qg = a.take<int32_t>((long long)B * d.k);
+  p.ids = a.take<int32_t>(3LL * B);
   p.wblob = a.take<bf16>(frontend_blob_bytes(dd, D, p.IL) / 2 + 64);
   take_packed(p, a);
   // tokens
@@ -507,9 +514,7 @@ int pack_weights(const Plan& p, const float* params, void* ws, cudaStream_t st) 
 
 // ------------------------------------------------------------------ forward
 bool use_attn_tc(const AttnArgs& a) {
-  const char* env = std::getenv("LONGER_ATTN_TC");
-  if (env && env[0] == '0') return false;
-  return attn_tc_supported(a) != 0;
+  return g_knobs.attn_tc && attn_tc_supported(a) != 0;
 }
 
 // One pre-norm attention block over the q query rows (pkg/src/longrec/attention.py:172-212).
@@ -898,6 +903,13 @@ int backward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs) {
   }
   TRY(block_bwd(c, ss, o.cross, p.cb, p.O, true, p.pk.c_wq, p.pk.c_wo, p.pk.c_w1, p.pk.c_w2, nullptr, nullptr,
                 nullptr));
+  if (g_grad_event) {
+    // grads[cross, total) (blocks, query bank, head) are final once the side stream has also
+    // drained their weight gradients: record there, after it joins main, so main never waits
+    const cudaStream_t es = ss == st ? st : ss;
+    fork_side(st, ss);
+    record_event(g_grad_event, es);
+  }
   // global-token MLP and raw rows
   cast_rows_bf16(p.dglob, (int)M, D, D, p.dglob_bf, D, nullptr, st);
   fork_side(st, ss);
@@ -1001,13 +1013,24 @@ int backward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs) {
 }
 
 bool use_fused(const Plan& p) {
-  const char* env = std::getenv("LONGER_FUSED");
-  if (env && env[0] == '0') return false;
+  if (!g_knobs.fused) return false;
   return frontend_supported(p.d, p.K, p.D, p.F, p.IL) != 0 && p.dims.n_actions <= 32;
+}
+
+// The caller's batch with its per-sample ids replaced by range-checked copies in the workspace.
+LongerBatch checked_batch(const Plan& p, const LongerBatch& bt, cudaStream_t st) {
+  LongerBatch b = bt;
+  check_sample_ids(bt.uid, bt.profile, bt.cand_item, p.B, p.dims.n_users, p.dims.n_profiles, p.dims.vocab, p.ids,
+                   p.status, st);
+  b.uid = p.ids;
+  b.profile = p.ids + p.B;
+  if (bt.cand_item) b.cand_item = p.ids + 2 * p.B;
+  return b;
 }
 
 int check_call(const LongerDims* dims, size_t ws_bytes, Plan* out, void* ws) {
   g_err.clear();
+  refresh_knobs();
   if (!dims) return fail(LONGER_EDIM, "null dims");
   int rc = validate(*dims);
   if (rc) return rc;
@@ -1212,38 +1235,62 @@ extern "C" int longer_workspace_bytes(const LongerDims* dims, size_t* bytes) {
 // training / inference entry points run the last self block's tail on the two head rows
 // (LONGER_HEAD_ROWS=0: all rows); the serving cache build keeps every row (it caches them)
 static bool compact_head_ok(const Plan& p) {
-  const char* e = std::getenv("LONGER_HEAD_ROWS");
-  return p.N >= 1 && p.m >= 3 && !(e && e[0] == '0');
+  return p.N >= 1 && p.m >= 3 && g_knobs.head_rows;
 }
 
 extern "C" int longer_forward(const LongerDims* dims, const float* params, const LongerBatch* batch, void* ws,
                               size_t ws_bytes, float* probs, void* stream) {
-  static Plan p;   // large struct; one driving thread per device (see longer.h)
+  Plan p;          // per call: no state survives between calls (re-entrant)
   int rc = check_call(dims, ws_bytes, &p, ws);
   if (rc) return rc;
   p.fused_fe = use_fused(p);
   p.compact_head = compact_head_ok(p);
   Ctx c{p, params, nullptr, (cudaStream_t)stream};
-  return forward(c, p, *batch, probs, nullptr, 0);
+  return forward(c, p, checked_batch(p, *batch, c.st), probs, nullptr, 0);
+}
+
+extern "C" int longer_forward_trace(const LongerDims* dims, const float* params, const LongerBatch* batch,
+                                    void* ws, size_t ws_bytes, float* probs, LongerTrace* trace, void* stream) {
+  Plan p;
+  int rc = check_call(dims, ws_bytes, &p, ws);
+  if (rc) return rc;
+  if (!batch || !probs || !trace) return fail(LONGER_EDIM, "null argument");
+  p.fused_fe = use_fused(p);
+  p.compact_head = false;                // every row of every layer is kept for the trace
+  Ctx c{p, params, nullptr, (cudaStream_t)stream};
+  rc = forward(c, p, checked_batch(p, *batch, c.st), probs, nullptr, 0);
+  if (rc) return rc;
+  LongerTrace t{};
+  t.h = p.IL ? p.h : p.merged;
+  t.merged = p.merged;
+  t.query_groups = (p.qs == QS_UNIFORM || p.qs == QS_RECENT_UNIFORM) ? p.qg : nullptr;
+  t.n_layers = 1 + p.N;
+  t.layers[0] = p.cb.out;
+  for (int i = 0; i < p.N; ++i) t.layers[1 + i] = p.sb[i].out;
+  t.head_input = p.hin;
+  t.Lp = p.Lp; t.G = p.G; t.q = p.q; t.head_width = p.HIN;
+  *trace = t;
+  return 0;
 }
 
 extern "C" int longer_forward_backward(const LongerDims* dims, const float* params, const LongerBatch* batch,
                                        void* ws, size_t ws_bytes, float* probs, float* loss, float* grads,
                                        void* stream) {
-  static Plan p;
+  Plan p;
   int rc = check_call(dims, ws_bytes, &p, ws);
   p.fused_fe = use_fused(p);
   if (rc) return rc;
   p.compact_head = compact_head_ok(p);
   Ctx c{p, params, grads, (cudaStream_t)stream};
-  rc = forward(c, p, *batch, probs, loss, 1);
+  const LongerBatch bt = checked_batch(p, *batch, c.st);
+  rc = forward(c, p, bt, probs, loss, 1);
   if (rc) return rc;
-  return backward(c, p, *batch, probs);
+  return backward(c, p, bt, probs);
 }
 
 extern "C" int longer_backward(const LongerDims* dims, const float* params, const LongerBatch* batch, void* ws,
                                size_t ws_bytes, const float* probs, const float* dprobs, float* grads, void* stream) {
-  static Plan p;
+  Plan p;
   int rc = check_call(dims, ws_bytes, &p, ws);
   if (rc) return rc;
   if (!batch || !probs || !dprobs || !grads) return fail(LONGER_EDIM, "null argument");
@@ -1251,7 +1298,7 @@ extern "C" int longer_backward(const LongerDims* dims, const float* params, cons
   p.compact_head = compact_head_ok(p);
   Ctx c{p, params, grads, (cudaStream_t)stream};
   dz_from_dprobs(probs, dprobs, p.B, p.dz, c.st);     // dL/dz = dL/dp · p(1 − p)
-  return backward(c, p, *batch, const_cast<float*>(probs));
+  return backward(c, p, checked_batch(p, *batch, c.st), const_cast<float*>(probs));
 }
 
 extern "C" int longer_adam_step(float* params, const float* grads, float* m, float* v, int64_t count, float lr,
@@ -1284,14 +1331,14 @@ extern "C" int longer_cache_bytes(const LongerDims* dims, size_t* bytes) {
 
 extern "C" int longer_cache_build(const LongerDims* dims, const float* params, const LongerBatch* batch, void* ws,
                                   size_t ws_bytes, void* cache, size_t cache_bytes, void* stream) {
-  static Plan p;
+  Plan p;
   int rc = check_call(dims, ws_bytes, &p, ws);
   if (rc) return rc;
   if (!batch || !cache) return fail(LONGER_EDIM, "null batch or cache");
   if (cache_bytes < cache_layout(p).bytes) return fail(LONGER_EDIM, "cache buffer too small");
   p.fused_fe = use_fused(p);
   Ctx c{p, params, nullptr, (cudaStream_t)stream};
-  return cache_build(c, p, *batch, reinterpret_cast<char*>(cache));
+  return cache_build(c, p, checked_batch(p, *batch, c.st), reinterpret_cast<char*>(cache));
 }
 
 extern "C" int longer_score_workspace_bytes(const LongerDims* dims, int32_t candidates_per_user, size_t* bytes) {
@@ -1311,14 +1358,27 @@ extern "C" int longer_cache_score(const LongerDims* dims, const float* params, c
   int rc = validate(*dims);
   if (rc) return rc;
   if (candidates_per_user < 1) return fail(LONGER_EDIM, "candidates_per_user must be >= 1");
-  static ScorePlan s;
-  s = make_score_plan(*dims, candidates_per_user, ws);
+  refresh_knobs();
+  ScorePlan s = make_score_plan(*dims, candidates_per_user, ws);
   if (ws_bytes < s.bytes) return fail(LONGER_EDIM, "workspace too small");
   if (reinterpret_cast<uintptr_t>(ws) & 255) return fail(LONGER_EDIM, "workspace must be 256-byte aligned");
   if (cache_bytes != cache_layout(s.p).bytes)
     return fail(LONGER_ESTALE, "cache was built for different dimensions (rebuild it)");
   Ctx c{s.p, params, nullptr, (cudaStream_t)stream};
   return cache_score(c, s, reinterpret_cast<const char*>(cache), cand_items, probs);
+}
+
+extern "C" int longer_grad_early_begin(const LongerDims* dims, int64_t* begin) {
+  if (!dims || !begin) return fail(LONGER_EDIM, "null argument");
+  int rc = validate(*dims);
+  if (rc) return rc;
+  *begin = param_offsets(*dims).cross.w_q;
+  return 0;
+}
+
+extern "C" int longer_set_grad_event(void* ev) {
+  g_grad_event = (cudaEvent_t)ev;
+  return 0;
 }
 
 extern "C" int longer_set_probe(int32_t phase, void* ev_begin, void* ev_end) {

@@ -144,8 +144,7 @@ void embed_bwd(const EmbedBwdArgs& a, cudaStream_t st) {
   int item_in_smem = (a.vocab * a.d_item <= 12288) ? 1 : 0;
   const int smem = 4 * (F * a.d + a.nb * a.d_time + a.n_actions * a.d_act + (item_in_smem ? a.vocab * a.d_item : 0));
   const int tpb = 4096;
-  static int attr_done = 0;
-  if (!attr_done) { cudaFuncSetAttribute(embed_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024); attr_done = 1; }
+  smem_attr(embed_bwd_kernel, 96 * 1024);
   launch(embed_bwd_kernel, cdiv(T, tpb), 256, smem, st, a, tpb, item_in_smem);
   launch(pos_grad_kernel, a.L, 32 * cdiv(a.d, 32), 0, st, a);
 }
@@ -408,112 +407,6 @@ __global__ void ln_bwd_kernel(RowMap x, int W, const float* __restrict__ g, cons
   }
 }
 
-// Lean LN backward for W = 128 with a bf16 dy and no extras: a warp takes R rows at a time (all
-// their loads issued before any reduction), lane owns 4 contiguous columns; gain / bias partials
-// stay in registers and are flushed once per block.
-template <typename TY>
-__device__ __forceinline__ void ld4(const TY* p, int lane, float* d);
-template <>
-__device__ __forceinline__ void ld4<bf16>(const bf16* p, int lane, float* d) {
-  const uint2 v = __ldg(reinterpret_cast<const uint2*>(p) + lane);
-  d[0] = sm100::bf16_lo(v.x); d[1] = sm100::bf16_hi(v.x); d[2] = sm100::bf16_lo(v.y); d[3] = sm100::bf16_hi(v.y);
-}
-template <>
-__device__ __forceinline__ void ld4<float>(const float* p, int lane, float* d) {
-  const float4 v = __ldg(reinterpret_cast<const float4*>(p) + lane);
-  d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
-}
-
-// optional per-row operands of the query-row LN backward: + addend (fp32), bf16 copy of the
-// output, column sums of the output (the next bias gradient)
-template <int R, typename TY, bool EX>
-__global__ void __launch_bounds__(256) ln_bwd128_kernel(RowMap x, const float* __restrict__ g,
-                                                        const float* __restrict__ mean,
-                                                        const float* __restrict__ rstd, const TY* __restrict__ dy,
-                                                        int ldy, RowMapW out, float* dgain, float* dbias,
-                                                        LnBwdExtra ex) {
-  pdl_trigger();
-  pdl_wait();
-  __shared__ float sg[8][128], sb[8][128];
-  const int wid = threadIdx.x / 32, lane = threadIdx.x & 31;
-  const int rows = x.rows();
-  const int per = x.na + x.nb;
-  const float4 gv = __ldg(reinterpret_cast<const float4*>(g) + lane);
-  float pg[4] = {0.f, 0.f, 0.f, 0.f}, pb[4] = {0.f, 0.f, 0.f, 0.f}, pc[4] = {0.f, 0.f, 0.f, 0.f};
-  const int stride = gridDim.x * 8 * R;
-  for (int r0 = (blockIdx.x * 8 + wid) * R; r0 < rows; r0 += stride) {
-    float4 xv[R];
-    float dv[R][4], ad[R][4];
-    float mu[R], inv[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const int row = r0 + i;
-      if (row < rows) {
-        const int b = row / per, j = row % per;
-        const float* src = j < x.na ? x.A + (long long)(b * x.a_rows + x.a_off + j) * x.lda
-                                    : x.Bsrc + (long long)(b * x.nb + j - x.na) * x.ldb;
-        xv[i] = __ldg(reinterpret_cast<const float4*>(src) + lane);
-        ld4<TY>(dy + (long long)row * ldy, lane, dv[i]);
-        if (EX && ex.addend) ld4<float>(ex.addend + (long long)row * 128, lane, ad[i]);
-        mu[i] = mean[row];
-        inv[i] = rstd[row];
-      } else {
-        xv[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) { dv[i][u] = 0.f; ad[i][u] = 0.f; }
-        mu[i] = 0.f;
-        inv[i] = 0.f;
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const int row = r0 + i;
-      const float xr[4] = {xv[i].x, xv[i].y, xv[i].z, xv[i].w};
-      const float* d = dv[i];
-      const float gg[4] = {gv.x, gv.y, gv.z, gv.w};
-      float xh[4], gh[4], s1 = 0.f, s2 = 0.f;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        xh[u] = (xr[u] - mu[i]) * inv[i];
-        gh[u] = d[u] * gg[u];
-        s1 += gh[u];
-        s2 += gh[u] * xh[u];
-        if (row < rows) { pg[u] += d[u] * xh[u]; pb[u] += d[u]; }
-      }
-      const float m1 = warp_sum(s1) * (1.f / 128), m2 = warp_sum(s2) * (1.f / 128);
-      if (row < rows) {
-        const int b = row / per, j = row % per;
-        float* dst = j < out.na ? out.A + (long long)(b * out.a_rows + out.a_off + j) * out.lda
-                                : out.Bsrc + (long long)(b * out.nb + j - out.na) * out.ldb;
-        float o[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          o[u] = (gh[u] - m1 - xh[u] * m2) * inv[i];
-          if (EX && ex.addend) o[u] += ad[i][u];
-          if (EX) pc[u] += o[u];
-        }
-        reinterpret_cast<float4*>(dst)[lane] = make_float4(o[0], o[1], o[2], o[3]);
-        if (EX && ex.out_bf)
-          reinterpret_cast<uint2*>(ex.out_bf + (long long)row * 128)[lane] =
-              make_uint2(sm100::pack_bf16(o[0], o[1]), sm100::pack_bf16(o[2], o[3]));
-      }
-    }
-  }
-  __shared__ float sc[8][128];
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    sg[wid][lane * 4 + u] = pg[u]; sb[wid][lane * 4 + u] = pb[u]; sc[wid][lane * 4 + u] = pc[u];
-  }
-  __syncthreads();
-  if (threadIdx.x < 128) {
-    float a = 0.f, bb = 0.f, cc = 0.f;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) { a += sg[w][threadIdx.x]; bb += sb[w][threadIdx.x]; cc += sc[w][threadIdx.x]; }
-    if (dgain) { atomicAdd(&dgain[threadIdx.x], a); atomicAdd(&dbias[threadIdx.x], bb); }
-    if (EX && ex.colsum_out) atomicAdd(&ex.colsum_out[threadIdx.x], cc);
-  }
-}
-
 // Pipelined lean LN backward (W = 128, bf16 dy, no extras): each warp streams its rows through an
 // S-stage ring of shared memory with per-lane cp.async (16 B of x, 8 B of dy per lane and row, the
 // row statistics by lanes 0..R-1), so S-1 groups of R rows stay in flight while the current group
@@ -535,117 +428,6 @@ struct LnAsync {
   static constexpr int STAGE = R * 768 + 32 * 4;   // x rows fp32 | dy rows bf16 | mean[R], rstd[R]
   static constexpr int SMEM = 8 * S * STAGE;
 };
-
-template <int R, int S>
-__global__ void __launch_bounds__(256) ln_bwd128_async_kernel(RowMap x, const float* __restrict__ g,
-                                                              const float* __restrict__ mean,
-                                                              const float* __restrict__ rstd,
-                                                              const bf16* __restrict__ dy, int ldy, RowMapW out,
-                                                              float* dgain, float* dbias) {
-  pdl_trigger();
-  pdl_wait();
-  using L = LnAsync<R, S>;
-  extern __shared__ __align__(16) uint8_t lsm[];
-  __shared__ float sg[8][128], sb[8][128];
-  const int wid = threadIdx.x / 32, lane = threadIdx.x & 31;
-  uint8_t* wbase = lsm + wid * S * L::STAGE;
-  const int rows = x.rows();
-  const int per = x.na + x.nb;
-  const float4 gv = __ldg(reinterpret_cast<const float4*>(g) + lane);
-  float pg[4] = {0.f, 0.f, 0.f, 0.f}, pb[4] = {0.f, 0.f, 0.f, 0.f};
-  const int stride = gridDim.x * 8 * R;
-  const int first = (blockIdx.x * 8 + wid) * R;
-  // row → (sample, row in sample) without an integer division: (row + ½)/per is ≥ ½/per away from
-  // an integer, far above the fp32 rounding at these sizes; one correction step makes it exact
-  const float inv_per = 1.f / (float)per;
-  auto split = [&](int row, int& b, int& j) {
-    b = (int)(((float)row + 0.5f) * inv_per);
-    j = row - b * per;
-    if (j < 0) { --b; j += per; } else if (j >= per) { ++b; j -= per; }
-  };
-  auto issue = [&](int r0, int s) {
-    uint8_t* sp = wbase + s * L::STAGE;
-    float* sx = reinterpret_cast<float*>(sp);
-    bf16* sd = reinterpret_cast<bf16*>(sp + R * 512);
-    float* ss = reinterpret_cast<float*>(sp + R * 768);
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const int row = r0 + i;
-      if (row < rows) {
-        int b, j;
-        split(row, b, j);
-        const float* src = j < x.na ? x.A + (long long)(b * x.a_rows + x.a_off + j) * x.lda
-                                    : x.Bsrc + (long long)(b * x.nb + j - x.na) * x.ldb;
-        cpa16(sx + i * 128 + lane * 4, src + lane * 4);
-        cpa8(sd + i * 128 + lane * 4, dy + (long long)row * ldy + lane * 4);
-      }
-    }
-    if (lane < R && r0 + lane < rows) {
-      cpa4(ss + lane, mean + r0 + lane);
-      cpa4(ss + R + lane, rstd + r0 + lane);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-#pragma unroll
-  for (int s = 0; s < S - 1; ++s) issue(first + s * stride, s);
-  int it = 0;
-  for (int r0 = first; r0 < rows; r0 += stride, ++it) {
-    __syncwarp();                                   // every lane is done with the stage refilled next
-    issue(r0 + (S - 1) * stride, (it + S - 1) % S);
-    cpa_wait<S - 1>();
-    __syncwarp();                                   // the statistics copied by lanes 0..R-1
-    const uint8_t* sp = wbase + (it % S) * L::STAGE;
-    const float* sx = reinterpret_cast<const float*>(sp);
-    const bf16* sd = reinterpret_cast<const bf16*>(sp + R * 512);
-    const float* ss = reinterpret_cast<const float*>(sp + R * 768);
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const int row = r0 + i;
-      if (row >= rows) break;
-      const float4 xv = *reinterpret_cast<const float4*>(sx + i * 128 + lane * 4);
-      const uint2 dvv = *reinterpret_cast<const uint2*>(sd + i * 128 + lane * 4);
-      const float mu = ss[i], inv = ss[R + i];
-      const float xr[4] = {xv.x, xv.y, xv.z, xv.w};
-      const float d[4] = {sm100::bf16_lo(dvv.x), sm100::bf16_hi(dvv.x), sm100::bf16_lo(dvv.y), sm100::bf16_hi(dvv.y)};
-      const float gg[4] = {gv.x, gv.y, gv.z, gv.w};
-      float xh[4], gh[4], s1 = 0.f, s2 = 0.f;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        xh[u] = (xr[u] - mu) * inv;
-        gh[u] = d[u] * gg[u];
-        s1 += gh[u];
-        s2 += gh[u] * xh[u];
-        pg[u] += d[u] * xh[u];
-        pb[u] += d[u];
-      }
-      // both row sums in 7 shuffles: after the first exchange lanes 0-15 carry s1, lanes 16-31 s2
-      float kp = (lane & 16) ? s2 : s1;
-      kp += __shfl_xor_sync(0xffffffffu, (lane & 16) ? s1 : s2, 16);
-#pragma unroll
-      for (int o = 8; o > 0; o >>= 1) kp += __shfl_xor_sync(0xffffffffu, kp, o);
-      const float m1 = __shfl_sync(0xffffffffu, kp, 0) * (1.f / 128);
-      const float m2 = __shfl_sync(0xffffffffu, kp, 16) * (1.f / 128);
-      int b, j;
-      split(row, b, j);
-      float* dst = j < out.na ? out.A + (long long)(b * out.a_rows + out.a_off + j) * out.lda
-                              : out.Bsrc + (long long)(b * out.nb + j - out.na) * out.ldb;
-      float o[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) o[u] = (gh[u] - m1 - xh[u] * m2) * inv;
-      reinterpret_cast<float4*>(dst)[lane] = make_float4(o[0], o[1], o[2], o[3]);
-    }
-  }
-  cpa_wait<0>();
-#pragma unroll
-  for (int u = 0; u < 4; ++u) { sg[wid][lane * 4 + u] = pg[u]; sb[wid][lane * 4 + u] = pb[u]; }
-  __syncthreads();
-  if (threadIdx.x < 128) {
-    float a = 0.f, bb = 0.f;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) { a += sg[w][threadIdx.x]; bb += sb[w][threadIdx.x]; }
-    if (dgain) { atomicAdd(&dgain[threadIdx.x], a); atomicAdd(&dbias[threadIdx.x], bb); }
-  }
-}
 
 // Half-warp-per-row variant: 16 lanes × 8 columns per row, the two half-warps on neighbouring rows,
 // so every address computation, shuffle and loop step covers two rows (R = rows per stage, even).
@@ -780,44 +562,9 @@ template <int R, int S>
 static void launch_ln_hw(int bps, const RowMap& x, const float* g, const float* mean, const float* rstd,
                          const bf16* dy, int ldy, const RowMapW& out, float* dgain, float* dbias, cudaStream_t st) {
   constexpr int smem = LnAsync<R, S>::SMEM;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(ln_bwd128_hw_kernel<R, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  smem_attr(ln_bwd128_hw_kernel<R, S>, smem);
   const int grid = std::max(1, std::min(cdiv(x.rows(), 8 * R), 148 * bps));
   launch(ln_bwd128_hw_kernel<R, S>, grid, 256, smem, st, x, g, mean, rstd, dy, ldy, out, dgain, dbias);
-}
-
-template <int R, int S>
-static void launch_ln_async(int bps, const RowMap& x, const float* g, const float* mean, const float* rstd,
-                            const bf16* dy, int ldy, const RowMapW& out, float* dgain, float* dbias,
-                            cudaStream_t st) {
-  constexpr int smem = LnAsync<R, S>::SMEM;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(ln_bwd128_async_kernel<R, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
-  const int grid = std::max(1, std::min(cdiv(x.rows(), 8 * R), 148 * bps));
-  launch(ln_bwd128_async_kernel<R, S>, grid, 256, smem, st, x, g, mean, rstd, dy, ldy, out, dgain, dbias);
-}
-
-// 0: register version (ln_bwd128_kernel); 1: R=2, S=4 at 3 blocks/SM; 2: R=2, S=3 at 4 blocks/SM;
-// 3: R=4, S=3 at 2 blocks/SM; 4 / 5: half-warp rows (ln_bwd128_hw_kernel) R=2, S=4 / R=4, S=3
-// (read per launch, so a test can switch variants within one process)
-static int ln_async() {
-  const char* e = std::getenv("LONGER_LN_ASYNC");
-  return e ? std::atoi(e) : 5;
-}
-
-static int ln_lean() {
-  static int lean = -1;
-  if (lean < 0) {
-    const char* e = std::getenv("LONGER_LN_LEAN");
-    lean = (e && e[0] == '0') ? 0 : 1;
-  }
-  return lean;
 }
 
 // bf16 dy (a dX GEMM written in bf16: half the bytes of the HBM-bound K/V-row LN backward)
@@ -829,22 +576,9 @@ void layernorm_bwd(const RowMap& x, int W, const float* g, const float* mean, co
   const bool ct = W == 128 && ln_contig(W, 4, x.A, x.lda, x.nb ? x.Bsrc : nullptr, x.ldb) &&
                   ln_contig(W, 4, out.A, out.lda, out.nb ? out.Bsrc : nullptr, out.ldb) && ldy % 4 == 0 &&
                   (reinterpret_cast<uintptr_t>(dy) & 7) == 0;
-  int la = ln_async();
-  if (la >= 4 && (ldy % 8 != 0 || (reinterpret_cast<uintptr_t>(dy) & 15) != 0)) la = 1;   // 16-byte dy rows
-  if (ct && ln_lean() && la == 1) {
-    launch_ln_async<2, 4>(3, x, g, mean, rstd, dy, ldy, out, dgain, dbias, st);
-  } else if (ct && ln_lean() && la == 2) {
-    launch_ln_async<2, 3>(4, x, g, mean, rstd, dy, ldy, out, dgain, dbias, st);
-  } else if (ct && ln_lean() && la == 3) {
-    launch_ln_async<4, 3>(2, x, g, mean, rstd, dy, ldy, out, dgain, dbias, st);
-  } else if (ct && ln_lean() && la == 4) {
-    launch_ln_hw<2, 4>(3, x, g, mean, rstd, dy, ldy, out, dgain, dbias, st);
-  } else if (ct && ln_lean() && la == 5) {
+  const bool dy16 = ldy % 8 == 0 && (reinterpret_cast<uintptr_t>(dy) & 15) == 0;   // 16-byte dy rows
+  if (ct && dy16) {
     launch_ln_hw<4, 3>(2, x, g, mean, rstd, dy, ldy, out, dgain, dbias, st);
-  } else if (ct && ln_lean()) {
-    constexpr int R = 4;
-    const int grid2 = std::max(1, std::min(cdiv(rows, 8 * R), 148 * 3));        // 3 blocks fit per SM
-    launch(ln_bwd128_kernel<R, bf16, false>, grid2, 256, 0, st, x, g, mean, rstd, dy, ldy, out, dgain, dbias, LnBwdExtra());
   } else if (ct)
     launch(ln_bwd_kernel<4, true, bf16>, grid, 256, 0, st, x, W, g, mean, rstd, dy, ldy, out, 0,
            static_cast<const float*>(nullptr), dgain, dbias, LnBwdExtra());
@@ -863,11 +597,7 @@ void layernorm_bwd(const RowMap& x, int W, const float* g, const float* mean, co
   if (rows <= 0) return;
   // ~32 rows per 8-warp block: enough blocks to cover the SMs, few enough that the per-block
   // atomic flush of the column partials stays cheap
-  static int rpb = -1;
-  if (rpb < 0) {
-    const char* e = std::getenv("LONGER_LN_RPB");
-    rpb = e ? std::max(8, std::atoi(e)) : 32;
-  }
+  constexpr int rpb = 32;                      // 8 / 16 / 64 measured slower (round 1)
   const int grid = std::max(1, std::min(cdiv(rows, rpb), 148 * 8));
   const int vpt = W <= 32 ? 1 : W <= 64 ? 2 : W <= 128 ? 4 : 8;
   const bool ct = ln_contig(W, vpt, x.A, x.lda, x.nb ? x.Bsrc : nullptr, x.ldb) &&
@@ -1193,14 +923,10 @@ __global__ void group_attn_bwd_kernel(const float* __restrict__ qkv, const float
 void group_attn_fwd(const float* qkv, int T, int K, int w, bf16* ctx, float* probs, cudaStream_t st) {
   const int TT = (128 / K) * K;
   const int smem = 4 * (TT * (3 * w + 1) + TT * (w + 1));
-  static int done = 0;
-  if (!done) {
-    cudaFuncSetAttribute(group_attn_fwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(group_attn_fwd_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(group_attn_fwd_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(group_attn_fwd_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    done = 1;
-  }
+  smem_attr(group_attn_fwd_kernel<2>, 200 * 1024);
+  smem_attr(group_attn_fwd_kernel<4>, 200 * 1024);
+  smem_attr(group_attn_fwd_kernel<8>, 200 * 1024);
+  smem_attr(group_attn_fwd_kernel<0>, 200 * 1024);
   const int grid = cdiv(T, TT);
   if (K == 2) launch(group_attn_fwd_kernel<2>, grid, 128, smem, st, qkv, T, K, w, ctx, probs);
   else if (K == 4) launch(group_attn_fwd_kernel<4>, grid, 128, smem, st, qkv, T, K, w, ctx, probs);
@@ -1211,14 +937,10 @@ void group_attn_bwd(const float* qkv, const float* probs, const float* dctx, int
                     cudaStream_t st) {
   const int TT = (128 / K) * K;
   const int smem = 4 * (2 * TT * (3 * w + 1) + TT * (w + 1));
-  static int done = 0;
-  if (!done) {
-    cudaFuncSetAttribute(group_attn_bwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(group_attn_bwd_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(group_attn_bwd_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(group_attn_bwd_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    done = 1;
-  }
+  smem_attr(group_attn_bwd_kernel<2>, 220 * 1024);
+  smem_attr(group_attn_bwd_kernel<4>, 220 * 1024);
+  smem_attr(group_attn_bwd_kernel<8>, 220 * 1024);
+  smem_attr(group_attn_bwd_kernel<0>, 220 * 1024);
   const int grid = cdiv(T, TT);
   if (K == 2) launch(group_attn_bwd_kernel<2>, grid, 128, smem, st, qkv, probs, dctx, T, K, w, dqkv);
   else if (K == 4) launch(group_attn_bwd_kernel<4>, grid, 128, smem, st, qkv, probs, dctx, T, K, w, dqkv);
@@ -1322,8 +1044,7 @@ __global__ void attn_fwd_kernel(AttnArgs a) {
 void attn_fwd(const AttnArgs& a, cudaStream_t st) {
   const int dh = a.D / a.heads;
   const int smem = 4 * (a.nq + 2 * kAttnChunk) * (dh + 1);
-  static int done = 0;
-  if (!done) { cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); done = 1; }
+  smem_attr(attn_fwd_kernel, 200 * 1024);
   const int threads = std::min(1024, 32 * std::max(4, (a.nq + 7) / 8));
   launch(attn_fwd_kernel, a.B * a.heads, threads, smem, st, a);
 }
@@ -1427,8 +1148,7 @@ void attn_bwd(const AttnArgs& a, cudaStream_t st) {
   auto smem_for = [&](int c) { return 4 * (3 * a.nq * ldp + 2 * c * ldp + 2 * a.nq * c + 2 * a.nq); };
   while (C > 8 && smem_for(C) > 220 * 1024) C /= 2;
   const int smem = smem_for(C);
-  static int done = 0;
-  if (!done) { cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); done = 1; }
+  smem_attr(attn_bwd_kernel, 220 * 1024);
   launch(attn_bwd_kernel, a.B * a.heads, 256, smem, st, a, C);
 }
 
@@ -1474,6 +1194,26 @@ __global__ void globals_raw_fwd_kernel(GlobalsArgs a) {
       a.raw_bf[(r0 + r) * a.D + c] = __float2bfloat16(v);
     }
   }
+}
+
+__global__ void check_sample_ids_kernel(const int32_t* uid, const int32_t* profile, const int32_t* cand, int B,
+                                        int n_users, int n_profiles, int vocab, int32_t* out, int* status) {
+  pdl_trigger();
+  pdl_wait();
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int u = uid[b], p = profile[b], c = cand ? cand[b] : 0;
+  const bool bu = u < 0 || u >= n_users, bp = p < 0 || p >= n_profiles, bc = c < 0 || c >= vocab;
+  out[b] = bu ? 0 : u;
+  out[B + b] = bp ? 0 : p;
+  out[2 * B + b] = bc ? 0 : c;
+  if (bu || bp || bc) atomicOr(status, 1);
+}
+
+void check_sample_ids(const int32_t* uid, const int32_t* profile, const int32_t* cand, int B, int n_users,
+                      int n_profiles, int vocab, int32_t* out, int* status, cudaStream_t st) {
+  launch(check_sample_ids_kernel, cdiv(B, 128), 128, 0, st, uid, profile, cand, B, n_users, n_profiles, vocab, out,
+         status);
 }
 
 void globals_raw_fwd(const GlobalsArgs& a, cudaStream_t st) {
@@ -1565,16 +1305,8 @@ __global__ void globals_raw_bwd_kernel(GlobalsArgs a, int per_block) {
 void globals_raw_bwd(const GlobalsArgs& a, cudaStream_t st) {
   const int F = a.d_item + a.d_act + a.d_time;
   const int smem = 4 * (a.d * a.D + a.D + (a.m - 2) * a.D + F * a.d + a.d + 3 * 64 + 64);
-  static int done = 0;
-  if (!done) { cudaFuncSetAttribute(globals_raw_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); done = 1; }
-  // samples per block: each block flushes d·D + … partial sums by atomics into the same few
-  // thousand addresses, so fewer, longer blocks contend less (LONGER_GLOB_PER overrides)
-  static int per_env = -1;
-  if (per_env < 0) {
-    const char* e = std::getenv("LONGER_GLOB_PER");
-    per_env = e ? std::max(1, std::atoi(e)) : 0;
-  }
-  const int per = per_env ? per_env : 1;   // one sample per block measured best (2: +6 µs, 8: +70 µs)
+  smem_attr(globals_raw_bwd_kernel, 200 * 1024);
+  constexpr int per = 1;   // samples per block: 1 measured best (2: +6 µs, 8: +70 µs)
   launch(globals_raw_bwd_kernel, cdiv(a.B, per), 256, smem, st, a, per);
 }
 
@@ -1782,7 +1514,8 @@ __global__ void head_fwd_kernel(HeadArgs a) {
       const float sp_pos = fmaxf(z, 0.f) + log1pf(__expf(-fabsf(z)));    // softplus(z)
       const float sp_neg = sp_pos - z;                                   // softplus(-z)
       const float log_p = fmaxf(-sp_neg, kLog12), log_q = fmaxf(-sp_pos, kLog12);
-      a.loss_per[b] = -(y * log_p + (1.f - y) * log_q);
+      // a NaN logit must reach the loss (NumericalError, model.py:563-566): fmaxf drops NaN
+      a.loss_per[b] = !isnan(z) ? -(y * log_p + (1.f - y) * log_q) : __int_as_float(0x7fc00000);
       const bool inr = fabsf(z) < 27.631021115928547f;
       a.dz[b] = inr ? (p - y) / (float)a.B : 0.f;
     }
@@ -1817,8 +1550,7 @@ void head_fwd(const HeadArgs& a, int with_loss, cudaStream_t st) {
   const int smem = 4 * kHeadWarps * (4 * a.D + 2 * a.d);
   const bool stage = smem + head_smem_w1(a) <= kHeadSmemMax;
   if (stage) {
-    static int done = 0;
-    if (!done) { cudaFuncSetAttribute(head_fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHeadSmemMax); done = 1; }
+    smem_attr(head_fwd_kernel<true>, kHeadSmemMax);
     launch(head_fwd_kernel<true>, cdiv(a.B, kHeadWarps), 32 * kHeadWarps, smem + head_smem_w1(a), st, a);
   } else {
     launch(head_fwd_kernel<false>, cdiv(a.B, kHeadWarps), 32 * kHeadWarps, smem, st, a);
@@ -1926,8 +1658,7 @@ void head_bwd(const HeadArgs& a, cudaStream_t st) {
   const int HIN = 4 * a.D + 2 * a.d;
   const int smem = 4 * kHeadWarps * (a.hh + HIN);
   if (smem + head_smem_w1(a) <= kHeadSmemMax) {
-    static int done = 0;
-    if (!done) { cudaFuncSetAttribute(head_bwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHeadSmemMax); done = 1; }
+    smem_attr(head_bwd_kernel<true>, kHeadSmemMax);
     launch(head_bwd_kernel<true>, cdiv(a.B, kHeadWarps), 32 * kHeadWarps, smem + head_smem_w1(a), st, a);
   } else {
     launch(head_bwd_kernel<false>, cdiv(a.B, kHeadWarps), 32 * kHeadWarps, smem, st, a);

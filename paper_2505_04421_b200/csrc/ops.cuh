@@ -144,6 +144,12 @@ struct GlobalsArgs {
   float *g_uid, *g_item, *g_time, *g_cls, *g_tok_w, *g_tok_b, *g_lift_w, *g_lift_b;
 };
 void globals_raw_fwd(const GlobalsArgs& a, cudaStream_t st);
+
+// _checked_ids for the per-sample ids (pkg/src/longrec/inputs.py:406-411): out[0:B) uid,
+// out[B:2B) profile, out[2B:3B) candidate item — each copied, or 0 with status bit 0 set when out
+// of range, so no kernel ever reads outside a table and the call reports EmbeddingLookupError.
+void check_sample_ids(const int32_t* uid, const int32_t* profile, const int32_t* cand, int B, int n_users,
+                      int n_profiles, int vocab, int32_t* out, int* status, cudaStream_t st);
 void globals_raw_bwd(const GlobalsArgs& a, cudaStream_t st);
 
 struct HeadArgs {

@@ -260,8 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1) serve_attn_kernel(ServeAttnArgs a
 template <int DH>
 int launch_serve(const ServeAttnArgs& a, cudaStream_t st) {
   const int smem = (128 * DH + 2 * 128 * DH + 128 * 128) * 2 + 64;
-  static int done = 0;
-  if (!done) { cudaFuncSetAttribute(serve_attn_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); done = 1; }
+  smem_attr(serve_attn_kernel<DH>, 227 * 1024);
   const int tiles = (a.C + 127) / 128;
   launch(serve_attn_kernel<DH>, a.U * tiles * a.heads, kThreads, std::max(smem, 116 * 1024), st, a);
   return (int)cudaGetLastError();

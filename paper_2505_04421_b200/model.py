@@ -16,6 +16,7 @@ import ctypes
 import hashlib
 import json
 import math
+from dataclasses import dataclass, field
 from typing import Optional, Sequence, Union
 
 import numpy as np
@@ -29,6 +30,27 @@ from .params import init_params, param_shapes
 def _torch():
     import torch
     return torch
+
+
+@dataclass
+class ForwardTrace:
+    """Detached copies of every stage of one sample's forward (``ForwardTrace``,
+    pkg/src/longrec/model.py:129-143): ``h`` [L, d] token-MLP output (zero rows for pad events),
+    ``merged`` [G, D], the query indices (-1 for the learnable bank) and grid positions,
+    ``layers`` = the [q, D] output of the cross block and of each self block, ``head_input``
+    [1, 4D + 2d] and ``p``."""
+
+    h: np.ndarray
+    merged: np.ndarray
+    query_indices: np.ndarray
+    query_positions: np.ndarray
+    layers: list = field(default_factory=list)
+    head_input: Optional[np.ndarray] = None
+    p: float = 0.0
+
+    def sequence_branch(self) -> list:
+        """All candidate-independent activations: everything but the target row."""
+        return [self.h, self.merged] + [a[:-1] for a in self.layers]
 
 
 class LongerModel:
@@ -142,7 +164,12 @@ class LongerModel:
 
     # ------------------------------------------------------------------ compute
     def forward(self, batch, sync_check: bool = False):
-        """Probabilities [B] for a batch (``forward_tensor`` + sigmoid, model.py:307-377)."""
+        """Probabilities [B] (a new device tensor) for a batch (``forward_tensor`` + sigmoid,
+        model.py:307-377).  A single ``Sample`` gives ``(p, ForwardTrace)`` like the reference's
+        ``LongRecModel.forward(sample)`` (model.py:365-372)."""
+        if isinstance(batch, Sample):
+            p, traces = self.forward_traces([batch])
+            return float(p[0]), traces[0]
         b = self.to_device_batch(batch)
         B = b.size
         base, nbytes = self._workspace(B)
@@ -154,7 +181,53 @@ class LongerModel:
         _lib.check(rc)
         if sync_check:
             self.read_status(B)
-        return probs
+        return probs.clone()
+
+    def forward_traces(self, batch):
+        """(probabilities [B] as numpy, [ForwardTrace per sample]): the forward with every row of
+        every layer kept (``longer_forward_trace``), copied to the host."""
+        torch = _torch()
+        b = self.to_device_batch(batch)
+        B = b.size
+        base, nbytes = self._workspace(B)
+        probs = self._probs[B]
+        self._fwd_gen = getattr(self, "_fwd_gen", 0) + 1
+        tr = _lib.LongerTrace()
+        _lib.check(self._lib.longer_forward_trace(
+            ctypes.byref(_lib.dims_of(self.cfg, B)), ctypes.c_void_p(self.flat.data_ptr()),
+            ctypes.byref(self._struct(b)), ctypes.c_void_p(base), nbytes, ctypes.c_void_p(probs.data_ptr()),
+            ctypes.byref(tr), self._stream()))
+        self.read_status(B)
+        ws = self._ws[B]
+        cfg = self.cfg
+
+        def view(ptr, shape, dtype=torch.float32):
+            n = int(np.prod(shape))
+            off = int(ptr) - ws.data_ptr()
+            esz = torch.tensor([], dtype=dtype).element_size()
+            return ws[off:off + n * esz].view(dtype).view(*shape).cpu().numpy()
+
+        d, D, Lp, G, q = cfg.d, cfg.D, tr.Lp, tr.G, tr.q
+        h = view(tr.h, (B, Lp, d))[:, Lp - cfg.L:].astype(np.float64)
+        merged = view(tr.merged, (B, G, D)).astype(np.float64)
+        layers = [view(tr.layers[i], (B, q, D)).astype(np.float64) for i in range(tr.n_layers)]
+        head_in = view(tr.head_input, (B, tr.head_width)).astype(np.float64)
+        k, K = cfg.k, cfg.K
+        if cfg.query_strategy == "learnable":
+            qidx = np.full((B, k), -1, np.int64)
+            qpos_seq = np.full((B, k), (G - 1) * K + K - 1, np.int64)
+        else:
+            if tr.query_groups:
+                qidx = view(tr.query_groups, (B, k), torch.int32).astype(np.int64)
+            else:
+                qidx = np.broadcast_to(np.arange(G - k, G, dtype=np.int64), (B, k)).copy()
+            qpos_seq = qidx * K + K - 1
+        qpos = np.concatenate([qpos_seq, np.zeros((B, cfg.m), np.int64)], axis=1)
+        p = probs.cpu().numpy().astype(np.float64)
+        traces = [ForwardTrace(h=h[i], merged=merged[i], query_indices=qidx[i], query_positions=qpos[i],
+                               layers=[a[i] for a in layers], head_input=head_in[i:i + 1], p=float(p[i]))
+                  for i in range(B)]
+        return p, traces
 
     def vjp(self, batch, probs, dprobs):
         """(dprobs/dparams)ᵀ·dprobs into ``grad_flat`` (overwritten) for the batch the most recent
@@ -184,13 +257,18 @@ class LongerModel:
         return LongerFunction.apply(self.autograd_params(), self, b)
 
     def score(self, sample: Sample) -> float:
+        """``LongRecModel.score`` (model.py:374-377)."""
         return float(self.forward([sample], sync_check=True)[0].item())
 
-    def loss_backward(self, batch, check: bool = True):
-        """Train-step body (model.py:555-567): grads ← d(mean BCE)/dparams; returns the loss.
+    def loss_backward(self, batch, check: Union[bool, str] = True):
+        """Train-step body (model.py:555-567): grads ← d(mean BCE)/dparams.
 
-        With ``check`` the loss is read back (one D2H sync) and a non-finite value raises
-        ``NumericalError`` exactly like ``train`` (model.py:563-566)."""
+        ``check=True``: the status flags and the loss come back in one D2H copy and one sync; a
+        non-finite loss raises ``NumericalError`` exactly like ``train`` (model.py:563-566), a bad
+        id ``EmbeddingLookupError``.  Returns the loss as a float.
+        ``check="async"``: the same copy is queued to pinned host memory without a sync and
+        inspected by later calls (``poll_checks``), so an error surfaces one or more steps late;
+        returns the device loss tensor.  ``check=False``: no check, device loss tensor."""
         b = self.to_device_batch(batch)
         B = b.size
         base, nbytes = self._workspace(B)
@@ -203,10 +281,57 @@ class LongerModel:
         _lib.check(rc)
         if not check:
             return self._loss
-        self.read_status(B)
-        value = float(self._loss.item())
-        if not math.isfinite(value):
-            raise NumericalError("non-finite loss")
+        slot = self._queue_check(B)
+        if check == "async":
+            self.poll_checks(block=False)
+            return self._loss
+        return self.poll_checks(block=True, until=slot)
+
+    # ------------------------------------------------------------------ deferred input / loss checks
+    def _queue_check(self, B: int):
+        """[status flags, loss] → a pinned host slot (one D2H each, no sync); status reset."""
+        torch = _torch()
+        if not hasattr(self, "_chk_free"):
+            from collections import deque
+            self._chk_free = [torch.zeros(2, dtype=torch.int32).pin_memory() for _ in range(4)]
+            self._chk_pending = deque()
+        if not self._chk_free:                                 # ring full: retire the oldest
+            self.poll_checks(block=True, until=self._chk_pending[0])
+        host = self._chk_free.pop()
+        base, _ = self._workspace(B)
+        ws = self._ws[B]
+        status = ws[base - ws.data_ptr():base - ws.data_ptr() + 4].view(torch.int32)
+        host[0:1].copy_(status, non_blocking=True)
+        status.zero_()
+        host[1:2].copy_(self._loss.view(torch.int32), non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        slot = (host, ev)
+        self._chk_pending.append(slot)
+        return slot
+
+    def poll_checks(self, block: bool = False, until=None):
+        """Inspect queued checks in order (waiting for them with ``block``, up to ``until``);
+        raises the reference error of the first bad one.  Returns the last inspected loss."""
+        value = None
+        pend = getattr(self, "_chk_pending", None)
+        while pend:
+            host, ev = pend[0]
+            if not block and not ev.query():
+                break
+            ev.synchronize()
+            pend.popleft()
+            flags = int(host[0])
+            value = float(host[1:2].view(_torch().float32)[0])
+            self._chk_free.append(host)
+            if flags & 1:
+                raise EmbeddingLookupError("an id fell outside its embedding table")
+            if flags & 2:
+                raise ConfigError("future event: negative time delta")
+            if not math.isfinite(value):
+                raise NumericalError("non-finite loss")
+            if until is not None and (host, ev) is until:
+                break
         return value
 
     # ------------------------------------------------------------------ checkpoints

@@ -86,6 +86,9 @@ def build_caches_batch(model, batch: Batch, scoring_times: Sequence[int]) -> KVC
     buf = torch.empty(nbytes + 256, dtype=torch.uint8, device=model.device)
     base = (buf.data_ptr() + 255) & ~255
     ws, ws_bytes = model._workspace(U)
+    # the cache build runs a forward in the training workspace of batch size U: any pending
+    # LongerFunction.backward of that workspace must see its activations as gone
+    model._fwd_gen = getattr(model, "_fwd_gen", 0) + 1
     _lib.check(model._lib.longer_cache_build(
         ctypes.byref(_lib.dims_of(model.cfg, U)), ctypes.c_void_p(model.flat.data_ptr()),
         ctypes.byref(model._struct(b)), ctypes.c_void_p(ws), ws_bytes, ctypes.c_void_p(base), nbytes,

@@ -71,8 +71,8 @@ def make_samples(cfg, n_events_list, seed):
         ev = []
         for j in range(n):
             gap = int(rng.integers(30, 900))
-            if i == 1 and j == 0:
-                gap = 2 ** 40          # huge delta → bucket clamp
+            if i == 1 and j == 1:
+                gap = 2 ** 40          # the oldest event lies > 2^40 s before the candidate → bucket clamp
             t += gap
             ev.append(Event(int(rng.integers(cfg["vocab"] if "vocab" in cfg else 200)),
                             int(rng.integers(cfg.get("n_actions", 4))), t))

@@ -66,3 +66,54 @@ def test_shard_bounds_cover_batch():
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
             sizes = [hi - lo for lo, hi in spans]
             assert max(sizes) - min(sizes) <= 1
+
+
+def _product_worker(rank, world, port, B, out_dir, overlap):
+    """The product path: LongerModel.loss_backward on this rank's shard of a CUDA batch, gradients
+    reduced by dp.DataParallel over gloo (CUDA tensors, host-staged: the two ranks share one GPU
+    but never wait on each other's kernels)."""
+    import torch
+    from paper_2505_04421_b200.dp import DataParallel
+    from paper_2505_04421_b200.model import LongerModel
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    cfg = ModelConfig(**GPU_CFG).validate()
+    model = LongerModel(cfg, seed=0, device="cuda:0")
+    batch = synthetic_batch(cfg, B, seed=5, min_events=40)
+    lo, hi = shard_bounds(B, rank, world)
+    dpm = DataParallel(model, overlap=overlap)
+    dpm.loss_backward(shard_batch(batch, rank, world), global_batch=B)
+    torch.cuda.synchronize()
+    if rank == 0:
+        np.save(os.path.join(out_dir, "grad.npy"), model.grad_flat.cpu().numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+GPU_CFG = dict(L=256, d=32, K=4, k=16, N=2, m=3, merge_mode="inner")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("B,overlap", [(8, True), (7, True), (8, False)])
+def test_product_dp_step_matches_single_process(tmp_path, B, overlap):
+    import torch
+    from paper_2505_04421_b200.model import LongerModel
+    world = 2
+    mp.spawn(_product_worker, args=(world, _free_port(), B, str(tmp_path), overlap), nprocs=world, join=True)
+    cfg = ModelConfig(**GPU_CFG).validate()
+    model = LongerModel(cfg, seed=0, device="cuda:0")
+    batch = synthetic_batch(cfg, B, seed=5, min_events=40)
+    model.loss_backward(batch)
+    full = model.grad_flat.cpu().numpy()
+    dp = np.load(tmp_path / "grad.npy")
+    # same kernels on shards: equal up to fp32 summation order and the bf16 rounding of the
+    # shard-mean loss gradient (1/n_r vs 1/N scales round differently): per-group rel-L2 ≤ 1e-2
+    off = 0
+    for name, shape in model.shapes.items():
+        n = int(np.prod(shape))
+        a, b = dp[off:off + n].astype(np.float64), full[off:off + n].astype(np.float64)
+        nb = np.linalg.norm(b)
+        if nb > 1e-6 * np.abs(full).max():
+            assert np.linalg.norm(a - b) <= 1e-2 * nb, (name, np.linalg.norm(a - b) / nb)
+        off += n

@@ -1,0 +1,93 @@
+"""Parity at the benchmarked configuration, and in the kernels' multi-tile modes.
+
+`bench.py` times the train-step body (pkg/src/longrec/model.py:555-567) at c2 with B = 256 per
+GPU.  At that batch every fused front-end CTA walks many 128-token tiles and accumulates its
+weight gradients (token MLP, featuriser one-hots, InnerTrans layer) in TMEM across them, and the
+row-level GEMMs take their 128/256-wide fused-epilogue tiles.  These tests run exactly that call
+(`LongerModel.loss_backward`, through the C ABI) against the float64 oracle:
+
+* c2-inner and c2-concat at B = 256 — the bench batch itself, with full-length and with mixed
+  lengths; the oracle runs in chunks of 32 samples and the batch gradient is the size-weighted
+  mean of the chunk gradients (the loss is a batch mean, model.py:558-562);
+* a small batch with the fused grids capped (LONGER_FE_GRID) so that each CTA takes ≥ 8 tiles,
+  and LONGER_GEMM_MIN_TILES=1 so every GEMM takes its widest tile and fused epilogue.
+
+Stated tolerance: as tests/test_parity_gpu.py (|Δp| ≤ 5e-3; loss within the BCE slope of that;
+per-group gradients rel-L2 ≤ 0.15 and cosine ≥ 0.995, ~0 groups absolute).
+"""
+import numpy as np
+import pytest
+
+from oracle import longer_oracle as O
+from paper_2505_04421_b200 import ModelConfig, synthetic_batch
+from paper_2505_04421_b200.params import init_params
+
+from test_parity_gpu import _model, _run, assert_grads_close, loss_tol
+
+pytestmark = pytest.mark.gpu
+
+C2 = dict(L=2000, d=32, K=4, k=32, N=2, m=3, merge_mode="inner")
+
+
+def oracle_chunked(P, cfg, batch, chunk=32):
+    """p, mean loss and mean gradients of the whole batch, from float64 oracle chunks."""
+    B = batch.size
+    d = batch.as_dict()
+    ps, loss, G = [], 0.0, None
+    for lo in range(0, B, chunk):
+        sub = {k: v[lo:lo + chunk] for k, v in d.items()}
+        n = len(sub["label"])
+        p, l, g = O.forward_backward(P, cfg, sub)
+        ps.append(p)
+        loss += l * n
+        if G is None:
+            G = {k: v * n for k, v in g.items()}
+        else:
+            for k, v in g.items():
+                G[k] += v * n
+    return np.concatenate(ps), loss / B, {k: v / B for k, v in G.items()}
+
+
+def _perturbed(cfg, seed):
+    rng = np.random.default_rng(seed)
+    return {n: a + 0.02 * rng.standard_normal(a.shape) for n, a in init_params(cfg, seed=0).items()}
+
+
+@pytest.mark.parametrize("merge,min_events", [("inner", None), ("concat", None), ("inner", 1)],
+                         ids=["c2-inner", "c2-concat", "c2-inner-mixed"])
+def test_bench_batch_matches_oracle(merge, min_events):
+    cfg = ModelConfig(**dict(C2, merge_mode=merge)).validate()
+    P = _perturbed(cfg, 21)
+    batch = synthetic_batch(cfg, 256, seed=1, min_events=min_events)
+    model = _model(cfg, P)
+    p, loss, grads = _run(model, batch)
+    p_ref, loss_ref, G = oracle_chunked(P, cfg, batch)
+    dp = np.abs(p - p_ref)
+    assert dp.max() <= 5e-3, (dp.max(), int(dp.argmax()))
+    assert abs(loss - loss_ref) <= loss_tol(p_ref, batch.label), (loss, loss_ref)
+    assert_grads_close(grads, G, f"B=256 {merge} min_events={min_events}")
+
+
+@pytest.mark.parametrize("merge", ["inner", "concat"])
+def test_multi_tile_per_cta_matches_oracle(merge, monkeypatch):
+    """Fused grids capped at 3 CTAs (fe_fwd / fe_inner_bwd: ~30 tiles each; fe_mlp_bwd: one CTA
+    per 128-token column block, each walking every sample), every GEMM at its widest tile."""
+    monkeypatch.setenv("LONGER_FE_GRID", "3")
+    monkeypatch.setenv("LONGER_GEMM_MIN_TILES", "1")
+    cfg = ModelConfig(**dict(C2, merge_mode=merge)).validate()
+    P = _perturbed(cfg, 13)
+    batch = synthetic_batch(cfg, 10, seed=5, min_events=1)
+    model = _model(cfg, P)
+    p, loss, grads = _run(model, batch)
+    p_ref, loss_ref, G = O.forward_backward(P, cfg, batch.as_dict())
+    assert np.max(np.abs(p - p_ref)) <= 5e-3
+    assert abs(loss - loss_ref) <= loss_tol(p_ref, batch.label)
+    assert_grads_close(grads, G, f"capped grid {merge}")
+    # the capped and the full grids compute the same step (fp32 accumulation order aside)
+    monkeypatch.delenv("LONGER_FE_GRID")
+    monkeypatch.delenv("LONGER_GEMM_MIN_TILES")
+    p2, loss2, grads2 = _run(model, batch)
+    np.testing.assert_allclose(p2, p, atol=1e-4)
+    for name in grads:
+        scale = np.abs(grads[name]).max() + 1e-12
+        assert np.abs(grads2[name] - grads[name]).max() <= 2e-3 * scale + 1e-7, name
