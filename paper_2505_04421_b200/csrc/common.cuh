@@ -71,16 +71,23 @@ inline Knobs read_knobs() {
 inline thread_local Knobs g_knobs = read_knobs();
 inline void refresh_knobs() { g_knobs = read_knobs(); }
 
-// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the limit is a
-// per-device setting, so a process driving several GPUs raises it on each of them.
+// Raise a kernel's dynamic shared-memory limit to the opt-in maximum (227 KB less its static
+// shared memory), once per (kernel, device): the limit is a per-device setting, so a process
+// driving several GPUs raises it on each.  (`bytes` only documents the launch's need: the limit is
+// not an occupancy hint, and one limit serves every launch shape of the kernel.)
 inline void smem_attr(const void* kernel, int bytes) {
   static std::mutex mu;
   static std::set<std::pair<const void*, int>> done;
+  (void)bytes;
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(mu);
-  if (done.insert({kernel, dev}).second)
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (done.insert({kernel, dev}).second) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, kernel);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024 - static_cast<int>(fa.sharedSizeBytes));
+  }
 }
 template <typename... KArgs>
 inline void smem_attr(void (*kernel)(KArgs...), int bytes) {
@@ -164,6 +171,22 @@ __device__ __forceinline__ float gelu_and_grad(float x, float& grad) {
   const float h = 0.5f * x;
   grad = fmaf(h * fmaf(-t, t, 1.f), fmaf(x2, 3.f * kGeluC * kGeluA, kGeluC), fmaf(0.5f, t, 0.5f));
   return fmaf(h, t, h);
+}
+
+// tanh-GELU of two values in packed f16x2 arithmetic (half the instructions of the fp32 form;
+// f16 keeps 11 significant bits, more than the bf16 operands the result feeds):
+// returns f16x2 {gelu(lo), gelu(hi)}
+__device__ __forceinline__ uint32_t gelu2_f16(float lo, float hi) {
+  uint32_t x, x2, t, u, th, hh, g;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(x) : "f"(hi), "f"(lo));
+  // constants: c = sqrt(2/pi) = 0x3A62, c*a = 0.0356774 = 0x2891, 0.5 = 0x3800 (f16, both halves)
+  asm("mul.rn.f16x2 %0, %1, %1;" : "=r"(x2) : "r"(x));
+  asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(t) : "r"(x2), "r"(0x28912891u), "r"(0x3A623A62u));
+  asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(u) : "r"(x), "r"(t));
+  asm("tanh.approx.f16x2 %0, %1;" : "=r"(th) : "r"(u));
+  asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(hh) : "r"(x), "r"(0x38003800u));
+  asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(g) : "r"(hh), "r"(th), "r"(hh));
+  return g;
 }
 
 __device__ __forceinline__ float warp_sum(float v) {

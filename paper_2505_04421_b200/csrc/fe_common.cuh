@@ -129,6 +129,26 @@ __device__ __forceinline__ void tmem_row(uint32_t taddr, float* out) {
   }
 }
 
+// park a row's N fp32 values in TMEM columns [taddr, taddr + N) (N = 16 or a multiple of 32)
+template <int N>
+__device__ __forceinline__ void tmem_row_st(uint32_t taddr, const float* v) {
+#pragma unroll
+  for (int c = 0; c < N; c += 32) {
+    if (c + 32 <= N) {
+      uint32_t r[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(v[c + j]);
+      sm100::tmem_st32(taddr + c, r);
+    } else {
+      uint32_t r[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(v[c + j]);
+      sm100::tmem_st16(taddr + c, r);
+    }
+  }
+  sm100::tmem_st_wait();
+}
+
 template <int DT>
 __device__ __forceinline__ void ln_row(const float* x, const float* g, const float* b, float* y, float* xhat,
                                        float& inv_out) {

@@ -24,7 +24,7 @@ namespace {
 // ------------------------------------------------------------------ weight packing
 struct PackW {
   int n;
-  struct { long long src; int in, out, trans, n_off, k_off, Kdim, dst; } s[96];
+  struct { long long src; int in, out, trans, n_off, k_off, Kdim, dst, f16; } s[96];
 };
 
 // trans = 1: image of Wᵀ ([out][in]: element (n=j, k=i) = W[i][j]); trans = 0: image of W as
@@ -38,7 +38,8 @@ __global__ void pack_canon_kernel(const float* __restrict__ params, PackW pw, bf
     const int i = e / s.out, j = e % s.out;
     const float v = params[s.src + e];
     const int idx = s.trans ? canon(s.n_off + j, s.k_off + i, s.Kdim) : canon(s.n_off + i, s.k_off + j, s.Kdim);
-    blob[s.dst + idx] = __float2bfloat16(v);
+    if (s.f16) reinterpret_cast<__half*>(blob)[s.dst + idx] = __float2half_rn(v);
+    else blob[s.dst + idx] = __float2bfloat16(v);
   }
 }
 
@@ -142,6 +143,19 @@ __device__ __forceinline__ void kv_store(bf16* skv, int row, const float* kv) {
     *reinterpret_cast<uint4*>(skv + row * 2 * DT + ((ch ^ (row % CPR)) * 8)) = w;
   }
 }
+// one half of the row (k: part 0, v: part 1), DT values
+template <int DT>
+__device__ __forceinline__ void kv_store_part(bf16* skv, int row, int part, const float* x) {
+  constexpr int CPR = 2 * DT / 8;
+#pragma unroll
+  for (int c = 0; c < DT / 8; ++c) {
+    const int ch = part * (DT / 8) + c;
+    uint4 w;
+    w.x = sm100::pack_bf16(x[8 * c], x[8 * c + 1]); w.y = sm100::pack_bf16(x[8 * c + 2], x[8 * c + 3]);
+    w.z = sm100::pack_bf16(x[8 * c + 4], x[8 * c + 5]); w.w = sm100::pack_bf16(x[8 * c + 6], x[8 * c + 7]);
+    *reinterpret_cast<uint4*>(skv + row * 2 * DT + ((ch ^ (row % CPR)) * 8)) = w;
+  }
+}
 template <int DT>
 __device__ __forceinline__ void kv_load8(const bf16* skv, int row, int col, float* out) {
   constexpr int CPR = 2 * DT / 8;
@@ -151,40 +165,105 @@ __device__ __forceinline__ void kv_load8(const bf16* skv, int row, int col, floa
 }
 
 // ------------------------------------------------------------------ forward kernel
+// S independent token tiles ("slots") in flight per CTA, one CTA per SM.  Slot s owns an MMA
+// issuer warp (warp s, one thread), four worker warps S+4s … S+4s+3 (one per TMEM lane quadrant:
+// thread = token row), TMEM columns [128s, 128s+128), an A tile and a hidden / k|v tile in shared
+// memory, and a barrier pair: bar_a[s] (its 128 rows have written the next operand) and bar_d[s]
+// (its MMAs are done).  Each slot alternates strictly — workers signal stage k, the issuer issues
+// stage k and commits, workers wait — so a barrier never completes twice before its waiter consumed
+// the phase; each issuer sleeps on its own barrier and its commits track only its own MMAs, so the
+// slots never wait for each other.  While one slot's rows run GELU / LayerNorm / group attention,
+// the tensor core works for another and the SIMT pipes always have 4S independent warps of work.
+// The weights are loaded once per CTA and shared by all slots.
+//
+// Per tile (TMEM columns relative to the slot base): [feat|1]·[W_tp;b] → X [0,32);
+// [x0|1]·[W1;b1] in 64-column parts → A [0,64), GELU (f16x2) → H, H·W2 (f16) accumulates h in
+// [64,96); per InnerTrans layer: [LN1|1]·[Wqkv;b] → [0,96), group attention → ctx, ctx·Wo →
+// [0,32), [LN2|1]·[W1;b1] parts → [0,64), GELU → H, H·W2 (f16) → [64,96).
+constexpr int kSlotCols = 128;
+
 template <int DT, int KG>
-__global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
+struct FwdPlan {
+  static constexpr int D = DT * KG, H2 = 2 * D, nh = H2 / 64, nf = 4 * DT / 64, XK = DT + 16;
+  static __host__ __device__ int stages(int IL) { return 2 + nh + IL * (3 + nf); }
+};
+
+template <int DT, int KG>
+__device__ __forceinline__ void fwd_issue(int st, uint32_t t0, uint32_t wA, uint32_t wH, uint32_t wW,
+                                          const BlobOff& bo) {
+  using P = FwdPlan<DT, KG>;
+  constexpr int XK = P::XK, nh = P::nh, nf = P::nf, H2 = P::H2;
+  auto W = [&](int off, int kdim) { return Opnd{wW + off * 2, kdim, 0}; };
+  auto w2mma = [&](uint32_t d, int off, int kdim, bool acc) {       // H (f16) · W2 image (f16)
+    const uint32_t idesc = sm100::make_idesc_f16(128, DT, 0, 0);
+    const Opnd A{wH, 64, 0}, B = W(off, kdim);
+    for (int ks = 0; ks < 4; ++ks) sm100::mma_bf16(d, A.desc(ks), B.desc(ks), idesc, (acc || ks > 0) ? 1u : 0u);
+  };
+  if (st == 0) { mma(t0, Opnd{wA, kFP, 0}, W(bo.tp, kFP), kFP / 16, DT, false); return; }
+  if (st == 1) { mma(t0, Opnd{wA, XK, 0}, W(bo.w1, XK), XK / 16, 64, false); return; }
+  st -= 2;
+  if (st < nh) {
+    w2mma(t0 + 64, bo.w2 + canon(0, 64 * st, H2), H2, st > 0);
+    if (st + 1 < nh) mma(t0, Opnd{wA, XK, 0}, W(bo.w1 + canon(64 * (st + 1), 0, XK), XK), XK / 16, 64, false);
+    return;
+  }
+  st -= nh;
+  const int l = st / (3 + nf), r = st % (3 + nf);
+  if (r == 0) { mma(t0, Opnd{wA, XK, 0}, W(bo.qkv[l], XK), XK / 16, 3 * DT, false); return; }
+  if (r == 1) { mma(t0, Opnd{wA, XK, 0}, W(bo.wo[l], DT), DT / 16, DT, false); return; }
+  if (r == 2) { mma(t0, Opnd{wA, XK, 0}, W(bo.w1i[l], XK), XK / 16, 64, false); return; }
+  const int j = r - 3;
+  w2mma(t0 + 64, bo.w2i[l] + canon(0, 64 * j, 4 * DT), 4 * DT, j > 0);
+  if (j + 1 < nf) mma(t0, Opnd{wA, XK, 0}, W(bo.w1i[l] + canon(64 * (j + 1), 0, XK), XK), XK / 16, 64, false);
+}
+
+// 32 fp32 values of a row → GELU in f16 → 4 × 16-byte stores into a canonical f16 tile
+__device__ __forceinline__ void gelu_store_f16(bf16* tile, int row, int kdim, int k0, const float* v) {
+#pragma unroll
+  for (int c = 0; c < 32; c += 8) {
+    uint4 w;
+    w.x = gelu2_f16(v[c], v[c + 1]); w.y = gelu2_f16(v[c + 2], v[c + 3]);
+    w.z = gelu2_f16(v[c + 4], v[c + 5]); w.w = gelu2_f16(v[c + 6], v[c + 7]);
+    *reinterpret_cast<uint4*>(tile + canon(row, k0 + c, kdim)) = w;
+  }
+}
+
+// [· | 1 | 0 …] bias column block of an XK-wide operand row (columns DT … DT+15)
+template <int DT>
+__device__ __forceinline__ void store_ones_col(bf16* tile, int row) {
+  constexpr int XK = DT + 16;
+  *reinterpret_cast<uint4*>(tile + canon(row, DT, XK)) = make_uint4(0x3F80u, 0u, 0u, 0u);
+  *reinterpret_cast<uint4*>(tile + canon(row, DT + 8, XK)) = make_uint4(0u, 0u, 0u, 0u);
+}
+
+template <int DT, int KG, int S>
+__global__ void __launch_bounds__(32 * 5 * S, 1) fe_fwd_kernel(FrontArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  constexpr int D = DT * KG;
-  constexpr int H2 = 2 * D;                        // token-MLP hidden width
-  constexpr int nh = H2 / 64;                      // 64-column parts of the hidden
-  constexpr int nf = 4 * DT / 64;                  // 64-column parts of the InnerTrans FFN hidden
-  constexpr int XK = DT + 16;                      // activation tile row: [x | 1 | 0…] (bias column)
+  using P = FwdPlan<DT, KG>;
+  constexpr int D = P::D, nh = P::nh, nf = P::nf, XK = P::XK;
   const BlobOff bo = blob_offsets(DT, D, a.inner_layers);
   bf16* sW = reinterpret_cast<bf16*>(smem_raw);
-  bf16* sA = sW + ((bo.fwd_total + 63) & ~63);             // 128 x XK bf16 (feat uses 128 x 32)
-  bf16* sH = sA + kTile * XK;                              // 128 x 64 bf16 hidden part (also k|v scratch)
-  bf16* sKV = sH;                                          // 128 x 2DT bf16, 16-byte chunks XOR-swizzled
-  float* s_par = reinterpret_cast<float*>(sH + kTile * 64);   // [IL][ln1_g, ln1_b, b_o, ln2_g, ln2_b, b2][DT]
-  float* s_kn = s_par + a.inner_layers * 6 * DT;              // cross LN1 [gain | bias] (2D) for the kn epilogue
+  bf16* sA0 = sW + ((bo.fwd_total + 63) & ~63);               // S x [128 x XK] bf16 (feat: 128 x 32)
+  bf16* sH0 = sA0 + S * kTile * XK;                           // S x [128 x 64] f16 hidden / bf16 k|v
+  float* s_par = reinterpret_cast<float*>(sH0 + S * kTile * 64);   // [IL][ln1_g, ln1_b, b_o, ln2_g, ln2_b, b2]
+  float* s_b2 = s_par + a.inner_layers * 6 * DT;              // token-MLP output bias [DT]
+  float* s_kn = s_b2 + DT;                                    // cross LN1 [gain | bias] (2D)
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_kn + 2 * D);
   uint64_t* bar_w = bars;
-  uint64_t* bar_a = bars + 1;
-  uint64_t* bar_d = bars + 2;
-  uint64_t* bar_p = bars + 3;                              // [2] MMA → workers: a1 part in TMEM buffer 0 / 1
-  uint64_t* bar_h = bars + 5;                              // MMA → workers: a W2 part has consumed sH
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6);
+  uint64_t* bar_a = bars + 1;                                 // [S]
+  uint64_t* bar_d = bars + 1 + S;                             // [S]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 1 + 2 * S);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     sm100::mbar_init(bar_w, 1);
-    sm100::mbar_init(bar_a, 32 * kWorkers);
-    sm100::mbar_init(bar_d, 1);
-    sm100::mbar_init(&bar_p[0], 1);
-    sm100::mbar_init(&bar_p[1], 1);
-    sm100::mbar_init(bar_h, 1);
+    for (int s = 0; s < S; ++s) {
+      sm100::mbar_init(&bar_a[s], 128);
+      sm100::mbar_init(&bar_d[s], 1);
+    }
     sm100::fence_barrier_init();
   }
-  if (warp == 0) sm100::tmem_alloc<256>(tmem_slot);
+  if (warp == 0) sm100::tmem_alloc<512>(tmem_slot);
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
@@ -197,209 +276,182 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
                      : v == 3 ? a.inner_ln[l][2] : v == 4 ? a.inner_ln[l][3] : a.inner_bias[l][5];
     s_par[i] = src[c];
   }
+  for (int i = threadIdx.x; i < DT; i += blockDim.x) s_b2[i] = a.seq_b2[i];
   if (a.kn)
     for (int i = threadIdx.x; i < 2 * D; i += blockDim.x) s_kn[i] = i < D ? a.kn_g[i] : a.kn_b[i - D];
   __syncthreads();
   const long long ntiles = (a.T + kTile - 1) / kTile;
+  const long long stride = (long long)gridDim.x * S;
 
-  if (warp == 0) {
+  if (warp < S) {
     if (lane == 0) {
-      // ---------------- MMA issuer
-      sm100::mbar_arrive_expect_tx(bar_w, bo.fwd_total * 2);
-      load_blob(reinterpret_cast<uint8_t*>(sW), reinterpret_cast<const uint8_t*>(a.wblob), bo.fwd_total * 2, bar_w);
+      // ---------------- MMA issuer of slot s = warp: sleeps on its slot's operand barrier, issues
+      // the stage, commits (a commit tracks only this thread's MMAs: slots never wait for each other)
+      const int s = warp;
+      if (s == 0) {
+        sm100::mbar_arrive_expect_tx(bar_w, bo.fwd_total * 2);
+        load_blob(reinterpret_cast<uint8_t*>(sW), reinterpret_cast<const uint8_t*>(a.wblob), bo.fwd_total * 2,
+                  bar_w);
+      }
       sm100::mbar_wait(bar_w, 0);
-      const uint32_t wA = sm100::smem_u32(sA), wH = sm100::smem_u32(sH), wW = sm100::smem_u32(sW);
+      const int NS = P::stages(a.inner_layers);
+      const uint32_t wW = sm100::smem_u32(sW), wA = sm100::smem_u32(sA0 + s * kTile * XK);
+      const uint32_t wH = sm100::smem_u32(sH0 + s * kTile * 64), t0 = tmem + s * kSlotCols;
       uint32_t pa = 0;
-      auto wait_a = [&]() { sm100::mbar_wait(bar_a, pa); pa ^= 1; sm100::tc_fence_after(); };
-      auto W = [&](int off, int kdim) { return Opnd{wW + off * 2, kdim, 0}; };
-      const uint32_t accH = tmem + 128;          // h / f2 accumulator columns
-      for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        wait_a();                                // [feat | 1]
-        mma(tmem, Opnd{wA, kFP, 0}, W(bo.tp, kFP), kFP / 16, DT, false);
-        sm100::mma_commit(bar_d);
-        // token MLP: a1 parts run two ahead of the workers in TMEM columns [0,64) / [64,128), each
-        // buffer with its own barrier.  A buffer's next commit needs every worker's signal of the
-        // part after the one it waited for, so no barrier completes twice before a worker's wait
-        // (parity aliasing would hang); W2 parts commit to bar_h the same way.
-        wait_a();                                // [x0 | 1]
-        mma(tmem, Opnd{wA, XK, 0}, W(bo.w1, XK), XK / 16, 64, false);
-        sm100::mma_commit(&bar_p[0]);
-        if (nh > 1) {
-          mma(tmem + 64, Opnd{wA, XK, 0}, W(bo.w1 + canon(64, 0, XK), XK), XK / 16, 64, false);
-          sm100::mma_commit(&bar_p[1]);
-        }
-        for (int j = 0; j < nh; ++j) {
-          wait_a();                              // GELU(a1 part j) in sH
-          mma(accH, Opnd{wH, 64, 0}, W(bo.w2 + canon(0, 64 * j, H2), H2), 4, DT, j > 0);
-          sm100::mma_commit(bar_h);
-          if (j + 2 < nh) {
-            mma(tmem + 64 * (j & 1), Opnd{wA, XK, 0}, W(bo.w1 + canon(64 * (j + 2), 0, XK), XK), XK / 16, 64, false);
-            sm100::mma_commit(&bar_p[j & 1]);
-          }
-        }
-        for (int l = 0; l < a.inner_layers; ++l) {
-          wait_a();                              // [LN1(x) | 1]
-          mma(tmem, Opnd{wA, XK, 0}, W(bo.qkv[l], XK), XK / 16, 3 * DT, false);
-          sm100::mma_commit(bar_d);
-          wait_a();                              // ctx
-          mma(tmem, Opnd{wA, XK, 0}, W(bo.wo[l], DT), DT / 16, DT, false);
-          sm100::mma_commit(bar_d);
-          wait_a();                              // [LN2(x1) | 1]
-          mma(tmem, Opnd{wA, XK, 0}, W(bo.w1i[l], XK), XK / 16, 64, false);
-          sm100::mma_commit(bar_d);
-          for (int j = 0; j < nf; ++j) {
-            wait_a();                            // GELU(f1 part j) in sH
-            mma(accH, Opnd{wH, 64, 0}, W(bo.w2i[l] + canon(0, 64 * j, 4 * DT), 4 * DT), 4, DT, j > 0);
-            if (j + 1 < nf) mma(tmem, Opnd{wA, XK, 0}, W(bo.w1i[l] + canon(64 * (j + 1), 0, XK), XK), XK / 16, 64, false);
-            sm100::mma_commit(bar_d);
-          }
+      for (long long tile = (long long)blockIdx.x * S + s; tile < ntiles; tile += stride) {
+        for (int st = 0; st < NS; ++st) {
+          sm100::mbar_wait(&bar_a[s], pa);
+          pa ^= 1;
+          sm100::tc_fence_after();
+          fwd_issue<DT, KG>(st, t0, wA, wH, wW, bo);
+          sm100::mma_commit(&bar_d[s]);
         }
       }
     }
   } else {
-    // ---------------- workers: one token row per thread
+    // ---------------- workers: slot s, one token row per thread
+    const int s = (warp - S) >> 2;
     const int q = warp & 3;
     const int row = q * 32 + lane;
-    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+    const uint32_t trow = tmem + s * kSlotCols + ((uint32_t)(q * 32) << 16);
+    bf16* sA = sA0 + s * kTile * XK;
+    bf16* sH = sH0 + s * kTile * 64;
+    bf16* sKV = sH;                                  // 128 x 2DT bf16, 16-byte chunks XOR-swizzled
     const float scale_in = rsqrtf((float)DT);
     uint32_t pd = 0;
-    auto signal = [&]() { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(bar_a); };
-    auto wait_d = [&]() { sm100::mbar_wait(bar_d, pd); pd ^= 1; sm100::tc_fence_after(); };
-    uint32_t pp0 = 0, pp1 = 0, ph = 0;
-    auto wait_p = [&](int buf) {
-      if (buf) { sm100::mbar_wait(&bar_p[1], pp1); pp1 ^= 1; } else { sm100::mbar_wait(&bar_p[0], pp0); pp0 ^= 1; }
-      sm100::tc_fence_after();
-    };
-    auto wait_h = [&]() { sm100::mbar_wait(bar_h, ph); ph ^= 1; sm100::tc_fence_after(); };
-    float b2[DT];                                  // narrow biases live in registers
-#pragma unroll
-    for (int c = 0; c < DT; ++c) b2[c] = __ldg(a.seq_b2 + c);
-    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    auto signal = [&]() { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(&bar_a[s]); };
+    auto wait_d = [&]() { sm100::mbar_wait(&bar_d[s], pd); pd ^= 1; sm100::tc_fence_after(); };
+    for (long long tile = (long long)blockIdx.x * S + s; tile < ntiles; tile += stride) {
       const TokenInfo ti = token_info(a, tile, row);
       if (ti.in_range && ti.j == 0 && a.npg) a.npg[ti.b] = (a.Lp - ti.n) / a.K;
       if (ti.in_range && a.real_out) {
         a.real_out[ti.t] = ti.real ? 1.f : 0.f;
         a.keep_out[ti.t] = ti.keep ? 1.f : 0.f;
       }
-      float v[kFP];
-      int ids[3];
-      featurise(a, ti, v, ids, true);
-      v[kFP - 1] = 1.f;                            // bias column (b_tp rides in the W_tp image)
-      store_row(sA, row, kFP, v, kFP);
-      signal();
-      // abs-pos row: issued before waiting for the MMA so the gather overlaps it
-      float x[XK];
       {
+        float v[kFP];
+        int ids[3];
+        featurise(a, ti, v, ids, true);
+        v[kFP - 1] = 1.f;                          // bias column (b_tp rides in the W_tp image)
+        store_row(sA, row, kFP, v, kFP);
+      }
+      signal();
+      float h[DT];
+      {
+        // abs-pos row: gathered while the MMA runs
         const float4* pp = reinterpret_cast<const float4*>(a.pos_tab + (long long)ti.rec * DT);
 #pragma unroll
         for (int c = 0; c < DT; c += 4) {
           const float4 p4 = __ldg(pp + c / 4);
-          x[c] = p4.x; x[c + 1] = p4.y; x[c + 2] = p4.z; x[c + 3] = p4.w;
+          h[c] = p4.x; h[c + 1] = p4.y; h[c + 2] = p4.z; h[c + 3] = p4.w;
         }
-      }
-      // x0 = [feat | 1]·[W_tp ; b_tp] + abs_pos[recency]
-      wait_d();
-      {
+        // x0 = [feat | 1]·[W_tp ; b_tp] + abs_pos[recency]
+        wait_d();
         float acc[DT];
         tmem_row<DT>(trow, acc);
 #pragma unroll
-        for (int c = 0; c < DT; ++c) x[c] = ti.real ? x[c] + acc[c] : 0.f;
+        for (int c = 0; c < DT; ++c) h[c] = ti.real ? h[c] + acc[c] : 0.f;
+        store_row(sA, row, XK, h, DT);
+        store_ones_col<DT>(sA, row);
       }
-#pragma unroll
-      for (int c = DT; c < XK; ++c) x[c] = c == DT ? 1.f : 0.f;
-      store_row(sA, row, XK, x, XK);
       signal();
-      // token MLP: GELU([x0 | 1]·[W1 ; b1]) (64-column parts → sH) · W2 accumulates in TMEM
+      // token MLP: GELU([x0 | 1]·[W1 ; b1]) in 64-column parts (f16) · W2 accumulates in TMEM
       for (int hj = 0; hj < nh; ++hj) {
-        wait_p(hj & 1);                          // a1 part hj
-        if (hj > 0) wait_h();                    // W2 of the previous part has read sH
+        wait_d();
 #pragma unroll
         for (int c0 = 0; c0 < 64; c0 += 32) {
           float hv[32];
-          tmem_row<32>(trow + 64 * (hj & 1) + c0, hv);
-#pragma unroll
-          for (int u = 0; u < 32; ++u) hv[u] = gelu_f(hv[u]);
-          store_row(sH, row, 64, hv, 32, c0);
+          tmem_row<32>(trow + c0, hv);
+          gelu_store_f16(sH, row, 64, c0, hv);
         }
         signal();
       }
-      wait_h();
-      float h[DT];
-      tmem_row<DT>(trow + 128, h);
+      wait_d();
+      tmem_row<DT>(trow + 64, h);
 #pragma unroll
-      for (int c = 0; c < DT; ++c) h[c] = ti.real ? h[c] + b2[c] : 0.f;
+      for (int c = 0; c < DT; ++c) h[c] = ti.real ? h[c] + s_b2[c] : 0.f;
       if (a.h_out && ti.in_range) {
         float4* dst = reinterpret_cast<float4*>(a.h_out + ti.t * DT);
 #pragma unroll
         for (int c = 0; c < DT; c += 4) dst[c / 4] = make_float4(h[c], h[c + 1], h[c + 2], h[c + 3]);
       }
+      // the residual stream h is parked in the slot's TMEM columns [96, 128) while the attention
+      // and FFN stages run (registers: 4S warps share the SM)
+      const uint32_t tres = trow + 96;
       for (int l = 0; l < a.inner_layers; ++l) {
         const float* par = s_par + l * 6 * DT;
-        float xn[XK], inv;
-        ln_row_s<DT>(h, par, par + DT, xn, inv);
-#pragma unroll
-        for (int c = DT; c < XK; ++c) xn[c] = c == DT ? 1.f : 0.f;
-        store_row(sA, row, XK, xn, XK);
-        signal();
-        wait_d();
-        float qv[DT];
-        tmem_row<DT>(trow, qv);                    // q, k, v already carry their biases
         {
-          float kv[2 * DT];
-          tmem_row<DT>(trow + DT, kv);
-          tmem_row<DT>(trow + 2 * DT, kv + DT);
-          kv_store<DT>(sKV, row, kv);
+          float xn[DT], inv;
+          ln_row_s<DT>(h, par, par + DT, xn, inv);
+          store_row(sA, row, XK, xn, DT);
+          store_ones_col<DT>(sA, row);
         }
-        __syncwarp();
-        const int g0 = row - row % KG;
-        float s[KG];
-        float mx = -INFINITY;
-#pragma unroll
-        for (int jj = 0; jj < KG; ++jj) {
-          float acc = 0.f;
-#pragma unroll
-          for (int c = 0; c < DT; c += 8) {
-            float kk[8];
-            kv_load8<DT>(sKV, g0 + jj, c, kk);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) acc = fmaf(qv[c + u], kk[u], acc);
-          }
-          s[jj] = acc * scale_in;
-          mx = fmaxf(mx, s[jj]);
-        }
-        float tot = 0.f;
-#pragma unroll
-        for (int jj = 0; jj < KG; ++jj) { s[jj] = __expf(s[jj] - mx); tot += s[jj]; }
-        const float rinv = 1.f / tot;
-        float ctx[XK];
-#pragma unroll
-        for (int c = 0; c < DT; ++c) ctx[c] = 0.f;
-#pragma unroll
-        for (int jj = 0; jj < KG; ++jj) {
-#pragma unroll
-          for (int c = 0; c < DT; c += 8) {
-            float vv[8];
-            kv_load8<DT>(sKV, g0 + jj, DT + c, vv);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) ctx[c + u] = fmaf(s[jj], vv[u], ctx[c + u]);
-          }
-        }
-#pragma unroll
-        for (int c = 0; c < DT; ++c) ctx[c] *= rinv;
-#pragma unroll
-        for (int c = DT; c < XK; ++c) ctx[c] = 0.f;
-        __syncwarp();
-        store_row(sA, row, XK, ctx, XK);
+        tmem_row_st<DT>(tres, h);
         signal();
         wait_d();
-        float o[DT];
-        tmem_row<DT>(trow, o);
+        float ctx[DT];
+        {
+          float kv[DT];                              // q, k, v already carry their biases
+          tmem_row<DT>(trow + DT, kv);
+          kv_store_part<DT>(sKV, row, 0, kv);
+          tmem_row<DT>(trow + 2 * DT, kv);
+          kv_store_part<DT>(sKV, row, 1, kv);
+        }
+        __syncwarp();
+        {
+          float qv[DT];
+          tmem_row<DT>(trow, qv);
+          const int g0 = row - row % KG;
+          float sc[KG];
+          float mx = -INFINITY;
 #pragma unroll
-        for (int c = 0; c < DT; ++c) h[c] += o[c] + par[2 * DT + c];      // x1
-        ln_row_s<DT>(h, par + 3 * DT, par + 4 * DT, xn, inv);
+          for (int jj = 0; jj < KG; ++jj) {
+            float acc = 0.f;
 #pragma unroll
-        for (int c = DT; c < XK; ++c) xn[c] = c == DT ? 1.f : 0.f;
-        store_row(sA, row, XK, xn, XK);
+            for (int c = 0; c < DT; c += 8) {
+              float kk[8];
+              kv_load8<DT>(sKV, g0 + jj, c, kk);
+#pragma unroll
+              for (int u = 0; u < 8; ++u) acc = fmaf(qv[c + u], kk[u], acc);
+            }
+            sc[jj] = acc * scale_in;
+            mx = fmaxf(mx, sc[jj]);
+          }
+          float tot = 0.f;
+#pragma unroll
+          for (int jj = 0; jj < KG; ++jj) { sc[jj] = __expf(sc[jj] - mx); tot += sc[jj]; }
+          const float rinv = 1.f / tot;
+#pragma unroll
+          for (int c = 0; c < DT; ++c) ctx[c] = 0.f;
+#pragma unroll
+          for (int jj = 0; jj < KG; ++jj) {
+            const float pj = sc[jj] * rinv;
+#pragma unroll
+            for (int c = 0; c < DT; c += 8) {
+              float vv[8];
+              kv_load8<DT>(sKV, g0 + jj, DT + c, vv);
+#pragma unroll
+              for (int u = 0; u < 8; ++u) ctx[c + u] = fmaf(pj, vv[u], ctx[c + u]);
+            }
+          }
+        }
+        __syncwarp();
+        store_row(sA, row, XK, ctx, DT);
+        store_ones_col<DT>(sA, row);                   // Woᵀ has K = DT: the ones column is unread
+        signal();
+        wait_d();
+        {
+          float o[DT];
+          tmem_row<DT>(trow, o);
+          tmem_row<DT>(tres, h);
+#pragma unroll
+          for (int c = 0; c < DT; ++c) h[c] += o[c] + par[2 * DT + c];      // x1
+          float xn[DT], inv;
+          ln_row_s<DT>(h, par + 3 * DT, par + 4 * DT, xn, inv);
+          store_row(sA, row, XK, xn, DT);
+          store_ones_col<DT>(sA, row);
+          tmem_row_st<DT>(tres, h);
+        }
         signal();
         for (int fj = 0; fj < nf; ++fj) {
           wait_d();
@@ -407,16 +459,18 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
           for (int c0 = 0; c0 < 64; c0 += 32) {
             float hv[32];
             tmem_row<32>(trow + c0, hv);
-#pragma unroll
-            for (int u = 0; u < 32; ++u) hv[u] = gelu_f(hv[u]);
-            store_row(sH, row, 64, hv, 32, c0);
+            gelu_store_f16(sH, row, 64, c0, hv);
           }
           signal();
         }
         wait_d();
-        tmem_row<DT>(trow + 128, o);
+        {
+          float o[DT];
+          tmem_row<DT>(trow + 64, o);
+          tmem_row<DT>(tres, h);
 #pragma unroll
-        for (int c = 0; c < DT; ++c) h[c] += o[c] + par[5 * DT + c];      // x2
+          for (int c = 0; c < DT; ++c) h[c] += o[c] + par[5 * DT + c];      // x2
+        }
       }
       if (a.inner_layers > 0 && !ti.keep) {
 #pragma unroll
@@ -468,7 +522,7 @@ __global__ void __launch_bounds__(kThreads, 2) fe_fwd_kernel(FrontArgs a) {
   }
   sm100::tc_fence_before();
   __syncthreads();
-  if (warp == 0) sm100::tmem_dealloc<256>(tmem);
+  if (warp == 0) sm100::tmem_dealloc<512>(tmem);
 }
 
 // ------------------------------------------------------------------ token-MLP + featuriser backward
@@ -851,9 +905,10 @@ void pack_frontend_weights(const float* params, long long tok_w, long long seq_w
   cudaMemsetAsync(blob, 0, (size_t)o.total * 2, st);
   PackW pw;
   pw.n = 0;
-  auto add = [&](long long src, int in, int out, int trans, int n_off, int k_off, int Kdim, int dst) {
+  auto add = [&](long long src, int in, int out, int trans, int n_off, int k_off, int Kdim, int dst, int f16 = 0) {
     auto& s = pw.s[pw.n++];
     s.src = src; s.in = in; s.out = out; s.trans = trans; s.n_off = n_off; s.k_off = k_off; s.Kdim = Kdim; s.dst = dst;
+    s.f16 = f16;
   };
   // forward images (Wᵀ, K = in)
   const int XK = d + 16;
@@ -862,7 +917,7 @@ void pack_frontend_weights(const float* params, long long tok_w, long long seq_w
   add(tok_w + (long long)F * d, 1, d, 1, 0, kFP - 1, kFP, o.tp);            // b_tp at k = 31
   add(seq_w1, d, 2 * D, 1, 0, 0, XK, o.w1);
   add(seq_w1 + (long long)d * 2 * D, 1, 2 * D, 1, 0, d, XK, o.w1);          // b1 at k = d
-  add(seq_w2, 2 * D, d, 1, 0, 0, 2 * D, o.w2);
+  add(seq_w2, 2 * D, d, 1, 0, 0, 2 * D, o.w2, 1);                           // f16: GELU output operand
   // backward images (W, K = out)
   add(tok_w, F, d, 0, 0, 0, d, o.tp_n);
   add(seq_w1, d, 2 * D, 0, 0, 0, 2 * D, o.w1_n);
@@ -879,7 +934,7 @@ void pack_frontend_weights(const float* params, long long tok_w, long long seq_w
     add(wo, d, d, 1, 0, 0, d, o.wo[l]);
     add(w1, d, 4 * d, 1, 0, 0, XK, o.w1i[l]);
     add(w1 + 4LL * d * d, 1, 4 * d, 1, 0, d, XK, o.w1i[l]);                  // b1 at k = d
-    add(w2, 4 * d, d, 1, 0, 0, 4 * d, o.w2i[l]);
+    add(w2, 4 * d, d, 1, 0, 0, 4 * d, o.w2i[l], 1);                         // f16: GELU output operand
     add(wq, d, d, 0, 0, 0, 3 * d, o.qkv_n[l]);
     add(wk, d, d, 0, 0, d, 3 * d, o.qkv_n[l]);
     add(wv, d, d, 0, 0, 2 * d, 3 * d, o.qkv_n[l]);
@@ -890,18 +945,32 @@ void pack_frontend_weights(const float* params, long long tok_w, long long seq_w
   launch(pack_canon_kernel, dim3(16, pw.n), 256, 0, st, params, pw, blob);
 }
 
+template <int DT, int KG, int S>
+static int fwd_smem(const FrontArgs& a) {
+  const BlobOff bo = blob_offsets(DT, DT * KG, a.inner_layers);
+  return ((bo.fwd_total + 63) & ~63) * 2 + S * kTile * (DT + 16 + 64) * 2 +
+         (a.inner_layers * 6 * DT + DT + 2 * DT * KG) * 4 + (1 + 2 * S) * 8 + 16;
+}
+
+template <int DT, int KG, int S>
+static int launch_fwd_s(const FrontArgs& a, cudaStream_t st) {
+  const int smem = fwd_smem<DT, KG, S>(a);
+  smem_attr(fe_fwd_kernel<DT, KG, S>, smem);
+  const long long ntiles = (a.T + kTile - 1) / kTile;
+  int grid = (int)std::min<long long>((ntiles + S - 1) / S, 148);
+  if (g_knobs.fe_grid > 0) grid = std::min(grid, g_knobs.fe_grid);   // testing: many tiles per CTA
+  launch(fe_fwd_kernel<DT, KG, S>, grid, 32 * 5 * S, smem, st, a);
+  return (int)cudaGetLastError();
+}
+
+// as many slots as the weights leave shared memory for (4 at d = 32, D = 128; 3 at D = 256)
 template <int DT, int KG>
 static int launch_fwd(const FrontArgs& a, cudaStream_t st) {
-  const BlobOff bo = blob_offsets(DT, DT * KG, a.inner_layers);
-  const int smem = ((bo.fwd_total + 63) & ~63) * 2 + kTile * std::max(DT + 16, kFP) * 2 + kTile * 64 * 2 +
-                   a.inner_layers * 6 * DT * 4 + 2 * DT * KG * 4 + 64;
-  smem_attr(fe_fwd_kernel<DT, KG>, 227 * 1024);
-  const long long ntiles = (a.T + kTile - 1) / kTile;
-  const int per_sm = smem <= 113 * 1024 ? 2 : 1;
-  int grid = (int)std::min<long long>(ntiles, per_sm * 148);
-  if (g_knobs.fe_grid > 0) grid = std::min(grid, g_knobs.fe_grid);   // testing: many tiles per CTA
-  launch(fe_fwd_kernel<DT, KG>, grid, kThreads, smem, st, a);
-  return (int)cudaGetLastError();
+  constexpr int kMax = 227 * 1024;
+  if (fwd_smem<DT, KG, 4>(a) <= kMax) return launch_fwd_s<DT, KG, 4>(a, st);
+  if (fwd_smem<DT, KG, 3>(a) <= kMax) return launch_fwd_s<DT, KG, 3>(a, st);
+  if (fwd_smem<DT, KG, 2>(a) <= kMax) return launch_fwd_s<DT, KG, 2>(a, st);
+  return (int)cudaErrorInvalidValue;
 }
 
 int frontend_fwd(const FrontArgs& a, cudaStream_t st) {
