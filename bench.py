@@ -36,6 +36,7 @@ CONFIGS = {
     "c2_concat": dict(L=2000, d=32, K=4, k=32, N=2, m=3, merge_mode="concat"),
     "c1": dict(L=256, d=16, K=4, k=16, N=1, m=3),
     "c5_inner": dict(L=10000, d=32, K=8, k=32, N=4, m=3, merge_mode="inner"),
+    "c4": dict(L=2000, d=32, K=4, k=32, N=2, m=3, merge_mode="inner"),   # serving on c2 weights
 }
 
 
@@ -54,6 +55,122 @@ def flops_per_sample(cfg) -> int:
     total += cfg.N * (12 * q * D * D + 2 * q * q * D)
     total += (4 * D + 2 * d) * cfg.head_hidden + cfg.head_hidden
     return 6 * total
+
+
+def serve_macs(cfg):
+    """(cache build MACs per user, scoring MACs per candidate): the reference's exact model,
+    muladds_cache_build / muladds_incremental (pkg/src/longrec/analysis.py:174-198)."""
+    d, D, F = cfg.d, cfg.D, cfg.feat_width
+    q, v = cfg.k + cfg.m - 1, cfg.merged_len + cfg.m - 1
+    hh = (4 * D + 2 * d) * cfg.head_hidden + cfg.head_hidden
+    build = cfg.L * (F * d + 4 * d * D) + d * D + (cfg.m - 1) * 4 * D * D
+    if cfg.merge_mode == "inner":
+        build += cfg.inner_layers * (12 * cfg.L_padded * d * d + 2 * cfg.L_padded * cfg.K * d)
+    build += 10 * q * D * D + 2 * v * D * D + 2 * q * v * D + cfg.N * (12 * q * D * D + 2 * q * q * D)
+    v1, vs = cfg.merged_len + cfg.m, cfg.k + cfg.m
+    inc = F * d + d * D + 4 * D * D + 12 * D * D + 2 * v1 * D + cfg.N * (12 * D * D + 2 * vs * D) + hh
+    return build, inc
+
+
+def run_serving(args):
+    """--config c4 (BASELINE config 4): c2 weights, per-user KV cache built once, then `--cands`
+    candidates per user scored against it; `--users` users per call.  value = cached candidates/s
+    (cache and candidate ids resident in HBM, L2 flushed between steps); e2e = the same through
+    serving.score_candidates from a pinned host id array with the probabilities read back."""
+    import numpy as np
+    import torch
+    from paper_2505_04421_b200 import ModelConfig, serving as S, synthetic_batch
+    from paper_2505_04421_b200.model import LongerModel
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    cfg = ModelConfig(**CONFIGS["c2_inner"]).validate()
+    U, C = args.users, args.cands
+    model = LongerModel(cfg, seed=0)
+    users = synthetic_batch(cfg, U, seed=3).to("cuda")
+    times = [0] * U
+    cand_host = torch.from_numpy(np.random.default_rng(5).integers(0, cfg.vocab, (U, C)).astype(np.int32)).pin_memory()
+    cand_dev = cand_host.to("cuda")
+    cache = S.build_caches_batch(model, users, times)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+
+    def timed(fn, steps, warmup):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        tot = 0.0
+        for i in range(steps):
+            flush.fill_(i & 0xFF)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            tot += e0.elapsed_time(e1)
+        return tot / steps
+
+    probs = torch.empty((U, C), dtype=torch.float32, device="cuda")
+    clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    clocks.start()
+    ms_build = timed(lambda: S.build_caches_batch(model, users, times), args.steps, args.warmup)
+    ms_score = timed(lambda: S.score_device(model, cache, cand_dev, probs), args.steps, args.warmup)
+    host_out = torch.empty((U, C), dtype=torch.float32).pin_memory()
+
+    def e2e_step():
+        p = S.score_candidates(model, cache, cand_host.numpy(), check=False)
+        host_out.copy_(p, non_blocking=True)
+    ms_e2e = timed(e2e_step, args.steps, args.warmup)
+    clk = clocks.stop()
+    # parity beside the number: cached scores vs this library's full forward of the same pairs
+    n = min(C, 256)
+    full = S.full_batch_for(users, cand_dev[0, :n], user=0)
+    p_full = model.forward(full)
+    dmax = float((probs[0, :n] - p_full).abs().max())
+    burst, sustained, hbm, src = peaks()
+    b_macs, inc_macs = serve_macs(cfg)
+    value = U * C / (ms_score / 1e3)
+    achieved = value * 2 * inc_macs / 1e12
+    line = {
+        "metric": "cached candidates/sec at L=2000 (c4 serving)", "value": value, "unit": "candidates/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_score,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": "c4", **CONFIGS["c2_inner"], "users_per_call": U, "candidates_per_user": C,
+                   "l2": "flushed between steps"},
+        "cache_build": {"users_per_s": U / (ms_build / 1e3), "ms_per_call": ms_build,
+                        "tflops": U * 2 * b_macs / (ms_build / 1e3) / 1e12,
+                        "cache_bytes_per_user": S.cache_size_bytes(model, 1)},
+        "roofline": {"bound": "tensor", "kernel": "cache_score (whole call)", "achieved": achieved, "peak": burst,
+                     "unit": "TFLOP/s", "frac": achieved / burst, "traffic": None, "peak_source": src,
+                     "flop_per_candidate": 2 * inc_macs},
+        "e2e": {"value": U * C / (ms_e2e / 1e3), "unit": "candidates/s", "h2d_bytes_per_step": U * C * 4,
+                "d2h_bytes_per_step": U * C * 4, "ms_per_step": ms_e2e},
+        "parity": {"max_abs_cached_minus_full_forward": dmax, "pairs": n},
+        "clocks": clk,
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_serving_entry(cfg, C)
+    print(json.dumps(line), flush=True)
+
+
+def cpu_serving_entry(cfg, C):
+    """The reference's serving algorithm on the host: oracle/serving_oracle.py (float64
+    build_cache + score_with_cache, pinned to the reference's own cached scores) for one user
+    and C candidates, all BLAS threads."""
+    from oracle import serving_oracle as SO
+    from oracle.cpu_pool import cpu_model_name
+    from paper_2505_04421_b200 import init_params, synthetic_batch
+    import numpy as np
+    P = init_params(cfg, 0)
+    user = synthetic_batch(cfg, 1, seed=3).as_dict()
+    cand = np.random.default_rng(5).integers(0, cfg.vocab, (1, C))
+    t0 = time.perf_counter()
+    cache = SO.build_cache(P, cfg, user)
+    t1 = time.perf_counter()
+    SO.score(P, cfg, cache, cand)
+    t2 = time.perf_counter()
+    return {"value": C / (t2 - t1), "unit": "candidates/s", "cores": os.cpu_count(), "kind": "port",
+            "cpu_model": cpu_model_name(), "cache_build_s_per_user": t1 - t0,
+            "sample": f"1 user: float64 build_cache ({t1 - t0:.2f} s) + score_with_cache of {C} candidates "
+                      f"({t2 - t1:.2f} s), oracle/serving_oracle.py, one process, all BLAS threads"}
 
 
 def phase_flops(cfg, B):
@@ -187,6 +304,18 @@ def run_reference(args, cfg):
     same config and metric; rank 0 only under torchrun."""
     if int(os.environ.get("RANK", "0")) != 0:
         return
+    if args.config == "c4":
+        base = cpu_serving_entry(cfg, args.cands)
+        v = base["value"]
+        print(json.dumps({"impl": "reference", "metric": "cached candidates/sec at L=2000 (c4 serving)",
+                          "value": v, "unit": "candidates/s", "n_gpus": args.gpus, "steps": 1, "warmup": 0,
+                          "ms_per_step": 1e3 * args.cands / v, "higher_is_better": True, "scaling": "weak",
+                          "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                          "config": {"workload": "c4", **CONFIGS["c4"], "candidates_per_user": args.cands},
+                          "cpu_baseline": base,
+                          "e2e": {"value": v, "unit": "candidates/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}), flush=True)
+        return
     n = args.cpu_samples or cpu_samples_default()
     base = cpu_baseline_entry(cfg, n, args.steps, args.warmup)
     value = base["value"]
@@ -225,6 +354,8 @@ def main():
     ap.add_argument("--batch", type=int, default=256, help="samples per GPU per step")
     ap.add_argument("--cpu-samples", type=int, default=0, help="CPU arm samples per step (0: 4 x cores)")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--users", type=int, default=64, help="c4: users per serving call")
+    ap.add_argument("--cands", type=int, default=512, help="c4: candidates per user")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -233,6 +364,9 @@ def main():
     cfg = ModelConfig(**CONFIGS[args.config]).validate()
     if args.impl == "reference":
         run_reference(args, cfg)
+        return
+    if args.config == "c4":
+        run_serving(args)
         return
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(relaunch_under_torchrun(args))

@@ -143,6 +143,26 @@ def score_candidates(model, cache: KVCache, candidates, check: bool = True) -> "
         return torch.zeros((U, 0), dtype=torch.float32, device=model.device)
     if items.size and (items.min() < 0 or items.max() >= model.cfg.vocab):
         raise EmbeddingLookupError(f"item id out of range [0, {model.cfg.vocab})")
+    cand_dev = torch.from_numpy(items.astype(np.int32)).to(model.device, non_blocking=True)
+    probs = torch.empty((U, C), dtype=torch.float32, device=model.device)
+    base = score_device(model, cache, cand_dev, probs)
+    if not check:
+        return probs
+    flags = ctypes.c_int32()
+    _lib.check(model._lib.longer_read_status(ctypes.c_void_p(base), ctypes.byref(flags), model._stream()))
+    if flags.value & 1:
+        raise EmbeddingLookupError("candidate item id outside the item table")
+    return probs
+
+
+def score_device(model, cache: KVCache, cand_dev, probs) -> int:
+    """Stage 2 on device-resident inputs, no host work or sync (graph-capturable): ``cand_dev``
+    int32 [users, C] item ids (checked on device: the status flag), ``probs`` float32 [users, C]
+    output.  Returns the workspace base address (its first word is the status flag)."""
+    torch = _torch()
+    U, C = int(cand_dev.shape[0]), int(cand_dev.shape[1])
+    if U != cache.users:
+        raise ConfigError(f"candidate ids must be [users={cache.users}, C]")
     dims = _lib.dims_of(model.cfg, U)
     key = ("score", U, C)
     if key not in model._ws:
@@ -151,19 +171,21 @@ def score_candidates(model, cache: KVCache, candidates, check: bool = True) -> "
         model._ws[key] = torch.zeros(n.value + 256, dtype=torch.uint8, device=model.device)
     ws = model._ws[key]
     base = (ws.data_ptr() + 255) & ~255
-    cand_dev = torch.from_numpy(items.astype(np.int32)).to(model.device)
-    probs = torch.empty((U, C), dtype=torch.float32, device=model.device)
     _lib.check(model._lib.longer_cache_score(
         ctypes.byref(dims), ctypes.c_void_p(model.flat.data_ptr()), ctypes.c_void_p(cache._base), cache.nbytes,
         ctypes.c_void_p(cand_dev.data_ptr()), C, ctypes.c_void_p(base), ws.numel() - (base - ws.data_ptr()),
         ctypes.c_void_p(probs.data_ptr()), model._stream()))
-    if not check:
-        return probs
-    flags = ctypes.c_int32()
-    _lib.check(model._lib.longer_read_status(ctypes.c_void_p(base), ctypes.byref(flags), model._stream()))
-    if flags.value & 1:
-        raise EmbeddingLookupError("candidate item id outside the item table")
-    return probs
+    return base
+
+
+def full_batch_for(users: Batch, cand_items, user: int = 0) -> Batch:
+    """The full-forward batch of one cached user paired with each candidate item (checking aid)."""
+    n = int(cand_items.shape[0])
+    rep = lambda a: a[user:user + 1].repeat_interleave(n, dim=0) if hasattr(a, "repeat_interleave") \
+        else np.repeat(np.asarray(a)[user:user + 1], n, axis=0)
+    out = {f: rep(getattr(users, f)) for f in Batch.FIELDS}
+    out["cand_item"] = cand_items.to(out["items"].device).int() if hasattr(cand_items, "to") else cand_items
+    return Batch(**out)
 
 
 def score_with_cache(model, cache: KVCache, candidate: Candidate) -> float:

@@ -91,3 +91,25 @@ def test_multi_tile_per_cta_matches_oracle(merge, monkeypatch):
     for name in grads:
         scale = np.abs(grads[name]).max() + 1e-12
         assert np.abs(grads2[name] - grads[name]).max() <= 2e-3 * scale + 1e-7, name
+
+
+C5 = dict(L=10000, d=32, K=8, k=32, N=4, m=3, merge_mode="inner")
+
+
+@pytest.mark.parametrize("min_events", [None, 3000], ids=["full", "mixed"])
+def test_c5_real_shape_matches_oracle(min_events):
+    """BASELINE config 5 at its real shape (L = 10,000, d = 32, K = 8 → D = 256, N = 4 self
+    layers, InnerTrans): 1,250 merged keys = 10 key chunks of the tensor-core attention at head
+    width 256, the fused forward at D = 256 (three tile slots per CTA), the per-stage token-MLP
+    backward with activation recompute (2D = 512 > 256)."""
+    cfg = ModelConfig(**C5).validate()
+    P = _perturbed(cfg, 31)
+    batch = synthetic_batch(cfg, 4, seed=2, min_events=min_events)
+    model = _model(cfg, P)
+    p, loss, grads = _run(model, batch)
+    p_ref, loss_ref, G = oracle_chunked(P, cfg, batch, chunk=2)
+    assert np.max(np.abs(p - p_ref)) <= 5e-3, np.abs(p - p_ref)
+    assert abs(loss - loss_ref) <= loss_tol(p_ref, batch.label), (loss, loss_ref)
+    assert_grads_close(grads, G, f"c5 min_events={min_events}")
+    pf = model.forward(batch).cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(pf - p_ref)) <= 5e-3

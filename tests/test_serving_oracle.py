@@ -32,3 +32,17 @@ def test_oracle_full_forward_equals_reference_cached_scores(path):
 
 def test_serving_fixtures_exist():
     assert len(SERVING) >= 3
+
+
+@pytest.mark.parametrize("path", SERVING, ids=[os.path.basename(p)[:-4] for p in SERVING])
+def test_serving_oracle_equals_reference_cached_scores(path):
+    """oracle/serving_oracle.py (batched build_cache / score_with_cache) against the reference's
+    own cached scores."""
+    from oracle import serving_oracle as SO
+    z = np.load(path)
+    cfg = ModelConfig(**json.loads(str(z["cfg"])))
+    P = {k[2:]: z[k] for k in z.files if k.startswith("P/")}
+    users = {k[6:]: z[k] for k in z.files if k.startswith("users/")}
+    cache = SO.build_cache(P, cfg, users)
+    p = SO.score(P, cfg, cache, z["cand"])
+    np.testing.assert_allclose(p, z["p_cached"], rtol=0, atol=1e-10)
