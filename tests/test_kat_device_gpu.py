@@ -116,9 +116,9 @@ def test_device_flag_raises_reference_errors(field, idx, val, exc, fused, monkey
     model.loss_backward(good)                          # flags were reset
     with pytest.raises(exc):
         model.forward(bad, sync_check=True)
-    # deferred check: raised by a later call, once the step's flags reach the host
-    model.loss_backward(bad, check="async")
+    # deferred check: raised by this or a later call, once the step's flags reach the host
     with pytest.raises(exc):
+        model.loss_backward(bad, check="async")
         for _ in range(3):
             model.loss_backward(good, check="async")
         model.poll_checks(block=True)
