@@ -43,6 +43,28 @@ __global__ void pack_canon_kernel(const float* __restrict__ params, PackW pw, bf
   }
 }
 
+// P[r] = table_row(r) · W_tp[cols of its table] (+ b_tp on the time rows), fp32 (inputs.py:434-444
+// restated: the featuriser's linear map is applied per table row once per step, not per token)
+__global__ void project_tables_kernel(const float* __restrict__ item_tab, const float* __restrict__ act_tab,
+                                      const float* __restrict__ time_tab, const float* __restrict__ tok_w,
+                                      const float* __restrict__ tok_b, int vocab, int n_actions, int nb, int d_item,
+                                      int d_act, int d_time, int d, float* __restrict__ proj) {
+  pdl_trigger();
+  pdl_wait();
+  const int rows = vocab + n_actions + nb;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < rows * d; e += gridDim.x * blockDim.x) {
+    const int r = e / d, c = e % d;
+    const float* src;
+    int w, k0;
+    float acc = 0.f;
+    if (r < vocab) { src = item_tab + (long long)r * d_item; w = d_item; k0 = 0; }
+    else if (r < vocab + n_actions) { src = act_tab + (long long)(r - vocab) * d_act; w = d_act; k0 = d_item; }
+    else { src = time_tab + (long long)(r - vocab - n_actions) * d_time; w = d_time; k0 = d_item + d_act; acc = tok_b[c]; }
+    for (int k = 0; k < w; ++k) acc = fmaf(src[k], tok_w[(k0 + k) * d + c], acc);
+    proj[e] = acc;
+  }
+}
+
 // ------------------------------------------------------------------ shared worker pieces
 struct TokenInfo {
   long long t;
@@ -90,6 +112,24 @@ __device__ __forceinline__ void featurise_raw(const FrontArgs& a, const TokenInf
                             : a.time_tab + bucket * a.d_time + (c - e2);
     v[c] = c < e3 ? __ldg(p) : 0.f;
   }
+}
+
+// rows of FrontArgs::proj for the token's item, action and time bucket (time_bucket, inputs.py:307-315);
+// out-of-range ids raise the device flag (EmbeddingLookupError / ConfigError) and read row 0
+__device__ __forceinline__ void proj_rows(const FrontArgs& a, const TokenInfo& ti, int* rows) {
+  int item = 0, act = 0, dt = 0;
+  if (ti.real) {
+    const long long src = (long long)ti.b * a.L + (ti.j - (a.Lp - a.L));
+    item = a.items[src]; act = a.actions[src]; dt = a.dt[src];
+    int bad = 0;
+    if (item < 0 || item >= a.vocab) { bad |= 1; item = 0; }
+    if (act < 0 || act >= a.n_actions) { bad |= 1; act = 0; }
+    if (dt < 0) { bad |= 2; dt = 0; }
+    if (bad) atomicOr(a.status, bad);
+  }
+  rows[0] = item;
+  rows[1] = a.vocab + act;
+  rows[2] = a.vocab + a.n_actions + min(32 - __clz(dt), a.nb - 1);
 }
 
 __device__ __forceinline__ void featurise(const FrontArgs& a, const TokenInfo& ti, float* v, int* ids, bool flag) {
@@ -185,7 +225,7 @@ constexpr int kSlotCols = 128;
 template <int DT, int KG>
 struct FwdPlan {
   static constexpr int D = DT * KG, H2 = 2 * D, nh = H2 / 64, nf = 4 * DT / 64, XK = DT + 16;
-  static __host__ __device__ int stages(int IL) { return 2 + nh + IL * (3 + nf); }
+  static __host__ __device__ int stages(int IL) { return 1 + nh + IL * (3 + nf); }
 };
 
 template <int DT, int KG>
@@ -199,9 +239,8 @@ __device__ __forceinline__ void fwd_issue(int st, uint32_t t0, uint32_t wA, uint
     const Opnd A{wH, 64, 0}, B = W(off, kdim);
     for (int ks = 0; ks < 4; ++ks) sm100::mma_bf16(d, A.desc(ks), B.desc(ks), idesc, (acc || ks > 0) ? 1u : 0u);
   };
-  if (st == 0) { mma(t0, Opnd{wA, kFP, 0}, W(bo.tp, kFP), kFP / 16, DT, false); return; }
-  if (st == 1) { mma(t0, Opnd{wA, XK, 0}, W(bo.w1, XK), XK / 16, 64, false); return; }
-  st -= 2;
+  if (st == 0) { mma(t0, Opnd{wA, XK, 0}, W(bo.w1, XK), XK / 16, 64, false); return; }
+  st -= 1;
   if (st < nh) {
     w2mma(t0 + 64, bo.w2 + canon(0, 64 * st, H2), H2, st > 0);
     if (st + 1 < nh) mma(t0, Opnd{wA, XK, 0}, W(bo.w1 + canon(64 * (st + 1), 0, XK), XK), XK / 16, 64, false);
@@ -328,29 +367,24 @@ __global__ void __launch_bounds__(32 * 5 * S, 1) fe_fwd_kernel(FrontArgs a) {
         a.real_out[ti.t] = ti.real ? 1.f : 0.f;
         a.keep_out[ti.t] = ti.keep ? 1.f : 0.f;
       }
-      {
-        float v[kFP];
-        int ids[3];
-        featurise(a, ti, v, ids, true);
-        v[kFP - 1] = 1.f;                          // bias column (b_tp rides in the W_tp image)
-        store_row(sA, row, kFP, v, kFP);
-      }
-      signal();
       float h[DT];
       {
-        // abs-pos row: gathered while the MMA runs
+        // x0 = P[item] + P[action] + P[bucket] + abs_pos[recency]  (the featuriser's tok_proj
+        // applied per table row: FrontArgs::proj)
+        int pr[3];
+        proj_rows(a, ti, pr);
         const float4* pp = reinterpret_cast<const float4*>(a.pos_tab + (long long)ti.rec * DT);
+        const float4* p0 = reinterpret_cast<const float4*>(a.proj + (long long)pr[0] * DT);
+        const float4* p1 = reinterpret_cast<const float4*>(a.proj + (long long)pr[1] * DT);
+        const float4* p2 = reinterpret_cast<const float4*>(a.proj + (long long)pr[2] * DT);
 #pragma unroll
         for (int c = 0; c < DT; c += 4) {
-          const float4 p4 = __ldg(pp + c / 4);
-          h[c] = p4.x; h[c + 1] = p4.y; h[c + 2] = p4.z; h[c + 3] = p4.w;
+          const float4 x = __ldg(pp + c / 4), y0 = __ldg(p0 + c / 4), y1 = __ldg(p1 + c / 4), y2 = __ldg(p2 + c / 4);
+          h[c] = ti.real ? (y0.x + y1.x) + (y2.x + x.x) : 0.f;
+          h[c + 1] = ti.real ? (y0.y + y1.y) + (y2.y + x.y) : 0.f;
+          h[c + 2] = ti.real ? (y0.z + y1.z) + (y2.z + x.z) : 0.f;
+          h[c + 3] = ti.real ? (y0.w + y1.w) + (y2.w + x.w) : 0.f;
         }
-        // x0 = [feat | 1]·[W_tp ; b_tp] + abs_pos[recency]
-        wait_d();
-        float acc[DT];
-        tmem_row<DT>(trow, acc);
-#pragma unroll
-        for (int c = 0; c < DT; ++c) h[c] = ti.real ? h[c] + acc[c] : 0.f;
         store_row(sA, row, XK, h, DT);
         store_ones_col<DT>(sA, row);
       }
@@ -894,6 +928,14 @@ int frontend_supported(int d, int K, int D, int F, int inner_layers) {
 int frontend_mlp_bwd_supported(int d, int K, int D) {
   (void)d; (void)K;
   return 2 * D <= 256;
+}
+
+void project_tables(const float* item_tab, const float* act_tab, const float* time_tab, const float* tok_w,
+                    const float* tok_b, int vocab, int n_actions, int nb, int d_item, int d_act, int d_time, int d,
+                    float* proj, cudaStream_t st) {
+  const int n = (vocab + n_actions + nb) * d;
+  launch(project_tables_kernel, std::min((n + 255) / 256, 592), 256, 0, st, item_tab, act_tab, time_tab, tok_w, tok_b,
+         vocab, n_actions, nb, d_item, d_act, d_time, d, proj);
 }
 
 int frontend_blob_bytes(int d, int D, int inner_layers) { return blob_offsets(d, D, inner_layers).total * 2; }

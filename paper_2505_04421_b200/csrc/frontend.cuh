@@ -25,6 +25,10 @@ struct FrontArgs {
   const float* inner_ln[8][4];     // per layer: ln1_g, ln1_b, ln2_g, ln2_b
   // packed bf16 weight blob (see pack_frontend_weights)
   const bf16* wblob;
+  // the embedding tables projected through tok_proj (fp32): rows [0, vocab) item_table·W_tp[item
+  // cols], then n_actions rows action_table·W_tp[action cols], then nb rows
+  // time_table·W_tp[time cols] + b_tp — so x0 = P[item] + P[action] + P[bucket] + abs_pos
+  const float* proj;
   // forward outputs
   float* merged;               // [T, d]  (== [B*G, D])
   float* h_out;                // [T, d]  token-MLP output (InnerTrans input), saved for backward (or null)
@@ -59,6 +63,10 @@ int frontend_supported(int d, int K, int D, int F, int inner_layers);
 // the fused token-MLP backward additionally needs 2D ≤ 256 (TMEM / shared-memory budget)
 int frontend_mlp_bwd_supported(int d, int K, int D);
 int frontend_fwd(const FrontArgs& a, cudaStream_t st);
+// P (see FrontArgs::proj) from the fp32 master tables: (vocab + n_actions + nb) x d floats
+void project_tables(const float* item_tab, const float* act_tab, const float* time_tab, const float* tok_w,
+                    const float* tok_b, int vocab, int n_actions, int nb, int d_item, int d_act, int d_time, int d,
+                    float* proj, cudaStream_t st);
 // token-MLP + featuriser backward: dh → all front-end MLP/featuriser/table/pos gradients
 int frontend_mlp_bwd(const FrontArgs& a, cudaStream_t st);
 // InnerTrans (one layer) backward: recompute the layer from h, dmerged → dh + layer gradients

@@ -236,6 +236,7 @@ struct Plan {
   float *hc_x, *hc_g, *hc_dctx;   // compact [2B, D] buffers of that tail
   bf16 *hc_ctx, *hc_g_bf;
   bf16* wblob;     // its canonical-layout weight blob
+  float* proj;     // the embedding tables projected through tok_proj (FrontArgs::proj)
   int B, L, Lp, d, K, G, D, m, k, q, v, N, heads, inner, IL, hh, F, FP, HIN;
   long long T;
   ParamOff po;
@@ -316,6 +317,7 @@ Plan make_plan(const LongerDims& d, void* ws) {
   p.qg = a.take<int32_t>((long long)B * d.k);
   p.ids = a.take<int32_t>(3LL * B);
   p.wblob = a.take<bf16>(frontend_blob_bytes(dd, D, p.IL) / 2 + 64);
+  p.proj = a.take<float>((long long)(d.vocab + d.n_actions + d.n_time_buckets) * dd);
   take_packed(p, a);
   // tokens
   p.feat = a.take<bf16>(T * p.FP); p.x0 = a.take<bf16>(T * dd);
@@ -645,6 +647,7 @@ FrontArgs front_args(const Ctx& c, const Plan& p, const LongerBatch& bt) {
     f.inner_ln[l][2] = c.w(b.ln2_g); f.inner_ln[l][3] = c.w(b.ln2_b);
   }
   f.wblob = p.wblob;
+  f.proj = p.proj;
   f.merged = p.merged; f.status = p.status; f.npg = p.npg;
   f.h_out = p.IL ? p.h : nullptr;
   f.real_out = p.real; f.keep_out = p.keep;
@@ -664,6 +667,9 @@ int frontend_fused_fwd(const Ctx& c, const Plan& p, const LongerBatch& bt) {
     iw[l][0] = o.inner[l].w_q; iw[l][1] = o.inner[l].w_k; iw[l][2] = o.inner[l].w_v; iw[l][3] = o.inner[l].w_o;
   }
   pack_frontend_weights(c.P, o.tok_w, o.seq_w1, o.seq_w2, iw, p.d, p.D, p.F, p.IL, p.wblob, c.st);
+  const LongerDims& dm = p.dims;
+  project_tables(c.w(o.item), c.w(o.act), c.w(o.time), c.w(o.tok_w), c.w(o.tok_b), dm.vocab, dm.n_actions,
+                 dm.n_time_buckets, dm.d_item, dm.d_act, dm.d_time, p.d, p.proj, c.st);
   FrontArgs f = front_args(c, p, bt);
   // epilogue: the cross block's LN1 of the merged rows straight into the K/V operand (kn)
   f.kn = p.kn; f.kn_g = c.w(o.cross.ln1_g); f.kn_b = c.w(o.cross.ln1_b);

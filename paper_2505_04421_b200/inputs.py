@@ -13,8 +13,10 @@ from __future__ import annotations
 
 import gzip
 import json
-
+import threading
 from dataclasses import dataclass
+from itertools import chain
+from operator import attrgetter
 from typing import Optional, Sequence
 
 import numpy as np
@@ -96,11 +98,75 @@ class Dataset:
     def labels(self) -> np.ndarray:
         return np.array([s.label for s in self.samples], dtype=np.int64)
 
-    def batches(self, cfg: ModelConfig, batch_size: int, pin: bool = True):
-        """Host ``Batch``es (pinned for async H2D) of ``batch_size`` samples, in file order."""
-        for i in range(0, len(self.samples), batch_size):
-            b = tensorize(self.samples[i:i + batch_size], cfg)
-            yield b.pin() if pin else b
+    def tensorized(self, cfg: ModelConfig) -> Batch:
+        """The whole dataset in the C-ABI layout (host numpy, checked once), cached per L."""
+        cache = self.__dict__.setdefault("_columns", {})
+        if cfg.L not in cache:
+            cache[cfg.L] = tensorize(self.samples, cfg)
+        return cache[cfg.L]
+
+    def batches(self, cfg: ModelConfig, batch_size: int, pin: bool = True, device=None, prefetch: int = 2,
+                shuffle: bool = False, seed: int = 0):
+        """``Batch``es of ``batch_size`` samples (file order, or a seeded permutation with
+        ``shuffle``), sliced from the tensorised dataset.  ``pin``: host batches in pinned memory.
+        ``device``: a background thread slices, pins and copies the next ``prefetch`` batches
+        host→device on its own CUDA stream while the caller's step runs; each yielded device batch
+        is ready on the caller's current stream (it waits on the copy's event)."""
+        cols = self.tensorized(cfg)
+        N = len(self)
+        order = np.random.default_rng(seed).permutation(N) if shuffle else None
+
+        def host(i):
+            idx = slice(i, min(i + batch_size, N)) if order is None else order[i:i + batch_size]
+            b = Batch(**{f: np.ascontiguousarray(getattr(cols, f)[idx]) for f in Batch.FIELDS})
+            return b.pin() if (pin or device is not None) else b
+
+        starts = range(0, N, batch_size)
+        if device is None:
+            for i in starts:
+                yield host(i)
+            return
+        yield from _prefetched(host, starts, device, prefetch)
+
+
+def _prefetched(host, starts, device, depth):
+    """Background host slicing + pinned H2D on a side stream, ``depth`` batches ahead."""
+    import queue
+
+    import torch
+    q = queue.Queue(maxsize=max(1, depth))
+    stream = torch.cuda.Stream(device)
+    stop = threading.Event()
+
+    def work():
+        try:
+            for i in starts:
+                if stop.is_set():
+                    break
+                hb = host(i)
+                with torch.cuda.stream(stream):
+                    db = hb.to(device, non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(stream)
+                q.put((db, ev, hb))
+        except BaseException as exc:           # surfaced on the consumer side
+            q.put(exc)
+        q.put(None)
+
+    t = threading.Thread(target=work, daemon=True)
+    t.start()
+    try:
+        while True:
+            item = q.get()
+            if item is None:
+                break
+            if isinstance(item, BaseException):
+                raise item
+            db, ev, hb = item
+            torch.cuda.current_stream(device).wait_event(ev)
+            yield db
+    finally:
+        stop.set()
 
 
 def save_dataset(dataset: Dataset, path: str) -> None:
@@ -181,42 +247,45 @@ def _check_ids(name: str, arr: np.ndarray, rows: int) -> None:
 
 
 def tensorize(samples: Sequence[Sample], cfg: ModelConfig, check: bool = True) -> Batch:
-    """Samples → ``Batch`` (host numpy).  Raises the reference's errors for bad input."""
+    """Samples → ``Batch`` (host numpy).  Raises the reference's errors for bad input.
+
+    Each event field is pulled from all events of the batch by one C-level iterator chain
+    (≈ 1.5 M attribute reads for 256 x 2000 events: this, not the placement, bounds it), then placed
+    into the right-aligned [B, L] grid and range-checked with vector operations.  Training loops
+    should tensorise a dataset once (``Dataset.tensorized``) and slice batches from it
+    (``Dataset.batches``)."""
     B, L = len(samples), cfg.L
+    evs = [tuple(s.events)[-L:] for s in samples]
+    n = np.fromiter((len(e) for e in evs), np.int64, B)
+    tot = int(n.sum())
+    flat = np.stack([np.fromiter(map(attrgetter(k), chain.from_iterable(evs)), np.int64, tot)
+                     for k in ("item_id", "action_type", "timestamp")], axis=1)
+    cand_ts = np.fromiter((s.candidate.timestamp for s in samples), np.int64, B)
+    rows = np.repeat(np.arange(B), n)
+    starts = np.cumsum(n) - n
+    cols = np.arange(tot) - np.repeat(starts, n) + np.repeat(L - n, n)
+    delta = np.repeat(cand_ts, n) - flat[:, 2]
+    if check:
+        _check_ids("item", flat[:, 0], cfg.vocab)
+        _check_ids("action", flat[:, 1], cfg.n_actions)
+        if (delta < 0).any():
+            raise ConfigError("future event: negative time delta")
     items = np.zeros((B, L), np.int32)
     actions = np.zeros((B, L), np.int32)
     dt = np.zeros((B, L), np.int32)
-    n_events = np.zeros(B, np.int32)
-    uid = np.zeros(B, np.int32)
-    profile = np.zeros(B, np.int32)
-    cand = np.zeros(B, np.int32)
-    label = np.zeros(B, np.float32)
-    for b, s in enumerate(samples):
-        ev = tuple(s.events)[-L:]
-        n = len(ev)
-        n_events[b] = n
-        if n:
-            it = np.fromiter((e.item_id for e in ev), np.int64, n)
-            ac = np.fromiter((e.action_type for e in ev), np.int64, n)
-            ts = np.fromiter((e.timestamp for e in ev), np.int64, n)
-            delta = int(s.candidate.timestamp) - ts
-            if check:
-                _check_ids("item", it, cfg.vocab)
-                _check_ids("action", ac, cfg.n_actions)
-                if (delta < 0).any():
-                    raise ConfigError("future event: negative time delta")
-            items[b, L - n:] = it
-            actions[b, L - n:] = ac
-            dt[b, L - n:] = np.minimum(delta, INT32_MAX)
-        uid[b] = s.user_features.uid
-        profile[b] = s.user_features.profile_bucket
-        cand[b] = s.candidate.item_id
-        label[b] = s.label
+    items[rows, cols] = flat[:, 0]
+    actions[rows, cols] = flat[:, 1]
+    dt[rows, cols] = np.minimum(delta, INT32_MAX)
+    uid = np.fromiter((s.user_features.uid for s in samples), np.int64, B)
+    profile = np.fromiter((s.user_features.profile_bucket for s in samples), np.int64, B)
+    cand = np.fromiter((s.candidate.item_id for s in samples), np.int64, B)
+    label = np.fromiter((s.label for s in samples), np.float64, B)
     if check:
         _check_ids("uid", uid, cfg.n_users)
         _check_ids("profile", profile, cfg.n_profiles)
         _check_ids("item", cand, cfg.vocab)
-    return Batch(items, actions, dt, n_events, uid, profile, cand, label)
+    return Batch(items, actions, dt, n.astype(np.int32), uid.astype(np.int32), profile.astype(np.int32),
+                 cand.astype(np.int32), label.astype(np.float32))
 
 
 def check_batch(batch: Batch, cfg: ModelConfig) -> None:

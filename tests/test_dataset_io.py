@@ -50,3 +50,30 @@ def test_reads_and_writes_the_reference_format(tmp_path):
     p2 = str(tmp_path / "theirs.jsonl.gz")
     RI.save_dataset(theirs, p2)                              # we read the reference's file
     assert load_dataset(p2).samples == ours
+
+
+def test_vectorised_tensorize_matches_per_sample_layout():
+    """tensorize places every sample's last L events right-aligned, with deltas from its own
+    candidate timestamp (encode_events, pkg/src/longrec/inputs.py:457-482)."""
+    cfg = ModelConfig(L=16, d=16, K=4, k=2, N=1, m=3).validate()
+    smp = synthetic_samples(cfg, 5, seed=9, n_events=30)[:2] + synthetic_samples(cfg, 3, seed=4, n_events=7)
+    b = tensorize(smp, cfg)
+    for i, s in enumerate(smp):
+        ev = s.events[-cfg.L:]
+        n = len(ev)
+        assert b.n_events[i] == n
+        np.testing.assert_array_equal(b.items[i, cfg.L - n:], [e.item_id for e in ev])
+        np.testing.assert_array_equal(b.actions[i, cfg.L - n:], [e.action_type for e in ev])
+        np.testing.assert_array_equal(b.dt[i, cfg.L - n:], [s.candidate.timestamp - e.timestamp for e in ev])
+        assert not b.items[i, :cfg.L - n].any() and not b.dt[i, :cfg.L - n].any()
+
+
+def test_dataset_batches_slice_the_tensorised_dataset():
+    cfg = ModelConfig(L=16, d=16, K=4, k=2, N=1, m=3).validate()
+    ds = Dataset(synthetic_samples(cfg, 11, seed=2, n_events=9))
+    full = tensorize(ds.samples, cfg)
+    got = list(ds.batches(cfg, 4, pin=False))
+    assert [g.size for g in got] == [4, 4, 3]
+    np.testing.assert_array_equal(np.concatenate([g.items for g in got]), full.items)
+    sh = list(ds.batches(cfg, 4, pin=False, shuffle=True, seed=1))
+    assert sorted(np.concatenate([g.uid for g in sh]).tolist()) == sorted(full.uid.tolist())
