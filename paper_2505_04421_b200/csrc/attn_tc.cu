@@ -251,6 +251,7 @@ __global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a, cons
           uint32_t r[32];
           sm100::tmem_ld32(T_O + lo_lane + cc, r);
           sm100::tmem_ld_wait();
+          sm100::reg_fence(r);
 #pragma unroll
           for (int u = 0; u < 32; ++u) r[u] = __float_as_uint(__uint_as_float(r[u]) * factor);
           sm100::tmem_st32(T_O + lo_lane + cc, r);
@@ -526,8 +527,7 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
 #pragma unroll 1
       for (int j0 = grp * (kC / 2); j0 < grp * (kC / 2) + kC / 2; j0 += 32) {
         float s[32], dp[32];
-        tmem_row<32>(T_A + lo + j0, s);
-        tmem_row<32>(T_B + lo + j0, dp);
+        tmem_row2<32>(T_A + lo + j0, s, T_B + lo + j0, dp);
         const uint32_t bits = vis_bits(vlo, vhi, c0 + j0);
         if (bits) {
 #pragma unroll
@@ -552,8 +552,7 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
 #pragma unroll 1
       for (int j0 = grp * (kC / 2); j0 < grp * (kC / 2) + kC / 2; j0 += 32) {
         float s[32], dp[32];
-        tmem_row<32>(T_A + lo + j0, s);
-        tmem_row<32>(T_B + lo + j0, dp);
+        tmem_row2<32>(T_A + lo + j0, s, T_B + lo + j0, dp);
         const uint32_t bits = vis_bits(vlo, vhi, c0 + j0);
 #pragma unroll
         for (int u = 0; u < 32; ++u) {
@@ -579,8 +578,7 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
 #pragma unroll 1
         for (int c1 = r0; c1 < r1; c1 += 32) {
           float dv[32], dk[32];
-          tmem_row<32>(T_A + lo + c1, dv);
-          tmem_row<32>(T_B + lo + c1, dk);
+          tmem_row2<32>(T_A + lo + c1, dv, T_B + lo + c1, dk);
           if (!krow) continue;
 #pragma unroll
           for (int cc = 0; cc < 32; cc += 8) {

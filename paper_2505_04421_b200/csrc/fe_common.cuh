@@ -109,24 +109,41 @@ __device__ __forceinline__ void mma(uint32_t tmem_d, const OA& A, const OB& B, i
     sm100::mma_bf16(tmem_d, A.desc(ks), B.desc(ks), idesc, (acc || ks > 0) ? 1u : 0u);
 }
 
+// issue the loads of N columns (N = 16 or a multiple of 32) without waiting
 template <int N>
-__device__ __forceinline__ void tmem_row(uint32_t taddr, float* out) {
+__device__ __forceinline__ void tmem_row_issue(uint32_t taddr, uint32_t* r) {
 #pragma unroll
   for (int c = 0; c < N; c += 32) {
-    if (c + 32 <= N) {
-      uint32_t r[32];
-      sm100::tmem_ld32(taddr + c, r);
-      sm100::tmem_ld_wait();
-#pragma unroll
-      for (int j = 0; j < 32; ++j) out[c + j] = __uint_as_float(r[j]);
-    } else {
-      uint32_t r[16];
-      sm100::tmem_ld16(taddr + c, r);
-      sm100::tmem_ld_wait();
-#pragma unroll
-      for (int j = 0; j < 16; ++j) out[c + j] = __uint_as_float(r[j]);
-    }
+    if (c + 32 <= N) sm100::tmem_ld32(taddr + c, *reinterpret_cast<uint32_t(*)[32]>(r + c));
+    else sm100::tmem_ld16(taddr + c, *reinterpret_cast<uint32_t(*)[16]>(r + c));
   }
+}
+// after tcgen05.wait::ld: tie each loaded register to the wait, so no use is scheduled above it
+template <int N>
+__device__ __forceinline__ void tmem_row_take(uint32_t* r, float* out) {
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    asm volatile("" : "+r"(r[j]));
+    out[j] = __uint_as_float(r[j]);
+  }
+}
+// one row's N TMEM columns → out (all loads in flight together, one wait)
+template <int N>
+__device__ __forceinline__ void tmem_row(uint32_t taddr, float* out) {
+  uint32_t r[N];
+  tmem_row_issue<N>(taddr, r);
+  sm100::tmem_ld_wait();
+  tmem_row_take<N>(r, out);
+}
+// two rows of columns (e.g. an accumulator and its gradient) with one wait
+template <int N>
+__device__ __forceinline__ void tmem_row2(uint32_t ta, float* a, uint32_t tb, float* b) {
+  uint32_t ra[N], rb[N];
+  tmem_row_issue<N>(ta, ra);
+  tmem_row_issue<N>(tb, rb);
+  sm100::tmem_ld_wait();
+  tmem_row_take<N>(ra, a);
+  tmem_row_take<N>(rb, b);
 }
 
 // park a row's N fp32 values in TMEM columns [taddr, taddr + N) (N = 16 or a multiple of 32)

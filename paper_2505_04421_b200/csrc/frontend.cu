@@ -776,8 +776,7 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
 #pragma unroll 1
         for (int c0 = 64 * grp; c0 < 64 * grp + 64; c0 += 32) {
           float av[32], gv[32];
-          tmem_row<32>(T_A1 + lane_off + c0, av);
-          tmem_row<32>(T_G1 + lane_off + c0, gv);
+          tmem_row2<32>(T_A1 + lane_off + c0, av, T_G1 + lane_off + c0, gv);
 #pragma unroll
           for (int u = 0; u < 32; ++u) {
             float gd;                                               // b1 added by the MMA

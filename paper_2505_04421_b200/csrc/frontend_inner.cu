@@ -329,8 +329,7 @@ __global__ void __launch_bounds__(32 * (1 + kWorkers * NG), 1) fe_inner_bwd_kern
 #pragma unroll 1
       for (int cc = grp * FH; cc < grp * FH + FH; cc += 32) {
         float fv[32], gv[32];
-        tmem_row<32>(T_W0 + lo + cc, fv);
-        tmem_row<32>(T_W1 + lo + cc, gv);
+        tmem_row2<32>(T_W0 + lo + cc, fv, T_W1 + lo + cc, gv);
 #pragma unroll
         for (int u = 0; u < 32; ++u) {
           float gd;                                                   // b1 added by the MMA

@@ -220,6 +220,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       uint32_t r[32];
       sm100::tmem_ld32(tmem_acc + ((uint32_t)(q * 32) << 16) + c, r);
       sm100::tmem_ld_wait();
+      sm100::reg_fence(r);
       const int nb = n0 + c;
       if (nb >= g.N) continue;                                   // warp-uniform
       const int m_base = m0 + q * 32;
