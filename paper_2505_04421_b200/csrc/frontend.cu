@@ -712,11 +712,23 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
         act_pf = a.actions[src];
         dt_pf = a.dt[src];
       } else {
-        const float4* srcd = reinterpret_cast<const float4*>(a.dh + ((long long)bb * a.Lp + j) * DT);
+        if (a.dh_bf) {
+          const uint4* srcb = reinterpret_cast<const uint4*>(a.dh_bf + ((long long)bb * a.Lp + j) * DT);
 #pragma unroll
-        for (int c = 0; c < DT; c += 4) {
-          const float4 f4 = srcd[c / 4];
-          dh_pf[c] = f4.x; dh_pf[c + 1] = f4.y; dh_pf[c + 2] = f4.z; dh_pf[c + 3] = f4.w;
+          for (int c = 0; c < DT; c += 8) {
+            const uint4 u = srcb[c / 8];
+            dh_pf[c] = sm100::bf16_lo(u.x); dh_pf[c + 1] = sm100::bf16_hi(u.x);
+            dh_pf[c + 2] = sm100::bf16_lo(u.y); dh_pf[c + 3] = sm100::bf16_hi(u.y);
+            dh_pf[c + 4] = sm100::bf16_lo(u.z); dh_pf[c + 5] = sm100::bf16_hi(u.z);
+            dh_pf[c + 6] = sm100::bf16_lo(u.w); dh_pf[c + 7] = sm100::bf16_hi(u.w);
+          }
+        } else {
+          const float4* srcd = reinterpret_cast<const float4*>(a.dh + ((long long)bb * a.Lp + j) * DT);
+#pragma unroll
+          for (int c = 0; c < DT; c += 4) {
+            const float4 f4 = srcd[c / 4];
+            dh_pf[c] = f4.x; dh_pf[c + 1] = f4.y; dh_pf[c + 2] = f4.z; dh_pf[c + 3] = f4.w;
+          }
         }
       }
     };

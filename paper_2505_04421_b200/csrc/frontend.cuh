@@ -43,12 +43,15 @@ struct FrontArgs {
   int v;                       // rows per sample in kn (G + m)
   // backward
   const float* dh;             // [T, d] gradient w.r.t. the token-MLP output (MLP backward input)
+  const bf16* dh_bf = nullptr; // or the same in bf16 (the InnerTrans backward's output): read instead
+                               // of dh — the MLP backward takes it as a bf16 MMA operand anyway
   float *g_tok_w, *g_tok_b, *g_seq_w1, *g_seq_b1, *g_seq_w2, *g_seq_b2;
   float *g_item, *g_act, *g_time, *g_pos;
   // InnerTrans backward (layer 0): h saved by the forward, dmerged in, dh out
   const float* h_in;           // [T, d]
   const float* dmerged;        // [T, d]
   float* dh_out;               // [T, d]
+  bf16* dh_out_bf = nullptr;   // [T, d] bf16 instead of dh_out (when the fused MLP backward reads it)
   float* g_inner[16];          // grads of w_q,b_q,w_k,b_k,w_v,b_v,w_o,b_o,w1,b1,w2,b2,ln1_g,ln1_b,ln2_g,ln2_b
 };
 

@@ -434,9 +434,13 @@ __global__ void __launch_bounds__(32 * (1 + kWorkers * NG), 1) fe_inner_bwd_kern
       cs_l1g += warp_colsum<HD>(tmp);
       cs_l1b += warp_colsum<HD>(g);
       if (in_range) {
+        if (a.dh_out_bf) {
+          store8_bf16<HD>(a.dh_out_bf + t * DT + c0, dx1);
+        } else {
 #pragma unroll
-        for (int c = 0; c < HD; c += 4)
-          *reinterpret_cast<float4*>(a.dh_out + t * DT + c0 + c) = make_float4(dx1[c], dx1[c + 1], dx1[c + 2], dx1[c + 3]);
+          for (int c = 0; c < HD; c += 4)
+            *reinterpret_cast<float4*>(a.dh_out + t * DT + c0 + c) = make_float4(dx1[c], dx1[c + 1], dx1[c + 2], dx1[c + 3]);
+        }
       }
     }
     // ---- flush this CTA's accumulators (gradient slots: 0 w_q,1 b_q,2 w_k,3 b_k,4 w_v,5 b_v,

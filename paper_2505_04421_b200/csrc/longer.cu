@@ -943,6 +943,8 @@ int backward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs) {
   if (p.fused_fe && p.IL == 1) {
     FrontArgs f = front_args(c, p, bt);
     f.h_in = p.h; f.dmerged = p.dmerged; f.dh_out = p.t_dx;
+    // the fused MLP backward takes dh as a bf16 MMA operand: hand it over in bf16 (half the bytes)
+    if (frontend_mlp_bwd_supported(p.d, p.K, p.D)) { f.dh_out = nullptr; f.dh_out_bf = reinterpret_cast<bf16*>(p.t_dx); }
     const BlockOff& bo = o.inner[0];
     const long long offs[16] = {bo.w_q, bo.b_q, bo.w_k, bo.b_k, bo.w_v, bo.b_v, bo.w_o, bo.b_o,
                                 bo.w1, bo.b1, bo.w2, bo.b2, bo.ln1_g, bo.ln1_b, bo.ln2_g, bo.ln2_b};
@@ -992,6 +994,7 @@ int backward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs) {
   } else if (p.fused_fe) {
     FrontArgs f = front_args(c, p, bt);
     f.dh = dxt;
+    if (dxt == p.t_dx && first_unfused < 0) { f.dh = nullptr; f.dh_bf = reinterpret_cast<const bf16*>(p.t_dx); }
     probe(PH_FE_MLP_BWD, 0, st); TRY(frontend_mlp_bwd(f, st)); probe(PH_FE_MLP_BWD, 1, st);
     join_side(st, ss);
     TRY((int)cudaGetLastError());
