@@ -6,6 +6,8 @@
 
 #include <math.h>
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 namespace longer {
 
@@ -71,24 +73,31 @@ void embed_fwd(const EmbedArgs& a, cudaStream_t st) {
   launch(embed_fwd_kernel, cdiv(T, 256), 256, smem, st, a);
 }
 
-// Backward of the featuriser: dfeat = dx0·W_tpᵀ scattered into the item/action/time tables with
-// shared-memory privatised accumulators (gather_rows bw = np.add.at, tensors.py:505-510).
-__global__ void embed_bwd_kernel(EmbedBwdArgs a, int tokens_per_block, int item_in_smem) {
+// Backward of the featuriser (gather_rows bw = np.add.at, tensors.py:505-510): dfeat = dx0·W_tpᵀ
+// scattered into the item / action / time tables.  A warp takes one token at a time, lane = channel
+// of dx0 (one coalesced row read).  The action and time tables have few rows, so their gradient is
+// linear in the per-row SUM of dx0: the block accumulates Σ dx0 per action and per time bucket in
+// shared memory (32 lanes → 32 consecutive words, no intra-warp conflicts) and multiplies by W_tpᵀ
+// once at the end.  The item part (vocab rows) is a per-token shuffle GEMV against W_tpᵀ in shared
+// memory, added into a shared-memory item-gradient copy when the table fits, else into HBM.
+constexpr int kEmbedBwdThreads = 256;
+
+__global__ void __launch_bounds__(kEmbedBwdThreads) embed_bwd_kernel(EmbedBwdArgs a, int item_in_smem) {
   pdl_trigger();
   pdl_wait();
   extern __shared__ float sm[];
-  const int F = a.d_item + a.d_act + a.d_time;
-  float* s_w = sm;                                   // F*d
-  float* s_time = s_w + F * a.d;                     // nb*d_time
-  float* s_act = s_time + a.nb * a.d_time;           // n_actions*d_act
-  float* s_item = s_act + a.n_actions * a.d_act;     // vocab*d_item (optional)
+  const int F = a.d_item + a.d_act + a.d_time, d = a.d;
+  float* s_wt = sm;                                  // [d][F]  W_tpᵀ
+  float* s_act = s_wt + d * F;                       // [n_actions][d]  Σ dx0 per action
+  float* s_time = s_act + a.n_actions * d;           // [nb][d]         Σ dx0 per time bucket
+  float* s_item = s_time + a.nb * d;                 // [vocab][d_item] (optional)
   const int n_item = item_in_smem ? a.vocab * a.d_item : 0;
-  const int tot = F * a.d + a.nb * a.d_time + a.n_actions * a.d_act + n_item;
-  for (int i = threadIdx.x; i < tot; i += blockDim.x) sm[i] = i < F * a.d ? a.tok_w[i] : 0.f;
+  for (int i = threadIdx.x; i < d * F; i += blockDim.x) s_wt[(i % d) * F + i / d] = a.tok_w[i];
+  for (int i = threadIdx.x; i < (a.n_actions + a.nb) * d + n_item; i += blockDim.x) s_act[i] = 0.f;
   __syncthreads();
+  const int lane = threadIdx.x & 31, nw = blockDim.x / 32;
   const long long T = (long long)a.B * a.Lp;
-  const long long t0 = (long long)blockIdx.x * tokens_per_block;
-  for (long long t = t0 + threadIdx.x; t < min(T, t0 + tokens_per_block); t += blockDim.x) {
+  for (long long t = (long long)blockIdx.x * nw + threadIdx.x / 32; t < T; t += (long long)gridDim.x * nw) {
     const int b = (int)(t / a.Lp), j = (int)(t % a.Lp);
     const int n = min(max(a.n_events[b], 0), a.L);
     if (j < a.Lp - n) continue;
@@ -98,26 +107,42 @@ __global__ void embed_bwd_kernel(EmbedBwdArgs a, int tokens_per_block, int item_
     if (act < 0 || act >= a.n_actions) act = 0;
     if (dt < 0) dt = 0;
     const int bucket = min(32 - __clz(dt), a.nb - 1);
-    float dx[64];
-    for (int c = 0; c < a.d; ++c) dx[c] = a.dx0[t * a.d + c];
-    for (int fi = 0; fi < F; ++fi) {
+    const float* dx = a.dx0 + t * d;
+    const float v0 = lane < d ? dx[lane] : 0.f;
+    const float v1 = lane + 32 < d ? dx[lane + 32] : 0.f;
+    if (lane < d) {
+      atomicAdd(&s_act[act * d + lane], v0);
+      atomicAdd(&s_time[bucket * d + lane], v0);
+    }
+    if (lane + 32 < d) {
+      atomicAdd(&s_act[act * d + lane + 32], v1);
+      atomicAdd(&s_time[bucket * d + lane + 32], v1);
+    }
+    for (int f0 = 0; f0 < a.d_item; f0 += 32) {
+      const int fi = f0 + lane;
+      const int fc = min(fi, F - 1);
       float g = 0.f;
-      for (int c = 0; c < a.d; ++c) g = fmaf(dx[c], s_w[fi * a.d + c], g);
+#pragma unroll 8
+      for (int c = 0; c < min(d, 32); ++c) g = fmaf(__shfl_sync(0xffffffffu, v0, c), s_wt[c * F + fc], g);
+      for (int c = 32; c < d; ++c) g = fmaf(__shfl_sync(0xffffffffu, v1, c - 32), s_wt[c * F + fc], g);
       if (fi < a.d_item) {
         if (item_in_smem) atomicAdd(&s_item[item * a.d_item + fi], g);
-        else atomicAdd(&a.g_item[item * a.d_item + fi], g);
-      } else if (fi < a.d_item + a.d_act) {
-        atomicAdd(&s_act[act * a.d_act + fi - a.d_item], g);
-      } else {
-        atomicAdd(&s_time[bucket * a.d_time + fi - a.d_item - a.d_act], g);
+        else atomicAdd(&a.g_item[(long long)item * a.d_item + fi], g);
       }
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < a.nb * a.d_time; i += blockDim.x)
-    if (s_time[i] != 0.f) atomicAdd(&a.g_time[i], s_time[i]);
-  for (int i = threadIdx.x; i < a.n_actions * a.d_act; i += blockDim.x)
-    if (s_act[i] != 0.f) atomicAdd(&a.g_act[i], s_act[i]);
+  // g_act[r, f] += Σ_c S_act[r, c]·W_tp[d_item + f, c]; likewise the time rows
+  for (int i = threadIdx.x; i < a.n_actions * a.d_act + a.nb * a.d_time; i += blockDim.x) {
+    const bool is_act = i < a.n_actions * a.d_act;
+    const int k = is_act ? i : i - a.n_actions * a.d_act;
+    const int w = is_act ? a.d_act : a.d_time;
+    const int r = k / w, f = (is_act ? a.d_item : a.d_item + a.d_act) + k % w;
+    const float* S = (is_act ? s_act : s_time) + r * d;
+    float g = 0.f;
+    for (int c = 0; c < d; ++c) g = fmaf(S[c], s_wt[c * F + f], g);
+    if (g != 0.f) atomicAdd(is_act ? &a.g_act[k] : &a.g_time[k], g);
+  }
   for (int i = threadIdx.x; i < n_item; i += blockDim.x)
     if (s_item[i] != 0.f) atomicAdd(&a.g_item[i], s_item[i]);
 }
@@ -141,11 +166,13 @@ __global__ void pos_grad_kernel(EmbedBwdArgs a) {
 void embed_bwd(const EmbedBwdArgs& a, cudaStream_t st) {
   const long long T = (long long)a.B * a.Lp;
   const int F = a.d_item + a.d_act + a.d_time;
-  int item_in_smem = (a.vocab * a.d_item <= 12288) ? 1 : 0;
-  const int smem = 4 * (F * a.d + a.nb * a.d_time + a.n_actions * a.d_act + (item_in_smem ? a.vocab * a.d_item : 0));
-  const int tpb = 4096;
-  smem_attr(embed_bwd_kernel, 96 * 1024);
-  launch(embed_bwd_kernel, cdiv(T, tpb), 256, smem, st, a, tpb, item_in_smem);
+  if (a.d > 64) { fprintf(stderr, "embed_bwd: d = %d > 64 not supported\n", a.d); abort(); }
+  const int base = 4 * (F * a.d + (a.n_actions + a.nb) * a.d);
+  const int item_in_smem = (base + 4LL * a.vocab * a.d_item <= 64 * 1024) ? 1 : 0;
+  const int smem = base + (item_in_smem ? 4 * a.vocab * a.d_item : 0);
+  smem_attr(embed_bwd_kernel, smem);
+  const int grid = (int)std::min<long long>(cdiv(T, kEmbedBwdThreads / 32), 148 * 4);
+  launch(embed_bwd_kernel, grid, kEmbedBwdThreads, smem, st, a, item_in_smem);
   launch(pos_grad_kernel, a.L, 32 * cdiv(a.d, 32), 0, st, a);
 }
 

@@ -10,6 +10,8 @@
 #include "serve.cuh"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 namespace longer {
 
@@ -93,18 +95,75 @@ void target_rows(const TargetArgs& a, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ cached attention
-// One CTA per (user, 128-candidate tile, head).  All queries are target rows (global rank m-1):
-// they see every non-pad sequence key and every cached global, plus their own key appended last.
-// Exact two-pass softmax; S = Q·K_cacheᵀ on the tensor core (TMEM), the own key in registers.
+// One CTA per (user, 128-candidate tile, head); two CTAs per SM.  All queries are target rows
+// (global rank m-1): they see every non-pad sequence key and every cached global, plus their own
+// key appended last (attention_block_cached, attention.py:215-236).  One pass over the cached
+// keys: per 128-key chunk, S = Q·Kᵀ on the tensor core (TMEM), the row max / sum online, P (bf16)
+// written over the chunk's K tile, O += P·V in TMEM.  The running max m is only moved when a chunk
+// exceeds it by more than kRescale (then O is rescaled in TMEM): numerator and denominator share
+// the same m, so the result is exact, and P ≤ e^kRescale stays well inside bf16 / fp32 range.  The
+// own key is handled in registers.  Rows move between HBM and the canonical tiles with
+// warp-cooperative loads (8 rows × 64 contiguous bytes per instruction; conflict-free 16-byte
+// shared stores), each worker warp owning the 32 rows of its TMEM lane quarter.
+constexpr float kRescale = 8.f;
+
+// the warp's 32 rows [0, 32) of a row-major bf16 matrix (row stride ld) → canonical tile rows
+// [t0, t0 + 32) (K = DH); rows ≥ nvalid are zero-filled
 template <int DH>
-__global__ void __launch_bounds__(kThreads, 1) serve_attn_kernel(ServeAttnArgs a) {
+__device__ __forceinline__ void warp_rows_to_canon(bf16* tile, int t0, const bf16* src, long long ld, int nvalid,
+                                                   int lane) {
+  const int lr = lane & 7, kc = lane >> 3;
+  uint4 v[4][DH / 32];
+#pragma unroll
+  for (int rb = 0; rb < 4; ++rb)
+#pragma unroll
+    for (int k = 0; k < DH / 32; ++k) {
+      const int r = rb * 8 + lr;
+      v[rb][k] = r < nvalid ? *reinterpret_cast<const uint4*>(src + r * ld + (4 * k + kc) * 8) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+  for (int rb = 0; rb < 4; ++rb)
+#pragma unroll
+    for (int k = 0; k < DH / 32; ++k)
+      *reinterpret_cast<uint4*>(tile + canon(t0 + rb * 8 + lr, (4 * k + kc) * 8, DH)) = v[rb][k];
+}
+
+// the reverse: canonical tile rows [t0, t0 + 32) → the warp's rows of dst (rows ≥ nvalid skipped)
+template <int DH>
+__device__ __forceinline__ void warp_canon_to_rows(bf16* dst, long long ld, const bf16* tile, int t0, int nvalid,
+                                                   int lane) {
+  const int lr = lane & 7, kc = lane >> 3;
+#pragma unroll
+  for (int rb = 0; rb < 4; ++rb)
+#pragma unroll
+    for (int k = 0; k < DH / 32; ++k) {
+      const int r = rb * 8 + lr;
+      const uint4 v = *reinterpret_cast<const uint4*>(tile + canon(t0 + r, (4 * k + kc) * 8, DH));
+      if (r < nvalid) *reinterpret_cast<uint4*>(dst + r * ld + (4 * k + kc) * 8) = v;
+    }
+}
+
+__device__ __forceinline__ float dot8_bf16(uint4 a, uint4 b) {
+  const __nv_bfloat162* x = reinterpret_cast<const __nv_bfloat162*>(&a);
+  const __nv_bfloat162* y = reinterpret_cast<const __nv_bfloat162*>(&b);
+  float acc = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 p = __bfloat1622float2(x[i]), q = __bfloat1622float2(y[i]);
+    acc = fmaf(p.x, q.x, fmaf(p.y, q.y, acc));
+  }
+  return acc;
+}
+
+template <int DH>
+__global__ void __launch_bounds__(kThreads, 2) serve_attn_kernel(ServeAttnArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   constexpr int kC = 128;
+  constexpr int kKP = 128 * (DH > kC ? DH : kC);     // K tile, then the chunk's P tile
   bf16* sQ = reinterpret_cast<bf16*>(smem_raw);
-  bf16* sK = sQ + 128 * DH;
-  bf16* sV = sK + kC * DH;
-  bf16* sP = sV + kC * DH;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 128 * kC);
+  bf16* sV = sQ + 128 * DH;
+  bf16* sKP = sV + kC * DH;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKP + kKP);
   uint64_t* bar_a = bars;
   uint64_t* bar_d = bars + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
@@ -129,21 +188,15 @@ __global__ void __launch_bounds__(kThreads, 1) serve_attn_kernel(ServeAttnArgs a
   const int nchunk = (a.nk + kC - 1) / kC;
   if (warp == 0) {
     if (lane == 0) {
-      const uint32_t aQ = sm100::smem_u32(sQ), aK = sm100::smem_u32(sK), aV = sm100::smem_u32(sV);
-      const uint32_t aP = sm100::smem_u32(sP);
+      const uint32_t aQ = sm100::smem_u32(sQ), aV = sm100::smem_u32(sV), aKP = sm100::smem_u32(sKP);
       uint32_t pa = 0;
       auto wait_a = [&]() { sm100::mbar_wait(bar_a, pa); pa ^= 1; sm100::tc_fence_after(); };
       for (int c = 0; c < nchunk; ++c) {
         wait_a();
-        mma(T_S, Opnd{aQ, DH, 0}, Opnd{aK, DH, 0}, DH / 16, kC, false);
-        sm100::mma_commit(bar_d);
-      }
-      for (int c = 0; c < nchunk; ++c) {
-        wait_a();
-        mma(T_S, Opnd{aQ, DH, 0}, Opnd{aK, DH, 0}, DH / 16, kC, false);
+        mma(T_S, Opnd{aQ, DH, 0}, Opnd{aKP, DH, 0}, DH / 16, kC, false);
         sm100::mma_commit(bar_d);
         wait_a();
-        mma(T_O, Opnd{aP, kC, 0}, Opnd{aV, DH, 1}, kC / 16, DH, c > 0);
+        mma(T_O, Opnd{aKP, kC, 0}, Opnd{aV, DH, 1}, kC / 16, DH, c > 0);
         sm100::mma_commit(bar_d);
       }
     }
@@ -153,104 +206,119 @@ __global__ void __launch_bounds__(kThreads, 1) serve_attn_kernel(ServeAttnArgs a
     const uint32_t lo = (uint32_t)(q * 32) << 16;
     const float scale = rsqrtf((float)(a.D / a.heads));
     const int npg = a.npg[u];
-    const int cand = tile * 128 + row;
-    const bool qrow = cand < a.C;
-    const long long qr = (long long)u * a.C + cand;                 // candidate row index
-    const bf16* Kb = a.K + u * a.sk + hd * DH;
-    const bf16* Vb = a.V + u * a.sv + hd * DH;
+    const int c_base = tile * 128 + q * 32;                         // the warp's first candidate
+    const int nrow = min(32, a.C - c_base);                         // its valid rows
+    const bool qrow = lane < nrow;
+    const long long r_base = (long long)u * a.C + c_base;
     uint32_t pd = 0;
     auto signal = [&]() { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(bar_a); };
     auto wait_d = [&]() { sm100::mbar_wait(bar_d, pd); pd ^= 1; sm100::tc_fence_after(); };
-    // own query / key / value rows
+    // own query rows → sQ, and q·k_own for each of them (lanes lr + 8·kc share a row)
+    float s_own;
+    {
+      const int lr = lane & 7, kc = lane >> 3;
+      float part[4];
 #pragma unroll
-    for (int c = 0; c < DH; c += 8) {
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (qrow) v = *reinterpret_cast<const uint4*>(a.Q + qr * a.ldq + hd * DH + c);
-      *reinterpret_cast<uint4*>(sQ + canon(row, c, DH)) = v;
-    }
-    float s_own = -INFINITY;
-    if (qrow) {
-      float acc = 0.f;
-      const bf16* qp = a.Q + qr * a.ldq + hd * DH;
-      const bf16* kp = a.Kown + qr * a.ldown + hd * DH;
-      for (int c = 0; c < DH; ++c) acc = fmaf(__bfloat162float(qp[c]), __bfloat162float(kp[c]), acc);
-      s_own = acc * scale;
+      for (int rb = 0; rb < 4; ++rb) {
+        const int r = rb * 8 + lr;
+        part[rb] = 0.f;
+#pragma unroll
+        for (int k = 0; k < DH / 32; ++k) {
+          const int col = hd * DH + (4 * k + kc) * 8;
+          uint4 qv = make_uint4(0, 0, 0, 0), kv = qv;
+          if (r < nrow) {
+            qv = *reinterpret_cast<const uint4*>(a.Q + (r_base + r) * a.ldq + col);
+            kv = *reinterpret_cast<const uint4*>(a.Kown + (r_base + r) * a.ldown + col);
+          }
+          *reinterpret_cast<uint4*>(sQ + canon(q * 32 + r, (4 * k + kc) * 8, DH)) = qv;
+          part[rb] += dot8_bf16(qv, kv);
+        }
+        part[rb] += __shfl_xor_sync(0xffffffffu, part[rb], 8);
+        part[rb] += __shfl_xor_sync(0xffffffffu, part[rb], 16);
+      }
+      s_own = 0.f;
+#pragma unroll
+      for (int rb = 0; rb < 4; ++rb) {
+        const float v = __shfl_sync(0xffffffffu, part[rb], lane & 7);
+        if ((lane >> 3) == rb) s_own = v;
+      }
+      s_own = qrow ? s_own * scale : -INFINITY;
     }
     float m = s_own, l = qrow ? 1.f : 0.f;                          // the own key is always visible
     auto visible = [&](int key) { return key < a.nk && (key >= a.ns || a.goff + key >= npg); };
+    const bf16* Kb = a.K + u * a.sk + hd * DH;
+    const bf16* Vb = a.V + u * a.sv + hd * DH;
     for (int c = 0; c < nchunk; ++c) {
-      const int c0 = c * kC;
-#pragma unroll
-      for (int cc = 0; cc < DH; cc += 8) {
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (c0 + row < a.nk) v = *reinterpret_cast<const uint4*>(Kb + (long long)(c0 + row) * a.ldk + cc);
-        *reinterpret_cast<uint4*>(sK + canon(row, cc, DH)) = v;
-      }
+      const int c0 = c * kC, k0 = c0 + q * 32;
+      // the P·V MMA of chunk c-1 has completed (wait_d below): both tiles are free
+      warp_rows_to_canon<DH>(sKP, q * 32, Kb + (long long)k0 * a.ldk, a.ldk, a.nk - k0, lane);
+      warp_rows_to_canon<DH>(sV, q * 32, Vb + (long long)k0 * a.ldv, a.ldv, a.nk - k0, lane);
       signal();
-      wait_d();
+      wait_d();                                                     // S = Q·Kᵀ
+      float cm = -INFINITY;
 #pragma unroll 1
       for (int j0 = 0; j0 < kC; j0 += 32) {
         float s[32];
         tmem_row<32>(T_S + lo + j0, s);
-        if (!qrow) continue;
-        float cm = -INFINITY;
 #pragma unroll
-        for (int v = 0; v < 32; ++v) {
-          s[v] = visible(c0 + j0 + v) ? s[v] * scale : -INFINITY;
-          cm = fmaxf(cm, s[v]);
+        for (int v = 0; v < 32; ++v)
+          if (visible(c0 + j0 + v)) cm = fmaxf(cm, s[v] * scale);
+      }
+      const bool grow = qrow && cm > m + kRescale;
+      if (__any_sync(0xffffffffu, grow)) {
+        const float f = grow ? __expf(m - cm) : 1.f;
+        if (grow) { l *= f; m = cm; }
+        if (c > 0) {
+#pragma unroll 1
+          for (int j0 = 0; j0 < DH; j0 += 32) {
+            float o[32];
+            tmem_row<32>(T_O + lo + j0, o);
+#pragma unroll
+            for (int v = 0; v < 32; ++v) o[v] *= f;
+            tmem_row_st<32>(T_O + lo + j0, o);
+          }
         }
-        if (cm == -INFINITY) continue;
-        const float mn = fmaxf(m, cm);
+      }
+#pragma unroll 1
+      for (int j0 = 0; j0 < kC; j0 += 32) {
+        float s[32];
+        tmem_row<32>(T_S + lo + j0, s);
         float add = 0.f;
 #pragma unroll
-        for (int v = 0; v < 32; ++v) add += __expf(s[v] - mn);
-        l = l * __expf(m - mn) + add;
-        m = mn;
-      }
-    }
-    const float rl = l > 0.f ? 1.f / l : 0.f;
-    for (int c = 0; c < nchunk; ++c) {
-      const int c0 = c * kC;
-#pragma unroll
-      for (int cc = 0; cc < DH; cc += 8) {
-        uint4 kv = make_uint4(0, 0, 0, 0), vv = kv;
-        if (c0 + row < a.nk) {
-          kv = *reinterpret_cast<const uint4*>(Kb + (long long)(c0 + row) * a.ldk + cc);
-          vv = *reinterpret_cast<const uint4*>(Vb + (long long)(c0 + row) * a.ldv + cc);
+        for (int v = 0; v < 32; ++v) {
+          s[v] = (qrow && visible(c0 + j0 + v)) ? __expf(s[v] * scale - m) : 0.f;
+          add += s[v];
         }
-        *reinterpret_cast<uint4*>(sK + canon(row, cc, DH)) = kv;
-        *reinterpret_cast<uint4*>(sV + canon(row, cc, DH)) = vv;
+        l += add;
+        store_row(sKP, row, kC, s, 32, j0);                         // P over the (consumed) K tile
       }
       signal();
-      wait_d();
+      wait_d();                                                     // O += P·V
+    }
+    // epilogue: ctx = (O + p_own·v_own) / l, staged through the (free) tiles for coalesced I/O
+    const float rl = l > 0.f ? 1.f / l : 0.f;
+    const float p_own = qrow ? __expf(s_own - m) : 0.f;
+    warp_rows_to_canon<DH>(sV, q * 32, a.Vown + r_base * a.ldown + hd * DH, a.ldown, nrow, lane);
+    __syncwarp();
 #pragma unroll 1
-      for (int j0 = 0; j0 < kC; j0 += 32) {
-        float s[32];
-        tmem_row<32>(T_S + lo + j0, s);
+    for (int j0 = 0; j0 < DH; j0 += 32) {
+      float o[32];
+      tmem_row<32>(T_O + lo + j0, o);
 #pragma unroll
-        for (int v = 0; v < 32; ++v) s[v] = (qrow && visible(c0 + j0 + v)) ? __expf(s[v] * scale - m) * rl : 0.f;
-        store_row(sP, row, kC, s, 32, j0);
+      for (int cc = 0; cc < 32; cc += 8) {
+        const uint4 vv = *reinterpret_cast<const uint4*>(sV + canon(row, j0 + cc, DH));
+        const __nv_bfloat162* vp = reinterpret_cast<const __nv_bfloat162*>(&vv);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 w = __bfloat1622float2(vp[i]);
+          o[cc + 2 * i] = (o[cc + 2 * i] + p_own * w.x) * rl;
+          o[cc + 2 * i + 1] = (o[cc + 2 * i + 1] + p_own * w.y) * rl;
+        }
       }
-      signal();
-      wait_d();
+      store_row(sKP, row, DH, o, 32, j0);
     }
-    float o[DH];
-    tmem_row<DH>(T_O + lo, o);
-    if (qrow) {
-      const float p_own = __expf(s_own - m) * rl;
-      const bf16* vp = a.Vown + qr * a.ldown + hd * DH;
-      bf16* dst = a.ctx + qr * a.ldc + hd * DH;
-#pragma unroll
-      for (int cc = 0; cc < DH; cc += 8) {
-        float w[8];
-#pragma unroll
-        for (int v = 0; v < 8; ++v) w[v] = o[cc + v] + p_own * __bfloat162float(vp[cc + v]);
-        uint4 pk;
-        pk.x = sm100::pack_bf16(w[0], w[1]); pk.y = sm100::pack_bf16(w[2], w[3]);
-        pk.z = sm100::pack_bf16(w[4], w[5]); pk.w = sm100::pack_bf16(w[6], w[7]);
-        *reinterpret_cast<uint4*>(dst + cc) = pk;
-      }
-    }
+    __syncwarp();
+    warp_canon_to_rows<DH>(a.ctx + r_base * a.ldc + hd * DH, a.ldc, sKP, q * 32, nrow, lane);
   }
   sm100::tc_fence_before();
   __syncthreads();
@@ -259,10 +327,10 @@ __global__ void __launch_bounds__(kThreads, 1) serve_attn_kernel(ServeAttnArgs a
 
 template <int DH>
 int launch_serve(const ServeAttnArgs& a, cudaStream_t st) {
-  const int smem = (128 * DH + 2 * 128 * DH + 128 * 128) * 2 + 64;
-  smem_attr(serve_attn_kernel<DH>, 227 * 1024);
+  const int smem = (128 * DH + 128 * DH + 128 * (DH > 128 ? DH : 128)) * 2 + 64;
+  smem_attr(serve_attn_kernel<DH>, smem);
   const int tiles = (a.C + 127) / 128;
-  launch(serve_attn_kernel<DH>, a.U * tiles * a.heads, kThreads, std::max(smem, 116 * 1024), st, a);
+  launch(serve_attn_kernel<DH>, a.U * tiles * a.heads, kThreads, smem, st, a);
   return (int)cudaGetLastError();
 }
 
@@ -344,47 +412,124 @@ int serve_attn(const ServeAttnArgs& a, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ head over candidate rows
-// head of forward_tensor (pkg/src/longrec/model.py:346-362) with the cached CLS row and user-side
-// features of the candidate's user (score_with_cache, serving.py:160-166).
-__global__ void serve_head_kernel(ServeHeadArgs a) {
+// Head of every target row: forward_tensor's head (pkg/src/longrec/model.py:346-362) with the
+// cached CLS row and user-side features of the candidate's user (score_with_cache,
+// serving.py:160-166), in fp32 like the training head.  A warp takes kHeadRows rows at a time,
+// lane j = hidden unit j (+32, …).  W1 / b1 / w2 stay in shared memory for the whole persistent
+// kernel (lane j reads column j of W1: conflict-free).  A row group is kHeadRows candidates of ONE
+// user.  The head input [t, c, t·c, t·t, u_d] is never materialised: the warp stages its rows' t
+// and the user's c and u_d (coalesced), and for every 4 input columns i the 16 W1 words of the
+// four segments (rows i, D+i, 2D+i, 3D+i) are loaded once and applied to all kHeadRows rows from
+// float4 broadcasts of t and c.
+constexpr int kHeadRows = 8, kHeadThreads = 512;
+
+template <bool kSmemW>
+__global__ void __launch_bounds__(kHeadThreads) serve_head_kernel(ServeHeadArgs a) {
   pdl_trigger();
   pdl_wait();
-  extern __shared__ float s_in[];
-  const long long r = blockIdx.x;
-  const int u = (int)(r / a.C);
-  const int D = a.D, HIN = 4 * D + 2 * a.d;
-  const float* t = a.x + r * D;
-  const float* c = a.cls + (long long)u * D;
-  for (int i = threadIdx.x; i < D; i += blockDim.x) {
-    const float tv = t[i], cv = c[i];
-    s_in[i] = tv; s_in[D + i] = cv; s_in[2 * D + i] = tv * cv; s_in[3 * D + i] = tv * tv;
-  }
-  for (int i = threadIdx.x; i < 2 * a.d; i += blockDim.x) s_in[4 * D + i] = a.ud[(long long)u * 2 * a.d + i];
+  extern __shared__ float4 sm4[];
+  float* sm = reinterpret_cast<float*>(sm4);
+  const int D = a.D, d2 = 2 * a.d, HIN = 4 * D + d2, hh = a.hh;
+  const int XS = kHeadRows * D + D + d2;                   // per warp: t [kHeadRows][D], c [D], u_d [2d]
+  float* sX = sm;
+  float* sW = sX + (kHeadThreads / 32) * XS;               // [HIN][hh]
+  float* sB = sW + (kSmemW ? HIN * hh : 0);                 // b1 [hh], w2 [hh]
+  if (kSmemW)
+    for (int i = threadIdx.x; i < HIN * hh; i += blockDim.x) sW[i] = a.w1[i];
+  for (int i = threadIdx.x; i < hh; i += blockDim.x) { sB[i] = a.b1[i]; sB[hh + i] = a.w2[i]; }
+  const float* W = kSmemW ? sW : a.w1;
   __syncthreads();
-  float* s_h = s_in + HIN;
   const int wid = threadIdx.x / 32, lane = threadIdx.x & 31, nw = blockDim.x / 32;
-  for (int j = wid; j < a.hh; j += nw) {
-    float acc = 0.f;
-    for (int i = lane; i < HIN; i += 32) acc = fmaf(s_in[i], __ldg(a.w1 + i * a.hh + j), acc);
-    acc = warp_sum(acc) + a.b1[j];
-    if (lane == 0) s_h[j] = gelu_f(acc);
-  }
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    float acc = 0.f;
-    for (int j = threadIdx.x; j < a.hh; j += 32) acc = fmaf(s_h[j], a.w2[j], acc);
-    acc = warp_sum(acc);
-    if (threadIdx.x == 0) {
-      const float z = acc + a.b2[0];
-      const float e = __expf(-fabsf(z));
-      a.probs[r] = z >= 0.f ? 1.f / (1.f + e) : e / (1.f + e);
+  float* x = sX + wid * XS;
+  float* xc = x + kHeadRows * D;
+  float* xu = xc + D;
+  const float b2 = a.b2[0];
+  const int gpu_ = (a.C + kHeadRows - 1) / kHeadRows;      // groups per user
+  const long long ngroups = (a.R / a.C) * gpu_;
+  for (long long g = (long long)blockIdx.x * nw + wid; g < ngroups; g += (long long)gridDim.x * nw) {
+    const int u = (int)(g / gpu_);
+    const int c0 = (int)(g % gpu_) * kHeadRows;
+    const long long r0 = (long long)u * a.C + c0;
+    const int nr = min(kHeadRows, a.C - c0);
+    __syncwarp();
+    const float4* t = reinterpret_cast<const float4*>(a.x + r0 * D);
+    for (int i = lane; i < kHeadRows * D / 4; i += 32)
+      reinterpret_cast<float4*>(x)[i] = i < nr * D / 4 ? t[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4* c = reinterpret_cast<const float4*>(a.cls + (long long)u * D);
+    for (int i = lane; i < D / 4; i += 32) reinterpret_cast<float4*>(xc)[i] = c[i];
+    for (int i = lane; i < d2; i += 32) xu[i] = a.ud[(long long)u * d2 + i];
+    __syncwarp();
+    float zp[kHeadRows];
+#pragma unroll
+    for (int q = 0; q < kHeadRows; ++q) zp[q] = 0.f;
+    for (int j = lane; j < hh; j += 32) {
+      float acc[kHeadRows];
+#pragma unroll
+      for (int q = 0; q < kHeadRows; ++q) acc[q] = sB[j];
+#pragma unroll 1
+      for (int i = 0; i < D; i += 4) {
+        float wt[4], wc[4], wtc[4], wtt[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          wt[e] = W[(i + e) * hh + j];
+          wc[e] = W[(D + i + e) * hh + j];
+          wtc[e] = W[(2 * D + i + e) * hh + j];
+          wtt[e] = W[(3 * D + i + e) * hh + j];
+        }
+        const float4 c4 = *reinterpret_cast<const float4*>(xc + i);
+        const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+        for (int q = 0; q < kHeadRows; ++q) {
+          const float4 t4 = *reinterpret_cast<const float4*>(x + q * D + i);
+          const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
+          float v = acc[q];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            v = fmaf(tv[e], wt[e], v);
+            v = fmaf(cv[e], wc[e], v);
+            v = fmaf(tv[e] * cv[e], wtc[e], v);
+            v = fmaf(tv[e] * tv[e], wtt[e], v);
+          }
+          acc[q] = v;
+        }
+      }
+#pragma unroll 1
+      for (int i = 0; i < d2; ++i) {
+        const float w = W[(4 * D + i) * hh + j];
+#pragma unroll
+        for (int q = 0; q < kHeadRows; ++q) acc[q] = fmaf(xu[i], w, acc[q]);
+      }
+      const float w2j = sB[hh + j];
+#pragma unroll
+      for (int q = 0; q < kHeadRows; ++q) zp[q] = fmaf(gelu_f(acc[q]), w2j, zp[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < kHeadRows; ++q) {
+      const float z = warp_sum(zp[q]) + b2;
+      if (lane == q && q < nr) {
+        const float e = __expf(-fabsf(z));
+        a.probs[r0 + q] = z >= 0.f ? 1.f / (1.f + e) : e / (1.f + e);
+      }
     }
   }
 }
 
 void serve_head(const ServeHeadArgs& a, cudaStream_t st) {
-  const int smem = 4 * (4 * a.D + 2 * a.d + a.hh);
-  if (a.R) launch(serve_head_kernel, (unsigned)a.R, 128, smem, st, a);
+  if (!a.R) return;
+  if (a.D % 4) { fprintf(stderr, "serve_head: D = %d not a multiple of 4\n", a.D); abort(); }
+  const int XS = kHeadRows * a.D + a.D + 2 * a.d;
+  const int sx = 4 * ((kHeadThreads / 32) * XS + 2 * a.hh);
+  const int sw = 4 * (4 * a.D + 2 * a.d) * a.hh;
+  const long long groups = (a.R / a.C) * ((a.C + kHeadRows - 1) / kHeadRows);
+  const long long blocks = (groups + kHeadThreads / 32 - 1) / (kHeadThreads / 32);
+  const unsigned grid = (unsigned)std::min<long long>(blocks, 148);
+  if (sx + sw <= 220 * 1024) {
+    smem_attr(serve_head_kernel<true>, sx + sw);
+    launch(serve_head_kernel<true>, grid, kHeadThreads, sx + sw, st, a);
+  } else {
+    smem_attr(serve_head_kernel<false>, sx);
+    launch(serve_head_kernel<false>, grid, kHeadThreads, sx, st, a);
+  }
 }
 
 }  // namespace longer

@@ -104,6 +104,33 @@ def test_many_users_many_candidates_equal_full_forward():
     assert np.max(np.abs(p - pf)) <= 2e-3
 
 
+@pytest.mark.parametrize("heads,qk_gain", [(1, 1.0), (1, 6.0), (4, 6.0)], ids=["dh128", "dh128-sharp", "dh32-sharp"])
+def test_c2_partial_tiles_and_rescaled_softmax_equal_full_forward(heads, qk_gain):
+    """c2 widths (502 cached cross keys = 4 key chunks of 128), 3 users × 300 candidates (a partial
+    128-candidate tile and a partial 8-row head group), mixed history lengths.  qk_gain scales the
+    query / key projections so that the scores spread over tens of units: the single-pass cached
+    attention must then move its running max (and rescale O in TMEM) between key chunks."""
+    from paper_2505_04421_b200 import serving as S
+    from paper_2505_04421_b200.params import init_params
+    cfg = ModelConfig(**dict(C2, heads=heads)).validate()
+    P = init_params(cfg, seed=0)
+    rng = np.random.default_rng(7)
+    for name in list(P):
+        if name.endswith(("w_q", "w_k")):
+            P[name] = P[name] * qk_gain
+        elif name.startswith("tables."):
+            P[name] = P[name] + 0.05 * rng.standard_normal(P[name].shape)
+    model = _model(cfg, P)
+    samples = [synthetic_samples(cfg, 1, seed=70 + i, n_events=n)[0] for i, n in enumerate([2000, 900, 17])]
+    users = tensorize([Sample(s.events, s.user_features, Candidate(0, s.candidate.timestamp), 0)
+                       for s in samples], cfg)
+    cand = rng.integers(cfg.vocab, size=(3, 300)).astype(np.int32)
+    cache = S.build_caches_batch(model, users, [s.candidate.timestamp for s in samples])
+    p = S.score_candidates(model, cache, cand).cpu().numpy()
+    pf = model.forward(_expand(users, cand)).cpu().numpy().reshape(cand.shape)
+    assert np.max(np.abs(p - pf)) <= 3e-3, np.abs(p - pf).max()
+
+
 def test_single_user_api_and_errors():
     from paper_2505_04421_b200 import serving as S
     cfg = ModelConfig(L=64, d=16, K=4, k=8, N=2, m=3, merge_mode="inner", n_users=64).validate()
