@@ -314,31 +314,37 @@ __global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a, cons
 // [key][column], rows past the sample's keys read as zero) into 128-byte-swizzled tiles, issuing
 // the next chunk as soon as the MMAs reading the current one have completed.
 // Packing as in the forward (pack > 1: non-BIG only; key rows of dV / dK map back to their samples).
-template <int DH, bool TMA>
+// SHORT (head width ≤ 128, one sample per CTA with nq ≤ 64 — the cross layer): the 64-row query
+// tiles of BIG free 64 KB of shared memory for a second K / V buffer, so the TMA of chunk i+2 is in
+// flight while chunk i+1 is computed (the chunk sequence is pass 1 then pass 2), and the dV / dK
+// rows leave through a per-warp shared-memory transpose as 64-byte row segments.
+template <int DH, bool TMA, bool SHORT>
 __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, const __grid_constant__ CUtensorMap tmK,
                                                                   const __grid_constant__ CUtensorMap tmV, int pack) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   constexpr bool BIG = DH > 128;
-  constexpr int QR = BIG ? 64 : 128;              // stored query rows
+  static_assert(!SHORT || (TMA && !BIG), "SHORT: TMA path at head width <= 128");
+  constexpr int QR = (BIG || SHORT) ? 64 : 128;   // stored query rows
+  constexpr int KVB = SHORT ? 2 : 1;              // K / V buffers
   bf16* sQ = reinterpret_cast<bf16*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   bf16* sdO = sQ + QR * DH;
-  bf16* sK = sdO + QR * DH;
+  bf16* sK = sdO + QR * DH;                       // buffer b: K at sK + b·2·kC·DH, V right after it
   bf16* sV = sK + kC * DH;
-  bf16* sdS = sV + kC * DH;                       // QR x kC  (pre-scaled by 1/sqrt(dh))
+  bf16* sdS = sK + KVB * 2 * kC * DH;             // QR x kC  (pre-scaled by 1/sqrt(dh))
   bf16* sP = sdS + QR * kC;                       // QR x kC  (after dS: dS's M-row overread stays in smem)
   float* sDp = reinterpret_cast<float*>(sP + QR * kC);       // [2][128] partial D_i of the two groups
   uint64_t* bars = reinterpret_cast<uint64_t*>(sDp + 256);
   uint64_t* bar_a = bars;
   uint64_t* bar_d = bars + 1;
-  uint64_t* bar_kv = bars + 2;                    // TMA: K / V chunk landed
-  uint64_t* bar_m = bars + 3;                     // TMA: the MMAs reading the chunk are done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+  uint64_t* bar_m = bars + 2;                     // TMA: the MMAs reading a chunk are done
+  uint64_t* bar_kv = bars + 3;                    // [KVB] TMA: K / V chunk landed in buffer b
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 + KVB);
   const int b0 = (blockIdx.x / a.heads) * pack, hd = blockIdx.x % a.heads;
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     sm100::mbar_init(bar_a, 32 * 2 * kWorkers);
     sm100::mbar_init(bar_d, 1);
-    sm100::mbar_init(bar_kv, 1);
+    for (int b = 0; b < KVB; ++b) sm100::mbar_init(&bar_kv[b], 1);
     sm100::mbar_init(bar_m, 1);
     sm100::fence_barrier_init();
   }
@@ -354,27 +360,43 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint32_t aQ = sm100::smem_u32(sQ), adO = sm100::smem_u32(sdO), aK = sm100::smem_u32(sK);
-      const uint32_t aV = sm100::smem_u32(sV), aP = sm100::smem_u32(sP), adS = sm100::smem_u32(sdS);
-      uint32_t pa = 0, pkv = 0, pm = 0;
+      const uint32_t aQ = sm100::smem_u32(sQ), adO = sm100::smem_u32(sdO), aK0 = sm100::smem_u32(sK);
+      const uint32_t aP = sm100::smem_u32(sP), adS = sm100::smem_u32(sdS);
+      constexpr uint32_t kBufBytes = 2 * kC * DH * 2;
+      uint32_t pa = 0, pkv0 = 0, pkv1 = 0, pm = 0;
       auto wait_a = [&]() { sm100::mbar_wait(bar_a, pa); pa ^= 1; sm100::tc_fence_after(); };
-      auto load_kv = [&](int c) {
-        sm100::mbar_arrive_expect_tx(bar_kv, 2 * kC * DH * 2);
+      // the chunk sequence: pass 1 over chunks 0..n-1, then (n > 1) pass 2 over them again; load i
+      // goes to buffer i % KVB
+      const int nload = nchunk > 1 ? 2 * nchunk : 1;
+      auto load_kv = [&](int i) {
+        const int c = i % nchunk, bsel = i % KVB;
+        bf16* dK = sK + bsel * 2 * kC * DH;
+        bf16* dV = dK + kC * DH;
+        sm100::mbar_arrive_expect_tx(&bar_kv[bsel], 2 * kC * DH * 2);
 #pragma unroll
-        for (int i = 0; i < DH / 64; ++i) {
+        for (int i2 = 0; i2 < DH / 64; ++i2) {
           if (pack > 1) {
-            sm100::tma_load_2d(sK + i * kC * 64, &tmK, bar_kv, hd * DH + 64 * i, b0 * a.nk);
-            sm100::tma_load_2d(sV + i * kC * 64, &tmV, bar_kv, hd * DH + 64 * i, b0 * a.nk);
+            sm100::tma_load_2d(dK + i2 * kC * 64, &tmK, &bar_kv[bsel], hd * DH + 64 * i2, b0 * a.nk);
+            sm100::tma_load_2d(dV + i2 * kC * 64, &tmV, &bar_kv[bsel], hd * DH + 64 * i2, b0 * a.nk);
           } else {
-            sm100::tma_load_3d(sK + i * kC * 64, &tmK, bar_kv, hd * DH + 64 * i, c * kC, b0);
-            sm100::tma_load_3d(sV + i * kC * 64, &tmV, bar_kv, hd * DH + 64 * i, c * kC, b0);
+            sm100::tma_load_3d(dK + i2 * kC * 64, &tmK, &bar_kv[bsel], hd * DH + 64 * i2, c * kC, b0);
+            sm100::tma_load_3d(dV + i2 * kC * 64, &tmV, &bar_kv[bsel], hd * DH + 64 * i2, c * kC, b0);
           }
         }
       };
-      auto wait_kv = [&]() { sm100::mbar_wait(bar_kv, pkv); pkv ^= 1; };
+      auto wait_kv = [&](int i) {
+        if (i % KVB == 0) { sm100::mbar_wait(&bar_kv[0], pkv0); pkv0 ^= 1; }
+        else { sm100::mbar_wait(&bar_kv[KVB - 1], pkv1); pkv1 ^= 1; }
+      };
       auto mma_done = [&]() { sm100::mma_commit(bar_m); sm100::mbar_wait(bar_m, pm); pm ^= 1; };
-      // S = Q·Kᵀ and dP = dO·Vᵀ of the resident chunk
-      auto mma_s_dp = [&]() {
+      // once the MMAs reading load i are done, its buffer takes load i + KVB
+      auto refill = [&](int i) {
+        if (i + KVB < nload) { mma_done(); load_kv(i + KVB); }
+      };
+      auto kaddr = [&](int i) { return aK0 + (uint32_t)(i % KVB) * kBufBytes; };
+      // S = Q·Kᵀ and dP = dO·Vᵀ of the chunk of load i
+      auto mma_s_dp = [&](int i) {
+        const uint32_t aK = kaddr(i), aV = aK + kC * DH * 2;
         if constexpr (TMA) {
           mma(T_A, Opnd{aQ, DH, 0}, OpndSW{aK, kC, 0}, DH / 16, kC, false);
           mma(T_B, Opnd{adO, DH, 0}, OpndSW{aV, kC, 0}, DH / 16, kC, false);
@@ -386,28 +408,25 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
       if constexpr (TMA) {
         sm100::tma_prefetch(&tmK);
         sm100::tma_prefetch(&tmV);
-        load_kv(0);
+        for (int i = 0; i < KVB && i < nload; ++i) load_kv(i);
       }
       for (int c = 0; c < nchunk; ++c) {                            // pass 1: D = Σ_j P·dP
         wait_a();
-        if constexpr (TMA) wait_kv();
-        mma_s_dp();
+        if constexpr (TMA) wait_kv(c);
+        mma_s_dp(c);
         sm100::mma_commit(bar_d);
-        if constexpr (TMA) {
-          if (nchunk > 1) {                                         // next chunk (pass 2: chunk 0)
-            mma_done();
-            load_kv(c + 1 < nchunk ? c + 1 : 0);
-          }
-        }
+        if constexpr (TMA) refill(c);
       }
       constexpr int NH = BIG ? 2 : 1, NW = DH / NH;                // dV / dK column halves
       for (int c = 0; c < nchunk; ++c) {
+        const int i = nchunk > 1 ? nchunk + c : 0;                  // load index of this chunk
         if (nchunk > 1) {           // a single chunk's S and dP are still in TMEM from pass 1
           wait_a();                                                 // K, V chunk (+ Q, dO)
-          if constexpr (TMA) wait_kv();
-          mma_s_dp();
+          if constexpr (TMA) wait_kv(i);
+          mma_s_dp(i);
           sm100::mma_commit(bar_d);
         }
+        const uint32_t aK = kaddr(i);
         for (int h = 0; h < NH; ++h) {
           wait_a();                                                 // P, dS (h = 1: halves read out)
           const uint32_t co = (uint32_t)h * NW * 16;                // byte offset of column half h
@@ -424,10 +443,7 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
           sm100::mma_commit(bar_d);
         }
         if constexpr (TMA) {
-          if (nchunk > 1 && c + 1 < nchunk) {
-            mma_done();
-            load_kv(c + 1);
-          }
+          if (nchunk > 1) refill(i);
         }
       }
     }
@@ -462,9 +478,9 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
         *reinterpret_cast<uint4*>(tile + canon(row, grp * HC + c, DH)) = v;
       }
     };
-    const int qi = pack > 1 ? row % a.nq : (BIG ? row : query_of_row(row));
+    const int qi = pack > 1 ? row % a.nq : ((BIG || SHORT) ? row : query_of_row(row));
     const bool qrow = qi < a.nq && sr < pack && b0 + sr < a.B;
-    if (!BIG || row < QR) {
+    if (QR == 128 || row < QR) {
 #pragma unroll
       for (int c = grp * HC; c < grp * HC + HC; c += 8) {
         uint4 v = make_uint4(0, 0, 0, 0);
@@ -478,7 +494,7 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
       const float* dOr = a.dctx + b * a.sdc + (long long)qi * a.lddc + hd * DH;
 #pragma unroll
       for (int c = grp * HC; c < grp * HC + HC; c += 8) {
-        if (BIG && row >= QR) break;
+        if (QR < 128 && row >= QR) break;
         float v[8];
         if (qrow) {
           const float4 x = *reinterpret_cast<const float4*>(dOr + c), y = *reinterpret_cast<const float4*>(dOr + c + 4);
@@ -560,7 +576,7 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
           s[u] = p;
           dp[u] = p * (dp[u] - Di) * scale;
         }
-        if (!BIG || row < QR) {
+        if (QR == 128 || row < QR) {
           store_row(sP, row, kC, s, 32, j0);
           store_row(sdS, row, kC, dp, 32, j0);
         }
@@ -579,6 +595,33 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
         for (int c1 = r0; c1 < r1; c1 += 32) {
           float dv[32], dk[32];
           tmem_row2<32>(T_A + lo + c1, dv, T_B + lo + c1, dk);
+          if constexpr (SHORT) {
+            // through this warp's 2 × 2 KB of the (consumed) dS / P tiles: 16-byte segments
+            // XOR-swizzled, conflict-free both ways; out as 64-byte row segments
+            uint4* stg = reinterpret_cast<uint4*>(sdS) + (warp - 1) * 256;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int sl = lane * 4 + (j ^ ((lane >> 1) & 3));
+              stg[sl] = make_uint4(sm100::pack_bf16(dv[8 * j], dv[8 * j + 1]), sm100::pack_bf16(dv[8 * j + 2], dv[8 * j + 3]),
+                                   sm100::pack_bf16(dv[8 * j + 4], dv[8 * j + 5]), sm100::pack_bf16(dv[8 * j + 6], dv[8 * j + 7]));
+              stg[128 + sl] = make_uint4(sm100::pack_bf16(dk[8 * j], dk[8 * j + 1]), sm100::pack_bf16(dk[8 * j + 2], dk[8 * j + 3]),
+                                         sm100::pack_bf16(dk[8 * j + 4], dk[8 * j + 5]), sm100::pack_bf16(dk[8 * j + 6], dk[8 * j + 7]));
+            }
+            __syncwarp();
+            const int kbase = c0 + q * 32;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int r = k * 8 + (lane >> 2), sgm = lane & 3;
+              if (kbase + r < a.nk) {
+                const long long off = (long long)(kbase + r);
+                const int sl = r * 4 + (sgm ^ ((r >> 1) & 3));
+                *reinterpret_cast<uint4*>(a.dV + (long long)b0 * a.sdv + off * a.lddv + hd * DH + c1 + sgm * 8) = stg[sl];
+                *reinterpret_cast<uint4*>(a.dK + (long long)b0 * a.sdk + off * a.lddk + hd * DH + c1 + sgm * 8) = stg[128 + sl];
+              }
+            }
+            __syncwarp();
+            continue;
+          }
           if (!krow) continue;
 #pragma unroll
           for (int cc = 0; cc < 32; cc += 8) {
@@ -661,13 +704,13 @@ int launch_fwd(const AttnArgs& a, cudaStream_t st) {
   return launch_fwd_t<DH, false>(a, tK, tV, pack, st);
 }
 
-template <int DH, bool TMA>
+template <int DH, bool TMA, bool SHORT>
 int launch_bwd_t(const AttnArgs& a, const CUtensorMap& tK, const CUtensorMap& tV, int pack, cudaStream_t st) {
-  const int QR = DH > 128 ? 64 : 128;
-  const int smem = (2 * QR * DH + 2 * kC * DH + 2 * QR * kC) * 2 + 256 * 4 + 64 + 1024;
-  smem_attr(xattn_bwd_kernel<DH, TMA>, 227 * 1024);
-  launch(xattn_bwd_kernel<DH, TMA>, ((a.B + pack - 1) / pack) * a.heads, kThreads8, std::max(smem, 116 * 1024), st, a,
-         tK, tV, pack);
+  const int QR = (DH > 128 || SHORT) ? 64 : 128, KVB = SHORT ? 2 : 1;
+  const int smem = (2 * QR * DH + KVB * 2 * kC * DH + 2 * QR * kC) * 2 + 256 * 4 + 64 + 1024;
+  smem_attr(xattn_bwd_kernel<DH, TMA, SHORT>, 227 * 1024);
+  launch(xattn_bwd_kernel<DH, TMA, SHORT>, ((a.B + pack - 1) / pack) * a.heads, kThreads8, std::max(smem, 116 * 1024),
+         st, a, tK, tV, pack);
   return (int)cudaGetLastError();
 }
 
@@ -676,9 +719,16 @@ int launch_bwd(const AttnArgs& a, cudaStream_t st) {
   CUtensorMap tK{}, tV{};
   const int pack = pack_of<DH>(a);
   if constexpr (DH >= 64) {
-    if (kv_maps<DH>(a, pack, tK, tV)) return launch_bwd_t<DH, true>(a, tK, tV, pack, st);
+    if (kv_maps<DH>(a, pack, tK, tV)) {
+      if constexpr (DH <= 128) {
+        // one sample per CTA, ≤ 64 queries, several key chunks: double-buffered K / V
+        if (pack == 1 && a.nq <= 64 && a.nk > kC && g_knobs.attn_short)
+          return launch_bwd_t<DH, true, true>(a, tK, tV, pack, st);
+      }
+      return launch_bwd_t<DH, true, false>(a, tK, tV, pack, st);
+    }
   }
-  return launch_bwd_t<DH, false>(a, tK, tV, pack, st);
+  return launch_bwd_t<DH, false, false>(a, tK, tV, pack, st);
 }
 
 }  // namespace

@@ -113,3 +113,27 @@ def test_c5_real_shape_matches_oracle(min_events):
     assert_grads_close(grads, G, f"c5 min_events={min_events}")
     pf = model.forward(batch).cpu().numpy().astype(np.float64)
     assert np.max(np.abs(pf - p_ref)) <= 5e-3
+
+
+@pytest.mark.parametrize("heads", [1, 2], ids=["dh128", "dh64"])
+def test_cross_attention_backward_double_buffered_path(heads, monkeypatch):
+    """The cross layer's attention backward (35 queries, 503 keys = 4 chunks, one sample per CTA)
+    runs the SHORT variant: 64-row query tiles, two K / V buffers with the TMA of chunk i+2 in
+    flight, staged dV / dK stores.  Same oracle bar as above, and the same step as the
+    single-buffer variant (LONGER_ATTN_SHORT=0) up to fp32 accumulation order."""
+    cfg = ModelConfig(**dict(C2, heads=heads)).validate()
+    P = _perturbed(cfg, 17)
+    batch = synthetic_batch(cfg, 6, seed=9, min_events=1)
+    model = _model(cfg, P)
+    p, loss, grads = _run(model, batch)
+    p_ref, loss_ref, G = O.forward_backward(P, cfg, batch.as_dict())
+    assert np.max(np.abs(p - p_ref)) <= 5e-3
+    assert abs(loss - loss_ref) <= loss_tol(p_ref, batch.label)
+    assert_grads_close(grads, G, f"cross bwd short heads={heads}")
+    monkeypatch.setenv("LONGER_ATTN_SHORT", "0")
+    p2, loss2, grads2 = _run(model, batch)
+    np.testing.assert_allclose(p2, p, atol=1e-6)
+    top = max(np.abs(g).max() for g in grads.values())
+    for name in grads:                    # ~0 groups (e.g. b_k: softmax-invariant) are rounding noise
+        scale = max(np.abs(grads[name]).max(), 1e-2 * top)
+        assert np.abs(grads2[name] - grads[name]).max() <= 1e-3 * scale, name

@@ -1,29 +1,47 @@
-"""Top source lines by warp-stall samples from `ncu --page source --csv --print-source cuda,sass`."""
+"""Per-CUDA-source-line instruction and warp-stall shares from an ncu report's source page.
+Usage: python tools/ncu_lines.py report.ncu-rep [n] [kernel-substring]"""
+import collections
 import csv
+import io
+import subprocess
 import sys
-from collections import defaultdict
 
-rows = list(csv.reader(open(sys.argv[1])))
-top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
-fname, hdr = None, None
-agg = []
+rep = sys.argv[1]
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"]
+if len(sys.argv) > 3:
+    cmd += ["-k", sys.argv[3]]
+rows = list(csv.reader(io.StringIO(subprocess.run(cmd, capture_output=True, text=True).stdout)))
+cur_file, hdr, cur = None, None, None
+inst, stall, src = collections.Counter(), collections.Counter(), {}
 for r in rows:
-    if r and r[0] == "File Path":
-        fname = r[1].split("/")[-1]
+    if not r:
         continue
-    if r and r[0] == "Line No":
+    if r[0] == "File Path":
+        cur_file = r[1].split("/")[-1]
+        continue
+    if r[0] in ("Function Name",):
+        continue
+    if r[0] == "Line No":
         hdr = r
         continue
-    if not hdr or not r or not r[0] or not r[0].isdigit():
+    if hdr is None:
         continue
-    si = hdr.index("Warp Stall Sampling (All Samples)")
+    if r[0] != "":
+        cur = (cur_file, r[0])
+        src[cur] = r[1].strip()[:80]
+    if r[2] == "" or cur is None:
+        continue
     try:
-        samples = int(r[si])
-    except ValueError:
+        inst[cur] += float(r[7]) if r[7] not in ("", "-") else 0.0
+        stall[cur] += float(r[4]) if r[4] not in ("", "-") else 0.0
+    except (ValueError, IndexError):      # a source row whose text held the delimiter
         continue
-    stalls = {h: r[i] for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h}
-    top_stalls = sorted(((int(v), k) for k, v in stalls.items() if v.isdigit()), reverse=True)[:3]
-    agg.append((samples, fname, r[0], r[1].strip()[:70], top_stalls))
-tot = sum(a[0] for a in agg)
-for s, f, ln, src, st in sorted(agg, reverse=True)[:top]:
-    print(f"{100 * s / tot:5.1f}% {f}:{ln:5s} {src:70s} {' '.join(f'{k[6:]}={v}' for v, k in st)}")
+ti, ts = sum(inst.values()) or 1, sum(stall.values()) or 1
+print(f"# {ti:.4g} warp instructions, {ts:.0f} stall samples")
+print("# top by instructions")
+for k, v in inst.most_common(n):
+    print(f"{100 * v / ti:5.1f}% inst {100 * stall[k] / ts:5.1f}% stall  {k[0]}:{k[1]}  {src.get(k, '')}")
+print("# top by stall samples")
+for k, v in stall.most_common(n):
+    print(f"{100 * inst[k] / ti:5.1f}% inst {100 * v / ts:5.1f}% stall  {k[0]}:{k[1]}  {src.get(k, '')}")
