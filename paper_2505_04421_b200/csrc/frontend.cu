@@ -105,6 +105,20 @@ __device__ __forceinline__ void featurise_raw(const FrontArgs& a, const TokenInf
   const int bucket = min(32 - __clz(dt), a.nb - 1);      // time_bucket (inputs.py:307-315)
   ids[0] = item; ids[1] = act; ids[2] = bucket;
   const int e1 = a.d_item, e2 = a.d_item + a.d_act, e3 = e2 + a.d_time;
+  const float* pi = a.item_tab + item * a.d_item;
+  const float* pa = a.act_tab + act * a.d_act;
+  const float* pt = a.time_tab + bucket * a.d_time;
+  if ((((e1 | a.d_act | a.d_time) & 3) | ((reinterpret_cast<uintptr_t>(a.item_tab) | reinterpret_cast<uintptr_t>(a.act_tab) |
+                                            reinterpret_cast<uintptr_t>(a.time_tab)) & 15)) == 0) {
+    // widths in multiples of 4 (16-byte rows): one float4 per 4 columns
+#pragma unroll
+    for (int c = 0; c < kFP; c += 4) {
+      const float* p = c < e1 ? pi + c : c < e2 ? pa + (c - e1) : pt + (c - e2);
+      const float4 x = c < e3 ? __ldg(reinterpret_cast<const float4*>(p)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[c] = x.x; v[c + 1] = x.y; v[c + 2] = x.z; v[c + 3] = x.w;
+    }
+    return;
+  }
 #pragma unroll
   for (int c = 0; c < kFP; ++c) {
     const float* p = c < e1 ? a.item_tab + item * a.d_item + c
@@ -616,6 +630,8 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
     s_pos[rr * (DT + 1) + c] = (rec >= 0 && rec < a.L) ? a.pos_tab[(long long)rec * DT + c] : 0.f;
     s_gpos[rr * (DT + 1) + c] = 0.f;
   }
+  // the one-hot tile stays zero apart from each row's two ones (rewritten per tile)
+  for (int i = threadIdx.x; i < kTile * 64 / 8; i += blockDim.x) reinterpret_cast<uint4*>(sOH)[i] = make_uint4(0, 0, 0, 0);
   if (threadIdx.x == 0) {
     sm100::mbar_init(bar_w, 1);
     sm100::mbar_init(bar_a, 32 * 2 * kWorkers);
@@ -734,6 +750,7 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
     };
     if (b0 < a.B) prefetch(b0);
     int my_tiles = 0;
+    int oh_b = -1, oh_a = -1;                          // this row's one-hot columns in sOH
     for (int b = b0; b < a.B; b += r, ++my_tiles) {
       TokenInfo ti;
       ti.b = b; ti.j = j;
@@ -749,10 +766,12 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
         featurise_raw(a, ti, item_pf, act_pf, dt_pf, v, ids, false);
         v[kFP - 1] = 1.f;                                              // bias column
         store_row(sFeat, row, kFP, v, kFP);
-        float oh[64];
-#pragma unroll
-        for (int c = 0; c < 64; ++c) oh[c] = (ti.real && (c == ids[2] || c == 32 + ids[1])) ? 1.f : 0.f;
-        store_row(sOH, row, 64, oh, 64);
+        // [onehot(bucket) | onehot(action)]: clear the previous tile's two ones, set this tile's
+        const bf16 one = __float2bfloat16(1.f), zero = __float2bfloat16(0.f);
+        if (oh_b >= 0) { sOH[canon(row, oh_b, 64)] = zero; sOH[canon(row, oh_a, 64)] = zero; }
+        oh_b = ti.real ? ids[2] : -1;
+        oh_a = ti.real ? 32 + ids[1] : -1;
+        if (oh_b >= 0) { sOH[canon(row, oh_b, 64)] = one; sOH[canon(row, oh_a, 64)] = one; }
       } else {
         float dh[DT];
 #pragma unroll
