@@ -211,11 +211,9 @@ __device__ __forceinline__ void kv_store_part(bf16* skv, int row, int part, cons
   }
 }
 template <int DT>
-__device__ __forceinline__ void kv_load8(const bf16* skv, int row, int col, float* out) {
+__device__ __forceinline__ uint4 kv_raw8(const bf16* skv, int row, int col) {
   constexpr int CPR = 2 * DT / 8;
-  const uint4 w = *reinterpret_cast<const uint4*>(skv + row * 2 * DT + (((col / 8) ^ (row % CPR)) * 8));
-  out[0] = sm100::bf16_lo(w.x); out[1] = sm100::bf16_hi(w.x); out[2] = sm100::bf16_lo(w.y); out[3] = sm100::bf16_hi(w.y);
-  out[4] = sm100::bf16_lo(w.z); out[5] = sm100::bf16_hi(w.z); out[6] = sm100::bf16_lo(w.w); out[7] = sm100::bf16_hi(w.w);
+  return *reinterpret_cast<const uint4*>(skv + row * 2 * DT + (((col / 8) ^ (row % CPR)) * 8));
 }
 
 // ------------------------------------------------------------------ forward kernel
@@ -447,8 +445,15 @@ __global__ void __launch_bounds__(32 * 5 * S, 1) fe_fwd_kernel(FrontArgs a) {
         }
         __syncwarp();
         {
-          float qv[DT];
-          tmem_row<DT>(trow, qv);
+          // scores and context with fp32 += bf16·bf16 FMAs (q rounded to bf16 like k and v; the
+          // probabilities rounded to bf16 for the context)
+          uint32_t qp[DT / 2];
+          {
+            float qv[DT];
+            tmem_row<DT>(trow, qv);
+#pragma unroll
+            for (int c = 0; c < DT; c += 2) qp[c / 2] = sm100::pack_bf16(qv[c], qv[c + 1]);
+          }
           const int g0 = row - row % KG;
           float sc[KG];
           float mx = -INFINITY;
@@ -457,10 +462,11 @@ __global__ void __launch_bounds__(32 * 5 * S, 1) fe_fwd_kernel(FrontArgs a) {
             float acc = 0.f;
 #pragma unroll
             for (int c = 0; c < DT; c += 8) {
-              float kk[8];
-              kv_load8<DT>(sKV, g0 + jj, c, kk);
-#pragma unroll
-              for (int u = 0; u < 8; ++u) acc = fmaf(qv[c + u], kk[u], acc);
+              const uint4 w = kv_raw8<DT>(sKV, g0 + jj, c);
+              acc = sm100::dot2_bf16(qp[c / 2], w.x, acc);
+              acc = sm100::dot2_bf16(qp[c / 2 + 1], w.y, acc);
+              acc = sm100::dot2_bf16(qp[c / 2 + 2], w.z, acc);
+              acc = sm100::dot2_bf16(qp[c / 2 + 3], w.w, acc);
             }
             sc[jj] = acc * scale_in;
             mx = fmaxf(mx, sc[jj]);
@@ -473,13 +479,14 @@ __global__ void __launch_bounds__(32 * 5 * S, 1) fe_fwd_kernel(FrontArgs a) {
           for (int c = 0; c < DT; ++c) ctx[c] = 0.f;
 #pragma unroll
           for (int jj = 0; jj < KG; ++jj) {
-            const float pj = sc[jj] * rinv;
+            const uint32_t pj = sm100::bf16_scalar(sc[jj] * rinv);
 #pragma unroll
             for (int c = 0; c < DT; c += 8) {
-              float vv[8];
-              kv_load8<DT>(sKV, g0 + jj, DT + c, vv);
-#pragma unroll
-              for (int u = 0; u < 8; ++u) ctx[c + u] = fmaf(pj, vv[u], ctx[c + u]);
+              const uint4 w = kv_raw8<DT>(sKV, g0 + jj, DT + c);
+              sm100::axpy2_bf16(pj, w.x, ctx[c], ctx[c + 1]);
+              sm100::axpy2_bf16(pj, w.y, ctx[c + 2], ctx[c + 3]);
+              sm100::axpy2_bf16(pj, w.z, ctx[c + 4], ctx[c + 5]);
+              sm100::axpy2_bf16(pj, w.w, ctx[c + 6], ctx[c + 7]);
             }
           }
         }

@@ -27,34 +27,36 @@ __device__ __forceinline__ void store8_bf16(bf16* dst, const float* v) {
         make_uint4(sm100::pack_bf16(v[c], v[c + 1]), sm100::pack_bf16(v[c + 2], v[c + 3]),
                    sm100::pack_bf16(v[c + 4], v[c + 5]), sm100::pack_bf16(v[c + 6], v[c + 7]));
 }
-// Σ_c x[c]·row[c], summed in c order
+// x (N fp32 values) as packed bf16 pairs
 template <int N>
-__device__ __forceinline__ float dot8_bf16(const float* x, const bf16* row) {
+__device__ __forceinline__ void pack_pairs(const float* x, uint32_t* xp) {
+#pragma unroll
+  for (int c = 0; c < N; c += 2) xp[c / 2] = sm100::pack_bf16(x[c], x[c + 1]);
+}
+// Σ_c x[c]·row[c] in c order, x as packed bf16 pairs: fp32 += bf16·bf16, one FHFMA per product
+template <int N>
+__device__ __forceinline__ float dot8_bf16(const uint32_t* xp, const bf16* row) {
   float acc = 0.f;
 #pragma unroll
   for (int c = 0; c < N; c += 8) {
     const uint4 u = *reinterpret_cast<const uint4*>(row + c);
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      acc = fmaf(x[c + 2 * t], sm100::bf16_lo(w[t]), acc);
-      acc = fmaf(x[c + 2 * t + 1], sm100::bf16_hi(w[t]), acc);
-    }
+    acc = sm100::dot2_bf16(xp[c / 2], u.x, acc);
+    acc = sm100::dot2_bf16(xp[c / 2 + 1], u.y, acc);
+    acc = sm100::dot2_bf16(xp[c / 2 + 2], u.z, acc);
+    acc = sm100::dot2_bf16(xp[c / 2 + 3], u.w, acc);
   }
   return acc;
 }
-// y[c] += a·row[c]
+// y[c] += a·row[c] with a rounded to bf16 (sm100::bf16_scalar)
 template <int N>
-__device__ __forceinline__ void axpy8_bf16(float* y, float a, const bf16* row) {
+__device__ __forceinline__ void axpy8_bf16(float* y, uint32_t a, const bf16* row) {
 #pragma unroll
   for (int c = 0; c < N; c += 8) {
     const uint4 u = *reinterpret_cast<const uint4*>(row + c);
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      y[c + 2 * t] = fmaf(a, sm100::bf16_lo(w[t]), y[c + 2 * t]);
-      y[c + 2 * t + 1] = fmaf(a, sm100::bf16_hi(w[t]), y[c + 2 * t + 1]);
-    }
+    sm100::axpy2_bf16(a, u.x, y[c], y[c + 1]);
+    sm100::axpy2_bf16(a, u.y, y[c + 2], y[c + 3]);
+    sm100::axpy2_bf16(a, u.z, y[c + 4], y[c + 5]);
+    sm100::axpy2_bf16(a, u.w, y[c + 6], y[c + 7]);
   }
 }
 
@@ -269,12 +271,15 @@ __global__ void __launch_bounds__(32 * (1 + kWorkers * NG), 1) fe_inner_bwd_kern
       signal();
       // ---- R1: q, k, v; group attention (scratch keeps q|k|v (bf16) and P (fp32) for the peers)
       wait_d();
-      float qv[HD];
+      uint32_t qp[HD / 2];                       // q as bf16 pairs (the scores' operand)
       {
         float kvv[HD];
-        tmem_row<HD>(T_W0 + lo + c0, qv);
+        tmem_row<HD>(T_W0 + lo + c0, kvv);
+        pack_pairs<HD>(kvv, qp);
         bf16* qs = sQKV + row * QS;
-        store8_bf16<HD>(qs + c0, qv);
+#pragma unroll
+        for (int c = 0; c < HD; c += 8)
+          *reinterpret_cast<uint4*>(qs + c0 + c) = make_uint4(qp[c / 2], qp[c / 2 + 1], qp[c / 2 + 2], qp[c / 2 + 3]);
         tmem_row<HD>(T_W0 + lo + DT + c0, kvv);
         store8_bf16<HD>(qs + DT + c0, kvv);
         tmem_row<HD>(T_W0 + lo + 2 * DT + c0, kvv);
@@ -286,7 +291,7 @@ __global__ void __launch_bounds__(32 * (1 + kWorkers * NG), 1) fe_inner_bwd_kern
       float p[KG];
       {
 #pragma unroll
-        for (int jj = 0; jj < KG; ++jj) p[jj] = dot8_bf16<HD>(qv, sQKV + (g0 + jj) * QS + DT + c0);
+        for (int jj = 0; jj < KG; ++jj) p[jj] = dot8_bf16<HD>(qp, sQKV + (g0 + jj) * QS + DT + c0);
         xsum(p, KG);
         float mx = -INFINITY;
 #pragma unroll
@@ -303,7 +308,7 @@ __global__ void __launch_bounds__(32 * (1 + kWorkers * NG), 1) fe_inner_bwd_kern
 #pragma unroll
         for (int c = 0; c < HD; ++c) ctx[c] = 0.f;
 #pragma unroll
-        for (int jj = 0; jj < KG; ++jj) axpy8_bf16<HD>(ctx, p[jj], sQKV + (g0 + jj) * QS + 2 * DT + c0);
+        for (int jj = 0; jj < KG; ++jj) axpy8_bf16<HD>(ctx, sm100::bf16_scalar(p[jj]), sQKV + (g0 + jj) * QS + 2 * DT + c0);
         store_row(sCTX, row, XK, ctx, HD, c0);
       }
       ones_col(sCTX);
@@ -375,8 +380,10 @@ __global__ void __launch_bounds__(32 * (1 + kWorkers * NG), 1) fe_inner_bwd_kern
         for (int c = 0; c < HD; c += 4)
           *reinterpret_cast<float4*>(sDC + row * DCS + c0 + c) = make_float4(dc[c], dc[c + 1], dc[c + 2], dc[c + 3]);
         float dp[KG];
+        uint32_t dcp[HD / 2];
+        pack_pairs<HD>(dc, dcp);
 #pragma unroll
-        for (int jj = 0; jj < KG; ++jj) dp[jj] = dot8_bf16<HD>(dc, sQKV + (g0 + jj) * QS + 2 * DT + c0);
+        for (int jj = 0; jj < KG; ++jj) dp[jj] = dot8_bf16<HD>(dcp, sQKV + (g0 + jj) * QS + 2 * DT + c0);
         xsum(dp, KG);
         float D = 0.f;
 #pragma unroll
@@ -392,8 +399,8 @@ __global__ void __launch_bounds__(32 * (1 + kWorkers * NG), 1) fe_inner_bwd_kern
 #pragma unroll
         for (int jj = 0; jj < KG; ++jj) {         // same per-element summation order as a c-outer loop
           const bf16* pr = sQKV + (g0 + jj) * QS;
-          axpy8_bf16<HD>(dqkv, sSg[row * KG + jj], pr + DT + c0);           // dq += dS_ij k_j
-          axpy8_bf16<HD>(dqkv + HD, sSg[(g0 + jj) * KG + me], pr + c0);     // dk += dS_ji q_j
+          axpy8_bf16<HD>(dqkv, sm100::bf16_scalar(sSg[row * KG + jj]), pr + DT + c0);           // dq += dS_ij k_j
+          axpy8_bf16<HD>(dqkv + HD, sm100::bf16_scalar(sSg[(g0 + jj) * KG + me]), pr + c0);     // dk += dS_ji q_j
           const float pj = sPg[(g0 + jj) * KG + me];                        // dv += P_ji dctx_j
           const float* dcr = sDC + (g0 + jj) * DCS + c0;
 #pragma unroll

@@ -243,6 +243,23 @@ __host__ __device__ constexpr uint32_t make_idesc_f16(uint32_t M, uint32_t N, ui
 // ------------------------------------------------------------------ misc math
 __device__ __forceinline__ float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
+// fp32 += bf16 × bf16 (FHFMA.BF16, one instruction per product, either half of a packed pair):
+// acc += x.lo·w.lo + x.hi·w.hi (in that order)
+__device__ __forceinline__ float dot2_bf16(uint32_t x, uint32_t w, float acc) {
+  asm("{\n\t.reg .b16 xl, xh, wl, wh;\n\tmov.b32 {xl, xh}, %1;\n\tmov.b32 {wl, wh}, %2;\n\t"
+      "fma.rn.f32.bf16 %0, xl, wl, %0;\n\tfma.rn.f32.bf16 %0, xh, wh, %0;\n\t}"
+      : "+f"(acc) : "r"(x), "r"(w));
+  return acc;
+}
+// ylo += a·w.lo, yhi += a·w.hi with the bf16 scalar a in the low half of `a`
+__device__ __forceinline__ void axpy2_bf16(uint32_t a, uint32_t w, float& ylo, float& yhi) {
+  asm("{\n\t.reg .b16 al, ah, wl, wh;\n\tmov.b32 {al, ah}, %2;\n\tmov.b32 {wl, wh}, %3;\n\t"
+      "fma.rn.f32.bf16 %0, al, wl, %0;\n\tfma.rn.f32.bf16 %1, al, wh, %1;\n\t}"
+      : "+f"(ylo), "+f"(yhi) : "r"(a), "r"(w));
+}
+__device__ __forceinline__ uint32_t bf16_scalar(float a) {
+  return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(a));
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);
