@@ -758,11 +758,16 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
     if (b0 < a.B) prefetch(b0);
     int my_tiles = 0;
     int oh_b = -1, oh_a = -1;                          // this row's one-hot columns in sOH
-    for (int b = b0; b < a.B; b += r, ++my_tiles) {
-      TokenInfo ti;
-      ti.b = b; ti.j = j;
+    // stage A of a tile: its feature / one-hot / dh rows into shared memory (from the prefetched
+    // raw inputs), then the signal for its feat·W_tp MMA.  It runs for tile b+r right after tile
+    // b's last MMAs (which read those tiles) completed, before tile b's item-gradient CAS loop,
+    // so that loop overlaps the next tile's first MMA round trip.
+    TokenInfo ti;
+    int cas_item = 0;
+    auto stage_a = [&](int bb) {
+      ti.b = bb; ti.j = j;
       ti.in_range = col_ok;
-      ti.t = (long long)b * a.Lp + j;
+      ti.t = (long long)bb * a.Lp + j;
       ti.n = min(max(n_pf, 0), a.L);
       ti.real = col_ok && j >= a.Lp - ti.n;
       ti.keep = col_ok && (j / a.K) >= (a.Lp - ti.n) / a.K;
@@ -787,8 +792,14 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
         store_row(sDX0, row, 64, dh, DT, 32);                          // [· | dh] for the db2 row sums
         if (ti.real) ids[0] = (item_pf < 0 || item_pf >= a.vocab) ? 0 : item_pf;   // for the dfeat split
       }
+      cas_item = ids[0];
       signal();
-      if (b + r < a.B) prefetch(b + r);
+    };
+    if (b0 < a.B) {
+      stage_a(b0);
+      if (b0 + r < a.B) prefetch(b0 + r);
+    }
+    for (int b = b0; b < a.B; b += r, ++my_tiles) {
       wait_d();
       // x0 recompute; with DT = 32 the two groups take 16 columns each
       constexpr int XH = (DT % 32 == 0) ? DT / 2 : DT;
@@ -843,11 +854,17 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
       {                                                                // item rows: dfeat[:d_item]
         float df[kFP];
         tmem_row<kFP>(T_X + lane_off, df);
-        if (ti.real) {
+        const bool cas_real = ti.real;
+        const int cas_tile_item = cas_item;
+        if (b + r < a.B) {
+          stage_a(b + r);
+          if (b + 2 * r < a.B) prefetch(b + 2 * r);
+        }
+        if (cas_real) {
           if (item_smem && (a.d_item & 3) == 0 && (reinterpret_cast<uintptr_t>(s_item) & 15) == 0) {
             // shared-memory float adds are CAS loops on sm_100: one 128-bit CAS per 4 columns
             // (quads alternate between the two warp groups)
-            uint4* gi = reinterpret_cast<uint4*>(s_item + ids[0] * a.d_item);
+            uint4* gi = reinterpret_cast<uint4*>(s_item + cas_tile_item * a.d_item);
 #pragma unroll
             for (int c = 0; c + 3 < kFP; c += 4) {
               if (c >= a.d_item || ((c >> 2) & 1) != grp) continue;
@@ -864,7 +881,7 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
             }
           } else if (item_smem && (a.d_item & 1) == 0) {
             // one 64-bit CAS per column pair (pairs alternate between the two warp groups)
-            unsigned long long* gi = reinterpret_cast<unsigned long long*>(s_item + ids[0] * a.d_item);
+            unsigned long long* gi = reinterpret_cast<unsigned long long*>(s_item + cas_tile_item * a.d_item);
 #pragma unroll
             for (int c = 0; c + 1 < kFP; c += 2) {
               if (c >= a.d_item || ((c >> 1) & 1) != grp) continue;
@@ -878,7 +895,7 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
               } while (old != assumed);
             }
           } else {
-            float* gi = (item_smem ? s_item : a.g_item) + ids[0] * a.d_item;
+            float* gi = (item_smem ? s_item : a.g_item) + cas_tile_item * a.d_item;
 #pragma unroll
             for (int c = 0; c < kFP; ++c)
               if (c < a.d_item && (c & 1) == grp) atomicAdd(gi + c, df[c]);
