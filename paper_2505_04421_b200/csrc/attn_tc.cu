@@ -599,6 +599,10 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
             // through this warp's 2 × 2 KB of the (consumed) dS / P tiles: 16-byte segments
             // XOR-swizzled, conflict-free both ways; out as 64-byte row segments
             uint4* stg = reinterpret_cast<uint4*>(sdS) + (warp - 1) * 256;
+            if (a.sum_kv) {
+#pragma unroll
+              for (int u = 0; u < 32; ++u) dk[u] += dv[u];
+            }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               const int sl = lane * 4 + (j ^ ((lane >> 1) & 3));
@@ -615,7 +619,8 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
               if (kbase + r < a.nk) {
                 const long long off = (long long)(kbase + r);
                 const int sl = r * 4 + (sgm ^ ((r >> 1) & 3));
-                *reinterpret_cast<uint4*>(a.dV + (long long)b0 * a.sdv + off * a.lddv + hd * DH + c1 + sgm * 8) = stg[sl];
+                if (!a.sum_kv)
+                  *reinterpret_cast<uint4*>(a.dV + (long long)b0 * a.sdv + off * a.lddv + hd * DH + c1 + sgm * 8) = stg[sl];
                 *reinterpret_cast<uint4*>(a.dK + (long long)b0 * a.sdk + off * a.lddk + hd * DH + c1 + sgm * 8) = stg[128 + sl];
               }
             }
@@ -623,6 +628,10 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
             continue;
           }
           if (!krow) continue;
+          if (a.sum_kv) {
+#pragma unroll
+            for (int u = 0; u < 32; ++u) dk[u] += dv[u];
+          }
 #pragma unroll
           for (int cc = 0; cc < 32; cc += 8) {
             uint4 x, y;
@@ -630,7 +639,7 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
             x.z = sm100::pack_bf16(dv[cc + 4], dv[cc + 5]); x.w = sm100::pack_bf16(dv[cc + 6], dv[cc + 7]);
             y.x = sm100::pack_bf16(dk[cc], dk[cc + 1]); y.y = sm100::pack_bf16(dk[cc + 2], dk[cc + 3]);
             y.z = sm100::pack_bf16(dk[cc + 4], dk[cc + 5]); y.w = sm100::pack_bf16(dk[cc + 6], dk[cc + 7]);
-            *reinterpret_cast<uint4*>(pv + h * NW + c1 + cc) = x;
+            if (!a.sum_kv) *reinterpret_cast<uint4*>(pv + h * NW + c1 + cc) = x;
             *reinterpret_cast<uint4*>(pk + h * NW + c1 + cc) = y;
           }
         }

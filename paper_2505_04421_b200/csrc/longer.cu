@@ -233,6 +233,11 @@ struct Plan {
   void* ws;
   bool fused_fe;   // fused front-end kernel (frontend.cu) for this call
   bool compact_head = false;   // last self block's row-wise tail on the two head rows only
+  // cross layer with absorbed K/V projections (heads = 1): scores Q'·knᵀ with Q' = Q·W_kᵀ, context
+  // (P·kn)·W_v + b_v — no [K | V] rows over the B·v key rows (absorb_ok)
+  bool absorb = false;
+  bf16 *xa_qabs, *xa_craw, *xa_dctx_bf, *xa_dqabs;   // Q', P·kn, dL/dctx (bf16), dL/dQ'
+  float *xa_craw32, *xa_dC;                           // P·kn (fp32), dL/d(P·kn)
   float *hc_x, *hc_g, *hc_dctx;   // compact [2B, D] buffers of that tail
   bf16 *hc_ctx, *hc_g_bf;
   bf16* wblob;     // its canonical-layout weight blob
@@ -351,6 +356,8 @@ Plan make_plan(const LongerDims& d, void* ws) {
   };
   block_bufs(p.cb, D);
   for (int i = 0; i < p.N; ++i) block_bufs(p.sb[i], 3 * D);
+  p.xa_qabs = a.take<bf16>(Q * D); p.xa_craw = a.take<bf16>(Q * D); p.xa_dctx_bf = a.take<bf16>(Q * D);
+  p.xa_dqabs = a.take<bf16>(Q * D); p.xa_craw32 = a.take<float>(Q * D); p.xa_dC = a.take<float>(Q * D);
   // head
   p.hin = a.take<float>((long long)B * p.HIN); p.z1 = a.take<float>((long long)B * p.hh);
   p.loss_per = a.take<float>(B); p.dz = a.take<float>(B); p.dz1 = a.take<float>((long long)B * p.hh);
@@ -437,6 +444,15 @@ int lin_dw(cudaStream_t st, const bf16* X, int ldx, int in, const bf16* dY, int 
   g.flags = EPI_OUT_F32 | EPI_ATOMIC;
   g.split_k = 0;
   g.C = dW; g.ldc = out;
+  return gemm_launch(g, st);
+}
+
+// Y[rows, out] (bf16) = X·W (+ bias) with W a column block of a wider row-major matrix (row stride ldw)
+int lin_fwd_w(cudaStream_t st, const bf16* X, int ldx, long long rows, const bf16* W, int ldw, int in, int out,
+              const float* bias, bf16* Y, int ldy) {
+  GemmArgs g = G_(X, ldx, 0, W, ldw, 1, rows, out, in);
+  g.flags = (bias ? EPI_BIAS : 0u) | EPI_OUT_BF16;
+  g.bias = bias; g.C_bf16 = Y; g.ldc_bf = ldy;
   return gemm_launch(g, st);
 }
 
@@ -535,10 +551,23 @@ int block_fwd(const Ctx& c, const BlockOff& bo, BlockBufs& b, const float* xq, b
   if (cross) {
     // K/V rows: LN1 + [K | V] projection were forked onto the side stream by forward()
     TRY(lin_fwd(st, b.qn, D, Q, Wqkv, D, D, c.w(bo.b_q), 0, nullptr, b.qkv, nullptr));
+    if (p.absorb) {
+      // S = Q·Kᵀ = (Q·W_kᵀ)·knᵀ + Q·b_k (constant per row: the softmax drops it), so the
+      // attention runs on Q' = Q·W_kᵀ against the LN'd key rows kn themselves, both as keys and
+      // as values: P·V = (P·kn)·W_v + b_v (rows of P sum to 1)
+      TRY(lin_dx(st, b.qkv, D, Q, p.pk.c_wkv, 2 * D, D, D, nullptr, 0, p.xa_qabs, D));
+    }
     join_side(st, side_stream(st));
-    a.Q = b.qkv; a.ldq = D; a.sq = (long long)p.q * D;
-    a.Kp = p.KV; a.ldk = 2 * D; a.sk = (long long)p.v * 2 * D;
-    a.V = p.KV + D; a.ldv = 2 * D; a.sv = (long long)p.v * 2 * D;
+    if (p.absorb) {
+      a.Q = p.xa_qabs; a.ldq = D; a.sq = (long long)p.q * D;
+      a.Kp = p.kn; a.ldk = D; a.sk = (long long)p.v * D;
+      a.V = p.kn; a.ldv = D; a.sv = (long long)p.v * D;
+      a.ctx = p.xa_craw; a.ctx32 = p.xa_craw32;
+    } else {
+      a.Q = b.qkv; a.ldq = D; a.sq = (long long)p.q * D;
+      a.Kp = p.KV; a.ldk = 2 * D; a.sk = (long long)p.v * 2 * D;
+      a.V = p.KV + D; a.ldv = 2 * D; a.sv = (long long)p.v * 2 * D;
+    }
     a.nk = p.v; a.ns = p.G; a.goff = 0;
   } else {
     TRY(lin_fwd(st, b.qn, D, Q, Wqkv, D, 3 * D, bqkv, 0, nullptr, b.qkv, nullptr));
@@ -554,6 +583,8 @@ int block_fwd(const Ctx& c, const BlockOff& bo, BlockBufs& b, const float* xq, b
   } else {
     attn_fwd(a, st);
   }
+  if (cross && p.absorb)   // ctx = (P·kn)·W_v + b_v
+    TRY(lin_fwd_w(st, p.xa_craw, D, Q, p.pk.c_wkv + D, 2 * D, D, D, p.pk.c_bkv + D, b.ctx, D));
   // compact: only the two rows the head reads leave the last block (model.py:346-362), so its
   // row-wise tail (W_o + residual, LN2, FFN) runs on [2B, D] gathered rows
   const long long R = compact ? 2LL * p.B : Q;
@@ -722,7 +753,8 @@ int forward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs, fl
     }
     r.batch = p.B;
     layernorm_fwd(r, D, c.w(o.cross.ln1_g), c.w(o.cross.ln1_b), p.kn, p.mk, p.rk, ss);
-    TRY(lin_fwd(ss, p.kn, D, (long long)p.B * p.v, p.pk.c_wkv, D, 2 * D, p.pk.c_bkv, 0, nullptr, p.KV, nullptr));
+    if (!p.absorb)
+      TRY(lin_fwd(ss, p.kn, D, (long long)p.B * p.v, p.pk.c_wkv, D, 2 * D, p.pk.c_bkv, 0, nullptr, p.KV, nullptr));
   }
   // sequence queries (select_queries, model.py:58-123)
   if (p.qs == QS_RECENT) {
@@ -794,7 +826,9 @@ int block_bwd(const Ctx& c, cudaStream_t ss, const BlockOff& bo, const BlockBufs
   // output projection
   fork_side(st, ss);
   TRY(lin_dw(ss, compact ? p.hc_ctx : b.ctx, D, D, dx1_bf_rows, D, D, R, c.g(bo.w_o)));
-  TRY(lin_dx(st, dx1_bf_rows, D, R, Wo, D, D, D, compact ? p.hc_dctx : b.g_dctx, D, nullptr, 0));
+  const bool absorb = cross && p.absorb;
+  TRY(lin_dx(st, dx1_bf_rows, D, R, Wo, D, D, D, compact ? p.hc_dctx : b.g_dctx, D, absorb ? p.xa_dctx_bf : nullptr,
+             D));
   if (compact) {   // back to full [B·q, D] rows (zero elsewhere) for the attention and LN1 backward
     head_rows_scatter_f32(p.hc_dctx, b.g_dctx, p.B, p.q, p.k + 1, p.k + p.m - 1, D, st);
     head_rows_scatter_f32(p.hc_g, b.g_dx1, p.B, p.q, p.k + 1, p.k + p.m - 1, D, st);
@@ -806,7 +840,26 @@ int block_bwd(const Ctx& c, cudaStream_t ss, const BlockOff& bo, const BlockBufs
   a.learn = p.qs == QS_LEARNABLE; a.self_keys = cross ? 0 : 1;
   a.ctx = b.ctx; a.ldc = D; a.sc = (long long)p.q * D; a.lse = b.lse; a.ctx32 = b.ctx32;
   a.dctx = b.g_dctx; a.lddc = D; a.sdc = (long long)p.q * D; a.ctx_in = b.ctx;
-  if (cross) {
+  if (absorb) {
+    // ctx = C·W_v + b_v with C = P·kn: dW_v = Cᵀ·dctx, db_v = Σ dctx (side stream), dC = dctx·W_vᵀ;
+    // the attention backward then runs on (Q', kn, kn) with dO = dC: dQ', and dK + dV summed
+    // straight into d(kn) (the K / V rows are kn itself)
+    fork_side(st, ss);
+    TRY(lin_dw(ss, p.xa_craw, D, D, p.xa_dctx_bf, D, D, Q, c.g(bo.w_v)));
+    colsum_f32(b.g_dctx, (int)Q, D, D, c.g(bo.b_v), ss);
+    TRY(lin_dx(st, p.xa_dctx_bf, D, Q, p.pk.c_wkv + D, 2 * D, D, D, p.xa_dC, D, nullptr, 0));
+    a.ctx = p.xa_craw; a.ctx32 = p.xa_craw32; a.ctx_in = p.xa_craw;
+    a.dctx = p.xa_dC;
+    a.Q = p.xa_qabs; a.ldq = D; a.sq = (long long)p.q * D;
+    a.Kp = p.kn; a.ldk = D; a.sk = (long long)p.v * D;
+    a.V = p.kn; a.ldv = D; a.sv = a.sk;
+    a.nk = p.v; a.ns = p.G; a.goff = 0;
+    a.dQ = p.xa_dqabs; a.lddq = D; a.sdq = (long long)p.q * D;
+    bf16* dkn_bf = reinterpret_cast<bf16*>(p.dkn);
+    a.dK = dkn_bf; a.lddk = D; a.sdk = (long long)p.v * D;
+    a.dV = dkn_bf; a.lddv = D; a.sdv = a.sdk;
+    a.sum_kv = 1;
+  } else if (cross) {
     a.Q = b.qkv; a.ldq = D; a.sq = (long long)p.q * D;
     a.Kp = p.KV; a.ldk = 2 * D; a.sk = (long long)p.v * 2 * D;
     a.V = p.KV + D; a.ldv = 2 * D; a.sv = a.sk;
@@ -830,18 +883,25 @@ int block_bwd(const Ctx& c, cudaStream_t ss, const BlockOff& bo, const BlockBufs
   } else {
     attn_bwd(a, st);
   }
+  // absorbed: dQ = dQ'·W_k, dW_k = dQ'ᵀ·Q (S = Q·W_kᵀ·knᵀ); b_k's gradient is exactly 0 (the
+  // softmax is invariant to it) and stays so
+  if (absorb) TRY(lin_fwd_w(st, p.xa_dqabs, D, Q, p.pk.c_wkv, 2 * D, D, D, nullptr, b.g_dqkv, D));
   fork_side(st, ss);
   if (cross) {
     TRY(lin_dw(ss, b.qn, D, D, b.g_dqkv, D, D, Q, c.g(bo.w_q)));
     colsum_bf16(b.g_dqkv, (int)Q, D, D, c.g(bo.b_q), ss);
-    TRY(lin_dw(ss, p.kn, D, D, p.dKV, 2 * D, D, V, c.g(bo.w_k)));
-    TRY(lin_dw(ss, p.kn, D, D, p.dKV + D, 2 * D, D, V, c.g(bo.w_v)));
-    colsum_bf16(p.dKV, (int)V, D, 2 * D, c.g(bo.b_k), ss);
-    colsum_bf16(p.dKV + D, (int)V, D, 2 * D, c.g(bo.b_v), ss);
+    bf16* dkn_bf = reinterpret_cast<bf16*>(p.dkn);
+    if (absorb) {
+      TRY(lin_dw(ss, p.xa_dqabs, D, D, b.qkv, D, D, Q, c.g(bo.w_k)));
+    } else {
+      TRY(lin_dw(ss, p.kn, D, D, p.dKV, 2 * D, D, V, c.g(bo.w_k)));
+      TRY(lin_dw(ss, p.kn, D, D, p.dKV + D, 2 * D, D, V, c.g(bo.w_v)));
+      colsum_bf16(p.dKV, (int)V, D, 2 * D, c.g(bo.b_k), ss);
+      colsum_bf16(p.dKV + D, (int)V, D, 2 * D, c.g(bo.b_v), ss);
+    }
     TRY(lin_dx(st, b.g_dqkv, D, Q, Wqkv, D, D, D, b.g_dqn, D, nullptr, 0));
     // dK|dV → d(kn) in bf16 (it only feeds the HBM-bound LN backward below), in p.dkn's storage
-    bf16* dkn_bf = reinterpret_cast<bf16*>(p.dkn);
-    TRY(lin_dx(st, p.dKV, 2 * D, V, p.pk.c_wkv, 2 * D, D, 2 * D, nullptr, 0, dkn_bf, D));
+    if (!absorb) TRY(lin_dx(st, p.dKV, 2 * D, V, p.pk.c_wkv, 2 * D, D, 2 * D, nullptr, 0, dkn_bf, D));
     RowMap r{};
     r.A = p.merged; r.lda = D; r.a_rows = p.G; r.a_off = 0; r.na = p.G; r.Bsrc = p.glob; r.ldb = D; r.nb = p.m;
     r.batch = p.B;
@@ -1246,6 +1306,12 @@ extern "C" int longer_workspace_bytes(const LongerDims* dims, size_t* bytes) {
 static bool compact_head_ok(const Plan& p) {
   return p.N >= 1 && p.m >= 3 && g_knobs.head_rows;
 }
+// absorbed cross-layer K/V projections: one head (per-head absorption would widen every head to D)
+// on the tensor-core attention; the serving cache build keeps explicit K/V rows (it caches them)
+static bool absorb_ok(const Plan& p) {
+  const bool tc = (p.q <= 128 && (p.D == 32 || p.D == 64 || p.D == 128)) || (p.q <= 64 && p.D == 256);
+  return g_knobs.absorb_kv && g_knobs.attn_tc && p.heads == 1 && tc;
+}
 
 extern "C" int longer_forward(const LongerDims* dims, const float* params, const LongerBatch* batch, void* ws,
                               size_t ws_bytes, float* probs, void* stream) {
@@ -1254,6 +1320,7 @@ extern "C" int longer_forward(const LongerDims* dims, const float* params, const
   if (rc) return rc;
   p.fused_fe = use_fused(p);
   p.compact_head = compact_head_ok(p);
+  p.absorb = absorb_ok(p);
   Ctx c{p, params, nullptr, (cudaStream_t)stream};
   return forward(c, p, checked_batch(p, *batch, c.st), probs, nullptr, 0);
 }
@@ -1266,6 +1333,7 @@ extern "C" int longer_forward_trace(const LongerDims* dims, const float* params,
   if (!batch || !probs || !trace) return fail(LONGER_EDIM, "null argument");
   p.fused_fe = use_fused(p);
   p.compact_head = false;                // every row of every layer is kept for the trace
+  p.absorb = absorb_ok(p);
   Ctx c{p, params, nullptr, (cudaStream_t)stream};
   rc = forward(c, p, checked_batch(p, *batch, c.st), probs, nullptr, 0);
   if (rc) return rc;
@@ -1290,6 +1358,7 @@ extern "C" int longer_forward_backward(const LongerDims* dims, const float* para
   p.fused_fe = use_fused(p);
   if (rc) return rc;
   p.compact_head = compact_head_ok(p);
+  p.absorb = absorb_ok(p);
   Ctx c{p, params, grads, (cudaStream_t)stream};
   const LongerBatch bt = checked_batch(p, *batch, c.st);
   rc = forward(c, p, bt, probs, loss, 1);
@@ -1305,6 +1374,7 @@ extern "C" int longer_backward(const LongerDims* dims, const float* params, cons
   if (!batch || !probs || !dprobs || !grads) return fail(LONGER_EDIM, "null argument");
   p.fused_fe = use_fused(p);
   p.compact_head = compact_head_ok(p);
+  p.absorb = absorb_ok(p);
   Ctx c{p, params, grads, (cudaStream_t)stream};
   dz_from_dprobs(probs, dprobs, p.B, p.dz, c.st);     // dL/dz = dL/dp · p(1 − p)
   return backward(c, p, checked_batch(p, *batch, c.st), const_cast<float*>(probs));

@@ -112,6 +112,8 @@ struct AttnArgs {
   bf16* dQ; int lddq; long long sdq;
   bf16* dK; int lddk; long long sdk;
   bf16* dV; int lddv; long long sdv;
+  int sum_kv;                                // K and V are the same rows (absorbed projections):
+                                             // dK + dV go to dK (tensor-core path only)
 };
 void attn_fwd(const AttnArgs& a, cudaStream_t st);
 void attn_bwd(const AttnArgs& a, cudaStream_t st);

@@ -137,3 +137,28 @@ def test_cross_attention_backward_double_buffered_path(heads, monkeypatch):
     for name in grads:                    # ~0 groups (e.g. b_k: softmax-invariant) are rounding noise
         scale = max(np.abs(grads[name]).max(), 1e-2 * top)
         assert np.abs(grads2[name] - grads[name]).max() <= 1e-3 * scale, name
+
+
+@pytest.mark.parametrize("merge", ["inner", "concat"])
+def test_absorbed_cross_kv_projections(merge, monkeypatch):
+    """Cross layer with the K/V projections absorbed (heads = 1, the default): scores Q'·knᵀ with
+    Q' = Q·W_kᵀ, context (P·kn)·W_v + b_v, no [K | V] rows over the B·v key rows; backward through
+    dC = dctx·W_vᵀ, d(kn) = dK + dV from one attention pass, dQ = dQ'·W_k, dW_k = dQ'ᵀ·Q.  Both
+    the absorbed and the explicit path (LONGER_ABSORB_KV=0) meet the oracle bar; the absorbed
+    cross.b_k gradient is exactly 0 (the softmax is invariant to b_k; the reference's is rounding
+    noise around 0)."""
+    cfg = ModelConfig(**dict(C2, merge_mode=merge)).validate()
+    P = _perturbed(cfg, 23)
+    batch = synthetic_batch(cfg, 6, seed=4, min_events=1)
+    p_ref, loss_ref, G = O.forward_backward(P, cfg, batch.as_dict())
+    model = _model(cfg, P)
+    for absorb in ("1", "0"):
+        monkeypatch.setenv("LONGER_ABSORB_KV", absorb)
+        p, loss, grads = _run(model, batch)
+        assert np.max(np.abs(p - p_ref)) <= 5e-3, absorb
+        assert abs(loss - loss_ref) <= loss_tol(p_ref, batch.label), absorb
+        assert_grads_close(grads, G, f"absorb={absorb} {merge}")
+        if absorb == "1":
+            assert not np.any(grads["cross.b_k"])
+            pf = model.forward(batch).cpu().numpy().astype(np.float64)
+            assert np.max(np.abs(pf - p_ref)) <= 5e-3
