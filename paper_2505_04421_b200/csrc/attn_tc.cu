@@ -99,7 +99,9 @@ constexpr float kRescale = 8.f;
 // sample r / nq, key column j is key j % nk of sample j / nk (P·nq ≤ 128, P·nk ≤ 128: one chunk),
 // and a row sees only its own sample's key interval, shifted by (r / nq)·nk.  K / V then come
 // from a 2-D tensor map over the contiguous [B·nk] key rows.
-template <int DH, bool TMA>
+// KVS (the cross layer with absorbed projections: keys and values are the same rows): one TMA tile
+// per chunk serves as K (K-major, for S) and as V (MN-major, for P·V); P gets the K tile's slot.
+template <int DH, bool TMA, bool KVS>
 __global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a, const __grid_constant__ CUtensorMap tmK,
                                                                  const __grid_constant__ CUtensorMap tmV, int pack) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -139,14 +141,14 @@ __global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a, cons
       uint32_t pa = 0, pkv = 0, pm = 0;
       auto wait_a = [&]() { sm100::mbar_wait(bar_a, pa); pa ^= 1; sm100::tc_fence_after(); };
       auto load_kv = [&](int c) {
-        sm100::mbar_arrive_expect_tx(bar_kv, 2 * kC * DH * 2);
+        sm100::mbar_arrive_expect_tx(bar_kv, (KVS ? 1 : 2) * kC * DH * 2);
 #pragma unroll
         for (int i = 0; i < DH / 64; ++i) {
           if (pack > 1) {
-            sm100::tma_load_2d(sKP + i * kC * 64, &tmK, bar_kv, hd * DH + 64 * i, b0 * a.nk);
+            if (!KVS) sm100::tma_load_2d(sKP + i * kC * 64, &tmK, bar_kv, hd * DH + 64 * i, b0 * a.nk);
             sm100::tma_load_2d(sV + i * kC * 64, &tmV, bar_kv, hd * DH + 64 * i, b0 * a.nk);
           } else {
-            sm100::tma_load_3d(sKP + i * kC * 64, &tmK, bar_kv, hd * DH + 64 * i, c * kC, b0);
+            if (!KVS) sm100::tma_load_3d(sKP + i * kC * 64, &tmK, bar_kv, hd * DH + 64 * i, c * kC, b0);
             sm100::tma_load_3d(sV + i * kC * 64, &tmV, bar_kv, hd * DH + 64 * i, c * kC, b0);
           }
         }
@@ -161,7 +163,7 @@ __global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a, cons
         if constexpr (TMA) {
           sm100::mbar_wait(bar_kv, pkv);
           pkv ^= 1;
-          mma(T_S, Opnd{aQ, DH, 0}, OpndSW{aKP, kC, 0}, DH / 16, kC, false);
+          mma(T_S, Opnd{aQ, DH, 0}, OpndSW{KVS ? aV : aKP, kC, 0}, DH / 16, kC, false);
         } else {
           mma(T_S, Opnd{aQ, DH, 0}, Opnd{aKP, DH, 0}, DH / 16, kC, false);
         }
@@ -318,19 +320,23 @@ __global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a, cons
 // tiles of BIG free 64 KB of shared memory for a second K / V buffer, so the TMA of chunk i+2 is in
 // flight while chunk i+1 is computed (the chunk sequence is pass 1 then pass 2), and the dV / dK
 // rows leave through a per-warp shared-memory transpose as 64-byte row segments.
-template <int DH, bool TMA, bool SHORT>
+// KVS (with SHORT; keys = values, the absorbed cross layer): one TMA tile per chunk serves K and V
+// (32 KB buffers), and dV + dK accumulate into one TMEM region (Pᵀ·dO then += dSᵀ·Q).
+template <int DH, bool TMA, bool SHORT, bool KVS>
 __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, const __grid_constant__ CUtensorMap tmK,
                                                                   const __grid_constant__ CUtensorMap tmV, int pack) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   constexpr bool BIG = DH > 128;
   static_assert(!SHORT || (TMA && !BIG), "SHORT: TMA path at head width <= 128");
+  static_assert(!KVS || SHORT, "KVS: with SHORT");
+  constexpr int KVT = KVS ? 1 : 2;                // tiles per K / V buffer
   constexpr int QR = (BIG || SHORT) ? 64 : 128;   // stored query rows
   constexpr int KVB = SHORT ? 2 : 1;              // K / V buffers
   bf16* sQ = reinterpret_cast<bf16*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   bf16* sdO = sQ + QR * DH;
-  bf16* sK = sdO + QR * DH;                       // buffer b: K at sK + b·2·kC·DH, V right after it
+  bf16* sK = sdO + QR * DH;                       // buffer b: K at sK + b·KVT·kC·DH, V right after it
   bf16* sV = sK + kC * DH;
-  bf16* sdS = sK + KVB * 2 * kC * DH;             // QR x kC  (pre-scaled by 1/sqrt(dh))
+  bf16* sdS = sK + KVB * KVT * kC * DH;           // QR x kC  (pre-scaled by 1/sqrt(dh))
   bf16* sP = sdS + QR * kC;                       // QR x kC  (after dS: dS's M-row overread stays in smem)
   float* sDp = reinterpret_cast<float*>(sP + QR * kC);       // [2][128] partial D_i of the two groups
   uint64_t* bars = reinterpret_cast<uint64_t*>(sDp + 256);
@@ -362,7 +368,7 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
     if (lane == 0) {
       const uint32_t aQ = sm100::smem_u32(sQ), adO = sm100::smem_u32(sdO), aK0 = sm100::smem_u32(sK);
       const uint32_t aP = sm100::smem_u32(sP), adS = sm100::smem_u32(sdS);
-      constexpr uint32_t kBufBytes = 2 * kC * DH * 2;
+      constexpr uint32_t kBufBytes = KVT * kC * DH * 2;
       uint32_t pa = 0, pkv0 = 0, pkv1 = 0, pm = 0;
       auto wait_a = [&]() { sm100::mbar_wait(bar_a, pa); pa ^= 1; sm100::tc_fence_after(); };
       // the chunk sequence: pass 1 over chunks 0..n-1, then (n > 1) pass 2 over them again; load i
@@ -370,17 +376,17 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
       const int nload = nchunk > 1 ? 2 * nchunk : 1;
       auto load_kv = [&](int i) {
         const int c = i % nchunk, bsel = i % KVB;
-        bf16* dK = sK + bsel * 2 * kC * DH;
+        bf16* dK = sK + bsel * KVT * kC * DH;
         bf16* dV = dK + kC * DH;
-        sm100::mbar_arrive_expect_tx(&bar_kv[bsel], 2 * kC * DH * 2);
+        sm100::mbar_arrive_expect_tx(&bar_kv[bsel], KVT * kC * DH * 2);
 #pragma unroll
         for (int i2 = 0; i2 < DH / 64; ++i2) {
           if (pack > 1) {
             sm100::tma_load_2d(dK + i2 * kC * 64, &tmK, &bar_kv[bsel], hd * DH + 64 * i2, b0 * a.nk);
-            sm100::tma_load_2d(dV + i2 * kC * 64, &tmV, &bar_kv[bsel], hd * DH + 64 * i2, b0 * a.nk);
+            if (!KVS) sm100::tma_load_2d(dV + i2 * kC * 64, &tmV, &bar_kv[bsel], hd * DH + 64 * i2, b0 * a.nk);
           } else {
             sm100::tma_load_3d(dK + i2 * kC * 64, &tmK, &bar_kv[bsel], hd * DH + 64 * i2, c * kC, b0);
-            sm100::tma_load_3d(dV + i2 * kC * 64, &tmV, &bar_kv[bsel], hd * DH + 64 * i2, c * kC, b0);
+            if (!KVS) sm100::tma_load_3d(dV + i2 * kC * 64, &tmV, &bar_kv[bsel], hd * DH + 64 * i2, c * kC, b0);
           }
         }
       };
@@ -396,7 +402,7 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
       auto kaddr = [&](int i) { return aK0 + (uint32_t)(i % KVB) * kBufBytes; };
       // S = Q·Kᵀ and dP = dO·Vᵀ of the chunk of load i
       auto mma_s_dp = [&](int i) {
-        const uint32_t aK = kaddr(i), aV = aK + kC * DH * 2;
+        const uint32_t aK = kaddr(i), aV = KVS ? aK : aK + kC * DH * 2;
         if constexpr (TMA) {
           mma(T_A, Opnd{aQ, DH, 0}, OpndSW{aK, kC, 0}, DH / 16, kC, false);
           mma(T_B, Opnd{adO, DH, 0}, OpndSW{aV, kC, 0}, DH / 16, kC, false);
@@ -431,7 +437,7 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
           wait_a();                                                 // P, dS (h = 1: halves read out)
           const uint32_t co = (uint32_t)h * NW * 16;                // byte offset of column half h
           mma(T_A, Opnd{aP, kC, 1}, Opnd{adO + co, DH, 1}, QR / 16, NW, false);   // dV = Pᵀ·dO
-          mma(T_B, Opnd{adS, kC, 1}, Opnd{aQ + co, DH, 1}, QR / 16, NW, false);   // dK = dSᵀ·Q
+          mma(KVS ? T_A : T_B, Opnd{adS, kC, 1}, Opnd{aQ + co, DH, 1}, QR / 16, NW, KVS);   // dK = dSᵀ·Q
           if (h == 0)
             for (int hq = 0; hq < NH; ++hq) {                                      // dQ += dS·K
               if constexpr (TMA)
@@ -594,12 +600,18 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
 #pragma unroll 1
         for (int c1 = r0; c1 < r1; c1 += 32) {
           float dv[32], dk[32];
-          tmem_row2<32>(T_A + lo + c1, dv, T_B + lo + c1, dk);
+          if constexpr (KVS) {                  // T_A holds dV + dK
+            tmem_row<32>(T_A + lo + c1, dk);
+#pragma unroll
+            for (int u = 0; u < 32; ++u) dv[u] = 0.f;
+          } else {
+            tmem_row2<32>(T_A + lo + c1, dv, T_B + lo + c1, dk);
+          }
           if constexpr (SHORT) {
             // through this warp's 2 × 2 KB of the (consumed) dS / P tiles: 16-byte segments
             // XOR-swizzled, conflict-free both ways; out as 64-byte row segments
             uint4* stg = reinterpret_cast<uint4*>(sdS) + (warp - 1) * 256;
-            if (a.sum_kv) {
+            if (a.sum_kv && !KVS) {
 #pragma unroll
               for (int u = 0; u < 32; ++u) dk[u] += dv[u];
             }
@@ -692,13 +704,18 @@ int pack_of(const AttnArgs& a) {
   return std::max(1, std::min(p, a.B));
 }
 
-template <int DH, bool TMA>
+template <int DH, bool TMA, bool KVS = false>
 int launch_fwd_t(const AttnArgs& a, const CUtensorMap& tK, const CUtensorMap& tV, int pack, cudaStream_t st) {
   const int smem = (128 * DH + std::max(128 * kC, kC * DH) + kC * DH) * 2 + 64 + 1024;
-  smem_attr(xattn_fwd_kernel<DH, TMA>, 227 * 1024);
-  launch(xattn_fwd_kernel<DH, TMA>, ((a.B + pack - 1) / pack) * a.heads, kThreads, std::max(smem, 80 * 1024), st, a,
-         tK, tV, pack);
+  smem_attr(xattn_fwd_kernel<DH, TMA, KVS>, 227 * 1024);
+  launch(xattn_fwd_kernel<DH, TMA, KVS>, ((a.B + pack - 1) / pack) * a.heads, kThreads, std::max(smem, 80 * 1024), st,
+         a, tK, tV, pack);
   return (int)cudaGetLastError();
+}
+
+// keys and values are the same rows (sum_kv: the absorbed cross layer)
+inline bool kv_same(const AttnArgs& a) {
+  return a.sum_kv && a.Kp == a.V && a.ldk == a.ldv && a.sk == a.sv;
 }
 
 template <int DH>
@@ -708,18 +725,21 @@ int launch_fwd(const AttnArgs& a, cudaStream_t st) {
   // only idle SMs (measured +10 µs per step); LONGER_ATTN_PACK=2 forces it for testing
   const int pack = g_knobs.attn_pack == 2 ? pack_of<DH>(a) : 1;
   if constexpr (DH >= 64) {
-    if (kv_maps<DH>(a, pack, tK, tV)) return launch_fwd_t<DH, true>(a, tK, tV, pack, st);
+    if (kv_maps<DH>(a, pack, tK, tV)) {
+      if (kv_same(a) && g_knobs.attn_kvs) return launch_fwd_t<DH, true, true>(a, tK, tV, pack, st);
+      return launch_fwd_t<DH, true>(a, tK, tV, pack, st);
+    }
   }
   return launch_fwd_t<DH, false>(a, tK, tV, pack, st);
 }
 
-template <int DH, bool TMA, bool SHORT>
+template <int DH, bool TMA, bool SHORT, bool KVS = false>
 int launch_bwd_t(const AttnArgs& a, const CUtensorMap& tK, const CUtensorMap& tV, int pack, cudaStream_t st) {
-  const int QR = (DH > 128 || SHORT) ? 64 : 128, KVB = SHORT ? 2 : 1;
-  const int smem = (2 * QR * DH + KVB * 2 * kC * DH + 2 * QR * kC) * 2 + 256 * 4 + 64 + 1024;
-  smem_attr(xattn_bwd_kernel<DH, TMA, SHORT>, 227 * 1024);
-  launch(xattn_bwd_kernel<DH, TMA, SHORT>, ((a.B + pack - 1) / pack) * a.heads, kThreads8, std::max(smem, 116 * 1024),
-         st, a, tK, tV, pack);
+  const int QR = (DH > 128 || SHORT) ? 64 : 128, KVB = SHORT ? 2 : 1, KVT = KVS ? 1 : 2;
+  const int smem = (2 * QR * DH + KVB * KVT * kC * DH + 2 * QR * kC) * 2 + 256 * 4 + 64 + 1024;
+  smem_attr(xattn_bwd_kernel<DH, TMA, SHORT, KVS>, 227 * 1024);
+  launch(xattn_bwd_kernel<DH, TMA, SHORT, KVS>, ((a.B + pack - 1) / pack) * a.heads, kThreads8,
+         std::max(smem, 116 * 1024), st, a, tK, tV, pack);
   return (int)cudaGetLastError();
 }
 
@@ -731,8 +751,10 @@ int launch_bwd(const AttnArgs& a, cudaStream_t st) {
     if (kv_maps<DH>(a, pack, tK, tV)) {
       if constexpr (DH <= 128) {
         // one sample per CTA, ≤ 64 queries, several key chunks: double-buffered K / V
-        if (pack == 1 && a.nq <= 64 && a.nk > kC && g_knobs.attn_short)
+        if (pack == 1 && a.nq <= 64 && a.nk > kC && g_knobs.attn_short) {
+          if (kv_same(a) && g_knobs.attn_kvs) return launch_bwd_t<DH, true, true, true>(a, tK, tV, pack, st);
           return launch_bwd_t<DH, true, true>(a, tK, tV, pack, st);
+        }
       }
       return launch_bwd_t<DH, true, false>(a, tK, tV, pack, st);
     }

@@ -563,6 +563,7 @@ int block_fwd(const Ctx& c, const BlockOff& bo, BlockBufs& b, const float* xq, b
       a.Kp = p.kn; a.ldk = D; a.sk = (long long)p.v * D;
       a.V = p.kn; a.ldv = D; a.sv = (long long)p.v * D;
       a.ctx = p.xa_craw; a.ctx32 = p.xa_craw32;
+      a.sum_kv = 1;                                  // keys are values: one shared tile per chunk
     } else {
       a.Q = b.qkv; a.ldq = D; a.sq = (long long)p.q * D;
       a.Kp = p.KV; a.ldk = 2 * D; a.sk = (long long)p.v * 2 * D;

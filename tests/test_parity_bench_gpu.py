@@ -162,3 +162,21 @@ def test_absorbed_cross_kv_projections(merge, monkeypatch):
             assert not np.any(grads["cross.b_k"])
             pf = model.forward(batch).cpu().numpy().astype(np.float64)
             assert np.max(np.abs(pf - p_ref)) <= 5e-3
+
+
+def test_shared_kv_tile_matches_separate_tiles(monkeypatch):
+    """With absorbed projections the cross attention's keys and values are the same rows: one TMA
+    tile per chunk serves both (and dV + dK accumulate in one TMEM region).  Same step as loading
+    the rows twice (LONGER_ATTN_KVS=0) up to fp32 accumulation order."""
+    cfg = ModelConfig(**C2).validate()
+    P = _perturbed(cfg, 29)
+    batch = synthetic_batch(cfg, 6, seed=8, min_events=1)
+    model = _model(cfg, P)
+    p, loss, grads = _run(model, batch)
+    monkeypatch.setenv("LONGER_ATTN_KVS", "0")
+    p2, loss2, grads2 = _run(model, batch)
+    np.testing.assert_allclose(p2, p, atol=1e-6)
+    top = max(np.abs(g).max() for g in grads.values())
+    for name in grads:
+        scale = max(np.abs(grads[name]).max(), 1e-2 * top)
+        assert np.abs(grads2[name] - grads[name]).max() <= 1e-3 * scale, name
