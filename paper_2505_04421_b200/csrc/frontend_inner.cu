@@ -269,6 +269,15 @@ __global__ void __launch_bounds__(32 * (1 + kWorkers * NG), 1) fe_inner_bwd_kern
       ones_col(sXN);
       store_row(sDX2, row, DT, dx2, HD, c0);
       signal();
+      // the next tile's h / dmerged rows into L2 while this one runs (register-free: a register
+      // prefetch spills at the 168-register ceiling), so its R0 loads hit L2 instead of HBM
+      {
+        const long long tn = (tile + gridDim.x) * kTile + row;
+        if (grp == 0 && tn < a.T) {
+          sm100::prefetch_l2(a.h_in + tn * DT);
+          sm100::prefetch_l2(a.dmerged + tn * DT);
+        }
+      }
       // ---- R1: q, k, v; group attention (scratch keeps q|k|v (bf16) and P (fp32) for the peers)
       wait_d();
       uint32_t qp[HD / 2];                       // q as bf16 pairs (the scores' operand)
