@@ -677,6 +677,248 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_kernel(AttnArgs a, con
   if (warp == 0) sm100::tmem_dealloc<512>(tmem);
 }
 
+// ------------------------------------------------------------------ transposed backward (keys = values)
+// The absorbed cross layer's backward (one sample per CTA, nq ≤ 64 queries, nk keys = values = kn)
+// with the KEYS as the tile rows: Sᵀ = K·Q'ᵀ and dPᵀ = K·dOᵀ land as [128 keys × 64 queries] in
+// TMEM, double-buffered, so the tensor core computes chunk i+1 while the workers turn chunk i into
+// Pᵀ and dSᵀ — and every lane of every worker warp is a key row (in the query-row layout only the
+// 35 query rows of 128 lanes had work).  The chunk sequence is pass 1 then pass 2 (K tiles by 3-D
+// TMA, two buffers, the refill of one issued while the other is computed).
+//   pass 1: D_q = Σ_k P_kq·dP_kq (per-thread sums over the chunks, a warp column sum, a 4-quarter
+//           reduction in shared memory) — with exactly the P and dP of pass 2, so Σ_k dS_kq = 0;
+//   pass 2: Pᵀ, dSᵀ = Pᵀ ⊙ (dPᵀ − D)·scale → shared memory → dKV = Pᵀ·dO + dSᵀ·Q' (one TMEM
+//           accumulator: keys are values) and dQ' += dS·K (dS read MN-major from the dSᵀ tile).
+// TMEM: Sᵀ ×2, dPᵀ ×2 (64 columns each), dKV (DH), dQ' (DH) = 512 columns at DH = 128.
+template <int DH>
+__global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_t_kernel(AttnArgs a, const __grid_constant__ CUtensorMap tmK) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  constexpr int NQ = 64, PT = 128;                // query columns; P / dS tile row length (zero-padded)
+  bf16* sK = reinterpret_cast<bf16*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  bf16* sQ = sK + 2 * kC * DH;                    // NQ x DH  Q'  (canonical K-major)
+  bf16* sdO = sQ + NQ * DH;                       // NQ x DH  dO
+  bf16* sPT = sdO + NQ * DH;                      // kC x PT  Pᵀ  (keys x queries)
+  bf16* sdST = sPT + kC * PT;                     // kC x PT  dSᵀ
+  uint4* sStg = reinterpret_cast<uint4*>(sdST + kC * PT);      // per worker warp: 32 x 32 bf16
+  float* sL = reinterpret_cast<float*>(sStg + 8 * 128);        // lse [NQ]
+  float* sD = sL + NQ;                                         // D [NQ]
+  float* sDp = sD + NQ;                                        // [4][NQ] per-quarter partial D
+  int* sVlo = reinterpret_cast<int*>(sDp + 4 * NQ);            // visible key interval per query
+  int* sVhi = sVlo + NQ;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sVhi + NQ);
+  uint64_t* bar_kv = bars;            // [2] K tile landed
+  uint64_t* bar_sd = bars + 2;        // [2] Sᵀ / dPᵀ buffer ready
+  uint64_t* bar_fr = bars + 4;        // [2] Sᵀ / dPᵀ buffer read out by the workers
+  uint64_t* bar_kf = bars + 6;        // [2] the MMAs reading K buffer b are done
+  uint64_t* bar_pd = bars + 8;        // Pᵀ / dSᵀ written
+  uint64_t* bar_kvd = bars + 9;       // dKV / dQ' MMAs done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  const int b = blockIdx.x;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 8; ++i) sm100::mbar_init(&bars[i], (i >= 4 && i < 6) ? 32 * 2 * kWorkers : 1);
+    sm100::mbar_init(bar_pd, 32 * 2 * kWorkers);
+    sm100::mbar_init(bar_kvd, 1);
+    sm100::fence_barrier_init();
+  }
+  if (warp == 0) sm100::tmem_alloc<512>(tmem_slot);
+  pdl_trigger();
+  pdl_wait();
+  // operand tiles and per-query tables (every thread)
+  const float scale = rsqrtf((float)a.D);
+  const int nq = a.nq;
+  for (int e = threadIdx.x; e < NQ * DH / 8; e += blockDim.x) {
+    const int r = e / (DH / 8), c = (e % (DH / 8)) * 8;
+    uint4 qv = make_uint4(0, 0, 0, 0), ov = qv;
+    if (r < nq) {
+      qv = *reinterpret_cast<const uint4*>(a.Q + b * a.sq + (long long)r * a.ldq + c);
+      const float* src = a.dctx + b * a.sdc + (long long)r * a.lddc + c;
+      const float4 x = *reinterpret_cast<const float4*>(src), y = *reinterpret_cast<const float4*>(src + 4);
+      ov = make_uint4(sm100::pack_bf16(x.x, x.y), sm100::pack_bf16(x.z, x.w), sm100::pack_bf16(y.x, y.y),
+                      sm100::pack_bf16(y.z, y.w));
+    }
+    *reinterpret_cast<uint4*>(sQ + canon(r, c, DH)) = qv;
+    *reinterpret_cast<uint4*>(sdO + canon(r, c, DH)) = ov;
+  }
+  for (int e = threadIdx.x; e < 2 * kC * PT / 8; e += blockDim.x) reinterpret_cast<uint4*>(sPT)[e] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x < NQ) {
+    const int qi = threadIdx.x;
+    int lo = 0, hi = 0;
+    float lse = 0.f;
+    if (qi < nq) {
+      const VisRule vis{a.k, a.G, a.ns, a.goff, a.npg[b], a.qg ? a.qg + (long long)b * a.k : nullptr, a.learn,
+                       a.self_keys};
+      lse = a.lse[(long long)b * nq + qi];
+      if (lse != -INFINITY) vis_interval(vis, qi, a.nk, lo, hi);
+    }
+    sVlo[qi] = lo; sVhi[qi] = hi; sL[qi] = lse;
+  }
+  sm100::fence_async_smem();
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t T_KV = tmem + 256, T_Q = tmem + 256 + DH;
+  auto T_S = [&](int sb) { return tmem + 64 * sb; };
+  auto T_P = [&](int sb) { return tmem + 128 + 64 * sb; };
+  const int nchunk = (a.nk + kC - 1) / kC;
+  const int nload = 2 * nchunk;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t aK0 = sm100::smem_u32(sK), aQ = sm100::smem_u32(sQ), adO = sm100::smem_u32(sdO);
+      const uint32_t aPT = sm100::smem_u32(sPT), adST = sm100::smem_u32(sdST);
+      constexpr uint32_t kBuf = kC * DH * 2;
+      uint32_t kvph = 0, frph = 0, kfph = 0, pdph = 0;     // parity bits: bit b = buffer b
+      auto load = [&](int i) {
+        const int kb = i & 1;
+        bf16* dst = sK + kb * kC * DH;
+        sm100::mbar_arrive_expect_tx(&bar_kv[kb], kC * DH * 2);
+#pragma unroll
+        for (int i2 = 0; i2 < DH / 64; ++i2)
+          sm100::tma_load_3d(dst + i2 * kC * 64, &tmK, &bar_kv[kb], 64 * i2, (i % nchunk) * kC, b);
+      };
+      auto wait_bit = [&](uint64_t* bar, uint32_t& ph, int bit) {
+        sm100::mbar_wait(bar, (ph >> bit) & 1u);
+        ph ^= 1u << bit;
+      };
+      sm100::tma_prefetch(&tmK);
+      load(0);
+      if (nload > 1) load(1);
+      for (int i = 0; i < nload; ++i) {
+        const int kb = i & 1;
+        if (i >= 1 && i + 1 < nload) {                 // refill: load i+1 once use i-1 is done
+          wait_bit(&bar_kf[(i + 1) & 1], kfph, (i + 1) & 1);
+          load(i + 1);
+        }
+        wait_bit(&bar_kv[kb], kvph, kb);
+        if (i >= 2) wait_bit(&bar_fr[kb], frph, kb);    // Sᵀ / dPᵀ buffer kb read out (use i-2)
+        sm100::tc_fence_after();
+        const uint32_t aK = aK0 + kb * kBuf;
+        mma(T_S(kb), OpndSW{aK, kC, 0}, Opnd{aQ, DH, 0}, DH / 16, NQ, false);       // Sᵀ  = K·Q'ᵀ
+        mma(T_P(kb), OpndSW{aK, kC, 0}, Opnd{adO, DH, 0}, DH / 16, NQ, false);      // dPᵀ = K·dOᵀ
+        sm100::mma_commit(&bar_sd[kb]);
+        if (i >= nchunk) {
+          sm100::mbar_wait(bar_pd, pdph);
+          pdph ^= 1;
+          sm100::tc_fence_after();
+          mma(T_KV, Opnd{aPT, PT, 0}, Opnd{adO, DH, 1}, NQ / 16, DH, false);        // Pᵀ·dO
+          mma(T_KV, Opnd{adST, PT, 0}, Opnd{aQ, DH, 1}, NQ / 16, DH, true);         // + dSᵀ·Q'
+          mma(T_Q, Opnd{adST, PT, 1}, OpndSW{aK, kC, 1}, kC / 16, DH, i > nchunk);   // dQ' += dS·K
+          sm100::mma_commit(bar_kvd);
+        }
+        sm100::mma_commit(&bar_kf[kb]);
+      }
+    }
+  } else {
+    const int q = warp & 3, g = (warp - 1) >> 2;
+    const int row = q * 32 + lane;                    // key row within a chunk (= TMEM lane)
+    const uint32_t lo = (uint32_t)(q * 32) << 16;
+    const int c0 = 32 * g;                            // this warp's query columns
+    uint32_t sdph = 0, kvdph = 0;
+    auto signal = [&](uint64_t* bar) { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(bar); };
+    auto load_sd = [&](int i, float (&s)[32], float (&dp)[32]) {
+      const int sb = i & 1;
+      sm100::mbar_wait(&bar_sd[sb], (sdph >> sb) & 1u);
+      sdph ^= 1u << sb;
+      sm100::tc_fence_after();
+      tmem_row2<32>(T_S(sb) + lo + c0, s, T_P(sb) + lo + c0, dp);
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&bar_fr[sb]);
+    };
+    // pass 1: D
+    {
+      float dacc[32];
+#pragma unroll
+      for (int u = 0; u < 32; ++u) dacc[u] = 0.f;
+      for (int i = 0; i < nchunk; ++i) {
+        float s[32], dp[32];
+        load_sd(i, s, dp);
+        const int key = i * kC + row;
+#pragma unroll
+        for (int u = 0; u < 32; ++u)
+          if (key >= sVlo[c0 + u] && key < sVhi[c0 + u]) dacc[u] = fmaf(__expf(fmaf(s[u], scale, -sL[c0 + u])), dp[u], dacc[u]);
+      }
+      const float col = warp_colsum<32>(dacc);       // lane l: column c0 + l over this warp's rows
+      sDp[q * NQ + c0 + lane] = col;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (threadIdx.x - 32 < NQ) {
+        const int cc = threadIdx.x - 32;
+        sD[cc] = (sDp[cc] + sDp[NQ + cc]) + (sDp[2 * NQ + cc] + sDp[3 * NQ + cc]);
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+    }
+    // dKV rows of chunk c: staged through this warp's 2 KB, out as 64-byte row segments
+    uint4* stg = sStg + (warp - 1) * 128;
+    auto store_kv = [&](int c) {
+      const int kbase = c * kC + q * 32;
+#pragma unroll 1
+      for (int cc = (DH / 2) * g; cc < (DH / 2) * (g + 1); cc += 32) {
+        float v[32];
+        tmem_row<32>(T_KV + lo + cc, v);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          stg[lane * 4 + (j ^ ((lane >> 1) & 3))] =
+              make_uint4(sm100::pack_bf16(v[8 * j], v[8 * j + 1]), sm100::pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                         sm100::pack_bf16(v[8 * j + 4], v[8 * j + 5]), sm100::pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int r = k * 8 + (lane >> 2), sgm = lane & 3;
+          if (kbase + r < a.nk)
+            *reinterpret_cast<uint4*>(a.dK + (long long)b * a.sdk + (long long)(kbase + r) * a.lddk + cc + sgm * 8) =
+                stg[r * 4 + (sgm ^ ((r >> 1) & 3))];
+        }
+        __syncwarp();
+      }
+    };
+    // pass 2
+    for (int c = 0; c < nchunk; ++c) {
+      float s[32], dp[32];
+      load_sd(nchunk + c, s, dp);
+      const int key = c * kC + row;
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        const bool v = key >= sVlo[c0 + u] && key < sVhi[c0 + u];
+        const float p = v ? __expf(fmaf(s[u], scale, -sL[c0 + u])) : 0.f;
+        s[u] = p;
+        dp[u] = p * (dp[u] - sD[c0 + u]) * scale;
+      }
+      if (c > 0) {                                      // chunk c-1's dKV / dQ' MMAs (they read Pᵀ, dSᵀ)
+        sm100::mbar_wait(bar_kvd, kvdph);
+        kvdph ^= 1;
+        sm100::tc_fence_after();
+        store_kv(c - 1);
+      }
+      store_row(sPT, row, PT, s, 32, c0);
+      store_row(sdST, row, PT, dp, 32, c0);
+      signal(bar_pd);
+    }
+    sm100::mbar_wait(bar_kvd, kvdph);
+    kvdph ^= 1;
+    sm100::tc_fence_after();
+    store_kv(nchunk - 1);
+    // dQ' rows (queries) in lanes 0..63: quarters 0 and 1
+    if (q < 2) {
+#pragma unroll 1
+      for (int cc = (DH / 2) * g; cc < (DH / 2) * (g + 1); cc += 32) {
+        float v[32];
+        tmem_row<32>(T_Q + lo + cc, v);
+        if (row < nq) {
+          bf16* dst = a.dQ + b * a.sdq + (long long)row * a.lddq + cc;
+#pragma unroll
+          for (int u = 0; u < 32; u += 8)
+            *reinterpret_cast<uint4*>(dst + u) =
+                make_uint4(sm100::pack_bf16(v[u], v[u + 1]), sm100::pack_bf16(v[u + 2], v[u + 3]),
+                           sm100::pack_bf16(v[u + 4], v[u + 5]), sm100::pack_bf16(v[u + 6], v[u + 7]));
+        }
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) sm100::tmem_dealloc<512>(tmem);
+}
+
 // K / V tensor maps [B][nk][D] over the strided projections (false: the strides or base addresses
 // miss TMA's 16-byte rules, or LONGER_ATTN_TMA=0 → thread loads).
 template <int DH>
@@ -752,6 +994,14 @@ int launch_bwd(const AttnArgs& a, cudaStream_t st) {
       if constexpr (DH <= 128) {
         // one sample per CTA, ≤ 64 queries, several key chunks: double-buffered K / V
         if (pack == 1 && a.nq <= 64 && a.nk > kC && g_knobs.attn_short) {
+          if (kv_same(a) && a.heads == 1 && g_knobs.attn_bwd_t) {
+            // keys as tile rows (xattn_bwd_t_kernel)
+            const int smem = (2 * kC * DH + 2 * 64 * DH + 2 * kC * 128) * 2 + 8 * 2048 + (2 * 64 + 4 * 64) * 4 +
+                             2 * 64 * 4 + 16 * 8 + 1024;
+            smem_attr(xattn_bwd_t_kernel<DH>, smem);
+            launch(xattn_bwd_t_kernel<DH>, a.B, kThreads8, smem, st, a, tK);
+            return (int)cudaGetLastError();
+          }
           if (kv_same(a) && g_knobs.attn_kvs) return launch_bwd_t<DH, true, true, true>(a, tK, tV, pack, st);
           return launch_bwd_t<DH, true, true>(a, tK, tV, pack, st);
         }

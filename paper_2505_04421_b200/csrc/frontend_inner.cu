@@ -68,6 +68,10 @@ __global__ void __launch_bounds__(32 * (1 + kWorkers * NG), 1) fe_inner_bwd_kern
   extern __shared__ __align__(128) uint8_t smem_raw[];
   constexpr int XK = DT + 16;                 // activation rows carrying a ones column
   constexpr int F4 = 4 * DT;
+  // row length of the FFN tiles sGF / sDF: their weight-gradient MMAs read them MN-major with the
+  // hidden units as the M = 128 dimension, so d = 16 (F4 = 64) pads the rows to 128 (the padding
+  // columns only feed accumulator rows ≥ F4, which are never read)
+  constexpr int FP4 = F4 < 128 ? 128 : F4;
   constexpr int QS = 3 * DT + 8;              // bf16 q|k|v scratch row (16-byte rows; rows 4 apart
                                               // fall in different bank groups)
   constexpr int DCS = DT + 4;                 // fp32 dctx scratch row
@@ -91,11 +95,11 @@ __global__ void __launch_bounds__(32 * (1 + kWorkers * NG), 1) fe_inner_bwd_kern
   bf16* sX1N = sCTX + kTile * XK;             // 128 x XK
   bf16* sDX2 = sX1N + kTile * XK;             // 128 x DT
   bf16* sDX1 = sDX2 + kTile * DT;             // 128 x DT
-  bf16* sGF = sDX1 + kTile * DT;              // 128 x F4   (later: dqkv 128 x 3DT)
-  bf16* sDF = sGF + kTile * F4;               // 128 x F4   (later: dctx fp32 scratch)
+  bf16* sGF = sDX1 + kTile * DT;              // 128 x FP4  (later: dqkv 128 x 3DT)
+  bf16* sDF = sGF + kTile * FP4;              // 128 x FP4  (later: dctx fp32 scratch)
   bf16* sDQKV = sGF;
   float* sDC = reinterpret_cast<float*>(sDF); // 128 x DCS
-  bf16* sQKV = sDF + kTile * F4;              // 128 x QS bf16 (q, k, v for the group peers)
+  bf16* sQKV = sDF + kTile * FP4;              // 128 x QS bf16 (q, k, v for the group peers)
   float* sP = reinterpret_cast<float*>(sQKV + kTile * QS);   // NG x 128 x KG (one copy per group)
   float* sS = sP + NG * kTile * KG;                             // NG x 128 x KG (dS)
   float* s_par = sS + NG * kTile * KG;        // [ln1_g, ln1_b, b_o, ln2_g, ln2_b] x DT
@@ -167,10 +171,10 @@ __global__ void __launch_bounds__(32 * (1 + kWorkers * NG), 1) fe_inner_bwd_kern
         // behind that commit and are covered by the next one, which precedes any rewrite of
         // their operands (sGF / sDF are reused as dqkv / dctx scratch only after the dx1 commit).
         wait_a();                                                           // gf, df
-        mma(T_W2, Opnd{S(sDF), F4, 0}, Opnd{S(w_w1i_n), F4, 0}, F4 / 16, DT, false);
+        mma(T_W2, Opnd{S(sDF), FP4, 0}, Opnd{S(w_w1i_n), F4, 0}, F4 / 16, DT, false);
         sm100::mma_commit(bar_d);
-        mma(T_DW2, Opnd{S(sGF), F4, 1}, Opnd{S(sDX2), DT, 1}, kTile / 16, DT, !first);
-        mma(T_DW1, Opnd{S(sDF), F4, 1}, Opnd{S(sX1N), XK, 1}, kTile / 16, XK, !first);
+        mma(T_DW2, Opnd{S(sGF), FP4, 1}, Opnd{S(sDX2), DT, 1}, kTile / 16, DT, !first);
+        mma(T_DW1, Opnd{S(sDF), FP4, 1}, Opnd{S(sX1N), XK, 1}, kTile / 16, XK, !first);
         wait_a();                                                           // dx1
         mma(T_W2, Opnd{S(sDX1), DT, 0}, Opnd{S(w_wo_n), DT, 0}, DT / 16, DT, false);
         sm100::mma_commit(bar_d);
@@ -350,8 +354,8 @@ __global__ void __launch_bounds__(32 * (1 + kWorkers * NG), 1) fe_inner_bwd_kern
           fv[u] = gelu_and_grad(fv[u], gd);
           gv[u] *= gd;
         }
-        store_row(sGF, row, F4, fv, 32, cc);
-        store_row(sDF, row, F4, gv, 32, cc);
+        store_row(sGF, row, FP4, fv, 32, cc);
+        store_row(sDF, row, FP4, gv, 32, cc);
       }
       signal();
       // ---- R4: LN2 backward → dx1 = dX2 + LN2ᵀ(dx1n)
@@ -468,15 +472,19 @@ __global__ void __launch_bounds__(32 * (1 + kWorkers * NG), 1) fe_inner_bwd_kern
       float w[HD], wb[16];
       {   // dW2 [4d][d]: TMEM row f = hidden unit
         tmem_row<HD>(T_DW2 + lo + c0, w);
+        if (row < F4) {
 #pragma unroll
-        for (int c = 0; c < HD; ++c) atomicAdd(G[10] + row * DT + c0 + c, w[c]);
+          for (int c = 0; c < HD; ++c) atomicAdd(G[10] + row * DT + c0 + c, w[c]);
+        }
       }
       {   // [dW1ᵀ | db1]: row f = hidden unit
         tmem_row<HD>(T_DW1 + lo + c0, w);
         tmem_row<16>(T_DW1 + lo + DT, wb);
+        if (row < F4) {
 #pragma unroll
-        for (int c = 0; c < HD; ++c) atomicAdd(G[8] + (c0 + c) * F4 + row, w[c]);
-        if (bias_col) atomicAdd(G[9] + row, wb[0]);
+          for (int c = 0; c < HD; ++c) atomicAdd(G[8] + (c0 + c) * F4 + row, w[c]);
+          if (bias_col) atomicAdd(G[9] + row, wb[0]);
+        }
       }
       {   // [dWoᵀ | dbo]: row c = output column of W_o (first DT rows valid)
         tmem_row<HD>(T_DWO + lo + c0, w);
@@ -513,9 +521,9 @@ __global__ void __launch_bounds__(32 * (1 + kWorkers * NG), 1) fe_inner_bwd_kern
 
 template <int DT, int KG, int NG>
 int launch_inner_bwd_ng(const FrontArgs& a, cudaStream_t st) {
-  constexpr int XK = DT + 16, F4 = 4 * DT, QS = 3 * DT + 8;
+  constexpr int XK = DT + 16, F4 = 4 * DT, FP4 = F4 < 128 ? 128 : F4, QS = 3 * DT + 8;
   const int nW = 7 * DT * XK + DT * DT + 12 * DT * DT;
-  const int smem = nW * 2 + kTile * (3 * XK + 2 * DT + 2 * F4 + QS) * 2 + NG * kTile * KG * 8 + 5 * DT * 4 +
+  const int smem = nW * 2 + kTile * (3 * XK + 2 * DT + 2 * FP4 + QS) * 2 + NG * kTile * KG * 8 + 5 * DT * 4 +
                    (NG > 1 ? 2 * NG * kTile * 8 * 4 : 0) + 64;
   if (smem > 227 * 1024) return (int)cudaErrorInvalidValue;
   smem_attr(fe_inner_bwd_kernel<DT, KG, NG>, 227 * 1024);

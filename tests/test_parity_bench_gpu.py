@@ -180,3 +180,46 @@ def test_shared_kv_tile_matches_separate_tiles(monkeypatch):
     for name in grads:
         scale = max(np.abs(grads[name]).max(), 1e-2 * top)
         assert np.abs(grads2[name] - grads[name]).max() <= 1e-3 * scale, name
+
+
+@pytest.mark.parametrize("heads_D", [(1, 128), (1, 64)], ids=["D128", "D64"])
+def test_keys_as_rows_cross_attention_backward(heads_D, monkeypatch):
+    """The absorbed cross layer's attention backward with the keys as the tile rows (Sᵀ / dPᵀ
+    double-buffered in TMEM, every worker lane a key row): the oracle bar, and the same step as
+    the query-row kernel (LONGER_ATTN_BWD_T=0) up to fp32 accumulation order."""
+    heads, D = heads_D
+    cfg = ModelConfig(**dict(C2, d=D // 4, heads=heads)).validate()
+    P = _perturbed(cfg, 37)
+    batch = synthetic_batch(cfg, 6, seed=12, min_events=1)
+    model = _model(cfg, P)
+    p, loss, grads = _run(model, batch)
+    p_ref, loss_ref, G = O.forward_backward(P, cfg, batch.as_dict())
+    assert np.max(np.abs(p - p_ref)) <= 5e-3
+    assert abs(loss - loss_ref) <= loss_tol(p_ref, batch.label)
+    assert_grads_close(grads, G, f"bwd_t D={D}")
+    monkeypatch.setenv("LONGER_ATTN_BWD_T", "0")
+    p2, loss2, grads2 = _run(model, batch)
+    np.testing.assert_allclose(p2, p, atol=1e-6)
+    top = max(np.abs(g).max() for g in grads.values())
+    for name in grads:
+        scale = max(np.abs(grads[name]).max(), 1e-2 * top)
+        assert np.abs(grads2[name] - grads[name]).max() <= 2e-3 * scale, name
+
+
+@pytest.mark.parametrize("fe_grid", [None, "3"], ids=["full-grid", "capped-grid"])
+def test_d16_inner_trans_fused_backward(fe_grid, monkeypatch):
+    """Token width 16 with InnerTrans (D = 64, FFN hidden 4d = 64 < 128): the fused InnerTrans
+    backward's weight-gradient MMAs take the hidden units as their M = 128 dimension, so the
+    64-wide FFN tiles are padded to 128-element rows and only accumulator rows < 64 are flushed
+    (found by this test: before, rows 64-127 were misread and added past W2's gradient)."""
+    if fe_grid:
+        monkeypatch.setenv("LONGER_FE_GRID", fe_grid)
+    cfg = ModelConfig(**dict(C2, d=16)).validate()
+    P = _perturbed(cfg, 37)
+    batch = synthetic_batch(cfg, 6, seed=12, min_events=1)
+    model = _model(cfg, P)
+    p, loss, grads = _run(model, batch)
+    p_ref, loss_ref, G = O.forward_backward(P, cfg, batch.as_dict())
+    assert np.max(np.abs(p - p_ref)) <= 5e-3
+    assert abs(loss - loss_ref) <= loss_tol(p_ref, batch.label)
+    assert_grads_close(grads, G, f"d16 inner fe_grid={fe_grid}")
