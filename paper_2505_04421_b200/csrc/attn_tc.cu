@@ -704,7 +704,8 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_t_kernel(AttnArgs a, c
   float* sDp = sD + NQ;                                        // [4][NQ] per-quarter partial D
   int* sVlo = reinterpret_cast<int*>(sDp + 4 * NQ);            // visible key interval per query
   int* sVhi = sVlo + NQ;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sVhi + NQ);
+  int* sMono = sVhi + NQ;                                      // [2]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sMono + 2);
   uint64_t* bar_kv = bars;            // [2] K tile landed
   uint64_t* bar_sd = bars + 2;        // [2] Sᵀ / dPᵀ buffer ready
   uint64_t* bar_fr = bars + 4;        // [2] Sᵀ / dPᵀ buffer read out by the workers
@@ -752,6 +753,22 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_t_kernel(AttnArgs a, c
     }
     sVlo[qi] = lo; sVhi[qi] = hi; sL[qi] = lse;
   }
+  // Cross-layer intervals share one lower end (the first non-pad key) and their upper ends never
+  // decrease with the query index (sorted query groups, then the globals by rank; pad queries
+  // first with an empty interval): a key row's visible columns are then a suffix of the valid
+  // queries, found by a binary search instead of a test per column.  Verified here.
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int ok = 1, lo0 = -1;
+    for (int qi = 0; qi < nq; ++qi) {
+      if (qi > 0 && sVhi[qi] < sVhi[qi - 1]) ok = 0;
+      if (sVhi[qi] > sVlo[qi]) {
+        if (lo0 < 0) lo0 = sVlo[qi];
+        else if (sVlo[qi] != lo0) ok = 0;
+      } else if (sVhi[qi] != 0) ok = 0;
+    }
+    sMono[0] = ok ? (lo0 < 0 ? (1 << 30) : lo0) : -1;   // the shared lower end, or -1: test per column
+  }
   sm100::fence_async_smem();
   sm100::tc_fence_before();
   __syncthreads();
@@ -781,32 +798,41 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_t_kernel(AttnArgs a, c
         sm100::mbar_wait(bar, (ph >> bit) & 1u);
         ph ^= 1u << bit;
       };
-      sm100::tma_prefetch(&tmK);
-      load(0);
-      if (nload > 1) load(1);
-      for (int i = 0; i < nload; ++i) {
+      // Sᵀ / dPᵀ of load i into buffer i & 1 (its K tile landed; the workers read out use i-2)
+      auto issue_sd = [&](int i) {
         const int kb = i & 1;
-        if (i >= 1 && i + 1 < nload) {                 // refill: load i+1 once use i-1 is done
-          wait_bit(&bar_kf[(i + 1) & 1], kfph, (i + 1) & 1);
-          load(i + 1);
-        }
         wait_bit(&bar_kv[kb], kvph, kb);
-        if (i >= 2) wait_bit(&bar_fr[kb], frph, kb);    // Sᵀ / dPᵀ buffer kb read out (use i-2)
+        if (i >= 2) wait_bit(&bar_fr[kb], frph, kb);
         sm100::tc_fence_after();
         const uint32_t aK = aK0 + kb * kBuf;
         mma(T_S(kb), OpndSW{aK, kC, 0}, Opnd{aQ, DH, 0}, DH / 16, NQ, false);       // Sᵀ  = K·Q'ᵀ
         mma(T_P(kb), OpndSW{aK, kC, 0}, Opnd{adO, DH, 0}, DH / 16, NQ, false);      // dPᵀ = K·dOᵀ
         sm100::mma_commit(&bar_sd[kb]);
+      };
+      sm100::tma_prefetch(&tmK);
+      load(0);
+      if (nload > 1) load(1);
+      issue_sd(0);
+      for (int i = 0; i < nload; ++i) {
+        const int kb = i & 1;
+        // the next chunk's scores first: the tensor core works on them while the workers turn
+        // this chunk into Pᵀ / dSᵀ
+        if (i + 1 < nload) issue_sd(i + 1);
         if (i >= nchunk) {
           sm100::mbar_wait(bar_pd, pdph);
           pdph ^= 1;
           sm100::tc_fence_after();
+          const uint32_t aK = aK0 + kb * kBuf;
           mma(T_KV, Opnd{aPT, PT, 0}, Opnd{adO, DH, 1}, NQ / 16, DH, false);        // Pᵀ·dO
           mma(T_KV, Opnd{adST, PT, 0}, Opnd{aQ, DH, 1}, NQ / 16, DH, true);         // + dSᵀ·Q'
           mma(T_Q, Opnd{adST, PT, 1}, OpndSW{aK, kC, 1}, kC / 16, DH, i > nchunk);   // dQ' += dS·K
           sm100::mma_commit(bar_kvd);
         }
-        sm100::mma_commit(&bar_kf[kb]);
+        if (i + 2 < nload) {                            // K buffer kb: refill once use i is done
+          sm100::mma_commit(&bar_kf[kb]);
+          wait_bit(&bar_kf[kb], kfph, kb);
+          load(i + 2);
+        }
       }
     }
   } else {
@@ -825,6 +851,26 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_t_kernel(AttnArgs a, c
       sm100::tc_fence_before();
       sm100::mbar_arrive(&bar_fr[sb]);
     };
+    // visible columns [c0, c0 + 32) of key row `key`, bit u = column c0 + u
+    const int mono = sMono[0];
+    auto vis_mask = [&](int key) -> uint32_t {
+      if (mono >= 0) {
+        if (key < mono) return 0u;
+        int lo_c = c0, hi_c = min(c0 + 32, nq);       // first column with vhi > key (vhi sorted)
+        while (lo_c < hi_c) {
+          const int mid = (lo_c + hi_c) >> 1;
+          if (sVhi[mid] > key) hi_c = mid; else lo_c = mid + 1;
+        }
+        const int end = min(c0 + 32, nq);
+        if (lo_c >= end) return 0u;
+        const uint32_t from = lo_c - c0, to = end - c0;   // bits [from, to)
+        return (to >= 32 ? 0xffffffffu : ((1u << to) - 1u)) & ~((1u << from) - 1u);
+      }
+      uint32_t m = 0;
+#pragma unroll
+      for (int u = 0; u < 32; ++u) m |= (key >= sVlo[c0 + u] && key < sVhi[c0 + u]) ? (1u << u) : 0u;
+      return m;
+    };
     // pass 1: D
     {
       float dacc[32];
@@ -833,10 +879,12 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_t_kernel(AttnArgs a, c
       for (int i = 0; i < nchunk; ++i) {
         float s[32], dp[32];
         load_sd(i, s, dp);
-        const int key = i * kC + row;
+        const uint32_t m = vis_mask(i * kC + row);
+        if (m) {
 #pragma unroll
-        for (int u = 0; u < 32; ++u)
-          if (key >= sVlo[c0 + u] && key < sVhi[c0 + u]) dacc[u] = fmaf(__expf(fmaf(s[u], scale, -sL[c0 + u])), dp[u], dacc[u]);
+          for (int u = 0; u < 32; ++u)
+            if (m & (1u << u)) dacc[u] = fmaf(__expf(fmaf(s[u], scale, -sL[c0 + u])), dp[u], dacc[u]);
+        }
       }
       const float col = warp_colsum<32>(dacc);       // lane l: column c0 + l over this warp's rows
       sDp[q * NQ + c0 + lane] = col;
@@ -847,26 +895,36 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_t_kernel(AttnArgs a, c
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");
     }
-    // dKV rows of chunk c: staged through this warp's 2 KB, out as 64-byte row segments
+    // dKV rows of chunk c: read out of TMEM as bf16 pairs (so the next dKV MMA may start), then
+    // staged through this warp's 2 KB and stored as 64-byte row segments
     uint4* stg = sStg + (warp - 1) * 128;
+    constexpr int KVW = DH / 2;                       // dKV columns of this warp
+    uint32_t kvp[KVW / 2];
+    auto read_kv = [&]() {
+#pragma unroll
+      for (int cc = 0; cc < KVW; cc += 32) {
+        float v[32];
+        tmem_row<32>(T_KV + lo + KVW * g + cc, v);
+#pragma unroll
+        for (int u = 0; u < 32; u += 2) kvp[(cc + u) / 2] = sm100::pack_bf16(v[u], v[u + 1]);
+      }
+    };
     auto store_kv = [&](int c) {
       const int kbase = c * kC + q * 32;
-#pragma unroll 1
-      for (int cc = (DH / 2) * g; cc < (DH / 2) * (g + 1); cc += 32) {
-        float v[32];
-        tmem_row<32>(T_KV + lo + cc, v);
+#pragma unroll
+      for (int cc = 0; cc < KVW; cc += 32) {
 #pragma unroll
         for (int j = 0; j < 4; ++j)
           stg[lane * 4 + (j ^ ((lane >> 1) & 3))] =
-              make_uint4(sm100::pack_bf16(v[8 * j], v[8 * j + 1]), sm100::pack_bf16(v[8 * j + 2], v[8 * j + 3]),
-                         sm100::pack_bf16(v[8 * j + 4], v[8 * j + 5]), sm100::pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+              make_uint4(kvp[(cc + 8 * j) / 2], kvp[(cc + 8 * j) / 2 + 1], kvp[(cc + 8 * j) / 2 + 2],
+                         kvp[(cc + 8 * j) / 2 + 3]);
         __syncwarp();
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const int r = k * 8 + (lane >> 2), sgm = lane & 3;
           if (kbase + r < a.nk)
-            *reinterpret_cast<uint4*>(a.dK + (long long)b * a.sdk + (long long)(kbase + r) * a.lddk + cc + sgm * 8) =
-                stg[r * 4 + (sgm ^ ((r >> 1) & 3))];
+            *reinterpret_cast<uint4*>(a.dK + (long long)b * a.sdk + (long long)(kbase + r) * a.lddk + KVW * g + cc +
+                                      sgm * 8) = stg[r * 4 + (sgm ^ ((r >> 1) & 3))];
         }
         __syncwarp();
       }
@@ -875,10 +933,10 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_t_kernel(AttnArgs a, c
     for (int c = 0; c < nchunk; ++c) {
       float s[32], dp[32];
       load_sd(nchunk + c, s, dp);
-      const int key = c * kC + row;
+      const uint32_t m = vis_mask(c * kC + row);
 #pragma unroll
       for (int u = 0; u < 32; ++u) {
-        const bool v = key >= sVlo[c0 + u] && key < sVhi[c0 + u];
+        const bool v = (m >> u) & 1u;
         const float p = v ? __expf(fmaf(s[u], scale, -sL[c0 + u])) : 0.f;
         s[u] = p;
         dp[u] = p * (dp[u] - sD[c0 + u]) * scale;
@@ -887,15 +945,17 @@ __global__ void __launch_bounds__(kThreads8, 1) xattn_bwd_t_kernel(AttnArgs a, c
         sm100::mbar_wait(bar_kvd, kvdph);
         kvdph ^= 1;
         sm100::tc_fence_after();
-        store_kv(c - 1);
+        read_kv();
       }
       store_row(sPT, row, PT, s, 32, c0);
       store_row(sdST, row, PT, dp, 32, c0);
-      signal(bar_pd);
+      signal(bar_pd);                                  // tcgen05 fence included: the dKV read is done
+      if (c > 0) store_kv(c - 1);
     }
     sm100::mbar_wait(bar_kvd, kvdph);
     kvdph ^= 1;
     sm100::tc_fence_after();
+    read_kv();
     store_kv(nchunk - 1);
     // dQ' rows (queries) in lanes 0..63: quarters 0 and 1
     if (q < 2) {
@@ -997,7 +1057,7 @@ int launch_bwd(const AttnArgs& a, cudaStream_t st) {
           if (kv_same(a) && a.heads == 1 && g_knobs.attn_bwd_t) {
             // keys as tile rows (xattn_bwd_t_kernel)
             const int smem = (2 * kC * DH + 2 * 64 * DH + 2 * kC * 128) * 2 + 8 * 2048 + (2 * 64 + 4 * 64) * 4 +
-                             2 * 64 * 4 + 16 * 8 + 1024;
+                             2 * 64 * 4 + 16 + 16 * 8 + 1024;
             smem_attr(xattn_bwd_t_kernel<DH>, smem);
             launch(xattn_bwd_t_kernel<DH>, a.B, kThreads8, smem, st, a, tK);
             return (int)cudaGetLastError();
