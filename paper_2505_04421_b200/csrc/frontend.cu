@@ -382,22 +382,32 @@ __global__ void __launch_bounds__(32 * 5 * S, 1) fe_fwd_kernel(FrontArgs a) {
       float h[DT];
       {
         // x0 = P[item] + P[action] + P[bucket] + abs_pos[recency]  (the featuriser's tok_proj
-        // applied per table row: FrontArgs::proj)
+        // applied per table row: FrontArgs::proj).  The warp gathers its 32 rows cooperatively —
+        // DT / 4 lanes per row, one float4 each, so one load instruction covers whole 128-byte
+        // rows of 32 / (DT / 4) tokens instead of 32 scattered 16-byte pieces — and writes x0
+        // straight into its rows of the canonical A tile.
         int pr[3];
         proj_rows(a, ti, pr);
-        const float4* pp = reinterpret_cast<const float4*>(a.pos_tab + (long long)ti.rec * DT);
-        const float4* p0 = reinterpret_cast<const float4*>(a.proj + (long long)pr[0] * DT);
-        const float4* p1 = reinterpret_cast<const float4*>(a.proj + (long long)pr[1] * DT);
-        const float4* p2 = reinterpret_cast<const float4*>(a.proj + (long long)pr[2] * DT);
+        constexpr int LPR = DT / 4, RPS = 32 / LPR;      // lanes per row, rows per step
+        const int sub = lane % LPR, rsel = lane / LPR;
 #pragma unroll
-        for (int c = 0; c < DT; c += 4) {
-          const float4 x = __ldg(pp + c / 4), y0 = __ldg(p0 + c / 4), y1 = __ldg(p1 + c / 4), y2 = __ldg(p2 + c / 4);
-          h[c] = ti.real ? (y0.x + y1.x) + (y2.x + x.x) : 0.f;
-          h[c + 1] = ti.real ? (y0.y + y1.y) + (y2.y + x.y) : 0.f;
-          h[c + 2] = ti.real ? (y0.z + y1.z) + (y2.z + x.z) : 0.f;
-          h[c + 3] = ti.real ? (y0.w + y1.w) + (y2.w + x.w) : 0.f;
+        for (int st = 0; st < 32 / RPS; ++st) {
+          const int r = st * RPS + rsel;
+          const int i0 = __shfl_sync(0xffffffffu, pr[0], r), i1 = __shfl_sync(0xffffffffu, pr[1], r);
+          const int i2 = __shfl_sync(0xffffffffu, pr[2], r), rc = __shfl_sync(0xffffffffu, ti.rec, r);
+          const bool re = __shfl_sync(0xffffffffu, (int)ti.real, r) != 0;
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (re) {
+            const float4 x = __ldg(reinterpret_cast<const float4*>(a.pos_tab + (long long)rc * DT) + sub);
+            const float4 y0 = __ldg(reinterpret_cast<const float4*>(a.proj + (long long)i0 * DT) + sub);
+            const float4 y1 = __ldg(reinterpret_cast<const float4*>(a.proj + (long long)i1 * DT) + sub);
+            const float4 y2 = __ldg(reinterpret_cast<const float4*>(a.proj + (long long)i2 * DT) + sub);
+            v = make_float4((y0.x + y1.x) + (y2.x + x.x), (y0.y + y1.y) + (y2.y + x.y), (y0.z + y1.z) + (y2.z + x.z),
+                            (y0.w + y1.w) + (y2.w + x.w));
+          }
+          *reinterpret_cast<uint2*>(sA + canon(q * 32 + r, 4 * sub, XK)) =
+              make_uint2(sm100::pack_bf16(v.x, v.y), sm100::pack_bf16(v.z, v.w));
         }
-        store_row(sA, row, XK, h, DT);
         store_ones_col<DT>(sA, row);
       }
       signal();
