@@ -287,6 +287,24 @@ __device__ __forceinline__ void store_ones_col(bf16* tile, int row) {
   *reinterpret_cast<uint4*>(tile + canon(row, DT + 8, XK)) = make_uint4(0u, 0u, 0u, 0u);
 }
 
+// The warp's 32 token rows (thread = row, DT fp32 values) → dst rows [0, nvalid) (row stride DT),
+// through a 32 x DT fp32 staging area (16-byte chunks XOR-swizzled by row: conflict-free both ways)
+// so every store instruction writes whole 128-byte rows instead of 32 scattered 16-byte pieces.
+template <int DT>
+__device__ __forceinline__ void warp_store_rows_f32(float* dst, int nvalid, const float* h, float4* stg, int lane) {
+  constexpr int CH = DT / 4;                          // 16-byte chunks per row
+#pragma unroll
+  for (int j = 0; j < CH; ++j)
+    stg[lane * CH + (j ^ (lane & (CH - 1)))] = make_float4(h[4 * j], h[4 * j + 1], h[4 * j + 2], h[4 * j + 3]);
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < CH; ++k) {
+    const int idx = k * 32 + lane, r = idx / CH, sg = idx % CH;
+    if (r < nvalid) reinterpret_cast<float4*>(dst)[r * CH + sg] = stg[r * CH + (sg ^ (r & (CH - 1)))];
+  }
+  __syncwarp();
+}
+
 template <int DT, int KG, int S>
 __global__ void __launch_bounds__(32 * 5 * S, 1) fe_fwd_kernel(FrontArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -426,11 +444,12 @@ __global__ void __launch_bounds__(32 * 5 * S, 1) fe_fwd_kernel(FrontArgs a) {
       tmem_row<DT>(trow + 64, h);
 #pragma unroll
       for (int c = 0; c < DT; ++c) h[c] = ti.real ? h[c] + s_b2[c] : 0.f;
-      if (a.h_out && ti.in_range) {
-        float4* dst = reinterpret_cast<float4*>(a.h_out + ti.t * DT);
-#pragma unroll
-        for (int c = 0; c < DT; c += 4) dst[c / 4] = make_float4(h[c], h[c + 1], h[c + 2], h[c + 3]);
-      }
+      // rows staged through this warp's quarter of the slot's hidden tile (its W2 MMAs are done;
+      // the next writer is the k|v scratch after the QKV wait)
+      float4* stg = reinterpret_cast<float4*>(sH) + q * (32 * DT / 4);
+      const long long t0 = tile * kTile + q * 32;
+      const int nvalid = a.T - t0 < 32 ? (int)(a.T - t0) : 32;
+      if (a.h_out) warp_store_rows_f32<DT>(a.h_out + t0 * DT, nvalid, h, stg, lane);
       // the residual stream h is parked in the slot's TMEM columns [96, 128) while the attention
       // and FFN stages run (registers: 4S warps share the SM)
       const uint32_t tres = trow + 96;
@@ -541,11 +560,7 @@ __global__ void __launch_bounds__(32 * 5 * S, 1) fe_fwd_kernel(FrontArgs a) {
 #pragma unroll
         for (int c = 0; c < DT; ++c) h[c] = 0.f;
       }
-      if (ti.in_range) {
-        float4* dst = reinterpret_cast<float4*>(a.merged + ti.t * DT);
-#pragma unroll
-        for (int c = 0; c < DT; c += 4) dst[c / 4] = make_float4(h[c], h[c + 1], h[c + 2], h[c + 3]);
-      }
+      warp_store_rows_f32<DT>(a.merged + t0 * DT, nvalid, h, stg, lane);   // sH free: W2 MMAs done
       if (a.kn) {
         // cross LN1 of the merged row = the KG consecutive tokens of this group (adjacent lanes)
         float s1 = 0.f;
