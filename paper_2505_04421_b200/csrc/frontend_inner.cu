@@ -253,14 +253,34 @@ __global__ void __launch_bounds__(32 * (1 + kWorkers * NG), 1) fe_inner_bwd_kern
         keep = (j / a.K) >= (a.Lp - n) / a.K;
       }
       // ---- R0: x = h; LN1; dX2 = dmerged ⊙ keep
+      // The warp's 32 rows (its HD columns) of h and dmerged are loaded cooperatively — HD / 4
+      // lanes per row, so each instruction covers whole row segments — into a staging area in the
+      // (free: R5's MMAs are done) sGF tile, then each thread takes its own row.
       float h[HD], dx2[HD];
+      {
+        constexpr int CH = HD / 4, RPI = 32 / CH;        // 16-byte chunks per row, rows per instruction
+        float4* stg = reinterpret_cast<float4*>(sGF) + (warp - 1) * 2 * 32 * CH;
+        const long long tw = tile * kTile + q * 32;       // the warp's first token
 #pragma unroll
-      for (int c = 0; c < HD; c += 4) {
-        float4 hv = make_float4(0.f, 0.f, 0.f, 0.f), dv = hv;
-        if (in_range) hv = *reinterpret_cast<const float4*>(a.h_in + t * DT + c0 + c);
-        if (keep) dv = *reinterpret_cast<const float4*>(a.dmerged + t * DT + c0 + c);
-        h[c] = hv.x; h[c + 1] = hv.y; h[c + 2] = hv.z; h[c + 3] = hv.w;
-        dx2[c] = dv.x; dx2[c + 1] = dv.y; dx2[c + 2] = dv.z; dx2[c + 3] = dv.w;
+        for (int k = 0; k < 32 / RPI; ++k) {
+          const int r = k * RPI + lane / CH, sg = lane % CH;
+          float4 hv = make_float4(0.f, 0.f, 0.f, 0.f), dv = hv;
+          if (tw + r < a.T) {
+            hv = *reinterpret_cast<const float4*>(a.h_in + (tw + r) * DT + c0 + 4 * sg);
+            dv = *reinterpret_cast<const float4*>(a.dmerged + (tw + r) * DT + c0 + 4 * sg);
+          }
+          stg[r * CH + (sg ^ (r & (CH - 1)))] = hv;
+          stg[32 * CH + r * CH + (sg ^ (r & (CH - 1)))] = dv;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const float4 hv = stg[lane * CH + (j ^ (lane & (CH - 1)))];
+          const float4 dv = keep ? stg[32 * CH + lane * CH + (j ^ (lane & (CH - 1)))] : make_float4(0.f, 0.f, 0.f, 0.f);
+          h[4 * j] = hv.x; h[4 * j + 1] = hv.y; h[4 * j + 2] = hv.z; h[4 * j + 3] = hv.w;
+          dx2[4 * j] = dv.x; dx2[4 * j + 1] = dv.y; dx2[4 * j + 2] = dv.z; dx2[4 * j + 3] = dv.w;
+        }
+        __syncwarp();
       }
       float mu1, inv1;
       ln_stats(h, mu1, inv1);
