@@ -85,6 +85,15 @@ __device__ __forceinline__ uint32_t vis_bits(int lo, int hi, int j0) {
   return mb & ~((1u << a) - 1u);
 }
 
+// Tile row r of a (sample, head) CTA ↔ its query: packed rows r % nq of sample b0 + r / nq, else
+// query_of_row(r) of sample b0; false for rows past the queries / samples.
+__device__ __forceinline__ bool tile_query(const AttnArgs& a, int b0, int pack, int r, int& b, int& qi) {
+  const int sr = pack > 1 ? r / a.nq : 0;
+  qi = pack > 1 ? r % a.nq : query_of_row(r);
+  b = b0 + sr;
+  return qi < a.nq && sr < pack && b < a.B;
+}
+
 // Forward, ONE pass over the key chunks: S = Q·K_cᵀ in TMEM; the workers keep a running max m
 // and sum l per row and write P̃ = exp(s − m) (bf16) over the dead K tile; O += P̃·V_c accumulates
 // in TMEM.  When a chunk raises a row's max by more than kRescale the row's O is rescaled in TMEM
@@ -207,11 +216,25 @@ __global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a, cons
     uint32_t pd = 0;
     auto signal = [&]() { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(bar_a); };
     auto wait_d = [&]() { sm100::mbar_wait(bar_d, pd); pd ^= 1; sm100::tc_fence_after(); };
+    (void)Qb;
+    // the warp's 32 query rows into the canonical Q tile, cooperatively: 8 rows x 4 16-byte column
+    // chunks per instruction (whole 64-byte row segments instead of 32 scattered pieces)
+    {
+      const int lr = lane & 7, kc = lane >> 3;
 #pragma unroll
-    for (int c = 0; c < DH; c += 8) {
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (qrow) v = *reinterpret_cast<const uint4*>(Qb + (long long)qi * a.ldq + c);
-      *reinterpret_cast<uint4*>(sQ + canon(row, c, DH)) = v;
+      for (int rb = 0; rb < 4; ++rb) {
+        int bq, qq;
+        const int r = q * 32 + rb * 8 + lr;
+        const bool ok = tile_query(a, b0, pack, r, bq, qq);
+        const bf16* src = a.Q + bq * a.sq + (long long)qq * a.ldq + hd * DH;
+#pragma unroll
+        for (int k = 0; k < DH / 32; ++k) {
+          const int c = (4 * k + kc) * 8;
+          uint4 v = make_uint4(0, 0, 0, 0);
+          if (ok) v = *reinterpret_cast<const uint4*>(src + c);
+          *reinterpret_cast<uint4*>(sQ + canon(r, c, DH)) = v;
+        }
+      }
     }
     float m = -INFINITY, l = 0.f;
     for (int c = 0; c < nchunk; ++c) {
@@ -278,25 +301,39 @@ __global__ void __launch_bounds__(kThreads, 2) xattn_fwd_kernel(AttnArgs a, cons
       wait_d();                                     // O += P·V done: K|P and V tiles free
     }
     const float rl = l > 0.f ? 1.f / l : 0.f;
-    bf16* dst = a.ctx + b * a.sc + (long long)qi * a.ldc + hd * DH;
-    float* dst32 = a.ctx32 + b * a.sc + (long long)qi * a.ldc + hd * DH;
+    // O / l as bf16 rows through this warp's quarter of the (free: the last P·V is done) K|P tile,
+    // XOR-swizzled 16-byte chunks, out as whole rows; the fp32 copy (the SIMT backward's D_i input)
+    // only when asked for
+    constexpr int CH = DH / 8;                            // 16-byte chunks per bf16 row
+    constexpr int XM = CH >= 8 ? 7 : CH - 1;              // swizzle mask
+    uint4* stg = reinterpret_cast<uint4*>(sKP) + q * 32 * CH;
+    float* dst32 = a.ctx32 ? a.ctx32 + b * a.sc + (long long)qi * a.ldc + hd * DH : nullptr;
 #pragma unroll 1
     for (int c0 = 0; c0 < DH; c0 += 32) {
       float o[32];
       tmem_row<32>(T_O + lo_lane + c0, o);
-      if (!qrow) continue;
 #pragma unroll
       for (int c = 0; c < 32; c += 8) {
         float w[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) w[u] = o[c + u] * rl;
-        uint4 pk;
-        pk.x = sm100::pack_bf16(w[0], w[1]); pk.y = sm100::pack_bf16(w[2], w[3]);
-        pk.z = sm100::pack_bf16(w[4], w[5]); pk.w = sm100::pack_bf16(w[6], w[7]);
-        *reinterpret_cast<uint4*>(dst + c0 + c) = pk;
-        *reinterpret_cast<float4*>(dst32 + c0 + c) = make_float4(w[0], w[1], w[2], w[3]);
-        *reinterpret_cast<float4*>(dst32 + c0 + c + 4) = make_float4(w[4], w[5], w[6], w[7]);
+        const int j = (c0 + c) / 8;
+        stg[lane * CH + (j ^ (lane & XM))] = make_uint4(sm100::pack_bf16(w[0], w[1]), sm100::pack_bf16(w[2], w[3]),
+                                                       sm100::pack_bf16(w[4], w[5]), sm100::pack_bf16(w[6], w[7]));
+        if (dst32 && qrow) {
+          *reinterpret_cast<float4*>(dst32 + c0 + c) = make_float4(w[0], w[1], w[2], w[3]);
+          *reinterpret_cast<float4*>(dst32 + c0 + c + 4) = make_float4(w[4], w[5], w[6], w[7]);
+        }
       }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const int idx = k * 32 + lane, r = idx / CH, sg = idx % CH;
+      int bq, qq;
+      if (tile_query(a, b0, pack, q * 32 + r, bq, qq))
+        *reinterpret_cast<uint4*>(a.ctx + bq * a.sc + (long long)qq * a.ldc + hd * DH + sg * 8) =
+            stg[r * CH + (sg ^ (r & XM))];
     }
     if (qrow) a.lse[((long long)b * a.heads + hd) * a.nq + qi] = l > 0.f ? m + __logf(l) : -INFINITY;
   }

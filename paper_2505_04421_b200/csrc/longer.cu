@@ -578,6 +578,7 @@ int block_fwd(const Ctx& c, const BlockOff& bo, BlockBufs& b, const float* xq, b
     a.nk = p.q; a.ns = p.k; a.goff = p.G - p.k;
   }
   if (use_attn_tc(a)) {
+    a.ctx32 = nullptr;                  // only the SIMT backward reads the fp32 context
     if (cross) probe(PH_XATTN_FWD, 0, st);
     TRY(attn_tc_fwd(a, st));
     if (cross) probe(PH_XATTN_FWD, 1, st);
