@@ -536,13 +536,19 @@ bool use_attn_tc(const AttnArgs& a) {
 }
 
 // One pre-norm attention block over the q query rows (pkg/src/longrec/attention.py:172-212).
+// xq_src (optional): the query rows as [merged | globals] views; LN1 reads them there and
+// materialises xq (the residual) itself, instead of separate gather kernels
 int block_fwd(const Ctx& c, const BlockOff& bo, BlockBufs& b, const float* xq, bool cross, const bf16* Wqkv,
-              const float* bqkv, const bf16* Wo, const bf16* W1, const bf16* W2, bool compact = false) {
+              const float* bqkv, const bf16* Wo, const bf16* W1, const bf16* W2, bool compact = false,
+              const RowMap* xq_src = nullptr) {
   const Plan& p = c.p;
   cudaStream_t st = c.st;
   const int D = p.D;
   const long long Q = (long long)p.B * p.q;
-  layernorm_fwd(rows_plain(xq, D, Q), D, c.w(bo.ln1_g), c.w(bo.ln1_b), b.qn, b.m1, b.r1, st);
+  if (xq_src)
+    layernorm_fwd(*xq_src, D, c.w(bo.ln1_g), c.w(bo.ln1_b), b.qn, b.m1, b.r1, st, const_cast<float*>(xq));
+  else
+    layernorm_fwd(rows_plain(xq, D, Q), D, c.w(bo.ln1_g), c.w(bo.ln1_b), b.qn, b.m1, b.r1, st);
   AttnArgs a{};
   a.nq = p.q; a.D = D; a.heads = p.heads; a.k = p.k; a.G = p.G; a.npg = p.npg; a.B = p.B;
   a.qg = (p.qs == QS_UNIFORM || p.qs == QS_RECENT_UNIFORM) ? p.qg : nullptr;
@@ -710,6 +716,14 @@ int frontend_fused_fwd(const Ctx& c, const Plan& p, const LongerBatch& bt) {
   return frontend_fwd(f, c.st);
 }
 
+// O = [merged[G-k:]; globals] per sample (the "recent" strategy) as a RowMap over the two sources
+RowMap recent_query_rows(const Plan& p) {
+  RowMap r{};
+  r.A = p.merged; r.lda = p.D; r.a_rows = p.G; r.a_off = p.G - p.k; r.na = p.k;
+  r.Bsrc = p.glob; r.ldb = p.D; r.nb = p.m; r.batch = p.B;
+  return r;
+}
+
 int forward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs, float* loss, int with_loss) {
   cudaStream_t st = c.st;
   const ParamOff& o = p.po;
@@ -758,18 +772,19 @@ int forward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs, fl
     if (!p.absorb)
       TRY(lin_fwd(ss, p.kn, D, (long long)p.B * p.v, p.pk.c_wkv, D, 2 * D, p.pk.c_bkv, 0, nullptr, p.KV, nullptr));
   }
-  // sequence queries (select_queries, model.py:58-123)
-  if (p.qs == QS_RECENT) {
-    gather_rows_f32(p.merged, p.B, p.G, p.G - p.k, p.k, p.O, p.q, 0, D, st);
-  } else {
+  // sequence queries (select_queries, model.py:58-123).  "recent" queries are the last k merged
+  // rows: the cross block's LN1 reads them (and the globals) in place and materialises O itself
+  const RowMap qrows = recent_query_rows(p);
+  if (p.qs != QS_RECENT) {
     if (p.qs != QS_LEARNABLE) select_queries(p.npg, p.B, p.G, p.k, p.qs, p.qg, st);
     gather_query_rows(p.merged, p.qs == QS_LEARNABLE ? nullptr : p.qg, p.qs == QS_LEARNABLE ? c.w(o.qbank) : nullptr,
                       p.B, p.G, p.k, D, p.O, p.q, st);
   }
   wait_mark(st, ss);                                   // the global rows
-  gather_rows_f32(p.glob, p.B, p.m, 0, p.m, p.O, p.q, p.k, D, st);
+  if (p.qs != QS_RECENT) gather_rows_f32(p.glob, p.B, p.m, 0, p.m, p.O, p.q, p.k, D, st);
   Plan& pm = const_cast<Plan&>(p);
-  TRY(block_fwd(c, o.cross, pm.cb, p.O, true, p.pk.c_wq, nullptr, p.pk.c_wo, p.pk.c_w1, p.pk.c_w2));
+  TRY(block_fwd(c, o.cross, pm.cb, p.O, true, p.pk.c_wq, nullptr, p.pk.c_wo, p.pk.c_w1, p.pk.c_w2, false,
+                p.qs == QS_RECENT ? &qrows : nullptr));
   const float* xl = p.cb.out;
   for (int i = 0; i < p.N; ++i) {
     TRY(block_fwd(c, o.self_[i], pm.sb[i], xl, false, p.pk.s_wqkv[i], p.pk.s_bqkv[i], p.pk.s_wo[i], p.pk.s_w1[i],
@@ -913,14 +928,21 @@ int block_bwd(const Ctx& c, cudaStream_t ss, const BlockOff& bo, const BlockBufs
     layernorm_bwd(r, D, c.w(bo.ln1_g), p.mk, p.rk, dkn_bf, D, rw, c.g(bo.ln1_g), c.g(bo.ln1_b), st);
     LnBwdExtra ex;
     ex.addend = b.g_dx1;
-    layernorm_bwd(rows_plain(xq, D, Q), D, c.w(bo.ln1_g), b.m1, b.r1, b.g_dqn, D, rows_plain_w(p.dO, D, Q), 0,
-                  nullptr, c.g(bo.ln1_g), c.g(bo.ln1_b), st, ex);
-    if (p.qs == QS_RECENT)
-      add_rows_f32(p.dO, p.B, p.q, 0, p.k, p.dmerged, p.G, p.G - p.k, D, st);
-    else
+    if (p.qs == QS_RECENT) {
+      // straight into the query rows' sources: += into dmerged[G-k:] and dglob (which the K/V-row
+      // LN backward above has just written)
+      RowMapW qw{};
+      qw.A = p.dmerged; qw.lda = D; qw.a_rows = p.G; qw.a_off = p.G - p.k; qw.na = p.k;
+      qw.Bsrc = p.dglob; qw.ldb = D; qw.nb = p.m; qw.batch = p.B;
+      layernorm_bwd(recent_query_rows(p), D, c.w(bo.ln1_g), b.m1, b.r1, b.g_dqn, D, qw, 1, nullptr,
+                    c.g(bo.ln1_g), c.g(bo.ln1_b), st, ex);
+    } else {
+      layernorm_bwd(rows_plain(xq, D, Q), D, c.w(bo.ln1_g), b.m1, b.r1, b.g_dqn, D, rows_plain_w(p.dO, D, Q), 0,
+                    nullptr, c.g(bo.ln1_g), c.g(bo.ln1_b), st, ex);
       scatter_query_rows(p.dO, p.q, p.qg, p.B, p.G, p.k, D, p.dmerged,
                          p.qs == QS_LEARNABLE ? c.g(p.po.qbank) : nullptr, st);
-    add_rows_f32(p.dO, p.B, p.q, p.k, p.m, p.dglob, p.m, 0, D, st);
+      add_rows_f32(p.dO, p.B, p.q, p.k, p.m, p.dglob, p.m, 0, D, st);
+    }
   } else {
     for (int j = 0; j < 3; ++j) {
       const long long wo = j == 0 ? bo.w_q : (j == 1 ? bo.w_k : bo.w_v);

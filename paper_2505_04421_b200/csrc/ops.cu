@@ -224,7 +224,7 @@ __device__ __forceinline__ void ln_load(const bf16* __restrict__ p, int lane, in
 
 template <int VPT, bool CONTIG>
 __global__ void ln_fwd_kernel(RowMap x, int W, const float* __restrict__ g, const float* __restrict__ bta,
-                              bf16* y, float* mean, float* rstd) {
+                              bf16* y, float* mean, float* rstd, float* xcopy) {
   pdl_trigger();
   pdl_wait();
   const int warps = blockDim.x / 32;
@@ -252,6 +252,18 @@ __global__ void ln_fwd_kernel(RowMap x, int W, const float* __restrict__ g, cons
   const float inv = rsqrtf(var + kLnEps);
   const int orow = x.out_row(row);
   bf16* dst = y + (long long)orow * W;
+  if (xcopy) {                                        // the gathered input rows, materialised
+    float* xc = xcopy + (long long)orow * W;
+    if constexpr (CONTIG && VPT == 4) {
+      *reinterpret_cast<float4*>(xc + lane * 4) = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < VPT; ++u) {
+        const int c = ln_col<VPT, CONTIG>(lane, u);
+        if (c < W) xc[c] = v[u];
+      }
+    }
+  }
   if constexpr (CONTIG && VPT >= 2) {
     float gg[VPT], bb[VPT];
 #pragma unroll
@@ -284,15 +296,15 @@ bool ln_contig(int W, int vpt, const void* p0, int ld0, const void* p1, int ld1)
 }  // namespace
 
 void layernorm_fwd(const RowMap& x, int W, const float* g, const float* b, bf16* y, float* mean, float* rstd,
-                   cudaStream_t st) {
+                   cudaStream_t st, float* xcopy) {
   const int rows = x.rows();
   if (rows <= 0) return;
   const int grid = cdiv(rows, 8);
   const int vpt = W <= 32 ? 1 : W <= 64 ? 2 : W <= 128 ? 4 : 8;
   const bool ct = ln_contig(W, vpt, x.A, x.lda, x.nb ? x.Bsrc : nullptr, x.ldb);
-#define LNF(V) (ct ? launch(ln_fwd_kernel<V, true>, grid, 256, 0, st, x, W, g, b, y, mean, rstd) \
-                   : launch(ln_fwd_kernel<V, false>, grid, 256, 0, st, x, W, g, b, y, mean, rstd))
-  if (vpt == 1) launch(ln_fwd_kernel<1, false>, grid, 256, 0, st, x, W, g, b, y, mean, rstd);
+#define LNF(V) (ct ? launch(ln_fwd_kernel<V, true>, grid, 256, 0, st, x, W, g, b, y, mean, rstd, xcopy) \
+                   : launch(ln_fwd_kernel<V, false>, grid, 256, 0, st, x, W, g, b, y, mean, rstd, xcopy))
+  if (vpt == 1) launch(ln_fwd_kernel<1, false>, grid, 256, 0, st, x, W, g, b, y, mean, rstd, xcopy);
   else if (vpt == 2) LNF(2);
   else if (vpt == 4) LNF(4);
   else LNF(8);

@@ -47,9 +47,9 @@ struct RowMap {
     return o_per ? (row / (na + nb)) * o_per + o_off + row % (na + nb) : row;
   }
 };
-// y = LN(x)·g + b  → bf16 [rows, W]; mean/rstd saved
+// y = LN(x)·g + b  → bf16 [rows, W]; mean/rstd saved; xcopy (optional): the input rows, fp32 [rows, W]
 void layernorm_fwd(const RowMap& x, int W, const float* g, const float* b, bf16* y, float* mean, float* rstd,
-                   cudaStream_t st);
+                   cudaStream_t st, float* xcopy = nullptr);
 // out(remap-writable) (+)= LN_bw(dy); dgain/dbias accumulated (atomic) into grads.
 struct RowMapW {
   float* A; int lda; int a_rows; int a_off; int na;
