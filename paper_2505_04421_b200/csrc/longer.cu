@@ -1199,6 +1199,12 @@ struct ScorePlan {
   long long R;                 // users x candidates target rows
   bf16 *raw_bf, *gg, *qn, *qkv, *ctx, *x1n, *gf;
   float *x, *y, *m1, *r1, *x1, *m2, *r2;
+  // per-item mode (vocab ≤ R / 4): the target row's path up to the cross attention depends on the
+  // candidate item alone, so it runs once per vocabulary item and the candidates gather from it
+  bool items;
+  int V;
+  bf16 *i_raw, *i_gg, *i_qn, *i_qkv;
+  float *i_x, *i_m, *i_r;
   size_t bytes;
 };
 
@@ -1218,6 +1224,14 @@ ScorePlan make_score_plan(const LongerDims& d, int C, void* ws) {
   s.qkv = a.take<bf16>(R * 3 * D); s.ctx = a.take<bf16>(R * D);
   s.x1 = a.take<float>(R * D); s.x1n = a.take<bf16>(R * D); s.m2 = a.take<float>(R); s.r2 = a.take<float>(R);
   s.gf = a.take<bf16>(R * 4 * D);
+  s.V = d.vocab;
+  s.items = (long long)d.vocab * 4 <= R;
+  if (s.items) {
+    const long long V = d.vocab;
+    s.i_raw = a.take<bf16>(V * D); s.i_gg = a.take<bf16>(V * 2 * D); s.i_qn = a.take<bf16>(V * D);
+    s.i_qkv = a.take<bf16>(V * 3 * D); s.i_x = a.take<float>(V * D); s.i_m = a.take<float>(V);
+    s.i_r = a.take<float>(V);
+  }
   s.bytes = a.off + 256;
   return s;
 }
@@ -1232,19 +1246,22 @@ int lin_fwd_ld(cudaStream_t st, const bf16* X, int ldx, long long rows, const bf
 }
 
 // attention_block_cached (attention.py:215-236) for all R target rows: x → out.
+// pre_done: [Q | K_own | V_own] of the rows are already in s.qkv (the per-item mode)
 int serve_block(const Ctx& c, const ScorePlan& s, const BlockOff& bo, const float* x, float* out, bool cross,
                 const bf16* kv, int nk, int ns, int goff, const int32_t* npg, const bf16* Wqkv, const float* bqkv,
-                const bf16* Wo, const bf16* W1, const bf16* W2) {
+                const bf16* Wo, const bf16* W1, const bf16* W2, bool pre_done = false) {
   const Plan& p = s.p;
   cudaStream_t st = c.st;
   const int D = p.D;
   const long long R = s.R;
-  layernorm_fwd(rows_plain(x, D, R), D, c.w(bo.ln1_g), c.w(bo.ln1_b), s.qn, s.m1, s.r1, st);
-  if (cross) {   // cross weights are packed as W_q and [W_k | W_v]
-    TRY(lin_fwd_ld(st, s.qn, D, R, p.pk.c_wq, D, D, c.w(bo.b_q), s.qkv, 3 * D));
-    TRY(lin_fwd_ld(st, s.qn, D, R, p.pk.c_wkv, D, 2 * D, p.pk.c_bkv, s.qkv + D, 3 * D));
-  } else {
-    TRY(lin_fwd_ld(st, s.qn, D, R, Wqkv, D, 3 * D, bqkv, s.qkv, 3 * D));
+  if (!pre_done) {
+    layernorm_fwd(rows_plain(x, D, R), D, c.w(bo.ln1_g), c.w(bo.ln1_b), s.qn, s.m1, s.r1, st);
+    if (cross) {   // cross weights are packed as W_q and [W_k | W_v]
+      TRY(lin_fwd_ld(st, s.qn, D, R, p.pk.c_wq, D, D, c.w(bo.b_q), s.qkv, 3 * D));
+      TRY(lin_fwd_ld(st, s.qn, D, R, p.pk.c_wkv, D, 2 * D, p.pk.c_bkv, s.qkv + D, 3 * D));
+    } else {
+      TRY(lin_fwd_ld(st, s.qn, D, R, Wqkv, D, 3 * D, bqkv, s.qkv, 3 * D));
+    }
   }
   ServeAttnArgs a{};
   a.Q = s.qkv; a.ldq = 3 * D;
@@ -1272,18 +1289,33 @@ int cache_score(const Ctx& c, const ScorePlan& s, const char* cache, const int32
   const CacheLayout L = cache_layout(p);
   TRY(pack_weights(p, c.P, p.ws, st));
   TargetArgs t{};
-  t.cand = cand; t.R = R; t.d = p.d; t.D = D; t.d_item = dm.d_item; t.d_act = dm.d_act; t.d_time = dm.d_time;
+  t.d = p.d; t.D = D; t.d_item = dm.d_item; t.d_act = dm.d_act; t.d_time = dm.d_time;
   t.vocab = dm.vocab; t.item_tab = c.w(o.item); t.time_tab = c.w(o.time); t.tok_w = c.w(o.tok_w);
-  t.tok_b = c.w(o.tok_b); t.lift_w = c.w(o.lift_w); t.lift_b = c.w(o.lift_b); t.raw_bf = s.raw_bf;
+  t.tok_b = c.w(o.tok_b); t.lift_w = c.w(o.lift_w); t.lift_b = c.w(o.lift_b);
   t.status = p.status;
-  target_rows(t, st);
-  TRY(lin_fwd(st, s.raw_bf, D, R, p.pk.glob_w1, D, 2 * D, c.w(o.glob_b1), EPI_GELU, nullptr, s.gg, nullptr));
-  TRY(lin_fwd(st, s.gg, 2 * D, R, p.pk.glob_w2, 2 * D, D, c.w(o.glob_b2), 0, s.x, nullptr, nullptr));
+  if (s.items) {
+    // target_global_token → global MLP → cross LN1 → [Q | K_own | V_own] once per vocabulary item
+    // (the row depends on the candidate item alone), then one gather per candidate
+    const long long V = s.V;
+    t.cand = nullptr; t.R = V; t.raw_bf = s.i_raw;
+    target_rows(t, st);
+    TRY(lin_fwd(st, s.i_raw, D, V, p.pk.glob_w1, D, 2 * D, c.w(o.glob_b1), EPI_GELU, nullptr, s.i_gg, nullptr));
+    TRY(lin_fwd(st, s.i_gg, 2 * D, V, p.pk.glob_w2, 2 * D, D, c.w(o.glob_b2), 0, s.i_x, nullptr, nullptr));
+    layernorm_fwd(rows_plain(s.i_x, D, V), D, c.w(o.cross.ln1_g), c.w(o.cross.ln1_b), s.i_qn, s.i_m, s.i_r, st);
+    TRY(lin_fwd_ld(st, s.i_qn, D, V, p.pk.c_wq, D, D, c.w(o.cross.b_q), s.i_qkv, 3 * D));
+    TRY(lin_fwd_ld(st, s.i_qn, D, V, p.pk.c_wkv, D, 2 * D, p.pk.c_bkv, s.i_qkv + D, 3 * D));
+    gather_item_rows(cand, R, dm.vocab, s.i_x, s.i_qkv, D, s.x, s.qkv, p.status, st);
+  } else {
+    t.cand = cand; t.R = R; t.raw_bf = s.raw_bf;
+    target_rows(t, st);
+    TRY(lin_fwd(st, s.raw_bf, D, R, p.pk.glob_w1, D, 2 * D, c.w(o.glob_b1), EPI_GELU, nullptr, s.gg, nullptr));
+    TRY(lin_fwd(st, s.gg, 2 * D, R, p.pk.glob_w2, 2 * D, D, c.w(o.glob_b2), 0, s.x, nullptr, nullptr));
+  }
   const int32_t* npg = reinterpret_cast<const int32_t*>(cache + L.npg);
   float* x = s.x;
   float* y = s.y;
   TRY(serve_block(c, s, o.cross, x, y, true, reinterpret_cast<const bf16*>(cache + L.xkv), (int)L.xrows, p.G, 0, npg,
-                  nullptr, nullptr, p.pk.c_wo, p.pk.c_w1, p.pk.c_w2));
+                  nullptr, nullptr, p.pk.c_wo, p.pk.c_w1, p.pk.c_w2, s.items));
   std::swap(x, y);
   for (int i = 0; i < p.N; ++i) {
     const bf16* kv = reinterpret_cast<const bf16*>(cache + L.skv) + (size_t)i * p.B * L.srows * 2 * D;

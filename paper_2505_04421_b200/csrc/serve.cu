@@ -68,7 +68,7 @@ __global__ void target_rows_kernel(TargetArgs a) {
   __shared__ float s_tf[64], s_td[64];
   const long long r = blockIdx.x;
   const int F = a.d_item + a.d_act + a.d_time;
-  int item = a.cand[r];
+  int item = a.cand ? a.cand[r] : (int)r;
   if (item < 0 || item >= a.vocab) { if (threadIdx.x == 0) atomicOr(a.status, 1); item = 0; }
   for (int f = threadIdx.x; f < F; f += blockDim.x) {
     float v = 0.f;
@@ -92,6 +92,30 @@ __global__ void target_rows_kernel(TargetArgs a) {
 
 void target_rows(const TargetArgs& a, cudaStream_t st) {
   if (a.R) launch(target_rows_kernel, (unsigned)a.R, 128, 0, st, a);
+}
+
+// one warp per candidate row: D fp32 (x) + 3D bf16 (q | k_own | v_own) as 16-byte vectors
+__global__ void gather_item_rows_kernel(const int32_t* cand, long long R, int vocab, const float* item_x,
+                                        const bf16* item_qkv, int D, float* x, bf16* qkv, int* status) {
+  pdl_trigger();
+  pdl_wait();
+  const long long r = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (r >= R) return;
+  int item = cand[r];
+  if (item < 0 || item >= vocab) { if (lane == 0) atomicOr(status, 1); item = 0; }
+  const float4* sx = reinterpret_cast<const float4*>(item_x + (long long)item * D);
+  float4* dx = reinterpret_cast<float4*>(x + r * D);
+  for (int i = lane; i < D / 4; i += 32) dx[i] = sx[i];
+  const uint4* sq = reinterpret_cast<const uint4*>(item_qkv + (long long)item * 3 * D);
+  uint4* dq = reinterpret_cast<uint4*>(qkv + r * 3 * D);
+  for (int i = lane; i < 3 * D / 8; i += 32) dq[i] = sq[i];
+}
+
+void gather_item_rows(const int32_t* cand, long long R, int vocab, const float* item_x, const bf16* item_qkv, int D,
+                      float* x, bf16* qkv, int* status, cudaStream_t st) {
+  if (R) launch(gather_item_rows_kernel, (unsigned)((R + 7) / 8), 256, 0, st, cand, R, vocab, item_x, item_qkv, D, x, qkv,
+                status);
 }
 
 // ------------------------------------------------------------------ cached attention

@@ -23,7 +23,7 @@ struct CacheUserArgs {
 void cache_users(const CacheUserArgs& a, cudaStream_t st);
 
 struct TargetArgs {
-  const int32_t* cand;        // [R] candidate items
+  const int32_t* cand;        // [R] candidate items (nullptr: row r is item r)
   long long R;
   int d, D, d_item, d_act, d_time, vocab;
   const float *item_tab, *time_tab, *tok_w, *tok_b, *lift_w, *lift_b;
@@ -31,6 +31,12 @@ struct TargetArgs {
   int* status;
 };
 void target_rows(const TargetArgs& a, cudaStream_t st);
+
+// per-candidate rows from per-item tables (the candidate-only part of the target row's path):
+// x[r] = item_x[cand[r]] (fp32, D), qkv[r] = item_qkv[cand[r]] (bf16, 3D); out-of-range ids flag
+// status bit 0 and read item 0
+void gather_item_rows(const int32_t* cand, long long R, int vocab, const float* item_x, const bf16* item_qkv, int D,
+                      float* x, bf16* qkv, int* status, cudaStream_t st);
 
 struct ServeAttnArgs {
   const bf16* Q; int ldq;                 // [U*C rows] candidate queries
