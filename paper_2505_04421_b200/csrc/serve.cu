@@ -444,7 +444,8 @@ int serve_attn(const ServeAttnArgs& a, cudaStream_t st) {
 // user.  The head input [t, c, t·c, t·t, u_d] is never materialised: the warp stages its rows' t
 // and the user's c and u_d (coalesced), and for every 4 input columns i the 16 W1 words of the
 // four segments (rows i, D+i, 2D+i, 3D+i) are loaded once and applied to all kHeadRows rows from
-// float4 broadcasts of t and c.
+// float4 broadcasts of t (the user's c is folded into the t weights once per group: t·(W_t + c⊙W_tc)
+// + t²·W_tt, with t·(w_a + t·w_tt) one FMA pair per input).
 constexpr int kHeadRows = 8, kHeadThreads = 512;
 
 template <bool kSmemW>
@@ -487,42 +488,37 @@ __global__ void __launch_bounds__(kHeadThreads) serve_head_kernel(ServeHeadArgs 
 #pragma unroll
     for (int q = 0; q < kHeadRows; ++q) zp[q] = 0.f;
     for (int j = lane; j < hh; j += 32) {
+      // z1 = t·(W_t + diag(c)·W_tc) + (t⊙t)·W_tt + [c·W_c + u_d·W_ud + b1]: the user's c folds into
+      // the t weights once per row group, and the bracket is one value per group
       float acc[kHeadRows];
+      float kc = sB[j];
 #pragma unroll
-      for (int q = 0; q < kHeadRows; ++q) acc[q] = sB[j];
+      for (int q = 0; q < kHeadRows; ++q) acc[q] = 0.f;
 #pragma unroll 1
       for (int i = 0; i < D; i += 4) {
-        float wt[4], wc[4], wtc[4], wtt[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          wt[e] = W[(i + e) * hh + j];
-          wc[e] = W[(D + i + e) * hh + j];
-          wtc[e] = W[(2 * D + i + e) * hh + j];
-          wtt[e] = W[(3 * D + i + e) * hh + j];
-        }
         const float4 c4 = *reinterpret_cast<const float4*>(xc + i);
         const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
+        float wa[4], wtt[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          wa[e] = fmaf(cv[e], W[(2 * D + i + e) * hh + j], W[(i + e) * hh + j]);
+          kc = fmaf(cv[e], W[(D + i + e) * hh + j], kc);
+          wtt[e] = W[(3 * D + i + e) * hh + j];
+        }
 #pragma unroll
         for (int q = 0; q < kHeadRows; ++q) {
           const float4 t4 = *reinterpret_cast<const float4*>(x + q * D + i);
           const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
           float v = acc[q];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            v = fmaf(tv[e], wt[e], v);
-            v = fmaf(cv[e], wc[e], v);
-            v = fmaf(tv[e] * cv[e], wtc[e], v);
-            v = fmaf(tv[e] * tv[e], wtt[e], v);
-          }
+          for (int e = 0; e < 4; ++e) v = fmaf(tv[e], fmaf(tv[e], wtt[e], wa[e]), v);
           acc[q] = v;
         }
       }
 #pragma unroll 1
-      for (int i = 0; i < d2; ++i) {
-        const float w = W[(4 * D + i) * hh + j];
+      for (int i = 0; i < d2; ++i) kc = fmaf(xu[i], W[(4 * D + i) * hh + j], kc);
 #pragma unroll
-        for (int q = 0; q < kHeadRows; ++q) acc[q] = fmaf(xu[i], w, acc[q]);
-      }
+      for (int q = 0; q < kHeadRows; ++q) acc[q] += kc;
       const float w2j = sB[hh + j];
 #pragma unroll
       for (int q = 0; q < kHeadRows; ++q) zp[q] = fmaf(gelu_f(acc[q]), w2j, zp[q]);
