@@ -39,6 +39,7 @@ struct Knobs {
   int absorb_kv = 1;       // LONGER_ABSORB_KV: cross-layer K/V projections absorbed into the query rows
   int attn_kvs = 1;        // LONGER_ATTN_KVS: one shared K = V tile per key chunk when keys are values
   int attn_bwd_t = 1;      // LONGER_ATTN_BWD_T: keys-as-rows cross-attention backward (keys = values)
+  int glob_side = 1;       // LONGER_GLOB_SIDE: global-token backward chain on the side stream
   int head_rows = 1;       // LONGER_HEAD_ROWS: last block's row-wise tail on the two head rows
   int gemm_stage = 1;      // LONGER_GEMM_STAGE: smem-staged GEMM epilogue stores
   int split_items = 74;    // LONGER_SPLIT_ITEMS: split-K work-item target of the weight gradients
@@ -65,6 +66,7 @@ inline Knobs read_knobs() {
   k.absorb_kv = env_int("LONGER_ABSORB_KV", 1);
   k.attn_kvs = env_int("LONGER_ATTN_KVS", 1);
   k.attn_bwd_t = env_int("LONGER_ATTN_BWD_T", 1);
+  k.glob_side = env_int("LONGER_GLOB_SIDE", 1);
   k.head_rows = env_int("LONGER_HEAD_ROWS", 1);
   k.gemm_stage = env_int("LONGER_GEMM_STAGE", 1);
   k.split_items = env_int("LONGER_SPLIT_ITEMS", 74);

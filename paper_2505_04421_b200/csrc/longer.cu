@@ -1000,16 +1000,19 @@ int backward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs) {
     fork_side(st, ss);
     record_event(g_grad_event, es);
   }
-  // global-token MLP and raw rows
-  cast_rows_bf16(p.dglob, (int)M, D, D, p.dglob_bf, D, nullptr, st);
-  fork_side(st, ss);
+  // global-token MLP and raw rows: nothing on the token side needs them, so with the knob the
+  // whole chain runs on the side stream, launched ahead of the fused token backward
+  const cudaStream_t gs = g_knobs.glob_side ? ss : st;
+  if (gs != st) fork_side(st, ss);
+  cast_rows_bf16(p.dglob, (int)M, D, D, p.dglob_bf, D, nullptr, gs);
+  if (gs == st) fork_side(st, ss);
   TRY(lin_dw(ss, p.gg, 2 * D, 2 * D, p.dglob_bf, D, D, M, c.g(o.glob_w2)));
   colsum_f32(p.dglob, (int)M, D, D, c.g(o.glob_b2), ss);
-  TRY(lin_dx(st, p.dglob_bf, D, M, p.pk.glob_w2, D, 2 * D, D, nullptr, 0, p.dga, 2 * D, p.ga));
-  fork_side(st, ss);
+  TRY(lin_dx(gs, p.dglob_bf, D, M, p.pk.glob_w2, D, 2 * D, D, nullptr, 0, p.dga, 2 * D, p.ga));
+  if (gs == st) fork_side(st, ss);
   TRY(lin_dw(ss, p.raw_bf, D, D, p.dga, 2 * D, 2 * D, M, c.g(o.glob_w1)));
   colsum_bf16(p.dga, (int)M, 2 * D, 2 * D, c.g(o.glob_b1), ss);
-  TRY(lin_dx(st, p.dga, 2 * D, M, p.pk.glob_w1, 2 * D, D, 2 * D, p.draw, D, nullptr, 0));
+  TRY(lin_dx(gs, p.dga, 2 * D, M, p.pk.glob_w1, 2 * D, D, 2 * D, p.draw, D, nullptr, 0));
   GlobalsArgs ga{};
   ga.uid = bt.uid; ga.cand_item = bt.cand_item; ga.B = p.B; ga.m = p.m; ga.d = d; ga.D = D;
   ga.d_item = dm.d_item; ga.d_act = dm.d_act; ga.d_time = dm.d_time;
@@ -1018,7 +1021,7 @@ int backward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs) {
   ga.td = p.td; ga.draw = p.draw;
   ga.g_uid = c.g(o.uid); ga.g_item = c.g(o.item); ga.g_time = c.g(o.time); ga.g_cls = c.g(o.cls);
   ga.g_tok_w = c.g(o.tok_w); ga.g_tok_b = c.g(o.tok_b); ga.g_lift_w = c.g(o.lift_w); ga.g_lift_b = c.g(o.lift_b);
-  globals_raw_bwd(ga, st);
+  globals_raw_bwd(ga, gs);
   // InnerTrans backward (all-pad groups were zeroed after the last layer).  The fused forward
   // kept only its input h, so the per-stage activations are recomputed here first.
   float* dxt = p.dmerged;
