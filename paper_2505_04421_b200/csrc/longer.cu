@@ -984,6 +984,7 @@ int backward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs) {
   h.g_uid = c.g(o.uid); h.g_prof = c.g(o.prof);
   head_bwd(h, st);
   fork_side(st, ss);
+  head_wgrad(h, ss);                 // weight / table gradients: off the critical chain
   colsum_f32(last.g_dx, (int)(p.compact_head ? 2LL * p.B : Q), D, D, c.g(p.N ? o.self_[p.N - 1].b2 : o.cross.b2), ss);
   for (int i = p.N - 1; i >= 0; --i) {
     const float* xin = i == 0 ? p.cb.out : p.sb[i - 1].out;

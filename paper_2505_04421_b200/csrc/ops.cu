@@ -1702,6 +1702,10 @@ void head_bwd(const HeadArgs& a, cudaStream_t st) {
   } else {
     launch(head_bwd_kernel<false>, cdiv(a.B, kHeadWarps), 32 * kHeadWarps, smem, st, a);
   }
+}
+
+void head_wgrad(const HeadArgs& a, cudaStream_t st) {
+  const int HIN = 4 * a.D + 2 * a.d;
   const int n = HIN * a.hh + a.hh + 1;
   const int per = 16;
   launch(head_wgrad_kernel, dim3(cdiv(n, 128), cdiv(a.B, per)), 128, 0, st, a, per);

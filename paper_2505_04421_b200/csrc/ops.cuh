@@ -176,6 +176,8 @@ void loss_mean(const float* loss_per, int B, float* loss, cudaStream_t st);   //
 // dz[b] = dprobs[b] · p(1 − p): the head's logit gradient for an arbitrary upstream dL/dp
 void dz_from_dprobs(const float* probs, const float* dprobs, int B, float* dz, cudaStream_t st);
 void head_bwd(const HeadArgs& a, cudaStream_t st);
+// the head's weight / table gradients from head_bwd's dz1 (feeds only the gradient buffer)
+void head_wgrad(const HeadArgs& a, cudaStream_t st);
 // the two head rows of each sample (r0 = k+1, r1 = k+m−1) between a full [B·q, W] buffer and a
 // compact [2B, W] one (the scatter writes every row of `full`: zero outside the head rows)
 void head_rows_gather_f32(const float* full, float* compact, int B, int q, int r0, int r1, int W, cudaStream_t st);
