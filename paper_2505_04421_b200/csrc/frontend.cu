@@ -620,12 +620,15 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   const int Dm = DT * a.K;
   const int H2 = 2 * Dm;
-  const int nh = H2 / 128;
+  // this launch's hidden units [h0, h0 + HP) (all of them unless the MLP runs in passes)
+  const int h0 = a.mlp_hn ? a.mlp_h0 : 0, HP = a.mlp_hn ? a.mlp_hn : H2;
+  const bool last = a.mlp_last != 0;
+  const int nh = HP / 128;
   const int XK = DT + 16;                  // x0 tile row: [x0 | 1 | 0…] for the db1 column
   const BlobOff bo = blob_offsets(DT, Dm, a.inner_layers);
-  // smem carve-up
+  // smem carve-up (the weight images of this pass's hidden slice)
   bf16* sW = reinterpret_cast<bf16*>(smem_raw);                    // tp, w1 (fwd) + tp_n, w1_n, w2_n
-  const int n_tp = DT * kFP, n_w1 = H2 * DT, n_w1f = H2 * XK;
+  const int n_tp = DT * kFP, n_w1 = HP * DT, n_w1f = HP * XK;
   bf16* w_tp = sW;
   bf16* w_w1 = w_tp + n_tp;                    // [W1ᵀ | b1] image, K = XK
   bf16* w_tp_n = w_w1 + n_w1f;
@@ -687,10 +690,16 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
 
   if (warp == 0) {
     if (lane == 0) {
-      const int b1 = (n_tp + n_w1f) * 2, b2 = (n_tp + 2 * n_w1) * 2;
-      sm100::mbar_arrive_expect_tx(bar_w, b1 + b2);
-      load_blob(reinterpret_cast<uint8_t*>(w_tp), reinterpret_cast<const uint8_t*>(a.wblob + bo.tp), b1, bar_w);
-      load_blob(reinterpret_cast<uint8_t*>(w_tp_n), reinterpret_cast<const uint8_t*>(a.wblob + bo.tp_n), b2, bar_w);
+      sm100::mbar_arrive_expect_tx(bar_w, (2 * n_tp + n_w1f + 2 * n_w1) * 2);
+      auto copy = [&](bf16* dst, long long src_off, int elems) {
+        load_blob(reinterpret_cast<uint8_t*>(dst), reinterpret_cast<const uint8_t*>(a.wblob + src_off), elems * 2, bar_w);
+      };
+      copy(w_tp, bo.tp, n_tp);
+      copy(w_w1, bo.w1 + (long long)h0 * XK, n_w1f);                 // rows h0.. of [W1ᵀ | b1]
+      copy(w_tp_n, bo.tp_n, n_tp);
+      // W1 (backward image, K = 2D): columns [h0, h0 + HP) of each 8-row group are contiguous
+      for (int g8 = 0; g8 < DT / 8; ++g8) copy(w_w1_n + g8 * HP * 8, bo.w1_n + (long long)g8 * H2 * 8 + h0 * 8, HP * 8);
+      copy(w_w2_n, bo.w2_n + (long long)h0 * DT, n_w1);              // rows h0.. of W2 (K = d)
       sm100::mbar_wait(bar_w, 0);
       const uint32_t aW1 = sm100::smem_u32(w_w1), aTP = sm100::smem_u32(w_tp), aTPn = sm100::smem_u32(w_tp_n);
       const uint32_t aW1n = sm100::smem_u32(w_w1_n), aW2n = sm100::smem_u32(w_w2_n);
@@ -713,7 +722,7 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
           if (j + 1 < nh) {
             mma(T_DW2 + j * DT, Opnd{aG, 128, 1}, Opnd{aDH, DT, 1}, kTile / 16, DT, !first);
             mma(T_DW1 + j * XK, Opnd{aDA, 128, 1}, Opnd{aX0, XK, 1}, kTile / 16, XK, !first);
-            mma(T_X, Opnd{aDA, 128, 0}, Opnd{aW1n + canon(0, 128 * j, H2) * 2, H2, 0}, 8, DT, j > 0);
+            mma(T_X, Opnd{aDA, 128, 0}, Opnd{aW1n + canon(0, 128 * j, HP) * 2, HP, 0}, 8, DT, j > 0);
             mma(T_A1, Opnd{aX0, XK, 0}, Opnd{aW1 + canon(128 * (j + 1), 0, XK) * 2, XK, 0}, XK / 16, 128, false);
             mma(T_G1, Opnd{aDH, DT, 0}, Opnd{aW2n + canon(128 * (j + 1), 0, DT) * 2, DT, 0}, DT / 16, 128, false);
             sm100::mma_commit(bar_d);
@@ -721,17 +730,25 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
             // last half: the workers only wait for dx0 (T_X); the weight-gradient MMAs run on
             // behind that commit (sG / sDA / sDH / sX0 are next rewritten after the tile's final
             // commit, which covers them)
-            mma(T_X, Opnd{aDA, 128, 0}, Opnd{aW1n + canon(0, 128 * j, H2) * 2, H2, 0}, 8, DT, j > 0);
+            mma(T_X, Opnd{aDA, 128, 0}, Opnd{aW1n + canon(0, 128 * j, HP) * 2, HP, 0}, 8, DT, j > 0);
+            if (!last) {      // no later commit in this tile: this one covers the dW MMAs too
+              mma(T_DW2 + j * DT, Opnd{aG, 128, 1}, Opnd{aDH, DT, 1}, kTile / 16, DT, !first);
+              mma(T_DW1 + j * XK, Opnd{aDA, 128, 1}, Opnd{aX0, XK, 1}, kTile / 16, XK, !first);
+            }
             sm100::mma_commit(bar_d);
-            mma(T_DW2 + j * DT, Opnd{aG, 128, 1}, Opnd{aDH, DT, 1}, kTile / 16, DT, !first);
-            mma(T_DW1 + j * XK, Opnd{aDA, 128, 1}, Opnd{aX0, XK, 1}, kTile / 16, XK, !first);
+            if (last) {
+              mma(T_DW2 + j * DT, Opnd{aG, 128, 1}, Opnd{aDH, DT, 1}, kTile / 16, DT, !first);
+              mma(T_DW1 + j * XK, Opnd{aDA, 128, 1}, Opnd{aX0, XK, 1}, kTile / 16, XK, !first);
+            }
           }
         }
-        wait_a();                                                        // dx0 in sDX0
-        mma(T_DWTP, Opnd{aDX0, 64, 1}, Opnd{aFeat, kFP, 1}, kTile / 16, kFP, !first);
-        mma(T_Y, Opnd{aOH, 64, 1}, Opnd{aDX0, 64, 1}, kTile / 16, DT, !first);
-        mma(T_X, Opnd{aDX0, 64, 0}, Opnd{aTPn, DT, 0}, DT / 16, kFP, false);
-        sm100::mma_commit(bar_d);
+        if (last) {
+          wait_a();                                                      // dx0 in sDX0
+          mma(T_DWTP, Opnd{aDX0, 64, 1}, Opnd{aFeat, kFP, 1}, kTile / 16, kFP, !first);
+          mma(T_Y, Opnd{aOH, 64, 1}, Opnd{aDX0, 64, 1}, kTile / 16, DT, !first);
+          mma(T_X, Opnd{aDX0, 64, 0}, Opnd{aTPn, DT, 0}, DT / 16, kFP, false);
+          sm100::mma_commit(bar_d);
+        }
         first = false;
       }
     }
@@ -867,12 +884,35 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
         const int c0 = XH < DT ? grp * XH : 0;
         float dx0[XH];
         tmem_row<XH>(T_X + lane_off + c0, dx0);
+        float* part = a.dx0_part ? a.dx0_part + ((long long)b * a.Lp + j) * DT + c0 : nullptr;
+        if (h0 > 0 && col_ok) {                                        // earlier passes' hidden units
 #pragma unroll
-        for (int c = 0; c < XH; ++c) {
-          dx0[c] = ti.real ? dx0[c] : 0.f;
-          s_gpos[row * (DT + 1) + c0 + c] += dx0[c];                   // abs-pos row of this position
+          for (int c = 0; c < XH; c += 4) {
+            const float4 pv = *reinterpret_cast<const float4*>(part + c);
+            dx0[c] += pv.x; dx0[c + 1] += pv.y; dx0[c + 2] += pv.z; dx0[c + 3] += pv.w;
+          }
         }
-        store_row(sDX0, row, 64, dx0, XH, c0);
+        if (!last) {                                                   // hand the partial on
+          if (col_ok) {
+#pragma unroll
+            for (int c = 0; c < XH; c += 4)
+              *reinterpret_cast<float4*>(part + c) = make_float4(dx0[c], dx0[c + 1], dx0[c + 2], dx0[c + 3]);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < XH; ++c) {
+            dx0[c] = ti.real ? dx0[c] : 0.f;
+            s_gpos[row * (DT + 1) + c0 + c] += dx0[c];                 // abs-pos row of this position
+          }
+          store_row(sDX0, row, 64, dx0, XH, c0);
+        }
+      }
+      if (!last) {                                                     // no featuriser part in this pass
+        if (b + r < a.B) {
+          stage_a(b + r);
+          if (b + 2 * r < a.B) prefetch(b + 2 * r);
+        }
+        continue;
       }
       signal();
       wait_d();
@@ -932,7 +972,7 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
     if (my_tiles > 0) {
       const int F = a.d_item + a.d_act + a.d_time;
       for (int jh = 0; jh < nh; ++jh) {
-        const int f = 128 * jh + row;                                  // hidden unit
+        const int f = h0 + 128 * jh + row;                             // hidden unit
         if (grp == 0) {
           float w2[DT];
           tmem_row<DT>(T_DW2 + lane_off + jh * DT, w2);
@@ -946,7 +986,9 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
           atomicAdd(a.g_seq_b1 + f, w1[DT]);
         }
       }
-      if (grp == 0) {
+      if (!last) {
+        // the featuriser / table / db2 accumulators belong to the last pass
+      } else if (grp == 0) {
         // rows 0..DT-1: [dW_tpᵀ | db_tp]; rows 32..32+DT-1 (the dh half of sDX0): Σ dh (db2)
         float wt[kFP];
         tmem_row<kFP>(T_DWTP + lane_off, wt);                          // warp-collective load
@@ -1006,7 +1048,7 @@ int frontend_supported(int d, int K, int D, int F, int inner_layers) {
 
 int frontend_mlp_bwd_supported(int d, int K, int D) {
   (void)d; (void)K;
-  return 2 * D <= 256;
+  return 2 * D <= 256 || (2 * D) % 256 == 0;
 }
 
 void project_tables(const float* item_tab, const float* act_tab, const float* time_tab, const float* tok_w,
@@ -1108,12 +1150,13 @@ int frontend_fwd(const FrontArgs& a, cudaStream_t st) {
 template <int DT>
 static int launch_mlp_bwd(const FrontArgs& a, cudaStream_t st) {
   const int H2 = 2 * DT * a.K;
+  const int HP = H2 <= 256 ? H2 : 256;            // hidden units per pass
   const int XK = DT + 16;
   const int n_item = a.vocab * a.d_item;
   FrontArgs b = a;
   b.item_smem = g_knobs.item_smem != 0;
   const int tab = (b.item_smem && n_item <= 16384) ? n_item : 0;
-  const int smem = (2 * DT * kFP + 2 * H2 * DT + H2 * XK) * 2 + kTile * (kFP + XK + DT + 128 + 128 + 64 + 64) * 2 +
+  const int smem = (2 * DT * kFP + 2 * HP * DT + HP * XK) * 2 + kTile * (kFP + XK + DT + 128 + 128 + 64 + 64) * 2 +
                    (2 * kTile * (DT + 1) + tab) * 4 + 128;
   if (smem > 227 * 1024) return (int)cudaErrorInvalidValue;
   smem_attr(fe_mlp_bwd_kernel<DT>, 227 * 1024);
@@ -1122,7 +1165,18 @@ static int launch_mlp_bwd(const FrontArgs& a, cudaStream_t st) {
   int r = std::max(1, std::min(a.B, 148 / tps));
   if (g_knobs.fe_grid > 0) r = std::max(1, std::min(r, g_knobs.fe_grid / tps));   // testing: many tiles per CTA
   // > 113 KB of smem keeps one CTA per SM (the kernel allocates all 512 TMEM columns)
-  launch(fe_mlp_bwd_kernel<DT>, tps * r, kThreads8, std::max(smem, 116 * 1024), st, b);
+  if (H2 <= 256) {
+    b.mlp_h0 = 0; b.mlp_hn = 0; b.mlp_last = 1;
+    launch(fe_mlp_bwd_kernel<DT>, tps * r, kThreads8, std::max(smem, 116 * 1024), st, b);
+  } else {
+    // wider hidden layers: passes of 256 hidden units (TMEM / smem per pass as at 2D = 256), the
+    // partial dx0 carried in a.dx0_part; the last pass finishes the featuriser / table part
+    if (!a.dx0_part) return (int)cudaErrorInvalidValue;
+    for (int h = 0; h < H2; h += HP) {
+      b.mlp_h0 = h; b.mlp_hn = HP; b.mlp_last = h + HP >= H2;
+      launch(fe_mlp_bwd_kernel<DT>, tps * r, kThreads8, std::max(smem, 116 * 1024), st, b);
+    }
+  }
   return (int)cudaGetLastError();
 }
 

@@ -18,6 +18,12 @@ struct FrontArgs {
   const int32_t *items, *actions, *dt, *n_events;
   int B, L, Lp, K, d, d_item, d_act, d_time, nb, vocab, n_actions, inner_layers;
   int item_smem = 1;           // fe_mlp_bwd: stage the item-table gradient in shared memory when it fits
+  // fe_mlp_bwd hidden passes (set by frontend_mlp_bwd): this launch covers hidden units
+  // [mlp_h0, mlp_h0 + mlp_hn) of the 2D; mlp_last: it finishes dx0 (the featuriser / table part);
+  // dx0_part: [T, d] fp32 partial dx0 carried between passes (read when mlp_h0 > 0, written when
+  // not the last pass)
+  int mlp_h0 = 0, mlp_hn = 0, mlp_last = 1;
+  float* dx0_part = nullptr;
   long long T;                 // B * Lp tokens
   // fp32 master parameters (biases, tables)
   const float *item_tab, *act_tab, *time_tab, *pos_tab, *tok_w, *tok_b, *seq_b1, *seq_b2;
@@ -63,7 +69,8 @@ void pack_frontend_weights(const float* params, long long tok_w, long long seq_w
                            cudaStream_t st);
 
 int frontend_supported(int d, int K, int D, int F, int inner_layers);
-// the fused token-MLP backward additionally needs 2D ≤ 256 (TMEM / shared-memory budget)
+// the fused token-MLP backward takes 2D ≤ 256 in one pass, or 2D a multiple of 256 in passes of
+// 256 hidden units (TMEM / shared-memory budget per pass); FrontArgs::dx0_part must be set then
 int frontend_mlp_bwd_supported(int d, int K, int D);
 int frontend_fwd(const FrontArgs& a, cudaStream_t st);
 // P (see FrontArgs::proj) from the fp32 master tables: (vocab + n_actions + nb) x d floats

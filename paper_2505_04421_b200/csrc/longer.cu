@@ -1083,6 +1083,7 @@ int backward(const Ctx& c, const Plan& p, const LongerBatch& bt, float* probs) {
     FrontArgs f = front_args(c, p, bt);
     f.dh = dxt;
     if (dxt == p.t_dx && first_unfused < 0) { f.dh = nullptr; f.dh_bf = reinterpret_cast<const bf16*>(p.t_dx); }
+    f.dx0_part = p.dx0;                                  // partial dx0 between hidden passes (2D > 256)
     probe(PH_FE_MLP_BWD, 0, st); TRY(frontend_mlp_bwd(f, st)); probe(PH_FE_MLP_BWD, 1, st);
     join_side(st, ss);
     TRY((int)cudaGetLastError());
