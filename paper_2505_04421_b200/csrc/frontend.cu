@@ -655,9 +655,24 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   // column-block tiling: this CTA owns token positions [cb*128, cb*128+128) of samples b0, b0+r, …
+  // (tiles t = 0, 1, … of its sequence); split mode: tiles [t0, t1) of the column-block-major
+  // order (column block t / B, sample t % B) — the column block changes inside the range
   const int tps = (a.Lp + kTile - 1) / kTile;
-  const int r = gridDim.x / tps;
-  const int cb = blockIdx.x % tps, b0 = blockIdx.x / tps;
+  const bool split = a.mlp_split;
+  const int r = split ? 1 : gridDim.x / tps;
+  const int b0 = split ? 0 : blockIdx.x / tps;
+  int t0 = 0, t1 = 0;
+  if (split) {
+    const long long W = (long long)tps * a.B;
+    t0 = (int)(W * blockIdx.x / gridDim.x);
+    t1 = (int)(W * (blockIdx.x + 1) / gridDim.x);
+  } else if (b0 < a.B) {
+    t1 = (a.B - b0 + r - 1) / r;
+  }
+  auto tile_cb = [&](int t) { return split ? t / a.B : (int)(blockIdx.x % tps); };
+  auto tile_b = [&](int t) { return split ? t % a.B : b0 + t * r; };
+  const int cb = t0 < t1 ? tile_cb(t0) : 0;                   // column block of the first tile
+  const int cb_last = t0 < t1 ? tile_cb(t1 - 1) : 0;
   for (int i = threadIdx.x; i < (item_smem ? n_item : 0); i += blockDim.x) s_item[i] = 0.f;
   for (int i = threadIdx.x; i < kTile * DT; i += blockDim.x) {
     const int rr = i / DT, c = i % DT;
@@ -709,7 +724,7 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
       uint32_t pa = 0;
       auto wait_a = [&]() { sm100::mbar_wait(bar_a, pa); pa ^= 1; sm100::tc_fence_after(); };
       bool first = true;
-      for (int b = b0; b < a.B; b += r) {
+      for (int t = t0; t < t1; ++t) {
         wait_a();                                                        // feat, dh, onehot
         mma(T_X, Opnd{aFeat, kFP, 0}, Opnd{aTP, kFP, 0}, kFP / 16, DT, false);
         sm100::mma_commit(bar_d);
@@ -759,8 +774,9 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
     const int grp = (warp - 1) >> 2;
     const int row = q * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    const int j = cb * kTile + row;                    // token position inside the sample (fixed)
-    const bool col_ok = j < a.Lp;
+    // s_pos / s_gpos entries (row, c0..c0+XH) are read and written only by this thread: a change of
+    // column block flushes / reloads them here without a CTA barrier
+    int cur_cb = cb;
     uint32_t pd = 0;
     auto signal = [&]() { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(bar_a); };
     auto wait_d = [&]() { sm100::mbar_wait(bar_d, pd); pd ^= 1; sm100::tc_fence_after(); };
@@ -768,9 +784,10 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
     // current tile's first stage, so their latency overlaps the MMA round trips
     int n_pf = 0, item_pf = 0, act_pf = 0, dt_pf = 0;
     float dh_pf[DT];
-    auto prefetch = [&](int bb) {
+    auto prefetch = [&](int tt) {
+      const int bb = tile_b(tt), j = tile_cb(tt) * kTile + row;
       n_pf = a.n_events[bb];
-      if (!col_ok) return;
+      if (j >= a.Lp) return;
       const long long src = (long long)bb * a.L + max(j - (a.Lp - a.L), 0);
       item_pf = a.items[src];
       if (grp == 0) {
@@ -797,7 +814,7 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
         }
       }
     };
-    if (b0 < a.B) prefetch(b0);
+    if (t0 < t1) prefetch(t0);
     int my_tiles = 0;
     int oh_b = -1, oh_a = -1;                          // this row's one-hot columns in sOH
     // stage A of a tile: its feature / one-hot / dh rows into shared memory (from the prefetched
@@ -806,7 +823,9 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
     // so that loop overlaps the next tile's first MMA round trip.
     TokenInfo ti;
     int cas_item = 0;
-    auto stage_a = [&](int bb) {
+    auto stage_a = [&](int tt) {
+      const int bb = tile_b(tt), j = tile_cb(tt) * kTile + row;
+      const bool col_ok = j < a.Lp;
       ti.b = bb; ti.j = j;
       ti.in_range = col_ok;
       ti.t = (long long)bb * a.Lp + j;
@@ -837,16 +856,28 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
       cas_item = ids[0];
       signal();
     };
-    if (b0 < a.B) {
-      stage_a(b0);
-      if (b0 + r < a.B) prefetch(b0 + r);
+    if (t0 < t1) {
+      stage_a(t0);
+      if (t0 + 1 < t1) prefetch(t0 + 1);
     }
-    for (int b = b0; b < a.B; b += r, ++my_tiles) {
+    for (int t = t0; t < t1; ++t, ++my_tiles) {
+      const int b = tile_b(t), tcb = tile_cb(t), j = tcb * kTile + row;
+      const bool col_ok = j < a.Lp;
       wait_d();
       // x0 recompute; with DT = 32 the two groups take 16 columns each
       constexpr int XH = (DT % 32 == 0) ? DT / 2 : DT;
       if (XH < DT || grp == 0) {
         const int c0 = XH < DT ? grp * XH : 0;
+        if (tcb != cur_cb) {                                           // split mode: next column block
+          const int rec0 = a.Lp - 1 - (cur_cb * kTile + row), rec1 = a.Lp - 1 - j;
+          for (int c = 0; c < XH; ++c) {
+            float& g = s_gpos[row * (DT + 1) + c0 + c];
+            if (rec0 >= 0 && rec0 < a.L && g != 0.f) atomicAdd(a.g_pos + (long long)rec0 * DT + c0 + c, g);
+            g = 0.f;
+            s_pos[row * (DT + 1) + c0 + c] = (rec1 >= 0 && rec1 < a.L) ? a.pos_tab[(long long)rec1 * DT + c0 + c] : 0.f;
+          }
+          cur_cb = tcb;
+        }
         float x[XH], acc[XH];
         tmem_row<XH>(T_X + lane_off + c0, acc);
 #pragma unroll
@@ -908,9 +939,9 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
         }
       }
       if (!last) {                                                     // no featuriser part in this pass
-        if (b + r < a.B) {
-          stage_a(b + r);
-          if (b + 2 * r < a.B) prefetch(b + 2 * r);
+        if (t + 1 < t1) {
+          stage_a(t + 1);
+          if (t + 2 < t1) prefetch(t + 2);
         }
         continue;
       }
@@ -921,9 +952,9 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
         tmem_row<kFP>(T_X + lane_off, df);
         const bool cas_real = ti.real;
         const int cas_tile_item = cas_item;
-        if (b + r < a.B) {
-          stage_a(b + r);
-          if (b + 2 * r < a.B) prefetch(b + 2 * r);
+        if (t + 1 < t1) {
+          stage_a(t + 1);
+          if (t + 2 < t1) prefetch(t + 2);
         }
         if (cas_real) {
           if (item_smem && (a.d_item & 3) == 0 && (reinterpret_cast<uintptr_t>(s_item) & 15) == 0) {
@@ -1026,7 +1057,7 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
     if (s_item[i] != 0.f) atomicAdd(a.g_item + i, s_item[i]);
   for (int i = threadIdx.x; i < kTile * DT; i += blockDim.x) {
     const int rr = i / DT, c = i % DT;
-    const int rec = a.Lp - 1 - (cb * kTile + rr);
+    const int rec = a.Lp - 1 - (cb_last * kTile + rr);
     const float v = s_gpos[rr * (DT + 1) + c];
     if (rec >= 0 && rec < a.L && v != 0.f) atomicAdd(a.g_pos + (long long)rec * DT + c, v);
   }
@@ -1164,17 +1195,29 @@ static int launch_mlp_bwd(const FrontArgs& a, cudaStream_t st) {
   const int tps = (a.Lp + kTile - 1) / kTile;
   int r = std::max(1, std::min(a.B, 148 / tps));
   if (g_knobs.fe_grid > 0) r = std::max(1, std::min(r, g_knobs.fe_grid / tps));   // testing: many tiles per CTA
+  int grid = tps * r;
+  // split mode: equal ranges of the column-block-major tile order over (up to) every SM — for long
+  // sequences (c5: 79 column blocks) one column block per CTA leaves most of the machine idle
+  b.mlp_split = 0;
+  if (g_knobs.fe_split) {
+    const long long W = (long long)tps * a.B;
+    int gs = (int)std::min<long long>(W, 148);
+    if (g_knobs.fe_grid > 0) gs = std::min(gs, g_knobs.fe_grid);
+    const long long col_max = (a.B + r - 1) / r, split_max = (W + gs - 1) / gs;
+    // (only for a clear gain: the few SMs column mode leaves free run the side-stream work)
+    if (g_knobs.fe_split == 2 || 4 * split_max < 3 * col_max) { b.mlp_split = 1; grid = gs; }
+  }
   // > 113 KB of smem keeps one CTA per SM (the kernel allocates all 512 TMEM columns)
   if (H2 <= 256) {
     b.mlp_h0 = 0; b.mlp_hn = 0; b.mlp_last = 1;
-    launch(fe_mlp_bwd_kernel<DT>, tps * r, kThreads8, std::max(smem, 116 * 1024), st, b);
+    launch(fe_mlp_bwd_kernel<DT>, grid, kThreads8, std::max(smem, 116 * 1024), st, b);
   } else {
     // wider hidden layers: passes of 256 hidden units (TMEM / smem per pass as at 2D = 256), the
     // partial dx0 carried in a.dx0_part; the last pass finishes the featuriser / table part
     if (!a.dx0_part) return (int)cudaErrorInvalidValue;
     for (int h = 0; h < H2; h += HP) {
       b.mlp_h0 = h; b.mlp_hn = HP; b.mlp_last = h + HP >= H2;
-      launch(fe_mlp_bwd_kernel<DT>, tps * r, kThreads8, std::max(smem, 116 * 1024), st, b);
+      launch(fe_mlp_bwd_kernel<DT>, grid, kThreads8, std::max(smem, 116 * 1024), st, b);
     }
   }
   return (int)cudaGetLastError();

@@ -23,6 +23,9 @@ struct FrontArgs {
   // dx0_part: [T, d] fp32 partial dx0 carried between passes (read when mlp_h0 > 0, written when
   // not the last pass)
   int mlp_h0 = 0, mlp_hn = 0, mlp_last = 1;
+  // mlp_split: fe_mlp_bwd's CTAs take equal ranges of the column-block-major tile order instead of
+  // one column block each (long sequences: more column blocks than SMs would leave idle)
+  int mlp_split = 0;
   float* dx0_part = nullptr;
   long long T;                 // B * Lp tokens
   // fp32 master parameters (biases, tables)

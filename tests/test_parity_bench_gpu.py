@@ -68,11 +68,14 @@ def test_bench_batch_matches_oracle(merge, min_events):
     assert_grads_close(grads, G, f"B=256 {merge} min_events={min_events}")
 
 
+@pytest.mark.parametrize("fe_split", ["0", "2"], ids=["column-blocks", "split-ranges"])
 @pytest.mark.parametrize("merge", ["inner", "concat"])
-def test_multi_tile_per_cta_matches_oracle(merge, monkeypatch):
+def test_multi_tile_per_cta_matches_oracle(merge, fe_split, monkeypatch):
     """Fused grids capped at 3 CTAs (fe_fwd / fe_inner_bwd: ~30 tiles each; fe_mlp_bwd: one CTA
-    per 128-token column block, each walking every sample), every GEMM at its widest tile."""
+    per 128-token column block, each walking every sample — or, split, 3 CTAs each walking a third
+    of the column-block-major tile order across column-block changes), every GEMM at its widest tile."""
     monkeypatch.setenv("LONGER_FE_GRID", "3")
+    monkeypatch.setenv("LONGER_FE_SPLIT", fe_split)
     monkeypatch.setenv("LONGER_GEMM_MIN_TILES", "1")
     cfg = ModelConfig(**dict(C2, merge_mode=merge)).validate()
     P = _perturbed(cfg, 13)
@@ -86,6 +89,7 @@ def test_multi_tile_per_cta_matches_oracle(merge, monkeypatch):
     # the capped and the full grids compute the same step (fp32 accumulation order aside)
     monkeypatch.delenv("LONGER_FE_GRID")
     monkeypatch.delenv("LONGER_GEMM_MIN_TILES")
+    monkeypatch.delenv("LONGER_FE_SPLIT")
     p2, loss2, grads2 = _run(model, batch)
     np.testing.assert_allclose(p2, p, atol=1e-4)
     for name in grads:
