@@ -1047,6 +1047,7 @@ template <int DH, bool TMA, bool KVS = false>
 int launch_fwd_t(const AttnArgs& a, const CUtensorMap& tK, const CUtensorMap& tV, int pack, cudaStream_t st) {
   const int smem = (128 * DH + std::max(128 * kC, kC * DH) + kC * DH) * 2 + 64 + 1024;
   smem_attr(xattn_fwd_kernel<DH, TMA, KVS>, 227 * 1024);
+  g_launch_fence = kFenceAttnIn | kFenceAttnOut;
   launch(xattn_fwd_kernel<DH, TMA, KVS>, ((a.B + pack - 1) / pack) * a.heads, kThreads, std::max(smem, 80 * 1024), st,
          a, tK, tV, pack);
   return (int)cudaGetLastError();
@@ -1077,6 +1078,7 @@ int launch_bwd_t(const AttnArgs& a, const CUtensorMap& tK, const CUtensorMap& tV
   const int QR = (DH > 128 || SHORT) ? 64 : 128, KVB = SHORT ? 2 : 1, KVT = KVS ? 1 : 2;
   const int smem = (2 * QR * DH + KVB * KVT * kC * DH + 2 * QR * kC) * 2 + 256 * 4 + 64 + 1024;
   smem_attr(xattn_bwd_kernel<DH, TMA, SHORT, KVS>, 227 * 1024);
+  g_launch_fence = kFenceAttnIn | kFenceAttnOut;
   launch(xattn_bwd_kernel<DH, TMA, SHORT, KVS>, ((a.B + pack - 1) / pack) * a.heads, kThreads8,
          std::max(smem, 116 * 1024), st, a, tK, tV, pack);
   return (int)cudaGetLastError();
@@ -1096,6 +1098,7 @@ int launch_bwd(const AttnArgs& a, cudaStream_t st) {
             const int smem = (2 * kC * DH + 2 * 64 * DH + 2 * kC * 128) * 2 + 8 * 2048 + (2 * 64 + 4 * 64) * 4 +
                              2 * 64 * 4 + 16 + 16 * 8 + 1024;
             smem_attr(xattn_bwd_t_kernel<DH>, smem);
+            g_launch_fence = kFenceAttnIn | kFenceAttnOut;
             launch(xattn_bwd_t_kernel<DH>, a.B, kThreads8, smem, st, a, tK);
             return (int)cudaGetLastError();
           }

@@ -29,6 +29,9 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // the library never share them.  Defaults are the measured-best settings.
 struct Knobs {
   int pdl = 1;             // LONGER_PDL: programmatic dependent launch
+  int pdl_fence = 15;      // LONGER_PDL_FENCE: full (non-programmatic) dependencies around the big kernels:
+                           // bit 0 into the fused front-end kernels, bit 1 out of them, bits 2 / 3 the
+                           // same for the cross-attention kernels
   int prio = 1;            // LONGER_PRIO: side stream at the lowest launch priority
   int side = 1;            // LONGER_SIDE: weight-gradient side stream
   int fused = 1;           // LONGER_FUSED: fused front-end kernels
@@ -58,6 +61,7 @@ inline int env_int(const char* name, int dflt) {
 inline Knobs read_knobs() {
   Knobs k;
   k.pdl = env_int("LONGER_PDL", 1);
+  k.pdl_fence = env_int("LONGER_PDL_FENCE", 15);
   k.prio = env_int("LONGER_PRIO", 1);
   k.side = env_int("LONGER_SIDE", 1);
   k.fused = env_int("LONGER_FUSED", 1);
@@ -126,8 +130,21 @@ inline void launch_priorities(int& lo, int& hi) {
   hi = g_knobs.prio ? h : l;                   // LONGER_PRIO=0: all launches at the default priority
 }
 
+// PDL fences: a launch flagged `fence_in` gets a full dependency on its predecessor; one flagged
+// `fence_out` makes the next launch on its stream do so (see Knobs::pdl_fence)
+inline thread_local cudaStream_t g_fence_stream = nullptr;
+inline thread_local bool g_fence_pending = false;
+enum : int { kFenceNone = 0, kFenceFrontIn = 1, kFenceFrontOut = 2, kFenceAttnIn = 4, kFenceAttnOut = 8 };
+
+inline thread_local int g_launch_fence = 0;   // set by a launcher for its next launch() call
 template <typename... KArgs, typename... Args>
 inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  const int fence = g_launch_fence & g_knobs.pdl_fence;
+  g_launch_fence = 0;
+  bool pdl = g_knobs.pdl != 0;
+  if (g_fence_pending && g_fence_stream == st) { pdl = false; g_fence_pending = false; }
+  if (fence & (kFenceFrontIn | kFenceAttnIn)) pdl = false;
+  if (fence & (kFenceFrontOut | kFenceAttnOut)) { g_fence_pending = true; g_fence_stream = st; }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -142,7 +159,7 @@ inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
     at[n].val.priority = is_side_stream(st) ? lo : hi;
     ++n;
   }
-  if (g_knobs.pdl) {
+  if (pdl) {
     at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[n].val.programmaticStreamSerializationAllowed = 1;
     ++n;

@@ -1153,6 +1153,7 @@ static int launch_fwd_s(const FrontArgs& a, cudaStream_t st) {
   const long long ntiles = (a.T + kTile - 1) / kTile;
   int grid = (int)std::min<long long>((ntiles + S - 1) / S, 148);
   if (g_knobs.fe_grid > 0) grid = std::min(grid, g_knobs.fe_grid);   // testing: many tiles per CTA
+  g_launch_fence = kFenceFrontIn | kFenceFrontOut;
   launch(fe_fwd_kernel<DT, KG, S>, grid, 32 * 5 * S, smem, st, a);
   return (int)cudaGetLastError();
 }
@@ -1210,6 +1211,7 @@ static int launch_mlp_bwd(const FrontArgs& a, cudaStream_t st) {
   // > 113 KB of smem keeps one CTA per SM (the kernel allocates all 512 TMEM columns)
   if (H2 <= 256) {
     b.mlp_h0 = 0; b.mlp_hn = 0; b.mlp_last = 1;
+    g_launch_fence = kFenceFrontIn | kFenceFrontOut;
     launch(fe_mlp_bwd_kernel<DT>, grid, kThreads8, std::max(smem, 116 * 1024), st, b);
   } else {
     // wider hidden layers: passes of 256 hidden units (TMEM / smem per pass as at 2D = 256), the
@@ -1217,6 +1219,7 @@ static int launch_mlp_bwd(const FrontArgs& a, cudaStream_t st) {
     if (!a.dx0_part) return (int)cudaErrorInvalidValue;
     for (int h = 0; h < H2; h += HP) {
       b.mlp_h0 = h; b.mlp_hn = HP; b.mlp_last = h + HP >= H2;
+      g_launch_fence = kFenceFrontIn | kFenceFrontOut;
       launch(fe_mlp_bwd_kernel<DT>, grid, kThreads8, std::max(smem, 116 * 1024), st, b);
     }
   }

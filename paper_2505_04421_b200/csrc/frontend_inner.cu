@@ -550,6 +550,7 @@ int launch_inner_bwd_ng(const FrontArgs& a, cudaStream_t st) {
   const long long ntiles = (a.T + kTile - 1) / kTile;
   int grid = (int)std::min<long long>(ntiles, 148);
   if (g_knobs.fe_grid > 0) grid = std::min(grid, g_knobs.fe_grid);   // testing: many tiles per CTA
+  g_launch_fence = kFenceFrontIn | kFenceFrontOut;
   launch(fe_inner_bwd_kernel<DT, KG, NG>, grid, 32 * (1 + kWorkers * NG), std::max(smem, 116 * 1024), st, a);
   return (int)cudaGetLastError();
 }
