@@ -29,9 +29,13 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // the library never share them.  Defaults are the measured-best settings.
 struct Knobs {
   int pdl = 1;             // LONGER_PDL: programmatic dependent launch
-  int pdl_fence = 15;      // LONGER_PDL_FENCE: full (non-programmatic) dependencies around the big kernels:
+  int pdl_fence = 47;      // LONGER_PDL_FENCE: full (non-programmatic) dependencies around the big kernels:
                            // bit 0 into the fused front-end kernels, bit 1 out of them, bits 2 / 3 the
-                           // same for the cross-attention kernels
+                           // same for the cross-attention kernels, bits 4 / 5 for the GEMMs.  An early
+                           // (programmatic) launch parks the dependent grid's CTAs on SMs that the
+                           // predecessor's tail and the side stream's kernels could use: measured at
+                           // c2-inner, 47 (all but into the GEMMs) 1.280 ms, 15: 1.291, 0: 1.37,
+                           // PDL off: 1.30
   int prio = 1;            // LONGER_PRIO: side stream at the lowest launch priority
   int side = 1;            // LONGER_SIDE: weight-gradient side stream
   int fused = 1;           // LONGER_FUSED: fused front-end kernels
@@ -61,7 +65,7 @@ inline int env_int(const char* name, int dflt) {
 inline Knobs read_knobs() {
   Knobs k;
   k.pdl = env_int("LONGER_PDL", 1);
-  k.pdl_fence = env_int("LONGER_PDL_FENCE", 15);
+  k.pdl_fence = env_int("LONGER_PDL_FENCE", 47);
   k.prio = env_int("LONGER_PRIO", 1);
   k.side = env_int("LONGER_SIDE", 1);
   k.fused = env_int("LONGER_FUSED", 1);
@@ -134,7 +138,8 @@ inline void launch_priorities(int& lo, int& hi) {
 // `fence_out` makes the next launch on its stream do so (see Knobs::pdl_fence)
 inline thread_local cudaStream_t g_fence_stream = nullptr;
 inline thread_local bool g_fence_pending = false;
-enum : int { kFenceNone = 0, kFenceFrontIn = 1, kFenceFrontOut = 2, kFenceAttnIn = 4, kFenceAttnOut = 8 };
+enum : int { kFenceNone = 0, kFenceFrontIn = 1, kFenceFrontOut = 2, kFenceAttnIn = 4, kFenceAttnOut = 8,
+             kFenceGemmIn = 16, kFenceGemmOut = 32 };
 
 inline thread_local int g_launch_fence = 0;   // set by a launcher for its next launch() call
 template <typename... KArgs, typename... Args>
@@ -143,8 +148,8 @@ inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
   g_launch_fence = 0;
   bool pdl = g_knobs.pdl != 0;
   if (g_fence_pending && g_fence_stream == st) { pdl = false; g_fence_pending = false; }
-  if (fence & (kFenceFrontIn | kFenceAttnIn)) pdl = false;
-  if (fence & (kFenceFrontOut | kFenceAttnOut)) { g_fence_pending = true; g_fence_stream = st; }
+  if (fence & (kFenceFrontIn | kFenceAttnIn | kFenceGemmIn)) pdl = false;
+  if (fence & (kFenceFrontOut | kFenceAttnOut | kFenceGemmOut)) { g_fence_pending = true; g_fence_stream = st; }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;

@@ -396,6 +396,7 @@ int launch_cfg(const GemmArgs& g, const CUtensorMap& tA, const CUtensorMap& tB, 
   const int ctas = std::min(n_items, 148);
   GemmArgs ga = g;
   if (ga.staged < 0) ga.staged = g_knobs.gemm_stage ? 1 : 0;
+  g_launch_fence = kFenceGemmIn | kFenceGemmOut;
   launch(gemm_kernel<BN, STAGES>, dim3(ctas), kThreads, smem, st, tA, tB, ga, kb_per, (int)grid.x, (int)grid.y,
          n_items);
   return (int)cudaGetLastError();
