@@ -597,6 +597,143 @@ __global__ void __launch_bounds__(256) ln_bwd128_hw_kernel(RowMap x, const float
   }
 }
 
+// The same pipeline at W = 256 (c5's K/V rows): a full warp per row, 8 columns per lane, R rows per
+// stage (x fp32 | dy bf16 | mean, rstd), S stages per warp.
+template <int R, int S>
+struct LnAsync256 {
+  static constexpr int STAGE = R * 1536 + 32 * 4;
+  static constexpr int SMEM = 8 * S * STAGE;
+};
+
+template <int R, int S>
+__global__ void __launch_bounds__(256) ln_bwd256_kernel(RowMap x, const float* __restrict__ g,
+                                                        const float* __restrict__ mean,
+                                                        const float* __restrict__ rstd,
+                                                        const bf16* __restrict__ dy, int ldy, RowMapW out,
+                                                        float* dgain, float* dbias) {
+  pdl_trigger();
+  pdl_wait();
+  using L = LnAsync256<R, S>;
+  extern __shared__ __align__(16) uint8_t lsm[];
+  __shared__ float sg[8][256], sb[8][256];
+  const int wid = threadIdx.x / 32, lane = threadIdx.x & 31;
+  uint8_t* wbase = lsm + wid * S * L::STAGE;
+  const int rows = x.rows();
+  const int per = x.na + x.nb;
+  float gg[8];
+  {
+    const float4 g0 = __ldg(reinterpret_cast<const float4*>(g) + 2 * lane);
+    const float4 g1 = __ldg(reinterpret_cast<const float4*>(g) + 2 * lane + 1);
+    gg[0] = g0.x; gg[1] = g0.y; gg[2] = g0.z; gg[3] = g0.w; gg[4] = g1.x; gg[5] = g1.y; gg[6] = g1.z; gg[7] = g1.w;
+  }
+  float pg[8], pb[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) { pg[u] = 0.f; pb[u] = 0.f; }
+  const int stride = gridDim.x * 8 * R;
+  const int first = (blockIdx.x * 8 + wid) * R;
+  const float inv_per = 1.f / (float)per;
+  auto split = [&](int row, int& b, int& j) {
+    b = (int)(((float)row + 0.5f) * inv_per);
+    j = row - b * per;
+    if (j < 0) { --b; j += per; } else if (j >= per) { ++b; j -= per; }
+  };
+  auto issue = [&](int r0, int s) {
+    uint8_t* sp = wbase + s * L::STAGE;
+    float* sx = reinterpret_cast<float*>(sp);
+    bf16* sd = reinterpret_cast<bf16*>(sp + R * 1024);
+    float* ss = reinterpret_cast<float*>(sp + R * 1536);
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int row = r0 + i;
+      if (row < rows) {
+        int b, j;
+        split(row, b, j);
+        const float* src = j < x.na ? x.A + (long long)(b * x.a_rows + x.a_off + j) * x.lda
+                                    : x.Bsrc + (long long)(b * x.nb + j - x.na) * x.ldb;
+        cpa16(sx + i * 256 + lane * 8, src + lane * 8);
+        cpa16(sx + i * 256 + lane * 8 + 4, src + lane * 8 + 4);
+        cpa16(sd + i * 256 + lane * 8, dy + (long long)row * ldy + lane * 8);
+      }
+    }
+    if (lane < R && r0 + lane < rows) {
+      cpa4(ss + lane, mean + r0 + lane);
+      cpa4(ss + R + lane, rstd + r0 + lane);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) issue(first + s * stride, s);
+  int it = 0;
+  for (int r0 = first; r0 < rows; r0 += stride, ++it) {
+    __syncwarp();
+    issue(r0 + (S - 1) * stride, (it + S - 1) % S);
+    cpa_wait<S - 1>();
+    __syncwarp();
+    const uint8_t* sp = wbase + (it % S) * L::STAGE;
+    const float* sx = reinterpret_cast<const float*>(sp);
+    const bf16* sd = reinterpret_cast<const bf16*>(sp + R * 1024);
+    const float* ss = reinterpret_cast<const float*>(sp + R * 1536);
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int row = r0 + i;
+      if (row >= rows) break;                      // warp-uniform
+      float xr[8], d[8];
+      const float4 x0 = *reinterpret_cast<const float4*>(sx + i * 256 + lane * 8);
+      const float4 x1 = *reinterpret_cast<const float4*>(sx + i * 256 + lane * 8 + 4);
+      const uint4 dv = *reinterpret_cast<const uint4*>(sd + i * 256 + lane * 8);
+      xr[0] = x0.x; xr[1] = x0.y; xr[2] = x0.z; xr[3] = x0.w; xr[4] = x1.x; xr[5] = x1.y; xr[6] = x1.z; xr[7] = x1.w;
+      d[0] = sm100::bf16_lo(dv.x); d[1] = sm100::bf16_hi(dv.x); d[2] = sm100::bf16_lo(dv.y); d[3] = sm100::bf16_hi(dv.y);
+      d[4] = sm100::bf16_lo(dv.z); d[5] = sm100::bf16_hi(dv.z); d[6] = sm100::bf16_lo(dv.w); d[7] = sm100::bf16_hi(dv.w);
+      const float mu = ss[i], inv = ss[R + i];
+      float xh[8], gh[8], s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        xh[u] = (xr[u] - mu) * inv;
+        gh[u] = d[u] * gg[u];
+        s1 += gh[u];
+        s2 += gh[u] * xh[u];
+        pg[u] += d[u] * xh[u];
+        pb[u] += d[u];
+      }
+      // lanes < 16 end with the row's s1, lanes >= 16 with its s2
+      float kp = (lane & 16) ? s2 : s1;
+      kp += __shfl_xor_sync(0xffffffffu, (lane & 16) ? s1 : s2, 16);
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) kp += __shfl_xor_sync(0xffffffffu, kp, o);
+      const float m1 = __shfl_sync(0xffffffffu, kp, 0) * (1.f / 256);
+      const float m2 = __shfl_sync(0xffffffffu, kp, 16) * (1.f / 256);
+      int b, j;
+      split(row, b, j);
+      float* dst = j < out.na ? out.A + (long long)(b * out.a_rows + out.a_off + j) * out.lda
+                              : out.Bsrc + (long long)(b * out.nb + j - out.na) * out.ldb;
+      float o[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) o[u] = (gh[u] - m1 - xh[u] * m2) * inv;
+      reinterpret_cast<float4*>(dst + lane * 8)[0] = make_float4(o[0], o[1], o[2], o[3]);
+      reinterpret_cast<float4*>(dst + lane * 8)[1] = make_float4(o[4], o[5], o[6], o[7]);
+    }
+  }
+  cpa_wait<0>();
+#pragma unroll
+  for (int u = 0; u < 8; ++u) { sg[wid][lane * 8 + u] = pg[u]; sb[wid][lane * 8 + u] = pb[u]; }
+  __syncthreads();
+  {
+    float a = 0.f, bb = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) { a += sg[w][threadIdx.x]; bb += sb[w][threadIdx.x]; }
+    if (dgain) { atomicAdd(&dgain[threadIdx.x], a); atomicAdd(&dbias[threadIdx.x], bb); }
+  }
+}
+
+template <int R, int S>
+static void launch_ln256(int bps, const RowMap& x, const float* g, const float* mean, const float* rstd,
+                         const bf16* dy, int ldy, const RowMapW& out, float* dgain, float* dbias, cudaStream_t st) {
+  constexpr int smem = LnAsync256<R, S>::SMEM;
+  smem_attr(ln_bwd256_kernel<R, S>, smem);
+  const int grid = std::max(1, std::min(cdiv(x.rows(), 8 * R), 148 * bps));
+  launch(ln_bwd256_kernel<R, S>, grid, 256, smem, st, x, g, mean, rstd, dy, ldy, out, dgain, dbias);
+}
+
 template <int R, int S>
 static void launch_ln_hw(int bps, const RowMap& x, const float* g, const float* mean, const float* rstd,
                          const bf16* dy, int ldy, const RowMapW& out, float* dgain, float* dbias, cudaStream_t st) {
@@ -616,8 +753,12 @@ void layernorm_bwd(const RowMap& x, int W, const float* g, const float* mean, co
                   ln_contig(W, 4, out.A, out.lda, out.nb ? out.Bsrc : nullptr, out.ldb) && ldy % 4 == 0 &&
                   (reinterpret_cast<uintptr_t>(dy) & 7) == 0;
   const bool dy16 = ldy % 8 == 0 && (reinterpret_cast<uintptr_t>(dy) & 15) == 0;   // 16-byte dy rows
+  const bool ct256 = W == 256 && ln_contig(W, 8, x.A, x.lda, x.nb ? x.Bsrc : nullptr, x.ldb) &&
+                     ln_contig(W, 8, out.A, out.lda, out.nb ? out.Bsrc : nullptr, out.ldb);
   if (ct && dy16) {
     launch_ln_hw<4, 3>(2, x, g, mean, rstd, dy, ldy, out, dgain, dbias, st);
+  } else if (ct256 && dy16 && g_knobs.ln256) {
+    launch_ln256<4, 3>(1, x, g, mean, rstd, dy, ldy, out, dgain, dbias, st);
   } else if (ct)
     launch(ln_bwd_kernel<4, true, bf16>, grid, 256, 0, st, x, W, g, mean, rstd, dy, ldy, out, 0,
            static_cast<const float*>(nullptr), dgain, dbias, LnBwdExtra());
