@@ -34,8 +34,9 @@ struct Knobs {
                            // same for the cross-attention kernels, bits 4 / 5 for the GEMMs.  An early
                            // (programmatic) launch parks the dependent grid's CTAs on SMs that the
                            // predecessor's tail and the side stream's kernels could use: measured at
-                           // c2-inner, 47 (all but into the GEMMs) 1.280 ms, 15: 1.291, 0: 1.37,
-                           // PDL off: 1.30
+                           // c2-inner, 47 (all but into the GEMMs) 1.264-1.280 ms, 15: 1.291, 0: 1.37,
+                           // PDL off: 1.30; bits 6 / 7 (every other kernel) cost +8 / +20 us; without
+                           // bit 0 +18 us, without bit 3 +55 us, bits 1 and 2 within noise
   int prio = 1;            // LONGER_PRIO: side stream at the lowest launch priority
   int side = 1;            // LONGER_SIDE: weight-gradient side stream
   int fused = 1;           // LONGER_FUSED: fused front-end kernels
@@ -141,17 +142,17 @@ inline void launch_priorities(int& lo, int& hi) {
 inline thread_local cudaStream_t g_fence_stream = nullptr;
 inline thread_local bool g_fence_pending = false;
 enum : int { kFenceNone = 0, kFenceFrontIn = 1, kFenceFrontOut = 2, kFenceAttnIn = 4, kFenceAttnOut = 8,
-             kFenceGemmIn = 16, kFenceGemmOut = 32 };
+             kFenceGemmIn = 16, kFenceGemmOut = 32, kFenceOtherIn = 64, kFenceOtherOut = 128 };
 
 inline thread_local int g_launch_fence = 0;   // set by a launcher for its next launch() call
 template <typename... KArgs, typename... Args>
 inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
-  const int fence = g_launch_fence & g_knobs.pdl_fence;
+  const int fence = (g_launch_fence ? g_launch_fence : (kFenceOtherIn | kFenceOtherOut)) & g_knobs.pdl_fence;
   g_launch_fence = 0;
   bool pdl = g_knobs.pdl != 0;
   if (g_fence_pending && g_fence_stream == st) { pdl = false; g_fence_pending = false; }
-  if (fence & (kFenceFrontIn | kFenceAttnIn | kFenceGemmIn)) pdl = false;
-  if (fence & (kFenceFrontOut | kFenceAttnOut | kFenceGemmOut)) { g_fence_pending = true; g_fence_stream = st; }
+  if (fence & (kFenceFrontIn | kFenceAttnIn | kFenceGemmIn | kFenceOtherIn)) pdl = false;
+  if (fence & (kFenceFrontOut | kFenceAttnOut | kFenceGemmOut | kFenceOtherOut)) { g_fence_pending = true; g_fence_stream = st; }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;
