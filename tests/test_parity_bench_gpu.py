@@ -100,12 +100,16 @@ def test_multi_tile_per_cta_matches_oracle(merge, fe_split, monkeypatch):
 C5 = dict(L=10000, d=32, K=8, k=32, N=4, m=3, merge_mode="inner")
 
 
-@pytest.mark.parametrize("min_events", [None, 3000], ids=["full", "mixed"])
-def test_c5_real_shape_matches_oracle(min_events):
+@pytest.mark.parametrize("min_events,fe_split", [(None, "1"), (3000, "1"), (3000, "2")],
+                         ids=["full", "mixed", "mixed-split"])
+def test_c5_real_shape_matches_oracle(min_events, fe_split, monkeypatch):
     """BASELINE config 5 at its real shape (L = 10,000, d = 32, K = 8 → D = 256, N = 4 self
     layers, InnerTrans): 1,250 merged keys = 10 key chunks of the tensor-core attention at head
-    width 256, the fused forward at D = 256 (three tile slots per CTA), the per-stage token-MLP
-    backward with activation recompute (2D = 512 > 256)."""
+    width 256, the fused forward at D = 256 (three tile slots per CTA), the 256-wide K/V-row LN
+    backward, and the fused token-MLP backward in two passes of 256 hidden units (2D = 512) with the
+    partial dx0 handed between them — in column-block mode, and (mixed-split) in the split mode the
+    bench's B = 256 runs, where each CTA's tile range crosses column blocks."""
+    monkeypatch.setenv("LONGER_FE_SPLIT", fe_split)
     cfg = ModelConfig(**C5).validate()
     P = _perturbed(cfg, 31)
     batch = synthetic_batch(cfg, 4, seed=2, min_events=min_events)
@@ -227,3 +231,22 @@ def test_d16_inner_trans_fused_backward(fe_grid, monkeypatch):
     assert np.max(np.abs(p - p_ref)) <= 5e-3
     assert abs(loss - loss_ref) <= loss_tol(p_ref, batch.label)
     assert_grads_close(grads, G, f"d16 inner fe_grid={fe_grid}")
+
+
+def test_pdl_fences_do_not_change_the_step(monkeypatch):
+    """LONGER_PDL_FENCE only changes which launches may start early (scheduling): the step with
+    every fence, with none and with PDL off computes the same probabilities and gradients (fp32
+    atomic accumulation order aside)."""
+    cfg = ModelConfig(**C2).validate()
+    P = _perturbed(cfg, 23)
+    batch = synthetic_batch(cfg, 12, seed=4, min_events=1)
+    model = _model(cfg, P)
+    p, loss, grads = _run(model, batch)
+    for env in [("LONGER_PDL_FENCE", "0"), ("LONGER_PDL_FENCE", "255"), ("LONGER_PDL", "0")]:
+        monkeypatch.setenv(*env)
+        p2, loss2, grads2 = _run(model, batch)
+        monkeypatch.delenv(env[0])
+        np.testing.assert_allclose(p2, p, atol=1e-6)
+        for name in grads:
+            scale = np.abs(grads[name]).max() + 1e-12
+            assert np.abs(grads2[name] - grads[name]).max() <= 1e-4 * scale + 1e-9, (env, name)
