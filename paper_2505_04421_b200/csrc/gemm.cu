@@ -65,6 +65,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     sm100::fence_barrier_init();
   }
   if (warp == 1) sm100::tmem_alloc<TCOLS>(tmem_slot);
+  if (warp == 0 && threadIdx.x == 0) {             // descriptors are kernel parameters: before the wait
+    sm100::tma_prefetch(&tmA);
+    sm100::tma_prefetch(&tmB);
+  }
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
@@ -74,8 +78,6 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 
   if (warp == 0) {
     if (sm100::elect_one()) {
-      sm100::tma_prefetch(&tmA);
-      sm100::tma_prefetch(&tmB);
       int it = 0;
       for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
         int n0, m0, kb_begin, nkb;
