@@ -651,7 +651,8 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
   uint64_t* bar_w = bars;
   uint64_t* bar_a = bars + 1;
   uint64_t* bar_d = bars + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3);
+  uint64_t* bar_g = bars + 3;    // the dW_tp / one-hot MMAs done (they read sFeat / sOH / sDX0)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   // column-block tiling: this CTA owns token positions [cb*128, cb*128+128) of samples b0, b0+r, …
@@ -686,6 +687,7 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
     sm100::mbar_init(bar_w, 1);
     sm100::mbar_init(bar_a, 32 * 2 * kWorkers);
     sm100::mbar_init(bar_d, 1);
+    sm100::mbar_init(bar_g, 1);
     sm100::fence_barrier_init();
   }
   if (warp == 0) sm100::tmem_alloc<512>(tmem_slot);
@@ -759,10 +761,11 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
         }
         if (last) {
           wait_a();                                                      // dx0 in sDX0
+          mma(T_X, Opnd{aDX0, 64, 0}, Opnd{aTPn, DT, 0}, DT / 16, kFP, false);     // dfeat first
+          sm100::mma_commit(bar_d);
           mma(T_DWTP, Opnd{aDX0, 64, 1}, Opnd{aFeat, kFP, 1}, kTile / 16, kFP, !first);
           mma(T_Y, Opnd{aOH, 64, 1}, Opnd{aDX0, 64, 1}, kTile / 16, DT, !first);
-          mma(T_X, Opnd{aDX0, 64, 0}, Opnd{aTPn, DT, 0}, DT / 16, kFP, false);
-          sm100::mma_commit(bar_d);
+          sm100::mma_commit(bar_g);                                      // sFeat / sOH / sDX0 free
         }
         first = false;
       }
@@ -777,9 +780,10 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
     // s_pos / s_gpos entries (row, c0..c0+XH) are read and written only by this thread: a change of
     // column block flushes / reloads them here without a CTA barrier
     int cur_cb = cb;
-    uint32_t pd = 0;
+    uint32_t pd = 0, pg = 0;
     auto signal = [&]() { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(bar_a); };
     auto wait_d = [&]() { sm100::mbar_wait(bar_d, pd); pd ^= 1; sm100::tc_fence_after(); };
+    auto wait_g = [&]() { sm100::mbar_wait(bar_g, pg); pg ^= 1; sm100::tc_fence_after(); };
     // the next sample's raw inputs (n_events, ids, dh) are loaded a tile ahead, right after the
     // current tile's first stage, so their latency overlaps the MMA round trips
     int n_pf = 0, item_pf = 0, act_pf = 0, dt_pf = 0;
@@ -950,6 +954,7 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
       {                                                                // item rows: dfeat[:d_item]
         float df[kFP];
         tmem_row<kFP>(T_X + lane_off, df);
+        wait_g();                                                      // dW_tp / Y MMAs done
         const bool cas_real = ti.real;
         const int cas_tile_item = cas_item;
         if (t + 1 < t1) {
