@@ -752,7 +752,8 @@ void layernorm_bwd(const RowMap& x, int W, const float* g, const float* mean, co
   const bool ct = W == 128 && ln_contig(W, 4, x.A, x.lda, x.nb ? x.Bsrc : nullptr, x.ldb) &&
                   ln_contig(W, 4, out.A, out.lda, out.nb ? out.Bsrc : nullptr, out.ldb) && ldy % 4 == 0 &&
                   (reinterpret_cast<uintptr_t>(dy) & 7) == 0;
-  const bool dy16 = ldy % 8 == 0 && (reinterpret_cast<uintptr_t>(dy) & 15) == 0;   // 16-byte dy rows
+  const bool dy16 = ldy % 8 == 0 && (reinterpret_cast<uintptr_t>(dy) & 15) == 0 &&   // 16-byte dy rows,
+                    (reinterpret_cast<uintptr_t>(g) & 15) == 0;                      // float4 gains
   const bool ct256 = W == 256 && ln_contig(W, 8, x.A, x.lda, x.nb ? x.Bsrc : nullptr, x.ldb) &&
                      ln_contig(W, 8, out.A, out.lda, out.nb ? out.Bsrc : nullptr, out.ldb);
   if (ct && dy16) {
