@@ -249,7 +249,7 @@ def _check_ids(name: str, arr: np.ndarray, rows: int) -> None:
 def tensorize(samples: Sequence[Sample], cfg: ModelConfig, check: bool = True) -> Batch:
     """Samples → ``Batch`` (host numpy).  Raises the reference's errors for bad input.
 
-    Each event field is pulled from all events of the batch by one C-level iterator chain
+    The event fields are pulled from all events of the batch by one C-level iterator chain
     (≈ 1.5 M attribute reads for 256 x 2000 events: this, not the placement, bounds it), then placed
     into the right-aligned [B, L] grid and range-checked with vector operations.  Training loops
     should tensorise a dataset once (``Dataset.tensorized``) and slice batches from it
@@ -258,8 +258,9 @@ def tensorize(samples: Sequence[Sample], cfg: ModelConfig, check: bool = True) -
     evs = [tuple(s.events)[-L:] for s in samples]
     n = np.fromiter((len(e) for e in evs), np.int64, B)
     tot = int(n.sum())
-    flat = np.stack([np.fromiter(map(attrgetter(k), chain.from_iterable(evs)), np.int64, tot)
-                     for k in ("item_id", "action_type", "timestamp")], axis=1)
+    fields = attrgetter("item_id", "action_type", "timestamp")   # one pass, three reads per event
+    flat = np.fromiter(chain.from_iterable(map(fields, chain.from_iterable(evs))), np.int64,
+                       3 * tot).reshape(tot, 3)
     cand_ts = np.fromiter((s.candidate.timestamp for s in samples), np.int64, B)
     rows = np.repeat(np.arange(B), n)
     starts = np.cumsum(n) - n
