@@ -29,9 +29,29 @@ struct PackW {
 
 // trans = 1: image of Wᵀ ([out][in]: element (n=j, k=i) = W[i][j]); trans = 0: image of W as
 // [in][out] (element (n=i, k=j) = W[i][j]).  W is the fp32 master [in, out] row-major.
-__global__ void pack_canon_kernel(const float* __restrict__ params, PackW pw, bf16* blob) {
+__global__ void pack_canon_kernel(const float* __restrict__ params, PackW pw, bf16* blob, ProjArgs pj) {
   pdl_trigger();
   pdl_wait();
+  if (blockIdx.y == pw.n) {
+    // the extra row of blocks: P[r] = table_row(r) · W_tp[cols of its table] (+ b_tp on the time
+    // rows), fp32 (inputs.py:434-444 restated: the featuriser's linear map per table row, once per step)
+    const int rows = pj.vocab + pj.n_actions + pj.nb, d = pj.d;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < rows * d; e += gridDim.x * blockDim.x) {
+      const int r = e / d, c = e % d;
+      const float* src;
+      int w, k0;
+      float acc = 0.f;
+      if (r < pj.vocab) { src = pj.item_tab + (long long)r * pj.d_item; w = pj.d_item; k0 = 0; }
+      else if (r < pj.vocab + pj.n_actions) { src = pj.act_tab + (long long)(r - pj.vocab) * pj.d_act; w = pj.d_act; k0 = pj.d_item; }
+      else {
+        src = pj.time_tab + (long long)(r - pj.vocab - pj.n_actions) * pj.d_time; w = pj.d_time;
+        k0 = pj.d_item + pj.d_act; acc = pj.tok_b[c];
+      }
+      for (int k = 0; k < w; ++k) acc = fmaf(src[k], pj.tok_w[(k0 + k) * d + c], acc);
+      pj.proj[e] = acc;
+    }
+    return;
+  }
   const auto s = pw.s[blockIdx.y];
   const int n_el = s.in * s.out;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n_el; e += gridDim.x * blockDim.x) {
@@ -40,28 +60,6 @@ __global__ void pack_canon_kernel(const float* __restrict__ params, PackW pw, bf
     const int idx = s.trans ? canon(s.n_off + j, s.k_off + i, s.Kdim) : canon(s.n_off + i, s.k_off + j, s.Kdim);
     if (s.f16) reinterpret_cast<__half*>(blob)[s.dst + idx] = __float2half_rn(v);
     else blob[s.dst + idx] = __float2bfloat16(v);
-  }
-}
-
-// P[r] = table_row(r) · W_tp[cols of its table] (+ b_tp on the time rows), fp32 (inputs.py:434-444
-// restated: the featuriser's linear map is applied per table row once per step, not per token)
-__global__ void project_tables_kernel(const float* __restrict__ item_tab, const float* __restrict__ act_tab,
-                                      const float* __restrict__ time_tab, const float* __restrict__ tok_w,
-                                      const float* __restrict__ tok_b, int vocab, int n_actions, int nb, int d_item,
-                                      int d_act, int d_time, int d, float* __restrict__ proj) {
-  pdl_trigger();
-  pdl_wait();
-  const int rows = vocab + n_actions + nb;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < rows * d; e += gridDim.x * blockDim.x) {
-    const int r = e / d, c = e % d;
-    const float* src;
-    int w, k0;
-    float acc = 0.f;
-    if (r < vocab) { src = item_tab + (long long)r * d_item; w = d_item; k0 = 0; }
-    else if (r < vocab + n_actions) { src = act_tab + (long long)(r - vocab) * d_act; w = d_act; k0 = d_item; }
-    else { src = time_tab + (long long)(r - vocab - n_actions) * d_time; w = d_time; k0 = d_item + d_act; acc = tok_b[c]; }
-    for (int k = 0; k < w; ++k) acc = fmaf(src[k], tok_w[(k0 + k) * d + c], acc);
-    proj[e] = acc;
   }
 }
 
@@ -1087,19 +1085,11 @@ int frontend_mlp_bwd_supported(int d, int K, int D) {
   return 2 * D <= 256 || (2 * D) % 256 == 0;
 }
 
-void project_tables(const float* item_tab, const float* act_tab, const float* time_tab, const float* tok_w,
-                    const float* tok_b, int vocab, int n_actions, int nb, int d_item, int d_act, int d_time, int d,
-                    float* proj, cudaStream_t st) {
-  const int n = (vocab + n_actions + nb) * d;
-  launch(project_tables_kernel, std::min((n + 255) / 256, 592), 256, 0, st, item_tab, act_tab, time_tab, tok_w, tok_b,
-         vocab, n_actions, nb, d_item, d_act, d_time, d, proj);
-}
-
 int frontend_blob_bytes(int d, int D, int inner_layers) { return blob_offsets(d, D, inner_layers).total * 2; }
 
 void pack_frontend_weights(const float* params, long long tok_w, long long seq_w1, long long seq_w2,
                            const long long (*inner_w)[4], int d, int D, int F, int IL, bf16* blob,
-                           cudaStream_t st) {
+                           const ProjArgs& pj, cudaStream_t st) {
   const BlobOff o = blob_offsets(d, D, IL);
   cudaMemsetAsync(blob, 0, (size_t)o.total * 2, st);
   PackW pw;
@@ -1141,7 +1131,7 @@ void pack_frontend_weights(const float* params, long long tok_w, long long seq_w
     add(w1, d, 4 * d, 0, 0, 0, 4 * d, o.w1i_n[l]);
     add(w2, 4 * d, d, 0, 0, 0, d, o.w2i_n[l]);
   }
-  launch(pack_canon_kernel, dim3(16, pw.n), 256, 0, st, params, pw, blob);
+  launch(pack_canon_kernel, dim3(16, pw.n + 1), 256, 0, st, params, pw, blob, pj);   // + the table projection
 }
 
 template <int DT, int KG, int S>

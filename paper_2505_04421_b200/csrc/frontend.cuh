@@ -67,19 +67,22 @@ struct FrontArgs {
 int frontend_blob_bytes(int d, int D, int inner_layers);
 // inner_w[l] = param offsets of {w_q, w_k, w_v, w_o} of InnerTrans layer l (w1, w2 follow the
 // reference order after b_o).
+// P (see FrontArgs::proj) from the fp32 master tables: (vocab + n_actions + nb) x d floats,
+// computed by the same launch as the weight blob
+struct ProjArgs {
+  const float *item_tab, *act_tab, *time_tab, *tok_w, *tok_b;
+  int vocab, n_actions, nb, d_item, d_act, d_time, d;
+  float* proj;
+};
 void pack_frontend_weights(const float* params, long long tok_w, long long seq_w1, long long seq_w2,
                            const long long (*inner_w)[4], int d, int D, int F, int inner_layers, bf16* blob,
-                           cudaStream_t st);
+                           const ProjArgs& pj, cudaStream_t st);
 
 int frontend_supported(int d, int K, int D, int F, int inner_layers);
 // the fused token-MLP backward takes 2D ≤ 256 in one pass, or 2D a multiple of 256 in passes of
 // 256 hidden units (TMEM / shared-memory budget per pass); FrontArgs::dx0_part must be set then
 int frontend_mlp_bwd_supported(int d, int K, int D);
 int frontend_fwd(const FrontArgs& a, cudaStream_t st);
-// P (see FrontArgs::proj) from the fp32 master tables: (vocab + n_actions + nb) x d floats
-void project_tables(const float* item_tab, const float* act_tab, const float* time_tab, const float* tok_w,
-                    const float* tok_b, int vocab, int n_actions, int nb, int d_item, int d_act, int d_time, int d,
-                    float* proj, cudaStream_t st);
 // token-MLP + featuriser backward: dh → all front-end MLP/featuriser/table/pos gradients
 int frontend_mlp_bwd(const FrontArgs& a, cudaStream_t st);
 // InnerTrans (one layer) backward: recompute the layer from h, dmerged → dh + layer gradients

@@ -599,8 +599,7 @@ int block_fwd(const Ctx& c, const BlockOff& bo, BlockBufs& b, const float* xq, b
   const bf16* ctx_rows = b.ctx;
   const float* res_rows = xq;
   if (compact) {
-    head_rows_gather_bf16(b.ctx, p.hc_ctx, p.B, p.q, p.k + 1, p.k + p.m - 1, D, st);
-    head_rows_gather_f32(xq, p.hc_x, p.B, p.q, p.k + 1, p.k + p.m - 1, D, st);
+    head_rows_gather_pair(b.ctx, p.hc_ctx, xq, p.hc_x, p.B, p.q, p.k + 1, p.k + p.m - 1, D, st);
     ctx_rows = p.hc_ctx;
     res_rows = p.hc_x;
   }
@@ -705,10 +704,10 @@ int frontend_fused_fwd(const Ctx& c, const Plan& p, const LongerBatch& bt) {
   for (int l = 0; l < p.IL; ++l) {
     iw[l][0] = o.inner[l].w_q; iw[l][1] = o.inner[l].w_k; iw[l][2] = o.inner[l].w_v; iw[l][3] = o.inner[l].w_o;
   }
-  pack_frontend_weights(c.P, o.tok_w, o.seq_w1, o.seq_w2, iw, p.d, p.D, p.F, p.IL, p.wblob, c.st);
   const LongerDims& dm = p.dims;
-  project_tables(c.w(o.item), c.w(o.act), c.w(o.time), c.w(o.tok_w), c.w(o.tok_b), dm.vocab, dm.n_actions,
-                 dm.n_time_buckets, dm.d_item, dm.d_act, dm.d_time, p.d, p.proj, c.st);
+  const ProjArgs pj{c.w(o.item), c.w(o.act), c.w(o.time), c.w(o.tok_w), c.w(o.tok_b), dm.vocab, dm.n_actions,
+                    dm.n_time_buckets, dm.d_item, dm.d_act, dm.d_time, p.d, p.proj};
+  pack_frontend_weights(c.P, o.tok_w, o.seq_w1, o.seq_w2, iw, p.d, p.D, p.F, p.IL, p.wblob, pj, c.st);
   FrontArgs f = front_args(c, p, bt);
   // epilogue: the cross block's LN1 of the merged rows straight into the K/V operand (kn)
   f.kn = p.kn; f.kn_g = c.w(o.cross.ln1_g); f.kn_b = c.w(o.cross.ln1_b);
@@ -847,8 +846,7 @@ int block_bwd(const Ctx& c, cudaStream_t ss, const BlockOff& bo, const BlockBufs
   TRY(lin_dx(st, dx1_bf_rows, D, R, Wo, D, D, D, compact ? p.hc_dctx : b.g_dctx, D, absorb ? p.xa_dctx_bf : nullptr,
              D));
   if (compact) {   // back to full [B·q, D] rows (zero elsewhere) for the attention and LN1 backward
-    head_rows_scatter_f32(p.hc_dctx, b.g_dctx, p.B, p.q, p.k + 1, p.k + p.m - 1, D, st);
-    head_rows_scatter_f32(p.hc_g, b.g_dx1, p.B, p.q, p.k + 1, p.k + p.m - 1, D, st);
+    head_rows_scatter_pair(p.hc_dctx, b.g_dctx, p.hc_g, b.g_dx1, p.B, p.q, p.k + 1, p.k + p.m - 1, D, st);
   }
   // attention
   AttnArgs a{};
@@ -1421,7 +1419,11 @@ extern "C" int longer_forward_backward(const LongerDims* dims, const float* para
   p.compact_head = compact_head_ok(p);
   p.absorb = absorb_ok(p);
   Ctx c{p, params, grads, (cudaStream_t)stream};
-  const LongerBatch bt = checked_batch(p, *batch, c.st);
+  // the per-sample id check on the side stream: its first readers (the global tokens) run there, the
+  // main stream reaches the ids only after waiting for them (head), and the call ends joined
+  const cudaStream_t ss = side_stream(c.st);
+  fork_side(c.st, ss);
+  const LongerBatch bt = checked_batch(p, *batch, ss);
   rc = forward(c, p, bt, probs, loss, 1);
   if (rc) return rc;
   return backward(c, p, bt, probs);

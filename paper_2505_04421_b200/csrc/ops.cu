@@ -1984,6 +1984,70 @@ __global__ void head_rows_expand_kernel(const float* __restrict__ compact, float
   *reinterpret_cast<float4*>(full + e) = v;
 }
 
+// both gathers of the compact last-block tail in one launch: bf16 rows (W_b wide) and fp32 rows (W_f
+// wide), 16-byte vectors; the first 2B·W_b/8 threads take the bf16 part
+__global__ void head_rows_gather2_kernel(const uint4* __restrict__ fb, uint4* __restrict__ cb, int vb,
+                                         const uint4* __restrict__ ff, uint4* __restrict__ cf, int vf, int B, int q,
+                                         int r0, int r1) {
+  pdl_trigger();
+  pdl_wait();
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nb = (long long)2 * B * vb;
+  const uint4* src = fb;
+  uint4* dst = cb;
+  int V = vb;
+  if (i >= nb) { i -= nb; src = ff; dst = cf; V = vf; }
+  if (i >= (long long)2 * B * V) return;
+  const int c = (int)(i % V), r = (int)(i / V);
+  const long long full = (long long)(r >> 1) * q + ((r & 1) ? r1 : r0);
+  dst[(long long)r * V + c] = src[full * V + c];
+}
+
+void head_rows_gather_pair(const bf16* full_b, bf16* compact_b, const float* full_f, float* compact_f, int B, int q,
+                           int r0, int r1, int W, cudaStream_t st) {
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (W % 8 == 0 && al(full_b) && al(compact_b) && al(full_f) && al(compact_f)) {
+    const long long n = (long long)2 * B * (W / 8 + W / 4);
+    launch(head_rows_gather2_kernel, cdiv(n, 256), 256, 0, st, reinterpret_cast<const uint4*>(full_b),
+           reinterpret_cast<uint4*>(compact_b), W / 8, reinterpret_cast<const uint4*>(full_f),
+           reinterpret_cast<uint4*>(compact_f), W / 4, B, q, r0, r1);
+  } else {
+    head_rows_gather_bf16(full_b, compact_b, B, q, r0, r1, W, st);
+    head_rows_gather_f32(full_f, compact_f, B, q, r0, r1, W, st);
+  }
+}
+
+// both expansions of the compact tail's gradients in one launch (blockIdx.y picks the pair)
+__global__ void head_rows_expand2_kernel(const float* __restrict__ c0, float* __restrict__ f0,
+                                         const float* __restrict__ c1, float* __restrict__ f1, int B, int q, int r0,
+                                         int r1, int W) {
+  pdl_trigger();
+  pdl_wait();
+  const float* compact = blockIdx.y ? c1 : c0;
+  float* full = blockIdx.y ? f1 : f0;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)B * q * W / 4) return;
+  const long long e = i * 4;
+  const int c = (int)(e % W);
+  const long long row = e / W;
+  const int b = (int)(row / q), j = (int)(row % q);
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (j == r0 || j == r1)
+    v = *reinterpret_cast<const float4*>(compact + ((long long)2 * b + (j == r1 ? 1 : 0)) * W + c);
+  *reinterpret_cast<float4*>(full + e) = v;
+}
+
+void head_rows_scatter_pair(const float* c0, float* f0, const float* c1, float* f1, int B, int q, int r0, int r1,
+                            int W, cudaStream_t st) {
+  if (W % 4 == 0) {
+    launch(head_rows_expand2_kernel, dim3((unsigned)cdiv((long long)B * q * W / 4, 256), 2), 256, 0, st, c0, f0, c1,
+           f1, B, q, r0, r1, W);
+  } else {
+    head_rows_scatter_f32(c0, f0, B, q, r0, r1, W, st);
+    head_rows_scatter_f32(c1, f1, B, q, r0, r1, W, st);
+  }
+}
+
 void head_rows_scatter_f32(const float* compact, float* full, int B, int q, int r0, int r1, int W, cudaStream_t st) {
   if (W % 4 == 0) {
     launch(head_rows_expand_kernel, cdiv((long long)B * q * W / 4, 256), 256, 0, st, compact, full, B, q, r0, r1, W);

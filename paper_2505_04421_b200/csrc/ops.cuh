@@ -183,6 +183,11 @@ void head_wgrad(const HeadArgs& a, cudaStream_t st);
 void head_rows_gather_f32(const float* full, float* compact, int B, int q, int r0, int r1, int W, cudaStream_t st);
 void head_rows_gather_bf16(const bf16* full, bf16* compact, int B, int q, int r0, int r1, int W, cudaStream_t st);
 void head_rows_scatter_f32(const float* compact, float* full, int B, int q, int r0, int r1, int W, cudaStream_t st);
+// the two gathers (bf16 context rows + fp32 residual rows) / the two scatters in one launch each
+void head_rows_gather_pair(const bf16* full_b, bf16* compact_b, const float* full_f, float* compact_f, int B, int q,
+                           int r0, int r1, int W, cudaStream_t st);
+void head_rows_scatter_pair(const float* c0, float* f0, const float* c1, float* f1, int B, int q, int r0, int r1,
+                            int W, cudaStream_t st);
 
 // ---------------------------------------------------------------- weights
 // Packs fp32 master parameters into the bf16 / fp32 operand layouts the kernels use.
