@@ -735,12 +735,16 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
         for (int j = 0; j < nh; ++j) {
           wait_a();                                                      // g1, da1 of half j
           if (j + 1 < nh) {
-            mma(T_DW2 + j * DT, Opnd{aG, 128, 1}, Opnd{aDH, DT, 1}, kTile / 16, DT, !first);
-            mma(T_DW1 + j * XK, Opnd{aDA, 128, 1}, Opnd{aX0, XK, 1}, kTile / 16, XK, !first);
-            mma(T_X, Opnd{aDA, 128, 0}, Opnd{aW1n + canon(0, 128 * j, HP) * 2, HP, 0}, 8, DT, j > 0);
+            // the next half's a1 / g1 first (the workers wait for them), then this half's weight
+            // gradients and dx0 part behind the second barrier (the workers wait for it only before
+            // they overwrite sG / sDA)
             mma(T_A1, Opnd{aX0, XK, 0}, Opnd{aW1 + canon(128 * (j + 1), 0, XK) * 2, XK, 0}, XK / 16, 128, false);
             mma(T_G1, Opnd{aDH, DT, 0}, Opnd{aW2n + canon(128 * (j + 1), 0, DT) * 2, DT, 0}, DT / 16, 128, false);
             sm100::mma_commit(bar_d);
+            mma(T_DW2 + j * DT, Opnd{aG, 128, 1}, Opnd{aDH, DT, 1}, kTile / 16, DT, !first);
+            mma(T_DW1 + j * XK, Opnd{aDA, 128, 1}, Opnd{aX0, XK, 1}, kTile / 16, XK, !first);
+            mma(T_X, Opnd{aDA, 128, 0}, Opnd{aW1n + canon(0, 128 * j, HP) * 2, HP, 0}, 8, DT, j > 0);
+            sm100::mma_commit(bar_g);
           } else {
             // last half: the workers only wait for dx0 (T_X); the weight-gradient MMAs run on
             // behind that commit (sG / sDA / sDH / sX0 are next rewritten after the tile's final
@@ -785,7 +789,7 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
     // the next sample's raw inputs (n_events, ids, dh) are loaded a tile ahead, right after the
     // current tile's first stage, so their latency overlaps the MMA round trips
     int n_pf = 0, item_pf = 0, act_pf = 0, dt_pf = 0;
-    float dh_pf[DT];
+    uint4 dh_pf[DT / 8];                               // packed bf16 (the MMA operand type)
     auto prefetch = [&](int tt) {
       const int bb = tile_b(tt), j = tile_cb(tt) * kTile + row;
       n_pf = a.n_events[bb];
@@ -799,19 +803,14 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
         if (a.dh_bf) {
           const uint4* srcb = reinterpret_cast<const uint4*>(a.dh_bf + ((long long)bb * a.Lp + j) * DT);
 #pragma unroll
-          for (int c = 0; c < DT; c += 8) {
-            const uint4 u = srcb[c / 8];
-            dh_pf[c] = sm100::bf16_lo(u.x); dh_pf[c + 1] = sm100::bf16_hi(u.x);
-            dh_pf[c + 2] = sm100::bf16_lo(u.y); dh_pf[c + 3] = sm100::bf16_hi(u.y);
-            dh_pf[c + 4] = sm100::bf16_lo(u.z); dh_pf[c + 5] = sm100::bf16_hi(u.z);
-            dh_pf[c + 6] = sm100::bf16_lo(u.w); dh_pf[c + 7] = sm100::bf16_hi(u.w);
-          }
+          for (int c = 0; c < DT / 8; ++c) dh_pf[c] = srcb[c];
         } else {
           const float4* srcd = reinterpret_cast<const float4*>(a.dh + ((long long)bb * a.Lp + j) * DT);
 #pragma unroll
-          for (int c = 0; c < DT; c += 4) {
-            const float4 f4 = srcd[c / 4];
-            dh_pf[c] = f4.x; dh_pf[c + 1] = f4.y; dh_pf[c + 2] = f4.z; dh_pf[c + 3] = f4.w;
+          for (int c = 0; c < DT / 8; ++c) {
+            const float4 f0 = srcd[2 * c], f1 = srcd[2 * c + 1];
+            dh_pf[c] = make_uint4(sm100::pack_bf16(f0.x, f0.y), sm100::pack_bf16(f0.z, f0.w),
+                                  sm100::pack_bf16(f1.x, f1.y), sm100::pack_bf16(f1.z, f1.w));
           }
         }
       }
@@ -848,11 +847,12 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
         oh_a = ti.real ? 32 + ids[1] : -1;
         if (oh_b >= 0) { sOH[canon(row, oh_b, 64)] = one; sOH[canon(row, oh_a, 64)] = one; }
       } else {
-        float dh[DT];
 #pragma unroll
-        for (int c = 0; c < DT; ++c) dh[c] = ti.real ? dh_pf[c] : 0.f;
-        store_row(sDH, row, DT, dh, DT);
-        store_row(sDX0, row, 64, dh, DT, 32);                          // [· | dh] for the db2 row sums
+        for (int c = 0; c < DT / 8; ++c) {
+          const uint4 v = ti.real ? dh_pf[c] : make_uint4(0, 0, 0, 0);
+          *reinterpret_cast<uint4*>(sDH + canon(row, 8 * c, DT)) = v;
+          *reinterpret_cast<uint4*>(sDX0 + canon(row, 32 + 8 * c, 64)) = v;   // [· | dh] for the db2 row sums
+        }
         if (ti.real) ids[0] = (item_pf < 0 || item_pf >= a.vocab) ? 0 : item_pf;   // for the dfeat split
       }
       cas_item = ids[0];
@@ -907,6 +907,7 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
             av[u] = gelu_and_grad(av[u], gd);
             gv[u] *= gd;
           }
+          if (hj > 0 && c0 == 64 * grp) wait_g();                   // previous half's dW MMAs read sG / sDA
           store_row(sG, row, 128, av, 32, c0);
           store_row(sDA, row, 128, gv, 32, c0);
         }
