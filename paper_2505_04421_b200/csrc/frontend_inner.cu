@@ -243,6 +243,29 @@ __global__ void __launch_bounds__(32 * (1 + kWorkers * NG), 1) fe_inner_bwd_kern
     };
     float cs_l1g = 0.f, cs_l1b = 0.f, cs_l2g = 0.f, cs_l2b = 0.f, cs_b2 = 0.f;   // lane c ↔ column c0 + c
     int my_tiles = 0;
+    // R0's rows of tile tl (the warp's 32 rows, its HD columns, of h and dmerged) copied
+    // asynchronously into the warp's staging area in the sGF tile — HD / 4 lanes per row, so each
+    // instruction covers whole row segments; issued a stage ahead (once sGF is free), no registers
+    constexpr int CH = HD / 4, RPI = 32 / CH;          // 16-byte chunks per row, rows per instruction
+    float4* const stg = reinterpret_cast<float4*>(sGF) + (warp - 1) * 2 * 32 * CH;
+    auto issue_rows = [&](long long tl) {
+      const long long tw = tl * kTile + q * 32;         // the warp's first token
+#pragma unroll
+      for (int k = 0; k < 32 / RPI; ++k) {
+        const int r = k * RPI + lane / CH, sg = lane % CH;
+        float4* d0 = stg + r * CH + (sg ^ (r & (CH - 1)));
+        float4* d1 = d0 + 32 * CH;
+        if (tw + r < a.T) {
+          sm100::cp_async16(d0, a.h_in + (tw + r) * DT + c0 + 4 * sg);
+          sm100::cp_async16(d1, a.dmerged + (tw + r) * DT + c0 + 4 * sg);
+        } else {
+          *d0 = make_float4(0.f, 0.f, 0.f, 0.f);
+          *d1 = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      sm100::cp_async_commit();
+    };
+    if (blockIdx.x < ntiles) issue_rows(blockIdx.x);
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++my_tiles) {
       const long long t = tile * kTile + row;
       const bool in_range = t < a.T;
@@ -258,20 +281,7 @@ __global__ void __launch_bounds__(32 * (1 + kWorkers * NG), 1) fe_inner_bwd_kern
       // (free: R5's MMAs are done) sGF tile, then each thread takes its own row.
       float h[HD], dx2[HD];
       {
-        constexpr int CH = HD / 4, RPI = 32 / CH;        // 16-byte chunks per row, rows per instruction
-        float4* stg = reinterpret_cast<float4*>(sGF) + (warp - 1) * 2 * 32 * CH;
-        const long long tw = tile * kTile + q * 32;       // the warp's first token
-#pragma unroll
-        for (int k = 0; k < 32 / RPI; ++k) {
-          const int r = k * RPI + lane / CH, sg = lane % CH;
-          float4 hv = make_float4(0.f, 0.f, 0.f, 0.f), dv = hv;
-          if (tw + r < a.T) {
-            hv = *reinterpret_cast<const float4*>(a.h_in + (tw + r) * DT + c0 + 4 * sg);
-            dv = *reinterpret_cast<const float4*>(a.dmerged + (tw + r) * DT + c0 + 4 * sg);
-          }
-          stg[r * CH + (sg ^ (r & (CH - 1)))] = hv;
-          stg[32 * CH + r * CH + (sg ^ (r & (CH - 1)))] = dv;
-        }
+        sm100::cp_async_wait_all();                       // this tile's rows (issued a stage ahead)
         __syncwarp();
 #pragma unroll
         for (int j = 0; j < CH; ++j) {
@@ -453,6 +463,8 @@ __global__ void __launch_bounds__(32 * (1 + kWorkers * NG), 1) fe_inner_bwd_kern
       signal();
       // ---- R6: LN1 backward → dh = dx1 + LN1ᵀ(dxn)
       wait_d();
+      // the dqkv MMAs (the last readers of sGF) are done: the next tile's R0 rows start arriving
+      if (tile + gridDim.x < ntiles) issue_rows(tile + gridDim.x);
       tmem_row<HD>(T_W2 + lo + c0, g);                                // dxn
       {
         float m[2] = {0.f, 0.f};
