@@ -54,6 +54,7 @@ struct Knobs {
   int gemm_min_tiles = 200;  // LONGER_GEMM_MIN_TILES: fewest items a wider GEMM tile must give
   int fe_grid = 0;         // LONGER_FE_GRID: cap on the fused front-end grids (0: the full machine)
   int item_smem = 1;       // LONGER_ITEM_SMEM: item-table gradient staged in shared memory
+  int fe_kn_global = 1;    // LONGER_FE_KN_GLOBAL: fe_fwd's cross-LN1 params from L1 when that buys a fourth slot
   int ln256 = 1;           // LONGER_LN256: pipelined warp-per-row LN backward for 256-wide K/V rows
   int fe_split = 1;        // LONGER_FE_SPLIT: fe_mlp_bwd tile ranges across column blocks (0 off, 1 when
                            // it shortens the longest CTA by > 25%, 2 always)
@@ -87,6 +88,7 @@ inline Knobs read_knobs() {
   k.item_smem = env_int("LONGER_ITEM_SMEM", 1);
   k.fe_split = env_int("LONGER_FE_SPLIT", 1);
   k.ln256 = env_int("LONGER_LN256", 1);
+  k.fe_kn_global = env_int("LONGER_FE_KN_GLOBAL", 1);
   if (k.split_items < 1) k.split_items = 1;
   if (k.gemm_min_tiles < 1) k.gemm_min_tiles = 1;
   return k;

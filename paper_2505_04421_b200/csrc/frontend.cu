@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(32 * 5 * S, 1) fe_fwd_kernel(FrontArgs a) {
   float* s_par = reinterpret_cast<float*>(sH0 + S * kTile * 64);   // [IL][ln1_g, ln1_b, b_o, ln2_g, ln2_b, b2]
   float* s_b2 = s_par + a.inner_layers * 6 * DT;              // token-MLP output bias [DT]
   float* s_kn = s_b2 + DT;                                    // cross LN1 [gain | bias] (2D)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_kn + 2 * D);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_kn + (a.kn_global ? 0 : 2 * D));
   uint64_t* bar_w = bars;
   uint64_t* bar_a = bars + 1;                                 // [S]
   uint64_t* bar_d = bars + 1 + S;                             // [S]
@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(32 * 5 * S, 1) fe_fwd_kernel(FrontArgs a) {
     s_par[i] = src[c];
   }
   for (int i = threadIdx.x; i < DT; i += blockDim.x) s_b2[i] = a.seq_b2[i];
-  if (a.kn)
+  if (a.kn && !a.kn_global)
     for (int i = threadIdx.x; i < 2 * D; i += blockDim.x) s_kn[i] = i < D ? a.kn_g[i] : a.kn_b[i - D];
   __syncthreads();
   const long long ntiles = (a.T + kTile - 1) / kTile;
@@ -577,8 +577,8 @@ __global__ void __launch_bounds__(32 * 5 * S, 1) fe_fwd_kernel(FrontArgs a) {
           const int part = ti.j % KG;
           const long long krow = (long long)ti.b * a.v + ti.j / KG;
           bf16* dst = a.kn + krow * D + part * DT;
-          const float* gk = s_kn + part * DT;
-          const float* bk = s_kn + D + part * DT;
+          const float* gk = (a.kn_global ? a.kn_g : s_kn) + part * DT;
+          const float* bk = (a.kn_global ? a.kn_b : s_kn + D) + part * DT;
 #pragma unroll
           for (int c = 0; c < DT; c += 8) {
             const float4 g0 = *reinterpret_cast<const float4*>(gk + c), g1 = *reinterpret_cast<const float4*>(gk + c + 4);
@@ -1139,7 +1139,7 @@ template <int DT, int KG, int S>
 static int fwd_smem(const FrontArgs& a) {
   const BlobOff bo = blob_offsets(DT, DT * KG, a.inner_layers);
   return ((bo.fwd_total + 63) & ~63) * 2 + S * kTile * (DT + 16 + 64) * 2 +
-         (a.inner_layers * 6 * DT + DT + 2 * DT * KG) * 4 + (1 + 2 * S) * 8 + 16;
+         (a.inner_layers * 6 * DT + DT + (a.kn_global ? 0 : 2 * DT * KG)) * 4 + (1 + 2 * S) * 8 + 16;
 }
 
 template <int DT, int KG, int S>
@@ -1156,9 +1156,14 @@ static int launch_fwd_s(const FrontArgs& a, cudaStream_t st) {
 
 // as many slots as the weights leave shared memory for (4 at d = 32, D = 128; 3 at D = 256)
 template <int DT, int KG>
-static int launch_fwd(const FrontArgs& a, cudaStream_t st) {
+static int launch_fwd(const FrontArgs& a0, cudaStream_t st) {
   constexpr int kMax = 227 * 1024;
+  FrontArgs a = a0;
+  a.kn_global = 0;
   if (fwd_smem<DT, KG, 4>(a) <= kMax) return launch_fwd_s<DT, KG, 4>(a, st);
+  a.kn_global = g_knobs.fe_kn_global;              // c5 (D = 256): four slots with the LN1 params in L1
+  if (a.kn_global && fwd_smem<DT, KG, 4>(a) <= kMax) return launch_fwd_s<DT, KG, 4>(a, st);
+  a.kn_global = 0;
   if (fwd_smem<DT, KG, 3>(a) <= kMax) return launch_fwd_s<DT, KG, 3>(a, st);
   if (fwd_smem<DT, KG, 2>(a) <= kMax) return launch_fwd_s<DT, KG, 2>(a, st);
   return (int)cudaErrorInvalidValue;

@@ -26,6 +26,9 @@ struct FrontArgs {
   // mlp_split: fe_mlp_bwd's CTAs take equal ranges of the column-block-major tile order instead of
   // one column block each (long sequences: more column blocks than SMs would leave idle)
   int mlp_split = 0;
+  // fe_fwd: the cross-LN1 gain / bias read from global memory (L1) instead of shared memory, which
+  // lets c5's D = 256 fit a fourth tile slot
+  int kn_global = 0;
   float* dx0_part = nullptr;
   long long T;                 // B * Lp tokens
   // fp32 master parameters (biases, tables)
