@@ -857,6 +857,8 @@ __global__ void __launch_bounds__(kThreads8, 1) fe_mlp_bwd_kernel(FrontArgs a) {
       }
       cas_item = ids[0];
       signal();
+      // passes after the first read this tile's partial dx0 at its end: pull the rows into L2 now
+      if (h0 > 0 && col_ok) sm100::prefetch_l2(a.dx0_part + ((long long)bb * a.Lp + j) * DT + grp * (DT / 2));
     };
     if (t0 < t1) {
       stage_a(t0);
