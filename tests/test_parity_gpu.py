@@ -106,6 +106,11 @@ C2 = dict(L=2000, d=32, K=4, k=32, N=2, m=3, merge_mode="inner")
     (dict(C2, L=512, query_strategy="learnable"), 4, 1),
     # D = 256 with two heads: tensor-core attention at head width 128
     (dict(L=96, d=32, K=8, k=4, N=1, m=3, heads=2, merge_mode="inner"), 3, 20),
+    # the other fused front-end instantiations: token width 32 with K = 2 (D = 64) and token width
+    # 16 with K = 8 (D = 128), InnerTrans and concat, ragged lengths
+    (dict(L=300, d=32, K=2, k=8, N=1, m=3, merge_mode="inner"), 4, 50),
+    (dict(L=300, d=16, K=8, k=8, N=1, m=3, merge_mode="inner"), 4, 50),
+    (dict(L=300, d=16, K=8, k=8, N=2, m=3, merge_mode="concat"), 4, 50),
 ])
 def test_matches_oracle_on_synthetic(kw, B, min_events):
     cfg = ModelConfig(**kw).validate()
