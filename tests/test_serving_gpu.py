@@ -66,6 +66,8 @@ C2 = dict(L=2000, d=32, K=4, k=32, N=2, m=3, merge_mode="inner")
 @pytest.mark.parametrize("kw,n_events", [
     (C2, [2000, 700, 5]),
     (dict(C2, merge_mode="concat", heads=2), [2000, 31]),
+    # c5 widths (D = 256, K = 8): the cached attention at head width 256 on the SIMT kernel
+    (dict(L=96, d=32, K=8, k=4, N=2, m=3, merge_mode="inner"), [96, 40]),
 ])
 def test_cached_scores_match_oracle_c2(kw, n_events):
     from paper_2505_04421_b200 import serving as S
