@@ -8,6 +8,10 @@ A step = forward + backward (+ NCCL gradient allreduce when N>1) + Adam, through
 (`longer_forward_backward`, `longer_adam_step`), captured in one CUDA graph.  `value` times the
 device step with CUDA events (inputs resident in HBM, L2 flushed between steps); `e2e` times the
 same step with the batch copied from pinned host memory and the loss read back every step.
+The per-kernel times behind `roofline` / `kernels` / `sections` come from CUDA events recorded
+around the fused kernels in a second capture of the same step, replayed (L2 flushed) after each
+timed step and outside its events: the event-record nodes are full dependencies and would
+otherwise add their own cost to `ms_per_step`.
 
 `--impl reference` times the CPU reference algorithm (the float64 oracle port of longrec in
 oracle/, one single-threaded worker process per host core) on a bounded sample of the same step.
