@@ -304,7 +304,7 @@ __device__ __forceinline__ void warp_store_rows_f32(float* dst, int nvalid, cons
 }
 
 template <int DT, int KG, int S>
-__global__ void __launch_bounds__(32 * 5 * S, 1) fe_fwd_kernel(FrontArgs a) {
+__global__ void __launch_bounds__(32 * 4 * S, 1) fe_fwd_kernel(FrontArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   using P = FwdPlan<DT, KG>;
   constexpr int D = P::D, nh = P::nh, nf = P::nf, XK = P::XK;
@@ -350,34 +350,17 @@ __global__ void __launch_bounds__(32 * 5 * S, 1) fe_fwd_kernel(FrontArgs a) {
   const long long ntiles = (a.T + kTile - 1) / kTile;
   const long long stride = (long long)gridDim.x * S;
 
-  if (warp < S) {
-    if (lane == 0) {
-      // ---------------- MMA issuer of slot s = warp: sleeps on its slot's operand barrier, issues
-      // the stage, commits (a commit tracks only this thread's MMAs: slots never wait for each other)
-      const int s = warp;
-      if (s == 0) {
-        sm100::mbar_arrive_expect_tx(bar_w, bo.fwd_total * 2);
-        load_blob(reinterpret_cast<uint8_t*>(sW), reinterpret_cast<const uint8_t*>(a.wblob), bo.fwd_total * 2,
-                  bar_w);
-      }
-      sm100::mbar_wait(bar_w, 0);
-      const int NS = P::stages(a.inner_layers);
-      const uint32_t wW = sm100::smem_u32(sW), wA = sm100::smem_u32(sA0 + s * kTile * XK);
-      const uint32_t wH = sm100::smem_u32(sH0 + s * kTile * 64), t0 = tmem + s * kSlotCols;
-      uint32_t pa = 0;
-      for (long long tile = (long long)blockIdx.x * S + s; tile < ntiles; tile += stride) {
-        for (int st = 0; st < NS; ++st) {
-          sm100::mbar_wait(&bar_a[s], pa);
-          pa ^= 1;
-          sm100::tc_fence_after();
-          fwd_issue<DT, KG>(st, t0, wA, wH, wW, bo);
-          sm100::mma_commit(&bar_d[s]);
-        }
-      }
-    }
-  } else {
+  // The MMA issuer of slot s is lane 0 of the slot's first worker warp: right after its own arrival
+  // it waits for the slot's other 127 rows, issues the stage and commits (a commit tracks only this
+  // thread's MMAs: slots never wait for each other).  No separate issuer warps: 16 warps, so ptxas
+  // budgets 128 registers per thread instead of 96 (it sizes the budget for the CTA's warps).
+  if (threadIdx.x == 0) {
+    sm100::mbar_arrive_expect_tx(bar_w, bo.fwd_total * 2);
+    load_blob(reinterpret_cast<uint8_t*>(sW), reinterpret_cast<const uint8_t*>(a.wblob), bo.fwd_total * 2, bar_w);
+  }
+  {
     // ---------------- workers: slot s, one token row per thread
-    const int s = (warp - S) >> 2;
+    const int s = warp >> 2;
     const int q = warp & 3;
     const int row = q * 32 + lane;
     const uint32_t trow = tmem + s * kSlotCols + ((uint32_t)(q * 32) << 16);
@@ -386,7 +369,27 @@ __global__ void __launch_bounds__(32 * 5 * S, 1) fe_fwd_kernel(FrontArgs a) {
     bf16* sKV = sH;                                  // 128 x 2DT bf16, 16-byte chunks XOR-swizzled
     const float scale_in = rsqrtf((float)DT);
     uint32_t pd = 0;
-    auto signal = [&]() { sm100::fence_async_smem(); sm100::tc_fence_before(); sm100::mbar_arrive(&bar_a[s]); };
+    const bool issuer = q == 0 && lane == 0;
+    const int NS = P::stages(a.inner_layers);
+    const uint32_t wW = sm100::smem_u32(sW), wA = sm100::smem_u32(sA0 + s * kTile * XK);
+    const uint32_t wH = sm100::smem_u32(sH0 + s * kTile * 64), tslot = tmem + s * kSlotCols;
+    uint32_t pa = 0;
+    int st_i = 0;
+    bool w_ready = false;
+    auto signal = [&]() {
+      sm100::fence_async_smem();
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&bar_a[s]);
+      if (issuer) {
+        if (!w_ready) { sm100::mbar_wait(bar_w, 0); w_ready = true; }
+        sm100::mbar_wait(&bar_a[s], pa);
+        pa ^= 1;
+        sm100::tc_fence_after();
+        fwd_issue<DT, KG>(st_i, tslot, wA, wH, wW, bo);
+        sm100::mma_commit(&bar_d[s]);
+        if (++st_i == NS) st_i = 0;
+      }
+    };
     auto wait_d = [&]() { sm100::mbar_wait(&bar_d[s], pd); pd ^= 1; sm100::tc_fence_after(); };
     for (long long tile = (long long)blockIdx.x * S + s; tile < ntiles; tile += stride) {
       const TokenInfo ti = token_info(a, tile, row);
@@ -1152,7 +1155,7 @@ static int launch_fwd_s(const FrontArgs& a, cudaStream_t st) {
   int grid = (int)std::min<long long>((ntiles + S - 1) / S, 148);
   if (g_knobs.fe_grid > 0) grid = std::min(grid, g_knobs.fe_grid);   // testing: many tiles per CTA
   g_launch_fence = kFenceFrontIn | kFenceFrontOut;
-  launch(fe_fwd_kernel<DT, KG, S>, grid, 32 * 5 * S, smem, st, a);
+  launch(fe_fwd_kernel<DT, KG, S>, grid, 32 * 4 * S, smem, st, a);
   return (int)cudaGetLastError();
 }
 
