@@ -120,7 +120,7 @@ def run_serving(args):
     host_out = torch.empty((U, C), dtype=torch.float32).pin_memory()
 
     def e2e_step():
-        p = S.score_candidates(model, cache, cand_host.numpy(), check=False)
+        p = S.score_candidates(model, cache, cand_host, check=False)      # pinned host ids
         host_out.copy_(p, non_blocking=True)
     ms_e2e = timed(e2e_step, args.steps, args.warmup)
     clk = clocks.stop()

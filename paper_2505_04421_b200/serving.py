@@ -114,12 +114,32 @@ def _check_fresh(model, cache: KVCache) -> None:
 
 def score_candidates(model, cache: KVCache, candidates, check: bool = True) -> "object":
     """Stage 2, batched: ``candidates`` is a [users][C] nested list of ``Candidate`` (every user the
-    same C) or an int array of item ids [users, C] (then the timestamps are the caches' own).
+    same C), an int array of item ids [users, C] (then the timestamps are the caches' own), or an
+    int tensor of item ids (device or pinned host memory: copied asynchronously, checked on the device).
     Returns probabilities as a device tensor [users, C].  With ``check`` the device-side id check
     is read back (one host sync), as the reference raises ``EmbeddingLookupError`` eagerly."""
     torch = _torch()
     _check_fresh(model, cache)
     U = cache.users
+    if torch.is_tensor(candidates):
+        # an int tensor of item ids [users, C], on the device or in (pinned) host memory: no host
+        # conversion, an asynchronous copy; out-of-range ids are caught by the device-side check
+        if candidates.dim() != 2 or candidates.shape[0] != U:
+            raise ConfigError(f"candidate ids must be [users={U}, C]")
+        if candidates.dtype.is_floating_point or candidates.dtype == torch.bool:
+            raise ConfigError("candidate ids must be integers")
+        C = int(candidates.shape[1])
+        if C == 0:
+            return torch.zeros((U, 0), dtype=torch.float32, device=model.device)
+        cand_dev = candidates.to(device=model.device, dtype=torch.int32, non_blocking=True).contiguous()
+        probs = torch.empty((U, C), dtype=torch.float32, device=model.device)
+        base = score_device(model, cache, cand_dev, probs)
+        if check:
+            flags = ctypes.c_int32()
+            _lib.check(model._lib.longer_read_status(ctypes.c_void_p(base), ctypes.byref(flags), model._stream()))
+            if flags.value & 1:
+                raise EmbeddingLookupError("candidate item id outside the item table")
+        return probs
     if isinstance(candidates, np.ndarray) or hasattr(candidates, "dtype"):
         items = np.asarray(candidates.cpu() if hasattr(candidates, "cpu") else candidates, dtype=np.int64)
         if items.ndim != 2 or items.shape[0] != U:

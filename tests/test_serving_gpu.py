@@ -190,3 +190,26 @@ def test_cached_scores_other_query_strategies(strategy):
     p = S.score_candidates(model, cache, cand).cpu().numpy()
     pf = model.forward(_expand(users, cand)).cpu().numpy().reshape(cand.shape)
     assert np.max(np.abs(p - pf)) <= 2e-3, np.abs(p - pf)
+
+
+def test_tensor_candidate_ids():
+    """Candidate ids as a torch tensor (pinned host or device memory: asynchronous copy, no host
+    conversion) score like the numpy array, and an out-of-range id raises through the device flag."""
+    import torch
+    from paper_2505_04421_b200 import serving as S
+    cfg = ModelConfig(L=64, d=16, K=4, k=8, N=2, m=3, merge_mode="inner", n_users=64).validate()
+    model = _model(cfg, None, seed=1)
+    base = synthetic_samples(cfg, 3, seed=9)
+    cache = S.build_caches(model, [(s.events, s.user_features, s.candidate.timestamp) for s in base])
+    ids = np.random.default_rng(2).integers(0, cfg.vocab, size=(3, 5)).astype(np.int32)
+    p_np = S.score_candidates(model, cache, ids).cpu().numpy()
+    p_host = S.score_candidates(model, cache, torch.from_numpy(ids).pin_memory()).cpu().numpy()
+    p_dev = S.score_candidates(model, cache, torch.from_numpy(ids).to("cuda").long()).cpu().numpy()
+    np.testing.assert_array_equal(p_host, p_np)
+    np.testing.assert_array_equal(p_dev, p_np)
+    bad = ids.copy()
+    bad[1, 2] = cfg.vocab
+    with pytest.raises(EmbeddingLookupError):
+        S.score_candidates(model, cache, torch.from_numpy(bad).to("cuda"))
+    with pytest.raises(ConfigError):
+        S.score_candidates(model, cache, torch.zeros((2, 5), dtype=torch.int32))
