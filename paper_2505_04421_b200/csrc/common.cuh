@@ -51,7 +51,8 @@ struct Knobs {
   int head_rows = 1;       // LONGER_HEAD_ROWS: last block's row-wise tail on the two head rows
   int gemm_stage = 1;      // LONGER_GEMM_STAGE: smem-staged GEMM epilogue stores
   int split_items = 74;    // LONGER_SPLIT_ITEMS: split-K work-item target of the weight gradients
-  int gemm_min_tiles = 200;  // LONGER_GEMM_MIN_TILES: fewest items a wider GEMM tile must give
+  int gemm_min_tiles = 0;    // LONGER_GEMM_MIN_TILES: fewest items a wider GEMM tile must give
+                             // (0: 60 for K, N >= 256 — wide tiles re-read A less — else 200)
   int fe_grid = 0;         // LONGER_FE_GRID: cap on the fused front-end grids (0: the full machine)
   int item_smem = 1;       // LONGER_ITEM_SMEM: item-table gradient staged in shared memory
   int fe_kn_global = 1;    // LONGER_FE_KN_GLOBAL: fe_fwd's cross-LN1 params from L1 when that buys a fourth slot
@@ -83,14 +84,14 @@ inline Knobs read_knobs() {
   k.head_rows = env_int("LONGER_HEAD_ROWS", 1);
   k.gemm_stage = env_int("LONGER_GEMM_STAGE", 1);
   k.split_items = env_int("LONGER_SPLIT_ITEMS", 74);
-  k.gemm_min_tiles = env_int("LONGER_GEMM_MIN_TILES", 200);
+  k.gemm_min_tiles = env_int("LONGER_GEMM_MIN_TILES", 0);
   k.fe_grid = env_int("LONGER_FE_GRID", 0);
   k.item_smem = env_int("LONGER_ITEM_SMEM", 1);
   k.fe_split = env_int("LONGER_FE_SPLIT", 1);
   k.ln256 = env_int("LONGER_LN256", 1);
   k.fe_kn_global = env_int("LONGER_FE_KN_GLOBAL", 1);
   if (k.split_items < 1) k.split_items = 1;
-  if (k.gemm_min_tiles < 1) k.gemm_min_tiles = 1;
+  if (k.gemm_min_tiles < 0) k.gemm_min_tiles = 0;
   return k;
 }
 

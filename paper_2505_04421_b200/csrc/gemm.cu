@@ -447,7 +447,9 @@ int gemm_launch(const GemmArgs& g, cudaStream_t st) {
   const bool split = (g.flags & EPI_ATOMIC) != 0;           // split-K fills the machine itself
   if (g.N <= 64) return launch_bn<64>(g, st);
   // LONGER_GEMM_MIN_TILES overrides both thresholds (read per call; 1 forces the widest tile)
-  const int min_tiles = g_knobs.gemm_min_tiles;
+  // (auto: 60 when K and N are both >= 256 — c5's query-row GEMMs, where each narrower tile re-reads
+  // a 64 KB A tile: 6.73 -> 6.67 ms; at c2's K = 128 the 200 threshold measured best)
+  const int min_tiles = g_knobs.gemm_min_tiles > 0 ? g_knobs.gemm_min_tiles : (g.K >= 256 && g.N >= 256 ? 60 : 200);
   const int min_tiles128 = std::min(min_tiles, 120);        // N <= 128: 120 (measured in round 1)
   if (g.N <= 128) return (split || tiles(128) >= min_tiles128) ? launch_bn<128>(g, st) : launch_bn<64>(g, st);
   if (split || tiles(256) >= min_tiles) return launch_bn<256>(g, st);
