@@ -50,7 +50,8 @@ struct Knobs {
   int glob_side = 1;       // LONGER_GLOB_SIDE: global-token backward chain on the side stream
   int head_rows = 1;       // LONGER_HEAD_ROWS: last block's row-wise tail on the two head rows
   int gemm_stage = 1;      // LONGER_GEMM_STAGE: smem-staged GEMM epilogue stores
-  int split_items = 74;    // LONGER_SPLIT_ITEMS: split-K work-item target of the weight gradients
+  int split_items = 37;    // LONGER_SPLIT_ITEMS: split-K work-item target of the weight gradients
+                           // (37 vs 74 at the end of round 2: c2 equal over 4 A/B pairs, c5 -15 us)
   int gemm_min_tiles = 0;    // LONGER_GEMM_MIN_TILES: fewest items a wider GEMM tile must give
                              // (0: 60 for K, N >= 256 — wide tiles re-read A less — else 200)
   int fe_grid = 0;         // LONGER_FE_GRID: cap on the fused front-end grids (0: the full machine)
@@ -83,7 +84,7 @@ inline Knobs read_knobs() {
   k.glob_side = env_int("LONGER_GLOB_SIDE", 1);
   k.head_rows = env_int("LONGER_HEAD_ROWS", 1);
   k.gemm_stage = env_int("LONGER_GEMM_STAGE", 1);
-  k.split_items = env_int("LONGER_SPLIT_ITEMS", 74);
+  k.split_items = env_int("LONGER_SPLIT_ITEMS", 37);
   k.gemm_min_tiles = env_int("LONGER_GEMM_MIN_TILES", 0);
   k.fe_grid = env_int("LONGER_FE_GRID", 0);
   k.item_smem = env_int("LONGER_ITEM_SMEM", 1);

@@ -417,7 +417,8 @@ int launch_bn(const GemmArgs& g, cudaStream_t st) {
   const int nkb = (g.K + BK - 1) / BK;
   const int tiles = ((g.N + BN - 1) / BN) * ((g.M + BM - 1) / BM);
   int want = g.split_k;
-  // split-K for the weight gradients: about 74 items (the persistent CTAs stream their k-blocks back
+  // split-K for the weight gradients: about 37 items (74 in round 1; equal at c2 and 15 us better at
+  // c5 at the end of round 2) (the persistent CTAs stream their k-blocks back
   // to back; more splits only multiply the atomic epilogues, and these GEMMs run beside other
   // kernels on the side stream: 296 → 148 → 74 items measured 1.648 → 1.640 → 1.625 ms per step).
   // LONGER_SPLIT_ITEMS overrides the target.
