@@ -29,14 +29,17 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // the library never share them.  Defaults are the measured-best settings.
 struct Knobs {
   int pdl = 1;             // LONGER_PDL: programmatic dependent launch
-  int pdl_fence = 47;      // LONGER_PDL_FENCE: full (non-programmatic) dependencies around the big kernels:
+  int pdl_fence = 15;      // LONGER_PDL_FENCE: full (non-programmatic) dependencies around the big kernels:
                            // bit 0 into the fused front-end kernels, bit 1 out of them, bits 2 / 3 the
                            // same for the cross-attention kernels, bits 4 / 5 for the GEMMs.  An early
                            // (programmatic) launch parks the dependent grid's CTAs on SMs that the
                            // predecessor's tail and the side stream's kernels could use: measured at
                            // c2-inner, 47 (all but into the GEMMs) 1.264-1.280 ms, 15: 1.291, 0: 1.37,
                            // PDL off: 1.30; bits 6 / 7 (every other kernel) cost +8 / +20 us; without
-                           // bit 0 +18 us, without bit 3 +55 us, bits 1 and 2 within noise
+                           // bit 0 +18 us, without bit 3 +55 us, bits 1 and 2 within noise.  With the
+                           // GEMMs triggering their dependents only after their last MMA issue
+                           // (gemm_late_trigger), 15 (no fence out of the GEMMs) gives 1.245 ms
+                           // (47: 1.279); c5 6.65 -> 6.60, c2-concat 0.967 -> 0.941, c1 0.324 -> 0.304
   int prio = 1;            // LONGER_PRIO: side stream at the lowest launch priority
   int side = 1;            // LONGER_SIDE: weight-gradient side stream
   int fused = 1;           // LONGER_FUSED: fused front-end kernels
@@ -57,6 +60,7 @@ struct Knobs {
   int fe_grid = 0;         // LONGER_FE_GRID: cap on the fused front-end grids (0: the full machine)
   int item_smem = 1;       // LONGER_ITEM_SMEM: item-table gradient staged in shared memory
   int fe_kn_global = 1;    // LONGER_FE_KN_GLOBAL: fe_fwd's cross-LN1 params from L1 when that buys a fourth slot
+  int gemm_late_trigger = 1;  // LONGER_GEMM_LATE_TRIGGER: GEMM dependents launch after its last MMA issue
   int ln256 = 1;           // LONGER_LN256: pipelined warp-per-row LN backward for 256-wide K/V rows
   int fe_split = 1;        // LONGER_FE_SPLIT: fe_mlp_bwd tile ranges across column blocks (0 off, 1 when
                            // it shortens the longest CTA by > 25%, 2 always)
@@ -70,7 +74,7 @@ inline int env_int(const char* name, int dflt) {
 inline Knobs read_knobs() {
   Knobs k;
   k.pdl = env_int("LONGER_PDL", 1);
-  k.pdl_fence = env_int("LONGER_PDL_FENCE", 47);
+  k.pdl_fence = env_int("LONGER_PDL_FENCE", 15);
   k.prio = env_int("LONGER_PRIO", 1);
   k.side = env_int("LONGER_SIDE", 1);
   k.fused = env_int("LONGER_FUSED", 1);
@@ -90,6 +94,7 @@ inline Knobs read_knobs() {
   k.item_smem = env_int("LONGER_ITEM_SMEM", 1);
   k.fe_split = env_int("LONGER_FE_SPLIT", 1);
   k.ln256 = env_int("LONGER_LN256", 1);
+  k.gemm_late_trigger = env_int("LONGER_GEMM_LATE_TRIGGER", 1);
   k.fe_kn_global = env_int("LONGER_FE_KN_GLOBAL", 1);
   if (k.split_items < 1) k.split_items = 1;
   if (k.gemm_min_tiles < 0) k.gemm_min_tiles = 0;

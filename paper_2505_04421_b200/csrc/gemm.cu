@@ -73,7 +73,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  pdl_trigger();
+  // LONGER_GEMM_LATE_TRIGGER: dependents launch once this CTA has issued its last MMA (instead of
+  // at its start), so their CTAs do not sit on the SMs through the whole GEMM
+  if (!g.late_trigger) pdl_trigger();
   pdl_wait();
 
   if (warp == 0) {
@@ -135,6 +137,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         }
         sm100::mma_commit(&tmem_full[buf]);
       }
+      if (g.late_trigger) pdl_trigger();
     }
   } else {
     // Epilogue warps e = 0..7: TMEM lane quarter q = warp % 4, column chunks c ≡ e/4 (mod 2).
@@ -398,6 +401,7 @@ int launch_cfg(const GemmArgs& g, const CUtensorMap& tA, const CUtensorMap& tB, 
   const int ctas = std::min(n_items, 148);
   GemmArgs ga = g;
   if (ga.staged < 0) ga.staged = g_knobs.gemm_stage ? 1 : 0;
+  ga.late_trigger = g_knobs.gemm_late_trigger;
   g_launch_fence = kFenceGemmIn | kFenceGemmOut;
   launch(gemm_kernel<BN, STAGES>, dim3(ctas), kThreads, smem, st, tA, tB, ga, kb_per, (int)grid.x, (int)grid.y,
          n_items);

@@ -39,6 +39,7 @@ struct GemmArgs {
   void* C_bf16 = nullptr; int ldc_bf = 0;
   void* pre_bf16 = nullptr;         // pre-activation out (EPI_SAVE_PRE), ld = ldc_bf
   int staged = -1;                  // epilogue stores through a per-warp smem transpose (-1: LONGER_GEMM_STAGE)
+  int late_trigger = 0;             // set by the launcher (LONGER_GEMM_LATE_TRIGGER)
 };
 
 // Host: encodes the TMA descriptors and launches. Returns a cudaError_t value (0 = ok).
